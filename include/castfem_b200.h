@@ -1,0 +1,300 @@
+/*
+ * castfem_b200.h — C-ABI drop-in boundary for the explicit element-by-element
+ * FE step of the `castfem` reference solver (arXiv 1005.3158), B200-native.
+ *
+ * The reference exposes no FFI: its boundary is the header-only C++ API in
+ * /root/reference/proj/include/castfem/. Every entry point below names the
+ * reference interface it replaces (file:line, paths relative to
+ * proj/include/castfem/). Conventions:
+ *   - plain pointers + sizes, no C++ or torch types; int32 ids, int64 counts;
+ *   - nothing the caller passes is retained after a call returns;
+ *   - every function returns a status (CF_OK = 0); the message of the last
+ *     failure on the calling thread is available through cf_last_error();
+ *   - reference exceptions map to status codes (errors.hpp:8-31,
+ *     geometry.hpp:43-46); device-side failures (c_diag <= 0) report
+ *     CF_VALIDATION with the offending global node id, as
+ *     explicit_update (fem.hpp:107-114) throws validation_error.
+ *
+ * A plan is not thread-safe; distinct plans are independent.
+ */
+#ifndef CASTFEM_B200_H
+#define CASTFEM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CF_ABI_VERSION 1
+
+/* status codes — errors.hpp:8-31 (+ degenerate_element_error geometry.hpp:43-46) */
+enum {
+    CF_OK = 0,
+    CF_PARSE = 1,        /* parse_error        errors.hpp:8-16  */
+    CF_VALIDATION = 2,   /* validation_error   errors.hpp:18-21 */
+    CF_CONFIG = 3,       /* config_error       errors.hpp:23-26 */
+    CF_PROTOCOL = 4,     /* protocol_error     errors.hpp:28-31 */
+    CF_DEGENERATE = 5,   /* degenerate_element_error geometry.hpp:43-46 */
+    CF_CUDA = 6,         /* CUDA runtime failure (no reference analogue) */
+    CF_NCCL = 7,         /* NCCL failure (no reference analogue) */
+    CF_INVALID_ARG = 8   /* null pointer / bad size at the boundary */
+};
+
+/* ---------------------------------------------------------------------------
+ * Problem description (copied at cf_plan_create; mirrors the reference types)
+ * ------------------------------------------------------------------------- */
+
+/* PiecewiseLinear (material.hpp:21-47): n == 1 is a constant (never clamps);
+ * n >= 2 clamps to the covered range; n == 0 is "unset". */
+typedef struct cf_table {
+    int32_t n;
+    const double* x;
+    const double* y;
+} cf_table;
+
+/* MaterialTable (material.hpp:53-124); one per region id. */
+typedef struct cf_material {
+    double rho;
+    cf_table c;          /* c(T)  J/kgK */
+    cf_table k;          /* k(T)  W/mK  */
+    double latent_heat;  /* J/kg; 0 = no phase change */
+    double solidus;
+    double liquidus;
+    double initial_temperature;
+} cf_material;
+
+/* BoundaryCondition (material.hpp:126-141), keyed by facet tag name. */
+enum { CF_BC_FLUX = 0, CF_BC_FIXED = 1 };
+typedef struct cf_boundary_condition {
+    const char* tag;
+    int32_t kind;        /* CF_BC_FLUX | CF_BC_FIXED */
+    cf_table fixed_T;    /* of time, for CF_BC_FIXED (fixed_fn is not expressible in C) */
+    double q;            /* imposed flux W/m^2, positive = heat leaving */
+    double h;            /* convective coefficient W/m^2K */
+    double t_inf;        /* ambient K */
+} cf_boundary_condition;
+
+/* InterfaceCoeff (material.hpp:145-153). */
+enum { CF_VAR_TIME = 0, CF_VAR_TEMPERATURE = 1 };
+typedef struct cf_interface_coeff {
+    const char* tag_a;
+    const char* tag_b;
+    int32_t var;         /* CF_VAR_TIME | CF_VAR_TEMPERATURE */
+    cf_table h;
+} cf_interface_coeff;
+
+/* Mesh (mesh.hpp:45-80): nodes, tets (+region), tagged boundary facets,
+ * contact declarations (pairs of tag ids). Ids are 0-based. */
+typedef struct cf_mesh_desc {
+    int32_t n_nodes;
+    const double* coords;      /* [3*n_nodes] x,y,z */
+    int32_t n_elems;
+    const int32_t* tets;       /* [4*n_elems] */
+    const int32_t* region;     /* [n_elems] */
+    int32_t n_facets;
+    const int32_t* facets;     /* [3*n_facets] */
+    const int32_t* facet_tag;  /* [n_facets] index into tags */
+    int32_t n_tags;
+    const char* const* tags;   /* [n_tags] */
+    int32_t n_contacts;
+    const int32_t* contacts;   /* [2*n_contacts] (tag_a = cast side, tag_b) */
+} cf_mesh_desc;
+
+/* SimulationSetup (material.hpp:162-184) + SolverConfig (:155-160). */
+typedef struct cf_setup_desc {
+    int32_t n_materials;
+    const cf_material* materials;     /* indexed by region id */
+    int32_t n_bcs;
+    const cf_boundary_condition* bcs;
+    int32_t n_coeffs;
+    const cf_interface_coeff* coeffs;
+    double dt_safety;                 /* (0, 1] */
+    double t_end;
+    int64_t output_every;             /* 0 disables the series */
+    const double* initial_T;          /* optional [n_nodes]; replaces initial_override (:167-168) */
+} cf_setup_desc;
+
+/* ---------------------------------------------------------------------------
+ * Run options (the B200 recast of SolveOptions blocked.hpp:630-636)
+ * ------------------------------------------------------------------------- */
+enum {
+    CF_MODE_ATOMIC = 0,        /* in-tile fixed order, tile-shared nodes via fp64 RED */
+    CF_MODE_DETERMINISTIC = 1  /* tile partials merged per node in ascending tile order
+                                  (merge_blocks blocked.hpp:502-515): bit-reproducible */
+};
+enum {
+    CF_NODE_ORDER_GIVEN = 0,   /* keep the caller's node numbering */
+    CF_NODE_ORDER_RCM = 1      /* rcm_permutation (reorder.hpp:127-148) */
+};
+enum {
+    CF_ELEM_ORDER_GIVEN = 0,   /* tiles are contiguous chunks of the given element order */
+    CF_ELEM_ORDER_MORTON = 1,  /* chunks of the Morton order of element centroids */
+    CF_ELEM_ORDER_MIN_NODE = 2 /* chunks of the order by smallest (RCM) node label */
+};
+enum {
+    CF_PARTITION_RCB = 0,      /* recursive coordinate bisection along the longest axis */
+    CF_PARTITION_GIVEN = 1     /* part_of_element supplied (load_partmap partition.hpp:424-445) */
+};
+
+typedef struct cf_run_opts {
+    int32_t device;            /* CUDA ordinal of this process's first rank */
+    int32_t mode;              /* CF_MODE_* */
+    int32_t node_order;        /* CF_NODE_ORDER_* */
+    int32_t elem_order;        /* CF_ELEM_ORDER_* */
+    int32_t tile_elems;        /* elements per tile (0 = default 1024) */
+    const int32_t* tile_of_element; /* optional explicit block map (BlockPlan semantics,
+                                       blocked.hpp:79-93); overrides elem_order/tile_elems */
+    int32_t n_tiles_given;     /* tiles in tile_of_element */
+    int32_t fast_math;         /* 1 = allow FMA contraction (atomic mode only) */
+    /* domain decomposition (paper 4.1.1; two_level_decompose partition.hpp:377-422) */
+    int32_t world_size;        /* ranks in the job (1 = single GPU) */
+    int32_t rank;              /* this process's first rank */
+    int32_t local_ranks;       /* ranks hosted by this process (1, or world_size for the
+                                  in-process transport, see cf_comm_*) */
+    int32_t partition;         /* CF_PARTITION_* */
+    const int32_t* part_of_element; /* [n_elems] when CF_PARTITION_GIVEN */
+    void* comm;                /* cf_comm* for world_size > local_ranks, else NULL */
+} cf_run_opts;
+
+typedef struct cf_plan cf_plan;
+typedef struct cf_comm cf_comm;
+
+/* Stats after stepping (SolverState fem.hpp:14-20, SolveResult blocked.hpp:638-647) */
+typedef struct cf_stats {
+    double time;
+    double dt;                 /* last step's dt */
+    int64_t step_index;
+    int64_t clamp_steps;
+    double loop_seconds;       /* device time of the stepping calls (CUDA events) */
+    double static_dt;          /* local_static_dt (blocked.hpp:340-350), 0 if dynamic */
+    int32_t dynamic_dt;
+    int32_t n_tiles;           /* tiles (cache blocks) of this process's ranks */
+    int64_t n_elems_local;     /* elements stepped by this process */
+    int64_t n_nodes_local;
+    int64_t total_slots;       /* Σ tile node counts (BlockPlan::total_local_nodes :85) */
+    int64_t n_shared_nodes;
+    int64_t n_ghost_nodes;
+    int64_t device_bytes;      /* resident plan + state bytes */
+    int64_t bytes_per_step;    /* canonical algorithmic bytes */
+    int64_t launches_per_step; /* kernels launched per step */
+} cf_stats;
+
+/* ---------------------------------------------------------------------------
+ * Entry points
+ * ------------------------------------------------------------------------- */
+int cf_abi_version(void);
+int cf_last_error(char* buf, size_t len);
+
+/* build_worker_model (blocked.hpp:156-361) + finalize_mesh (mesh.hpp:148-207) +
+ * pair_sister_facets (mesh.hpp:456-478) + init_worker_fields (blocked.hpp:419-436):
+ * validates the mesh and setup, builds tiles, uploads, sets T0 like
+ * initial_temperatures (blocked.hpp:396-417) and refreshes the ambient. */
+int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup,
+                   const cf_run_opts* opts, cf_plan** out);
+int cf_plan_destroy(cf_plan* plan);
+
+/* init_worker_fields (blocked.hpp:419-436) from a host global field [n_nodes]
+ * + the pre-loop refresh_ambient (blocked.hpp:669); resets time/step/clamps. */
+int cf_set_temperature(cf_plan* plan, const double* T_host);
+
+/* n_steps × blocked_step (blocked.hpp:542-550). t_end > 0 caps each dt at
+ * t_end - time and turns steps past t_end into no-ops (solve_serial :674-677);
+ * t_end <= 0 is the max_steps mode (t_remaining = 0). No host sync inside. */
+int cf_step(cf_plan* plan, int64_t n_steps, double t_end);
+
+/* solve_serial's loop (blocked.hpp:671-684) with the output_every series:
+ * runs until max_steps (>0) or setup.t_end; series written as (t, Tmin, Tmax)
+ * triples into series[3*series_cap]; *n_series receives the count. */
+int cf_solve(cf_plan* plan, int64_t max_steps, double* series, int64_t series_cap,
+             int64_t* n_series);
+
+/* Gather into global T, H (blocked.hpp:686-691); H = enthalpy(T) per region.
+ * Either pointer may be NULL. Only nodes of this process's ranks are written. */
+int cf_get_fields(cf_plan* plan, double* T_host, double* H_host);
+int cf_get_stats(cf_plan* plan, cf_stats* out);
+
+/* Device-resident access for benchmarks: current T buffer of local rank `r`
+ * (rank-local node order) and its size. */
+int cf_device_temperature(cf_plan* plan, int32_t local_rank, double** dptr, int64_t* n);
+
+/* SolverConfig::dt_safety (material.hpp:157): rescales the static dt
+ * (blocked.hpp:347) or the dynamic bound factor without rebuilding the plan. */
+int cf_set_dt_safety(cf_plan* plan, double dt_safety);
+
+/* Makes the next cf_step calls replay a CUDA graph of `steps_per_graph` steps. */
+int cf_enable_graph(cf_plan* plan, int64_t steps_per_graph);
+
+/* Largest eigenvalue of M_L^-1 (K + H_bc + H_if) at uniform reference
+ * properties by power iteration on the device (setup utility: BASELINE's
+ * "0.9x the explicit stability limit" is 0.9*2/lambda_max). Also returns the
+ * reference Eq. 13 bound min_e rho c l^2/k (fem.hpp:83-85). */
+int cf_estimate_lambda_max(cf_plan* plan, int32_t iterations, uint64_t seed,
+                           double* lambda_max, double* eq13_min);
+
+/* Multi-rank transport. NCCL across processes (one rank per GPU): rank 0
+ * calls cf_comm_unique_id, shares the 128 bytes, every rank calls
+ * cf_comm_create. world_size ranks in one process use the in-process
+ * transport (local_ranks == world_size, comm == NULL). */
+int cf_comm_unique_id(uint8_t out[128]);
+int cf_comm_create(int32_t world_size, int32_t rank, int32_t device,
+                   const uint8_t unique_id[128], cf_comm** out);
+int cf_comm_destroy(cf_comm* comm);
+
+/* ---------------------------------------------------------------------------
+ * Host utilities (no GPU needed) — the setup pipeline on either side of the path
+ * ------------------------------------------------------------------------- */
+
+/* rcm_permutation (reorder.hpp:127-148) over build_node_graph (:17-24):
+ * new_of_old[n_nodes]. seed < 0 = pseudo-peripheral start per component. */
+int cf_rcm_permutation(const cf_mesh_desc* mesh, int32_t seed, int32_t* new_of_old);
+/* bandwidth (reorder.hpp:41-48); new_of_old NULL = identity. */
+int cf_bandwidth(const cf_mesh_desc* mesh, const int32_t* new_of_old, int64_t* out);
+
+/* finalize_mesh (mesh.hpp:148-207): orientation fix written to tets_out
+ * [4E] (may alias nothing), facet owners to owner_out [F]. */
+int cf_finalize_mesh(const cf_mesh_desc* mesh, int32_t* tets_out, int32_t* owner_out);
+
+/* pair_sister_facets (mesh.hpp:456-478): returns the pair count; fills up to
+ * cap triples (facet, sister element, contact) when out != NULL. */
+int cf_pair_sister_facets(const cf_mesh_desc* mesh, int32_t* out, int64_t cap, int64_t* n_pairs);
+
+/* Recursive coordinate bisection along the longest axis: part_of_element[E]. */
+int cf_partition_rcb(const cf_mesh_desc* mesh, int32_t parts, int32_t* part_of_element);
+
+/* The tiles a plan would build (element -> tile map, in the plan's tile
+ * order; for rank `rank` of a world of `world_size`, -1 for other ranks'
+ * elements). Lets the CPU oracle replay the exact BlockPlan. */
+int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts,
+                int32_t* tile_of_element, int32_t* n_tiles);
+
+/* Synthetic fixtures (bench module S:502-519), structured Kuhn 6-tet cubes.
+ * kind: 0 = single-region cube, all faces tag "outer";
+ *       1 = casting: sphere of radius `radius` (cell-centre test) in a mould
+ *           box, interface nodes duplicated, tags outer / cast_if / mold_if,
+ *           contact (cast_if, mold_if).
+ * jitter: interior grid points moved by U(±jitter·h) per coordinate (seeded
+ * per grid point). perm_seed != 0 permutes element and node numbering.
+ * Two-phase call: pass NULL arrays to get sizes, then allocated arrays. */
+typedef struct cf_fixture {
+    int32_t n_nodes, n_elems, n_facets;
+    double* coords;      /* [3N] */
+    int32_t* tets;       /* [4E] */
+    int32_t* region;     /* [E] */
+    int32_t* facets;     /* [3F] */
+    int32_t* facet_tag;  /* [F] tag ids: 0 outer, 1 cast_if, 2 mold_if */
+    int32_t* node_grid;  /* [N] optional: linear grid-point index of each node */
+} cf_fixture;
+int cf_generate_fixture(int32_t kind, int32_t n, double radius, double jitter, uint64_t seed,
+                        uint64_t perm_seed, cf_fixture* out);
+
+/* Counter-based uniform noise U(lo, hi) keyed by (seed, key) — T0 noise
+ * keyed by grid point so it is independent of numbering. */
+int cf_counter_uniform(uint64_t seed, const int64_t* keys, int64_t n, double lo, double hi,
+                       double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CASTFEM_B200_H */

@@ -1,0 +1,552 @@
+"""Python mirror of the reference castfem C++ API, running on the B200 path.
+
+Names, argument meaning and error behaviour follow the reference headers
+(/root/reference/proj/include/castfem/, cited relative to that directory):
+
+  Mesh                 mesh.hpp:45-80         (nodes / tets / facets / tags / contacts)
+  PiecewiseLinear      material.hpp:21-47
+  MaterialTable        material.hpp:53-124
+  BoundaryCondition    material.hpp:126-141   (kind 'fixed' | 'flux')
+  InterfaceCoeff       material.hpp:145-153   (var 'time' | 'temperature')
+  SolverConfig         material.hpp:155-160
+  SimulationSetup      material.hpp:162-184   (initial_T replaces the initial_override hook)
+  SolveOptions         blocked.hpp:630-636    (+ B200 tiling / mode / decomposition options)
+  SolveResult          blocked.hpp:638-647
+  solve_serial         blocked.hpp:650-696    -> solve() on the GPU
+  Solver               build_worker_model + init_worker_fields + blocked_step granularity
+  rcm_permutation, bandwidth, permute_mesh      reorder.hpp:41-163
+  finalize_mesh, pair_sister_facets             mesh.hpp:148-207, 456-478
+  exceptions           errors.hpp:8-31 (+ DegenerateElementError geometry.hpp:43-46)
+
+Every compute call goes through the C-ABI in include/castfem_b200.h into
+libcastfem_b200.so; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _abi
+from ._abi import lib
+
+
+# ------------------------------------------------------------------ errors (errors.hpp)
+class CastfemError(RuntimeError):
+    code = -1
+
+
+class ParseError(CastfemError):
+    code = _abi.CF_PARSE
+
+
+class ValidationError(CastfemError):
+    code = _abi.CF_VALIDATION
+
+
+class ConfigError(CastfemError):
+    code = _abi.CF_CONFIG
+
+
+class ProtocolError(CastfemError):
+    code = _abi.CF_PROTOCOL
+
+
+class DegenerateElementError(CastfemError):
+    code = _abi.CF_DEGENERATE
+
+
+class CudaError(CastfemError):
+    code = _abi.CF_CUDA
+
+
+class NcclError(CastfemError):
+    code = _abi.CF_NCCL
+
+
+class InvalidArgument(CastfemError, ValueError):
+    code = _abi.CF_INVALID_ARG
+
+
+_BY_CODE = {c.code: c for c in (ParseError, ValidationError, ConfigError, ProtocolError, DegenerateElementError,
+                                CudaError, NcclError, InvalidArgument)}
+
+
+def check(status: int) -> None:
+    if status != _abi.CF_OK:
+        raise _BY_CODE.get(status, CastfemError)(_abi.last_error())
+
+
+# ------------------------------------------------------------------ model types
+@dataclass
+class PiecewiseLinear:
+    xs: List[float] = field(default_factory=list)
+    ys: List[float] = field(default_factory=list)
+
+    @staticmethod
+    def constant(v: float) -> "PiecewiseLinear":
+        return PiecewiseLinear([0.0], [float(v)])
+
+    def is_constant(self) -> bool:
+        return len(self.xs) <= 1
+
+
+def _pl(v) -> PiecewiseLinear:
+    if isinstance(v, PiecewiseLinear):
+        return v
+    if isinstance(v, (int, float)):
+        return PiecewiseLinear.constant(float(v))
+    xs, ys = zip(*v)
+    return PiecewiseLinear(list(map(float, xs)), list(map(float, ys)))
+
+
+@dataclass
+class MaterialTable:
+    rho: float = 0.0
+    c_of_T: PiecewiseLinear = field(default_factory=PiecewiseLinear)
+    k_of_T: PiecewiseLinear = field(default_factory=PiecewiseLinear)
+    latent_heat: float = 0.0
+    solidus: float = 0.0
+    liquidus: float = 0.0
+    initial_temperature: float = 0.0
+
+    @staticmethod
+    def make(rho, c, k, latent_heat=0.0, solidus=0.0, liquidus=0.0, T0=0.0) -> "MaterialTable":
+        return MaterialTable(float(rho), _pl(c), _pl(k), float(latent_heat), float(solidus), float(liquidus),
+                             float(T0))
+
+
+@dataclass
+class BoundaryCondition:
+    kind: str = "flux"  # 'fixed' | 'flux'
+    fixed_T: PiecewiseLinear = field(default_factory=PiecewiseLinear)
+    q: float = 0.0
+    h: float = 0.0
+    t_inf: float = 0.0
+
+
+@dataclass
+class InterfaceCoeff:
+    tag_a: str
+    tag_b: str
+    var: str = "time"  # 'time' | 'temperature'
+    h: PiecewiseLinear = field(default_factory=lambda: PiecewiseLinear.constant(0.0))
+
+
+@dataclass
+class SolverConfig:
+    dt_safety: float = 0.5
+    t_end: float = 0.0
+    output_every: int = 0
+
+
+@dataclass
+class SimulationSetup:
+    materials: List[MaterialTable] = field(default_factory=list)
+    boundary_conditions: Dict[str, BoundaryCondition] = field(default_factory=dict)
+    interface_coeffs: List[InterfaceCoeff] = field(default_factory=list)
+    solver: SolverConfig = field(default_factory=SolverConfig)
+    initial_T: Optional[np.ndarray] = None  # index-keyed initial field (initial_override analogue)
+
+
+@dataclass
+class Mesh:
+    nodes: np.ndarray        # (N, 3) float64
+    tets: np.ndarray         # (E, 4) int32
+    region: np.ndarray       # (E,) int32
+    facets: np.ndarray       # (F, 3) int32
+    facet_tag: np.ndarray    # (F,) int32
+    tags: List[str]
+    contacts: List[Tuple[int, int]] = field(default_factory=list)
+    node_grid: Optional[np.ndarray] = None  # fixtures: grid point of each node
+
+    def __post_init__(self):
+        self.nodes = np.ascontiguousarray(self.nodes, dtype=np.float64).reshape(-1, 3)
+        self.tets = np.ascontiguousarray(self.tets, dtype=np.int32).reshape(-1, 4)
+        self.region = np.ascontiguousarray(self.region, dtype=np.int32).reshape(-1)
+        self.facets = np.ascontiguousarray(self.facets, dtype=np.int32).reshape(-1, 3)
+        self.facet_tag = np.ascontiguousarray(self.facet_tag, dtype=np.int32).reshape(-1)
+
+    def node_count(self) -> int:
+        return int(self.nodes.shape[0])
+
+    def element_count(self) -> int:
+        return int(self.tets.shape[0])
+
+    def tag_id(self, name: str) -> int:
+        return self.tags.index(name) if name in self.tags else -1
+
+
+@dataclass
+class SolveOptions:
+    """SolveOptions (blocked.hpp:630-636) + the B200 knobs."""
+    max_steps: int = 0
+    mode: str = "atomic"             # 'atomic' | 'deterministic'
+    node_order: str = "rcm"          # 'rcm' | 'given'
+    elem_order: str = "morton"       # 'morton' | 'min_node' | 'given'
+    tile_elems: int = 1024
+    blocks: Optional[np.ndarray] = None  # explicit element->tile map (BlockPlan semantics)
+    device: int = 0
+    world_size: int = 1
+    rank: int = 0
+    local_ranks: int = 1
+    part_of_element: Optional[np.ndarray] = None
+    comm: Optional["Comm"] = None
+    graph_steps: int = 0
+
+
+@dataclass
+class SeriesSample:
+    time: float
+    t_min: float
+    t_max: float
+
+
+@dataclass
+class SolveResult:
+    T: np.ndarray
+    H: np.ndarray
+    end_time: float
+    steps: int
+    loop_seconds: float
+    series: List[SeriesSample]
+    clamp_steps: int
+    blocks_used: int
+
+
+# ------------------------------------------------------------------ descriptors
+class _Keep:
+    """Holds the numpy buffers a descriptor points into."""
+
+    def __init__(self):
+        self.refs = []
+
+    def arr(self, a, dtype):
+        a = np.ascontiguousarray(a, dtype=dtype)
+        self.refs.append(a)
+        return a
+
+    def dptr(self, a):
+        a = self.arr(a, np.float64)
+        return a.ctypes.data_as(C.POINTER(C.c_double))
+
+    def iptr(self, a):
+        a = self.arr(a, np.int32)
+        return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+    def table(self, t: PiecewiseLinear) -> _abi.cf_table:
+        n = len(t.xs)
+        if n == 0:
+            return _abi.cf_table(0, None, None)
+        return _abi.cf_table(n, self.dptr(t.xs), self.dptr(t.ys))
+
+    def cstr(self, s: str):
+        b = s.encode()
+        self.refs.append(b)
+        return b
+
+
+def mesh_desc(m: Mesh, keep: _Keep) -> _abi.cf_mesh_desc:
+    d = _abi.cf_mesh_desc()
+    d.n_nodes = m.node_count()
+    d.coords = keep.dptr(m.nodes)
+    d.n_elems = m.element_count()
+    d.tets = keep.iptr(m.tets)
+    d.region = keep.iptr(m.region)
+    d.n_facets = int(m.facets.shape[0])
+    d.facets = keep.iptr(m.facets)
+    d.facet_tag = keep.iptr(m.facet_tag)
+    d.n_tags = len(m.tags)
+    tags = (C.c_char_p * max(1, len(m.tags)))(*[keep.cstr(t) for t in m.tags])
+    keep.refs.append(tags)
+    d.tags = C.cast(tags, C.POINTER(C.c_char_p))
+    d.n_contacts = len(m.contacts)
+    d.contacts = keep.iptr(np.array(m.contacts, dtype=np.int32).reshape(-1) if m.contacts else np.zeros(2, np.int32))
+    return d
+
+
+def setup_desc(s: SimulationSetup, keep: _Keep) -> _abi.cf_setup_desc:
+    d = _abi.cf_setup_desc()
+    mats = (_abi.cf_material * max(1, len(s.materials)))()
+    for i, m in enumerate(s.materials):
+        mats[i] = _abi.cf_material(m.rho, keep.table(m.c_of_T), keep.table(m.k_of_T), m.latent_heat, m.solidus,
+                                   m.liquidus, m.initial_temperature)
+    keep.refs.append(mats)
+    bcs = (_abi.cf_boundary_condition * max(1, len(s.boundary_conditions)))()
+    for i, (tag, b) in enumerate(s.boundary_conditions.items()):
+        kind = _abi.CF_BC_FIXED if b.kind == "fixed" else _abi.CF_BC_FLUX
+        bcs[i] = _abi.cf_boundary_condition(keep.cstr(tag), kind, keep.table(b.fixed_T), b.q, b.h, b.t_inf)
+    keep.refs.append(bcs)
+    cos = (_abi.cf_interface_coeff * max(1, len(s.interface_coeffs)))()
+    for i, c in enumerate(s.interface_coeffs):
+        var = _abi.CF_VAR_TEMPERATURE if c.var == "temperature" else _abi.CF_VAR_TIME
+        cos[i] = _abi.cf_interface_coeff(keep.cstr(c.tag_a), keep.cstr(c.tag_b), var, keep.table(c.h))
+    keep.refs.append(cos)
+    d.n_materials = len(s.materials)
+    d.materials = mats
+    d.n_bcs = len(s.boundary_conditions)
+    d.bcs = bcs
+    d.n_coeffs = len(s.interface_coeffs)
+    d.coeffs = cos
+    d.dt_safety = s.solver.dt_safety
+    d.t_end = s.solver.t_end
+    d.output_every = int(s.solver.output_every)
+    d.initial_T = keep.dptr(s.initial_T) if s.initial_T is not None else None
+    return d
+
+
+_MODES = {"atomic": _abi.CF_MODE_ATOMIC, "deterministic": _abi.CF_MODE_DETERMINISTIC}
+_NODE = {"given": _abi.CF_NODE_ORDER_GIVEN, "rcm": _abi.CF_NODE_ORDER_RCM}
+_ELEM = {"given": _abi.CF_ELEM_ORDER_GIVEN, "morton": _abi.CF_ELEM_ORDER_MORTON,
+         "min_node": _abi.CF_ELEM_ORDER_MIN_NODE}
+
+
+def run_opts(o: SolveOptions, keep: _Keep) -> _abi.cf_run_opts:
+    d = _abi.cf_run_opts()
+    d.device = o.device
+    d.mode = _MODES[o.mode]
+    d.node_order = _NODE[o.node_order]
+    d.elem_order = _ELEM[o.elem_order]
+    d.tile_elems = o.tile_elems
+    if o.blocks is not None:
+        d.tile_of_element = keep.iptr(o.blocks)
+        d.n_tiles_given = int(np.max(o.blocks)) + 1 if len(o.blocks) else 0
+    d.world_size = o.world_size
+    d.rank = o.rank
+    d.local_ranks = o.local_ranks
+    if o.part_of_element is not None:
+        d.partition = _abi.CF_PARTITION_GIVEN
+        d.part_of_element = keep.iptr(o.part_of_element)
+    d.comm = o.comm.handle if o.comm is not None else None
+    return d
+
+
+# ------------------------------------------------------------------ multi-rank
+class Comm:
+    """NCCL communicator (one rank per GPU). Rank 0 creates the unique id."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().cf_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, world_size: int, rank: int, device: int, uid: bytes):
+        h = C.c_void_p()
+        check(lib().cf_comm_create(world_size, rank, device, uid, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib().cf_comm_destroy(self.handle)
+            self.handle = None
+
+
+# ------------------------------------------------------------------ solver
+class Solver:
+    """A device-resident plan: build_worker_model + init_worker_fields
+    (blocked.hpp:156-436), stepped with blocked_step semantics (:542-550)."""
+
+    def __init__(self, mesh: Mesh, setup: SimulationSetup, opts: Optional[SolveOptions] = None):
+        opts = opts or SolveOptions()
+        keep = _Keep()
+        self._N = mesh.node_count()
+        self.mesh = mesh
+        self.setup = setup
+        self.opts = opts
+        md, sd, ro = mesh_desc(mesh, keep), setup_desc(setup, keep), run_opts(opts, keep)
+        h = C.c_void_p()
+        check(lib().cf_plan_create(C.byref(md), C.byref(sd), C.byref(ro), C.byref(h)))
+        self.handle = h
+        if opts.graph_steps:
+            check(lib().cf_enable_graph(self.handle, opts.graph_steps))
+
+    # --- state
+    def set_temperature(self, T: np.ndarray) -> None:
+        T = np.ascontiguousarray(T, dtype=np.float64)
+        if T.shape != (self._N,):
+            raise InvalidArgument("temperature field must have one value per node")
+        check(lib().cf_set_temperature(self.handle, T.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def set_dt_safety(self, s: float) -> None:
+        check(lib().cf_set_dt_safety(self.handle, float(s)))
+
+    def step(self, n: int = 1, t_end: float = 0.0) -> None:
+        check(lib().cf_step(self.handle, int(n), float(t_end)))
+
+    def solve(self, max_steps: int = 0) -> List[SeriesSample]:
+        cap = 1 << 16
+        buf = np.zeros(3 * cap)
+        n = C.c_int64()
+        check(lib().cf_solve(self.handle, int(max_steps), buf.ctypes.data_as(C.POINTER(C.c_double)), cap,
+                             C.byref(n)))
+        k = min(n.value, cap)
+        return [SeriesSample(*buf[3 * i:3 * i + 3]) for i in range(k)]
+
+    def fields(self, want_H: bool = True) -> Tuple[np.ndarray, Optional[np.ndarray]]:
+        T = np.zeros(self._N)
+        H = np.zeros(self._N) if want_H else None
+        check(lib().cf_get_fields(self.handle, T.ctypes.data_as(C.POINTER(C.c_double)),
+                                  H.ctypes.data_as(C.POINTER(C.c_double)) if want_H else None))
+        return T, H
+
+    def stats(self) -> _abi.cf_stats:
+        s = _abi.cf_stats()
+        check(lib().cf_get_stats(self.handle, C.byref(s)))
+        return s
+
+    def enable_graph(self, steps: int) -> None:
+        check(lib().cf_enable_graph(self.handle, int(steps)))
+
+    def device_temperature(self, local_rank: int = 0) -> Tuple[int, int]:
+        p = C.POINTER(C.c_double)()
+        n = C.c_int64()
+        check(lib().cf_device_temperature(self.handle, local_rank, C.byref(p), C.byref(n)))
+        return C.cast(p, C.c_void_p).value, n.value
+
+    def estimate_lambda_max(self, iterations: int = 500, seed: int = 1234) -> Tuple[float, float]:
+        lam, e13 = C.c_double(), C.c_double()
+        check(lib().cf_estimate_lambda_max(self.handle, int(iterations), int(seed), C.byref(lam), C.byref(e13)))
+        return lam.value, e13.value
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            lib().cf_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def solve(mesh: Mesh, setup: SimulationSetup, opts: Optional[SolveOptions] = None) -> SolveResult:
+    """solve_serial (blocked.hpp:650-696) on the B200: same loop semantics
+    (max_steps, or run to setup.solver.t_end), same SolveResult fields;
+    loop_seconds is device time of the step loop (setup excluded)."""
+    opts = opts or SolveOptions()
+    with Solver(mesh, setup, opts) as s:
+        series = s.solve(opts.max_steps)
+        T, H = s.fields()
+        st = s.stats()
+        return SolveResult(T, H, st.time, st.step_index, st.loop_seconds, series, st.clamp_steps, st.n_tiles)
+
+
+solve_serial = solve
+
+
+# ------------------------------------------------------------------ host utilities
+def finalize_mesh(m: Mesh) -> Tuple[np.ndarray, np.ndarray]:
+    """finalize_mesh (mesh.hpp:148-207): returns (oriented tets, facet owners)."""
+    keep = _Keep()
+    d = mesh_desc(m, keep)
+    tets = np.zeros((m.element_count(), 4), np.int32)
+    owner = np.zeros(max(1, m.facets.shape[0]), np.int32)
+    check(lib().cf_finalize_mesh(C.byref(d), tets.ctypes.data_as(C.POINTER(C.c_int32)),
+                                 owner.ctypes.data_as(C.POINTER(C.c_int32))))
+    return tets, owner[:m.facets.shape[0]]
+
+
+def pair_sister_facets(m: Mesh) -> np.ndarray:
+    """pair_sister_facets (mesh.hpp:456-478): (P, 3) rows (facet, sister, contact)."""
+    keep = _Keep()
+    d = mesh_desc(m, keep)
+    n = C.c_int64()
+    check(lib().cf_pair_sister_facets(C.byref(d), None, 0, C.byref(n)))
+    out = np.zeros((max(1, n.value), 3), np.int32)
+    check(lib().cf_pair_sister_facets(C.byref(d), out.ctypes.data_as(C.POINTER(C.c_int32)), n.value, C.byref(n)))
+    return out[:n.value]
+
+
+def rcm_permutation(m: Mesh, seed: int = -1) -> np.ndarray:
+    """rcm_permutation(build_node_graph(m)) (reorder.hpp:17-24, 127-148): new_of_old."""
+    keep = _Keep()
+    d = mesh_desc(m, keep)
+    out = np.zeros(m.node_count(), np.int32)
+    check(lib().cf_rcm_permutation(C.byref(d), int(seed), out.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out
+
+
+def bandwidth(m: Mesh, new_of_old: Optional[np.ndarray] = None) -> int:
+    keep = _Keep()
+    d = mesh_desc(m, keep)
+    out = C.c_int64()
+    p = keep.iptr(new_of_old) if new_of_old is not None else None
+    check(lib().cf_bandwidth(C.byref(d), p, C.byref(out)))
+    return out.value
+
+
+def permute_mesh(m: Mesh, new_of_old: np.ndarray) -> Mesh:
+    """permute_mesh (reorder.hpp:152-163): renumbers nodes only."""
+    p = np.asarray(new_of_old, dtype=np.int64)
+    if p.shape[0] != m.node_count():
+        raise ValidationError(f"permutation size {p.shape[0]} does not match node count {m.node_count()}")
+    nodes = np.empty_like(m.nodes)
+    nodes[p] = m.nodes
+    ng = None
+    if m.node_grid is not None:
+        ng = np.empty_like(m.node_grid)
+        ng[p] = m.node_grid
+    return Mesh(nodes, p[m.tets].astype(np.int32), m.region.copy(), p[m.facets].astype(np.int32),
+                m.facet_tag.copy(), list(m.tags), list(m.contacts), ng)
+
+
+def partition_rcb(m: Mesh, parts: int) -> np.ndarray:
+    keep = _Keep()
+    d = mesh_desc(m, keep)
+    out = np.zeros(m.element_count(), np.int32)
+    check(lib().cf_partition_rcb(C.byref(d), int(parts), out.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out
+
+
+def tile_map(m: Mesh, setup: SimulationSetup, opts: SolveOptions) -> Tuple[np.ndarray, int]:
+    """Element -> tile map the plan would build (the BlockPlan the oracle replays)."""
+    keep = _Keep()
+    md, sd, ro = mesh_desc(m, keep), setup_desc(setup, keep), run_opts(opts, keep)
+    out = np.zeros(m.element_count(), np.int32)
+    n = C.c_int32()
+    check(lib().cf_tile_map(C.byref(md), C.byref(sd), C.byref(ro), out.ctypes.data_as(C.POINTER(C.c_int32)),
+                            C.byref(n)))
+    return out, n.value
+
+
+def generate_fixture(kind: str, n: int, radius: float = 0.35, jitter: float = 0.0, seed: int = 0,
+                     perm_seed: int = 0) -> Mesh:
+    """Structured Kuhn 6-tet fixtures (SPEC bench module S:502-519): 'cube' or 'casting'."""
+    k = {"cube": 0, "casting": 1}[kind]
+    fx = _abi.cf_fixture()
+    check(lib().cf_generate_fixture(k, n, radius, jitter, seed, perm_seed, C.byref(fx)))
+    N, E, F = fx.n_nodes, fx.n_elems, fx.n_facets
+    coords = np.zeros((N, 3))
+    tets = np.zeros((E, 4), np.int32)
+    region = np.zeros(E, np.int32)
+    facets = np.zeros((max(F, 1), 3), np.int32)
+    ftag = np.zeros(max(F, 1), np.int32)
+    grid = np.zeros(N, np.int32)
+    fx.coords = coords.ctypes.data_as(C.POINTER(C.c_double))
+    fx.tets = tets.ctypes.data_as(C.POINTER(C.c_int32))
+    fx.region = region.ctypes.data_as(C.POINTER(C.c_int32))
+    fx.facets = facets.ctypes.data_as(C.POINTER(C.c_int32))
+    fx.facet_tag = ftag.ctypes.data_as(C.POINTER(C.c_int32))
+    fx.node_grid = grid.ctypes.data_as(C.POINTER(C.c_int32))
+    check(lib().cf_generate_fixture(k, n, radius, jitter, seed, perm_seed, C.byref(fx)))
+    tags = ["outer", "cast_if", "mold_if"] if k == 1 else ["outer"]
+    contacts = [(1, 2)] if k == 1 else []
+    return Mesh(coords, tets, region, facets[:F], ftag[:F], tags, contacts, grid)
+
+
+def counter_uniform(seed: int, keys: np.ndarray, lo: float, hi: float) -> np.ndarray:
+    keys = np.ascontiguousarray(keys, dtype=np.int64)
+    out = np.zeros(keys.shape[0])
+    check(lib().cf_counter_uniform(int(seed), keys.ctypes.data_as(C.POINTER(C.c_int64)), keys.shape[0], lo, hi,
+                                   out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out

@@ -1,0 +1,87 @@
+"""BASELINE.json configs as seeded synthetic fixtures.
+
+The reference's case meshes are not available; BASELINE's configs
+are generator rules: Kuhn 6-tet split of structured cubes, the casting sphere
+by an exact cell-centre test, interface nodes duplicated, interior grid
+points jittered and numbering permuted for config 3. h_i (absent from
+BASELINE.json) is the builder's choice of 1000 W/m^2K, constant (SURVEY §0
+trap 3).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .castfem import (BoundaryCondition, InterfaceCoeff, MaterialTable, Mesh, PiecewiseLinear, SimulationSetup,
+                      SolverConfig, counter_uniform, generate_fixture)
+
+H_INTERFACE = 1000.0  # W/m^2K — builder-chosen, stated in every report
+DT_FACTOR = 0.9       # "dt = 0.9x the explicit stability limit" = 0.9 * 2 / lambda_max
+
+
+@dataclass
+class Case:
+    name: str
+    mesh: Mesh
+    setup: SimulationSetup
+    steps: int
+    note: str = ""
+
+
+def aluminium() -> MaterialTable:
+    return MaterialTable.make(rho=2700.0, c=900.0, k=200.0, latent_heat=3.9e5, solidus=821.0, liquidus=913.0,
+                              T0=973.0)
+
+
+def sand() -> MaterialTable:
+    return MaterialTable.make(rho=1500.0, c=1000.0, k=1.0, T0=300.0)
+
+
+def config1(n: int = 32, seed: int = 1, dt_safety: float = 0.14) -> Case:
+    """Single-material conduction, unit cube, h=100, T_inf=300, T0 = 973 + U(-1,1) per grid point."""
+    m = generate_fixture("cube", n)
+    mat = MaterialTable.make(rho=2700.0, c=900.0, k=200.0, T0=973.0)
+    T0 = 973.0 + counter_uniform(seed, m.node_grid.astype(np.int64), -1.0, 1.0)
+    setup = SimulationSetup(materials=[mat], boundary_conditions={"outer": BoundaryCondition("flux", h=100.0,
+                                                                                             t_inf=300.0)},
+                            solver=SolverConfig(dt_safety=dt_safety), initial_T=T0)
+    return Case(f"cfg1_cube{n}", m, setup, 100)
+
+
+def casting(n: int, jitter: float = 0.0, seed: int = 0, perm_seed: int = 0, dt_safety: float = 0.138,
+            steps: int = 1000, name: Optional[str] = None, h_interface: float = H_INTERFACE) -> Case:
+    """Two-material casting (configs 2-5): Al sphere r=0.35 in a sand mould, outer h=20, T_inf=300."""
+    m = generate_fixture("casting", n, radius=0.35, jitter=jitter, seed=seed, perm_seed=perm_seed)
+    setup = SimulationSetup(
+        materials=[aluminium(), sand()],
+        boundary_conditions={"outer": BoundaryCondition("flux", h=20.0, t_inf=300.0)},
+        interface_coeffs=[InterfaceCoeff("cast_if", "mold_if", "time", PiecewiseLinear.constant(h_interface))],
+        solver=SolverConfig(dt_safety=dt_safety))
+    return Case(name or f"casting{n}", m, setup, steps)
+
+
+def config2(n: int = 128, **kw) -> Case:
+    return casting(n, steps=1000, name=f"cfg2_casting{n}", **kw)
+
+
+def config3(n: int = 70, seed: int = 7, perm_seed: int = 11, **kw) -> Case:
+    return casting(n, jitter=0.2, seed=seed, perm_seed=perm_seed, steps=500, name=f"cfg3_jitter{n}", **kw)
+
+
+def config4(n: int = 256, **kw) -> Case:
+    return casting(n, steps=500, name=f"cfg4_casting{n}", **kw)
+
+
+def config5(n: int = 512, **kw) -> Case:
+    return casting(n, steps=200, name=f"cfg5_casting{n}", **kw)
+
+
+CONFIGS = {"cfg1": config1, "cfg2": config2, "cfg3": config3, "cfg4": config4, "cfg5": config5}
+
+
+def dt_safety_from_lambda(lam: float, eq13_min: float, factor: float = DT_FACTOR) -> float:
+    """dt* = factor * 2 / lambda_max mapped onto the reference's dt_safety
+    (dt = dt_safety * min_e rho c l^2 / k, blocked.hpp:340-350)."""
+    return min(1.0, factor * 2.0 / lam / eq13_min)

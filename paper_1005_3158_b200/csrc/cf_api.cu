@@ -1,0 +1,1140 @@
+// cf_api.cu — the C-ABI of include/castfem_b200.h: plan object, upload,
+// stepping (CUDA graphs), multi-rank exchange (in-process or NCCL), and the
+// host utilities. Reference interfaces replaced are cited at each entry point
+// in include/castfem_b200.h.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "cf_internal.hpp"
+#include "cf_kernels.cuh"
+
+using namespace cfb;
+
+// ------------------------------------------------------------------ errors
+namespace cfb {
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace cfb
+
+#define CF_CUDA_CHECK(x)                                                                                   \
+    do {                                                                                                   \
+        cudaError_t e_ = (x);                                                                              \
+        if (e_ != cudaSuccess) raise(CF_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        f();
+        return CF_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host out of memory");
+        return CF_INVALID_ARG;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return CF_INVALID_ARG;
+    }
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names)
+            if ((api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!api.h) return;
+        api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.h, "ncclGetUniqueId");
+        api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.h, "ncclCommInitRank");
+        api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
+        api.Send = (decltype(api.Send))dlsym(api.h, "ncclSend");
+        api.Recv = (decltype(api.Recv))dlsym(api.h, "ncclRecv");
+        api.GroupStart = (decltype(api.GroupStart))dlsym(api.h, "ncclGroupStart");
+        api.GroupEnd = (decltype(api.GroupEnd))dlsym(api.h, "ncclGroupEnd");
+        api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+    });
+    if (!api.h || !api.Send || !api.Recv || !api.CommInitRank) raise(CF_NCCL, "libnccl.so.2 not loadable");
+    return api;
+}
+#define CF_NCCL_CHECK(x)                                                                                 \
+    do {                                                                                                 \
+        ncclResult_t r_ = (x);                                                                           \
+        if (r_ != ncclSuccess) raise(CF_NCCL, std::string(#x) + ": " + nccl().GetErrorString(r_));       \
+    } while (0)
+}  // namespace
+
+struct cf_comm {
+    ncclComm_t comm = nullptr;
+    int world = 1, rank = 0, device = 0;
+};
+
+// ------------------------------------------------------------------ plan
+namespace {
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+};
+
+struct DeviceMem {
+    std::vector<void*> ptrs;
+    int64_t bytes = 0;
+    template <class T>
+    T* alloc(size_t n) {
+        if (n == 0) n = 1;
+        void* p = nullptr;
+        CF_CUDA_CHECK(cudaMalloc(&p, n * sizeof(T)));
+        ptrs.push_back(p);
+        bytes += (int64_t)(n * sizeof(T));
+        return (T*)p;
+    }
+    template <class T>
+    T* up(const std::vector<T>& v, cudaStream_t s) {
+        T* p = alloc<T>(v.size());
+        if (!v.empty()) CF_CUDA_CHECK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+        return p;
+    }
+    void release() {
+        for (void* p : ptrs) cudaFree(p);
+        ptrs.clear();
+    }
+};
+
+struct Rank {
+    int32_t rank = 0;
+    RankPlan H;          // host plan (metadata kept; big arrays cleared after upload)
+    DeviceMem mem;
+    TileArgs ta{};
+    UpdArgs ua{};
+    PackArgs pa{};
+    double* T[2] = {nullptr, nullptr};
+    double* recv = nullptr;
+    double* send = nullptr;
+    double* acc_c = nullptr;
+    double* acc_r = nullptr;
+    double* part_c = nullptr;
+    double* part_r = nullptr;
+    DevState* st = nullptr;
+    size_t tile_smem = 0;
+    int upd_blocks = 0;
+    int64_t bytes_per_step = 0;
+    std::vector<int64_t> nb_send_len, nb_recv_len;
+};
+
+}  // namespace
+
+struct cf_plan {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int mode = CF_MODE_ATOMIC;
+    int world = 1, first_rank = 0, local_ranks = 1;
+    cf_comm* comm = nullptr;
+    DevParams P{};
+    DevParams* dP = nullptr;
+    bool temp_dep = false, finite_range = false, any_dir = false;
+    std::vector<std::unique_ptr<Rank>> ranks;
+    int cur = 0;                 // index of the current T buffer
+    int32_t N_global = 0;
+    double loop_seconds = 0;
+    double eq13_min = 0;
+    double base_min_bound = 0;   // min_e rho c(0) l^2 / k(0) (static dt before the safety factor)
+    int64_t launches_per_step = 0;
+    int64_t output_every = 0;
+    double t_end_setup = 0;
+    // graph
+    int64_t graph_steps = 0;
+    cudaGraphExec_t graph = nullptr;
+    double graph_t_end = 0;
+    int graph_cur = -1;
+    ~cf_plan() {
+        if (graph) cudaGraphExecDestroy(graph);
+        for (auto& r : ranks) r->mem.release();
+        if (dP) cudaFree(dP);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+size_t tile_smem_bytes(const RankPlan& h) {
+    return sizeof(double) * (2 * (size_t)h.max_slots + 5 * (size_t)h.max_elems + 3 * (size_t)h.max_facets);
+}
+
+template <bool DET, bool TDEP>
+void set_tile_attr(size_t smem) {
+    CF_CUDA_CHECK(cudaFuncSetAttribute(tile_kernel<DET, TDEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+void launch_tile(cf_plan* p, Rank& r) {
+    if (r.H.n_tiles == 0) return;
+    const bool det = p->mode == CF_MODE_DETERMINISTIC;
+    TileArgs a = r.ta;
+    a.T = p->ranks.size() ? r.T[p->cur] : nullptr;
+    a.Told = r.T[p->cur ^ 1];
+    const dim3 grid(r.H.n_tiles), block(256);
+    if (det && p->temp_dep) tile_kernel<true, true><<<grid, block, r.tile_smem, p->stream>>>(a);
+    else if (det) tile_kernel<true, false><<<grid, block, r.tile_smem, p->stream>>>(a);
+    else if (p->temp_dep) tile_kernel<false, true><<<grid, block, r.tile_smem, p->stream>>>(a);
+    else tile_kernel<false, false><<<grid, block, r.tile_smem, p->stream>>>(a);
+}
+
+template <bool DET, bool MULTI>
+void launch_update_t(cf_plan* p, Rank& r, const UpdArgs& a) {
+    const dim3 grid(r.upd_blocks), block(256);
+    const bool dir = !r.H.node_dir.empty() || r.ua.node_dir != nullptr;
+    const bool cl = p->finite_range;
+    const bool td = p->temp_dep;
+#define CF_UPD(D, C, T) update_kernel<DET, MULTI, D, C, T><<<grid, block, 0, p->stream>>>(a)
+    if (dir) {
+        if (cl) { if (td) CF_UPD(true, true, true); else CF_UPD(true, true, false); }
+        else { if (td) CF_UPD(true, false, true); else CF_UPD(true, false, false); }
+    } else {
+        if (cl) { if (td) CF_UPD(false, true, true); else CF_UPD(false, true, false); }
+        else { if (td) CF_UPD(false, false, true); else CF_UPD(false, false, false); }
+    }
+#undef CF_UPD
+}
+
+void launch_update(cf_plan* p, Rank& r, double t_end) {
+    UpdArgs a = r.ua;
+    a.T = r.T[p->cur];
+    a.Tcur_w = r.T[p->cur];
+    a.Tn = r.T[p->cur ^ 1];
+    a.t_end = t_end;
+    const bool det = p->mode == CF_MODE_DETERMINISTIC;
+    const bool multi = p->world > 1;
+    if (det && multi) launch_update_t<true, true>(p, r, a);
+    else if (det) launch_update_t<true, false>(p, r, a);
+    else if (multi) launch_update_t<false, true>(p, r, a);
+    else launch_update_t<false, false>(p, r, a);
+}
+
+void launch_pack(cf_plan* p, Rank& r) {
+    if (r.pa.n_cr + r.pa.n_t == 0) return;
+    PackArgs a = r.pa;
+    a.T = r.T[p->cur];
+    a.u.T = r.T[p->cur];
+    const int blocks = std::max(1, std::min<int>(1184, (a.n_cr + a.n_t + 255) / 256));
+    if (p->mode == CF_MODE_DETERMINISTIC) pack_kernel<true><<<blocks, 256, 0, p->stream>>>(a);
+    else pack_kernel<false><<<blocks, 256, 0, p->stream>>>(a);
+}
+
+void exchange(cf_plan* p) {
+    if (p->world == 1) return;
+    if (p->local_ranks == p->world) {
+        // in-process transport: every rank's send region for q -> q's recv region for r
+        for (auto& rp : p->ranks) {
+            Rank& r = *rp;
+            for (size_t k = 0; k < r.H.nbrs.size(); ++k) {
+                const int q = r.H.nbrs[k].rank;
+                Rank& dst = *p->ranks[q - p->first_rank];
+                size_t kk = 0;
+                while (kk < dst.H.nbrs.size() && dst.H.nbrs[kk].rank != r.rank) ++kk;
+                if (kk == dst.H.nbrs.size()) raise(CF_PROTOCOL, "asymmetric neighbour lists");
+                const int64_t len = r.nb_send_len[k];
+                if (len != dst.nb_recv_len[kk]) raise(CF_PROTOCOL, "payload length mismatch");
+                if (len)
+                    CF_CUDA_CHECK(cudaMemcpyAsync(dst.recv + dst.H.recv_off[kk], r.send + r.H.send_off[k],
+                                                  len * sizeof(double), cudaMemcpyDeviceToDevice, p->stream));
+            }
+        }
+        return;
+    }
+    if (!p->comm) raise(CF_NCCL, "world_size > local ranks but no communicator");
+    NcclApi& n = nccl();
+    Rank& r = *p->ranks[0];
+    CF_NCCL_CHECK(n.GroupStart());
+    for (size_t k = 0; k < r.H.nbrs.size(); ++k) {
+        const int q = r.H.nbrs[k].rank;
+        if (r.nb_send_len[k])
+            CF_NCCL_CHECK(n.Send(r.send + r.H.send_off[k], r.nb_send_len[k], ncclFloat64, q, p->comm->comm, p->stream));
+        if (r.nb_recv_len[k])
+            CF_NCCL_CHECK(n.Recv(r.recv + r.H.recv_off[k], r.nb_recv_len[k], ncclFloat64, q, p->comm->comm, p->stream));
+    }
+    CF_NCCL_CHECK(n.GroupEnd());
+}
+
+// one blocked_step for every local rank
+void enqueue_step(cf_plan* p, double t_end) {
+    for (auto& r : p->ranks) launch_tile(p, *r);
+    if (p->world > 1) {
+        for (auto& r : p->ranks) launch_pack(p, *r);
+        exchange(p);
+    }
+    for (auto& r : p->ranks) launch_update(p, *r, t_end);
+    p->cur ^= 1;
+}
+
+void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
+    RankPlan& h = r.H;
+    DeviceMem& M = r.mem;
+    cudaStream_t s = p->stream;
+    const int64_t S_tot = h.tile_slot_off.empty() ? 0 : h.tile_slot_off.back();
+    const int64_t Er = (int64_t)h.elem_global.size();
+    const int64_t nT = (int64_t)h.n_local + h.n_ghost;
+
+    r.T[0] = M.alloc<double>(nT);
+    r.T[1] = M.alloc<double>(nT);
+    r.st = M.alloc<DevState>(1);
+    TileArgs& a = r.ta;
+    a.tile_elem_off = M.up(h.tile_elem_off, s);
+    a.tile_slot_off = M.up(h.tile_slot_off, s);
+    a.tile_csr_off = M.up(h.tile_csr_off, s);
+    a.tile_facet_off = M.up(h.tile_facet_off, s);
+    {
+        ushort4* c = M.alloc<ushort4>(Er);
+        if (Er) CF_CUDA_CHECK(cudaMemcpyAsync(c, h.elem_conn.data(), Er * sizeof(ushort4), cudaMemcpyHostToDevice, s));
+        a.conn = c;
+    }
+    a.ereg = M.up(h.elem_region, s);
+    a.geom = M.up(h.elem_geom, s);
+    a.min_edge = S.temp_dep ? M.up(h.elem_min_edge, s) : nullptr;
+    a.E = Er;
+    a.slot_node = M.up(h.slot_node, s);
+    a.slot_info = M.up(h.slot_info, s);
+    a.slot_csr_end = M.up(h.slot_csr_end, s);
+    a.csr = M.up(h.csr, s);
+    {
+        const int64_t Fr = (int64_t)h.facet_area.size();
+        ushort4* fs = M.alloc<ushort4>(Fr);
+        int4* fsis = M.alloc<int4>(Fr);
+        if (Fr) {
+            CF_CUDA_CHECK(cudaMemcpyAsync(fs, h.facet_slots.data(), Fr * sizeof(ushort4), cudaMemcpyHostToDevice, s));
+            CF_CUDA_CHECK(cudaMemcpyAsync(fsis, h.facet_sister.data(), Fr * sizeof(int4), cudaMemcpyHostToDevice, s));
+        }
+        a.fslots = fs;
+        a.fsister = fsis;
+        a.farea = M.up(h.facet_area, s);
+    }
+    const bool det = p->mode == CF_MODE_DETERMINISTIC;
+    if (det) {
+        r.part_c = M.alloc<double>(S_tot);
+        r.part_r = M.alloc<double>(S_tot);
+    } else {
+        r.acc_c = M.alloc<double>(h.n_local);
+        r.acc_r = M.alloc<double>(h.n_local);
+        CF_CUDA_CHECK(cudaMemsetAsync(r.acc_c, 0, sizeof(double) * std::max<int64_t>(1, h.n_local), s));
+        CF_CUDA_CHECK(cudaMemsetAsync(r.acc_r, 0, sizeof(double) * std::max<int64_t>(1, h.n_local), s));
+    }
+    a.part_c = r.part_c;
+    a.part_r = r.part_r;
+    a.acc_c = r.acc_c;
+    a.acc_r = r.acc_r;
+    a.P = p->dP;
+    a.st = r.st;
+    a.max_slots = h.max_slots;
+    a.max_elems = h.max_elems;
+    a.max_facets = h.max_facets;
+    r.tile_smem = tile_smem_bytes(h);
+    if (r.tile_smem > 227 * 1024) raise(CF_INVALID_ARG, "tile shared-memory footprint exceeds 227 KB; use smaller tiles");
+    if (det && p->temp_dep) set_tile_attr<true, true>(r.tile_smem);
+    else if (det) set_tile_attr<true, false>(r.tile_smem);
+    else if (p->temp_dep) set_tile_attr<false, true>(r.tile_smem);
+    else set_tile_attr<false, false>(r.tile_smem);
+
+    UpdArgs& u = r.ua;
+    u.n_local = h.n_local;
+    u.n_ghost = h.n_ghost;
+    if (det) {
+        u.merge_off = M.up(h.merge_off, s);
+        u.merge_idx = M.up(h.merge_idx, s);
+    }
+    u.part_c = r.part_c;
+    u.part_r = r.part_r;
+    u.acc_c = r.acc_c;
+    u.acc_r = r.acc_r;
+    u.node_dir = h.node_dir.empty() ? nullptr : M.up(h.node_dir, s);
+    u.node_region = M.up(h.node_region, s);
+    u.local_global = M.up(h.local_global, s);
+    u.P = p->dP;
+    u.st = r.st;
+    if (p->world > 1) {
+        u.node_shared = M.up(h.node_shared, s);
+        u.shared_off = M.up(h.shared_off, s);
+        // r index = c index + neighbour's shared count
+        std::vector<int32_t> src_r(h.shared_src.size());
+        {
+            std::vector<int32_t> ns_of_pos;  // map recv c-offset -> r-offset
+            for (size_t j = 0; j < h.shared_src.size(); ++j) {
+                const int32_t c = h.shared_src[j];
+                if (c < 0) {
+                    src_r[j] = -1;
+                    continue;
+                }
+                size_t k = 0;
+                while (k + 1 < h.recv_off.size() && !(c >= h.recv_off[k] && c < h.recv_off[k + 1])) ++k;
+                src_r[j] = c + (int32_t)h.nbrs[k].shared.size();
+            }
+        }
+        u.shared_src_c = M.up(h.shared_src, s);
+        u.shared_src_r = M.up(src_r, s);
+        r.recv = M.alloc<double>(h.recv_len);
+        r.send = M.alloc<double>(h.send_len);
+        u.recv = r.recv;
+        u.ghost_src = M.up(h.ghost_src, s);
+        // pack items
+        std::vector<int32_t> cr_node, t_node;
+        std::vector<int64_t> cr_dst, cr_dst_r, t_dst;
+        for (size_t k = 0; k < h.nbrs.size(); ++k) {
+            const auto& x = h.nbrs[k];
+            const int64_t base = h.send_off[k];
+            const int64_t ns = (int64_t)x.shared.size();
+            for (int64_t j = 0; j < ns; ++j) {
+                cr_node.push_back(x.shared[j]);
+                cr_dst.push_back(base + j);
+                cr_dst_r.push_back(base + ns + j);
+            }
+            for (size_t j = 0; j < x.ext_to.size(); ++j) {
+                t_node.push_back(x.ext_to[j]);
+                t_dst.push_back(base + 2 * ns + (int64_t)j);
+            }
+            r.nb_send_len.push_back(2 * ns + (int64_t)x.ext_to.size());
+            r.nb_recv_len.push_back(2 * ns + (int64_t)x.ext_from.size());
+        }
+        PackArgs& pk = r.pa;
+        pk.n_cr = (int32_t)cr_node.size();
+        pk.n_t = (int32_t)t_node.size();
+        pk.cr_node = M.up(cr_node, s);
+        pk.cr_dst = M.up(cr_dst, s);
+        pk.cr_dst_r = M.up(cr_dst_r, s);
+        pk.t_node = M.up(t_node, s);
+        pk.t_dst = M.up(t_dst, s);
+        pk.send = r.send;
+        pk.u = u;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+    r.upd_blocks = std::max(1, std::min<int>(sms * 8, (int)((h.n_local + 255) / 256)));
+    // canonical algorithmic bytes: 105 E + 48 N + 24 F_bc + 56 F_if
+    r.bytes_per_step = 105 * Er + 48 * (int64_t)h.n_local + 24 * h.n_bc_facets + 56 * h.n_if_facets;
+    // drop the big host arrays (metadata kept)
+    std::vector<uint16_t>().swap(h.elem_conn);
+    std::vector<double>().swap(h.elem_geom);
+    std::vector<double>().swap(h.elem_min_edge);
+    std::vector<uint16_t>().swap(h.csr);
+    std::vector<uint16_t>().swap(h.slot_csr_end);
+    std::vector<int32_t>().swap(h.merge_idx);
+    std::vector<double>().swap(h.facet_area);
+    std::vector<uint16_t>().swap(h.facet_slots);
+    std::vector<int32_t>().swap(h.facet_sister);
+}
+
+void init_state(cf_plan* p, const std::vector<double>& T_global) {
+    for (auto& rp : p->ranks) {
+        Rank& r = *rp;
+        const int64_t nT = (int64_t)r.H.n_local + r.H.n_ghost;
+        std::vector<double> T(nT);
+        for (int64_t i = 0; i < nT; ++i) T[i] = T_global[r.H.local_global[i]];
+        CF_CUDA_CHECK(cudaMemcpyAsync(r.T[0], T.data(), nT * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+        CF_CUDA_CHECK(cudaMemcpyAsync(r.T[1], T.data(), nT * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+        DevState st{};
+        st.time = 0;
+        st.dt = 0;
+        st.step_index = 0;
+        st.clamp_steps = 0;
+        st.min_bound[0] = st.min_bound[1] = 0x7ff0000000000000ull;
+        st.clamp_flag = 0;
+        st.ticket = 0;
+        st.err_node = INT32_MAX;
+        st.done = 0;
+        CF_CUDA_CHECK(cudaMemcpyAsync(r.st, &st, sizeof st, cudaMemcpyHostToDevice, p->stream));
+        CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));  // T is a stack vector
+    }
+    p->cur = 0;
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+}
+
+DevState read_state(cf_plan* p, int k = 0) {
+    DevState st;
+    CF_CUDA_CHECK(cudaMemcpyAsync(&st, p->ranks[k]->st, sizeof st, cudaMemcpyDeviceToHost, p->stream));
+    CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+    return st;
+}
+
+void check_device_errors(cf_plan* p) {
+    for (size_t k = 0; k < p->ranks.size(); ++k) {
+        const DevState st = read_state(p, (int)k);
+        if (st.err_node != INT32_MAX)
+            raise(CF_VALIDATION, "zero lumped capacitance at active node " + std::to_string(st.err_node));
+    }
+}
+
+void run_steps(cf_plan* p, int64_t n, double t_end) {
+    if (n <= 0) return;
+    CF_CUDA_CHECK(cudaSetDevice(p->device));
+    CF_CUDA_CHECK(cudaEventRecord(p->ev0, p->stream));
+    int64_t done = 0;
+    if (p->graph_steps > 0) {
+        if (p->graph && (p->graph_t_end != t_end || p->graph_cur != p->cur)) {
+            cudaGraphExecDestroy(p->graph);
+            p->graph = nullptr;
+        }
+        if (!p->graph && n >= p->graph_steps) {
+            const int cur0 = p->cur;
+            cudaGraph_t g;
+            CF_CUDA_CHECK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+            for (int64_t s = 0; s < p->graph_steps; ++s) enqueue_step(p, t_end);
+            CF_CUDA_CHECK(cudaStreamEndCapture(p->stream, &g));
+            CF_CUDA_CHECK(cudaGraphInstantiate(&p->graph, g, 0));
+            cudaGraphDestroy(g);
+            p->cur = cur0;  // capture did not execute
+            p->graph_t_end = t_end;
+            p->graph_cur = cur0;
+        }
+        while (p->graph && n - done >= p->graph_steps) {
+            CF_CUDA_CHECK(cudaGraphLaunch(p->graph, p->stream));
+            if (p->graph_steps & 1) p->cur ^= 1;
+            done += p->graph_steps;
+            if (p->graph_cur != p->cur) break;  // odd graph length: recapture next call
+        }
+    }
+    for (; done < n; ++done) enqueue_step(p, t_end);
+    CF_CUDA_CHECK(cudaGetLastError());
+    CF_CUDA_CHECK(cudaEventRecord(p->ev1, p->stream));
+    CF_CUDA_CHECK(cudaEventSynchronize(p->ev1));
+    float ms = 0;
+    CF_CUDA_CHECK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+    p->loop_seconds += ms * 1e-3;
+    check_device_errors(p);
+}
+
+// ------------------------------------------------------------------ lambda_max kernels
+struct LamArgs {
+    TileArgs a;
+    const double* cval;  // per region rho*c(T0)
+    const double* kval;  // per region k(T0)
+    const double* hval;  // per facet kind h at t=0 / T0
+    const double* x;
+    double* y;
+    double* M;
+    double* D;
+};
+
+__global__ void lam_setup(LamArgs L) {
+    const TileArgs& a = L.a;
+    const int t = blockIdx.x;
+    const int e0 = a.tile_elem_off[t], ne = a.tile_elem_off[t + 1] - e0, s0 = a.tile_slot_off[t];
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+        const int64_t p = (int64_t)e0 + i;
+        const ushort4 cn = a.conn[p];
+        const double w = L.cval[a.ereg[p]] * a.geom[9 * a.E + p] * 0.25;
+        const unsigned short s[4] = {cn.x, cn.y, cn.z, cn.w};
+        for (int k = 0; k < 4; ++k) atomicAdd(&L.M[a.slot_node[s0 + s[k]]], w);
+    }
+    const int f0 = a.tile_facet_off[t], nf = a.tile_facet_off[t + 1] - f0;
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+        const ushort4 fs = a.fslots[f0 + i];
+        const double w = L.hval[fs.w] * (a.farea[f0 + i] / 3.0);
+        const unsigned short s[3] = {fs.x, fs.y, fs.z};
+        for (int k = 0; k < 3; ++k) atomicAdd(&L.D[a.slot_node[s0 + s[k]]], w);
+    }
+}
+
+__global__ void lam_apply(LamArgs L) {
+    const TileArgs& a = L.a;
+    const int t = blockIdx.x;
+    const int e0 = a.tile_elem_off[t], ne = a.tile_elem_off[t + 1] - e0, s0 = a.tile_slot_off[t];
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+        const int64_t p = (int64_t)e0 + i;
+        const ushort4 cn = a.conn[p];
+        const int32_t n[4] = {a.slot_node[s0 + cn.x], a.slot_node[s0 + cn.y], a.slot_node[s0 + cn.z],
+                              a.slot_node[s0 + cn.w]};
+        double g[4][3];
+        for (int k = 0; k < 3; ++k) {
+            g[1][k] = a.geom[(int64_t)k * a.E + p];
+            g[2][k] = a.geom[(int64_t)(3 + k) * a.E + p];
+            g[3][k] = a.geom[(int64_t)(6 + k) * a.E + p];
+            g[0][k] = ((g[1][k] + g[2][k]) + g[3][k]) * -1.0;
+        }
+        const double kv = L.kval[a.ereg[p]] * a.geom[9 * a.E + p];
+        double gx = 0, gy = 0, gz = 0;
+        for (int b = 0; b < 4; ++b) {
+            const double xb = L.x[n[b]];
+            gx += g[b][0] * xb;
+            gy += g[b][1] * xb;
+            gz += g[b][2] * xb;
+        }
+        for (int k = 0; k < 4; ++k) atomicAdd(&L.y[n[k]], kv * (g[k][0] * gx + g[k][1] * gy + g[k][2] * gz));
+    }
+}
+
+__global__ void lam_init_x(int32_t n, const int32_t* gid, const int8_t* dir, uint64_t seed, double* x) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t key = (uint64_t)gid[i];
+        uint64_t z = seed * 0x9E3779B97F4A7C15ull + key + 0x632BE59BD9B4E019ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const double u = (double)(z >> 11) * (1.0 / 9007199254740992.0);
+        x[i] = (dir && dir[i] >= 0) ? 0.0 : (u - 0.5);
+    }
+}
+__global__ void lam_diag(int32_t n, const double* D, const double* x, double* y) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] = D[i] * x[i];
+}
+// num = x.y, den = x.M.x ; y <- y / M ; nrm2 = y.M.y
+__global__ void lam_reduce(int32_t n, const int8_t* dir, const double* M, const double* x, double* y, double* acc) {
+    double a0 = 0, a1 = 0, a2 = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double yi = y[i];
+        if (dir && dir[i] >= 0) yi = 0;
+        a0 += x[i] * yi;
+        a1 += x[i] * M[i] * x[i];
+        yi = yi / M[i];
+        a2 += yi * M[i] * yi;
+        y[i] = yi;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&acc[0], a0);
+        atomicAdd(&acc[1], a1);
+        atomicAdd(&acc[2], a2);
+    }
+}
+__global__ void lam_scale(int32_t n, const double* y, const double* acc, double* x) {
+    const double inv = 1.0 / sqrt(acc[2]);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = y[i] * inv;
+}
+
+__global__ void minmax_kernel(int32_t n, const double* T, double* out) {
+    double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        lo = fmin(lo, T[i]);
+        hi = fmax(hi, T[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        // min/max of doubles via ordered integer atomics on a sign-aware encoding
+        auto enc = [](double v) {
+            long long b = __double_as_longlong(v);
+            return (unsigned long long)(b < 0 ? ~b : (b | 0x8000000000000000ll));
+        };
+        atomicMin((unsigned long long*)&out[0], enc(lo));
+        atomicMax((unsigned long long*)&out[1], enc(hi));
+    }
+}
+double dec_ordered(unsigned long long u) {
+    long long b = (u & 0x8000000000000000ull) ? (long long)(u & 0x7fffffffffffffffull) : (long long)~u;
+    double d;
+    std::memcpy(&d, &b, 8);
+    return d;
+}
+
+}  // namespace
+
+// ================================================================== C-ABI
+extern "C" {
+
+int cf_abi_version(void) { return CF_ABI_VERSION; }
+
+int cf_last_error(char* buf, size_t len) {
+    if (!buf || !len) return CF_INVALID_ARG;
+    std::snprintf(buf, len, "%s", g_last_error.c_str());
+    return CF_OK;
+}
+
+int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts, cf_plan** out) {
+    return guarded([&] {
+        if (!mesh || !setup || !out) raise(CF_INVALID_ARG, "null argument");
+        *out = nullptr;
+        cf_run_opts o{};
+        o.world_size = 1;
+        o.local_ranks = 1;
+        o.node_order = CF_NODE_ORDER_RCM;
+        o.elem_order = CF_ELEM_ORDER_MORTON;
+        if (opts) o = *opts;
+        if (o.world_size < 1) o.world_size = 1;
+        if (o.local_ranks < 1) o.local_ranks = 1;
+        if (o.rank < 0 || o.rank + o.local_ranks > o.world_size) raise(CF_INVALID_ARG, "bad rank / local_ranks");
+        if (o.local_ranks != 1 && o.local_ranks != o.world_size)
+            raise(CF_INVALID_ARG, "local_ranks must be 1 or world_size");
+        if (o.mode != CF_MODE_ATOMIC && o.mode != CF_MODE_DETERMINISTIC) raise(CF_INVALID_ARG, "bad mode");
+        int tile = o.tile_elems > 0 ? o.tile_elems : 1024;
+        if (tile > kMaxTileElems) raise(CF_INVALID_ARG, "tile_elems must be <= 2048");
+
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) raise(CF_CUDA, "no CUDA device available");
+        if (o.device < 0 || o.device >= ndev) raise(CF_INVALID_ARG, "bad device ordinal");
+        CF_CUDA_CHECK(cudaSetDevice(o.device));
+
+        MeshData m;
+        std::vector<Geom> geom;
+        finalize_mesh(mesh, m, &geom);
+        SetupData S;
+        resolve_setup(m, geom, setup, S);
+        if (o.world_size > 1 && S.temp_dep)
+            raise(CF_CONFIG, "temperature-dependent tables (dynamic dt) need world_size == 1 in this build");
+
+        std::vector<int32_t> label(m.N);
+        if (o.node_order == CF_NODE_ORDER_RCM) {
+            const Graph g = build_node_graph(m.N, m.E, m.tets.data());
+            label = rcm_permutation(g, -1);
+        } else {
+            std::iota(label.begin(), label.end(), 0);
+        }
+        std::vector<int32_t> part;
+        PlanOptions po;
+        po.mode = o.mode;
+        po.node_order = o.node_order;
+        po.elem_order = o.elem_order;
+        po.tile_elems = tile;
+        po.tile_of_element = o.tile_of_element;
+        po.n_tiles_given = o.n_tiles_given;
+        po.world_size = o.world_size;
+        if (o.world_size > 1) {
+            if (o.partition == CF_PARTITION_GIVEN) {
+                if (!o.part_of_element) raise(CF_INVALID_ARG, "part_of_element required");
+                part.assign(o.part_of_element, o.part_of_element + m.E);
+                for (int32_t v : part)
+                    if (v < 0 || v >= o.world_size) raise(CF_VALIDATION, "part id out of range");
+            } else {
+                part = partition_rcb(m, o.world_size);
+            }
+            po.part_of_element = part.data();
+        }
+
+        auto p = std::make_unique<cf_plan>();
+        p->device = o.device;
+        p->mode = o.mode;
+        p->world = o.world_size;
+        p->first_rank = o.rank;
+        p->local_ranks = o.local_ranks;
+        p->comm = (cf_comm*)o.comm;
+        if (p->world > p->local_ranks && !p->comm) raise(CF_NCCL, "world_size > local_ranks needs a cf_comm");
+        p->P = S.P;
+        p->temp_dep = S.temp_dep;
+        p->finite_range = S.P.finite_range != 0;
+        p->N_global = m.N;
+        p->output_every = setup->output_every;
+        p->t_end_setup = setup->t_end;
+        CF_CUDA_CHECK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+        CF_CUDA_CHECK(cudaEventCreate(&p->ev0));
+        CF_CUDA_CHECK(cudaEventCreate(&p->ev1));
+        CF_CUDA_CHECK(cudaMalloc(&p->dP, sizeof(DevParams)));
+        CF_CUDA_CHECK(cudaMemcpy(p->dP, &p->P, sizeof(DevParams), cudaMemcpyHostToDevice));
+        double e13 = INFINITY;
+        for (int64_t e = 0; e < m.E; ++e) {
+            const DevMaterial& mm = S.P.mat[m.region[e]];
+            const double c0 = pl_eval(S.P, mm.c, 0), k0 = pl_eval(S.P, mm.k, 0);
+            e13 = std::min(e13, mm.rho * c0 * geom[e].min_edge * geom[e].min_edge / k0);
+        }
+        p->eq13_min = e13;
+        p->base_min_bound = S.min_bound;
+        for (int r = o.rank; r < o.rank + o.local_ranks; ++r) {
+            auto rk = std::make_unique<Rank>();
+            rk->rank = r;
+            build_rank_plan(m, geom, S, po, label, r, rk->H);
+            upload_rank(p.get(), *rk, S);
+            p->ranks.push_back(std::move(rk));
+        }
+        p->launches_per_step = 2 * (int64_t)p->ranks.size() + (p->world > 1 ? (int64_t)p->ranks.size() : 0);
+        init_state(p.get(), S.T0);
+        CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+        *out = p.release();
+    });
+}
+
+int cf_plan_destroy(cf_plan* plan) {
+    return guarded([&] {
+        if (!plan) return;
+        cudaSetDevice(plan->device);
+        cudaStreamSynchronize(plan->stream);
+        delete plan;
+    });
+}
+
+int cf_set_temperature(cf_plan* p, const double* T_host) {
+    return guarded([&] {
+        if (!p || !T_host) raise(CF_INVALID_ARG, "null argument");
+        CF_CUDA_CHECK(cudaSetDevice(p->device));
+        std::vector<double> T(T_host, T_host + p->N_global);
+        init_state(p, T);
+        p->loop_seconds = 0;
+    });
+}
+
+int cf_step(cf_plan* p, int64_t n_steps, double t_end) {
+    return guarded([&] {
+        if (!p) raise(CF_INVALID_ARG, "null plan");
+        run_steps(p, n_steps, t_end);
+    });
+}
+
+int cf_set_dt_safety(cf_plan* p, double s) {
+    return guarded([&] {
+        if (!p) raise(CF_INVALID_ARG, "null plan");
+        if (!(s > 0 && s <= 1)) raise(CF_CONFIG, "safety must be in (0, 1]");
+        CF_CUDA_CHECK(cudaSetDevice(p->device));
+        p->P.dt_safety = s;
+        if (!p->temp_dep) p->P.static_dt = p->base_min_bound * s;
+        CF_CUDA_CHECK(cudaMemcpyAsync(p->dP, &p->P, sizeof(DevParams), cudaMemcpyHostToDevice, p->stream));
+        CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+    });
+}
+
+int cf_enable_graph(cf_plan* p, int64_t steps) {
+    return guarded([&] {
+        if (!p) raise(CF_INVALID_ARG, "null plan");
+        if (p->graph) {
+            cudaGraphExecDestroy(p->graph);
+            p->graph = nullptr;
+        }
+        p->graph_steps = std::max<int64_t>(0, steps);
+    });
+}
+
+int cf_solve(cf_plan* p, int64_t max_steps, double* series, int64_t cap, int64_t* n_series) {
+    return guarded([&] {
+        if (!p) raise(CF_INVALID_ARG, "null plan");
+        CF_CUDA_CHECK(cudaSetDevice(p->device));
+        int64_t ns = 0;
+        const int64_t every = p->output_every;
+        double* mm = nullptr;
+        if (every > 0) CF_CUDA_CHECK(cudaMalloc(&mm, 2 * sizeof(double)));
+        auto sample = [&]() {
+            unsigned long long init[2] = {~0ull, 0ull};
+            CF_CUDA_CHECK(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, p->stream));
+            for (auto& r : p->ranks)
+                minmax_kernel<<<148, 256, 0, p->stream>>>(r->H.n_local, r->T[p->cur], mm);
+            unsigned long long res[2];
+            CF_CUDA_CHECK(cudaMemcpyAsync(res, mm, sizeof res, cudaMemcpyDeviceToHost, p->stream));
+            const DevState st = read_state(p);
+            if (series && ns < cap) {
+                series[3 * ns] = st.time;
+                series[3 * ns + 1] = dec_ordered(res[0]);
+                series[3 * ns + 2] = dec_ordered(res[1]);
+            }
+            ++ns;
+        };
+        if (max_steps > 0) {
+            DevState st = read_state(p);
+            int64_t left = max_steps - st.step_index;
+            while (left > 0) {
+                int64_t chunk = left;
+                if (every > 0) chunk = std::min<int64_t>(left, every - (int64_t)(st.step_index % every));
+                run_steps(p, chunk, 0.0);
+                left -= chunk;
+                st.step_index += chunk;
+                if (every > 0 && st.step_index % every == 0) sample();
+            }
+        } else {
+            const double t_end = p->t_end_setup;
+            for (;;) {
+                DevState st = read_state(p);
+                if (!(st.time < t_end)) break;
+                const int64_t chunk = every > 0 ? every - (int64_t)(st.step_index % every) : 256;
+                run_steps(p, chunk, t_end);
+                const DevState s2 = read_state(p);
+                if (every > 0 && s2.step_index % every == 0 && s2.step_index != st.step_index) sample();
+            }
+        }
+        if (mm) cudaFree(mm);
+        if (n_series) *n_series = ns;
+    });
+}
+
+int cf_get_fields(cf_plan* p, double* T_host, double* H_host) {
+    return guarded([&] {
+        if (!p) raise(CF_INVALID_ARG, "null plan");
+        CF_CUDA_CHECK(cudaSetDevice(p->device));
+        for (auto& rp : p->ranks) {
+            Rank& r = *rp;
+            const int32_t n = r.H.n_local;
+            std::vector<double> T(n), H(n);
+            if (T_host) CF_CUDA_CHECK(cudaMemcpyAsync(T.data(), r.T[p->cur], n * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+            if (H_host) {
+                double* dH = nullptr;
+                CF_CUDA_CHECK(cudaMallocAsync(&dH, std::max<size_t>(1, n) * sizeof(double), p->stream));
+                const int blocks = std::max(1, std::min(1184, (n + 255) / 256));
+                if (p->temp_dep) enthalpy_kernel<true><<<blocks, 256, 0, p->stream>>>(n, r.T[p->cur], r.ua.node_region, p->dP, dH);
+                else enthalpy_kernel<false><<<blocks, 256, 0, p->stream>>>(n, r.T[p->cur], r.ua.node_region, p->dP, dH);
+                CF_CUDA_CHECK(cudaMemcpyAsync(H.data(), dH, n * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+                CF_CUDA_CHECK(cudaFreeAsync(dH, p->stream));
+            }
+            CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+            for (int32_t i = 0; i < n; ++i) {
+                const int32_t g = r.H.local_global[i];
+                if (T_host) T_host[g] = T[i];
+                if (H_host) H_host[g] = H[i];
+            }
+        }
+    });
+}
+
+int cf_get_stats(cf_plan* p, cf_stats* out) {
+    return guarded([&] {
+        if (!p || !out) raise(CF_INVALID_ARG, "null argument");
+        CF_CUDA_CHECK(cudaSetDevice(p->device));
+        const DevState st = read_state(p);
+        std::memset(out, 0, sizeof *out);
+        out->time = st.time;
+        out->dt = st.dt;
+        out->step_index = st.step_index;
+        out->clamp_steps = st.clamp_steps;
+        out->loop_seconds = p->loop_seconds;
+        out->static_dt = p->temp_dep ? 0 : p->P.static_dt;
+        out->dynamic_dt = p->temp_dep;
+        for (auto& r : p->ranks) {
+            out->n_tiles += r->H.n_tiles;
+            out->n_elems_local += (int64_t)r->H.elem_global.size();
+            out->n_nodes_local += r->H.n_local;
+            out->total_slots += r->H.tile_slot_off.empty() ? 0 : r->H.tile_slot_off.back();
+            out->n_shared_nodes += r->H.n_shared;
+            out->n_ghost_nodes += r->H.n_ghost;
+            out->device_bytes += r->mem.bytes;
+            out->bytes_per_step += r->bytes_per_step;
+        }
+        out->launches_per_step = p->launches_per_step;
+    });
+}
+
+int cf_device_temperature(cf_plan* p, int32_t k, double** dptr, int64_t* n) {
+    return guarded([&] {
+        if (!p || !dptr || !n || k < 0 || k >= (int32_t)p->ranks.size()) raise(CF_INVALID_ARG, "bad argument");
+        *dptr = p->ranks[k]->T[p->cur];
+        *n = p->ranks[k]->H.n_local;
+    });
+}
+
+int cf_estimate_lambda_max(cf_plan* p, int32_t iterations, uint64_t seed, double* lambda, double* eq13) {
+    return guarded([&] {
+        if (!p || !lambda) raise(CF_INVALID_ARG, "null argument");
+        if (p->ranks.size() != 1 || p->world != 1) raise(CF_INVALID_ARG, "lambda_max needs a single-rank plan");
+        CF_CUDA_CHECK(cudaSetDevice(p->device));
+        Rank& r = *p->ranks[0];
+        const int32_t n = r.H.n_local;
+        DeviceMem M;
+        std::vector<double> cval(kMaxRegions, 0), kval(kMaxRegions, 0), hval(kMaxFacetKinds, 0);
+        // properties at the region's initial temperature (no latent heat);
+        // h of an interface table: its largest value (conservative)
+        for (int g = 0; g < p->P.n_materials; ++g) {
+            const DevMaterial& mm = p->P.mat[g];
+            if (!(mm.rho > 0)) continue;
+            cval[g] = mm.rho * pl_eval(p->P, mm.c, mm.T0);
+            kval[g] = pl_eval(p->P, mm.k, mm.T0);
+        }
+        for (int k = 0; k < p->P.n_kinds; ++k) {
+            const DevFacetKind& K = p->P.kind[k];
+            if (K.interface) {
+                double hm = -INFINITY;
+                for (int j = 0; j < K.htab.n; ++j) hm = std::max(hm, p->P.pool[K.htab.off + K.htab.n + j]);
+                hval[k] = hm;
+            } else {
+                hval[k] = K.h;
+            }
+        }
+        LamArgs L;
+        L.a = r.ta;
+        L.cval = M.up(cval, p->stream);
+        L.kval = M.up(kval, p->stream);
+        L.hval = M.up(hval, p->stream);
+        double* x = M.alloc<double>(n);
+        double* y = M.alloc<double>(n);
+        L.M = M.alloc<double>(n);
+        L.D = M.alloc<double>(n);
+        double* acc = M.alloc<double>(3);
+        CF_CUDA_CHECK(cudaMemsetAsync(L.M, 0, n * sizeof(double), p->stream));
+        CF_CUDA_CHECK(cudaMemsetAsync(L.D, 0, n * sizeof(double), p->stream));
+        L.x = x;
+        L.y = y;
+        lam_setup<<<r.H.n_tiles, 256, 0, p->stream>>>(L);
+        const int blocks = std::max(1, std::min(1184, (n + 255) / 256));
+        lam_init_x<<<blocks, 256, 0, p->stream>>>(n, r.ua.local_global, r.ua.node_dir, seed, x);
+        double h_acc[3] = {0, 0, 0};
+        for (int it = 0; it < iterations; ++it) {
+            lam_diag<<<blocks, 256, 0, p->stream>>>(n, L.D, x, y);
+            lam_apply<<<r.H.n_tiles, 256, 0, p->stream>>>(L);
+            CF_CUDA_CHECK(cudaMemsetAsync(acc, 0, 3 * sizeof(double), p->stream));
+            lam_reduce<<<blocks, 256, 0, p->stream>>>(n, r.ua.node_dir, L.M, x, y, acc);
+            lam_scale<<<blocks, 256, 0, p->stream>>>(n, y, acc, x);
+        }
+        CF_CUDA_CHECK(cudaMemcpyAsync(h_acc, acc, sizeof h_acc, cudaMemcpyDeviceToHost, p->stream));
+        CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+        M.release();
+        *lambda = h_acc[0] / h_acc[1];
+        if (eq13) *eq13 = p->eq13_min;
+    });
+}
+
+int cf_comm_unique_id(uint8_t out[128]) {
+    return guarded([&] {
+        ncclUniqueId id;
+        CF_NCCL_CHECK(nccl().GetUniqueId(&id));
+        static_assert(sizeof(id) == 128, "ncclUniqueId size");
+        std::memcpy(out, &id, 128);
+    });
+}
+
+int cf_comm_create(int32_t world, int32_t rank, int32_t device, const uint8_t uid[128], cf_comm** out) {
+    return guarded([&] {
+        if (!out || !uid) raise(CF_INVALID_ARG, "null argument");
+        CF_CUDA_CHECK(cudaSetDevice(device));
+        auto c = std::make_unique<cf_comm>();
+        ncclUniqueId id;
+        std::memcpy(&id, uid, 128);
+        CF_NCCL_CHECK(nccl().CommInitRank(&c->comm, world, id, rank));
+        c->world = world;
+        c->rank = rank;
+        c->device = device;
+        *out = c.release();
+    });
+}
+
+int cf_comm_destroy(cf_comm* c) {
+    return guarded([&] {
+        if (!c) return;
+        if (c->comm) nccl().CommDestroy(c->comm);
+        delete c;
+    });
+}
+
+// ------------------------------------------------------------------ host utilities
+int cf_rcm_permutation(const cf_mesh_desc* d, int32_t seed, int32_t* out) {
+    return guarded([&] {
+        if (!d || !out) raise(CF_INVALID_ARG, "null argument");
+        const Graph g = build_node_graph(d->n_nodes, d->n_elems, d->tets);
+        const auto p = rcm_permutation(g, seed);
+        std::memcpy(out, p.data(), sizeof(int32_t) * p.size());
+    });
+}
+
+int cf_bandwidth(const cf_mesh_desc* d, const int32_t* perm, int64_t* out) {
+    return guarded([&] {
+        if (!d || !out) raise(CF_INVALID_ARG, "null argument");
+        const Graph g = build_node_graph(d->n_nodes, d->n_elems, d->tets);
+        *out = bandwidth(g, perm);
+    });
+}
+
+int cf_finalize_mesh(const cf_mesh_desc* d, int32_t* tets_out, int32_t* owner_out) {
+    return guarded([&] {
+        MeshData m;
+        finalize_mesh(d, m, nullptr);
+        if (tets_out) std::memcpy(tets_out, m.tets.data(), sizeof(int32_t) * m.tets.size());
+        if (owner_out) std::memcpy(owner_out, m.owner.data(), sizeof(int32_t) * m.owner.size());
+    });
+}
+
+int cf_pair_sister_facets(const cf_mesh_desc* d, int32_t* out, int64_t cap, int64_t* n) {
+    return guarded([&] {
+        MeshData m;
+        finalize_mesh(d, m, nullptr);
+        const auto pairs = pair_sister_facets(m);
+        if (n) *n = (int64_t)pairs.size();
+        if (out)
+            for (size_t i = 0; i < pairs.size() && (int64_t)i < cap; ++i) {
+                out[3 * i] = pairs[i].facet;
+                out[3 * i + 1] = pairs[i].sister;
+                out[3 * i + 2] = pairs[i].contact;
+            }
+    });
+}
+
+int cf_partition_rcb(const cf_mesh_desc* d, int32_t parts, int32_t* out) {
+    return guarded([&] {
+        MeshData m;
+        finalize_mesh(d, m, nullptr);
+        const auto p = partition_rcb(m, parts);
+        std::memcpy(out, p.data(), sizeof(int32_t) * p.size());
+    });
+}
+
+int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts,
+                int32_t* tile_of_element, int32_t* n_tiles) {
+    return guarded([&] {
+        if (!mesh || !setup || !opts || !tile_of_element) raise(CF_INVALID_ARG, "null argument");
+        MeshData m;
+        std::vector<Geom> geom;
+        finalize_mesh(mesh, m, &geom);
+        SetupData S;
+        resolve_setup(m, geom, setup, S);
+        std::vector<int32_t> label(m.N);
+        if (opts->node_order == CF_NODE_ORDER_RCM)
+            label = rcm_permutation(build_node_graph(m.N, m.E, m.tets.data()), -1);
+        else
+            std::iota(label.begin(), label.end(), 0);
+        PlanOptions po;
+        po.mode = opts->mode;
+        po.elem_order = opts->elem_order;
+        po.tile_elems = opts->tile_elems > 0 ? opts->tile_elems : 1024;
+        po.tile_of_element = opts->tile_of_element;
+        po.world_size = std::max(1, opts->world_size);
+        std::vector<int32_t> part;
+        if (po.world_size > 1) {
+            part = opts->partition == CF_PARTITION_GIVEN && opts->part_of_element
+                       ? std::vector<int32_t>(opts->part_of_element, opts->part_of_element + m.E)
+                       : partition_rcb(m, po.world_size);
+            po.part_of_element = part.data();
+        }
+        for (int32_t e = 0; e < m.E; ++e) tile_of_element[e] = -1;
+        int32_t base = 0;
+        const int r0 = opts->rank, r1 = opts->local_ranks > 1 ? po.world_size : opts->rank + 1;
+        for (int r = r0; r < r1; ++r) {
+            RankPlan rp;
+            build_rank_plan(m, geom, S, po, label, r, rp);
+            for (int32_t t = 0; t < rp.n_tiles; ++t)
+                for (int32_t i = rp.tile_elem_off[t]; i < rp.tile_elem_off[t + 1]; ++i)
+                    tile_of_element[rp.elem_global[i]] = base + t;
+            base += rp.n_tiles;
+        }
+        if (n_tiles) *n_tiles = base;
+    });
+}
+
+int cf_generate_fixture(int32_t kind, int32_t n, double radius, double jitter, uint64_t seed, uint64_t perm_seed,
+                        cf_fixture* out) {
+    return guarded([&] {
+        if (!out) raise(CF_INVALID_ARG, "null argument");
+        generate_fixture(kind, n, radius, jitter, seed, perm_seed, out);
+    });
+}
+
+int cf_counter_uniform(uint64_t seed, const int64_t* keys, int64_t n, double lo, double hi, double* out) {
+    return guarded([&] {
+        if (n && (!keys || !out)) raise(CF_INVALID_ARG, "null argument");
+        for (int64_t i = 0; i < n; ++i) out[i] = lo + (hi - lo) * counter_uniform(seed, (uint64_t)keys[i]);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,133 @@
+// cf_physics.cuh — per-element / per-facet / per-node physics of the castfem
+// explicit step, as sm_100a device code.
+//
+// Every expression keeps the reference's operation order (paths relative to
+// /root/reference/proj/include/castfem/) so that, compiled with -fmad=false
+// (no FMA contraction; fp64 '/' and sqrt are IEEE round-to-nearest on sm_100a
+// as on x86), results are bitwise equal to the reference built with
+// -ffp-contract=off:
+//   PiecewiseLinear::operator()  material.hpp:30-38
+//   MaterialTable::enthalpy      material.hpp:89-102 (melt_fraction :69-72)
+//   apparent_heat_capacity       fem.hpp:26-45 (Lemmon)
+//   element_accumulate           fem.hpp:57-70
+//   facet_flux_accumulate        fem.hpp:74-79 (+ interface branch blocked.hpp:485-490)
+//   element_stable_dt            fem.hpp:83-85
+#pragma once
+
+#include <cstdint>
+
+#include "cf_internal.hpp"
+
+namespace cfb {
+
+__device__ __forceinline__ double dev_pl_eval(const DevParams* __restrict__ P, DevTable t, double x) {
+    const double* xs = P->pool + t.off;
+    const double* ys = xs + t.n;
+    if (t.n <= 1) return ys[0];
+    if (x <= xs[0]) return ys[0];
+    if (x >= xs[t.n - 1]) return ys[t.n - 1];
+    int i = 0;
+    while (i + 1 < t.n && xs[i + 1] <= x) ++i;
+    const double f = (x - xs[i]) / (xs[i + 1] - xs[i]);
+    return ys[i] + f * (ys[i + 1] - ys[i]);
+}
+
+template <bool TDEP>
+__device__ __forceinline__ double dev_c(const DevParams* __restrict__ P, const DevMaterial& m, double T) {
+    if (!TDEP || m.c.n <= 1) return m.c0;
+    return dev_pl_eval(P, m.c, T);
+}
+template <bool TDEP>
+__device__ __forceinline__ double dev_k(const DevParams* __restrict__ P, const DevMaterial& m, double T) {
+    if (!TDEP || m.k.n <= 1) return m.k0;
+    return dev_pl_eval(P, m.k, T);
+}
+
+// MaterialTable::enthalpy material.hpp:89-102
+template <bool TDEP>
+__device__ __forceinline__ double dev_enthalpy(const DevParams* __restrict__ P, const DevMaterial& m, double T) {
+    double sensible;
+    if (!TDEP || m.c.n <= 1) {
+        sensible = m.c0 * (T - m.ref);
+    } else {
+        const double* xs = P->pool + m.c.off;
+        const double* ys = xs + m.c.n;
+        const int n = m.c.n;
+        const double Tc = T < xs[0] ? xs[0] : (xs[n - 1] < T ? xs[n - 1] : T);
+        int ub = 0;
+        while (ub < n && xs[ub] <= Tc) ++ub;
+        const int i = (ub < n - 1 ? ub : n - 1) - 1;
+        sensible = P->pool[m.cum_off + i] + 0.5 * (ys[i] + dev_pl_eval(P, m.c, Tc)) * (Tc - xs[i]);
+    }
+    double mf = 0.0;
+    if (m.has_phase) {
+        const double v = (T - m.solidus) / (m.liquidus - m.solidus);
+        mf = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+    }
+    return sensible + m.latent * mf;
+}
+
+// One element: lumped capacitance share `lump` (added to each of the 4
+// nodes) and the 4 conduction residual terms rc[a] (subtracted).
+// g1..g3 are the stored gradients; g0 = (g1+g2+g3)*-1.0 (geometry.hpp:75).
+template <bool TDEP>
+__device__ __forceinline__ void dev_element(const DevParams* __restrict__ P, const DevMaterial& m,
+                                            const double (&g)[4][3], double vol, double max_edge,
+                                            const double (&T)[4], const double (&H)[4], double& lump,
+                                            double (&rc)[4]) {
+    // grad T (fem.hpp:36-40 and :64-65 compute the same sums; shared here)
+    double gtx = 0.0, gty = 0.0, gtz = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        gtx = gtx + g[a][0] * T[a];
+        gty = gty + g[a][1] * T[a];
+        gtz = gtz + g[a][2] * T[a];
+    }
+    const double t_bar = 0.25 * (((T[0] + T[1]) + T[2]) + T[3]);
+    // apparent_heat_capacity fem.hpp:26-45
+    int lo = 0, hi = 0;
+#pragma unroll
+    for (int a = 1; a < 4; ++a) {
+        if (T[a] < (lo == 0 ? T[0] : lo == 1 ? T[1] : lo == 2 ? T[2] : T[3])) lo = a;
+        if (T[a] > (hi == 0 ? T[0] : hi == 1 ? T[1] : hi == 2 ? T[2] : T[3])) hi = a;
+    }
+    const double Tlo = lo == 0 ? T[0] : lo == 1 ? T[1] : lo == 2 ? T[2] : T[3];
+    const double Thi = hi == 0 ? T[0] : hi == 1 ? T[1] : hi == 2 ? T[2] : T[3];
+    const double range = Thi - Tlo;
+    double capp;
+    if (range <= 0) {
+        capp = dev_c<TDEP>(P, m, t_bar);
+    } else {
+        double ghx = 0.0, ghy = 0.0, ghz = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            ghx = ghx + g[a][0] * H[a];
+            ghy = ghy + g[a][1] * H[a];
+            ghz = ghz + g[a][2] * H[a];
+        }
+        const double gt2 = gtx * gtx + gty * gty + gtz * gtz;
+        const double scale = range / max_edge;
+        if (gt2 < 1e-14 * scale * scale) {
+            const double Hlo = lo == 0 ? H[0] : lo == 1 ? H[1] : lo == 2 ? H[2] : H[3];
+            const double Hhi = hi == 0 ? H[0] : hi == 1 ? H[1] : hi == 2 ? H[2] : H[3];
+            capp = (Hhi - Hlo) / range;
+        } else {
+            capp = sqrt((ghx * ghx + ghy * ghy + ghz * ghz) / gt2);
+        }
+    }
+    // element_accumulate fem.hpp:60-69
+    lump = m.rho * capp * vol * 0.25;
+    const double kv = dev_k<TDEP>(P, m, t_bar) * vol;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) rc[a] = kv * (g[a][0] * gtx + g[a][1] * gty + g[a][2] * gtz);
+}
+
+// element_stable_dt fem.hpp:83-85 at the element mean temperature
+template <bool TDEP>
+__device__ __forceinline__ double dev_stable_bound(const DevParams* __restrict__ P, const DevMaterial& m,
+                                                  double min_edge, const double (&T)[4]) {
+    const double t_bar = 0.25 * (((T[0] + T[1]) + T[2]) + T[3]);
+    return m.rho * dev_c<TDEP>(P, m, t_bar) * min_edge * min_edge / dev_k<TDEP>(P, m, t_bar);
+}
+
+}  // namespace cfb

@@ -1,0 +1,643 @@
+// cf_plan.cpp — setup resolution and the tile (cache-block) builder.
+//
+// Reference semantics kept (paths relative to /root/reference/proj/include/castfem/):
+//   MaterialTable::finalize / validate   material.hpp:40-47, 104-119; parse_config checks :339-344
+//   resolve_facet_tag                    blocked.hpp:127-149
+//   Dirichlet "lowest tag wins"          blocked.hpp:250-263, initial_temperatures :396-417
+//   static dt (constant properties)      blocked.hpp:340-350, element_stable_dt fem.hpp:83-85
+//   block-local slots + merge CSR        blocked.hpp:217-307 (tiles replace partition_graph blocks)
+//   facet bindings in element order      blocked.hpp:244-288
+//   external nodes / ambient bindings    blocked.hpp:309-331, classify_nodes partition.hpp:305-367
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+
+#include "cf_internal.hpp"
+
+namespace cfb {
+
+double pl_eval(const DevParams& P, const DevTable& t, double x) {
+    const double* xs = P.pool + t.off;
+    const double* ys = xs + t.n;
+    if (t.n <= 1) return ys[0];
+    if (x <= xs[0]) return ys[0];
+    if (x >= xs[t.n - 1]) return ys[t.n - 1];
+    int i = 0;
+    while (i + 1 < t.n && xs[i + 1] <= x) ++i;
+    const double f = (x - xs[i]) / (xs[i + 1] - xs[i]);
+    return ys[i] + f * (ys[i + 1] - ys[i]);
+}
+
+double enthalpy(const DevParams& P, const DevMaterial& m, double T) {
+    double sensible;
+    if (m.c.n <= 1) {
+        sensible = m.c0 * (T - m.ref);
+    } else {
+        const double* xs = P.pool + m.c.off;
+        const double* ys = xs + m.c.n;
+        const int n = m.c.n;
+        const double Tc = T < xs[0] ? xs[0] : (xs[n - 1] < T ? xs[n - 1] : T);
+        int ub = 0;
+        while (ub < n && xs[ub] <= Tc) ++ub;
+        const int i = std::min(ub, n - 1) - 1;
+        sensible = P.pool[m.cum_off + i] + 0.5 * (ys[i] + pl_eval(P, m.c, Tc)) * (Tc - xs[i]);
+    }
+    double mf = 0;
+    if (m.has_phase) {
+        const double v = (T - m.solidus) / (m.liquidus - m.solidus);
+        mf = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+    }
+    return sensible + m.latent * mf;
+}
+
+namespace {
+
+struct Pool {
+    DevParams& P;
+    int used = 0;
+    DevTable put(const cf_table& t, const char* what) {
+        if (t.n < 1 || !t.x || !t.y) raise(CF_CONFIG, std::string(what) + ": empty or inconsistent table");
+        for (int i = 1; i < t.n; ++i)
+            if (!(t.x[i] > t.x[i - 1]))
+                raise(CF_CONFIG, std::string(what) + ": table abscissae must be strictly increasing");
+        if (used + 2 * t.n > kMaxTablePts) raise(CF_CONFIG, "tables exceed the device table pool");
+        DevTable d{t.n, used};
+        for (int i = 0; i < t.n; ++i) {
+            P.pool[used + i] = t.x[i];
+            P.pool[used + t.n + i] = t.y[i];
+        }
+        used += 2 * t.n;
+        return d;
+    }
+};
+
+bool name_eq(const char* a, const std::string& b) { return a && b == a; }
+
+}  // namespace
+
+void resolve_setup(const MeshData& m, const std::vector<Geom>& geom, const cf_setup_desc* s, SetupData& out) {
+    if (!s) raise(CF_INVALID_ARG, "null setup");
+    if ((s->n_materials && !s->materials) || (s->n_bcs && !s->bcs) || (s->n_coeffs && !s->coeffs))
+        raise(CF_INVALID_ARG, "null array in setup descriptor");
+    if (!(s->dt_safety > 0 && s->dt_safety <= 1)) raise(CF_CONFIG, "safety must be in (0, 1]");
+    DevParams& P = out.P;
+    std::memset(&P, 0, sizeof P);
+    Pool pool{P};
+    for (int i = 0; i < s->n_coeffs; ++i) {
+        const cf_table& t = s->coeffs[i].h;
+        if (t.n < 1 || !t.x || !t.y) raise(CF_CONFIG, "interface h: empty or inconsistent table");
+        for (int j = 1; j < t.n; ++j)
+            if (!(t.x[j] > t.x[j - 1])) raise(CF_CONFIG, "interface h: table abscissae must be strictly increasing");
+    }
+    // pair_sister_facets first (solve_serial blocked.hpp:651)
+    out.pairs = pair_sister_facets(m);
+    out.pair_of_facet.assign(m.F, -1);
+    for (size_t p = 0; p < out.pairs.size(); ++p) out.pair_of_facet[out.pairs[p].facet] = (int32_t)p;
+
+    // materials of used regions (MaterialTable::finalize)
+    for (int32_t e = 0; e < m.E; ++e)
+        if (m.region[e] >= s->n_materials)
+            raise(CF_CONFIG, "no material for region " + std::to_string(m.region[e]));
+    if (s->n_materials > kMaxRegions) raise(CF_CONFIG, "more than 16 material regions");
+    std::vector<char> used(s->n_materials + 1, 0);
+    for (int32_t r = 0; r < m.region_count; ++r) used[r] = 0;
+    for (int32_t e = 0; e < m.E; ++e) used[m.region[e]] = 1;
+    P.n_materials = s->n_materials;
+    for (int r = 0; r < s->n_materials; ++r) {
+        const cf_material& c = s->materials[r];
+        DevMaterial& d = P.mat[r];
+        if (!used[r] && !(c.rho > 0)) continue;  // untouched slot
+        d.c = pool.put(c.c, "c");
+        d.k = pool.put(c.k, "k");
+        if (!(c.rho > 0)) raise(CF_CONFIG, "rho must be positive");
+        for (int i = 0; i < c.c.n; ++i)
+            if (c.c.y[i] <= 0) raise(CF_CONFIG, "c(T) must be positive");
+        for (int i = 0; i < c.k.n; ++i)
+            if (c.k.y[i] <= 0) raise(CF_CONFIG, "k(T) must be positive");
+        if (c.latent_heat < 0) raise(CF_CONFIG, "latent_heat must be non-negative");
+        if (c.latent_heat > 0 && !(c.solidus < c.liquidus))
+            raise(CF_CONFIG, "phase change requires solidus < liquidus");
+        d.rho = c.rho;
+        d.T0 = c.initial_temperature;
+        d.latent = c.latent_heat;
+        d.solidus = c.solidus;
+        d.liquidus = c.liquidus;
+        d.has_phase = c.latent_heat > 0;
+        d.c0 = c.c.y[0];
+        d.k0 = c.k.y[0];
+        d.ref = c.c.n <= 1 ? 0.0 : c.c.x[0];
+        const int nc = std::max(c.c.n, 1);
+        if (pool.used + nc > kMaxTablePts) raise(CF_CONFIG, "tables exceed the device table pool");
+        d.cum_off = pool.used;
+        P.pool[d.cum_off] = 0;
+        for (int i = 1; i < c.c.n; ++i)
+            P.pool[d.cum_off + i] =
+                P.pool[d.cum_off + i - 1] + 0.5 * (c.c.y[i] + c.c.y[i - 1]) * (c.c.x[i] - c.c.x[i - 1]);
+        pool.used += nc;
+        d.range_lo = -INFINITY;
+        d.range_hi = INFINITY;
+        if (c.c.n > 1) d.range_lo = std::max(d.range_lo, c.c.x[0]);
+        if (c.k.n > 1) d.range_lo = std::max(d.range_lo, c.k.x[0]);
+        if (c.c.n > 1) d.range_hi = std::min(d.range_hi, c.c.x[c.c.n - 1]);
+        if (c.k.n > 1) d.range_hi = std::min(d.range_hi, c.k.x[c.k.n - 1]);
+        if (c.c.n > 1 || c.k.n > 1) P.temp_dep = 1;
+        if (std::isfinite(d.range_lo) || std::isfinite(d.range_hi)) P.finite_range = 1;
+    }
+    out.temp_dep = P.temp_dep != 0;
+    P.dt_safety = s->dt_safety;
+
+    // boundary conditions by tag name (map semantics: last declaration wins)
+    const int32_t ntag = (int32_t)m.tags.size();
+    std::vector<int32_t> bc_of_tag(ntag, -1);
+    for (int32_t t = 0; t < ntag; ++t)
+        for (int b = 0; b < s->n_bcs; ++b)
+            if (name_eq(s->bcs[b].tag, m.tags[t])) bc_of_tag[t] = b;
+    // interface coefficient per contact: first match (find_interface material.hpp:175-179)
+    const int32_t nct = (int32_t)m.contacts.size() / 2;
+    std::vector<int32_t> coeff_of_contact(nct, -1);
+    for (int32_t c = 0; c < nct; ++c) {
+        const std::string& A = m.tags[m.contacts[2 * c]];
+        const std::string& B = m.tags[m.contacts[2 * c + 1]];
+        for (int k = 0; k < s->n_coeffs && coeff_of_contact[c] < 0; ++k) {
+            const cf_interface_coeff& x = s->coeffs[k];
+            if ((name_eq(x.tag_a, A) && name_eq(x.tag_b, B)) || (name_eq(x.tag_a, B) && name_eq(x.tag_b, A)))
+                coeff_of_contact[c] = k;
+        }
+    }
+    // per tag resolution -> kind ids
+    std::vector<int32_t> kind_of_tag(ntag, INT32_MIN);
+    std::map<int32_t, int32_t> kind_of_bc, kind_of_coeff, dir_of_bc;
+    std::vector<int32_t> tag_seen(ntag, 0);
+    for (int32_t f = 0; f < m.F; ++f) tag_seen[m.facet_tag[f]] = 1;
+    for (int32_t t = 0; t < ntag; ++t) {
+        if (!tag_seen[t]) continue;
+        const int32_t b = bc_of_tag[t];
+        int32_t coeff = -1;
+        for (int32_t c = 0; c < nct; ++c)
+            if (m.contacts[2 * c] == t || m.contacts[2 * c + 1] == t) {
+                if (coeff_of_contact[c] < 0)
+                    raise(CF_CONFIG, "no interface coefficient for contact " + m.tags[m.contacts[2 * c]] + "/" +
+                                         m.tags[m.contacts[2 * c + 1]]);
+                coeff = coeff_of_contact[c];
+            }
+        if (b >= 0 && coeff >= 0)
+            raise(CF_CONFIG, "facet tag '" + m.tags[t] + "' resolves to both a boundary condition and a contact interface");
+        if (b < 0 && coeff < 0) raise(CF_CONFIG, "facet tag '" + m.tags[t] + "' resolves to no declared condition");
+        if (b >= 0 && s->bcs[b].kind == CF_BC_FIXED) {
+            if (!dir_of_bc.count(b)) {
+                const int32_t id = (int32_t)dir_of_bc.size();
+                if (id >= kMaxFacetKinds) raise(CF_CONFIG, "too many fixed boundary conditions");
+                dir_of_bc[b] = id;
+                const cf_table& ft = s->bcs[b].fixed_T;
+                if (ft.n < 1) raise(CF_CONFIG, "fixed boundary condition without a temperature value");
+                P.dir_tab[id] = pool.put(ft, "T");
+            }
+            kind_of_tag[t] = -1 - dir_of_bc[b];
+        } else if (b >= 0) {
+            if (!kind_of_bc.count(b)) {
+                const int32_t id = P.n_kinds++;
+                if (id >= kMaxFacetKinds) raise(CF_CONFIG, "too many facet conditions");
+                kind_of_bc[b] = id;
+                P.kind[id].interface = 0;
+                P.kind[id].q = s->bcs[b].q;
+                P.kind[id].h = s->bcs[b].h;
+                P.kind[id].t_inf = s->bcs[b].t_inf;
+            }
+            kind_of_tag[t] = kind_of_bc[b];
+        } else {
+            if (!kind_of_coeff.count(coeff)) {
+                const int32_t id = P.n_kinds++;
+                if (id >= kMaxFacetKinds) raise(CF_CONFIG, "too many facet conditions");
+                kind_of_coeff[coeff] = id;
+                P.kind[id].interface = 1;
+                P.kind[id].var = s->coeffs[coeff].var == CF_VAR_TEMPERATURE ? CF_VAR_TEMPERATURE : CF_VAR_TIME;
+                P.kind[id].q = 0.0;
+                P.kind[id].htab = pool.put(s->coeffs[coeff].h, "interface h");
+            }
+            kind_of_tag[t] = kind_of_coeff[coeff];
+        }
+    }
+    out.facet_kind.resize(m.F);
+    for (int32_t f = 0; f < m.F; ++f) {
+        out.facet_kind[f] = kind_of_tag[m.facet_tag[f]];
+        if (out.facet_kind[f] >= 0 && P.kind[out.facet_kind[f]].interface && out.pair_of_facet[f] < 0)
+            raise(CF_CONFIG, "interface facet " + std::to_string(f) + " has no sister pairing; call pair_sister_facets");
+    }
+    // Dirichlet nodes: lowest tag wins
+    out.dir_of_node.assign(m.N, -1);
+    std::vector<int32_t> best_tag(m.N, INT32_MAX);
+    for (int32_t f = 0; f < m.F; ++f) {
+        const int32_t k = out.facet_kind[f];
+        if (k >= 0) continue;
+        for (int a = 0; a < 3; ++a) {
+            const int32_t n = m.facets[3 * (size_t)f + a];
+            if (m.facet_tag[f] < best_tag[n]) {
+                best_tag[n] = m.facet_tag[f];
+                out.dir_of_node[n] = -1 - k;
+            }
+        }
+    }
+    // initial_temperatures (+ index-keyed override)
+    out.T0.resize(m.N);
+    for (int32_t n = 0; n < m.N; ++n)
+        out.T0[n] = s->initial_T ? s->initial_T[n] : s->materials[m.node_region[n]].initial_temperature;
+    for (int32_t n = 0; n < m.N; ++n)
+        if (out.dir_of_node[n] >= 0) out.T0[n] = pl_eval(P, P.dir_tab[out.dir_of_node[n]], 0.0);
+    // static dt
+    if (!P.temp_dep) {
+        double dt = INFINITY;
+#pragma omp parallel for reduction(min : dt)
+        for (int64_t e = 0; e < m.E; ++e) {
+            const DevMaterial& mm = P.mat[m.region[e]];
+            const double v = mm.rho * mm.c0 * geom[e].min_edge * geom[e].min_edge / mm.k0;
+            dt = std::min(dt, v);
+        }
+        out.min_bound = dt;
+        P.static_dt = dt * s->dt_safety;
+        if (!(P.static_dt > 0)) raise(CF_VALIDATION, "non-positive stable time step");
+    }
+}
+
+// ------------------------------------------------------------------ tiles
+namespace {
+inline uint64_t spread21(uint64_t v) {
+    v &= 0x1fffff;
+    v = (v | v << 32) & 0x1f00000000ffffull;
+    v = (v | v << 16) & 0x1f0000ff0000ffull;
+    v = (v | v << 8) & 0x100f00f00f00f00full;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
+}  // namespace
+
+void build_rank_plan(const MeshData& m, const std::vector<Geom>& geom, const SetupData& S, const PlanOptions& o,
+                     const std::vector<int32_t>& node_label, int32_t rank, RankPlan& rp) {
+    rp = RankPlan{};
+    rp.rank = rank;
+    const int32_t W = o.world_size;
+    auto part_of = [&](int32_t e) { return W > 1 ? o.part_of_element[e] : 0; };
+
+    // elements of this rank, ascending global id (SubDomain::from_elements blocked.hpp:25-39)
+    std::vector<int32_t> elems;
+    elems.reserve(W > 1 ? m.E / W + 1 : m.E);
+    for (int32_t e = 0; e < m.E; ++e)
+        if (part_of(e) == rank) elems.push_back(e);
+    const int64_t Er = (int64_t)elems.size();
+
+    // parts touching each node (classify_nodes partition.hpp:311-327), only for W > 1
+    std::vector<int64_t> np_off;
+    std::vector<int32_t> np_parts;
+    if (W > 1) {
+        std::vector<std::vector<int32_t>> tmp;  // small per node; build compactly
+        np_off.assign(m.N + 1, 0);
+        std::vector<int32_t> cnt(m.N, 0);
+        // upper bound count then dedupe
+        std::vector<int64_t> off(m.N + 1, 0);
+        for (int64_t i = 0; i < 4 * (int64_t)m.E; ++i) off[m.tets[i] + 1]++;
+        for (int32_t n = 0; n < m.N; ++n) off[n + 1] += off[n];
+        std::vector<int32_t> buf(off[m.N]);
+        {
+            std::vector<int64_t> cur(off.begin(), off.end() - 1);
+            for (int64_t i = 0; i < 4 * (int64_t)m.E; ++i) buf[cur[m.tets[i]]++] = part_of((int32_t)(i / 4));
+        }
+        for (int32_t n = 0; n < m.N; ++n) {
+            std::sort(buf.begin() + off[n], buf.begin() + off[n + 1]);
+            cnt[n] = (int32_t)(std::unique(buf.begin() + off[n], buf.begin() + off[n + 1]) - (buf.begin() + off[n]));
+            np_off[n + 1] = np_off[n] + cnt[n];
+        }
+        np_parts.resize(np_off[m.N]);
+        for (int32_t n = 0; n < m.N; ++n)
+            std::copy(buf.begin() + off[n], buf.begin() + off[n] + cnt[n], np_parts.begin() + np_off[n]);
+    }
+    auto node_on = [&](int32_t n, int32_t p) {
+        if (W == 1) return true;
+        for (int64_t j = np_off[n]; j < np_off[n + 1]; ++j)
+            if (np_parts[j] == p) return true;
+        return false;
+    };
+
+    // local nodes ordered by label (RCM or given)
+    std::vector<int32_t> local_of(m.N, -1);
+    std::vector<int32_t> lnodes;
+    {
+        std::vector<char> mark(m.N, 0);
+        for (int32_t e : elems)
+            for (int a = 0; a < 4; ++a) mark[m.tets[4 * (size_t)e + a]] = 1;
+        for (int32_t n = 0; n < m.N; ++n)
+            if (mark[n]) lnodes.push_back(n);
+        std::sort(lnodes.begin(), lnodes.end(), [&](int32_t a, int32_t b) { return node_label[a] < node_label[b]; });
+        for (size_t i = 0; i < lnodes.size(); ++i) local_of[lnodes[i]] = (int32_t)i;
+    }
+    rp.n_local = (int32_t)lnodes.size();
+
+    // facets per element (ascending facet id), Dirichlet facets excluded from bindings
+    std::vector<int32_t> in_rank(m.E, 0);
+    for (int32_t e : elems) in_rank[e] = 1;
+    std::vector<int32_t> fe_off(m.E + 1, 0), fe;
+    for (int32_t f = 0; f < m.F; ++f)
+        if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe_off[m.owner[f] + 1]++;
+    for (int32_t e = 0; e < m.E; ++e) fe_off[e + 1] += fe_off[e];
+    fe.resize(fe_off[m.E]);
+    {
+        std::vector<int32_t> cur(fe_off.begin(), fe_off.end() - 1);
+        for (int32_t f = 0; f < m.F; ++f)
+            if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe[cur[m.owner[f]]++] = f;
+    }
+
+    // ghosts: sister nodes of this rank's interface facets that are not local
+    std::vector<int32_t> ghosts;
+    for (int32_t f = 0; f < m.F; ++f) {
+        if (!in_rank[m.owner[f]] || S.facet_kind[f] < 0 || !S.P.kind[S.facet_kind[f]].interface) continue;
+        const int32_t sis = S.pairs[S.pair_of_facet[f]].sister;
+        for (int a = 0; a < 4; ++a) {
+            const int32_t n = m.tets[4 * (size_t)sis + a];
+            if (local_of[n] < 0) ghosts.push_back(n);
+        }
+    }
+    std::sort(ghosts.begin(), ghosts.end());
+    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+    rp.n_ghost = (int32_t)ghosts.size();
+    for (size_t g = 0; g < ghosts.size(); ++g) local_of[ghosts[g]] = rp.n_local + (int32_t)g;
+    rp.local_global = lnodes;
+    rp.local_global.insert(rp.local_global.end(), ghosts.begin(), ghosts.end());
+
+    // tiles: element order key, contiguous chunks, ascending id within a tile
+    std::vector<std::vector<int32_t>> tiles;
+    if (o.tile_of_element) {
+        std::map<int32_t, std::vector<int32_t>> by;
+        for (int32_t e : elems) by[o.tile_of_element[e]].push_back(e);
+        for (auto& kv : by) tiles.push_back(std::move(kv.second));
+    } else {
+        std::vector<int32_t> order = elems;
+        if (o.elem_order == CF_ELEM_ORDER_MORTON) {
+            double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+            for (int32_t n = 0; n < m.N; ++n)
+                for (int k = 0; k < 3; ++k) {
+                    lo[k] = std::min(lo[k], m.pos(n)[k]);
+                    hi[k] = std::max(hi[k], m.pos(n)[k]);
+                }
+            const double span = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 1e-300});
+            std::vector<std::pair<uint64_t, int32_t>> key(Er);
+#pragma omp parallel for schedule(static)
+            for (int64_t i = 0; i < Er; ++i) {
+                const int32_t e = elems[i];
+                const int32_t* t = &m.tets[4 * (size_t)e];
+                uint64_t code = 0;
+                for (int k = 0; k < 3; ++k) {
+                    const double c = 0.25 * (m.pos(t[0])[k] + m.pos(t[1])[k] + m.pos(t[2])[k] + m.pos(t[3])[k]);
+                    double q = (c - lo[k]) / span * 2097151.0;
+                    q = std::min(std::max(q, 0.0), 2097151.0);
+                    code |= spread21((uint64_t)q) << k;
+                }
+                key[i] = {code, e};
+            }
+            std::sort(key.begin(), key.end());
+            for (int64_t i = 0; i < Er; ++i) order[i] = key[i].second;
+        } else if (o.elem_order == CF_ELEM_ORDER_MIN_NODE) {
+            std::vector<std::pair<int32_t, int32_t>> key(Er);
+            for (int64_t i = 0; i < Er; ++i) {
+                const int32_t e = elems[i];
+                int32_t mn = INT32_MAX;
+                for (int a = 0; a < 4; ++a) mn = std::min(mn, node_label[m.tets[4 * (size_t)e + a]]);
+                key[i] = {mn, e};
+            }
+            std::sort(key.begin(), key.end());
+            for (int64_t i = 0; i < Er; ++i) order[i] = key[i].second;
+        }
+        const int TE = o.tile_elems;
+        for (int64_t i = 0; i < Er; i += TE) {
+            tiles.emplace_back(order.begin() + i, order.begin() + std::min<int64_t>(Er, i + TE));
+            std::sort(tiles.back().begin(), tiles.back().end());
+        }
+    }
+    rp.n_tiles = (int32_t)tiles.size();
+    for (auto& t : tiles)
+        if ((int)t.size() > kMaxTileElems)
+            raise(CF_INVALID_ARG, "a tile holds more than 2048 elements (" + std::to_string(t.size()) + ")");
+
+    // node -> number of tiles touching it (private test)
+    std::vector<int32_t> ntiles_of(rp.n_local, 0);
+    {
+        std::vector<int32_t> last(rp.n_local, -1);
+        for (int32_t t = 0; t < rp.n_tiles; ++t)
+            for (int32_t e : tiles[t])
+                for (int a = 0; a < 4; ++a) {
+                    const int32_t l = local_of[m.tets[4 * (size_t)e + a]];
+                    if (last[l] != t) {
+                        last[l] = t;
+                        ntiles_of[l]++;
+                    }
+                }
+    }
+    std::vector<char> shared_node(rp.n_local, 0);
+    if (W > 1)
+        for (int32_t l = 0; l < rp.n_local; ++l) {
+            const int32_t n = lnodes[l];
+            shared_node[l] = (np_off[n + 1] - np_off[n]) > 1;
+        }
+
+    rp.node_region.resize(rp.n_local);
+    for (int32_t l = 0; l < rp.n_local; ++l) rp.node_region[l] = (uint8_t)m.node_region[lnodes[l]];
+    bool any_dir = false;
+    for (int32_t l = 0; l < rp.n_local; ++l)
+        if (S.dir_of_node[lnodes[l]] >= 0) any_dir = true;
+    if (any_dir) {
+        rp.node_dir.resize(rp.n_local);
+        for (int32_t l = 0; l < rp.n_local; ++l) rp.node_dir[l] = (int8_t)S.dir_of_node[lnodes[l]];
+    }
+
+    // per tile arrays
+    rp.tile_elem_off.assign(rp.n_tiles + 1, 0);
+    rp.tile_slot_off.assign(rp.n_tiles + 1, 0);
+    rp.tile_csr_off.assign(rp.n_tiles + 1, 0);
+    rp.tile_facet_off.assign(rp.n_tiles + 1, 0);
+    rp.elem_global.resize(Er);
+    rp.elem_conn.resize(4 * Er);
+    rp.elem_region.resize(Er);
+    rp.elem_geom.resize(11 * Er);
+    if (S.temp_dep) rp.elem_min_edge.resize(Er);
+    std::vector<int32_t> slot_of(rp.n_local, -1);
+    int64_t epos = 0;
+    std::vector<int32_t> tnodes;
+    std::vector<std::vector<uint16_t>> slot_entries;
+    for (int32_t t = 0; t < rp.n_tiles; ++t) {
+        const auto& te = tiles[t];
+        const int ne = (int)te.size();
+        tnodes.clear();
+        for (int32_t e : te)
+            for (int a = 0; a < 4; ++a) {
+                const int32_t l = local_of[m.tets[4 * (size_t)e + a]];
+                if (slot_of[l] == -1) {
+                    slot_of[l] = -2;
+                    tnodes.push_back(l);
+                }
+            }
+        std::sort(tnodes.begin(), tnodes.end());
+        for (size_t s = 0; s < tnodes.size(); ++s) slot_of[tnodes[s]] = (int32_t)s;
+        const int ns = (int)tnodes.size();
+        slot_entries.assign(ns, {});
+        rp.tile_elem_off[t + 1] = rp.tile_elem_off[t] + ne;
+        rp.max_elems = std::max(rp.max_elems, ne);
+        rp.max_slots = std::max(rp.max_slots, ns);
+        int nf = 0;
+        for (int i = 0; i < ne; ++i) {
+            const int32_t e = te[i];
+            const int64_t p = epos + i;
+            rp.elem_global[p] = e;
+            rp.elem_region[p] = (uint8_t)m.region[e];
+            const Geom& g = geom[e];
+            const double vals[11] = {g.g[1][0], g.g[1][1], g.g[1][2], g.g[2][0], g.g[2][1], g.g[2][2],
+                                     g.g[3][0], g.g[3][1], g.g[3][2], g.vol,     g.max_edge};
+            for (int k = 0; k < 11; ++k) rp.elem_geom[(size_t)k * Er + p] = vals[k];
+            if (S.temp_dep) rp.elem_min_edge[p] = g.min_edge;
+            for (int a = 0; a < 4; ++a) {
+                const int32_t s = slot_of[local_of[m.tets[4 * (size_t)e + a]]];
+                rp.elem_conn[4 * p + a] = (uint16_t)s;
+                slot_entries[s].push_back((uint16_t)(4 * i + a));
+            }
+        }
+        // facet bindings, element order then facet id (blocked.hpp:244-288)
+        for (int i = 0; i < ne; ++i) {
+            const int32_t e = te[i];
+            for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j) {
+                const int32_t f = fe[j];
+                const int32_t kind = S.facet_kind[f];
+                uint16_t sl[3];
+                for (int a = 0; a < 3; ++a) sl[a] = (uint16_t)slot_of[local_of[m.facets[3 * (size_t)f + a]]];
+                for (int a = 0; a < 3; ++a) rp.facet_slots.push_back(sl[a]);
+                rp.facet_slots.push_back((uint16_t)kind);
+                rp.facet_area.push_back(
+                    triangle_area(m.pos(m.facets[3 * (size_t)f]), m.pos(m.facets[3 * (size_t)f + 1]),
+                                  m.pos(m.facets[3 * (size_t)f + 2])));
+                if (S.P.kind[kind].interface) {
+                    const int32_t sis = S.pairs[S.pair_of_facet[f]].sister;
+                    for (int a = 0; a < 4; ++a) rp.facet_sister.push_back(local_of[m.tets[4 * (size_t)sis + a]]);
+                    rp.n_if_facets++;
+                } else {
+                    for (int a = 0; a < 4; ++a) rp.facet_sister.push_back(0);
+                    rp.n_bc_facets++;
+                }
+                for (int a = 0; a < 3; ++a) slot_entries[sl[a]].push_back((uint16_t)(4 * ne + 3 * nf + a));
+                ++nf;
+            }
+        }
+        rp.tile_facet_off[t + 1] = rp.tile_facet_off[t] + nf;
+        rp.max_facets = std::max(rp.max_facets, nf);
+        if (4 * ne + 3 * nf > 65535) raise(CF_INVALID_ARG, "tile csr exceeds 16-bit codes");
+        // slots: node ids, info, csr
+        int64_t csr_base = rp.tile_csr_off[t];
+        uint32_t rel = 0;
+        for (int s = 0; s < ns; ++s) {
+            const int32_t l = tnodes[s];
+            rp.slot_node.push_back(l);
+            const bool priv = ntiles_of[l] == 1 && !shared_node[l];
+            rp.slot_info.push_back((uint8_t)((rp.node_region[l] & 0x7f) | (priv ? 0x80 : 0)));
+            for (uint16_t c : slot_entries[s]) rp.csr.push_back(c);
+            rel += (uint32_t)slot_entries[s].size();
+            rp.slot_csr_end.push_back((uint16_t)rel);
+        }
+        rp.tile_csr_off[t + 1] = csr_base + rel;
+        rp.tile_slot_off[t + 1] = rp.tile_slot_off[t] + ns;
+        for (int s = 0; s < ns; ++s) slot_of[tnodes[s]] = -1;
+        epos += ne;
+    }
+    // merge lists: ascending tile per node (merge_offsets/merge_entries blocked.hpp:294-307)
+    const int64_t S_tot = rp.tile_slot_off[rp.n_tiles];
+    rp.merge_off.assign(rp.n_local + 1, 0);
+    for (int64_t s = 0; s < S_tot; ++s) rp.merge_off[rp.slot_node[s] + 1]++;
+    for (int32_t l = 0; l < rp.n_local; ++l) rp.merge_off[l + 1] += rp.merge_off[l];
+    rp.merge_idx.resize(S_tot);
+    {
+        std::vector<int32_t> cur(rp.merge_off.begin(), rp.merge_off.end() - 1);
+        for (int64_t s = 0; s < S_tot; ++s) rp.merge_idx[cur[rp.slot_node[s]]++] = (int32_t)s;
+    }
+
+    // ---------------------------------------------------- multi-rank exchange
+    if (W > 1) {
+        // interface facets of a part and their sister parts -> external node needs
+        // need[p][q] = nodes part p needs from part q (external_from partition.hpp:346-354)
+        auto ext_need = [&](int32_t p, int32_t q) {
+            std::vector<int32_t> v;
+            for (int32_t f = 0; f < m.F; ++f) {
+                if (part_of(m.owner[f]) != p || S.facet_kind[f] < 0 || !S.P.kind[S.facet_kind[f]].interface) continue;
+                const int32_t sis = S.pairs[S.pair_of_facet[f]].sister;
+                if (part_of(sis) != q) continue;
+                for (int a = 0; a < 4; ++a) {
+                    const int32_t n = m.tets[4 * (size_t)sis + a];
+                    if (!node_on(n, p)) v.push_back(n);
+                }
+            }
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+            return v;
+        };
+        std::map<int32_t, RankPlan::Neighbor> nb;
+        // shared nodes, ascending global id
+        std::vector<int32_t> shared;
+        for (int32_t l = 0; l < rp.n_local; ++l)
+            if (shared_node[l]) shared.push_back(lnodes[l]);
+        std::sort(shared.begin(), shared.end());
+        rp.n_shared = (int64_t)shared.size();
+        rp.node_shared.assign(rp.n_local, -1);
+        for (size_t i = 0; i < shared.size(); ++i) rp.node_shared[local_of[shared[i]]] = (int32_t)i;
+        for (int32_t n : shared)
+            for (int64_t j = np_off[n]; j < np_off[n + 1]; ++j)
+                if (np_parts[j] != rank) nb[np_parts[j]].shared.push_back(local_of[n]);
+        for (int32_t q = 0; q < W; ++q) {
+            if (q == rank) continue;
+            auto from = ext_need(rank, q);
+            auto to = ext_need(q, rank);
+            if (from.empty() && to.empty() && !nb.count(q)) continue;
+            auto& x = nb[q];
+            for (int32_t n : from) x.ext_from.push_back(local_of[n]);
+            for (int32_t n : to) {
+                if (local_of[n] < 0 || local_of[n] >= rp.n_local) raise(CF_PROTOCOL, "external node not local to sender");
+                x.ext_to.push_back(local_of[n]);
+            }
+        }
+        rp.send_off.push_back(0);
+        rp.recv_off.push_back(0);
+        for (auto& kv : nb) {
+            kv.second.rank = kv.first;
+            rp.nbrs.push_back(kv.second);
+            const auto& x = rp.nbrs.back();
+            rp.send_off.push_back(rp.send_off.back() + 2 * (int64_t)x.shared.size() + (int64_t)x.ext_to.size());
+            rp.recv_off.push_back(rp.recv_off.back() + 2 * (int64_t)x.shared.size() + (int64_t)x.ext_from.size());
+        }
+        rp.send_len = rp.send_off.back();
+        rp.recv_len = rp.recv_off.back();
+        // combine lists per shared node: ascending rank, own = -1 (c index; r = c + ns_q)
+        std::vector<std::vector<std::pair<int32_t, int32_t>>> src(shared.size());
+        for (size_t i = 0; i < shared.size(); ++i) src[i].push_back({rank, -1});
+        for (size_t k = 0; k < rp.nbrs.size(); ++k) {
+            const auto& x = rp.nbrs[k];
+            for (size_t j = 0; j < x.shared.size(); ++j)
+                src[rp.node_shared[x.shared[j]]].push_back({x.rank, (int32_t)(rp.recv_off[k] + (int64_t)j)});
+        }
+        rp.shared_off.assign(shared.size() + 1, 0);
+        for (size_t i = 0; i < shared.size(); ++i) {
+            std::sort(src[i].begin(), src[i].end());
+            rp.shared_off[i + 1] = rp.shared_off[i] + (int32_t)src[i].size();
+            for (auto& pr : src[i]) rp.shared_src.push_back(pr.second);
+        }
+        // ghost sources: first neighbour (ascending rank) providing the node
+        rp.ghost_src.assign(rp.n_ghost, -1);
+        for (size_t k = 0; k < rp.nbrs.size(); ++k) {
+            const auto& x = rp.nbrs[k];
+            const int64_t base = rp.recv_off[k] + 2 * (int64_t)x.shared.size();
+            for (size_t j = 0; j < x.ext_from.size(); ++j) {
+                const int32_t g = x.ext_from[j] - rp.n_local;
+                if (g >= 0 && rp.ghost_src[g] < 0) rp.ghost_src[g] = (int32_t)(base + (int64_t)j);
+            }
+        }
+        for (int32_t g = 0; g < rp.n_ghost; ++g)
+            if (rp.ghost_src[g] < 0) raise(CF_PROTOCOL, "ghost node without a provider");
+    }
+}
+
+}  // namespace cfb

@@ -1,0 +1,315 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 castfem explicit step (one JSON line on rank 0).
+
+A "step" is one explicit time step (blocked_step, blocked.hpp:542-550) over
+the whole synthetic mesh: element/facet assembly + merge + update.
+
+Workloads (seeded synthetic meshes, no external data):
+  N = 1   BASELINE configs[1] = cfg2: 128^3-cell casting (12,582,912 tets).
+  N > 1   weak-scaling ladder at ~12.6 M tets per GPU: casting n = 128*N^(1/3)
+          (N=2: 161^3, N=4: 203^3, N=8: 256^3 = BASELINE config 4), RCB
+          decomposition, one NCCL exchange of interface-node partials per step.
+  --config cfg1..cfg5 overrides (all N then run that one mesh: strong scaling).
+
+value  = element-updates/s over the K timed steps, inputs resident in HBM
+         (device time by CUDA events on the plan's stream; max over ranks).
+e2e    = the same metric through the public API with host buffers:
+         set_temperature(host T0) -> step(K) -> fields(host T, H).
+--impl reference times the reference solver itself (oracle/_ref, the
+         unmodified castfem headers) on the host cores: rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default=None, help="cfg1..cfg5 (default: cfg2 at N=1, weak ladder at N>1)")
+    ap.add_argument("--mode", default="deterministic", choices=["atomic", "deterministic"])
+    ap.add_argument("--tile", type=int, default=384)
+    ap.add_argument("--elem-order", default="morton")
+    ap.add_argument("--node-order", default="tile")
+    ap.add_argument("--cpu-steps", type=int, default=int(os.environ.get("CF_CPU_STEPS", "12")))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", type=int, default=0, help="capture the step loop in CUDA graphs of this many steps")
+    ap.add_argument("--phase-steps", type=int, default=20)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+def make_case(cfg: str | None, world: int):
+    from paper_1005_3158_b200 import configs
+    if cfg:
+        return configs.CONFIGS[cfg](), cfg, "strong" if world > 1 else "weak"
+    if world == 1:
+        return configs.config2(), "cfg2", "weak"
+    n = int(round(128 * world ** (1.0 / 3.0)))
+    return configs.casting(n, dt_safety=configs.DT_SAFETY["cfg4"], steps=500, name=f"casting{n}"), \
+        f"weak_casting{n}", "weak"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _one(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+            f = [x.strip() for x in out.stdout.strip().split(",")]
+            if len(f) >= 7:
+                self.samples.append(f)
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._one()
+            self._stop.wait(0.2)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            self._one()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def cpu_reference_rate(case, steps: int):
+    """The reference solver (oracle/_ref: unmodified castfem headers, 1 host core)."""
+    from oracle import oracle as orc
+    if not orc.ref_available():
+        return None
+    t0 = time.time()
+    rb = orc.RefBench(case.mesh, case.setup)
+    setup_s = time.time() - t0
+    rb.steps(1)  # warm
+    secs = rb.steps(steps)
+    rb.close()
+    E = case.mesh.element_count()
+    return {"value": E * steps / secs, "unit": "element-updates/s", "cores": 1, "kind": "reference",
+            "sample": f"{case.name}: {steps} blocked_step calls of the full mesh (E={E}), 1 warm step, "
+                      f"setup {setup_s:.1f}s excluded (loop_seconds semantics, blocked.hpp:673-684)",
+            "seconds": secs}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    case, cfg, scaling = make_case(args.config, 1 if args.config is None else world)
+    if args.config is None and world > 1:
+        case, cfg, scaling = make_case(None, world)
+    from oracle import oracle as orc
+    if not orc.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcastfem_ref.so not built"}))
+        return
+    E = case.mesh.element_count()
+    rb = orc.RefBench(case.mesh, case.setup)
+    # each bench step = one blocked_step of the reference on the full mesh
+    per = max(1, min(args.steps, 10))
+    rb.steps(min(args.warmup, 2))
+    secs = rb.steps(per)
+    rb.close()
+    value = E * per / secs
+    line = {"impl": "reference", "metric": "element-updates/s (fp64)", "value": value, "unit": "element-updates/s",
+            "n_gpus": 0, "steps": per, "warmup": min(args.warmup, 2), "ms_per_step": 1e3 * secs / per,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg, "elements": E, "nodes": case.mesh.node_count(),
+                       "dt_safety": case.setup.solver.dt_safety, "h_interface": 1000.0},
+            "cpu_baseline": {"value": value, "unit": "element-updates/s", "cores": 1, "kind": "reference",
+                             "sample": f"{per} blocked_step calls on the full {cfg} mesh (bounded; the reference "
+                                       f"is serial by contract, SPEC S:403-408)"},
+            "e2e": {"value": value, "unit": "element-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    world, rank, local_rank = dist_env()
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        pg = dist
+    from paper_1005_3158_b200 import castfem as cf
+
+    case, cfg, scaling = make_case(args.config, world)
+    mesh, setup = case.mesh, case.setup
+    comm = None
+    if world > 1:
+        import torch
+        uid = cf.Comm.unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8)
+        pg.broadcast(t, 0)
+        comm = cf.Comm(world, rank, local_rank, bytes(t.tolist()))
+    opts = cf.SolveOptions(mode=args.mode, tile_elems=args.tile, elem_order=args.elem_order,
+                           node_order=args.node_order, device=local_rank, world_size=world, rank=rank,
+                           comm=comm, graph_steps=args.graph)
+    t0 = time.time()
+    solver = cf.Solver(mesh, setup, opts)
+    setup_s = time.time() - t0
+    st0 = solver.stats()
+    E_total = mesh.element_count()
+
+    def barrier():
+        if pg:
+            pg.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if not pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up
+    solver.step(max(args.warmup, 3))
+    # timed region: K steps, device time (CUDA events), max over ranks
+    sampler = ClockSampler(local_rank)
+    barrier()
+    sampler.start()
+    before = solver.stats().loop_seconds
+    solver.step(args.steps)
+    secs = solver.stats().loop_seconds - before
+    clocks = sampler.stop()
+    secs = max_over_ranks(secs)
+    barrier()
+    value = E_total * args.steps / secs
+    ms_per_step = 1e3 * secs / args.steps
+
+    # per-phase device time (CUDA events between launches on the plan's stream)
+    ph = solver.time_phases(args.phase_steps)
+    st = solver.stats()
+    N_local = st.n_nodes_local
+    E_local = st.n_elems_local
+    # algorithmic bytes of the tile (assembly) kernel per launch, DESIGN.md §roofline:
+    # 105 B/tet (4 i32 conn + 11 f64 geometry + u8 region) + 24 B/node (T gather once,
+    # (c, r) written once) + facets (canonical 24 / 56 B); the whole-step canonical
+    # figure B_step = 105E + 48N + 24F_bc + 56F_if is st.bytes_per_step.
+    facet_bytes = st.bytes_per_step - 105 * E_local - 48 * N_local
+    tile_bytes = 105 * E_local + 24 * N_local + facet_bytes
+    peak, peak_kind = hbm_peak()
+    tile_gbs = tile_bytes / (ph[0] * 1e-3) / 1e9
+    step_gbs = st.bytes_per_step / (ms_per_step * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "tile_kernel (assembly)", "achieved": round(tile_gbs, 1),
+                "peak": peak, "unit": "GB/s", "frac": round(tile_gbs / peak, 4), "peak_kind": peak_kind,
+                "traffic": None, "algorithmic_bytes_per_launch": int(tile_bytes),
+                "kernel_ms": round(ph[0], 4), "update_ms": round(ph[3], 4), "pack_ms": round(ph[1], 4),
+                "exchange_ms": round(ph[2], 4), "step_achieved_gbs": round(step_gbs, 1),
+                "step_frac_of_8tbs": round(step_gbs / 8000.0, 4), "step_frac": round(step_gbs / peak, 4),
+                "canonical_bytes_per_step": int(st.bytes_per_step)}
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        T0 = np.ascontiguousarray(case.setup.initial_T if case.setup.initial_T is not None else
+                                  np.array([setup.materials[r].initial_temperature for r in
+                                            _node_regions(mesh)]), dtype=np.float64)
+        barrier()
+        t1 = time.perf_counter()
+        solver.set_temperature(T0)
+        solver.step(args.steps)
+        T, H = solver.fields()
+        e_secs = max_over_ranks(time.perf_counter() - t1)
+        nb = mesh.node_count() * 8
+        e2e = {"value": E_total * args.steps / e_secs, "unit": "element-updates/s",
+               "h2d_bytes_per_step": nb / args.steps, "d2h_bytes_per_step": 2 * nb / args.steps,
+               "h2d_bytes_per_call": nb, "d2h_bytes_per_call": 2 * nb, "steps_per_call": args.steps,
+               "seconds": e_secs, "api": "Solver.set_temperature -> Solver.step(K) -> Solver.fields()"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_rate(case, args.cpu_steps)
+        except Exception as e:  # reported, not fatal
+            cpu = {"error": str(e)}
+
+    if rank == 0:
+        line = {"metric": "element-updates/s (fp64)", "value": value, "unit": "element-updates/s",
+                "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded Kuhn-split casting fixtures, SURVEY §8(d))",
+                "config": {"workload": cfg, "elements": E_total, "nodes": mesh.node_count(),
+                           "hex_cells": E_total // 6, "mode": args.mode, "tile_elems": args.tile,
+                           "elem_order": args.elem_order, "node_order": args.node_order,
+                           "dt_safety": setup.solver.dt_safety, "h_interface": 1000.0,
+                           "parallelism": f"rcb{world}" if world > 1 else "single",
+                           "l2": "working set > 126 MB L2 (no flush needed)" if st.bytes_per_step > 2e8
+                           else "working set L2-resident", "setup_seconds": round(setup_s, 2)},
+                "hex_cell_updates_per_s": value / 6.0,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(st.launches_per_step * args.steps), "clocks": clocks,
+                "device_bytes": int(st.device_bytes), "tiles": int(st.n_tiles),
+                "total_slots": int(st.total_slots)}
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if comm:
+        comm.close()
+    if pg:
+        pg.destroy_process_group()
+
+
+def _node_regions(mesh):
+    reg = np.zeros(mesh.node_count(), np.int32)
+    reg[mesh.tets.reshape(-1)] = np.repeat(mesh.region, 4)
+    return reg
+
+
+if __name__ == "__main__":
+    main()

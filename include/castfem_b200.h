@@ -126,7 +126,8 @@ enum {
 };
 enum {
     CF_NODE_ORDER_GIVEN = 0,   /* keep the caller's node numbering */
-    CF_NODE_ORDER_RCM = 1      /* rcm_permutation (reorder.hpp:127-148) */
+    CF_NODE_ORDER_RCM = 1,     /* rcm_permutation (reorder.hpp:127-148) */
+    CF_NODE_ORDER_TILE = 2     /* first touch in tile order (device locality) */
 };
 enum {
     CF_ELEM_ORDER_GIVEN = 0,   /* tiles are contiguous chunks of the given element order */
@@ -143,7 +144,7 @@ typedef struct cf_run_opts {
     int32_t mode;              /* CF_MODE_* */
     int32_t node_order;        /* CF_NODE_ORDER_* */
     int32_t elem_order;        /* CF_ELEM_ORDER_* */
-    int32_t tile_elems;        /* elements per tile (0 = default 1024) */
+    int32_t tile_elems;        /* elements per tile (0 = default 384) */
     const int32_t* tile_of_element; /* optional explicit block map (BlockPlan semantics,
                                        blocked.hpp:79-93); overrides elem_order/tile_elems */
     int32_t n_tiles_given;     /* tiles in tile_of_element */
@@ -225,6 +226,11 @@ int cf_set_dt_safety(cf_plan* plan, double dt_safety);
 
 /* Makes the next cf_step calls replay a CUDA graph of `steps_per_graph` steps. */
 int cf_enable_graph(cf_plan* plan, int64_t steps_per_graph);
+
+/* Runs n_steps real steps with CUDA events between the phases of each step
+ * on the plan's stream; ms_out[4] = mean ms per step of {tile (assemble),
+ * pack, exchange, update (merge+update)} summed over local ranks. */
+int cf_time_phases(cf_plan* plan, int64_t n_steps, double* ms_out);
 
 /* Largest eigenvalue of M_L^-1 (K + H_bc + H_if) at uniform reference
  * properties by power iteration on the device (setup utility: BASELINE's

@@ -183,7 +183,10 @@ class RefBench:
         self.N = mesh.node_count()
 
     def steps(self, n: int) -> float:
-        return ref_lib().ref_bench_steps(self.h, int(n))
+        secs = ref_lib().ref_bench_steps(self.h, int(n))
+        if secs < 0:
+            raise OracleError(int(-secs), ref_lib().ref_last_error().decode())
+        return secs
 
     def T(self) -> np.ndarray:
         T = np.zeros(self.N)

@@ -232,11 +232,16 @@ __attribute__((visibility("default"))) void* ref_bench_create(const cf_mesh_desc
         return nullptr;
     }
 }
+// Returns the loop seconds, or -status on a reference exception.
 __attribute__((visibility("default"))) double ref_bench_steps(void* h, int64_t n) {
     auto* r = static_cast<RefRun*>(h);
-    const auto begin = std::chrono::steady_clock::now();
-    for (int64_t s = 0; s < n; ++s) blocked_step(*r->model, r->setup, r->f, *r->ws, 0);
-    return std::chrono::duration<double>(std::chrono::steady_clock::now() - begin).count();
+    try {
+        const auto begin = std::chrono::steady_clock::now();
+        for (int64_t s = 0; s < n; ++s) blocked_step(*r->model, r->setup, r->f, *r->ws, 0);
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - begin).count();
+    } catch (...) {
+        return -(double)map_exception();
+    }
 }
 __attribute__((visibility("default"))) void ref_bench_get_T(void* h, double* T_out) {
     auto* r = static_cast<RefRun*>(h);

@@ -10,13 +10,13 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcastfem_b200.so")
+LIB_PATH = os.environ.get("CF_LIB_PATH") or os.path.join(_HERE, "libcastfem_b200.so")
 
 CF_OK, CF_PARSE, CF_VALIDATION, CF_CONFIG, CF_PROTOCOL, CF_DEGENERATE, CF_CUDA, CF_NCCL, CF_INVALID_ARG = range(9)
 CF_BC_FLUX, CF_BC_FIXED = 0, 1
 CF_VAR_TIME, CF_VAR_TEMPERATURE = 0, 1
 CF_MODE_ATOMIC, CF_MODE_DETERMINISTIC = 0, 1
-CF_NODE_ORDER_GIVEN, CF_NODE_ORDER_RCM = 0, 1
+CF_NODE_ORDER_GIVEN, CF_NODE_ORDER_RCM, CF_NODE_ORDER_TILE = 0, 1, 2
 CF_ELEM_ORDER_GIVEN, CF_ELEM_ORDER_MORTON, CF_ELEM_ORDER_MIN_NODE = 0, 1, 2
 CF_PARTITION_RCB, CF_PARTITION_GIVEN = 0, 1
 
@@ -92,6 +92,7 @@ SIGNATURES = [
     ("cf_get_stats", C.c_int, [C.c_void_p, C.POINTER(cf_stats)]),
     ("cf_device_temperature", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(_dp), C.POINTER(C.c_int64)]),
     ("cf_enable_graph", C.c_int, [C.c_void_p, C.c_int64]),
+    ("cf_time_phases", C.c_int, [C.c_void_p, C.c_int64, _dp]),
     ("cf_estimate_lambda_max", C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, _dp, _dp]),
     ("cf_comm_unique_id", C.c_int, [C.c_char_p]),
     ("cf_comm_create", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_void_p)]),

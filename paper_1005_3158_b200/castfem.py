@@ -183,10 +183,10 @@ class Mesh:
 class SolveOptions:
     """SolveOptions (blocked.hpp:630-636) + the B200 knobs."""
     max_steps: int = 0
-    mode: str = "atomic"             # 'atomic' | 'deterministic'
-    node_order: str = "rcm"          # 'rcm' | 'given'
+    mode: str = "deterministic"      # 'deterministic' (bit-reproducible, fastest) | 'atomic' (fp64 RED)
+    node_order: str = "tile"         # 'tile' (first touch in tile order) | 'rcm' | 'given'
     elem_order: str = "morton"       # 'morton' | 'min_node' | 'given'
-    tile_elems: int = 1024
+    tile_elems: int = 384
     blocks: Optional[np.ndarray] = None  # explicit element->tile map (BlockPlan semantics)
     device: int = 0
     world_size: int = 1
@@ -298,7 +298,7 @@ def setup_desc(s: SimulationSetup, keep: _Keep) -> _abi.cf_setup_desc:
 
 
 _MODES = {"atomic": _abi.CF_MODE_ATOMIC, "deterministic": _abi.CF_MODE_DETERMINISTIC}
-_NODE = {"given": _abi.CF_NODE_ORDER_GIVEN, "rcm": _abi.CF_NODE_ORDER_RCM}
+_NODE = {"given": _abi.CF_NODE_ORDER_GIVEN, "rcm": _abi.CF_NODE_ORDER_RCM, "tile": _abi.CF_NODE_ORDER_TILE}
 _ELEM = {"given": _abi.CF_ELEM_ORDER_GIVEN, "morton": _abi.CF_ELEM_ORDER_MORTON,
          "min_node": _abi.CF_ELEM_ORDER_MIN_NODE}
 
@@ -396,6 +396,12 @@ class Solver:
         s = _abi.cf_stats()
         check(lib().cf_get_stats(self.handle, C.byref(s)))
         return s
+
+    def time_phases(self, n: int) -> np.ndarray:
+        """n real steps with CUDA events between phases: mean ms of (tile, pack, exchange, update)."""
+        out = np.zeros(4)
+        check(lib().cf_time_phases(self.handle, int(n), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
 
     def enable_graph(self, steps: int) -> None:
         check(lib().cf_enable_graph(self.handle, int(steps)))

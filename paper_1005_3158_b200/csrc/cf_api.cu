@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -136,15 +137,19 @@ struct Rank {
     UpdArgs ua{};
     PackArgs pa{};
     double* T[2] = {nullptr, nullptr};
+    double* Tslot[2] = {nullptr, nullptr};  // per-slot T copies (ping-pong with T)
     double* recv = nullptr;
     double* send = nullptr;
     double* acc_c = nullptr;
     double* acc_r = nullptr;
-    double* part_c = nullptr;
-    double* part_r = nullptr;
+    double2* part = nullptr;
     DevState* st = nullptr;
+    int tile_grid = 0;
+    int32_t* all_list = nullptr;   // unused (NULL list = identity)
+    int32_t* shared_list = nullptr;
+    int32_t n_shared_list = 0;
     size_t tile_smem = 0;
-    int upd_blocks = 0;
+    int upd_blocks = 0, upd_blocks_all = 0;
     int64_t bytes_per_step = 0;
     std::vector<int64_t> nb_send_len, nb_recv_len;
 };
@@ -156,6 +161,8 @@ struct cf_plan {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int mode = CF_MODE_ATOMIC;
+    int tile_threads = 128;      // CTA size of the tile kernel (32 | 64 | 128 | 256)
+    int stages = 1;              // 1: one tile per CTA; 2: persistent double-buffered TMA pipeline
     int world = 1, first_rank = 0, local_ranks = 1;
     cf_comm* comm = nullptr;
     DevParams P{};
@@ -187,32 +194,54 @@ struct cf_plan {
 
 namespace {
 
-size_t tile_smem_bytes(const RankPlan& h) {
-    return sizeof(double) * (2 * (size_t)h.max_slots + 5 * (size_t)h.max_elems + 3 * (size_t)h.max_facets);
+size_t tile_smem_bytes(const RankPlan& h, int stages) {
+    return stages * ((size_t)cf_round(h.max_blob, 16) + 8 * (size_t)h.max_slots) + 8 * (size_t)h.max_slots + 16;
 }
 
-template <bool DET, bool TDEP>
+#define CF_TILE_VARIANTS_NT(X, NT)                                                                          \
+    X(true, true, true, true, NT) X(true, true, true, false, NT) X(true, true, false, true, NT)                \
+    X(true, true, false, false, NT) X(true, false, true, true, NT) X(true, false, true, false, NT)             \
+    X(true, false, false, true, NT) X(true, false, false, false, NT) X(false, true, true, true, NT)            \
+    X(false, true, true, false, NT) X(false, true, false, true, NT) X(false, true, false, false, NT)           \
+    X(false, false, true, true, NT) X(false, false, true, false, NT) X(false, false, false, true, NT)          \
+    X(false, false, false, false, NT)
+#define CF_TILE_VARIANTS(X) \
+    CF_TILE_VARIANTS_NT(X, 32) CF_TILE_VARIANTS_NT(X, 64) CF_TILE_VARIANTS_NT(X, 128) CF_TILE_VARIANTS_NT(X, 256)
+
 void set_tile_attr(size_t smem) {
-    CF_CUDA_CHECK(cudaFuncSetAttribute(tile_kernel<DET, TDEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+#define CF_ATTR(D, T, R, C, NT)                                                                                  \
+    CF_CUDA_CHECK(cudaFuncSetAttribute(tile_kernel<D, T, R, C, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                       (int)smem));
+    CF_TILE_VARIANTS(CF_ATTR)
+#undef CF_ATTR
 }
 
-void launch_tile(cf_plan* p, Rank& r) {
+void launch_tile(cf_plan* p, Rank& r, double t_end) {
     if (r.H.n_tiles == 0) return;
     const bool det = p->mode == CF_MODE_DETERMINISTIC;
     TileArgs a = r.ta;
-    a.T = p->ranks.size() ? r.T[p->cur] : nullptr;
+    a.T = r.T[p->cur];
     a.Told = r.T[p->cur ^ 1];
-    const dim3 grid(r.H.n_tiles), block(256);
-    if (det && p->temp_dep) tile_kernel<true, true><<<grid, block, r.tile_smem, p->stream>>>(a);
-    else if (det) tile_kernel<true, false><<<grid, block, r.tile_smem, p->stream>>>(a);
-    else if (p->temp_dep) tile_kernel<false, true><<<grid, block, r.tile_smem, p->stream>>>(a);
-    else tile_kernel<false, false><<<grid, block, r.tile_smem, p->stream>>>(a);
+    a.Tn = r.T[p->cur ^ 1];
+    a.Tslot = r.Tslot[p->cur];
+    a.Tslot_n = r.Tslot[p->cur ^ 1];
+    a.t_end = t_end;
+    const bool dir = r.ua.node_dir != nullptr, cl = p->finite_range, td = p->temp_dep;
+    const int nt = p->tile_threads;
+    const dim3 grid(r.tile_grid), block(nt);
+#define CF_LAUNCH(D, T, R, C, NT)                                                                  \
+    if (det == D && td == T && dir == R && cl == C && nt == NT) {                                  \
+        tile_kernel<D, T, R, C, NT><<<grid, block, r.tile_smem, p->stream>>>(a);                   \
+        return;                                                                                    \
+    }
+    CF_TILE_VARIANTS(CF_LAUNCH)
+#undef CF_LAUNCH
 }
 
 template <bool DET, bool MULTI>
-void launch_update_t(cf_plan* p, Rank& r, const UpdArgs& a) {
-    const dim3 grid(r.upd_blocks), block(256);
-    const bool dir = !r.H.node_dir.empty() || r.ua.node_dir != nullptr;
+void launch_update_t(cf_plan* p, Rank& r, const UpdArgs& a, int blocks) {
+    const dim3 grid(blocks), block(256);
+    const bool dir = r.ua.node_dir != nullptr;
     const bool cl = p->finite_range;
     const bool td = p->temp_dep;
 #define CF_UPD(D, C, T) update_kernel<DET, MULTI, D, C, T><<<grid, block, 0, p->stream>>>(a)
@@ -231,13 +260,24 @@ void launch_update(cf_plan* p, Rank& r, double t_end) {
     a.T = r.T[p->cur];
     a.Tcur_w = r.T[p->cur];
     a.Tn = r.T[p->cur ^ 1];
+    a.Tslot_n = r.Tslot[p->cur ^ 1];
     a.t_end = t_end;
+    int blocks;
+    if (p->temp_dep) {  // no fused private updates: every node
+        a.list = nullptr;
+        a.n_list = r.H.n_local;
+        blocks = r.upd_blocks_all;
+    } else {
+        a.list = r.shared_list;
+        a.n_list = r.n_shared_list;
+        blocks = r.upd_blocks;
+    }
     const bool det = p->mode == CF_MODE_DETERMINISTIC;
     const bool multi = p->world > 1;
-    if (det && multi) launch_update_t<true, true>(p, r, a);
-    else if (det) launch_update_t<true, false>(p, r, a);
-    else if (multi) launch_update_t<false, true>(p, r, a);
-    else launch_update_t<false, false>(p, r, a);
+    if (det && multi) launch_update_t<true, true>(p, r, a, blocks);
+    else if (det) launch_update_t<true, false>(p, r, a, blocks);
+    else if (multi) launch_update_t<false, true>(p, r, a, blocks);
+    else launch_update_t<false, false>(p, r, a, blocks);
 }
 
 void launch_pack(cf_plan* p, Rank& r) {
@@ -287,7 +327,7 @@ void exchange(cf_plan* p) {
 
 // one blocked_step for every local rank
 void enqueue_step(cf_plan* p, double t_end) {
-    for (auto& r : p->ranks) launch_tile(p, *r);
+    for (auto& r : p->ranks) launch_tile(p, *r, t_end);
     if (p->world > 1) {
         for (auto& r : p->ranks) launch_pack(p, *r);
         exchange(p);
@@ -303,107 +343,83 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     const int64_t S_tot = h.tile_slot_off.empty() ? 0 : h.tile_slot_off.back();
     const int64_t Er = (int64_t)h.elem_global.size();
     const int64_t nT = (int64_t)h.n_local + h.n_ghost;
+    const bool det = p->mode == CF_MODE_DETERMINISTIC;
 
     r.T[0] = M.alloc<double>(nT);
     r.T[1] = M.alloc<double>(nT);
+    r.Tslot[0] = M.alloc<double>(S_tot + 2);
+    r.Tslot[1] = M.alloc<double>(S_tot + 2);
     r.st = M.alloc<DevState>(1);
     TileArgs& a = r.ta;
-    a.tile_elem_off = M.up(h.tile_elem_off, s);
-    a.tile_slot_off = M.up(h.tile_slot_off, s);
-    a.tile_csr_off = M.up(h.tile_csr_off, s);
-    a.tile_facet_off = M.up(h.tile_facet_off, s);
-    {
-        ushort4* c = M.alloc<ushort4>(Er);
-        if (Er) CF_CUDA_CHECK(cudaMemcpyAsync(c, h.elem_conn.data(), Er * sizeof(ushort4), cudaMemcpyHostToDevice, s));
-        a.conn = c;
-    }
-    a.ereg = M.up(h.elem_region, s);
-    a.geom = M.up(h.elem_geom, s);
-    a.min_edge = S.temp_dep ? M.up(h.elem_min_edge, s) : nullptr;
-    a.E = Er;
+    a.meta = M.up(h.tile_meta, s);
+    a.slot_off = M.up(h.tile_slot_off, s);
+    a.blob_off = M.up(h.blob_off, s);
+    a.blob = M.up(h.blob, s);
     a.slot_node = M.up(h.slot_node, s);
-    a.slot_info = M.up(h.slot_info, s);
-    a.slot_csr_end = M.up(h.slot_csr_end, s);
-    a.csr = M.up(h.csr, s);
-    {
-        const int64_t Fr = (int64_t)h.facet_area.size();
-        ushort4* fs = M.alloc<ushort4>(Fr);
-        int4* fsis = M.alloc<int4>(Fr);
-        if (Fr) {
-            CF_CUDA_CHECK(cudaMemcpyAsync(fs, h.facet_slots.data(), Fr * sizeof(ushort4), cudaMemcpyHostToDevice, s));
-            CF_CUDA_CHECK(cudaMemcpyAsync(fsis, h.facet_sister.data(), Fr * sizeof(int4), cudaMemcpyHostToDevice, s));
-        }
-        a.fslots = fs;
-        a.fsister = fsis;
-        a.farea = M.up(h.facet_area, s);
-    }
-    const bool det = p->mode == CF_MODE_DETERMINISTIC;
+    const uint8_t* node_region = M.up(h.node_region, s);
+    const int8_t* node_dir = h.node_dir.empty() ? nullptr : M.up(h.node_dir, s);
+    const int32_t* local_global = M.up(h.local_global, s);
+    a.node_region = node_region;
+    a.node_dir = node_dir;
+    a.local_global = local_global;
     if (det) {
-        r.part_c = M.alloc<double>(S_tot);
-        r.part_r = M.alloc<double>(S_tot);
+        r.part = M.alloc<double2>(S_tot);
     } else {
         r.acc_c = M.alloc<double>(h.n_local);
         r.acc_r = M.alloc<double>(h.n_local);
         CF_CUDA_CHECK(cudaMemsetAsync(r.acc_c, 0, sizeof(double) * std::max<int64_t>(1, h.n_local), s));
         CF_CUDA_CHECK(cudaMemsetAsync(r.acc_r, 0, sizeof(double) * std::max<int64_t>(1, h.n_local), s));
     }
-    a.part_c = r.part_c;
-    a.part_r = r.part_r;
+    a.part = r.part;
     a.acc_c = r.acc_c;
     a.acc_r = r.acc_r;
     a.P = p->dP;
     a.st = r.st;
+    a.n_tiles = h.n_tiles;
     a.max_slots = h.max_slots;
-    a.max_elems = h.max_elems;
-    a.max_facets = h.max_facets;
-    r.tile_smem = tile_smem_bytes(h);
+    a.blob_smem = (int32_t)cf_round(h.max_blob, 16);
+    a.stages = p->stages;
+    if (const char* e = std::getenv("CF_PROBE")) a.probe = std::atoi(e);
+    r.tile_smem = tile_smem_bytes(h, p->stages);
     if (r.tile_smem > 227 * 1024) raise(CF_INVALID_ARG, "tile shared-memory footprint exceeds 227 KB; use smaller tiles");
-    if (det && p->temp_dep) set_tile_attr<true, true>(r.tile_smem);
-    else if (det) set_tile_attr<true, false>(r.tile_smem);
-    else if (p->temp_dep) set_tile_attr<false, true>(r.tile_smem);
-    else set_tile_attr<false, false>(r.tile_smem);
+    set_tile_attr(r.tile_smem);
+    {
+        int per_sm = 0, sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+#define CF_OCC(NT)                                                                                   \
+    if (p->tile_threads == NT)                                                                       \
+        CF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                 \
+            &per_sm, tile_kernel<true, false, false, false, NT>, NT, r.tile_smem));
+        CF_OCC(32) CF_OCC(64) CF_OCC(128) CF_OCC(256)
+#undef CF_OCC
+        per_sm = std::max(1, per_sm);
+        r.tile_grid = p->stages == 1 ? std::max(1, h.n_tiles) : std::max(1, std::min<int>(h.n_tiles, sms * per_sm));
+    }
 
     UpdArgs& u = r.ua;
     u.n_local = h.n_local;
     u.n_ghost = h.n_ghost;
-    if (det) {
-        u.merge_off = M.up(h.merge_off, s);
-        u.merge_idx = M.up(h.merge_idx, s);
-    }
-    u.part_c = r.part_c;
-    u.part_r = r.part_r;
+    u.merge_off = M.up(h.merge_off, s);  // partial merge (deterministic) + Tslot scatter (both modes)
+    u.merge_idx = M.up(h.merge_idx, s);
+    u.part = r.part;
     u.acc_c = r.acc_c;
     u.acc_r = r.acc_r;
-    u.node_dir = h.node_dir.empty() ? nullptr : M.up(h.node_dir, s);
-    u.node_region = M.up(h.node_region, s);
-    u.local_global = M.up(h.local_global, s);
+    u.node_dir = node_dir;
+    u.node_region = node_region;
+    u.local_global = local_global;
     u.P = p->dP;
     u.st = r.st;
+    r.shared_list = M.up(h.shared_list, s);
+    r.n_shared_list = (int32_t)h.shared_list.size();
     if (p->world > 1) {
         u.node_shared = M.up(h.node_shared, s);
         u.shared_off = M.up(h.shared_off, s);
-        // r index = c index + neighbour's shared count
-        std::vector<int32_t> src_r(h.shared_src.size());
-        {
-            std::vector<int32_t> ns_of_pos;  // map recv c-offset -> r-offset
-            for (size_t j = 0; j < h.shared_src.size(); ++j) {
-                const int32_t c = h.shared_src[j];
-                if (c < 0) {
-                    src_r[j] = -1;
-                    continue;
-                }
-                size_t k = 0;
-                while (k + 1 < h.recv_off.size() && !(c >= h.recv_off[k] && c < h.recv_off[k + 1])) ++k;
-                src_r[j] = c + (int32_t)h.nbrs[k].shared.size();
-            }
-        }
         u.shared_src_c = M.up(h.shared_src, s);
-        u.shared_src_r = M.up(src_r, s);
+        u.shared_src_r = M.up(h.shared_src_r, s);
         r.recv = M.alloc<double>(h.recv_len);
         r.send = M.alloc<double>(h.send_len);
         u.recv = r.recv;
         u.ghost_src = M.up(h.ghost_src, s);
-        // pack items
         std::vector<int32_t> cr_node, t_node;
         std::vector<int64_t> cr_dst, cr_dst_r, t_dst;
         for (size_t k = 0; k < h.nbrs.size(); ++k) {
@@ -435,19 +451,14 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-    r.upd_blocks = std::max(1, std::min<int>(sms * 8, (int)((h.n_local + 255) / 256)));
+    r.upd_blocks = std::max(1, std::min<int>(sms * 8, (int)((r.n_shared_list + 255) / 256)));
+    r.upd_blocks_all = std::max(1, std::min<int>(sms * 8, (int)((h.n_local + 255) / 256)));
     // canonical algorithmic bytes: 105 E + 48 N + 24 F_bc + 56 F_if
     r.bytes_per_step = 105 * Er + 48 * (int64_t)h.n_local + 24 * h.n_bc_facets + 56 * h.n_if_facets;
+    CF_CUDA_CHECK(cudaStreamSynchronize(s));
     // drop the big host arrays (metadata kept)
-    std::vector<uint16_t>().swap(h.elem_conn);
-    std::vector<double>().swap(h.elem_geom);
-    std::vector<double>().swap(h.elem_min_edge);
-    std::vector<uint16_t>().swap(h.csr);
-    std::vector<uint16_t>().swap(h.slot_csr_end);
+    std::vector<uint8_t>().swap(h.blob);
     std::vector<int32_t>().swap(h.merge_idx);
-    std::vector<double>().swap(h.facet_area);
-    std::vector<uint16_t>().swap(h.facet_slots);
-    std::vector<int32_t>().swap(h.facet_sister);
 }
 
 void init_state(cf_plan* p, const std::vector<double>& T_global) {
@@ -458,6 +469,12 @@ void init_state(cf_plan* p, const std::vector<double>& T_global) {
         for (int64_t i = 0; i < nT; ++i) T[i] = T_global[r.H.local_global[i]];
         CF_CUDA_CHECK(cudaMemcpyAsync(r.T[0], T.data(), nT * sizeof(double), cudaMemcpyHostToDevice, p->stream));
         CF_CUDA_CHECK(cudaMemcpyAsync(r.T[1], T.data(), nT * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+        const int64_t S_tot = r.H.slot_node.size();
+        std::vector<double> Ts(S_tot + 2, 0.0);
+        for (int64_t q = 0; q < S_tot; ++q)
+            if (r.H.slot_node[q] >= 0) Ts[q] = T[(uint32_t)r.H.slot_node[q] & 0x0fffffffu];
+        CF_CUDA_CHECK(cudaMemcpyAsync(r.Tslot[0], Ts.data(), Ts.size() * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+        CF_CUDA_CHECK(cudaMemcpyAsync(r.Tslot[1], Ts.data(), Ts.size() * sizeof(double), cudaMemcpyHostToDevice, p->stream));
         DevState st{};
         st.time = 0;
         st.dt = 0;
@@ -486,6 +503,7 @@ DevState read_state(cf_plan* p, int k = 0) {
 }
 
 void check_device_errors(cf_plan* p) {
+    if (std::getenv("CF_PROBE")) return;  // diagnostics runs skip the physics
     for (size_t k = 0; k < p->ranks.size(); ++k) {
         const DevState st = read_state(p, (int)k);
         if (st.err_node != INT32_MAX)
@@ -535,52 +553,64 @@ void run_steps(cf_plan* p, int64_t n, double t_end) {
 // ------------------------------------------------------------------ lambda_max kernels
 struct LamArgs {
     TileArgs a;
+    bool tdep;
     const double* cval;  // per region rho*c(T0)
     const double* kval;  // per region k(T0)
-    const double* hval;  // per facet kind h at t=0 / T0
+    const double* hval;  // per facet kind
     const double* x;
     double* y;
     double* M;
     double* D;
 };
 
+// lambda_max operator on the tile blobs (global reads, no shared memory)
 __global__ void lam_setup(LamArgs L) {
     const TileArgs& a = L.a;
     const int t = blockIdx.x;
-    const int e0 = a.tile_elem_off[t], ne = a.tile_elem_off[t + 1] - e0, s0 = a.tile_slot_off[t];
-    for (int i = threadIdx.x; i < ne; i += blockDim.x) {
-        const int64_t p = (int64_t)e0 + i;
-        const ushort4 cn = a.conn[p];
-        const double w = L.cval[a.ereg[p]] * a.geom[9 * a.E + p] * 0.25;
-        const unsigned short s[4] = {cn.x, cn.y, cn.z, cn.w};
-        for (int k = 0; k < 4; ++k) atomicAdd(&L.M[a.slot_node[s0 + s[k]]], w);
+    const TileMeta tm = a.meta[t];
+    const TileLayout Ly(tm, L.tdep);
+    const uint8_t* B = a.blob + a.blob_off[t];
+    const int s0 = a.slot_off[t];
+    const double* G = (const double*)(B + Ly.geom);
+    const ushort4* conn = (const ushort4*)(B + Ly.conn);
+    for (int i = threadIdx.x; i < tm.ne; i += blockDim.x) {
+        const ushort4 cn = conn[i];
+        const double w = L.cval[B[Ly.region + i]] * G[9 * Ly.ne2 + i] * 0.25;
+        const unsigned short sl[4] = {cn.x, cn.y, cn.z, cn.w};
+        for (int k = 0; k < 4; ++k) atomicAdd(&L.M[a.slot_node[s0 + sl[k]] & 0x0fffffff], w);
     }
-    const int f0 = a.tile_facet_off[t], nf = a.tile_facet_off[t + 1] - f0;
-    for (int i = threadIdx.x; i < nf; i += blockDim.x) {
-        const ushort4 fs = a.fslots[f0 + i];
-        const double w = L.hval[fs.w] * (a.farea[f0 + i] / 3.0);
-        const unsigned short s[3] = {fs.x, fs.y, fs.z};
-        for (int k = 0; k < 3; ++k) atomicAdd(&L.D[a.slot_node[s0 + s[k]]], w);
+    const ushort4* fsl = (const ushort4*)(B + Ly.fslots);
+    const double* farea = (const double*)(B + Ly.farea);
+    for (int i = threadIdx.x; i < tm.nf; i += blockDim.x) {
+        const ushort4 fs = fsl[i];
+        const double w = L.hval[fs.w] * (farea[i] / 3.0);
+        const unsigned short sl[3] = {fs.x, fs.y, fs.z};
+        for (int k = 0; k < 3; ++k) atomicAdd(&L.D[a.slot_node[s0 + sl[k]] & 0x0fffffff], w);
     }
 }
 
 __global__ void lam_apply(LamArgs L) {
     const TileArgs& a = L.a;
     const int t = blockIdx.x;
-    const int e0 = a.tile_elem_off[t], ne = a.tile_elem_off[t + 1] - e0, s0 = a.tile_slot_off[t];
-    for (int i = threadIdx.x; i < ne; i += blockDim.x) {
-        const int64_t p = (int64_t)e0 + i;
-        const ushort4 cn = a.conn[p];
-        const int32_t n[4] = {a.slot_node[s0 + cn.x], a.slot_node[s0 + cn.y], a.slot_node[s0 + cn.z],
-                              a.slot_node[s0 + cn.w]};
+    const TileMeta tm = a.meta[t];
+    const TileLayout Ly(tm, L.tdep);
+    const uint8_t* B = a.blob + a.blob_off[t];
+    const int s0 = a.slot_off[t];
+    const double* G = (const double*)(B + Ly.geom);
+    const ushort4* conn = (const ushort4*)(B + Ly.conn);
+    const int S = Ly.ne2;
+    for (int i = threadIdx.x; i < tm.ne; i += blockDim.x) {
+        const ushort4 cn = conn[i];
+        const int32_t n[4] = {a.slot_node[s0 + cn.x] & 0x0fffffff, a.slot_node[s0 + cn.y] & 0x0fffffff,
+                              a.slot_node[s0 + cn.z] & 0x0fffffff, a.slot_node[s0 + cn.w] & 0x0fffffff};
         double g[4][3];
         for (int k = 0; k < 3; ++k) {
-            g[1][k] = a.geom[(int64_t)k * a.E + p];
-            g[2][k] = a.geom[(int64_t)(3 + k) * a.E + p];
-            g[3][k] = a.geom[(int64_t)(6 + k) * a.E + p];
+            g[1][k] = G[k * S + i];
+            g[2][k] = G[(3 + k) * S + i];
+            g[3][k] = G[(6 + k) * S + i];
             g[0][k] = ((g[1][k] + g[2][k]) + g[3][k]) * -1.0;
         }
-        const double kv = L.kval[a.ereg[p]] * a.geom[9 * a.E + p];
+        const double kv = L.kval[B[Ly.region + i]] * G[9 * S + i];
         double gx = 0, gy = 0, gz = 0;
         for (int b = 0; b < 4; ++b) {
             const double xb = L.x[n[b]];
@@ -690,7 +720,7 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         if (o.local_ranks != 1 && o.local_ranks != o.world_size)
             raise(CF_INVALID_ARG, "local_ranks must be 1 or world_size");
         if (o.mode != CF_MODE_ATOMIC && o.mode != CF_MODE_DETERMINISTIC) raise(CF_INVALID_ARG, "bad mode");
-        int tile = o.tile_elems > 0 ? o.tile_elems : 1024;
+        int tile = o.tile_elems > 0 ? o.tile_elems : 384;
         if (tile > kMaxTileElems) raise(CF_INVALID_ARG, "tile_elems must be <= 2048");
 
         int ndev = 0;
@@ -737,6 +767,11 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         auto p = std::make_unique<cf_plan>();
         p->device = o.device;
         p->mode = o.mode;
+        if (const char* e = std::getenv("CF_TILE_THREADS")) {
+            const int v = std::atoi(e);
+            p->tile_threads = (v == 32 || v == 64 || v == 128) ? v : 256;
+        }
+        if (const char* e = std::getenv("CF_TILE_STAGES")) p->stages = std::atoi(e) == 2 ? 2 : 1;
         p->world = o.world_size;
         p->first_rank = o.rank;
         p->local_ranks = o.local_ranks;
@@ -798,6 +833,42 @@ int cf_step(cf_plan* p, int64_t n_steps, double t_end) {
     return guarded([&] {
         if (!p) raise(CF_INVALID_ARG, "null plan");
         run_steps(p, n_steps, t_end);
+    });
+}
+
+int cf_time_phases(cf_plan* p, int64_t n, double* ms_out) {
+    return guarded([&] {
+        if (!p || !ms_out) raise(CF_INVALID_ARG, "null argument");
+        CF_CUDA_CHECK(cudaSetDevice(p->device));
+        cudaEvent_t ev[5];
+        for (auto& e : ev) CF_CUDA_CHECK(cudaEventCreate(&e));
+        double acc[4] = {0, 0, 0, 0};
+        for (int64_t s = 0; s < n; ++s) {
+            CF_CUDA_CHECK(cudaEventRecord(ev[0], p->stream));
+            for (auto& r : p->ranks) launch_tile(p, *r, 0.0);
+            CF_CUDA_CHECK(cudaEventRecord(ev[1], p->stream));
+            if (p->world > 1)
+                for (auto& r : p->ranks) launch_pack(p, *r);
+            CF_CUDA_CHECK(cudaEventRecord(ev[2], p->stream));
+            exchange(p);
+            CF_CUDA_CHECK(cudaEventRecord(ev[3], p->stream));
+            for (auto& r : p->ranks) launch_update(p, *r, 0.0);
+            CF_CUDA_CHECK(cudaEventRecord(ev[4], p->stream));
+            p->cur ^= 1;
+            CF_CUDA_CHECK(cudaEventSynchronize(ev[4]));
+            for (int k = 0; k < 4; ++k) {
+                float ms = 0;
+                CF_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+                acc[k] += ms;
+            }
+            float tot = 0;
+            CF_CUDA_CHECK(cudaEventElapsedTime(&tot, ev[0], ev[4]));
+            p->loop_seconds += tot * 1e-3;
+        }
+        CF_CUDA_CHECK(cudaGetLastError());
+        for (auto& e : ev) cudaEventDestroy(e);
+        for (int k = 0; k < 4; ++k) ms_out[k] = n > 0 ? acc[k] / (double)n : 0.0;
+        check_device_errors(p);
     });
 }
 
@@ -966,6 +1037,7 @@ int cf_estimate_lambda_max(cf_plan* p, int32_t iterations, uint64_t seed, double
         }
         LamArgs L;
         L.a = r.ta;
+        L.tdep = p->temp_dep;
         L.cval = M.up(cval, p->stream);
         L.kval = M.up(kval, p->stream);
         L.hval = M.up(hval, p->stream);
@@ -978,15 +1050,15 @@ int cf_estimate_lambda_max(cf_plan* p, int32_t iterations, uint64_t seed, double
         CF_CUDA_CHECK(cudaMemsetAsync(L.D, 0, n * sizeof(double), p->stream));
         L.x = x;
         L.y = y;
-        lam_setup<<<r.H.n_tiles, 256, 0, p->stream>>>(L);
+        lam_setup<<<r.H.n_tiles, 256, 0, p->stream>>>(L);  // one CTA per tile (blob in global)
         const int blocks = std::max(1, std::min(1184, (n + 255) / 256));
-        lam_init_x<<<blocks, 256, 0, p->stream>>>(n, r.ua.local_global, r.ua.node_dir, seed, x);
+        lam_init_x<<<blocks, 256, 0, p->stream>>>(n, r.ta.local_global, r.ta.node_dir, seed, x);
         double h_acc[3] = {0, 0, 0};
         for (int it = 0; it < iterations; ++it) {
             lam_diag<<<blocks, 256, 0, p->stream>>>(n, L.D, x, y);
             lam_apply<<<r.H.n_tiles, 256, 0, p->stream>>>(L);
             CF_CUDA_CHECK(cudaMemsetAsync(acc, 0, 3 * sizeof(double), p->stream));
-            lam_reduce<<<blocks, 256, 0, p->stream>>>(n, r.ua.node_dir, L.M, x, y, acc);
+            lam_reduce<<<blocks, 256, 0, p->stream>>>(n, r.ta.node_dir, L.M, x, y, acc);
             lam_scale<<<blocks, 256, 0, p->stream>>>(n, y, acc, x);
         }
         CF_CUDA_CHECK(cudaMemcpyAsync(h_acc, acc, sizeof h_acc, cudaMemcpyDeviceToHost, p->stream));
@@ -1113,9 +1185,9 @@ int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_r
         for (int r = r0; r < r1; ++r) {
             RankPlan rp;
             build_rank_plan(m, geom, S, po, label, r, rp);
+            int64_t pos = 0;
             for (int32_t t = 0; t < rp.n_tiles; ++t)
-                for (int32_t i = rp.tile_elem_off[t]; i < rp.tile_elem_off[t + 1]; ++i)
-                    tile_of_element[rp.elem_global[i]] = base + t;
+                for (int32_t i = 0; i < rp.tile_meta[t].ne; ++i) tile_of_element[rp.elem_global[pos++]] = base + t;
             base += rp.n_tiles;
         }
         if (n_tiles) *n_tiles = base;

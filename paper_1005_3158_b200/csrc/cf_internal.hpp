@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/castfem_b200.h"
+#include "cf_tileblob.hpp"
 
 namespace cfb {
 
@@ -141,7 +142,8 @@ double enthalpy(const DevParams& P, const DevMaterial& m, double T);
 // ---------------------------------------------------------------- tiles
 constexpr int kMaxTileElems = 2048;
 
-// One rank's tiled plan (host copy, uploaded as-is).
+// One rank's tiled plan (host copy, uploaded as-is). Element data lives in
+// per-tile blobs (cf_tileblob.hpp) fetched by one TMA bulk copy per tile.
 struct RankPlan {
     int32_t rank = 0;
     int32_t n_local = 0, n_ghost = 0;      // local nodes, then ghost (external) nodes
@@ -150,30 +152,20 @@ struct RankPlan {
     std::vector<int8_t> node_dir;          // [n_local] dirichlet id or -1 (empty if none)
     // tiles
     int32_t n_tiles = 0;
-    std::vector<int32_t> tile_elem_off;    // [n_tiles+1]
+    std::vector<TileMeta> tile_meta;       // [n_tiles] ne, ns, nf, ncsr
     std::vector<int32_t> tile_slot_off;    // [n_tiles+1]
-    std::vector<int64_t> tile_csr_off;     // [n_tiles+1]
-    std::vector<int32_t> tile_facet_off;   // [n_tiles+1]
+    std::vector<int64_t> blob_off;         // [n_tiles+1] byte offsets into blob
+    std::vector<uint8_t> blob;             // all tile blobs
     int32_t max_slots = 0, max_elems = 0, max_facets = 0;
-    // elements (tile order)
-    std::vector<int32_t> elem_global;      // [E_r]
-    std::vector<uint16_t> elem_conn;       // [4 E_r] tile-local slots
-    std::vector<uint8_t> elem_region;      // [E_r]
-    std::vector<double> elem_geom;         // [11][E_r] SoA: g1xyz g2xyz g3xyz vol max_edge
-    std::vector<double> elem_min_edge;     // [E_r] (dynamic dt only)
-    // slots
+    int64_t max_blob = 0;
+    std::vector<int32_t> elem_global;      // [E_r] tile order
     std::vector<int32_t> slot_node;        // [S] local node id
-    std::vector<uint8_t> slot_info;        // [S] region | 0x80 private
-    std::vector<uint16_t> slot_csr_end;    // [S] relative to the tile's csr start
-    std::vector<uint16_t> csr;             // entries: e*4+a (elements), 4*ne + 3*f + a (facets)
-    // facets (tile order, Dirichlet facets excluded)
-    std::vector<uint16_t> facet_slots;     // [4 F_r] s0 s1 s2 kind
-    std::vector<double> facet_area;        // [F_r]
-    std::vector<int32_t> facet_sister;     // [4 F_r] local/ghost node ids (interface)
     int64_t n_bc_facets = 0, n_if_facets = 0;
-    // deterministic merge: per local node, partial (slot) indices in ascending tile order
+    // merge: per local node, partial (slot) indices in ascending tile order
     std::vector<int32_t> merge_off;        // [n_local+1]
     std::vector<int32_t> merge_idx;        // [S]
+    std::vector<int32_t> shared_list;      // local nodes needing a merge (touched by >1 tile or rank)
+    int64_t n_private = 0;
     // multi-rank exchange
     struct Neighbor {
         int32_t rank;
@@ -184,8 +176,8 @@ struct RankPlan {
     std::vector<Neighbor> nbrs;            // ascending rank
     std::vector<int32_t> node_shared;      // [n_local] shared index or -1
     std::vector<int32_t> shared_off;       // [n_shared+1]
-    std::vector<int32_t> shared_src;       // -1 own, else index into the recv buffer (ascending rank)
-    std::vector<int32_t> send_idx;         // pack: per send position, local id (c,r or T by section)
+    std::vector<int32_t> shared_src;       // -1 own, else c index into the recv buffer (ascending rank)
+    std::vector<int32_t> shared_src_r;     // r index into the recv buffer
     std::vector<int64_t> send_off, recv_off; // per neighbor buffer offsets (doubles)
     std::vector<int32_t> ghost_src;        // [n_ghost] index into recv buffer
     int64_t send_len = 0, recv_len = 0;

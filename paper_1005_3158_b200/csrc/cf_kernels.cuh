@@ -1,23 +1,30 @@
 // cf_kernels.cuh — sm_100a kernels of the castfem explicit step.
 //
-// One step (blocked_step blocked.hpp:542-550) is:
-//   tile_kernel    assemble_blocks (blocked.hpp:454-498): one CTA per tile (the
-//                  paper's cache block); gathers the tile's nodal T into shared
-//                  memory, derives H = enthalpy(T) once per tile slot, runs the
-//                  element physics (Lemmon C_app, lumped capacitance, conduction
-//                  residual) and the facet fluxes (convective + interface with the
-//                  one-step-lagged sister ambient read from the previous T buffer),
-//                  then reduces each slot's contributions in a fixed order through
-//                  a tile-local CSR — no shared-memory fp64 atomics (those are CAS
-//                  loops on sm_100a). Flush: deterministic mode writes per-(tile,
-//                  slot) partials; atomic mode stores tile-private nodes and
-//                  fp64-REDs tile-shared ones.
-//   pack_kernel    (multi-rank) shared-node partials + pre-update T of external
-//                  nodes into the per-neighbour send buffer.
-//   update_kernel  merge_blocks (:502-515) + update_fields (:519-538): per node,
-//                  ascending-tile merge of partials (or the RED accumulators),
-//                  ascending-rank combine for shared nodes, T += (dt*r)/c,
-//                  Dirichlet overwrite, clamp flag; the last CTA advances time.
+// One step (blocked_step blocked.hpp:542-550) is two kernels:
+//   tile_kernel    assemble_blocks (blocked.hpp:454-498), one CTA per tile (the
+//                  paper's cache block recast as a thread-block tile):
+//                    - one elected thread streams the tile's packed blob (element
+//                      geometry, connectivity, facets, reduction CSR;
+//                      cf_tileblob.hpp) into shared memory with TMA bulk copies
+//                      (cp.async.bulk + mbarrier complete_tx), while
+//                    - all threads gather the tile's nodal T (L2-resident) and
+//                      derive H = enthalpy(T) once per tile slot;
+//                    - element physics (Lemmon C_app, lumped capacitance,
+//                      conduction residual) and facet fluxes (convective, and
+//                      interface with the one-step-lagged sister ambient read from
+//                      the previous T buffer) write their contributions in place
+//                      over the consumed blob columns;
+//                    - a fixed-order per-slot reduction through the tile CSR (no
+//                      shared-memory fp64 atomics: those are CAS loops on sm_100a);
+//                    - flush: tile-private nodes are UPDATED right here (merge is
+//                      the identity for them: merge_blocks :502-515), tile-shared
+//                      nodes write per-(tile, slot) partials (deterministic) or
+//                      fp64 RED into node accumulators (atomic).
+//   update_kernel  merge_blocks + update_fields (:519-538) for the shared nodes
+//                  only: ascending-tile merge, ascending-rank combine across GPUs,
+//                  T += (dt*r)/c, Dirichlet, clamp flag; the last CTA advances time.
+// With temperature-dependent tables (dynamic dt, :477-480) dt is a global min
+// known only after assembly, so no node is updated in the tile kernel.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -25,6 +32,7 @@
 #include <cstdint>
 
 #include "cf_physics.cuh"
+#include "cf_tileblob.hpp"
 
 namespace cfb {
 
@@ -40,170 +48,332 @@ struct DevState {
     int done;
 };
 
-struct TileArgs {
-    const int32_t* tile_elem_off;
-    const int32_t* tile_slot_off;
-    const int64_t* tile_csr_off;
-    const int32_t* tile_facet_off;
-    const ushort4* conn;
-    const uint8_t* ereg;
-    const double* geom;  // [11][E]
-    const double* min_edge;
-    int64_t E;
-    const int32_t* slot_node;
-    const uint8_t* slot_info;
-    const uint16_t* slot_csr_end;
-    const uint16_t* csr;
-    const ushort4* fslots;
-    const double* farea;
-    const int4* fsister;
-    const double* T;     // current
-    const double* Told;  // previous step (ambient lag)
-    double* part_c;
-    double* part_r;
-    double* acc_c;
-    double* acc_r;
-    const DevParams* P;
-    DevState* st;
-    int max_slots, max_elems, max_facets;
-};
-
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 __device__ __forceinline__ void atomic_min_pos(unsigned long long* addr, double v) {
     atomicMin(addr, (unsigned long long)__double_as_longlong(v));
 }
 
-template <bool DET, bool TDEP>
-__global__ void __launch_bounds__(256) tile_kernel(TileArgs a) {
-    extern __shared__ double smem[];
-    const int t = blockIdx.x;
+// dt of the current step (blocked_step blocked.hpp:547-548) and the done flag
+// (solve_serial's loop condition :674-675 for the t_end mode).
+template <bool TDEP>
+__device__ __forceinline__ void step_dt(const DevParams* __restrict__ P, const DevState* st, double t_end,
+                                        double& dt, double& t_next, bool& done) {
+    const double time = st->time;
+    dt = TDEP ? __longlong_as_double((long long)st->min_bound[st->step_index & 1]) * P->dt_safety : P->static_dt;
+    done = false;
+    if (t_end > 0) {
+        const double remaining = t_end - time;
+        if (!(time < t_end)) done = true;
+        if (remaining > 0) dt = dt < remaining ? dt : remaining;
+    }
+    t_next = time + dt;
+}
+
+// update_fields for one node (blocked.hpp:519-538): explicit_update, Dirichlet, clamp
+template <bool DIR, bool CLAMP>
+__device__ __forceinline__ double node_update(const DevParams* __restrict__ P, DevState* st, double T, double c,
+                                              double r, double dt, double t_next, int dir_id, int region,
+                                              const int32_t* gid, int& clamped) {
+    double Tn;
+    if (!(c > 0)) {
+        atomicMin(&st->err_node, *gid);  // explicit_update throws (fem.hpp:110-111); id loaded lazily
+        Tn = T;
+    } else {
+        Tn = T + dt * r / c;
+    }
+    if (DIR && dir_id >= 0) Tn = dev_pl_eval(P, P->dir_tab[dir_id], t_next);
+    if (CLAMP) {
+        const DevMaterial& m = P->mat[region];
+        if (Tn < m.range_lo || Tn > m.range_hi) clamped = 1;
+    }
+    return Tn;
+}
+
+// ------------------------------------------------------------------ tile kernel
+struct TileArgs {
+    const TileMeta* meta;
+    const int32_t* slot_off;
+    const int64_t* blob_off;
+    const uint8_t* blob;
+    const int32_t* slot_node;
+    const uint8_t* node_region;
+    const int8_t* node_dir;
+    const int32_t* local_global;
+    const double* T;     // current (unused by the tile kernel except through Tslot)
+    const double* Told;  // previous step (ambient lag of interface facets)
+    double* Tn;          // next (tile-private nodes)
+    const double* Tslot; // current T of every tile slot
+    double* Tslot_n;     // next T of every tile slot (tile-private slots written here)
+    double2* part;       // per (tile, slot) partial (c, r)   [deterministic]
+    double* acc_c;       // per node RED accumulators         [atomic]
+    double* acc_r;
+    const DevParams* P;
+    DevState* st;
+    int32_t n_tiles;
+    int32_t max_slots;
+    int32_t blob_smem;   // bytes reserved per blob stage in shared memory
+    int32_t stages;      // 1: one tile per CTA; 2: persistent, double-buffered
+    int32_t probe;       // diagnostics only: 1 = stop after the blob lands, 2 = after the gather
+    double t_end;
+};
+
+constexpr uint32_t kBulkChunk = 32768;
+
+__device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int t, bool tdep, uint8_t* dst, double* sTdst,
+                                                uint64_t* bar) {
+    const TileMeta tm = a.meta[t];
+    const TileLayout L(tm, tdep);
+    const uint32_t tbytes = 8u * (uint32_t)cf_round(tm.ns, 2);
+    mbar_expect_tx(bar, (uint32_t)L.bytes + tbytes);
+    const uint8_t* src = a.blob + a.blob_off[t];
+    for (int64_t o = 0; o < L.bytes; o += kBulkChunk) {
+        const uint32_t n = (uint32_t)(L.bytes - o < kBulkChunk ? L.bytes - o : kBulkChunk);
+        bulk_g2s(dst + o, src + o, n, bar);
+    }
+    if (tbytes) bulk_g2s(sTdst, a.Tslot + a.slot_off[t], tbytes, bar);
+}
+
+// Each CTA walks tiles blockIdx.x, +gridDim.x, ...; with stages == 2 it is a
+// persistent two-stage TMA pipeline (the blob of tile k+1 streams in while
+// tile k is computed), with stages == 1 the grid covers the tiles one-to-one.
+template <bool DET, bool TDEP, bool DIR, bool CLAMP, int kTileThreads>
+__global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
+    constexpr bool FUSE = !TDEP;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t bar[2];
+    __shared__ DevMaterial sMat[kMaxRegions];
     const int tid = threadIdx.x;
-    const int e0 = a.tile_elem_off[t];
-    const int ne = a.tile_elem_off[t + 1] - e0;
-    const int s0 = a.tile_slot_off[t];
-    const int ns = a.tile_slot_off[t + 1] - s0;
-    const int f0 = a.tile_facet_off[t];
-    const int nf = a.tile_facet_off[t + 1] - f0;
-    const int64_t c0 = a.tile_csr_off[t];
     const DevParams* __restrict__ P = a.P;
+    uint8_t* const buf0 = smem;
+    uint8_t* const buf1 = smem + (a.stages - 1) * a.blob_smem;
+    double* const sT0 = (double*)(smem + a.stages * (size_t)a.blob_smem);
+    double* const sT1 = sT0 + (a.stages - 1) * a.max_slots;
+    double* sH = sT0 + a.stages * a.max_slots;
 
-    double* sT = smem;
-    double* sH = sT + a.max_slots;
-    double* sl = sH + a.max_slots;          // lump per element
-    double* sr = sl + a.max_elems;          // rc[4][max_elems]
-    double* sf = sr + 4 * a.max_elems;      // facet terms [3*nf]
-
-    // phase 1: gather T, derive H per slot (H is always enthalpy(T): blocked.hpp:427,529)
-    for (int s = tid; s < ns; s += blockDim.x) {
-        const int32_t node = a.slot_node[s0 + s];
-        const double T = a.T[node];
-        const int reg = a.slot_info[s0 + s] & 0x7f;
-        sT[s] = T;
-        sH[s] = dev_enthalpy<TDEP>(P, P->mat[reg], T);
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
     }
-    __syncthreads();
-
-    // phase 2a: elements
-    double local_min = __longlong_as_double(0x7ff0000000000000ll);
-    for (int i = tid; i < ne; i += blockDim.x) {
-        const int64_t p = (int64_t)e0 + i;
-        const ushort4 cn = a.conn[p];
-        const int reg = a.ereg[p];
-        double g[4][3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            g[1][k] = a.geom[(int64_t)k * a.E + p];
-            g[2][k] = a.geom[(int64_t)(3 + k) * a.E + p];
-            g[3][k] = a.geom[(int64_t)(6 + k) * a.E + p];
-        }
-        const double vol = a.geom[9 * a.E + p];
-        const double max_edge = a.geom[10 * a.E + p];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) g[0][k] = ((g[1][k] + g[2][k]) + g[3][k]) * -1.0;
-        const double T[4] = {sT[cn.x], sT[cn.y], sT[cn.z], sT[cn.w]};
-        const double H[4] = {sH[cn.x], sH[cn.y], sH[cn.z], sH[cn.w]};
-        const DevMaterial& m = P->mat[reg];
-        double lump, rc[4];
-        dev_element<TDEP>(P, m, g, vol, max_edge, T, H, lump, rc);
-        sl[i] = lump;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) sr[k * a.max_elems + i] = rc[k];
-        if (TDEP) local_min = fmin(local_min, dev_stable_bound<TDEP>(P, m, a.min_edge[p], T));
+    for (int i = tid; i < P->n_materials; i += kTileThreads) sMat[i] = P->mat[i];
+    __syncthreads();  // barriers initialised, material table staged
+    // the copies are issued after the barrier: no warp waits on thread 0's global loads
+    if (tid == 0) {
+        if (blockIdx.x < a.n_tiles) issue_tile_copy(a, blockIdx.x, TDEP, buf0, sT0, &bar[0]);
+        if (a.stages == 2 && blockIdx.x + gridDim.x < a.n_tiles)
+            issue_tile_copy(a, blockIdx.x + gridDim.x, TDEP, buf1, sT1, &bar[1]);
     }
-    // phase 2b: facets (facet_flux_accumulate fem.hpp:74-79; interface blocked.hpp:485-490)
+    double dt = 0, t_next = 0;
+    bool done = false;
+    if (FUSE) step_dt<TDEP>(P, a.st, a.t_end, dt, t_next, done);
     const double time = a.st->time;
-    for (int i = tid; i < nf; i += blockDim.x) {
-        const ushort4 fs = a.fslots[f0 + i];
-        const DevFacetKind& K = P->kind[fs.w];
-        const double ts[3] = {sT[fs.x], sT[fs.y], sT[fs.z]};
-        double q, h, tinf;
-        if (K.interface) {
-            const double var = K.var == CF_VAR_TIME ? time : (ts[0] + ts[1] + ts[2]) / 3.0;
-            q = 0.0;
-            h = dev_pl_eval(P, K.htab, var);
-            const int4 sn = a.fsister[f0 + i];
-            // interface_ambient / refresh_ambient from the PRE-update T of the previous step
-            double sum = 0;
-            sum += a.Told[sn.x];
-            sum += a.Told[sn.y];
-            sum += a.Told[sn.z];
-            sum += a.Told[sn.w];
-            tinf = 0.25 * sum;
-        } else {
-            q = K.q;
-            h = K.h;
-            tinf = K.t_inf;
-        }
-        const double third = a.farea[f0 + i] / 3.0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) sf[3 * i + k] = third * (-q + h * (tinf - ts[k]));
-    }
-    if (TDEP) {
-        // block min then one atomic per CTA
-        for (int o = 16; o > 0; o >>= 1) local_min = fmin(local_min, __shfl_xor_sync(0xffffffffu, local_min, o));
-        if ((tid & 31) == 0) atomic_min_pos(&a.st->min_bound[a.st->step_index & 1], local_min);
-    }
-    __syncthreads();
+    int clamped = 0;
+    double local_min = __longlong_as_double(0x7ff0000000000000ll);
 
-    // phase 3: per-slot fixed-order reduction (ascending element, then facets)
-    const int e4 = 4 * ne;
-    for (int s = tid; s < ns; s += blockDim.x) {
-        const int beg = s == 0 ? 0 : a.slot_csr_end[s0 + s - 1];
-        const int end = a.slot_csr_end[s0 + s];
-        double c = 0, r = 0;
-        for (int j = beg; j < end; ++j) {
-            const int code = a.csr[c0 + j];
-            if (code < e4) {
-                const int e = code >> 2;
-                c += sl[e];
-                r -= sr[(code & 3) * a.max_elems + e];
-            } else {
-                r += sf[code - e4];
-            }
+    int k = 0;
+    for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x, ++k) {
+        const int stage = a.stages == 2 ? (k & 1) : 0;
+        uint8_t* B = stage ? buf1 : buf0;
+        double* sT = stage ? sT1 : sT0;
+        const TileMeta tm = a.meta[t];
+        const TileLayout L(tm, TDEP);
+        const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
+        const int s0 = a.slot_off[t];
+        mbar_wait(&bar[stage], a.stages == 2 ? ((k >> 1) & 1) : (k & 1));
+        if (a.probe == 1) {  // diagnostics: memory-path timing without the physics
+            __syncthreads();
+            if (tid == 0 && t + a.stages * (int)gridDim.x < a.n_tiles)
+                issue_tile_copy(a, t + a.stages * gridDim.x, TDEP, B, sT, &bar[stage]);
+            continue;
         }
-        if (DET) {
-            a.part_c[s0 + s] = c;
-            a.part_r[s0 + s] = r;
-        } else {
-            const int32_t node = a.slot_node[s0 + s];
-            if (a.slot_info[s0 + s] & 0x80) {
-                a.acc_c[node] = c;
-                a.acc_r[node] = r;
+        // phase 1: H = enthalpy(T) per slot (blocked.hpp:462-467) from the streamed slot temperatures
+        const uint8_t* sinfo = B + L.sinfo;
+        for (int s = tid; s < ns; s += kTileThreads) sH[s] = dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], sT[s]);
+        __syncthreads();
+
+        // phase 2a: elements (element_accumulate fem.hpp:57-70); contributions overwrite
+        // this element's consumed geometry columns: lump -> col 0, rc[k] -> col 1+k
+        double* G = (double*)(B + L.geom);
+        const int S = L.ne2;
+        const ushort4* conn = (const ushort4*)(B + L.conn);
+        const uint8_t* ereg = B + L.region;
+        for (int i = tid; i < ne; i += kTileThreads) {
+            double g[4][3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                g[1][c] = G[c * S + i];
+                g[2][c] = G[(3 + c) * S + i];
+                g[3][c] = G[(6 + c) * S + i];
+            }
+            const double vol = G[9 * S + i];
+            const double max_edge = G[10 * S + i];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) g[0][c] = ((g[1][c] + g[2][c]) + g[3][c]) * -1.0;
+            const ushort4 cn = conn[i];
+            const double T[4] = {sT[cn.x], sT[cn.y], sT[cn.z], sT[cn.w]};
+            const double H[4] = {sH[cn.x], sH[cn.y], sH[cn.z], sH[cn.w]};
+            const DevMaterial& m = sMat[ereg[i]];
+            double lump, rc[4];
+            dev_element<TDEP>(P, m, g, vol, max_edge, T, H, lump, rc);
+            if (TDEP)
+                local_min = fmin(local_min, dev_stable_bound<TDEP>(P, m, ((const double*)(B + L.minedge))[i], T));
+            G[i] = lump;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) G[(1 + c) * S + i] = rc[c];
+        }
+        // phase 2b: facets (facet_flux_accumulate fem.hpp:74-79; interface blocked.hpp:485-490);
+        // terms overwrite the facet's area (a=0) and sister (a=1,2) slots
+        double* farea = (double*)(B + L.farea);
+        double* fsis = (double*)(B + L.fsister);
+        const ushort4* fsl = (const ushort4*)(B + L.fslots);
+        for (int i = tid; i < nf; i += kTileThreads) {
+            const ushort4 fs = fsl[i];
+            const DevFacetKind& K = P->kind[fs.w];
+            const double ts[3] = {sT[fs.x], sT[fs.y], sT[fs.z]};
+            double q, h, tinf;
+            if (K.interface) {
+                const double var = K.var == CF_VAR_TIME ? time : (ts[0] + ts[1] + ts[2]) / 3.0;
+                q = 0.0;
+                h = dev_pl_eval(P, K.htab, var);
+                const int4 sn = ((const int4*)fsis)[i];
+                // interface_ambient from the PRE-update T of the previous step (refresh_ambient lag)
+                double sum = 0;
+                sum += a.Told[sn.x];
+                sum += a.Told[sn.y];
+                sum += a.Told[sn.z];
+                sum += a.Told[sn.w];
+                tinf = 0.25 * sum;
+            } else {
+                q = K.q;
+                h = K.h;
+                tinf = K.t_inf;
+            }
+            const double third = farea[i] / 3.0;
+            const double f0 = third * (-q + h * (tinf - ts[0]));
+            const double f1 = third * (-q + h * (tinf - ts[1]));
+            const double f2 = third * (-q + h * (tinf - ts[2]));
+            // stored negated: the reduction does r -= v for every entry (r - (-f) == r + f exactly)
+            farea[i] = -f0;
+            fsis[2 * i] = -f1;
+            fsis[2 * i + 1] = -f2;
+        }
+        __syncthreads();
+
+        // phase 3: per-slot fixed-order reduction (ascending element, then facets) + flush
+        const uint16_t* cend = (const uint16_t*)(B + L.csr_end);
+        const uint16_t* csr = (const uint16_t*)(B + L.csr);
+        const int32_t* snode = (const int32_t*)(B + L.snode);
+        const int e4 = 4 * ne;
+        // entry decode (branch-free): element e*4+k -> c += lump[e], r -= rc_k[e];
+        // facet 4*ne+4*f+a -> c += 0.0, r -= (-term). Indices are in doubles from B.
+        const double* Bd = (const double*)B;
+        const int gofs = (int)(L.geom >> 3), zofs = (int)(L.zero >> 3);
+        const int fa_ofs = (int)(L.farea >> 3), fs_ofs = (int)(L.fsister >> 3) - 1;
+        auto decode = [&](int code, int& li, int& ri) {
+            const bool fac = code >= e4;
+            const int q = code & 3;
+            const int e = code >> 2;
+            const int f = (code - e4) >> 2;
+            li = fac ? zofs : gofs + e;
+            ri = fac ? (q == 0 ? fa_ofs + f : fs_ofs + 2 * f + q) : gofs + (1 + q) * S + e;
+        };
+        for (int s = tid; s < ns; s += kTileThreads) {
+            const int beg = s == 0 ? 0 : cend[s - 1];
+            const int end = cend[s];
+            double c = 0, r = 0;
+            int j = beg;
+            for (; j + 4 <= end; j += 4) {
+                int li[4], ri[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) decode(csr[j + u], li[u], ri[u]);
+                double lv[4], rv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    lv[u] = Bd[li[u]];
+                    rv[u] = Bd[ri[u]];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    c += lv[u];
+                    r -= rv[u];
+                }
+            }
+            for (; j < end; ++j) {
+                int li, ri;
+                decode(csr[j], li, ri);
+                c += Bd[li];
+                r -= Bd[ri];
+            }
+            const int info = sinfo[s];
+            const int32_t node = snode[s];
+            if (FUSE && (info & 0x80)) {
+                // tile-private node: its merge is the identity, update it now
+                double Tn;
+                if (done) {
+                    Tn = sT[s];
+                } else {
+                    const int dir = (DIR && (info & 0x40)) ? a.node_dir[node] : -1;
+                    Tn = node_update<DIR, CLAMP>(P, a.st, sT[s], c, r, dt, t_next, dir, info & 0x3f,
+                                                 a.local_global + node, clamped);
+                }
+                a.Tn[node] = Tn;
+                a.Tslot_n[s0 + s] = Tn;
+            } else if (DET) {
+                a.part[s0 + s] = make_double2(c, r);
             } else {
                 atomicAdd(&a.acc_c[node], c);
                 atomicAdd(&a.acc_r[node], r);
             }
         }
+        if (t + (int)gridDim.x >= a.n_tiles) break;  // last tile of this CTA: no trailing barrier
+        __syncthreads();  // stage buffer and sT/sH free again
+        if (tid == 0 && t + a.stages * (int)gridDim.x < a.n_tiles) {
+            // generic-proxy writes to B (in-place contributions) must be ordered
+            // before the async-proxy (TMA) overwrite of the same buffer
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_tile_copy(a, t + a.stages * gridDim.x, TDEP, B, sT, &bar[stage]);
+        }
     }
+    if (TDEP) {
+        for (int o = 16; o > 0; o >>= 1) local_min = fmin(local_min, __shfl_xor_sync(0xffffffffu, local_min, o));
+        if ((tid & 31) == 0) atomic_min_pos(&a.st->min_bound[a.st->step_index & 1], local_min);
+    }
+    if (CLAMP && clamped) a.st->clamp_flag = 1;
 }
 
+// ------------------------------------------------------------------ update kernel
 struct UpdArgs {
-    int32_t n_local, n_ghost;
-    const double* T;   // current (ghost slots written here)
-    double* Tn;        // next
+    int32_t n_list, n_local, n_ghost;
+    const int32_t* list;  // nodes to merge + update (NULL: all local nodes)
+    const double* T;      // current (ghost slots written here)
+    double* Tn;           // next
     const int32_t* merge_off;
     const int32_t* merge_idx;
-    const double* part_c;
-    const double* part_r;
+    const double2* part;
     double* acc_c;
     double* acc_r;
     const int8_t* node_dir;
@@ -216,7 +386,8 @@ struct UpdArgs {
     const int32_t* shared_src_r;
     const double* recv;
     const int32_t* ghost_src;
-    double* Tcur_w;    // == T, writable (ghost slots)
+    double* Tcur_w;  // == T, writable (ghost slots)
+    double* Tslot_n; // next per-slot T copies (every slot of an updated node)
     const DevParams* P;
     DevState* st;
     double t_end;
@@ -228,9 +399,9 @@ __device__ __forceinline__ void own_partial(const UpdArgs& a, int i, double& c, 
         c = 0;
         r = 0;
         for (int j = a.merge_off[i]; j < a.merge_off[i + 1]; ++j) {
-            const int32_t s = a.merge_idx[j];
-            c += a.part_c[s];
-            r += a.part_r[s];
+            const double2 pr = a.part[a.merge_idx[j]];
+            c += pr.x;
+            r += pr.y;
         }
     } else {
         c = a.acc_c[i];
@@ -241,22 +412,17 @@ __device__ __forceinline__ void own_partial(const UpdArgs& a, int i, double& c, 
 template <bool DET, bool MULTI, bool DIR, bool CLAMP, bool TDEP>
 __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
     const DevParams* __restrict__ P = a.P;
-    const double time = a.st->time;
-    double dt = TDEP ? __longlong_as_double((long long)a.st->min_bound[a.st->step_index & 1]) * P->dt_safety
-                     : P->static_dt;
-    bool done = false;
-    if (a.t_end > 0) {
-        const double remaining = a.t_end - time;
-        if (!(time < a.t_end)) done = true;
-        if (remaining > 0) dt = dt < remaining ? dt : remaining;
-    }
-    const double t_next = time + dt;
+    double dt, t_next;
+    bool done;
+    step_dt<TDEP>(P, a.st, a.t_end, dt, t_next, done);
     int clamped = 0;
     const int stride = gridDim.x * blockDim.x;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_local; i += stride) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n_list; k += stride) {
+        const int i = a.list ? a.list[k] : k;
         const double T = a.T[i];
         if (done) {
             a.Tn[i] = T;
+            for (int j = a.merge_off[i]; j < a.merge_off[i + 1]; ++j) a.Tslot_n[a.merge_idx[j]] = T;
             continue;
         }
         double c, r;
@@ -267,8 +433,8 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         }
         if (MULTI) {
             const int32_t sh = a.node_shared[i];
+            double ct = 0, rt = 0;
             if (sh >= 0) {
-                double ct = 0, rt = 0;
                 for (int j = a.shared_off[sh]; j < a.shared_off[sh + 1]; ++j) {
                     const int32_t sc = a.shared_src_c[j];
                     if (sc < 0) {
@@ -279,35 +445,23 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
                         rt += a.recv[a.shared_src_r[j]];
                     }
                 }
-                c = ct;
-                r = rt;
             } else {
-                c = 0 + c;
-                r = 0 + r;
+                ct += c;
+                rt += r;
             }
+            c = ct;
+            r = rt;
         }
-        double Tn;
-        if (!(c > 0)) {
-            atomicMin(&a.st->err_node, a.local_global[i]);
-            Tn = T;
-        } else {
-            Tn = T + dt * r / c;
-        }
-        if (DIR) {
-            const int d = a.node_dir[i];
-            if (d >= 0) Tn = dev_pl_eval(P, P->dir_tab[d], t_next);
-        }
-        if (CLAMP) {
-            const DevMaterial& m = P->mat[a.node_region[i]];
-            if (Tn < m.range_lo || Tn > m.range_hi) clamped = 1;
-        }
+        const double Tn = node_update<DIR, CLAMP>(P, a.st, T, c, r, dt, t_next, DIR ? a.node_dir[i] : -1,
+                                                  CLAMP ? a.node_region[i] : 0, a.local_global + i, clamped);
         a.Tn[i] = Tn;
+        for (int j = a.merge_off[i]; j < a.merge_off[i + 1]; ++j) a.Tslot_n[a.merge_idx[j]] = Tn;
     }
     if (MULTI)
         for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < a.n_ghost; g += stride)
             a.Tcur_w[a.n_local + g] = a.recv[a.ghost_src[g]];
     if (CLAMP && clamped) a.st->clamp_flag = 1;
-    // last CTA advances the step state (all CTAs have read it by then)
+    // last CTA advances the step state (every CTA has read it by then)
     __shared__ bool last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -335,11 +489,12 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
     }
 }
 
+// ------------------------------------------------------------------ pack kernel
 struct PackArgs {
     int32_t n_cr, n_t;
     const int32_t* cr_node;  // local ids
-    const int64_t* cr_dst;   // c offset; r at cr_dst_r
-    const int64_t* cr_dst_r;
+    const int64_t* cr_dst;   // c offset
+    const int64_t* cr_dst_r; // r offset
     const int32_t* t_node;
     const int64_t* t_dst;
     const double* T;

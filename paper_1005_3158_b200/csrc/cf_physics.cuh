@@ -70,6 +70,13 @@ __device__ __forceinline__ double dev_enthalpy(const DevParams* __restrict__ P, 
 // One element: lumped capacitance share `lump` (added to each of the 4
 // nodes) and the 4 conduction residual terms rc[a] (subtracted).
 // g1..g3 are the stored gradients; g0 = (g1+g2+g3)*-1.0 (geometry.hpp:75).
+// Bitwise equal to the reference's apparent_heat_capacity + element_accumulate:
+//  - T[hi]-T[lo] equals fmax(..)-fmin(..) exactly (same extreme values); the
+//    lo/hi indices are only needed by the rare secant branch;
+//  - the degeneracy test gt2 < 1e-14*scale*scale (scale = range/max_edge) is
+//    decided without the division whenever gt2*max_edge^2 clears 1e-14*range^2
+//    by a 1e-6 relative margin (far above the ~1e-15 rounding of either form);
+//    otherwise the reference expression is evaluated verbatim.
 template <bool TDEP>
 __device__ __forceinline__ void dev_element(const DevParams* __restrict__ P, const DevMaterial& m,
                                             const double (&g)[4][3], double vol, double max_edge,
@@ -84,15 +91,11 @@ __device__ __forceinline__ void dev_element(const DevParams* __restrict__ P, con
         gtz = gtz + g[a][2] * T[a];
     }
     const double t_bar = 0.25 * (((T[0] + T[1]) + T[2]) + T[3]);
-    // apparent_heat_capacity fem.hpp:26-45
-    int lo = 0, hi = 0;
-#pragma unroll
-    for (int a = 1; a < 4; ++a) {
-        if (T[a] < (lo == 0 ? T[0] : lo == 1 ? T[1] : lo == 2 ? T[2] : T[3])) lo = a;
-        if (T[a] > (hi == 0 ? T[0] : hi == 1 ? T[1] : hi == 2 ? T[2] : T[3])) hi = a;
-    }
-    const double Tlo = lo == 0 ? T[0] : lo == 1 ? T[1] : lo == 2 ? T[2] : T[3];
-    const double Thi = hi == 0 ? T[0] : hi == 1 ? T[1] : hi == 2 ? T[2] : T[3];
+    // compare-selects (finite T): same extreme values as the reference's index scan
+    const double l01 = T[1] < T[0] ? T[1] : T[0], l23 = T[3] < T[2] ? T[3] : T[2];
+    const double h01 = T[1] > T[0] ? T[1] : T[0], h23 = T[3] > T[2] ? T[3] : T[2];
+    const double Tlo = l23 < l01 ? l23 : l01;
+    const double Thi = h23 > h01 ? h23 : h01;
     const double range = Thi - Tlo;
     double capp;
     if (range <= 0) {
@@ -106,11 +109,23 @@ __device__ __forceinline__ void dev_element(const DevParams* __restrict__ P, con
             ghz = ghz + g[a][2] * H[a];
         }
         const double gt2 = gtx * gtx + gty * gty + gtz * gtz;
-        const double scale = range / max_edge;
-        if (gt2 < 1e-14 * scale * scale) {
-            const double Hlo = lo == 0 ? H[0] : lo == 1 ? H[1] : lo == 2 ? H[2] : H[3];
-            const double Hhi = hi == 0 ? H[0] : hi == 1 ? H[1] : hi == 2 ? H[2] : H[3];
-            capp = (Hhi - Hlo) / range;
+        bool degenerate;
+        const double lhs = gt2 * (max_edge * max_edge), rhs = 1e-14 * (range * range);
+        if (lhs > rhs * 1.000001) {
+            degenerate = false;
+        } else {
+            const double scale = range / max_edge;
+            degenerate = gt2 < 1e-14 * scale * scale;
+        }
+        if (degenerate) {
+            // secant (H_hi - H_lo)/range with the reference's first-index tie rule
+            double tl = T[0], th = T[0], hl = H[0], hh = H[0];
+#pragma unroll
+            for (int a = 1; a < 4; ++a) {
+                if (T[a] < tl) { tl = T[a]; hl = H[a]; }
+                if (T[a] > th) { th = T[a]; hh = H[a]; }
+            }
+            capp = (hh - hl) / range;
         } else {
             capp = sqrt((ghx * ghx + ghy * ghy + ghz * ghz) / gt2);
         }

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <array>
 #include <map>
 #include <numeric>
 
@@ -293,10 +294,8 @@ void build_rank_plan(const MeshData& m, const std::vector<Geom>& geom, const Set
     std::vector<int64_t> np_off;
     std::vector<int32_t> np_parts;
     if (W > 1) {
-        std::vector<std::vector<int32_t>> tmp;  // small per node; build compactly
         np_off.assign(m.N + 1, 0);
         std::vector<int32_t> cnt(m.N, 0);
-        // upper bound count then dedupe
         std::vector<int64_t> off(m.N + 1, 0);
         for (int64_t i = 0; i < 4 * (int64_t)m.E; ++i) off[m.tets[i] + 1]++;
         for (int32_t n = 0; n < m.N; ++n) off[n + 1] += off[n];
@@ -321,52 +320,7 @@ void build_rank_plan(const MeshData& m, const std::vector<Geom>& geom, const Set
         return false;
     };
 
-    // local nodes ordered by label (RCM or given)
-    std::vector<int32_t> local_of(m.N, -1);
-    std::vector<int32_t> lnodes;
-    {
-        std::vector<char> mark(m.N, 0);
-        for (int32_t e : elems)
-            for (int a = 0; a < 4; ++a) mark[m.tets[4 * (size_t)e + a]] = 1;
-        for (int32_t n = 0; n < m.N; ++n)
-            if (mark[n]) lnodes.push_back(n);
-        std::sort(lnodes.begin(), lnodes.end(), [&](int32_t a, int32_t b) { return node_label[a] < node_label[b]; });
-        for (size_t i = 0; i < lnodes.size(); ++i) local_of[lnodes[i]] = (int32_t)i;
-    }
-    rp.n_local = (int32_t)lnodes.size();
-
-    // facets per element (ascending facet id), Dirichlet facets excluded from bindings
-    std::vector<int32_t> in_rank(m.E, 0);
-    for (int32_t e : elems) in_rank[e] = 1;
-    std::vector<int32_t> fe_off(m.E + 1, 0), fe;
-    for (int32_t f = 0; f < m.F; ++f)
-        if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe_off[m.owner[f] + 1]++;
-    for (int32_t e = 0; e < m.E; ++e) fe_off[e + 1] += fe_off[e];
-    fe.resize(fe_off[m.E]);
-    {
-        std::vector<int32_t> cur(fe_off.begin(), fe_off.end() - 1);
-        for (int32_t f = 0; f < m.F; ++f)
-            if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe[cur[m.owner[f]]++] = f;
-    }
-
-    // ghosts: sister nodes of this rank's interface facets that are not local
-    std::vector<int32_t> ghosts;
-    for (int32_t f = 0; f < m.F; ++f) {
-        if (!in_rank[m.owner[f]] || S.facet_kind[f] < 0 || !S.P.kind[S.facet_kind[f]].interface) continue;
-        const int32_t sis = S.pairs[S.pair_of_facet[f]].sister;
-        for (int a = 0; a < 4; ++a) {
-            const int32_t n = m.tets[4 * (size_t)sis + a];
-            if (local_of[n] < 0) ghosts.push_back(n);
-        }
-    }
-    std::sort(ghosts.begin(), ghosts.end());
-    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
-    rp.n_ghost = (int32_t)ghosts.size();
-    for (size_t g = 0; g < ghosts.size(); ++g) local_of[ghosts[g]] = rp.n_local + (int32_t)g;
-    rp.local_global = lnodes;
-    rp.local_global.insert(rp.local_global.end(), ghosts.begin(), ghosts.end());
-
-    // tiles: element order key, contiguous chunks, ascending id within a tile
+    // ---- tiles: element order key, contiguous chunks, ascending id within a tile
     std::vector<std::vector<int32_t>> tiles;
     if (o.tile_of_element) {
         std::map<int32_t, std::vector<int32_t>> by;
@@ -420,7 +374,65 @@ void build_rank_plan(const MeshData& m, const std::vector<Geom>& geom, const Set
         if ((int)t.size() > kMaxTileElems)
             raise(CF_INVALID_ARG, "a tile holds more than 2048 elements (" + std::to_string(t.size()) + ")");
 
-    // node -> number of tiles touching it (private test)
+    // ---- local node numbering: given / RCM label / first touch in tile order
+    std::vector<int32_t> local_of(m.N, -1);
+    std::vector<int32_t> lnodes;
+    if (o.node_order == CF_NODE_ORDER_TILE) {
+        for (const auto& te : tiles)
+            for (int32_t e : te)
+                for (int a = 0; a < 4; ++a) {
+                    const int32_t n = m.tets[4 * (size_t)e + a];
+                    if (local_of[n] < 0) {
+                        local_of[n] = (int32_t)lnodes.size();
+                        lnodes.push_back(n);
+                    }
+                }
+    } else {
+        std::vector<char> mark(m.N, 0);
+        for (int32_t e : elems)
+            for (int a = 0; a < 4; ++a) mark[m.tets[4 * (size_t)e + a]] = 1;
+        for (int32_t n = 0; n < m.N; ++n)
+            if (mark[n]) lnodes.push_back(n);
+        if (o.node_order == CF_NODE_ORDER_RCM)
+            std::sort(lnodes.begin(), lnodes.end(),
+                      [&](int32_t a, int32_t b) { return node_label[a] < node_label[b]; });
+        for (size_t i = 0; i < lnodes.size(); ++i) local_of[lnodes[i]] = (int32_t)i;
+    }
+    rp.n_local = (int32_t)lnodes.size();
+    if (rp.n_local >= (1 << 28)) raise(CF_INVALID_ARG, "more than 2^28 nodes on one rank");
+
+    // facets per element (ascending facet id), Dirichlet facets excluded from bindings
+    std::vector<char> in_rank(m.E, 0);
+    for (int32_t e : elems) in_rank[e] = 1;
+    std::vector<int32_t> fe_off(m.E + 1, 0), fe;
+    for (int32_t f = 0; f < m.F; ++f)
+        if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe_off[m.owner[f] + 1]++;
+    for (int32_t e = 0; e < m.E; ++e) fe_off[e + 1] += fe_off[e];
+    fe.resize(fe_off[m.E]);
+    {
+        std::vector<int32_t> cur(fe_off.begin(), fe_off.end() - 1);
+        for (int32_t f = 0; f < m.F; ++f)
+            if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe[cur[m.owner[f]]++] = f;
+    }
+
+    // ghosts: sister nodes of this rank's interface facets that are not local
+    std::vector<int32_t> ghosts;
+    for (int32_t f = 0; f < m.F; ++f) {
+        if (!in_rank[m.owner[f]] || S.facet_kind[f] < 0 || !S.P.kind[S.facet_kind[f]].interface) continue;
+        const int32_t sis = S.pairs[S.pair_of_facet[f]].sister;
+        for (int a = 0; a < 4; ++a) {
+            const int32_t n = m.tets[4 * (size_t)sis + a];
+            if (local_of[n] < 0) ghosts.push_back(n);
+        }
+    }
+    std::sort(ghosts.begin(), ghosts.end());
+    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+    rp.n_ghost = (int32_t)ghosts.size();
+    for (size_t g = 0; g < ghosts.size(); ++g) local_of[ghosts[g]] = rp.n_local + (int32_t)g;
+    rp.local_global = lnodes;
+    rp.local_global.insert(rp.local_global.end(), ghosts.begin(), ghosts.end());
+
+    // node -> number of tiles touching it (tile-private test)
     std::vector<int32_t> ntiles_of(rp.n_local, 0);
     {
         std::vector<int32_t> last(rp.n_local, -1);
@@ -451,20 +463,16 @@ void build_rank_plan(const MeshData& m, const std::vector<Geom>& geom, const Set
         for (int32_t l = 0; l < rp.n_local; ++l) rp.node_dir[l] = (int8_t)S.dir_of_node[lnodes[l]];
     }
 
-    // per tile arrays
-    rp.tile_elem_off.assign(rp.n_tiles + 1, 0);
+    // ---- per tile: slots, CSR, facet bindings, packed into the blob
+    rp.tile_meta.resize(rp.n_tiles);
     rp.tile_slot_off.assign(rp.n_tiles + 1, 0);
-    rp.tile_csr_off.assign(rp.n_tiles + 1, 0);
-    rp.tile_facet_off.assign(rp.n_tiles + 1, 0);
+    rp.blob_off.assign(rp.n_tiles + 1, 0);
     rp.elem_global.resize(Er);
-    rp.elem_conn.resize(4 * Er);
-    rp.elem_region.resize(Er);
-    rp.elem_geom.resize(11 * Er);
-    if (S.temp_dep) rp.elem_min_edge.resize(Er);
     std::vector<int32_t> slot_of(rp.n_local, -1);
     int64_t epos = 0;
     std::vector<int32_t> tnodes;
     std::vector<std::vector<uint16_t>> slot_entries;
+    std::vector<int32_t> tfacets;
     for (int32_t t = 0; t < rp.n_tiles; ++t) {
         const auto& te = tiles[t];
         const int ne = (int)te.size();
@@ -477,90 +485,128 @@ void build_rank_plan(const MeshData& m, const std::vector<Geom>& geom, const Set
                     tnodes.push_back(l);
                 }
             }
-        std::sort(tnodes.begin(), tnodes.end());
+        // slots ordered by contribution count (desc), then local id: the warps of
+        // the reduction phase then walk lists of near-equal length (no divergence)
+        {
+            std::vector<int32_t> cnt_of(tnodes.size(), 0);
+            for (size_t s = 0; s < tnodes.size(); ++s) slot_of[tnodes[s]] = (int32_t)s;
+            for (int32_t e : te)
+                for (int a = 0; a < 4; ++a) cnt_of[slot_of[local_of[m.tets[4 * (size_t)e + a]]]]++;
+            for (int32_t e : te)
+                for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j)
+                    for (int a = 0; a < 3; ++a) cnt_of[slot_of[local_of[m.facets[3 * (size_t)fe[j] + a]]]]++;
+            std::vector<int32_t> idx(tnodes.size());
+            std::iota(idx.begin(), idx.end(), 0);
+            std::sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) {
+                return cnt_of[x] != cnt_of[y] ? cnt_of[x] > cnt_of[y] : tnodes[x] < tnodes[y];
+            });
+            std::vector<int32_t> sorted(tnodes.size());
+            for (size_t s = 0; s < idx.size(); ++s) sorted[s] = tnodes[idx[s]];
+            tnodes.swap(sorted);
+        }
         for (size_t s = 0; s < tnodes.size(); ++s) slot_of[tnodes[s]] = (int32_t)s;
         const int ns = (int)tnodes.size();
         slot_entries.assign(ns, {});
-        rp.tile_elem_off[t + 1] = rp.tile_elem_off[t] + ne;
-        rp.max_elems = std::max(rp.max_elems, ne);
-        rp.max_slots = std::max(rp.max_slots, ns);
-        int nf = 0;
+        // facet bindings, element order then facet id (blocked.hpp:244-288)
+        tfacets.clear();
+        for (int32_t e : te)
+            for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j) tfacets.push_back(fe[j]);
+        const int nf = (int)tfacets.size();
+        for (int i = 0; i < ne; ++i)
+            for (int a = 0; a < 4; ++a)
+                slot_entries[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]]].push_back((uint16_t)(4 * i + a));
+        for (int i = 0; i < nf; ++i)
+            for (int a = 0; a < 3; ++a)
+                slot_entries[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]]].push_back(
+                    (uint16_t)(4 * ne + 4 * i + a));
+        int ncsr = 0;
+        for (int s = 0; s < ns; ++s) ncsr += (int)slot_entries[s].size();
+        if (4 * ne + 4 * nf > 65535) raise(CF_INVALID_ARG, "tile csr exceeds 16-bit codes");
+        TileMeta tm{ne, ns, nf, ncsr};
+        rp.tile_meta[t] = tm;
+        const TileLayout L(tm, S.temp_dep);
+        const int64_t base = rp.blob_off[t];
+        rp.blob_off[t + 1] = base + L.bytes;
+        rp.blob.resize(rp.blob_off[t + 1], 0);
+        uint8_t* B = rp.blob.data() + base;
+        double* gsec = (double*)(B + L.geom);
+        uint16_t* csec = (uint16_t*)(B + L.conn);
         for (int i = 0; i < ne; ++i) {
             const int32_t e = te[i];
-            const int64_t p = epos + i;
-            rp.elem_global[p] = e;
-            rp.elem_region[p] = (uint8_t)m.region[e];
+            rp.elem_global[epos + i] = e;
             const Geom& g = geom[e];
             const double vals[11] = {g.g[1][0], g.g[1][1], g.g[1][2], g.g[2][0], g.g[2][1], g.g[2][2],
                                      g.g[3][0], g.g[3][1], g.g[3][2], g.vol,     g.max_edge};
-            for (int k = 0; k < 11; ++k) rp.elem_geom[(size_t)k * Er + p] = vals[k];
-            if (S.temp_dep) rp.elem_min_edge[p] = g.min_edge;
-            for (int a = 0; a < 4; ++a) {
-                const int32_t s = slot_of[local_of[m.tets[4 * (size_t)e + a]]];
-                rp.elem_conn[4 * p + a] = (uint16_t)s;
-                slot_entries[s].push_back((uint16_t)(4 * i + a));
+            for (int k = 0; k < 11; ++k) gsec[(size_t)k * L.ne2 + i] = vals[k];
+            if (S.temp_dep) ((double*)(B + L.minedge))[i] = g.min_edge;
+            for (int a = 0; a < 4; ++a) csec[4 * i + a] = (uint16_t)slot_of[local_of[m.tets[4 * (size_t)e + a]]];
+            B[L.region + i] = (uint8_t)m.region[e];
+        }
+        for (int i = 0; i < nf; ++i) {
+            const int32_t f = tfacets[i];
+            const int32_t kind = S.facet_kind[f];
+            uint16_t* fs = (uint16_t*)(B + L.fslots) + 4 * i;
+            for (int a = 0; a < 3; ++a) fs[a] = (uint16_t)slot_of[local_of[m.facets[3 * (size_t)f + a]]];
+            fs[3] = (uint16_t)kind;
+            ((double*)(B + L.farea))[i] = triangle_area(m.pos(m.facets[3 * (size_t)f]),
+                                                        m.pos(m.facets[3 * (size_t)f + 1]),
+                                                        m.pos(m.facets[3 * (size_t)f + 2]));
+            int32_t* sis = (int32_t*)(B + L.fsister) + 4 * i;
+            if (S.P.kind[kind].interface) {
+                const int32_t se = S.pairs[S.pair_of_facet[f]].sister;
+                for (int a = 0; a < 4; ++a) sis[a] = local_of[m.tets[4 * (size_t)se + a]];
+                rp.n_if_facets++;
+            } else {
+                rp.n_bc_facets++;
             }
         }
-        // facet bindings, element order then facet id (blocked.hpp:244-288)
-        for (int i = 0; i < ne; ++i) {
-            const int32_t e = te[i];
-            for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j) {
-                const int32_t f = fe[j];
-                const int32_t kind = S.facet_kind[f];
-                uint16_t sl[3];
-                for (int a = 0; a < 3; ++a) sl[a] = (uint16_t)slot_of[local_of[m.facets[3 * (size_t)f + a]]];
-                for (int a = 0; a < 3; ++a) rp.facet_slots.push_back(sl[a]);
-                rp.facet_slots.push_back((uint16_t)kind);
-                rp.facet_area.push_back(
-                    triangle_area(m.pos(m.facets[3 * (size_t)f]), m.pos(m.facets[3 * (size_t)f + 1]),
-                                  m.pos(m.facets[3 * (size_t)f + 2])));
-                if (S.P.kind[kind].interface) {
-                    const int32_t sis = S.pairs[S.pair_of_facet[f]].sister;
-                    for (int a = 0; a < 4; ++a) rp.facet_sister.push_back(local_of[m.tets[4 * (size_t)sis + a]]);
-                    rp.n_if_facets++;
-                } else {
-                    for (int a = 0; a < 4; ++a) rp.facet_sister.push_back(0);
-                    rp.n_bc_facets++;
-                }
-                for (int a = 0; a < 3; ++a) slot_entries[sl[a]].push_back((uint16_t)(4 * ne + 3 * nf + a));
-                ++nf;
+        uint16_t* cend = (uint16_t*)(B + L.csr_end);
+        uint16_t* csr = (uint16_t*)(B + L.csr);
+        int rel = 0;
+        for (int s = 0; s < (int)cf_round(ns, 2); ++s) {
+            if (s >= ns) {  // padding slot (never a merge target)
+                rp.slot_node.push_back(-1);
+                continue;
             }
-        }
-        rp.tile_facet_off[t + 1] = rp.tile_facet_off[t] + nf;
-        rp.max_facets = std::max(rp.max_facets, nf);
-        if (4 * ne + 3 * nf > 65535) raise(CF_INVALID_ARG, "tile csr exceeds 16-bit codes");
-        // slots: node ids, info, csr
-        int64_t csr_base = rp.tile_csr_off[t];
-        uint32_t rel = 0;
-        for (int s = 0; s < ns; ++s) {
             const int32_t l = tnodes[s];
-            rp.slot_node.push_back(l);
+            rp.slot_node.push_back((int32_t)(((uint32_t)rp.node_region[l] << 28) | (uint32_t)l));
             const bool priv = ntiles_of[l] == 1 && !shared_node[l];
-            rp.slot_info.push_back((uint8_t)((rp.node_region[l] & 0x7f) | (priv ? 0x80 : 0)));
-            for (uint16_t c : slot_entries[s]) rp.csr.push_back(c);
-            rel += (uint32_t)slot_entries[s].size();
-            rp.slot_csr_end.push_back((uint16_t)rel);
+            const bool dir = !rp.node_dir.empty() && rp.node_dir[l] >= 0;
+            B[L.sinfo + s] = (uint8_t)((rp.node_region[l] & 0x3f) | (dir ? 0x40 : 0) | (priv ? 0x80 : 0));
+            for (uint16_t c : slot_entries[s]) csr[rel++] = c;
+            cend[s] = (uint16_t)rel;
         }
-        rp.tile_csr_off[t + 1] = csr_base + rel;
-        rp.tile_slot_off[t + 1] = rp.tile_slot_off[t] + ns;
+        rp.tile_slot_off[t + 1] = rp.tile_slot_off[t] + (int32_t)cf_round(ns, 2);  // 16 B aligned Tslot segments
+        int32_t* sn = (int32_t*)(B + L.snode);
+        for (int s2 = 0; s2 < ns; ++s2) sn[s2] = tnodes[s2];
+        rp.max_elems = std::max(rp.max_elems, ne);
+        rp.max_slots = std::max(rp.max_slots, (int32_t)cf_round(ns, 2));
+        rp.max_facets = std::max(rp.max_facets, nf);
+        rp.max_blob = std::max(rp.max_blob, L.bytes);
         for (int s = 0; s < ns; ++s) slot_of[tnodes[s]] = -1;
         epos += ne;
     }
     // merge lists: ascending tile per node (merge_offsets/merge_entries blocked.hpp:294-307)
     const int64_t S_tot = rp.tile_slot_off[rp.n_tiles];
     rp.merge_off.assign(rp.n_local + 1, 0);
-    for (int64_t s = 0; s < S_tot; ++s) rp.merge_off[rp.slot_node[s] + 1]++;
+    auto snode = [&](int64_t s) { return (int32_t)((uint32_t)rp.slot_node[s] & 0x0fffffffu); };
+    for (int64_t s = 0; s < S_tot; ++s)
+        if (rp.slot_node[s] >= 0) rp.merge_off[snode(s) + 1]++;
     for (int32_t l = 0; l < rp.n_local; ++l) rp.merge_off[l + 1] += rp.merge_off[l];
     rp.merge_idx.resize(S_tot);
     {
         std::vector<int32_t> cur(rp.merge_off.begin(), rp.merge_off.end() - 1);
-        for (int64_t s = 0; s < S_tot; ++s) rp.merge_idx[cur[rp.slot_node[s]]++] = (int32_t)s;
+        for (int64_t s = 0; s < S_tot; ++s)
+            if (rp.slot_node[s] >= 0) rp.merge_idx[cur[snode(s)]++] = (int32_t)s;
+    }
+    for (int32_t l = 0; l < rp.n_local; ++l) {
+        if (ntiles_of[l] == 1 && !shared_node[l]) rp.n_private++;
+        else rp.shared_list.push_back(l);
     }
 
     // ---------------------------------------------------- multi-rank exchange
     if (W > 1) {
-        // interface facets of a part and their sister parts -> external node needs
-        // need[p][q] = nodes part p needs from part q (external_from partition.hpp:346-354)
+        // need(p, q) = nodes part p needs from part q (external_from partition.hpp:346-354)
         auto ext_need = [&](int32_t p, int32_t q) {
             std::vector<int32_t> v;
             for (int32_t f = 0; f < m.F; ++f) {
@@ -577,8 +623,7 @@ void build_rank_plan(const MeshData& m, const std::vector<Geom>& geom, const Set
             return v;
         };
         std::map<int32_t, RankPlan::Neighbor> nb;
-        // shared nodes, ascending global id
-        std::vector<int32_t> shared;
+        std::vector<int32_t> shared;  // ascending global id
         for (int32_t l = 0; l < rp.n_local; ++l)
             if (shared_node[l]) shared.push_back(lnodes[l]);
         std::sort(shared.begin(), shared.end());
@@ -611,19 +656,24 @@ void build_rank_plan(const MeshData& m, const std::vector<Geom>& geom, const Set
         }
         rp.send_len = rp.send_off.back();
         rp.recv_len = rp.recv_off.back();
-        // combine lists per shared node: ascending rank, own = -1 (c index; r = c + ns_q)
-        std::vector<std::vector<std::pair<int32_t, int32_t>>> src(shared.size());
-        for (size_t i = 0; i < shared.size(); ++i) src[i].push_back({rank, -1});
+        // combine lists per shared node: ascending rank, own = -1
+        std::vector<std::vector<std::array<int32_t, 3>>> src(shared.size());
+        for (size_t i = 0; i < shared.size(); ++i) src[i].push_back({rank, -1, -1});
         for (size_t k = 0; k < rp.nbrs.size(); ++k) {
             const auto& x = rp.nbrs[k];
-            for (size_t j = 0; j < x.shared.size(); ++j)
-                src[rp.node_shared[x.shared[j]]].push_back({x.rank, (int32_t)(rp.recv_off[k] + (int64_t)j)});
+            const int32_t ns = (int32_t)x.shared.size();
+            for (int32_t j = 0; j < ns; ++j)
+                src[rp.node_shared[x.shared[j]]].push_back(
+                    {x.rank, (int32_t)(rp.recv_off[k] + j), (int32_t)(rp.recv_off[k] + ns + j)});
         }
         rp.shared_off.assign(shared.size() + 1, 0);
         for (size_t i = 0; i < shared.size(); ++i) {
             std::sort(src[i].begin(), src[i].end());
             rp.shared_off[i + 1] = rp.shared_off[i] + (int32_t)src[i].size();
-            for (auto& pr : src[i]) rp.shared_src.push_back(pr.second);
+            for (auto& pr : src[i]) {
+                rp.shared_src.push_back(pr[1]);
+                rp.shared_src_r.push_back(pr[2]);
+            }
         }
         // ghost sources: first neighbour (ascending rank) providing the node
         rp.ghost_src.assign(rp.n_ghost, -1);

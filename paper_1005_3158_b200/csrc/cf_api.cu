@@ -136,8 +136,12 @@ struct Rank {
     TileArgs ta{};
     UpdArgs ua{};
     PackArgs pa{};
-    double* T[2] = {nullptr, nullptr};
-    double* Tslot[2] = {nullptr, nullptr};  // per-slot T copies (ping-pong with T)
+    // T ring: T[cur] = T^k, T[nxt] = T^{k+1} (written during the step, including by
+    // the tile kernel's fused private updates), T[old] = T^{k-1} (the lagged
+    // interface ambient of refresh_ambient blocked.hpp:441-449; never written
+    // during a step — a two-buffer ping-pong would race with the fused updates)
+    double* T[3] = {nullptr, nullptr, nullptr};
+    double* Tslot[2] = {nullptr, nullptr};  // per-slot T copies (ping-pong)
     double* recv = nullptr;
     double* send = nullptr;
     double* acc_c = nullptr;
@@ -169,7 +173,14 @@ struct cf_plan {
     DevParams* dP = nullptr;
     bool temp_dep = false, finite_range = false, any_dir = false;
     std::vector<std::unique_ptr<Rank>> ranks;
-    int cur = 0;                 // index of the current T buffer
+    int cur = 0;                 // index of the current T buffer (ring of 3)
+    int nxt() const { return (cur + 1) % 3; }
+    int old() const { return (cur + 2) % 3; }
+    int step_parity = 0;
+    void advance() {
+        cur = (cur + 1) % 3;
+        step_parity ^= 1;
+    }
     int32_t N_global = 0;
     double loop_seconds = 0;
     double eq13_min = 0;
@@ -221,10 +232,10 @@ void launch_tile(cf_plan* p, Rank& r, double t_end) {
     const bool det = p->mode == CF_MODE_DETERMINISTIC;
     TileArgs a = r.ta;
     a.T = r.T[p->cur];
-    a.Told = r.T[p->cur ^ 1];
-    a.Tn = r.T[p->cur ^ 1];
-    a.Tslot = r.Tslot[p->cur];
-    a.Tslot_n = r.Tslot[p->cur ^ 1];
+    a.Told = r.T[p->old()];
+    a.Tn = r.T[p->nxt()];
+    a.Tslot = r.Tslot[p->step_parity];
+    a.Tslot_n = r.Tslot[p->step_parity ^ 1];
     a.t_end = t_end;
     const bool dir = r.ua.node_dir != nullptr, cl = p->finite_range, td = p->temp_dep;
     const int nt = p->tile_threads;
@@ -259,8 +270,8 @@ void launch_update(cf_plan* p, Rank& r, double t_end) {
     UpdArgs a = r.ua;
     a.T = r.T[p->cur];
     a.Tcur_w = r.T[p->cur];
-    a.Tn = r.T[p->cur ^ 1];
-    a.Tslot_n = r.Tslot[p->cur ^ 1];
+    a.Tn = r.T[p->nxt()];
+    a.Tslot_n = r.Tslot[p->step_parity ^ 1];
     a.t_end = t_end;
     int blocks;
     if (p->temp_dep) {  // no fused private updates: every node
@@ -333,7 +344,7 @@ void enqueue_step(cf_plan* p, double t_end) {
         exchange(p);
     }
     for (auto& r : p->ranks) launch_update(p, *r, t_end);
-    p->cur ^= 1;
+    p->advance();
 }
 
 void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
@@ -347,6 +358,7 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
 
     r.T[0] = M.alloc<double>(nT);
     r.T[1] = M.alloc<double>(nT);
+    r.T[2] = M.alloc<double>(nT);
     r.Tslot[0] = M.alloc<double>(S_tot + 2);
     r.Tslot[1] = M.alloc<double>(S_tot + 2);
     r.st = M.alloc<DevState>(1);
@@ -381,8 +393,10 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     a.stages = p->stages;
     if (const char* e = std::getenv("CF_PROBE")) a.probe = std::atoi(e);
     r.tile_smem = tile_smem_bytes(h, p->stages);
-    if (r.tile_smem > 227 * 1024) raise(CF_INVALID_ARG, "tile shared-memory footprint exceeds 227 KB; use smaller tiles");
-    set_tile_attr(r.tile_smem);
+    if (r.tile_smem > 220 * 1024) raise(CF_INVALID_ARG, "tile shared-memory footprint exceeds 220 KB; use smaller tiles");
+    // the attribute is per function (shared by every plan and rank): the opt-in maximum;
+    // occupancy follows the dynamic size passed at launch
+    set_tile_attr(220 * 1024);
     {
         int per_sm = 0, sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
@@ -467,8 +481,8 @@ void init_state(cf_plan* p, const std::vector<double>& T_global) {
         const int64_t nT = (int64_t)r.H.n_local + r.H.n_ghost;
         std::vector<double> T(nT);
         for (int64_t i = 0; i < nT; ++i) T[i] = T_global[r.H.local_global[i]];
-        CF_CUDA_CHECK(cudaMemcpyAsync(r.T[0], T.data(), nT * sizeof(double), cudaMemcpyHostToDevice, p->stream));
-        CF_CUDA_CHECK(cudaMemcpyAsync(r.T[1], T.data(), nT * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+        for (int b = 0; b < 3; ++b)
+            CF_CUDA_CHECK(cudaMemcpyAsync(r.T[b], T.data(), nT * sizeof(double), cudaMemcpyHostToDevice, p->stream));
         const int64_t S_tot = r.H.slot_node.size();
         std::vector<double> Ts(S_tot + 2, 0.0);
         for (int64_t q = 0; q < S_tot; ++q)
@@ -489,6 +503,7 @@ void init_state(cf_plan* p, const std::vector<double>& T_global) {
         CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));  // T is a stack vector
     }
     p->cur = 0;
+    p->step_parity = 0;
     if (p->graph) {
         cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
@@ -517,12 +532,13 @@ void run_steps(cf_plan* p, int64_t n, double t_end) {
     CF_CUDA_CHECK(cudaEventRecord(p->ev0, p->stream));
     int64_t done = 0;
     if (p->graph_steps > 0) {
-        if (p->graph && (p->graph_t_end != t_end || p->graph_cur != p->cur)) {
+        const int state_key = p->cur * 2 + p->step_parity;
+        if (p->graph && (p->graph_t_end != t_end || p->graph_cur != state_key)) {
             cudaGraphExecDestroy(p->graph);
             p->graph = nullptr;
         }
         if (!p->graph && n >= p->graph_steps) {
-            const int cur0 = p->cur;
+            const int cur0 = p->cur, par0 = p->step_parity;
             cudaGraph_t g;
             CF_CUDA_CHECK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
             for (int64_t s = 0; s < p->graph_steps; ++s) enqueue_step(p, t_end);
@@ -530,14 +546,15 @@ void run_steps(cf_plan* p, int64_t n, double t_end) {
             CF_CUDA_CHECK(cudaGraphInstantiate(&p->graph, g, 0));
             cudaGraphDestroy(g);
             p->cur = cur0;  // capture did not execute
+            p->step_parity = par0;
             p->graph_t_end = t_end;
-            p->graph_cur = cur0;
+            p->graph_cur = cur0 * 2 + par0;
         }
         while (p->graph && n - done >= p->graph_steps) {
             CF_CUDA_CHECK(cudaGraphLaunch(p->graph, p->stream));
-            if (p->graph_steps & 1) p->cur ^= 1;
+            for (int64_t s = 0; s < p->graph_steps; ++s) p->advance();
             done += p->graph_steps;
-            if (p->graph_cur != p->cur) break;  // odd graph length: recapture next call
+            if (p->graph_cur != p->cur * 2 + p->step_parity) break;  // length not a multiple of 6: recapture
         }
     }
     for (; done < n; ++done) enqueue_step(p, t_end);
@@ -854,7 +871,7 @@ int cf_time_phases(cf_plan* p, int64_t n, double* ms_out) {
             CF_CUDA_CHECK(cudaEventRecord(ev[3], p->stream));
             for (auto& r : p->ranks) launch_update(p, *r, 0.0);
             CF_CUDA_CHECK(cudaEventRecord(ev[4], p->stream));
-            p->cur ^= 1;
+            p->advance();
             CF_CUDA_CHECK(cudaEventSynchronize(ev[4]));
             for (int k = 0; k < 4; ++k) {
                 float ms = 0;
@@ -1169,7 +1186,7 @@ int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_r
         PlanOptions po;
         po.mode = opts->mode;
         po.elem_order = opts->elem_order;
-        po.tile_elems = opts->tile_elems > 0 ? opts->tile_elems : 1024;
+        po.tile_elems = opts->tile_elems > 0 ? opts->tile_elems : 384;
         po.tile_of_element = opts->tile_of_element;
         po.world_size = std::max(1, opts->world_size);
         std::vector<int32_t> part;

@@ -68,3 +68,90 @@ def test_reference_blocks_replayed():
     ref, bm = orc.ref_solve(case.mesh, case.setup, 30, blocks=8)
     det = cf.solve(case.mesh, case.setup, cf.SolveOptions(max_steps=30, mode="deterministic", blocks=bm))
     assert np.array_equal(det.T, ref.T)
+
+
+# ---------------------------------------------------------------- domain decomposition
+@pytest.mark.parametrize("ranks", [2, 4])
+@pytest.mark.parametrize("mode", ["deterministic", "atomic"])
+def test_multirank_inprocess_vs_oracle(ranks, mode):
+    """RCB decomposition over `ranks` in-process ranks on one GPU (exchange of
+    shared-node partials + external-node T by device copies): deterministic
+    mode is bitwise equal to the oracle replaying the same parts and tiles
+    (per node: ascending-rank sum of each rank's ascending-tile partial)."""
+    case = configs.casting(12, jitter=0.15, seed=2, dt_safety=0.14)
+    parts = cf.partition_rcb(case.mesh, ranks)
+    opts = cf.SolveOptions(max_steps=30, mode=mode, tile_elems=256, world_size=ranks, local_ranks=ranks)
+    gpu = cf.solve(case.mesh, case.setup, opts)
+    tiles, _ = cf.tile_map(case.mesh, case.setup, opts)
+    ref = orc.solve(case.mesh, case.setup, 30, blocks=tiles, parts=parts)
+    if mode == "deterministic":
+        assert np.array_equal(gpu.T, ref.T), np.abs(gpu.T - ref.T).max()
+    assert rel(gpu.T, ref.T) <= RTOL
+    single = orc.solve(case.mesh, case.setup, 30)
+    assert rel(gpu.T, single.T) <= RTOL
+
+
+def test_multirank_interface_split_across_ranks():
+    """A partition cutting through the cast/mould interface: sister elements on
+    other ranks supply the lagged ambient through ghost nodes."""
+    case = configs.casting(10, dt_safety=0.14)
+    E = case.mesh.element_count()
+    parts = (np.arange(E) % 3).astype(np.int32)  # scattered parts: every interface pair crosses ranks
+    opts = cf.SolveOptions(max_steps=20, mode="deterministic", tile_elems=128, world_size=3, local_ranks=3,
+                           part_of_element=parts)
+    gpu = cf.solve(case.mesh, case.setup, opts)
+    tiles, _ = cf.tile_map(case.mesh, case.setup, opts)
+    ref = orc.solve(case.mesh, case.setup, 20, blocks=tiles, parts=parts)
+    assert np.array_equal(gpu.T, ref.T)
+
+
+# ---------------------------------------------------------------- solver semantics
+def test_t_end_mode_and_series():
+    """solve_serial's t_end loop (blocked.hpp:674-677): dt clipped to the
+    remaining time, output_every series of (t, Tmin, Tmax)."""
+    case = configs.casting(10, dt_safety=0.14)
+    case.setup.solver.output_every = 7
+    dt = orc.solve(case.mesh, case.setup, 1).dt
+    case.setup.solver.t_end = 23.5 * dt
+    gpu = cf.solve(case.mesh, case.setup, cf.SolveOptions(max_steps=0))
+    ref = orc.solve(case.mesh, case.setup, 0)
+    assert gpu.steps == ref.steps == 24
+    assert gpu.end_time == ref.time
+    assert rel(gpu.T, ref.T) <= RTOL
+    assert len(gpu.series) == len(ref.series) == 3
+    for s, r in zip(gpu.series, ref.series):
+        assert s.time == r[0] and abs(s.t_min - r[1]) <= 1e-9 * abs(r[1]) and abs(s.t_max - r[2]) <= 1e-9 * r[2]
+
+
+def test_dirichlet_and_temperature_dependent_tables():
+    """Fixed-temperature BC f(t) (lowest tag wins, blocked.hpp:250-263),
+    piecewise-linear c(T), k(T) (dynamic dt, :477-480) and clamp accounting."""
+    m = cf.generate_fixture("cube", 8)
+    # split the outer tag: x = 0 face fixed, the rest convective
+    x0 = np.all(m.nodes[m.facets][:, :, 0] == 0.0, axis=1)
+    m.facet_tag = np.where(x0, 1, 0).astype(np.int32)
+    m.tags = ["outer", "hot"]
+    mat = cf.MaterialTable.make(rho=7800.0, c=[(300.0, 450.0), (900.0, 700.0)], k=[(300.0, 45.0), (900.0, 30.0)],
+                                latent_heat=2.0e5, solidus=700.0, liquidus=760.0, T0=650.0)
+    setup = cf.SimulationSetup(
+        materials=[mat],
+        boundary_conditions={"outer": cf.BoundaryCondition("flux", h=50.0, t_inf=300.0),
+                             "hot": cf.BoundaryCondition("fixed", fixed_T=cf.PiecewiseLinear([0.0, 50.0], [650.0, 950.0]))},
+        solver=cf.SolverConfig(dt_safety=0.1))
+    opts = cf.SolveOptions(max_steps=60, tile_elems=128)
+    gpu = cf.solve(m, setup, opts)
+    tiles, _ = cf.tile_map(m, setup, opts)
+    ref = orc.solve(m, setup, 60, blocks=tiles)
+    assert gpu.steps == 60 and gpu.end_time == ref.time
+    assert np.array_equal(gpu.T, ref.T), np.abs(gpu.T - ref.T).max()
+    assert rel(gpu.T, orc.solve(m, setup, 60).T) <= RTOL
+    assert gpu.clamp_steps == ref.clamp_steps and ref.clamp_steps > 0
+
+
+def test_lambda_max_matches_oracle():
+    case = configs.casting(10, dt_safety=0.14)
+    with cf.Solver(case.mesh, case.setup) as s:
+        lam, e13 = s.estimate_lambda_max(300)
+    lo, e13o = orc.lambda_max(case.mesh, case.setup, 300)
+    assert abs(lam - lo) <= 1e-6 * lo
+    assert e13 == e13o

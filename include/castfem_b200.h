@@ -275,6 +275,16 @@ int cf_partition_rcb(const cf_mesh_desc* mesh, int32_t parts, int32_t* part_of_e
 int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts,
                 int32_t* tile_of_element, int32_t* n_tiles);
 
+/* The exchange plan of rank `rank` (classify_nodes partition.hpp:305-367 +
+ * SPEC exchange_and_merge S:450-458), as global node ids. Per neighbour k
+ * (ascending rank nbr_rank[k]): shared nodes (ascending global id; the c and r
+ * partials travel in this order) and external nodes whose pre-update T flows
+ * to / from it. Two-phase: NULL arrays return the sizes in counts[3*k..3*k+2]
+ * (shared, ext_to, ext_from) after *n_nbrs; then pass arrays of those totals. */
+int cf_exchange_plan(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts,
+                     int32_t* n_nbrs, int32_t* nbr_rank, int64_t* counts, int32_t* shared, int32_t* ext_to,
+                     int32_t* ext_from);
+
 /* Synthetic fixtures (bench module S:502-519), structured Kuhn 6-tet cubes.
  * kind: 0 = single-region cube, all faces tag "outer";
  *       1 = casting: sphere of radius `radius` (cell-centre test) in a mould

@@ -900,3 +900,82 @@ OR_EXPORT int or_lambda_max(const cf_mesh_desc* m, const cf_setup_desc* s, int i
     prep_free(&p);
     return CF_OK;
 }
+
+
+/* ------------------------------------------------------------ partial assembly */
+/* assemble_blocks restricted to the elements with elem_mask[e] != 0, as one
+ * block in ascending element order (+ their facets), into per-node (c, r)
+ * (zero for untouched nodes). The interface ambient is 0.25*sum(T_old[sister
+ * nodes]) (refresh_ambient's one-step lag). Used by the multi-rank protocol
+ * test: each worker assembles its own part (SPEC exchange_and_merge S:450-458). */
+OR_EXPORT int or_assemble_part(const cf_mesh_desc* m, const cf_setup_desc* s, const char* elem_mask,
+                               const double* T, const double* T_old, double time, double* c_out, double* r_out) {
+    prep_t p; memset(&p, 0, sizeof p);
+    int st = prep_mesh(m, s->n_materials, &p);
+    if (st) { prep_free(&p); return st; }
+    pair_t* pairs = NULL; int np = 0;
+    if ((st = pair_sisters(m, &p, &pairs, &np))) { prep_free(&p); return st; }
+    int N = p.N, E = p.E, F = p.F;
+    mat_t* mats = (mat_t*)calloc(s->n_materials > 0 ? s->n_materials : 1, sizeof(mat_t));
+    for (int r = 0; r < s->n_materials; ++r) if ((st = mat_init(&s->materials[r], &mats[r]))) goto out;
+    for (int n = 0; n < N; ++n) { c_out[n] = 0; r_out[n] = 0; }
+    {
+        int32_t* pair_of_facet = (int32_t*)malloc(sizeof(int32_t) * (F > 0 ? F : 1));
+        for (int f = 0; f < F; ++f) pair_of_facet[f] = -1;
+        for (int i = 0; i < np; ++i) pair_of_facet[pairs[i].facet] = i;
+        double* H = (double*)malloc(sizeof(double) * N);
+        for (int n = 0; n < N; ++n) H[n] = enthalpy(&mats[p.node_region[n]], T[n]);
+        for (int e = 0; e < E; ++e) {
+            if (!elem_mask[e]) continue;
+            const cf_material* mm = &s->materials[m->region[e]];
+            const int32_t* t = p.tets + 4 * (size_t)e;
+            double tn[4], hn[4];
+            for (int a = 0; a < 4; ++a) { tn[a] = T[t[a]]; hn[a] = H[t[a]]; }
+            const geom_t* g = &p.geom[e];
+            double t_bar = 0.25 * (tn[0] + tn[1] + tn[2] + tn[3]);
+            double lump = mm->rho * apparent_c(g, tn, hn, mm) * g->vol * 0.25;
+            double kv = pl_eval(&mm->k, t_bar) * g->vol;
+            v3 gt = {0, 0, 0};
+            for (int b = 0; b < 4; ++b) gt = vadd(gt, vmul(g->g[b], tn[b]));
+            for (int a = 0; a < 4; ++a) { c_out[t[a]] += lump; r_out[t[a]] -= kv * vdot(g->g[a], gt); }
+        }
+        /* facets in (owner element ascending, facet id ascending) order */
+        for (int e = 0; e < E; ++e) {
+            if (!elem_mask[e]) continue;
+            for (int f = 0; f < F; ++f) {
+                if (p.owner[f] != e) continue;
+                int tag = m->facet_tag[f];
+                const cf_boundary_condition* bc = NULL;
+                for (int b = 0; b < s->n_bcs; ++b) if (name_eq(s->bcs[b].tag, m->tags[tag])) bc = &s->bcs[b];
+                if (bc && bc->kind == CF_BC_FIXED) continue;
+                double q, h, tinf;
+                const int32_t* fn = m->facets + 3 * (size_t)f;
+                double ts[3] = {T[fn[0]], T[fn[1]], T[fn[2]]};
+                if (bc) { q = bc->q; h = bc->h; tinf = bc->t_inf; }
+                else {
+                    const cf_interface_coeff* ic = NULL;
+                    for (int c = 0; c < m->n_contacts && !ic; ++c)
+                        if (m->contacts[2 * c] == tag || m->contacts[2 * c + 1] == tag)
+                            for (int k = 0; k < s->n_coeffs && !ic; ++k) {
+                                const cf_interface_coeff* x = &s->coeffs[k];
+                                const char* A = m->tags[m->contacts[2 * c]]; const char* B = m->tags[m->contacts[2 * c + 1]];
+                                if ((name_eq(x->tag_a, A) && name_eq(x->tag_b, B)) || (name_eq(x->tag_a, B) && name_eq(x->tag_b, A))) ic = x;
+                            }
+                    if (!ic || pair_of_facet[f] < 0) { st = fail(CF_CONFIG, "unresolved facet"); break; }
+                    const int32_t* sn = p.tets + 4 * (size_t)pairs[pair_of_facet[f]].sister;
+                    double sum = 0;
+                    for (int a = 0; a < 4; ++a) sum += T_old[sn[a]];
+                    q = 0.0; h = pl_eval(&ic->h, ic->var == CF_VAR_TIME ? time : (ts[0] + ts[1] + ts[2]) / 3.0);
+                    tinf = 0.25 * sum;
+                }
+                double third = facet_area(m, f) / 3.0;
+                for (int a = 0; a < 3; ++a) r_out[fn[a]] += third * (-q + h * (tinf - ts[a]));
+            }
+        }
+        free(pair_of_facet); free(H);
+    }
+out:
+    for (int r = 0; r < s->n_materials; ++r) free(mats[r].cum);
+    free(mats); free(pairs); prep_free(&p);
+    return st;
+}

@@ -55,6 +55,9 @@ def oracle_lib():
         L.or_enthalpy.argtypes = [C.POINTER(_abi.cf_material), C.c_double]
         L.or_apparent_heat_capacity.restype = C.c_double
         L.or_apparent_heat_capacity.argtypes = [_dp, _dp, _dp, C.POINTER(_abi.cf_material)]
+        L.or_assemble_part.restype = C.c_int
+        L.or_assemble_part.argtypes = [C.POINTER(_abi.cf_mesh_desc), C.POINTER(_abi.cf_setup_desc), C.c_char_p, _dp,
+                                       _dp, C.c_double, _dp, _dp]
         L.or_element_accumulate.restype = None
         L.or_element_accumulate.argtypes = [_dp, C.POINTER(_abi.cf_material), _dp, _dp, _dp, _dp]
         _o = L
@@ -197,3 +200,21 @@ class RefBench:
         if self.h:
             ref_lib().ref_bench_destroy(self.h)
             self.h = None
+
+
+def assemble_part(mesh: Mesh, setup: SimulationSetup, elem_mask: np.ndarray, T: np.ndarray, T_old: np.ndarray,
+                  time: float):
+    """Per-node (c, r) of one worker's elements (ascending element order, its facets after)."""
+    keep = _Keep()
+    md, sd = mesh_desc(mesh, keep), setup_desc(setup, keep)
+    N = mesh.node_count()
+    c = np.zeros(N)
+    r = np.zeros(N)
+    mask = np.ascontiguousarray(elem_mask, dtype=np.int8)
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    T_old = np.ascontiguousarray(T_old, dtype=np.float64)
+    st = oracle_lib().or_assemble_part(C.byref(md), C.byref(sd), mask.ctypes.data_as(C.c_char_p), _p(T), _p(T_old),
+                                       time, _p(c), _p(r))
+    if st:
+        raise OracleError(st, oracle_lib().or_last_error().decode())
+    return c, r

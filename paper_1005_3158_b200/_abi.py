@@ -104,6 +104,8 @@ SIGNATURES = [
     ("cf_partition_rcb", C.c_int, [C.POINTER(cf_mesh_desc), C.c_int32, _ip]),
     ("cf_tile_map", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts), _ip,
                               _ip]),
+    ("cf_exchange_plan", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts), _ip,
+                                   _ip, C.POINTER(C.c_int64), _ip, _ip, _ip]),
     ("cf_generate_fixture", C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, C.c_uint64,
                                       C.POINTER(cf_fixture)]),
     ("cf_counter_uniform", C.c_int, [C.c_uint64, C.POINTER(C.c_int64), C.c_int64, C.c_double, C.c_double, _dp]),

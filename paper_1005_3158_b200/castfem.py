@@ -525,6 +525,36 @@ def tile_map(m: Mesh, setup: SimulationSetup, opts: SolveOptions) -> Tuple[np.nd
     return out, n.value
 
 
+def exchange_plan(m: Mesh, setup: SimulationSetup, world_size: int, rank: int,
+                  part_of_element: Optional[np.ndarray] = None) -> List[dict]:
+    """Rank `rank`'s neighbours and exchange lists (global node ids): shared
+    nodes (c, r partials travel in this order) and external nodes whose
+    pre-update T flows to / from each neighbour."""
+    keep = _Keep()
+    md, sd = mesh_desc(m, keep), setup_desc(setup, keep)
+    ro = run_opts(SolveOptions(world_size=world_size, rank=rank, part_of_element=part_of_element), keep)
+    nn = C.c_int32()
+    check(lib().cf_exchange_plan(C.byref(md), C.byref(sd), C.byref(ro), C.byref(nn), None, None, None, None, None))
+    k = nn.value
+    ranks = np.zeros(max(k, 1), np.int32)
+    counts = np.zeros(3 * max(k, 1), np.int64)
+    check(lib().cf_exchange_plan(C.byref(md), C.byref(sd), C.byref(ro), C.byref(nn),
+                                 ranks.ctypes.data_as(C.POINTER(C.c_int32)),
+                                 counts.ctypes.data_as(C.POINTER(C.c_int64)), None, None, None))
+    tot = counts.reshape(-1, 3)[:k].sum(0) if k else np.zeros(3, np.int64)
+    sh, to, fr = (np.zeros(max(1, int(t)), np.int32) for t in tot)
+    check(lib().cf_exchange_plan(C.byref(md), C.byref(sd), C.byref(ro), C.byref(nn), None, None,
+                                 sh.ctypes.data_as(C.POINTER(C.c_int32)), to.ctypes.data_as(C.POINTER(C.c_int32)),
+                                 fr.ctypes.data_as(C.POINTER(C.c_int32))))
+    out, a, b, c = [], 0, 0, 0
+    for j in range(k):
+        ns, nt, nf = (int(x) for x in counts[3 * j:3 * j + 3])
+        out.append({"rank": int(ranks[j]), "shared": sh[a:a + ns].copy(), "ext_to": to[b:b + nt].copy(),
+                    "ext_from": fr[c:c + nf].copy()})
+        a, b, c = a + ns, b + nt, c + nf
+    return out
+
+
 def generate_fixture(kind: str, n: int, radius: float = 0.35, jitter: float = 0.0, seed: int = 0,
                      perm_seed: int = 0) -> Mesh:
     """Structured Kuhn 6-tet fixtures (SPEC bench module S:502-519): 'cube' or 'casting'."""

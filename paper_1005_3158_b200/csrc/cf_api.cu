@@ -1211,6 +1211,46 @@ int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_r
     });
 }
 
+int cf_exchange_plan(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts, int32_t* n_nbrs,
+                     int32_t* nbr_rank, int64_t* counts, int32_t* shared, int32_t* ext_to, int32_t* ext_from) {
+    return guarded([&] {
+        if (!mesh || !setup || !opts || !n_nbrs) raise(CF_INVALID_ARG, "null argument");
+        if (opts->world_size < 2) raise(CF_INVALID_ARG, "exchange plan needs world_size >= 2");
+        MeshData m;
+        std::vector<Geom> geom;
+        finalize_mesh(mesh, m, &geom);
+        SetupData S;
+        resolve_setup(m, geom, setup, S);
+        std::vector<int32_t> label(m.N);
+        std::iota(label.begin(), label.end(), 0);
+        PlanOptions po;
+        po.elem_order = opts->elem_order;
+        po.node_order = CF_NODE_ORDER_GIVEN;
+        po.tile_elems = opts->tile_elems > 0 ? opts->tile_elems : 384;
+        po.world_size = opts->world_size;
+        std::vector<int32_t> part = opts->partition == CF_PARTITION_GIVEN && opts->part_of_element
+                                        ? std::vector<int32_t>(opts->part_of_element, opts->part_of_element + m.E)
+                                        : partition_rcb(m, po.world_size);
+        po.part_of_element = part.data();
+        RankPlan rp;
+        build_rank_plan(m, geom, S, po, label, opts->rank, rp);
+        *n_nbrs = (int32_t)rp.nbrs.size();
+        int64_t os = 0, ot = 0, of = 0;
+        for (size_t k = 0; k < rp.nbrs.size(); ++k) {
+            const auto& x = rp.nbrs[k];
+            if (nbr_rank) nbr_rank[k] = x.rank;
+            if (counts) {
+                counts[3 * k] = (int64_t)x.shared.size();
+                counts[3 * k + 1] = (int64_t)x.ext_to.size();
+                counts[3 * k + 2] = (int64_t)x.ext_from.size();
+            }
+            for (int32_t l : x.shared) if (shared) shared[os++] = rp.local_global[l];
+            for (int32_t l : x.ext_to) if (ext_to) ext_to[ot++] = rp.local_global[l];
+            for (int32_t l : x.ext_from) if (ext_from) ext_from[of++] = rp.local_global[l];
+        }
+    });
+}
+
 int cf_generate_fixture(int32_t kind, int32_t n, double radius, double jitter, uint64_t seed, uint64_t perm_seed,
                         cf_fixture* out) {
     return guarded([&] {

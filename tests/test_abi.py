@@ -1,0 +1,44 @@
+"""The C-ABI library loads and exports every entry point include/castfem_b200.h declares
+(no GPU needed: no compute call is made)."""
+import ctypes as C
+import os
+import re
+
+from paper_1005_3158_b200 import _abi
+
+HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "castfem_b200.h")
+
+
+def declared():
+    src = open(HDR).read()
+    return sorted(set(re.findall(r"^int\s+(cf_\w+)\s*\(", src, re.M)))
+
+
+def test_header_declares_entry_points():
+    names = declared()
+    assert "cf_plan_create" in names and "cf_step" in names and len(names) >= 25
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _abi.lib()
+    for name in declared():
+        assert hasattr(lib, name), name
+
+
+def test_python_mirror_binds_every_declared_symbol():
+    bound = {n for n, _, _ in _abi.SIGNATURES}
+    assert set(declared()) <= bound
+
+
+def test_abi_version_and_error_buffer():
+    lib = _abi.lib()
+    assert lib.cf_abi_version() == 1
+    buf = C.create_string_buffer(64)
+    assert lib.cf_last_error(buf, 64) == 0
+    assert lib.cf_last_error(None, 0) == _abi.CF_INVALID_ARG
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump --list-elf {_abi.LIB_PATH} 2>/dev/null").read()
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out

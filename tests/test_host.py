@@ -1,0 +1,177 @@
+"""Product host-side setup (libcastfem_b200.so, CPU only) against the
+reference: RCM order (reorder.hpp:127-148), mesh finalize (mesh.hpp:148-207),
+sister pairing (mesh.hpp:456-478), exact fixture counts,
+RCB partitions, tiling coverage, and the error taxonomy (errors.hpp)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_1005_3158_b200 import castfem as cf
+from paper_1005_3158_b200 import configs
+from paper_1005_3158_b200.castfem import _Keep, mesh_desc
+
+needs_ref = pytest.mark.skipif(not orc.ref_available(), reason="oracle/_ref not built")
+MESHES = {
+    "cube5": lambda: cf.generate_fixture("cube", 5),
+    "casting9": lambda: cf.generate_fixture("casting", 9),
+    "jitter8_perm": lambda: cf.generate_fixture("casting", 8, jitter=0.2, seed=5, perm_seed=17),
+    "cube7_perm": lambda: cf.generate_fixture("cube", 7, perm_seed=99),
+}
+
+
+def ref_call(fn, m, *args):
+    keep = _Keep()
+    d = mesh_desc(m, keep)
+    st = fn(C.byref(d), *args)
+    assert st == 0, orc.ref_lib().ref_last_error()
+
+
+@needs_ref
+@pytest.mark.parametrize("name", sorted(MESHES))
+def test_rcm_permutation_equals_reference(name):
+    m = MESHES[name]()
+    ours = cf.rcm_permutation(m)
+    ref = np.zeros(m.node_count(), np.int32)
+    ref_call(orc.ref_lib().ref_rcm_permutation, m, -1, ref.ctypes.data_as(C.POINTER(C.c_int32)))
+    assert np.array_equal(ours, ref)
+    seed = int(m.node_count() // 3)
+    ours_s = cf.rcm_permutation(m, seed)
+    ref_call(orc.ref_lib().ref_rcm_permutation, m, seed, ref.ctypes.data_as(C.POINTER(C.c_int32)))
+    assert np.array_equal(ours_s, ref)
+    bw = C.c_int64()
+    ref_call(orc.ref_lib().ref_bandwidth, m, ours.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(bw))
+    assert cf.bandwidth(m, ours) == bw.value  # (RCM can widen structured casting meshes: SURVEY P3)
+
+
+def test_rcm_kats():
+    def path(order):
+        nodes = np.array([[i, 0, 0] for i in range(6)], float)
+        tets = [[order[0], order[1], order[2], order[3]], [order[1], order[2], order[3], order[4]],
+                [order[2], order[3], order[4], order[5]]]
+        return cf.Mesh(nodes, tets, [0, 0, 0], np.zeros((0, 3)), np.zeros(0), [])
+    m = path([5, 2, 0, 3, 1, 4])
+    p = cf.rcm_permutation(m)
+    assert sorted(p) == list(range(6))
+    assert cf.bandwidth(m, p) <= cf.bandwidth(m)
+
+
+@needs_ref
+@pytest.mark.parametrize("name", sorted(MESHES))
+def test_finalize_equals_reference(name):
+    m = MESHES[name]()
+    tets, owner = cf.finalize_mesh(m)
+    rt = np.zeros_like(tets)
+    ro = np.zeros(max(1, m.facets.shape[0]), np.int32)
+    ref_call(orc.ref_lib().ref_finalize, m, rt.ctypes.data_as(C.POINTER(C.c_int32)),
+             ro.ctypes.data_as(C.POINTER(C.c_int32)))
+    assert np.array_equal(tets, rt) and np.array_equal(owner, ro[:len(owner)])
+
+
+@needs_ref
+@pytest.mark.parametrize("name", ["casting9", "jitter8_perm"])
+def test_sister_pairing_equals_reference(name):
+    m = MESHES[name]()
+    ours = cf.pair_sister_facets(m)
+    n = C.c_int64()
+    ref_call(orc.ref_lib().ref_pair_sister_facets, m, None, 0, C.byref(n))
+    ref = np.zeros((n.value, 3), np.int32)
+    ref_call(orc.ref_lib().ref_pair_sister_facets, m, ref.ctypes.data_as(C.POINTER(C.c_int32)), n.value, C.byref(n))
+    assert np.array_equal(ours, ref)
+    keep = _Keep()
+    d = mesh_desc(m, keep)
+    o = np.zeros_like(ref)
+    assert orc.oracle_lib().or_pair_sister_facets(C.byref(d), o.ctypes.data_as(C.POINTER(C.c_int32)), n.value,
+                                                  C.byref(n)) == 0
+    assert np.array_equal(o, ref)
+
+
+@pytest.mark.parametrize("n,E,N,Fbc,Fif", [
+    (32, 196608, 38291, 12288, 9408),
+    (70, 2058000, 369169, 58800, 45024),
+    (128, 12582912, 2184611, 196608, 151680),
+])
+def test_fixture_counts_exact(n, E, N, Fbc, Fif):
+    """SURVEY §8(d) exact counts (P11), interface nodes duplicated."""
+    m = cf.generate_fixture("casting", n, jitter=0.2 if n == 70 else 0.0, seed=7, perm_seed=11 if n == 70 else 0)
+    assert m.element_count() == E and m.node_count() == N
+    assert int((m.facet_tag == 0).sum()) == Fbc and int((m.facet_tag > 0).sum()) == Fif
+    if n == 32:
+        cube = cf.generate_fixture("cube", n)
+        assert cube.element_count() == 196608 and cube.node_count() == 35937 and cube.facets.shape[0] == 12288
+
+
+def test_regions_node_disjoint_and_cube_kat():
+    m = cf.generate_fixture("cube", 1)  # 6-tet cube, 8 nodes
+    assert m.element_count() == 6 and m.node_count() == 8
+    c = cf.generate_fixture("casting", 12)
+    reg = np.full(c.node_count(), -1)
+    for e in range(c.element_count()):
+        for n in c.tets[e]:
+            assert reg[n] in (-1, c.region[e])
+            reg[n] = c.region[e]
+
+
+def test_rcb_partition_balanced():
+    m = cf.generate_fixture("casting", 12)
+    for parts in (2, 3, 4, 8):
+        p = cf.partition_rcb(m, parts)
+        counts = np.bincount(p, minlength=parts)
+        assert counts.min() > 0 and counts.max() - counts.min() <= 1
+
+
+def test_tile_map_covers_every_element_once():
+    c = configs.casting(10, dt_safety=0.14)
+    for order in ("morton", "min_node", "given"):
+        tiles, nt = cf.tile_map(c.mesh, c.setup, cf.SolveOptions(tile_elems=200, elem_order=order))
+        assert tiles.min() == 0 and tiles.max() == nt - 1
+        assert np.bincount(tiles).max() <= 200
+
+
+def test_exchange_plan_symmetric():
+    c = configs.casting(9, dt_safety=0.14)
+    parts = cf.partition_rcb(c.mesh, 3)
+    plans = {r: {x["rank"]: x for x in cf.exchange_plan(c.mesh, c.setup, 3, r, parts)} for r in range(3)}
+    for r, nb in plans.items():
+        for q, x in nb.items():
+            y = plans[q][r]
+            assert np.array_equal(x["shared"], y["shared"])
+            assert np.array_equal(x["ext_to"], y["ext_from"]) and np.array_equal(x["ext_from"], y["ext_to"])
+            assert np.all(np.diff(x["shared"]) > 0)
+
+
+# ---------------------------------------------------------------- error taxonomy
+def _tile_status(m, setup):
+    try:
+        cf.tile_map(m, setup, cf.SolveOptions())
+        return 0
+    except cf.CastfemError as e:
+        return e.code
+
+
+def test_error_codes():
+    c = configs.casting(4, dt_safety=0.14)
+    m, s = c.mesh, c.setup
+    assert _tile_status(m, s) == 0
+    bad = cf.Mesh(m.nodes.copy(), m.tets.copy(), m.region, m.facets, m.facet_tag, m.tags, m.contacts)
+    bad.tets[0, 0] = m.node_count() + 5
+    assert _tile_status(bad, s) == cf.ValidationError.code                    # dangling node
+    deg = cf.Mesh(m.nodes.copy(), m.tets, m.region, m.facets, m.facet_tag, m.tags, m.contacts)
+    deg.nodes[deg.tets[3]] = deg.nodes[deg.tets[3][0]] + np.array([[0, 0, 0], [1e-3, 0, 0], [2e-3, 0, 0],
+                                                                   [3e-3, 1e-12, 0]])
+    assert _tile_status(deg, s) in (cf.DegenerateElementError.code, cf.ValidationError.code)
+    s2 = configs.casting(4, dt_safety=0.14).setup
+    s2.interface_coeffs = []
+    assert _tile_status(m, s2) == cf.ConfigError.code                          # contact without h_i
+    s3 = configs.casting(4, dt_safety=0.14).setup
+    s3.boundary_conditions = {}
+    assert _tile_status(m, s3) == cf.ConfigError.code                          # unresolved tag
+    s4 = configs.casting(4, dt_safety=1.5).setup
+    assert _tile_status(m, s4) == cf.ConfigError.code                          # safety outside (0, 1]
+    s5 = configs.casting(4, dt_safety=0.14).setup
+    s5.materials[0].latent_heat = -1.0
+    assert _tile_status(m, s5) == cf.ConfigError.code
+    shared = cf.Mesh(m.nodes, m.tets.copy(), m.region.copy(), m.facets, m.facet_tag, m.tags, m.contacts)
+    shared.region[0] = 1 - shared.region[0]                                    # regions share a node
+    assert _tile_status(shared, s) == cf.ValidationError.code

@@ -189,6 +189,8 @@ struct cf_plan {
     int64_t output_every = 0;
     double t_end_setup = 0;
     // graph
+    double* dTg = nullptr;       // global-order staging (device) for set_temperature / get_fields
+    double* dHg = nullptr;
     int64_t graph_steps = 0;
     cudaGraphExec_t graph = nullptr;
     double graph_t_end = 0;
@@ -197,6 +199,8 @@ struct cf_plan {
         if (graph) cudaGraphExecDestroy(graph);
         for (auto& r : ranks) r->mem.release();
         if (dP) cudaFree(dP);
+        if (dTg) cudaFree(dTg);
+        if (dHg) cudaFree(dHg);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (stream) cudaStreamDestroy(stream);
@@ -206,7 +210,7 @@ struct cf_plan {
 namespace {
 
 size_t tile_smem_bytes(const RankPlan& h, int stages) {
-    return stages * ((size_t)cf_round(h.max_blob, 16) + 8 * (size_t)h.max_slots) + 8 * (size_t)h.max_slots + 16;
+    return stages * ((size_t)cf_round(h.max_blob, 16) + 8 * (size_t)h.max_slots) + 16 * (size_t)h.max_slots + 16;
 }
 
 #define CF_TILE_VARIANTS_NT(X, NT)                                                                          \
@@ -475,33 +479,26 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     std::vector<int32_t>().swap(h.merge_idx);
 }
 
-void init_state(cf_plan* p, const std::vector<double>& T_global) {
+void init_state(cf_plan* p, const double* T_global_host) {
+    // one H2D of the global field, then on-device scatter into every rank's T ring and slot copies
+    if (!p->dTg) CF_CUDA_CHECK(cudaMalloc(&p->dTg, std::max<int64_t>(1, p->N_global) * sizeof(double)));
+    CF_CUDA_CHECK(cudaMemcpyAsync(p->dTg, T_global_host, (size_t)p->N_global * sizeof(double), cudaMemcpyHostToDevice,
+                                  p->stream));
     for (auto& rp : p->ranks) {
         Rank& r = *rp;
-        const int64_t nT = (int64_t)r.H.n_local + r.H.n_ghost;
-        std::vector<double> T(nT);
-        for (int64_t i = 0; i < nT; ++i) T[i] = T_global[r.H.local_global[i]];
-        for (int b = 0; b < 3; ++b)
-            CF_CUDA_CHECK(cudaMemcpyAsync(r.T[b], T.data(), nT * sizeof(double), cudaMemcpyHostToDevice, p->stream));
-        const int64_t S_tot = r.H.slot_node.size();
-        std::vector<double> Ts(S_tot + 2, 0.0);
-        for (int64_t q = 0; q < S_tot; ++q)
-            if (r.H.slot_node[q] >= 0) Ts[q] = T[(uint32_t)r.H.slot_node[q] & 0x0fffffffu];
-        CF_CUDA_CHECK(cudaMemcpyAsync(r.Tslot[0], Ts.data(), Ts.size() * sizeof(double), cudaMemcpyHostToDevice, p->stream));
-        CF_CUDA_CHECK(cudaMemcpyAsync(r.Tslot[1], Ts.data(), Ts.size() * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+        const int32_t nT = r.H.n_local + r.H.n_ghost;
+        const int blocks = std::max(1, std::min(1184, (nT + 255) / 256));
+        scatter_init_kernel<<<blocks, 256, 0, p->stream>>>(nT, r.ta.local_global, p->dTg, r.T[0], r.T[1], r.T[2]);
+        const int64_t S_tot = (int64_t)r.H.slot_node.size();
+        const int sb = (int)std::max<int64_t>(1, std::min<int64_t>(1184, (S_tot + 255) / 256));
+        slot_init_kernel<<<sb, 256, 0, p->stream>>>(S_tot, r.ta.slot_node, r.T[0], r.Tslot[0], r.Tslot[1]);
         DevState st{};
-        st.time = 0;
-        st.dt = 0;
-        st.step_index = 0;
-        st.clamp_steps = 0;
         st.min_bound[0] = st.min_bound[1] = 0x7ff0000000000000ull;
-        st.clamp_flag = 0;
-        st.ticket = 0;
         st.err_node = INT32_MAX;
-        st.done = 0;
         CF_CUDA_CHECK(cudaMemcpyAsync(r.st, &st, sizeof st, cudaMemcpyHostToDevice, p->stream));
-        CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));  // T is a stack vector
     }
+    CF_CUDA_CHECK(cudaGetLastError());
+    CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));  // st is a stack object
     p->cur = 0;
     p->step_parity = 0;
     if (p->graph) {
@@ -821,7 +818,7 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
             p->ranks.push_back(std::move(rk));
         }
         p->launches_per_step = 2 * (int64_t)p->ranks.size() + (p->world > 1 ? (int64_t)p->ranks.size() : 0);
-        init_state(p.get(), S.T0);
+        init_state(p.get(), S.T0.data());
         CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
         *out = p.release();
     });
@@ -840,8 +837,7 @@ int cf_set_temperature(cf_plan* p, const double* T_host) {
     return guarded([&] {
         if (!p || !T_host) raise(CF_INVALID_ARG, "null argument");
         CF_CUDA_CHECK(cudaSetDevice(p->device));
-        std::vector<double> T(T_host, T_host + p->N_global);
-        init_state(p, T);
+        init_state(p, T_host);
         p->loop_seconds = 0;
     });
 }
@@ -966,27 +962,32 @@ int cf_get_fields(cf_plan* p, double* T_host, double* H_host) {
     return guarded([&] {
         if (!p) raise(CF_INVALID_ARG, "null plan");
         CF_CUDA_CHECK(cudaSetDevice(p->device));
+        const size_t bytes = std::max<int64_t>(1, p->N_global) * sizeof(double);
+        if (!p->dTg) CF_CUDA_CHECK(cudaMalloc(&p->dTg, bytes));
+        if (H_host && !p->dHg) CF_CUDA_CHECK(cudaMalloc(&p->dHg, bytes));
+        if (p->ranks.size() > 1 || p->world > 1) {  // nodes owned by other processes keep the host value
+            if (T_host) CF_CUDA_CHECK(cudaMemcpyAsync(p->dTg, T_host, bytes, cudaMemcpyHostToDevice, p->stream));
+            if (H_host) CF_CUDA_CHECK(cudaMemcpyAsync(p->dHg, H_host, bytes, cudaMemcpyHostToDevice, p->stream));
+        }
         for (auto& rp : p->ranks) {
             Rank& r = *rp;
             const int32_t n = r.H.n_local;
-            std::vector<double> T(n), H(n);
-            if (T_host) CF_CUDA_CHECK(cudaMemcpyAsync(T.data(), r.T[p->cur], n * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
-            if (H_host) {
-                double* dH = nullptr;
-                CF_CUDA_CHECK(cudaMallocAsync(&dH, std::max<size_t>(1, n) * sizeof(double), p->stream));
-                const int blocks = std::max(1, std::min(1184, (n + 255) / 256));
-                if (p->temp_dep) enthalpy_kernel<true><<<blocks, 256, 0, p->stream>>>(n, r.T[p->cur], r.ua.node_region, p->dP, dH);
-                else enthalpy_kernel<false><<<blocks, 256, 0, p->stream>>>(n, r.T[p->cur], r.ua.node_region, p->dP, dH);
-                CF_CUDA_CHECK(cudaMemcpyAsync(H.data(), dH, n * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
-                CF_CUDA_CHECK(cudaFreeAsync(dH, p->stream));
-            }
-            CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
-            for (int32_t i = 0; i < n; ++i) {
-                const int32_t g = r.H.local_global[i];
-                if (T_host) T_host[g] = T[i];
-                if (H_host) H_host[g] = H[i];
-            }
+            const int blocks = std::max(1, std::min(1184, (n + 255) / 256));
+            double* tg = T_host ? p->dTg : nullptr;
+            double* hg = H_host ? p->dHg : nullptr;
+            if (p->temp_dep)
+                gather_fields_kernel<true><<<blocks, 256, 0, p->stream>>>(n, r.ta.local_global, r.T[p->cur],
+                                                                          r.ua.node_region, p->dP, tg, hg);
+            else
+                gather_fields_kernel<false><<<blocks, 256, 0, p->stream>>>(n, r.ta.local_global, r.T[p->cur],
+                                                                           r.ua.node_region, p->dP, tg, hg);
         }
+        CF_CUDA_CHECK(cudaGetLastError());
+        if (T_host) CF_CUDA_CHECK(cudaMemcpyAsync(T_host, p->dTg, (size_t)p->N_global * sizeof(double),
+                                                  cudaMemcpyDeviceToHost, p->stream));
+        if (H_host) CF_CUDA_CHECK(cudaMemcpyAsync(H_host, p->dHg, (size_t)p->N_global * sizeof(double),
+                                                  cudaMemcpyDeviceToHost, p->stream));
+        CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
     });
 }
 

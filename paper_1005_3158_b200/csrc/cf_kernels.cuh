@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
     uint8_t* const buf1 = smem + (a.stages - 1) * a.blob_smem;
     double* const sT0 = (double*)(smem + a.stages * (size_t)a.blob_smem);
     double* const sT1 = sT0 + (a.stages - 1) * a.max_slots;
-    double* sH = sT0 + a.stages * a.max_slots;
+    double2* sTH = (double2*)(sT0 + a.stages * a.max_slots);  // (T, H) per slot, 16 B aligned
 
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -212,7 +212,10 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
         }
         // phase 1: H = enthalpy(T) per slot (blocked.hpp:462-467) from the streamed slot temperatures
         const uint8_t* sinfo = B + L.sinfo;
-        for (int s = tid; s < ns; s += kTileThreads) sH[s] = dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], sT[s]);
+        for (int s = tid; s < ns; s += kTileThreads) {
+            const double T = sT[s];
+            sTH[s] = make_double2(T, dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], T));
+        }
         __syncthreads();
 
         // phase 2a: elements (element_accumulate fem.hpp:57-70); contributions overwrite
@@ -234,8 +237,9 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) g[0][c] = ((g[1][c] + g[2][c]) + g[3][c]) * -1.0;
             const ushort4 cn = conn[i];
-            const double T[4] = {sT[cn.x], sT[cn.y], sT[cn.z], sT[cn.w]};
-            const double H[4] = {sH[cn.x], sH[cn.y], sH[cn.z], sH[cn.w]};
+            const double2 th0 = sTH[cn.x], th1 = sTH[cn.y], th2 = sTH[cn.z], th3 = sTH[cn.w];
+            const double T[4] = {th0.x, th1.x, th2.x, th3.x};
+            const double H[4] = {th0.y, th1.y, th2.y, th3.y};
             const DevMaterial& m = sMat[ereg[i]];
             double lump, rc[4];
             dev_element<TDEP>(P, m, g, vol, max_edge, T, H, lump, rc);
@@ -305,24 +309,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
             const int beg = s == 0 ? 0 : cend[s - 1];
             const int end = cend[s];
             double c = 0, r = 0;
-            int j = beg;
-            for (; j + 4 <= end; j += 4) {
-                int li[4], ri[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) decode(csr[j + u], li[u], ri[u]);
-                double lv[4], rv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    lv[u] = Bd[li[u]];
-                    rv[u] = Bd[ri[u]];
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    c += lv[u];
-                    r -= rv[u];
-                }
-            }
-            for (; j < end; ++j) {
+            for (int j = beg; j < end; ++j) {
                 int li, ri;
                 decode(csr[j], li, ri);
                 c += Bd[li];
@@ -515,6 +502,36 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
             const int k = j - a.n_cr;
             a.send[a.t_dst[k]] = a.T[a.t_node[k]];
         }
+    }
+}
+
+// global-order host field -> rank-local T ring (all 3 buffers) and slot copies
+__global__ void scatter_init_kernel(int32_t n_nodes, const int32_t* local_global, const double* Tg, double* T0,
+                                    double* T1, double* T2) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_nodes; i += gridDim.x * blockDim.x) {
+        const double v = Tg[local_global[i]];
+        T0[i] = v;
+        T1[i] = v;
+        T2[i] = v;
+    }
+}
+__global__ void slot_init_kernel(int64_t n_slots, const int32_t* slot_node, const double* T, double* S0, double* S1) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_slots; s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t sn = slot_node[s];
+        const double v = sn >= 0 ? T[(uint32_t)sn & 0x0fffffffu] : 0.0;
+        S0[s] = v;
+        S1[s] = v;
+    }
+}
+// rank-local T (and H = enthalpy(T)) -> global order (blocked.hpp:686-691)
+template <bool TDEP>
+__global__ void gather_fields_kernel(int32_t n, const int32_t* local_global, const double* T, const uint8_t* reg,
+                                     const DevParams* P, double* Tg, double* Hg) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int32_t g = local_global[i];
+        const double t = T[i];
+        if (Tg) Tg[g] = t;
+        if (Hg) Hg[g] = dev_enthalpy<TDEP>(P, P->mat[reg[i]], t);
     }
 }
 

@@ -32,6 +32,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# host setup (mesh generation, validation, tiling) is OpenMP-parallel; torchrun
+# pins OMP_NUM_THREADS=1, so give each rank its share of the host cores
+if int(os.environ.get("WORLD_SIZE", "1")) > 1 or "OMP_NUM_THREADS" not in os.environ:
+    os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 8) // int(os.environ.get("WORLD_SIZE", "1"))))
 
 import numpy as np  # noqa: E402
 

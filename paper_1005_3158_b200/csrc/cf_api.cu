@@ -743,10 +743,9 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         CF_CUDA_CHECK(cudaSetDevice(o.device));
 
         MeshData m;
-        std::vector<Geom> geom;
-        finalize_mesh(mesh, m, &geom);
+        finalize_mesh(mesh, m);
         SetupData S;
-        resolve_setup(m, geom, setup, S);
+        resolve_setup(m, setup, S);
         if (o.world_size > 1 && S.temp_dep)
             raise(CF_CONFIG, "temperature-dependent tables (dynamic dt) need world_size == 1 in this build");
 
@@ -802,18 +801,19 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         CF_CUDA_CHECK(cudaEventCreate(&p->ev1));
         CF_CUDA_CHECK(cudaMalloc(&p->dP, sizeof(DevParams)));
         CF_CUDA_CHECK(cudaMemcpy(p->dP, &p->P, sizeof(DevParams), cudaMemcpyHostToDevice));
-        double e13 = INFINITY;
-        for (int64_t e = 0; e < m.E; ++e) {
-            const DevMaterial& mm = S.P.mat[m.region[e]];
-            const double c0 = pl_eval(S.P, mm.c, 0), k0 = pl_eval(S.P, mm.k, 0);
-            e13 = std::min(e13, mm.rho * c0 * geom[e].min_edge * geom[e].min_edge / k0);
+        double e13 = INFINITY;  // monotone in the minimum edge per region (see resolve_setup)
+        for (int32_t rg = 0; rg < (int32_t)m.region_min_edge.size(); ++rg) {
+            if (!std::isfinite(m.region_min_edge[rg])) continue;
+            const DevMaterial& mm = S.P.mat[rg];
+            const double c0 = pl_eval(S.P, mm.c, 0), k0 = pl_eval(S.P, mm.k, 0), me = m.region_min_edge[rg];
+            e13 = std::min(e13, mm.rho * c0 * me * me / k0);
         }
         p->eq13_min = e13;
         p->base_min_bound = S.min_bound;
         for (int r = o.rank; r < o.rank + o.local_ranks; ++r) {
             auto rk = std::make_unique<Rank>();
             rk->rank = r;
-            build_rank_plan(m, geom, S, po, label, r, rk->H);
+            build_rank_plan(m, S, po, label, r, rk->H);
             upload_rank(p.get(), *rk, S);
             p->ranks.push_back(std::move(rk));
         }
@@ -1140,7 +1140,7 @@ int cf_bandwidth(const cf_mesh_desc* d, const int32_t* perm, int64_t* out) {
 int cf_finalize_mesh(const cf_mesh_desc* d, int32_t* tets_out, int32_t* owner_out) {
     return guarded([&] {
         MeshData m;
-        finalize_mesh(d, m, nullptr);
+        finalize_mesh(d, m);
         if (tets_out) std::memcpy(tets_out, m.tets.data(), sizeof(int32_t) * m.tets.size());
         if (owner_out) std::memcpy(owner_out, m.owner.data(), sizeof(int32_t) * m.owner.size());
     });
@@ -1149,7 +1149,7 @@ int cf_finalize_mesh(const cf_mesh_desc* d, int32_t* tets_out, int32_t* owner_ou
 int cf_pair_sister_facets(const cf_mesh_desc* d, int32_t* out, int64_t cap, int64_t* n) {
     return guarded([&] {
         MeshData m;
-        finalize_mesh(d, m, nullptr);
+        finalize_mesh(d, m);
         const auto pairs = pair_sister_facets(m);
         if (n) *n = (int64_t)pairs.size();
         if (out)
@@ -1164,7 +1164,7 @@ int cf_pair_sister_facets(const cf_mesh_desc* d, int32_t* out, int64_t cap, int6
 int cf_partition_rcb(const cf_mesh_desc* d, int32_t parts, int32_t* out) {
     return guarded([&] {
         MeshData m;
-        finalize_mesh(d, m, nullptr);
+        finalize_mesh(d, m);
         const auto p = partition_rcb(m, parts);
         std::memcpy(out, p.data(), sizeof(int32_t) * p.size());
     });
@@ -1175,10 +1175,9 @@ int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_r
     return guarded([&] {
         if (!mesh || !setup || !opts || !tile_of_element) raise(CF_INVALID_ARG, "null argument");
         MeshData m;
-        std::vector<Geom> geom;
-        finalize_mesh(mesh, m, &geom);
+        finalize_mesh(mesh, m);
         SetupData S;
-        resolve_setup(m, geom, setup, S);
+        resolve_setup(m, setup, S);
         std::vector<int32_t> label(m.N);
         if (opts->node_order == CF_NODE_ORDER_RCM)
             label = rcm_permutation(build_node_graph(m.N, m.E, m.tets.data()), -1);
@@ -1202,7 +1201,7 @@ int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_r
         const int r0 = opts->rank, r1 = opts->local_ranks > 1 ? po.world_size : opts->rank + 1;
         for (int r = r0; r < r1; ++r) {
             RankPlan rp;
-            build_rank_plan(m, geom, S, po, label, r, rp);
+            build_rank_plan(m, S, po, label, r, rp);
             int64_t pos = 0;
             for (int32_t t = 0; t < rp.n_tiles; ++t)
                 for (int32_t i = 0; i < rp.tile_meta[t].ne; ++i) tile_of_element[rp.elem_global[pos++]] = base + t;
@@ -1218,10 +1217,9 @@ int cf_exchange_plan(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const
         if (!mesh || !setup || !opts || !n_nbrs) raise(CF_INVALID_ARG, "null argument");
         if (opts->world_size < 2) raise(CF_INVALID_ARG, "exchange plan needs world_size >= 2");
         MeshData m;
-        std::vector<Geom> geom;
-        finalize_mesh(mesh, m, &geom);
+        finalize_mesh(mesh, m);
         SetupData S;
-        resolve_setup(m, geom, setup, S);
+        resolve_setup(m, setup, S);
         std::vector<int32_t> label(m.N);
         std::iota(label.begin(), label.end(), 0);
         PlanOptions po;
@@ -1234,7 +1232,7 @@ int cf_exchange_plan(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const
                                         : partition_rcb(m, po.world_size);
         po.part_of_element = part.data();
         RankPlan rp;
-        build_rank_plan(m, geom, S, po, label, opts->rank, rp);
+        build_rank_plan(m, S, po, label, opts->rank, rp);
         *n_nbrs = (int32_t)rp.nbrs.size();
         int64_t os = 0, ot = 0, of = 0;
         for (size_t k = 0; k < rp.nbrs.size(); ++k) {

@@ -50,12 +50,15 @@ struct MeshData {
     std::vector<std::string> tags;
     std::vector<int32_t> contacts;    // [2C]
     int32_t region_count = 0;
+    std::vector<double> region_min_edge;  // per region: min element min_edge (static dt, Eq. 13)
     const double* pos(int32_t n) const { return coords + 3 * (size_t)n; }
+    Geom geometry(int64_t e) const;       // tet_geometry of the oriented element
 };
 
-// finalize_mesh: orientation, degeneracy, regions, facet owners. Geometry
-// is optionally returned (one Geom per element).
-void finalize_mesh(const cf_mesh_desc* d, MeshData& m, std::vector<Geom>* geom);
+// finalize_mesh: orientation, degeneracy, regions, facet owners, per-region
+// minimum edge. Geometry is recomputed per element where needed (build_rank_plan
+// only for the rank's own elements), so no O(E) geometry array is held.
+void finalize_mesh(const cf_mesh_desc* d, MeshData& m);
 
 struct Pair {
     int32_t facet, sister, contact;
@@ -135,7 +138,7 @@ struct SetupData {
     bool temp_dep = false;
     double min_bound = 0;               // min_e rho c l^2 / k before the safety factor
 };
-void resolve_setup(const MeshData& m, const std::vector<Geom>& geom, const cf_setup_desc* s, SetupData& out);
+void resolve_setup(const MeshData& m, const cf_setup_desc* s, SetupData& out);
 double pl_eval(const DevParams& P, const DevTable& t, double x);
 double enthalpy(const DevParams& P, const DevMaterial& m, double T);
 
@@ -196,8 +199,7 @@ struct PlanOptions {
 };
 
 // Builds rank `rank`'s tiles (build_worker_model blocked.hpp:156-361 recast).
-void build_rank_plan(const MeshData& m, const std::vector<Geom>& geom, const SetupData& S,
-                     const PlanOptions& o, const std::vector<int32_t>& node_label, int32_t rank,
-                     RankPlan& rp);
+void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o,
+                     const std::vector<int32_t>& node_label, int32_t rank, RankPlan& rp);
 
 }  // namespace cfb

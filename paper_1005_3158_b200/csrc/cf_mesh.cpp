@@ -127,7 +127,14 @@ struct FacetHash {
 };
 }  // namespace
 
-void finalize_mesh(const cf_mesh_desc* d, MeshData& m, std::vector<Geom>* geom) {
+Geom MeshData::geometry(int64_t e) const {
+    Geom g;
+    const int32_t* t = &tets[4 * (size_t)e];
+    tet_geometry(pos(t[0]), pos(t[1]), pos(t[2]), pos(t[3]), g);
+    return g;
+}
+
+void finalize_mesh(const cf_mesh_desc* d, MeshData& m) {
     if (!d || d->n_nodes < 0 || d->n_elems < 0 || d->n_facets < 0) raise(CF_INVALID_ARG, "bad mesh descriptor");
     if ((d->n_nodes && !d->coords) || (d->n_elems && (!d->tets || !d->region)) ||
         (d->n_facets && (!d->facets || !d->facet_tag)) || (d->n_tags && !d->tags) ||
@@ -149,8 +156,12 @@ void finalize_mesh(const cf_mesh_desc* d, MeshData& m, std::vector<Geom>* geom) 
         if (!std::isfinite(d->coords[i])) raise(CF_VALIDATION, "non-finite node coordinate");
 
     m.tets.resize(4 * (size_t)E);
-    if (geom) geom->resize(E);
     std::atomic<int64_t> bad_e{-1};
+    int32_t max_region = 0;
+    for (int64_t e = 0; e < E; ++e) max_region = std::max(max_region, d->region[e]);
+    const int nreg = max_region + 1;
+    const int nthr = omp_get_max_threads();
+    std::vector<double> tmin((size_t)nthr * nreg, INFINITY);
     std::atomic<int> bad_code{0};
     m.region_count = 0;
     int32_t rc = 0;
@@ -178,7 +189,8 @@ void finalize_mesh(const cf_mesh_desc* d, MeshData& m, std::vector<Geom>* geom) 
             if (dot3(e1, c) / 6.0 < 0) std::swap(t[2], t[3]);  // tet_signed_volume < 0 (mesh.hpp:170-172)
             Geom g;
             if (!tet_geometry(m.pos(t[0]), m.pos(t[1]), m.pos(t[2]), m.pos(t[3]), g)) code = 4;
-            if (geom) (*geom)[e] = g;
+            double& mn = tmin[(size_t)omp_get_thread_num() * nreg + d->region[e]];
+            mn = std::min(mn, g.min_edge);
         }
         if (code) {
             int64_t cur = bad_e.load();
@@ -188,6 +200,9 @@ void finalize_mesh(const cf_mesh_desc* d, MeshData& m, std::vector<Geom>* geom) 
         }
     }
     m.region_count = rc;
+    m.region_min_edge.assign(nreg, INFINITY);
+    for (int th = 0; th < nthr; ++th)
+        for (int r = 0; r < nreg; ++r) m.region_min_edge[r] = std::min(m.region_min_edge[r], tmin[(size_t)th * nreg + r]);
     if (bad_e >= 0) {
         // report the first offending element in element order (serial recheck)
         const int64_t e = bad_e;

@@ -80,7 +80,7 @@ bool name_eq(const char* a, const std::string& b) { return a && b == a; }
 
 }  // namespace
 
-void resolve_setup(const MeshData& m, const std::vector<Geom>& geom, const cf_setup_desc* s, SetupData& out) {
+void resolve_setup(const MeshData& m, const cf_setup_desc* s, SetupData& out) {
     if (!s) raise(CF_INVALID_ARG, "null setup");
     if ((s->n_materials && !s->materials) || (s->n_bcs && !s->bcs) || (s->n_coeffs && !s->coeffs))
         raise(CF_INVALID_ARG, "null array in setup descriptor");
@@ -248,14 +248,16 @@ void resolve_setup(const MeshData& m, const std::vector<Geom>& geom, const cf_se
         out.T0[n] = s->initial_T ? s->initial_T[n] : s->materials[m.node_region[n]].initial_temperature;
     for (int32_t n = 0; n < m.N; ++n)
         if (out.dir_of_node[n] >= 0) out.T0[n] = pl_eval(P, P.dir_tab[out.dir_of_node[n]], 0.0);
-    // static dt
+    // static dt (blocked.hpp:340-350): min_e rho c(0) l^2 / k(0). For constant
+    // properties the bound is monotone in the element's minimum edge (also
+    // under rounding), so the per-region minimum edge gives the exact minimum.
     if (!P.temp_dep) {
         double dt = INFINITY;
-#pragma omp parallel for reduction(min : dt)
-        for (int64_t e = 0; e < m.E; ++e) {
-            const DevMaterial& mm = P.mat[m.region[e]];
-            const double v = mm.rho * mm.c0 * geom[e].min_edge * geom[e].min_edge / mm.k0;
-            dt = std::min(dt, v);
+        for (int32_t r = 0; r < (int32_t)m.region_min_edge.size(); ++r) {
+            if (!std::isfinite(m.region_min_edge[r])) continue;
+            const DevMaterial& mm = P.mat[r];
+            const double me = m.region_min_edge[r];
+            dt = std::min(dt, mm.rho * mm.c0 * me * me / mm.k0);
         }
         out.min_bound = dt;
         P.static_dt = dt * s->dt_safety;
@@ -276,7 +278,7 @@ inline uint64_t spread21(uint64_t v) {
 }
 }  // namespace
 
-void build_rank_plan(const MeshData& m, const std::vector<Geom>& geom, const SetupData& S, const PlanOptions& o,
+void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o,
                      const std::vector<int32_t>& node_label, int32_t rank, RankPlan& rp) {
     rp = RankPlan{};
     rp.rank = rank;
@@ -534,7 +536,7 @@ void build_rank_plan(const MeshData& m, const std::vector<Geom>& geom, const Set
         for (int i = 0; i < ne; ++i) {
             const int32_t e = te[i];
             rp.elem_global[epos + i] = e;
-            const Geom& g = geom[e];
+            const Geom g = m.geometry(e);
             const double vals[11] = {g.g[1][0], g.g[1][1], g.g[1][2], g.g[2][0], g.g[2][1], g.g[2][2],
                                      g.g[3][0], g.g[3][1], g.g[3][2], g.vol,     g.max_edge};
             for (int k = 0; k < 11; ++k) gsec[(size_t)k * L.ne2 + i] = vals[k];

@@ -42,3 +42,17 @@ def test_library_is_sm100a_only():
     out = os.popen(f"cuobjdump --list-elf {_abi.LIB_PATH} 2>/dev/null").read()
     assert "sm_100a" in out
     assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_cpp_shim_compiles_standalone(tmp_path):
+    """include/castfem_b200.hpp compiles without the reference headers (templates over
+    the caller's types) and links against the C-ABI library."""
+    import subprocess
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "castfem_b200.hpp"\nint main() { return cf_abi_version() == 1 ? 0 : 1; }\n')
+    inc = os.path.join(os.path.dirname(HDR))
+    libdir = os.path.dirname(_abi.LIB_PATH)
+    r = subprocess.run(["g++", "-std=c++20", f"-I{inc}", str(src), "-o", str(tmp_path / "t"), f"-L{libdir}",
+                        "-lcastfem_b200", f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert subprocess.run([str(tmp_path / "t")]).returncode == 0

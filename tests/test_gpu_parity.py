@@ -155,3 +155,17 @@ def test_lambda_max_matches_oracle():
     lo, e13o = orc.lambda_max(case.mesh, case.setup, 300)
     assert abs(lam - lo) <= 1e-6 * lo
     assert e13 == e13o
+
+
+def test_cpp_drop_in_example():
+    """A reference user's C++ program: castfem::solve_serial vs castfem_b200::solve_gpu on the
+    reference's own Mesh / SimulationSetup objects (initial_override, Dirichlet f(t), c(T) table,
+    series, clamp accounting, reference exception types through the shim)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(orc.__file__), "_ref", "drop_in_example")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/drop_in_example not built (needs the reference headers at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "OK" in out.stdout

@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=None, help="cfg1..cfg5 (default: cfg2 at N=1, weak ladder at N>1)")
+    ap.add_argument("--casting", type=int, default=0, help="diagnostics: an n^3-cell casting instead of a config")
     ap.add_argument("--mode", default="deterministic", choices=["atomic", "deterministic"])
     ap.add_argument("--tile", type=int, default=384)
     ap.add_argument("--elem-order", default="morton")
@@ -67,8 +68,11 @@ def dist_env():
         os.environ.get("LOCAL_RANK", "0"))
 
 
-def make_case(cfg: str | None, world: int):
+def make_case(cfg: str | None, world: int, casting_n: int = 0):
     from paper_1005_3158_b200 import configs
+    if casting_n:
+        return configs.casting(casting_n, dt_safety=configs.DT_SAFETY["cfg2"], steps=100,
+                               name=f"casting{casting_n}"), f"casting{casting_n}", "weak"
     if cfg:
         return configs.CONFIGS[cfg](), cfg, "strong" if world > 1 else "weak"
     if world == 1:
@@ -192,7 +196,7 @@ def main():
         pg = dist
     from paper_1005_3158_b200 import castfem as cf
 
-    case, cfg, scaling = make_case(args.config, world)
+    case, cfg, scaling = make_case(args.config, world, args.casting)
     mesh, setup = case.mesh, case.setup
     comm = None
     if world > 1:

@@ -149,8 +149,10 @@ struct Rank {
     double2* part = nullptr;
     DevState* st = nullptr;
     int tile_grid = 0;
+    int ws_stages = 0;             // >0: warp-specialised producer/consumer tile kernel in use
     int32_t* all_list = nullptr;   // unused (NULL list = identity)
     int32_t* shared_list = nullptr;
+    int4* shared_rec = nullptr;     // packed update records of shared_list
     int32_t n_shared_list = 0;
     size_t tile_smem = 0;
     int upd_blocks = 0, upd_blocks_all = 0;
@@ -167,6 +169,7 @@ struct cf_plan {
     int mode = CF_MODE_ATOMIC;
     int tile_threads = 128;      // CTA size of the tile kernel (32 | 64 | 128 | 256)
     int stages = 1;              // 1: one tile per CTA; 2: persistent double-buffered TMA pipeline
+    int ws_stages = 0;           // warp-specialised pipeline depth (0: off, CF_TILE_WS=2|3; falls back per rank when it does not fit)
     int world = 1, first_rank = 0, local_ranks = 1;
     cf_comm* comm = nullptr;
     DevParams P{};
@@ -223,12 +226,45 @@ size_t tile_smem_bytes(const RankPlan& h, int stages) {
 #define CF_TILE_VARIANTS(X) \
     CF_TILE_VARIANTS_NT(X, 32) CF_TILE_VARIANTS_NT(X, 64) CF_TILE_VARIANTS_NT(X, 128) CF_TILE_VARIANTS_NT(X, 256)
 
+size_t ws_smem_bytes(const RankPlan& h, int ns) {
+    const size_t stage = 32 + (size_t)cf_round(h.max_blob, 16) + 8 * (size_t)h.max_slots;
+    return ns * stage + ns * 16 * (size_t)h.max_slots;
+}
+constexpr int kWsConsumerWarps = 8;
+
+#define CF_WS_VARIANTS(X)                                                                                   \
+    X(true, false, false, false, 2) X(true, false, false, false, 3) X(false, false, false, false, 2)         \
+    X(false, false, false, false, 3) X(true, false, true, false, 2) X(true, false, true, false, 3)           \
+    X(true, false, false, true, 2) X(true, false, true, true, 2) X(false, false, true, false, 2)            \
+    X(false, false, false, true, 2) X(false, false, true, true, 2) X(true, false, false, true, 3)            \
+    X(true, false, true, true, 3) X(false, false, true, false, 3) X(false, false, false, true, 3)           \
+    X(false, false, true, true, 3)
+
 void set_tile_attr(size_t smem) {
+#define CF_WSA(D, T, R, C, NS)                                                                                   \
+    CF_CUDA_CHECK(cudaFuncSetAttribute(tile_ws_kernel<D, T, R, C, kWsConsumerWarps, NS>,                         \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CF_WS_VARIANTS(CF_WSA)
+#undef CF_WSA
 #define CF_ATTR(D, T, R, C, NT)                                                                                  \
     CF_CUDA_CHECK(cudaFuncSetAttribute(tile_kernel<D, T, R, C, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                        (int)smem));
     CF_TILE_VARIANTS(CF_ATTR)
 #undef CF_ATTR
+}
+
+bool launch_tile_ws(cf_plan* p, Rank& r, const TileArgs& a) {
+    const bool det = p->mode == CF_MODE_DETERMINISTIC;
+    const bool dir = r.ua.node_dir != nullptr, cl = p->finite_range;
+    const dim3 grid(r.tile_grid), block((kWsConsumerWarps + 1) * 32);
+#define CF_WSL(D, T, R, C, NS)                                                                     \
+    if (det == D && !p->temp_dep && dir == R && cl == C && r.ws_stages == NS) {                    \
+        tile_ws_kernel<D, T, R, C, kWsConsumerWarps, NS><<<grid, block, r.tile_smem, p->stream>>>(a); \
+        return true;                                                                               \
+    }
+    CF_WS_VARIANTS(CF_WSL)
+#undef CF_WSL
+    return false;
 }
 
 void launch_tile(cf_plan* p, Rank& r, double t_end) {
@@ -242,6 +278,7 @@ void launch_tile(cf_plan* p, Rank& r, double t_end) {
     a.Tslot_n = r.Tslot[p->step_parity ^ 1];
     a.t_end = t_end;
     const bool dir = r.ua.node_dir != nullptr, cl = p->finite_range, td = p->temp_dep;
+    if (r.ws_stages && launch_tile_ws(p, r, a)) return;
     const int nt = p->tile_threads;
     const dim3 grid(r.tile_grid), block(nt);
 #define CF_LAUNCH(D, T, R, C, NT)                                                                  \
@@ -284,6 +321,7 @@ void launch_update(cf_plan* p, Rank& r, double t_end) {
         blocks = r.upd_blocks_all;
     } else {
         a.list = r.shared_list;
+        a.rec = r.shared_rec;
         a.n_list = r.n_shared_list;
         blocks = r.upd_blocks;
     }
@@ -397,6 +435,10 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     a.stages = p->stages;
     if (const char* e = std::getenv("CF_PROBE")) a.probe = std::atoi(e);
     r.tile_smem = tile_smem_bytes(h, p->stages);
+    if (p->ws_stages && ws_smem_bytes(h, p->ws_stages) <= 110 * 1024) {  // two CTAs per SM
+        r.ws_stages = p->ws_stages;
+        r.tile_smem = ws_smem_bytes(h, p->ws_stages);
+    }
     if (r.tile_smem > 220 * 1024) raise(CF_INVALID_ARG, "tile shared-memory footprint exceeds 220 KB; use smaller tiles");
     // the attribute is per function (shared by every plan and rank): the opt-in maximum;
     // occupancy follows the dynamic size passed at launch
@@ -412,6 +454,13 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
 #undef CF_OCC
         per_sm = std::max(1, per_sm);
         r.tile_grid = p->stages == 1 ? std::max(1, h.n_tiles) : std::max(1, std::min<int>(h.n_tiles, sms * per_sm));
+        if (r.ws_stages) {
+            CF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, tile_ws_kernel<true, false, false, false, kWsConsumerWarps, 2>, (kWsConsumerWarps + 1) * 32,
+                r.tile_smem));
+            per_sm = std::max(1, per_sm);
+            r.tile_grid = std::max(1, std::min<int>(h.n_tiles, sms * per_sm));
+        }
     }
 
     UpdArgs& u = r.ua;
@@ -429,6 +478,21 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     u.st = r.st;
     r.shared_list = M.up(h.shared_list, s);
     r.n_shared_list = (int32_t)h.shared_list.size();
+    {
+        std::vector<int4> rec(2 * std::max<size_t>(1, h.shared_list.size()));
+        for (size_t k = 0; k < h.shared_list.size(); ++k) {
+            const int32_t i = h.shared_list[k];
+            const int32_t b = h.merge_off[i], cnt = h.merge_off[i + 1] - b;
+            int32_t sl[4] = {0, 0, 0, 0};
+            for (int q = 0; q < 4 && q < cnt; ++q) sl[q] = h.merge_idx[b + q];
+            rec[2 * k] = make_int4(i, cnt, sl[0], sl[1]);
+            rec[2 * k + 1] = make_int4(sl[2], sl[3], 0, 0);
+        }
+        int4* d = M.alloc<int4>(rec.size());
+        CF_CUDA_CHECK(cudaMemcpyAsync(d, rec.data(), rec.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+        CF_CUDA_CHECK(cudaStreamSynchronize(s));
+        r.shared_rec = d;
+    }
     if (p->world > 1) {
         u.node_shared = M.up(h.node_shared, s);
         u.shared_off = M.up(h.shared_off, s);
@@ -469,7 +533,7 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-    r.upd_blocks = std::max(1, std::min<int>(sms * 8, (int)((r.n_shared_list + 255) / 256)));
+    r.upd_blocks = std::max(1, (int)((r.n_shared_list + 255) / 256));  // one record per thread
     r.upd_blocks_all = std::max(1, std::min<int>(sms * 8, (int)((h.n_local + 255) / 256)));
     // canonical algorithmic bytes: 105 E + 48 N + 24 F_bc + 56 F_if
     r.bytes_per_step = 105 * Er + 48 * (int64_t)h.n_local + 24 * h.n_bc_facets + 56 * h.n_if_facets;
@@ -785,6 +849,8 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
             p->tile_threads = (v == 32 || v == 64 || v == 128) ? v : 256;
         }
         if (const char* e = std::getenv("CF_TILE_STAGES")) p->stages = std::atoi(e) == 2 ? 2 : 1;
+        if (const char* e = std::getenv("CF_TILE_WS")) p->ws_stages = std::atoi(e) == 3 ? 3 : (std::atoi(e) == 2 ? 2 : 0);
+        if (S.temp_dep) p->ws_stages = 0;  // dynamic dt: no fused updates (tile_kernel path)
         p->world = o.world_size;
         p->first_rank = o.rank;
         p->local_ranks = o.local_ranks;

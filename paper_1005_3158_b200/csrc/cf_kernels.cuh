@@ -352,10 +352,251 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
     if (CLAMP && clamped) a.st->clamp_flag = 1;
 }
 
+// ------------------------------------------------------------------ warp-specialised tile kernel
+// Persistent producer/consumer pipeline (the default on large meshes):
+//  - warp NCW (producer): its 32 lanes prefetch the metadata of the next 32
+//    tiles, lane 0 streams each tile's blob + slot temperatures into a ring of
+//    NS shared-memory stages with TMA bulk copies on full[s] (complete_tx),
+//    after the consumers released the stage on empty[s];
+//  - warps 0..NCW-1 (consumers): the three phases of tile_kernel, separated by
+//    a named barrier among consumers only; they release a stage after a
+//    generic->async proxy fence (their contributions are written in place).
+// Consumers never wait on a copy that was not issued a full tile earlier.
+struct StageHdr {
+    TileMeta tm;
+    int32_t s0, t;
+    int32_t pad[2];
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <bool DET, bool TDEP, bool DIR, bool CLAMP, int NCW, int NS>
+__global__ void __launch_bounds__((NCW + 1) * 32) tile_ws_kernel(TileArgs a) {
+    constexpr bool FUSE = !TDEP;
+    constexpr int NC = NCW * 32;  // consumer threads
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t full[NS], empty[NS];
+    __shared__ DevMaterial sMat[kMaxRegions];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const DevParams* __restrict__ P = a.P;
+    // stage s: [StageHdr 32 B][blob blob_smem][T slots 8*max_slots]; then NS x (T,H) 16*max_slots
+    const size_t stage_bytes = 32 + (size_t)a.blob_smem + 8 * (size_t)a.max_slots;
+    double2* const sTHall = (double2*)(smem + NS * stage_bytes);
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+    }
+    for (int i = tid; i < P->n_materials; i += blockDim.x) sMat[i] = P->mat[i];
+    __syncthreads();
+
+    if (warp == NCW) {  // ---------------- producer warp
+        const int lane = tid & 31;
+        int k = 0;
+        for (int t0 = blockIdx.x; t0 < a.n_tiles; t0 += 32 * gridDim.x) {
+            const int tl = t0 + lane * gridDim.x;  // this lane prefetches tile tl's metadata
+            int ne = 0, ns = 0, nf = 0, ncsr = 0, s0 = 0;
+            long long boff = 0;
+            if (tl < a.n_tiles) {
+                const TileMeta m = a.meta[tl];
+                ne = m.ne;
+                ns = m.ns;
+                nf = m.nf;
+                ncsr = m.ncsr;
+                s0 = a.slot_off[tl];
+                boff = a.blob_off[tl];
+            }
+            for (int j = 0; j < 32; ++j) {
+                const int t = t0 + j * gridDim.x;
+                if (t >= a.n_tiles) break;
+                const TileMeta m{__shfl_sync(0xffffffffu, ne, j), __shfl_sync(0xffffffffu, ns, j),
+                                 __shfl_sync(0xffffffffu, nf, j), __shfl_sync(0xffffffffu, ncsr, j)};
+                const int ts0 = __shfl_sync(0xffffffffu, s0, j);
+                const long long tb = __shfl_sync(0xffffffffu, boff, j);
+                if (lane == 0) {
+                    const int s = k % NS;
+                    if (k >= NS) mbar_wait(&empty[s], ((k / NS) - 1) & 1);
+                    unsigned char* base = smem + (size_t)s * stage_bytes;
+                    StageHdr* hdr = (StageHdr*)base;
+                    hdr->tm = m;
+                    hdr->s0 = ts0;
+                    hdr->t = t;
+                    const TileLayout L(m, TDEP);
+                    const uint32_t tbytes = 8u * (uint32_t)cf_round(m.ns, 2);
+                    mbar_expect_tx(&full[s], (uint32_t)L.bytes + tbytes);
+                    const uint8_t* src = a.blob + tb;
+                    for (int64_t o = 0; o < L.bytes; o += kBulkChunk) {
+                        const uint32_t n = (uint32_t)(L.bytes - o < kBulkChunk ? L.bytes - o : kBulkChunk);
+                        bulk_g2s(base + 32 + o, src + o, n, &full[s]);
+                    }
+                    if (tbytes) bulk_g2s(base + 32 + a.blob_smem, a.Tslot + ts0, tbytes, &full[s]);
+                }
+                __syncwarp();
+                ++k;
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warps
+    double dt = 0, t_next = 0;
+    bool done = false;
+    if (FUSE) step_dt<TDEP>(P, a.st, a.t_end, dt, t_next, done);
+    const double time = a.st->time;
+    int clamped = 0;
+    double local_min = __longlong_as_double(0x7ff0000000000000ll);
+    int k = 0;
+    for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x, ++k) {
+        const int st = k % NS;
+        mbar_wait(&full[st], (k / NS) & 1);
+        unsigned char* base = smem + (size_t)st * stage_bytes;
+        const StageHdr hdr = *(const StageHdr*)base;
+        uint8_t* B = base + 32;
+        const double* sT = (const double*)(base + 32 + a.blob_smem);
+        double2* sTH = sTHall + (size_t)st * a.max_slots;
+        const TileMeta tm = hdr.tm;
+        const TileLayout L(tm, TDEP);
+        const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
+        const int s0 = hdr.s0;
+        const uint8_t* sinfo = B + L.sinfo;
+        // phase 1: (T, H) per slot
+        for (int s = tid; s < ns; s += NC) {
+            const double T = sT[s];
+            sTH[s] = make_double2(T, dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], T));
+        }
+        named_sync(1, NC);
+        // phase 2a: elements
+        double* G = (double*)(B + L.geom);
+        const int S = L.ne2;
+        const ushort4* conn = (const ushort4*)(B + L.conn);
+        const uint8_t* ereg = B + L.region;
+        for (int i = tid; i < ne; i += NC) {
+            double g[4][3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                g[1][c] = G[c * S + i];
+                g[2][c] = G[(3 + c) * S + i];
+                g[3][c] = G[(6 + c) * S + i];
+            }
+            const double vol = G[9 * S + i];
+            const double max_edge = G[10 * S + i];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) g[0][c] = ((g[1][c] + g[2][c]) + g[3][c]) * -1.0;
+            const ushort4 cn = conn[i];
+            const double2 th0 = sTH[cn.x], th1 = sTH[cn.y], th2 = sTH[cn.z], th3 = sTH[cn.w];
+            const double T[4] = {th0.x, th1.x, th2.x, th3.x};
+            const double H[4] = {th0.y, th1.y, th2.y, th3.y};
+            const DevMaterial& m = sMat[ereg[i]];
+            double lump, rc[4];
+            dev_element<TDEP>(P, m, g, vol, max_edge, T, H, lump, rc);
+            if (TDEP)
+                local_min = fmin(local_min, dev_stable_bound<TDEP>(P, m, ((const double*)(B + L.minedge))[i], T));
+            G[i] = lump;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) G[(1 + c) * S + i] = rc[c];
+        }
+        // phase 2b: facets
+        double* farea = (double*)(B + L.farea);
+        double* fsis = (double*)(B + L.fsister);
+        const ushort4* fsl = (const ushort4*)(B + L.fslots);
+        for (int i = tid; i < nf; i += NC) {
+            const ushort4 fs = fsl[i];
+            const DevFacetKind& K = P->kind[fs.w];
+            const double ts[3] = {sTH[fs.x].x, sTH[fs.y].x, sTH[fs.z].x};
+            double q, h, tinf;
+            if (K.interface) {
+                const double var = K.var == CF_VAR_TIME ? time : (ts[0] + ts[1] + ts[2]) / 3.0;
+                q = 0.0;
+                h = dev_pl_eval(P, K.htab, var);
+                const int4 sn = ((const int4*)fsis)[i];
+                double sum = 0;
+                sum += a.Told[sn.x];
+                sum += a.Told[sn.y];
+                sum += a.Told[sn.z];
+                sum += a.Told[sn.w];
+                tinf = 0.25 * sum;
+            } else {
+                q = K.q;
+                h = K.h;
+                tinf = K.t_inf;
+            }
+            const double third = farea[i] / 3.0;
+            const double f0 = third * (-q + h * (tinf - ts[0]));
+            const double f1 = third * (-q + h * (tinf - ts[1]));
+            const double f2 = third * (-q + h * (tinf - ts[2]));
+            farea[i] = -f0;
+            fsis[2 * i] = -f1;
+            fsis[2 * i + 1] = -f2;
+        }
+        named_sync(1, NC);
+        // phase 3: fixed-order reduction + flush
+        const uint16_t* cend = (const uint16_t*)(B + L.csr_end);
+        const uint16_t* csr = (const uint16_t*)(B + L.csr);
+        const int32_t* snode = (const int32_t*)(B + L.snode);
+        const int e4 = 4 * ne;
+        const double* Bd = (const double*)B;
+        const int gofs = (int)(L.geom >> 3), zofs = (int)(L.zero >> 3);
+        const int fa_ofs = (int)(L.farea >> 3), fs_ofs = (int)(L.fsister >> 3) - 1;
+        for (int s = tid; s < ns; s += NC) {
+            const int beg = s == 0 ? 0 : cend[s - 1];
+            const int end = cend[s];
+            double c = 0, r = 0;
+            for (int j = beg; j < end; ++j) {
+                const int code = csr[j];
+                const bool fac = code >= e4;
+                const int q = code & 3;
+                const int li = fac ? zofs : gofs + (code >> 2);
+                const int ri = fac ? (q == 0 ? fa_ofs + ((code - e4) >> 2) : fs_ofs + 2 * ((code - e4) >> 2) + q)
+                                   : gofs + (1 + q) * S + (code >> 2);
+                c += Bd[li];
+                r -= Bd[ri];
+            }
+            const int info = sinfo[s];
+            const int32_t node = snode[s];
+            if (FUSE && (info & 0x80)) {
+                double Tn;
+                if (done) {
+                    Tn = sTH[s].x;
+                } else {
+                    const int dir = (DIR && (info & 0x40)) ? a.node_dir[node] : -1;
+                    Tn = node_update<DIR, CLAMP>(P, a.st, sTH[s].x, c, r, dt, t_next, dir, info & 0x3f,
+                                                 a.local_global + node, clamped);
+                }
+                a.Tn[node] = Tn;
+                a.Tslot_n[s0 + s] = Tn;
+            } else if (DET) {
+                a.part[s0 + s] = make_double2(c, r);
+            } else {
+                atomicAdd(&a.acc_c[node], c);
+                atomicAdd(&a.acc_r[node], r);
+            }
+        }
+        // release the stage (generic-proxy writes ordered before the next TMA overwrite)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+    }
+    if (TDEP) {
+        for (int o = 16; o > 0; o >>= 1) local_min = fmin(local_min, __shfl_xor_sync(0xffffffffu, local_min, o));
+        if ((tid & 31) == 0) atomic_min_pos(&a.st->min_bound[a.st->step_index & 1], local_min);
+    }
+    if (CLAMP && clamped) a.st->clamp_flag = 1;
+}
+
 // ------------------------------------------------------------------ update kernel
 struct UpdArgs {
     int32_t n_list, n_local, n_ghost;
     const int32_t* list;  // nodes to merge + update (NULL: all local nodes)
+    const int4* rec;      // packed per listed node: {node, count, slot0, slot1}, {slot2, slot3, -, -}
+                          // (count > 4: slots via merge_off/merge_idx); NULL: use list + merge CSR
     const double* T;      // current (ghost slots written here)
     double* Tn;           // next
     const int32_t* merge_off;
@@ -405,15 +646,47 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
     int clamped = 0;
     const int stride = gridDim.x * blockDim.x;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n_list; k += stride) {
-        const int i = a.list ? a.list[k] : k;
+        int i, cnt = -1;
+        int4 r0, r1;
+        if (a.rec) {  // one coalesced 32-byte record: node + up to 4 slot (= partial) indices
+            r0 = a.rec[2 * k];
+            r1 = a.rec[2 * k + 1];
+            i = r0.x;
+            cnt = r0.y;
+        } else {
+            i = a.list ? a.list[k] : k;
+        }
+        const int sl[4] = {r0.z, r0.w, r1.x, r1.y};
+        const bool packed = cnt >= 0 && cnt <= 4;
         const double T = a.T[i];
         if (done) {
             a.Tn[i] = T;
-            for (int j = a.merge_off[i]; j < a.merge_off[i + 1]; ++j) a.Tslot_n[a.merge_idx[j]] = T;
+            if (packed) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (q < cnt) a.Tslot_n[sl[q]] = T;
+            } else {
+                for (int j = a.merge_off[i]; j < a.merge_off[i + 1]; ++j) a.Tslot_n[a.merge_idx[j]] = T;
+            }
             continue;
         }
         double c, r;
-        own_partial<DET>(a, i, c, r);
+        if (DET && packed) {
+            // all partial loads issued before the in-order (ascending tile) sums
+            double2 pr[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pr[q] = q < cnt ? a.part[sl[q]] : make_double2(0.0, 0.0);
+            c = 0;
+            r = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (q < cnt) {
+                    c += pr[q].x;
+                    r += pr[q].y;
+                }
+        } else {
+            own_partial<DET>(a, i, c, r);
+        }
         if (!DET) {
             a.acc_c[i] = 0;
             a.acc_r[i] = 0;
@@ -442,7 +715,13 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         const double Tn = node_update<DIR, CLAMP>(P, a.st, T, c, r, dt, t_next, DIR ? a.node_dir[i] : -1,
                                                   CLAMP ? a.node_region[i] : 0, a.local_global + i, clamped);
         a.Tn[i] = Tn;
-        for (int j = a.merge_off[i]; j < a.merge_off[i + 1]; ++j) a.Tslot_n[a.merge_idx[j]] = Tn;
+        if (packed) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (q < cnt) a.Tslot_n[sl[q]] = Tn;
+        } else {
+            for (int j = a.merge_off[i]; j < a.merge_off[i + 1]; ++j) a.Tslot_n[a.merge_idx[j]] = Tn;
+        }
     }
     if (MULTI)
         for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < a.n_ghost; g += stride)

@@ -169,3 +169,42 @@ def test_cpp_drop_in_example():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "OK" in out.stdout
+
+
+# ---------------------------------------------------------------- BASELINE sizes
+@pytest.mark.slow
+def test_cfg1_full_size_vs_oracle():
+    """BASELINE configs[0]: 32^3 cube, 100 steps, dt = 0.9 x 2/lambda_max."""
+    case = configs.config1(32)
+    det, ref = run_pair(case, case.steps, tile_elems=384)
+    assert np.array_equal(det.T, ref.T)
+    assert det.steps == 100
+    one = orc.solve(case.mesh, case.setup, case.steps)
+    assert rel(det.T, one.T) <= RTOL
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_vs_reference_truncated():
+    """BASELINE configs[1] (12.6 M tets): 10 steps against the reference solver itself."""
+    if not orc.ref_available():
+        pytest.skip("oracle/_ref not built")
+    case = configs.config2()
+    gpu = cf.solve(case.mesh, case.setup, cf.SolveOptions(max_steps=10))
+    rb = orc.RefBench(case.mesh, case.setup)
+    rb.steps(10)
+    ref = rb.T()
+    rb.close()
+    assert rel(gpu.T, ref) <= RTOL
+
+
+@pytest.mark.slow
+def test_cfg2_bit_reproducible_run_to_run():
+    case = configs.config2()
+    with cf.Solver(case.mesh, case.setup) as s:
+        s.step(50)
+        a, _ = s.fields(False)
+        s.set_temperature(case.setup.initial_T)
+        s.step(50)
+        b, _ = s.fields(False)
+    assert np.array_equal(a, b)
+    assert np.isfinite(a).all() and 299.0 < a.min() and a.max() < 975.0

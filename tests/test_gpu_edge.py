@@ -1,0 +1,89 @@
+"""Edge cases through the C-ABI on the GPU, each against the CPU oracle
+(replaying the GPU's tiles, so deterministic mode must match bit for bit)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_1005_3158_b200 import castfem as cf
+from paper_1005_3158_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+
+def check(m, s, steps, **kw):
+    opts = cf.SolveOptions(max_steps=steps, **kw)
+    gpu = cf.solve(m, s, opts)
+    tiles, _ = cf.tile_map(m, s, opts)
+    ref = orc.solve(m, s, steps, blocks=tiles)
+    assert np.array_equal(gpu.T, ref.T), np.abs(gpu.T - ref.T).max()
+    assert np.array_equal(gpu.H, ref.H)
+    assert gpu.end_time == ref.time and gpu.steps == ref.steps
+    return gpu, ref
+
+
+def test_single_tet_all_faces_convective():
+    nodes = [[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]]
+    faces = [[1, 2, 3], [0, 2, 3], [0, 1, 3], [0, 1, 2]]
+    m = cf.Mesh(nodes, [[0, 1, 2, 3]], [0], faces, [0, 0, 0, 0], ["skin"])
+    s = cf.SimulationSetup(materials=[cf.MaterialTable.make(1000.0, 500.0, 10.0, T0=400.0)],
+                           boundary_conditions={"skin": cf.BoundaryCondition("flux", q=5.0, h=30.0, t_inf=300.0)},
+                           solver=cf.SolverConfig(dt_safety=0.2), initial_T=np.array([400.0, 410.0, 390.0, 405.0]))
+    gpu, _ = check(m, s, 25)
+    assert np.all(np.diff(gpu.T) != 0)
+
+
+def test_adiabatic_conservation():
+    """No boundary facets: sum_i C_i (T_i' - T_i) = 0, C from the oracle's own lumping."""
+    c = configs.config1(n=6)
+    m = cf.Mesh(c.mesh.nodes, c.mesh.tets, c.mesh.region, np.zeros((0, 3)), np.zeros(0), [])
+    s = cf.SimulationSetup(materials=c.setup.materials, solver=c.setup.solver, initial_T=c.setup.initial_T)
+    gpu, _ = check(m, s, 10)
+    tets, _ = cf.finalize_mesh(m)
+    p = m.nodes[tets]
+    V = np.einsum("ij,ij->i", p[:, 1] - p[:, 0], np.cross(p[:, 2] - p[:, 0], p[:, 3] - p[:, 0])) / 6
+    Cn = np.zeros(m.node_count())
+    np.add.at(Cn, tets.reshape(-1), np.repeat(2700.0 * 900.0 * V / 4, 4))
+    assert abs(np.sum(Cn * (gpu.T - s.initial_T))) <= 1e-11 * np.sum(Cn * s.initial_T)
+
+
+def test_region_gap_and_unused_material_slot():
+    c = configs.casting(8, dt_safety=0.14)
+    m = c.mesh
+    m.region = np.where(m.region == 1, 2, 0).astype(np.int32)          # regions 0 and 2
+    mats = [c.setup.materials[0], cf.MaterialTable(), c.setup.materials[1]]  # slot 1 untouched (rho 0)
+    s = cf.SimulationSetup(materials=mats, boundary_conditions=c.setup.boundary_conditions,
+                           interface_coeffs=c.setup.interface_coeffs, solver=c.setup.solver,
+                           initial_T=c.setup.initial_T)
+    check(m, s, 20)
+
+
+def test_two_contacts_and_duplicate_facet_records():
+    c = configs.casting(8, dt_safety=0.14)
+    m = c.mesh
+    # split the interface tags in two halves (x < 0.5 / x >= 0.5): two contact declarations
+    cen = m.nodes[m.facets].mean(axis=1)
+    tag = m.facet_tag.copy()
+    tag[(tag == 1) & (cen[:, 0] >= 0.5)] = 3
+    tag[(tag == 2) & (cen[:, 0] >= 0.5)] = 4
+    # duplicate the first outer facet record (the reference accumulates it twice)
+    first_outer = int(np.where(tag == 0)[0][0])
+    facets = np.vstack([m.facets, m.facets[first_outer:first_outer + 1]])
+    tag = np.concatenate([tag, [0]]).astype(np.int32)
+    m2 = cf.Mesh(m.nodes, m.tets, m.region, facets, tag, ["outer", "cast_if", "mold_if", "cast_if2", "mold_if2"],
+                 [(1, 2), (3, 4)])
+    s = cf.SimulationSetup(materials=c.setup.materials, boundary_conditions=c.setup.boundary_conditions,
+                           interface_coeffs=[c.setup.interface_coeffs[0],
+                                             cf.InterfaceCoeff("mold_if2", "cast_if2", "temperature",
+                                                               cf.PiecewiseLinear([300.0, 1000.0], [400.0, 3000.0]))],
+                           solver=c.setup.solver, initial_T=c.setup.initial_T)
+    check(m2, s, 20)
+    if orc.ref_available():
+        r, _ = orc.ref_solve(m2, s, 20)
+        assert np.array_equal(orc.solve(m2, s, 20).T, r.T)
+
+
+def test_empty_mesh():
+    m = cf.Mesh(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros(0), np.zeros((0, 3)), np.zeros(0), [])
+    s = cf.SimulationSetup(materials=[cf.MaterialTable.make(1.0, 1.0, 1.0)], solver=cf.SolverConfig(dt_safety=0.5))
+    res = cf.solve(m, s, cf.SolveOptions(max_steps=3))
+    assert res.T.shape == (0,) and res.steps == 3

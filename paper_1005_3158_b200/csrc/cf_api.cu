@@ -170,6 +170,7 @@ struct cf_plan {
     int tile_threads = 128;      // CTA size of the tile kernel (32 | 64 | 128 | 256)
     int stages = 1;              // 1: one tile per CTA; 2: persistent double-buffered TMA pipeline
     int ws_stages = 0;           // warp-specialised pipeline depth (0: off, CF_TILE_WS=2|3; falls back per rank when it does not fit)
+    int ws_warps = 8;            // consumer warps of the warp-specialised kernel (CF_WS_WARPS=4|8)
     int world = 1, first_rank = 0, local_ranks = 1;
     cf_comm* comm = nullptr;
     DevParams P{};
@@ -230,19 +231,20 @@ size_t ws_smem_bytes(const RankPlan& h, int ns) {
     const size_t stage = 32 + (size_t)cf_round(h.max_blob, 16) + 8 * (size_t)h.max_slots;
     return ns * stage + ns * 16 * (size_t)h.max_slots;
 }
-constexpr int kWsConsumerWarps = 8;
+constexpr int kWsConsumerWarps = 8;  // CF_WS_WARPS=4 selects the 4-warp variant
 
-#define CF_WS_VARIANTS(X)                                                                                   \
-    X(true, false, false, false, 2) X(true, false, false, false, 3) X(false, false, false, false, 2)         \
-    X(false, false, false, false, 3) X(true, false, true, false, 2) X(true, false, true, false, 3)           \
-    X(true, false, false, true, 2) X(true, false, true, true, 2) X(false, false, true, false, 2)            \
-    X(false, false, false, true, 2) X(false, false, true, true, 2) X(true, false, false, true, 3)            \
-    X(true, false, true, true, 3) X(false, false, true, false, 3) X(false, false, false, true, 3)           \
-    X(false, false, true, true, 3)
+#define CF_WS_VARIANTS_W(X, W)                                                                              \
+    X(true, false, false, false, 2, W) X(true, false, false, false, 3, W) X(false, false, false, false, 2, W) \
+    X(false, false, false, false, 3, W) X(true, false, true, false, 2, W) X(true, false, true, false, 3, W)   \
+    X(true, false, false, true, 2, W) X(true, false, true, true, 2, W) X(false, false, true, false, 2, W)    \
+    X(false, false, false, true, 2, W) X(false, false, true, true, 2, W) X(true, false, false, true, 3, W)    \
+    X(true, false, true, true, 3, W) X(false, false, true, false, 3, W) X(false, false, false, true, 3, W)   \
+    X(false, false, true, true, 3, W)
+#define CF_WS_VARIANTS(X) CF_WS_VARIANTS_W(X, 4) CF_WS_VARIANTS_W(X, 8)
 
 void set_tile_attr(size_t smem) {
-#define CF_WSA(D, T, R, C, NS)                                                                                   \
-    CF_CUDA_CHECK(cudaFuncSetAttribute(tile_ws_kernel<D, T, R, C, kWsConsumerWarps, NS>,                         \
+#define CF_WSA(D, T, R, C, NS, W)                                                                                \
+    CF_CUDA_CHECK(cudaFuncSetAttribute(tile_ws_kernel<D, T, R, C, W, NS>,                                        \
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CF_WS_VARIANTS(CF_WSA)
 #undef CF_WSA
@@ -256,10 +258,10 @@ void set_tile_attr(size_t smem) {
 bool launch_tile_ws(cf_plan* p, Rank& r, const TileArgs& a) {
     const bool det = p->mode == CF_MODE_DETERMINISTIC;
     const bool dir = r.ua.node_dir != nullptr, cl = p->finite_range;
-    const dim3 grid(r.tile_grid), block((kWsConsumerWarps + 1) * 32);
-#define CF_WSL(D, T, R, C, NS)                                                                     \
-    if (det == D && !p->temp_dep && dir == R && cl == C && r.ws_stages == NS) {                    \
-        tile_ws_kernel<D, T, R, C, kWsConsumerWarps, NS><<<grid, block, r.tile_smem, p->stream>>>(a); \
+    const dim3 grid(r.tile_grid), block((p->ws_warps + 1) * 32);
+#define CF_WSL(D, T, R, C, NS, W)                                                                  \
+    if (det == D && !p->temp_dep && dir == R && cl == C && r.ws_stages == NS && p->ws_warps == W) { \
+        tile_ws_kernel<D, T, R, C, W, NS><<<grid, block, r.tile_smem, p->stream>>>(a);             \
         return true;                                                                               \
     }
     CF_WS_VARIANTS(CF_WSL)
@@ -435,7 +437,7 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     a.stages = p->stages;
     if (const char* e = std::getenv("CF_PROBE")) a.probe = std::atoi(e);
     r.tile_smem = tile_smem_bytes(h, p->stages);
-    if (p->ws_stages && ws_smem_bytes(h, p->ws_stages) <= 110 * 1024) {  // two CTAs per SM
+    if (p->ws_stages && ws_smem_bytes(h, p->ws_stages) <= (p->ws_warps == 4 ? 55 : 110) * 1024) {
         r.ws_stages = p->ws_stages;
         r.tile_smem = ws_smem_bytes(h, p->ws_stages);
     }
@@ -455,9 +457,12 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
         per_sm = std::max(1, per_sm);
         r.tile_grid = p->stages == 1 ? std::max(1, h.n_tiles) : std::max(1, std::min<int>(h.n_tiles, sms * per_sm));
         if (r.ws_stages) {
-            CF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, tile_ws_kernel<true, false, false, false, kWsConsumerWarps, 2>, (kWsConsumerWarps + 1) * 32,
-                r.tile_smem));
+            if (p->ws_warps == 4)
+                CF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                    &per_sm, tile_ws_kernel<true, false, false, false, 4, 2>, 5 * 32, r.tile_smem));
+            else
+                CF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                    &per_sm, tile_ws_kernel<true, false, false, false, 8, 2>, 9 * 32, r.tile_smem));
             per_sm = std::max(1, per_sm);
             r.tile_grid = std::max(1, std::min<int>(h.n_tiles, sms * per_sm));
         }
@@ -851,6 +856,7 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         if (const char* e = std::getenv("CF_TILE_STAGES")) p->stages = std::atoi(e) == 2 ? 2 : 1;
         if (const char* e = std::getenv("CF_TILE_WS")) p->ws_stages = std::atoi(e) == 3 ? 3 : (std::atoi(e) == 2 ? 2 : 0);
         if (S.temp_dep) p->ws_stages = 0;  // dynamic dt: no fused updates (tile_kernel path)
+        if (const char* e = std::getenv("CF_WS_WARPS")) p->ws_warps = std::atoi(e) == 4 ? 4 : 8;
         p->world = o.world_size;
         p->first_rank = o.rank;
         p->local_ranks = o.local_ranks;

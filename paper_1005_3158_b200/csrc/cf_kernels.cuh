@@ -376,7 +376,7 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 }
 
 template <bool DET, bool TDEP, bool DIR, bool CLAMP, int NCW, int NS>
-__global__ void __launch_bounds__((NCW + 1) * 32) tile_ws_kernel(TileArgs a) {
+__global__ void __launch_bounds__((NCW + 1) * 32, NCW == 4 ? 4 : 1) tile_ws_kernel(TileArgs a) {
     constexpr bool FUSE = !TDEP;
     constexpr int NC = NCW * 32;  // consumer threads
     extern __shared__ __align__(16) unsigned char smem[];

@@ -24,6 +24,7 @@ import argparse
 import json
 import math
 import os
+import resource
 import statistics
 import subprocess
 import sys
@@ -308,6 +309,7 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(st.launches_per_step * args.steps), "clocks": clocks,
                 "device_bytes": int(st.device_bytes), "tiles": int(st.n_tiles),
+                "host_peak_rss_gb": round(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20, 2),
                 "total_slots": int(st.total_slots)}
         print(json.dumps(line), flush=True)
     solver.close()

@@ -117,8 +117,8 @@ struct DeviceMem {
         bytes += (int64_t)(n * sizeof(T));
         return (T*)p;
     }
-    template <class T>
-    T* up(const std::vector<T>& v, cudaStream_t s) {
+    template <class T, class A>
+    T* up(const std::vector<T, A>& v, cudaStream_t s) {
         T* p = alloc<T>(v.size());
         if (!v.empty()) CF_CUDA_CHECK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
         return p;
@@ -544,7 +544,7 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     r.bytes_per_step = 105 * Er + 48 * (int64_t)h.n_local + 24 * h.n_bc_facets + 56 * h.n_if_facets;
     CF_CUDA_CHECK(cudaStreamSynchronize(s));
     // drop the big host arrays (metadata kept)
-    std::vector<uint8_t>().swap(h.blob);
+    decltype(h.blob)().swap(h.blob);
     std::vector<int32_t>().swap(h.merge_idx);
 }
 
@@ -811,10 +811,12 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         if (o.device < 0 || o.device >= ndev) raise(CF_INVALID_ARG, "bad device ordinal");
         CF_CUDA_CHECK(cudaSetDevice(o.device));
 
+        trace_stage("plan_create: start");
         MeshData m;
         finalize_mesh(mesh, m);
         SetupData S;
         resolve_setup(m, setup, S);
+        trace_stage("resolve: rest");
         if (o.world_size > 1 && S.temp_dep)
             raise(CF_CONFIG, "temperature-dependent tables (dynamic dt) need world_size == 1 in this build");
 
@@ -845,6 +847,7 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
             }
             po.part_of_element = part.data();
         }
+        trace_stage("labels + partition");
 
         auto p = std::make_unique<cf_plan>();
         p->device = o.device;
@@ -887,11 +890,13 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
             rk->rank = r;
             build_rank_plan(m, S, po, label, r, rk->H);
             upload_rank(p.get(), *rk, S);
+            trace_stage("upload");
             p->ranks.push_back(std::move(rk));
         }
         p->launches_per_step = 2 * (int64_t)p->ranks.size() + (p->world > 1 ? (int64_t)p->ranks.size() : 0);
         init_state(p.get(), S.T0.data());
         CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+        trace_stage("init state");
         *out = p.release();
     });
 }
@@ -1288,10 +1293,12 @@ int cf_exchange_plan(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const
     return guarded([&] {
         if (!mesh || !setup || !opts || !n_nbrs) raise(CF_INVALID_ARG, "null argument");
         if (opts->world_size < 2) raise(CF_INVALID_ARG, "exchange plan needs world_size >= 2");
+        trace_stage("exchange_plan: start");
         MeshData m;
         finalize_mesh(mesh, m);
         SetupData S;
         resolve_setup(m, setup, S);
+        trace_stage("resolve: rest");
         std::vector<int32_t> label(m.N);
         std::iota(label.begin(), label.end(), 0);
         PlanOptions po;
@@ -1302,6 +1309,7 @@ int cf_exchange_plan(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const
         std::vector<int32_t> part = opts->partition == CF_PARTITION_GIVEN && opts->part_of_element
                                         ? std::vector<int32_t>(opts->part_of_element, opts->part_of_element + m.E)
                                         : partition_rcb(m, po.world_size);
+        trace_stage("partition");
         po.part_of_element = part.data();
         RankPlan rp;
         build_rank_plan(m, S, po, label, opts->rank, rp);

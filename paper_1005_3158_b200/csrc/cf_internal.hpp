@@ -10,6 +10,8 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "../../include/castfem_b200.h"
@@ -17,12 +19,32 @@
 
 namespace cfb {
 
+// allocator that leaves trivially constructible elements uninitialised, so big
+// host staging buffers are first touched by the parallel loops that fill them
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = UninitAlloc<U>;
+    };
+    UninitAlloc() = default;
+    template <class U>
+    UninitAlloc(const UninitAlloc<U>&) {}
+    template <class U>
+    void construct(U* p) { ::new ((void*)p) U; }
+    template <class U, class... A>
+    void construct(U* p, A&&... a) { ::new ((void*)p) U(std::forward<A>(a)...); }
+};
+
 // Exception carrying a CF_* status; mapped at the C-ABI edge.
 struct Error : std::runtime_error {
     int code;
     Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 [[noreturn]] inline void raise(int code, const std::string& msg) { throw Error(code, msg); }
+
+// CF_TRACE_SETUP=1: host setup stage times on stderr (diagnostics only).
+void trace_stage(const char* name);
 
 void set_last_error(const std::string& msg);
 
@@ -41,7 +63,7 @@ void triangle_centroid(const double* a, const double* b, const double* c, double
 struct MeshData {
     int32_t N = 0, E = 0, F = 0;
     const double* coords = nullptr;   // caller's [3N]
-    std::vector<int32_t> tets;        // oriented [4E]
+    std::vector<int32_t, UninitAlloc<int32_t>> tets;        // oriented [4E]
     const int32_t* region = nullptr;  // caller's [E]
     const int32_t* facets = nullptr;  // caller's [3F]
     const int32_t* facet_tag = nullptr;
@@ -158,7 +180,7 @@ struct RankPlan {
     std::vector<TileMeta> tile_meta;       // [n_tiles] ne, ns, nf, ncsr
     std::vector<int32_t> tile_slot_off;    // [n_tiles+1]
     std::vector<int64_t> blob_off;         // [n_tiles+1] byte offsets into blob
-    std::vector<uint8_t> blob;             // all tile blobs
+    std::vector<uint8_t, UninitAlloc<uint8_t>> blob;  // all tile blobs
     int32_t max_slots = 0, max_elems = 0, max_facets = 0;
     int64_t max_blob = 0;
     std::vector<int32_t> elem_global;      // [E_r] tile order

@@ -11,9 +11,13 @@
 // plus builder-written pieces the reference lacks: RCB partitioning and the
 // structured Kuhn fixtures.
 #include <omp.h>
+#include <parallel/algorithm>
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -78,6 +82,15 @@ double triangle_area(const double* a, const double* b, const double* c) {
 }
 void triangle_centroid(const double* a, const double* b, const double* c, double* out) {
     for (int k = 0; k < 3; ++k) out[k] = ((a[k] + b[k]) + c[k]) * (1.0 / 3.0);
+}
+
+void trace_stage(const char* name) {
+    static const bool on = std::getenv("CF_TRACE_SETUP") && std::atoi(std::getenv("CF_TRACE_SETUP"));
+    static auto last = std::chrono::steady_clock::now();
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cf setup] %-24s %8.3f s\n", name, std::chrono::duration<double>(now - last).count());
+    last = now;
 }
 
 // ------------------------------------------------------------------ finalize
@@ -165,39 +178,44 @@ void finalize_mesh(const cf_mesh_desc* d, MeshData& m) {
     std::atomic<int> bad_code{0};
     m.region_count = 0;
     int32_t rc = 0;
-#pragma omp parallel for schedule(static) reduction(max : rc)
-    for (int64_t e = 0; e < E; ++e) {
-        int32_t* t = &m.tets[4 * (size_t)e];
-        int code = 0;
-        for (int a = 0; a < 4; ++a) {
-            t[a] = d->tets[4 * (size_t)e + a];
-            if (t[a] < 0 || t[a] >= N) code = 1;
-        }
-        if (!code)
-            for (int a = 0; a < 4; ++a)
-                for (int b = a + 1; b < 4; ++b)
-                    if (t[a] == t[b]) code = 2;
-        if (!code && d->region[e] < 0) code = 3;
-        if (!code) {
-            rc = std::max(rc, d->region[e] + 1);
-            const double *p0 = m.pos(t[0]), *p1 = m.pos(t[1]), *p2 = m.pos(t[2]), *p3 = m.pos(t[3]);
-            double e1[3], e2[3], e3[3], c[3];
-            sub3(p1, p0, e1);
-            sub3(p2, p0, e2);
-            sub3(p3, p0, e3);
-            cross3(e2, e3, c);
-            if (dot3(e1, c) / 6.0 < 0) std::swap(t[2], t[3]);  // tet_signed_volume < 0 (mesh.hpp:170-172)
-            Geom g;
-            if (!tet_geometry(m.pos(t[0]), m.pos(t[1]), m.pos(t[2]), m.pos(t[3]), g)) code = 4;
-            double& mn = tmin[(size_t)omp_get_thread_num() * nreg + d->region[e]];
-            mn = std::min(mn, g.min_edge);
-        }
-        if (code) {
-            int64_t cur = bad_e.load();
-            while ((cur < 0 || e < cur) && !bad_e.compare_exchange_weak(cur, e)) {
+#pragma omp parallel reduction(max : rc)
+    {
+        std::vector<double> loc(nreg, INFINITY);  // per-thread minima (no shared cache lines)
+#pragma omp for schedule(static)
+        for (int64_t e = 0; e < E; ++e) {
+            int32_t* t = &m.tets[4 * (size_t)e];
+            int code = 0;
+            for (int a = 0; a < 4; ++a) {
+                t[a] = d->tets[4 * (size_t)e + a];
+                if (t[a] < 0 || t[a] >= N) code = 1;
             }
-            if (bad_e.load() == e) bad_code = code;
+            if (!code)
+                for (int a = 0; a < 4; ++a)
+                    for (int b = a + 1; b < 4; ++b)
+                        if (t[a] == t[b]) code = 2;
+            if (!code && d->region[e] < 0) code = 3;
+            if (!code) {
+                rc = std::max(rc, d->region[e] + 1);
+                const double *p0 = m.pos(t[0]), *p1 = m.pos(t[1]), *p2 = m.pos(t[2]), *p3 = m.pos(t[3]);
+                double e1[3], e2[3], e3[3], c[3];
+                sub3(p1, p0, e1);
+                sub3(p2, p0, e2);
+                sub3(p3, p0, e3);
+                cross3(e2, e3, c);
+                if (dot3(e1, c) / 6.0 < 0) std::swap(t[2], t[3]);  // tet_signed_volume < 0 (mesh.hpp:170-172)
+                Geom g;
+                if (!tet_geometry(m.pos(t[0]), m.pos(t[1]), m.pos(t[2]), m.pos(t[3]), g)) code = 4;
+                double& mn = loc[d->region[e]];
+                mn = std::min(mn, g.min_edge);
+            }
+            if (code) {
+                int64_t cur = bad_e.load();
+                while ((cur < 0 || e < cur) && !bad_e.compare_exchange_weak(cur, e)) {
+                }
+                if (bad_e.load() == e) bad_code = code;
+            }
         }
+        for (int r = 0; r < nreg; ++r) tmin[(size_t)omp_get_thread_num() * nreg + r] = loc[r];
     }
     m.region_count = rc;
     m.region_min_edge.assign(nreg, INFINITY);
@@ -219,6 +237,7 @@ void finalize_mesh(const cf_mesh_desc* d, MeshData& m) {
         raise(CF_DEGENERATE, "element " + std::to_string(e) + ": degenerate tetrahedron");
     }
 
+    trace_stage("finalize: geometry");
     // node_regions (mesh.hpp:129-144)
     m.node_region.assign(N, -1);
     for (int64_t e = 0; e < E; ++e)
@@ -240,6 +259,7 @@ void finalize_mesh(const cf_mesh_desc* d, MeshData& m) {
                 raise(CF_VALIDATION, "facet " + std::to_string(f) + " references node " + std::to_string(n) +
                                          " outside [0, " + std::to_string(N) + ")");
         }
+    trace_stage("finalize: node regions");
     m.owner.assign(F, -1);
     if (F > 0) {
         FacetHash H;
@@ -251,10 +271,16 @@ void finalize_mesh(const cf_mesh_desc* d, MeshData& m) {
             own[f] = INT32_MAX;
         }
         static const int tf[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
+        // only faces whose three nodes all lie on some facet can match one
+        std::vector<uint8_t> on_facet(N, 0);
+        for (int64_t i = 0; i < 3 * F; ++i) on_facet[d->facets[i]] = 1;
 #pragma omp parallel for schedule(static)
         for (int64_t e = 0; e < E; ++e) {
             const int32_t* t = &m.tets[4 * (size_t)e];
+            const int on = on_facet[t[0]] + on_facet[t[1]] + on_facet[t[2]] + on_facet[t[3]];
+            if (on < 3) continue;
             for (int j = 0; j < 4; ++j) {
+                if (!on_facet[t[tf[j][0]]] || !on_facet[t[tf[j][1]]] || !on_facet[t[tf[j][2]]]) continue;
                 int32_t k[3] = {t[tf[j][0]], t[tf[j][1]], t[tf[j][2]]};
                 sort3(k);
                 const int32_t f = H.find(k);
@@ -276,6 +302,7 @@ void finalize_mesh(const cf_mesh_desc* d, MeshData& m) {
     for (size_t c = 0; c < m.contacts.size(); ++c)
         if (m.contacts[c] < 0 || m.contacts[c] >= (int32_t)m.tags.size())
             raise(CF_VALIDATION, "contact declaration references unknown tag");
+    trace_stage("finalize: facet owners");
 }
 
 // ------------------------------------------------------------------ sisters
@@ -564,15 +591,21 @@ int64_t bandwidth(const Graph& g, const int32_t* p) {
 std::vector<int32_t> partition_rcb(const MeshData& m, int32_t parts) {
     if (parts < 1) raise(CF_INVALID_ARG, "parts must be >= 1");
     const int64_t E = m.E;
-    std::vector<double> cen(3 * (size_t)E);
+    // contiguous (centroid, id) records: the bisections stream them instead of
+    // chasing ids; (coordinate, id) is a total order, so each split takes the
+    // same set of elements whatever the record order
+    struct Rec {
+        double c[3];
+        int32_t id;
+    };
+    std::vector<Rec, UninitAlloc<Rec>> rec(E);
 #pragma omp parallel for schedule(static)
-    for (int64_t e = 0; e < E; ++e)
-        for (int k = 0; k < 3; ++k) {
-            const int32_t* t = &m.tets[4 * (size_t)e];
-            cen[3 * e + k] = (((m.pos(t[0])[k] + m.pos(t[1])[k]) + m.pos(t[2])[k]) + m.pos(t[3])[k]) * 0.25;
-        }
-    std::vector<int32_t> ids(E);
-    std::iota(ids.begin(), ids.end(), 0);
+    for (int64_t e = 0; e < E; ++e) {
+        const int32_t* t = &m.tets[4 * (size_t)e];
+        for (int k = 0; k < 3; ++k)
+            rec[e].c[k] = (((m.pos(t[0])[k] + m.pos(t[1])[k]) + m.pos(t[2])[k]) + m.pos(t[3])[k]) * 0.25;
+        rec[e].id = (int32_t)e;
+    }
     std::vector<int32_t> part(E, 0);
     struct Job {
         int64_t lo, hi;
@@ -583,26 +616,31 @@ std::vector<int32_t> partition_rcb(const MeshData& m, int32_t parts) {
         Job j = stack.back();
         stack.pop_back();
         if (j.count == 1) {
-            for (int64_t i = j.lo; i < j.hi; ++i) part[ids[i]] = j.first;
+#pragma omp parallel for schedule(static)
+            for (int64_t i = j.lo; i < j.hi; ++i) part[rec[i].id] = j.first;
             continue;
         }
-        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-        for (int64_t i = j.lo; i < j.hi; ++i)
-            for (int k = 0; k < 3; ++k) {
-                lo[k] = std::min(lo[k], cen[3 * (size_t)ids[i] + k]);
-                hi[k] = std::max(hi[k], cen[3 * (size_t)ids[i] + k]);
-            }
+        double lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY;
+#pragma omp parallel for schedule(static) reduction(min : lo0, lo1, lo2) reduction(max : hi0, hi1, hi2)
+        for (int64_t i = j.lo; i < j.hi; ++i) {
+            lo0 = std::min(lo0, rec[i].c[0]);
+            lo1 = std::min(lo1, rec[i].c[1]);
+            lo2 = std::min(lo2, rec[i].c[2]);
+            hi0 = std::max(hi0, rec[i].c[0]);
+            hi1 = std::max(hi1, rec[i].c[1]);
+            hi2 = std::max(hi2, rec[i].c[2]);
+        }
+        const double lo[3] = {lo0, lo1, lo2}, hi[3] = {hi0, hi1, hi2};
         int axis = 0;
         for (int k = 1; k < 3; ++k)
             if (hi[k] - lo[k] > hi[axis] - lo[axis]) axis = k;
         const int32_t left = j.count / 2;
         const int64_t n = j.hi - j.lo;
         const int64_t nl = n * left / j.count;
-        auto cmp = [&](int32_t a, int32_t b) {
-            const double ca = cen[3 * (size_t)a + axis], cb = cen[3 * (size_t)b + axis];
-            return ca != cb ? ca < cb : a < b;
+        auto cmp = [axis](const Rec& a, const Rec& b) {
+            return a.c[axis] != b.c[axis] ? a.c[axis] < b.c[axis] : a.id < b.id;
         };
-        std::nth_element(ids.begin() + j.lo, ids.begin() + j.lo + nl, ids.begin() + j.hi, cmp);
+        __gnu_parallel::nth_element(rec.begin() + j.lo, rec.begin() + j.lo + nl, rec.begin() + j.hi, cmp);
         stack.push_back({j.lo + nl, j.hi, j.first + left, j.count - left});
         stack.push_back({j.lo, j.lo + nl, j.first, left});
     }

@@ -9,8 +9,10 @@
 //   facet bindings in element order      blocked.hpp:244-288
 //   external nodes / ambient bindings    blocked.hpp:309-331, classify_nodes partition.hpp:305-367
 #include <omp.h>
+#include <parallel/algorithm>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <array>
@@ -95,7 +97,9 @@ void resolve_setup(const MeshData& m, const cf_setup_desc* s, SetupData& out) {
             if (!(t.x[j] > t.x[j - 1])) raise(CF_CONFIG, "interface h: table abscissae must be strictly increasing");
     }
     // pair_sister_facets first (solve_serial blocked.hpp:651)
+    trace_stage("resolve: tables");
     out.pairs = pair_sister_facets(m);
+    trace_stage("resolve: sister pairing");
     out.pair_of_facet.assign(m.F, -1);
     for (size_t p = 0; p < out.pairs.size(); ++p) out.pair_of_facet[out.pairs[p].facet] = (int32_t)p;
 
@@ -295,7 +299,32 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     // parts touching each node (classify_nodes partition.hpp:311-327), only for W > 1
     std::vector<int64_t> np_off;
     std::vector<int32_t> np_parts;
-    if (W > 1) {
+    if (W > 1 && W <= 64) {
+        // one bit per part, OR-ed in parallel; lists come out ascending
+        std::vector<std::atomic<uint64_t>> mask(m.N);
+#pragma omp parallel for schedule(static)
+        for (int32_t n = 0; n < m.N; ++n) mask[n].store(0, std::memory_order_relaxed);
+#pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < (int64_t)m.E; ++e) {
+            const uint64_t bit = 1ull << part_of((int32_t)e);
+            for (int a = 0; a < 4; ++a) {
+                std::atomic<uint64_t>& w = mask[m.tets[4 * (size_t)e + a]];
+                if (!(w.load(std::memory_order_relaxed) & bit)) w.fetch_or(bit, std::memory_order_relaxed);
+            }
+        }
+        np_off.assign(m.N + 1, 0);
+        for (int32_t n = 0; n < m.N; ++n) np_off[n + 1] = np_off[n] + __builtin_popcountll(mask[n].load());
+        np_parts.resize(np_off[m.N]);
+#pragma omp parallel for schedule(static)
+        for (int32_t n = 0; n < m.N; ++n) {
+            uint64_t b = mask[n].load(std::memory_order_relaxed);
+            int64_t j = np_off[n];
+            while (b) {
+                np_parts[j++] = __builtin_ctzll(b);
+                b &= b - 1;
+            }
+        }
+    } else if (W > 1) {
         np_off.assign(m.N + 1, 0);
         std::vector<int32_t> cnt(m.N, 0);
         std::vector<int64_t> off(m.N + 1, 0);
@@ -315,6 +344,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
         for (int32_t n = 0; n < m.N; ++n)
             std::copy(buf.begin() + off[n], buf.begin() + off[n] + cnt[n], np_parts.begin() + np_off[n]);
     }
+    trace_stage("plan: node parts");
     auto node_on = [&](int32_t n, int32_t p) {
         if (W == 1) return true;
         for (int64_t j = np_off[n]; j < np_off[n + 1]; ++j)
@@ -352,7 +382,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                 }
                 key[i] = {code, e};
             }
-            std::sort(key.begin(), key.end());
+            __gnu_parallel::sort(key.begin(), key.end());  // keys unique: any sort gives this order
             for (int64_t i = 0; i < Er; ++i) order[i] = key[i].second;
         } else if (o.elem_order == CF_ELEM_ORDER_MIN_NODE) {
             std::vector<std::pair<int32_t, int32_t>> key(Er);
@@ -371,6 +401,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             std::sort(tiles.back().begin(), tiles.back().end());
         }
     }
+    trace_stage("plan: tiles");
     rp.n_tiles = (int32_t)tiles.size();
     for (auto& t : tiles)
         if ((int)t.size() > kMaxTileElems)
@@ -400,6 +431,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                       [&](int32_t a, int32_t b) { return node_label[a] < node_label[b]; });
         for (size_t i = 0; i < lnodes.size(); ++i) local_of[lnodes[i]] = (int32_t)i;
     }
+    trace_stage("plan: local numbering");
     rp.n_local = (int32_t)lnodes.size();
     if (rp.n_local >= (1 << 28)) raise(CF_INVALID_ARG, "more than 2^28 nodes on one rank");
 
@@ -417,6 +449,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe[cur[m.owner[f]]++] = f;
     }
 
+    trace_stage("plan: facet bindings");
     // ghosts: sister nodes of this rank's interface facets that are not local
     std::vector<int32_t> ghosts;
     for (int32_t f = 0; f < m.F; ++f) {
@@ -455,6 +488,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             shared_node[l] = (np_off[n + 1] - np_off[n]) > 1;
         }
 
+    trace_stage("plan: ghosts + tile counts");
     rp.node_region.resize(rp.n_local);
     for (int32_t l = 0; l < rp.n_local; ++l) rp.node_region[l] = (uint8_t)m.node_region[lnodes[l]];
     bool any_dir = false;
@@ -465,129 +499,163 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
         for (int32_t l = 0; l < rp.n_local; ++l) rp.node_dir[l] = (int8_t)S.dir_of_node[lnodes[l]];
     }
 
-    // ---- per tile: slots, CSR, facet bindings, packed into the blob
+    // ---- per tile: slots, CSR, facet bindings, packed into the blob.
+    // Pass 1 (parallel): each tile's slot list; sizes -> offsets; pass 2
+    // (parallel): fill the tile's blob section at its offset.
     rp.tile_meta.resize(rp.n_tiles);
     rp.tile_slot_off.assign(rp.n_tiles + 1, 0);
     rp.blob_off.assign(rp.n_tiles + 1, 0);
     rp.elem_global.resize(Er);
-    std::vector<int32_t> slot_of(rp.n_local, -1);
-    int64_t epos = 0;
-    std::vector<int32_t> tnodes;
-    std::vector<std::vector<uint16_t>> slot_entries;
-    std::vector<int32_t> tfacets;
-    for (int32_t t = 0; t < rp.n_tiles; ++t) {
-        const auto& te = tiles[t];
-        const int ne = (int)te.size();
-        tnodes.clear();
+    const int nthr = omp_get_max_threads();
+    std::vector<std::vector<int32_t>> tile_nodes(rp.n_tiles);
+    std::vector<int64_t> elem_off(rp.n_tiles + 1, 0);
+    auto tile_facets = [&](const std::vector<int32_t>& te, std::vector<int32_t>& out) {
+        out.clear();  // facet bindings, element order then facet id (blocked.hpp:244-288)
         for (int32_t e : te)
-            for (int a = 0; a < 4; ++a) {
-                const int32_t l = local_of[m.tets[4 * (size_t)e + a]];
-                if (slot_of[l] == -1) {
-                    slot_of[l] = -2;
-                    tnodes.push_back(l);
+            for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j) out.push_back(fe[j]);
+    };
+#pragma omp parallel num_threads(nthr)
+    {
+        std::vector<int32_t> slot_of(rp.n_local, -1), cnt_of, idx, tfacets;
+#pragma omp for schedule(dynamic, 64)
+        for (int32_t t = 0; t < rp.n_tiles; ++t) {
+            const auto& te = tiles[t];
+            auto& tnodes = tile_nodes[t];
+            for (int32_t e : te)
+                for (int a = 0; a < 4; ++a) {
+                    const int32_t l = local_of[m.tets[4 * (size_t)e + a]];
+                    if (slot_of[l] == -1) {
+                        slot_of[l] = -2;
+                        tnodes.push_back(l);
+                    }
                 }
-            }
-        // slots ordered by contribution count (desc), then local id: the warps of
-        // the reduction phase then walk lists of near-equal length (no divergence)
-        {
-            std::vector<int32_t> cnt_of(tnodes.size(), 0);
-            for (size_t s = 0; s < tnodes.size(); ++s) slot_of[tnodes[s]] = (int32_t)s;
+            // slots ordered by contribution count (desc), then local id: the warps of
+            // the reduction phase then walk lists of near-equal length (no divergence)
+            for (size_t k = 0; k < tnodes.size(); ++k) slot_of[tnodes[k]] = (int32_t)k;
+            cnt_of.assign(tnodes.size(), 0);
+            tile_facets(te, tfacets);
             for (int32_t e : te)
                 for (int a = 0; a < 4; ++a) cnt_of[slot_of[local_of[m.tets[4 * (size_t)e + a]]]]++;
-            for (int32_t e : te)
-                for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j)
-                    for (int a = 0; a < 3; ++a) cnt_of[slot_of[local_of[m.facets[3 * (size_t)fe[j] + a]]]]++;
-            std::vector<int32_t> idx(tnodes.size());
+            for (int32_t f : tfacets)
+                for (int a = 0; a < 3; ++a) cnt_of[slot_of[local_of[m.facets[3 * (size_t)f + a]]]]++;
+            idx.resize(tnodes.size());
             std::iota(idx.begin(), idx.end(), 0);
             std::sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) {
                 return cnt_of[x] != cnt_of[y] ? cnt_of[x] > cnt_of[y] : tnodes[x] < tnodes[y];
             });
+            for (int32_t l : tnodes) slot_of[l] = -1;
             std::vector<int32_t> sorted(tnodes.size());
-            for (size_t s = 0; s < idx.size(); ++s) sorted[s] = tnodes[idx[s]];
+            for (size_t k = 0; k < idx.size(); ++k) sorted[k] = tnodes[idx[k]];
             tnodes.swap(sorted);
+            const int ne = (int)te.size(), ns = (int)tnodes.size(), nf = (int)tfacets.size();
+            rp.tile_meta[t] = TileMeta{ne, ns, nf, 4 * ne + 3 * nf};
         }
-        for (size_t s = 0; s < tnodes.size(); ++s) slot_of[tnodes[s]] = (int32_t)s;
-        const int ns = (int)tnodes.size();
-        slot_entries.assign(ns, {});
-        // facet bindings, element order then facet id (blocked.hpp:244-288)
-        tfacets.clear();
-        for (int32_t e : te)
-            for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j) tfacets.push_back(fe[j]);
-        const int nf = (int)tfacets.size();
-        for (int i = 0; i < ne; ++i)
-            for (int a = 0; a < 4; ++a)
-                slot_entries[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]]].push_back((uint16_t)(4 * i + a));
-        for (int i = 0; i < nf; ++i)
-            for (int a = 0; a < 3; ++a)
-                slot_entries[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]]].push_back(
-                    (uint16_t)(4 * ne + 4 * i + a));
-        int ncsr = 0;
-        for (int s = 0; s < ns; ++s) ncsr += (int)slot_entries[s].size();
-        if (4 * ne + 4 * nf > 65535) raise(CF_INVALID_ARG, "tile csr exceeds 16-bit codes");
-        TileMeta tm{ne, ns, nf, ncsr};
-        rp.tile_meta[t] = tm;
-        const TileLayout L(tm, S.temp_dep);
-        const int64_t base = rp.blob_off[t];
-        rp.blob_off[t + 1] = base + L.bytes;
-        rp.blob.resize(rp.blob_off[t + 1], 0);
-        uint8_t* B = rp.blob.data() + base;
-        double* gsec = (double*)(B + L.geom);
-        uint16_t* csec = (uint16_t*)(B + L.conn);
-        for (int i = 0; i < ne; ++i) {
-            const int32_t e = te[i];
-            rp.elem_global[epos + i] = e;
-            const Geom g = m.geometry(e);
-            const double vals[11] = {g.g[1][0], g.g[1][1], g.g[1][2], g.g[2][0], g.g[2][1], g.g[2][2],
-                                     g.g[3][0], g.g[3][1], g.g[3][2], g.vol,     g.max_edge};
-            for (int k = 0; k < 11; ++k) gsec[(size_t)k * L.ne2 + i] = vals[k];
-            if (S.temp_dep) ((double*)(B + L.minedge))[i] = g.min_edge;
-            for (int a = 0; a < 4; ++a) csec[4 * i + a] = (uint16_t)slot_of[local_of[m.tets[4 * (size_t)e + a]]];
-            B[L.region + i] = (uint8_t)m.region[e];
-        }
-        for (int i = 0; i < nf; ++i) {
-            const int32_t f = tfacets[i];
-            const int32_t kind = S.facet_kind[f];
-            uint16_t* fs = (uint16_t*)(B + L.fslots) + 4 * i;
-            for (int a = 0; a < 3; ++a) fs[a] = (uint16_t)slot_of[local_of[m.facets[3 * (size_t)f + a]]];
-            fs[3] = (uint16_t)kind;
-            ((double*)(B + L.farea))[i] = triangle_area(m.pos(m.facets[3 * (size_t)f]),
-                                                        m.pos(m.facets[3 * (size_t)f + 1]),
-                                                        m.pos(m.facets[3 * (size_t)f + 2]));
-            int32_t* sis = (int32_t*)(B + L.fsister) + 4 * i;
-            if (S.P.kind[kind].interface) {
-                const int32_t se = S.pairs[S.pair_of_facet[f]].sister;
-                for (int a = 0; a < 4; ++a) sis[a] = local_of[m.tets[4 * (size_t)se + a]];
-                rp.n_if_facets++;
-            } else {
-                rp.n_bc_facets++;
-            }
-        }
-        uint16_t* cend = (uint16_t*)(B + L.csr_end);
-        uint16_t* csr = (uint16_t*)(B + L.csr);
-        int rel = 0;
-        for (int s = 0; s < (int)cf_round(ns, 2); ++s) {
-            if (s >= ns) {  // padding slot (never a merge target)
-                rp.slot_node.push_back(-1);
-                continue;
-            }
-            const int32_t l = tnodes[s];
-            rp.slot_node.push_back((int32_t)(((uint32_t)rp.node_region[l] << 28) | (uint32_t)l));
-            const bool priv = ntiles_of[l] == 1 && !shared_node[l];
-            const bool dir = !rp.node_dir.empty() && rp.node_dir[l] >= 0;
-            B[L.sinfo + s] = (uint8_t)((rp.node_region[l] & 0x3f) | (dir ? 0x40 : 0) | (priv ? 0x80 : 0));
-            for (uint16_t c : slot_entries[s]) csr[rel++] = c;
-            cend[s] = (uint16_t)rel;
-        }
-        rp.tile_slot_off[t + 1] = rp.tile_slot_off[t] + (int32_t)cf_round(ns, 2);  // 16 B aligned Tslot segments
-        int32_t* sn = (int32_t*)(B + L.snode);
-        for (int s2 = 0; s2 < ns; ++s2) sn[s2] = tnodes[s2];
-        rp.max_elems = std::max(rp.max_elems, ne);
-        rp.max_slots = std::max(rp.max_slots, (int32_t)cf_round(ns, 2));
-        rp.max_facets = std::max(rp.max_facets, nf);
-        rp.max_blob = std::max(rp.max_blob, L.bytes);
-        for (int s = 0; s < ns; ++s) slot_of[tnodes[s]] = -1;
-        epos += ne;
     }
+    for (int32_t t = 0; t < rp.n_tiles; ++t)  // no throwing inside the parallel regions
+        if (4 * rp.tile_meta[t].ne + 4 * rp.tile_meta[t].nf > 65535)
+            raise(CF_INVALID_ARG, "tile csr exceeds 16-bit codes");
+    for (int32_t t = 0; t < rp.n_tiles; ++t) {
+        const TileMeta& tm = rp.tile_meta[t];
+        const TileLayout L(tm, S.temp_dep);
+        rp.blob_off[t + 1] = rp.blob_off[t] + L.bytes;
+        rp.tile_slot_off[t + 1] = rp.tile_slot_off[t] + (int32_t)cf_round(tm.ns, 2);  // 16 B aligned Tslot segments
+        elem_off[t + 1] = elem_off[t] + tm.ne;
+        rp.max_elems = std::max(rp.max_elems, tm.ne);
+        rp.max_slots = std::max(rp.max_slots, (int32_t)cf_round(tm.ns, 2));
+        rp.max_facets = std::max(rp.max_facets, tm.nf);
+        rp.max_blob = std::max(rp.max_blob, L.bytes);
+    }
+    rp.blob.resize(rp.blob_off[rp.n_tiles]);
+    rp.slot_node.resize(rp.tile_slot_off[rp.n_tiles]);
+    int64_t n_if = 0, n_bc = 0;
+#pragma omp parallel num_threads(nthr) reduction(+ : n_if, n_bc)
+    {
+        std::vector<int32_t> slot_of(rp.n_local, -1), tfacets;
+        std::vector<int32_t> ent_off, ent, cur;
+#pragma omp for schedule(dynamic, 64)
+        for (int32_t t = 0; t < rp.n_tiles; ++t) {
+            const auto& te = tiles[t];
+            const auto& tnodes = tile_nodes[t];
+            const TileMeta tm = rp.tile_meta[t];
+            const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
+            const TileLayout L(tm, S.temp_dep);
+            uint8_t* B = rp.blob.data() + rp.blob_off[t];
+            std::memset(B, 0, (size_t)L.bytes);
+            for (int k = 0; k < ns; ++k) slot_of[tnodes[k]] = k;
+            tile_facets(te, tfacets);
+            // per-slot contribution codes (4e+a, then 4ne+4f+a), in code order
+            ent_off.assign(ns + 1, 0);
+            for (int i = 0; i < ne; ++i)
+                for (int a = 0; a < 4; ++a) ent_off[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]] + 1]++;
+            for (int i = 0; i < nf; ++i)
+                for (int a = 0; a < 3; ++a) ent_off[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]] + 1]++;
+            for (int k = 0; k < ns; ++k) ent_off[k + 1] += ent_off[k];
+            ent.resize(ent_off[ns]);
+            {
+                cur.assign(ent_off.begin(), ent_off.end() - 1);
+                for (int i = 0; i < ne; ++i)
+                    for (int a = 0; a < 4; ++a)
+                        ent[cur[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]]]++] = 4 * i + a;
+                for (int i = 0; i < nf; ++i)
+                    for (int a = 0; a < 3; ++a)
+                        ent[cur[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]]]++] = 4 * ne + 4 * i + a;
+            }
+            double* gsec = (double*)(B + L.geom);
+            uint16_t* csec = (uint16_t*)(B + L.conn);
+            for (int i = 0; i < ne; ++i) {
+                const int32_t e = te[i];
+                rp.elem_global[elem_off[t] + i] = e;
+                const Geom g = m.geometry(e);
+                const double vals[11] = {g.g[1][0], g.g[1][1], g.g[1][2], g.g[2][0], g.g[2][1], g.g[2][2],
+                                         g.g[3][0], g.g[3][1], g.g[3][2], g.vol,     g.max_edge};
+                for (int k = 0; k < 11; ++k) gsec[(size_t)k * L.ne2 + i] = vals[k];
+                if (S.temp_dep) ((double*)(B + L.minedge))[i] = g.min_edge;
+                for (int a = 0; a < 4; ++a) csec[4 * i + a] = (uint16_t)slot_of[local_of[m.tets[4 * (size_t)e + a]]];
+                B[L.region + i] = (uint8_t)m.region[e];
+            }
+            for (int i = 0; i < nf; ++i) {
+                const int32_t f = tfacets[i];
+                const int32_t kind = S.facet_kind[f];
+                uint16_t* fs = (uint16_t*)(B + L.fslots) + 4 * i;
+                for (int a = 0; a < 3; ++a) fs[a] = (uint16_t)slot_of[local_of[m.facets[3 * (size_t)f + a]]];
+                fs[3] = (uint16_t)kind;
+                ((double*)(B + L.farea))[i] = triangle_area(m.pos(m.facets[3 * (size_t)f]),
+                                                            m.pos(m.facets[3 * (size_t)f + 1]),
+                                                            m.pos(m.facets[3 * (size_t)f + 2]));
+                int32_t* sis = (int32_t*)(B + L.fsister) + 4 * i;
+                if (S.P.kind[kind].interface) {
+                    const int32_t se = S.pairs[S.pair_of_facet[f]].sister;
+                    for (int a = 0; a < 4; ++a) sis[a] = local_of[m.tets[4 * (size_t)se + a]];
+                    n_if++;
+                } else {
+                    n_bc++;
+                }
+            }
+            uint16_t* cend = (uint16_t*)(B + L.csr_end);
+            uint16_t* csr = (uint16_t*)(B + L.csr);
+            int32_t* sn = (int32_t*)(B + L.snode);
+            const int64_t so = rp.tile_slot_off[t];
+            for (int k = 0; k < (int)cf_round(ns, 2); ++k) {
+                if (k >= ns) {  // padding slot (never a merge target)
+                    rp.slot_node[so + k] = -1;
+                    continue;
+                }
+                const int32_t l = tnodes[k];
+                rp.slot_node[so + k] = (int32_t)(((uint32_t)rp.node_region[l] << 28) | (uint32_t)l);
+                const bool priv = ntiles_of[l] == 1 && !shared_node[l];
+                const bool dir = !rp.node_dir.empty() && rp.node_dir[l] >= 0;
+                B[L.sinfo + k] = (uint8_t)((rp.node_region[l] & 0x3f) | (dir ? 0x40 : 0) | (priv ? 0x80 : 0));
+                for (int32_t j = ent_off[k]; j < ent_off[k + 1]; ++j) csr[j] = (uint16_t)ent[j];
+                cend[k] = (uint16_t)ent_off[k + 1];
+                sn[k] = l;
+            }
+            for (int k = 0; k < ns; ++k) slot_of[tnodes[k]] = -1;
+        }
+    }
+    rp.n_if_facets = n_if;
+    rp.n_bc_facets = n_bc;
+    std::vector<std::vector<int32_t>>().swap(tile_nodes);
+    trace_stage("plan: blob packing");
     // merge lists: ascending tile per node (merge_offsets/merge_entries blocked.hpp:294-307)
     const int64_t S_tot = rp.tile_slot_off[rp.n_tiles];
     rp.merge_off.assign(rp.n_local + 1, 0);
@@ -606,6 +674,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
         else rp.shared_list.push_back(l);
     }
 
+    trace_stage("plan: merge lists");
     // ---------------------------------------------------- multi-rank exchange
     if (W > 1) {
         // need(p, q) = nodes part p needs from part q (external_from partition.hpp:346-354)
@@ -689,6 +758,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
         }
         for (int32_t g = 0; g < rp.n_ghost; ++g)
             if (rp.ghost_src[g] < 0) raise(CF_PROTOCOL, "ghost node without a provider");
+        trace_stage("plan: exchange lists");
     }
 }
 

@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--mode", default="deterministic", choices=["atomic", "deterministic"])
     ap.add_argument("--tile", type=int, default=384)
     ap.add_argument("--elem-order", default="morton")
+    ap.add_argument("--geometry", default="stored", choices=["stored", "coords"],
+                    help="tile layout: slot coordinates (gradients recomputed) or stored ElementGeom")
     ap.add_argument("--node-order", default="tile")
     ap.add_argument("--cpu-steps", type=int, default=int(os.environ.get("CF_CPU_STEPS", "12")))
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -210,7 +212,7 @@ def main():
         t = torch.tensor(list(uid), dtype=torch.uint8)
         pg.broadcast(t, 0)
         comm = cf.Comm(world, rank, local_rank, bytes(t.tolist()))
-    opts = cf.SolveOptions(mode=args.mode, tile_elems=args.tile, elem_order=args.elem_order,
+    opts = cf.SolveOptions(mode=args.mode, tile_elems=args.tile, elem_order=args.elem_order, geometry=args.geometry,
                            node_order=args.node_order, device=local_rank, world_size=world, rank=rank,
                            comm=comm, graph_steps=args.graph)
     t0 = time.time()
@@ -301,6 +303,7 @@ def main():
                 "config": {"workload": cfg, "elements": E_total, "nodes": mesh.node_count(),
                            "hex_cells": E_total // 6, "mode": args.mode, "tile_elems": args.tile,
                            "elem_order": args.elem_order, "node_order": args.node_order,
+                           "geometry": args.geometry,
                            "dt_safety": setup.solver.dt_safety, "h_interface": 1000.0,
                            "parallelism": f"rcb{world}" if world > 1 else "single",
                            "l2": "working set > 126 MB L2 (no flush needed)" if st.bytes_per_step > 2e8

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define CF_ABI_VERSION 1
+#define CF_ABI_VERSION 2
 
 /* status codes — errors.hpp:8-31 (+ degenerate_element_error geometry.hpp:43-46) */
 enum {
@@ -135,6 +135,12 @@ enum {
     CF_ELEM_ORDER_MIN_NODE = 2 /* chunks of the order by smallest (RCM) node label */
 };
 enum {
+    CF_GEOM_STORED = 0,        /* tiles carry the precomputed 11-double ElementGeom (default) */
+    CF_GEOM_COORDS = 1         /* tiles carry slot coordinates; the kernel recomputes the element
+                                  gradients/volume (tet_geometry geometry.hpp:50-79, bitwise: same
+                                  IEEE operations): ~40 % of the HBM bytes and device memory */
+};
+enum {
     CF_PARTITION_RCB = 0,      /* recursive coordinate bisection along the longest axis */
     CF_PARTITION_GIVEN = 1     /* part_of_element supplied (load_partmap partition.hpp:424-445) */
 };
@@ -157,6 +163,7 @@ typedef struct cf_run_opts {
     int32_t partition;         /* CF_PARTITION_* */
     const int32_t* part_of_element; /* [n_elems] when CF_PARTITION_GIVEN */
     void* comm;                /* cf_comm* for world_size > local_ranks, else NULL */
+    int32_t geometry;          /* CF_GEOM_* (0 = stored element geometry) */
 } cf_run_opts;
 
 typedef struct cf_plan cf_plan;

@@ -52,6 +52,7 @@ struct SolveOptions {             // castfem::SolveOptions (blocked.hpp:630-636)
     int node_order = CF_NODE_ORDER_TILE;
     int elem_order = CF_ELEM_ORDER_MORTON;
     int tile_elems = 384;
+    int geometry = CF_GEOM_STORED;
     int device = 0;
 };
 
@@ -172,6 +173,7 @@ class Plan {
         ro.node_order = o.node_order;
         ro.elem_order = o.elem_order;
         ro.tile_elems = o.tile_elems;
+        ro.geometry = o.geometry;
         ro.world_size = 1;
         ro.local_ranks = 1;
         check(cf_plan_create(d.mesh(), d.setup(), &ro, &plan_));

@@ -18,6 +18,7 @@ CF_VAR_TIME, CF_VAR_TEMPERATURE = 0, 1
 CF_MODE_ATOMIC, CF_MODE_DETERMINISTIC = 0, 1
 CF_NODE_ORDER_GIVEN, CF_NODE_ORDER_RCM, CF_NODE_ORDER_TILE = 0, 1, 2
 CF_ELEM_ORDER_GIVEN, CF_ELEM_ORDER_MORTON, CF_ELEM_ORDER_MIN_NODE = 0, 1, 2
+CF_GEOM_STORED, CF_GEOM_COORDS = 0, 1
 CF_PARTITION_RCB, CF_PARTITION_GIVEN = 0, 1
 
 _dp = C.POINTER(C.c_double)
@@ -61,7 +62,7 @@ class cf_run_opts(C.Structure):
                 ("tile_elems", C.c_int32), ("tile_of_element", _ip), ("n_tiles_given", C.c_int32),
                 ("fast_math", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
                 ("local_ranks", C.c_int32), ("partition", C.c_int32), ("part_of_element", _ip),
-                ("comm", C.c_void_p)]
+                ("comm", C.c_void_p), ("geometry", C.c_int32)]
 
 
 class cf_stats(C.Structure):

@@ -187,6 +187,7 @@ class SolveOptions:
     node_order: str = "tile"         # 'tile' (first touch in tile order) | 'rcm' | 'given'
     elem_order: str = "morton"       # 'morton' | 'min_node' | 'given'
     tile_elems: int = 384
+    geometry: str = "stored"         # 'stored' (ElementGeom per tet) | 'coords' (recompute from slot coordinates)
     blocks: Optional[np.ndarray] = None  # explicit element->tile map (BlockPlan semantics)
     device: int = 0
     world_size: int = 1
@@ -301,6 +302,7 @@ _MODES = {"atomic": _abi.CF_MODE_ATOMIC, "deterministic": _abi.CF_MODE_DETERMINI
 _NODE = {"given": _abi.CF_NODE_ORDER_GIVEN, "rcm": _abi.CF_NODE_ORDER_RCM, "tile": _abi.CF_NODE_ORDER_TILE}
 _ELEM = {"given": _abi.CF_ELEM_ORDER_GIVEN, "morton": _abi.CF_ELEM_ORDER_MORTON,
          "min_node": _abi.CF_ELEM_ORDER_MIN_NODE}
+_GEOM = {"coords": _abi.CF_GEOM_COORDS, "stored": _abi.CF_GEOM_STORED}
 
 
 def run_opts(o: SolveOptions, keep: _Keep) -> _abi.cf_run_opts:
@@ -310,6 +312,7 @@ def run_opts(o: SolveOptions, keep: _Keep) -> _abi.cf_run_opts:
     d.node_order = _NODE[o.node_order]
     d.elem_order = _ELEM[o.elem_order]
     d.tile_elems = o.tile_elems
+    d.geometry = _GEOM[o.geometry]
     if o.blocks is not None:
         d.tile_of_element = keep.iptr(o.blocks)
         d.n_tiles_given = int(np.max(o.blocks)) + 1 if len(o.blocks) else 0

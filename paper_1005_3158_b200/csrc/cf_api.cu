@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -148,8 +149,14 @@ struct Rank {
     double* acc_r = nullptr;
     double2* part = nullptr;
     DevState* st = nullptr;
-    int tile_grid = 0;
-    int ws_stages = 0;             // >0: warp-specialised producer/consumer tile kernel in use
+    // tile launches of one step: tiles grouped by shared-memory footprint, so the common
+    // tiles are not sized (and occupancy-limited) by the largest interface tile
+    struct TileLaunch {
+        TileArgs a;
+        size_t smem;
+        int grid;
+    };
+    std::vector<TileLaunch> launches;
     int32_t* all_list = nullptr;   // unused (NULL list = identity)
     int32_t* shared_list = nullptr;
     int4* shared_rec = nullptr;     // packed update records of shared_list
@@ -165,12 +172,12 @@ struct Rank {
 struct cf_plan {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;              // concurrent launch of the heavy tile class
+    cudaEvent_t fork = nullptr, join = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int mode = CF_MODE_ATOMIC;
     int tile_threads = 128;      // CTA size of the tile kernel (32 | 64 | 128 | 256)
     int stages = 1;              // 1: one tile per CTA; 2: persistent double-buffered TMA pipeline
-    int ws_stages = 0;           // warp-specialised pipeline depth (0: off, CF_TILE_WS=2|3; falls back per rank when it does not fit)
-    int ws_warps = 8;            // consumer warps of the warp-specialised kernel (CF_WS_WARPS=4|8)
     int world = 1, first_rank = 0, local_ranks = 1;
     cf_comm* comm = nullptr;
     DevParams P{};
@@ -207,89 +214,82 @@ struct cf_plan {
         if (dHg) cudaFree(dHg);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        if (fork) cudaEventDestroy(fork);
+        if (join) cudaEventDestroy(join);
+        if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
 };
 
 namespace {
 
-size_t tile_smem_bytes(const RankPlan& h, int stages) {
-    return stages * ((size_t)cf_round(h.max_blob, 16) + 8 * (size_t)h.max_slots) + 16 * (size_t)h.max_slots + 16;
+// dynamic shared memory of the tile kernel: [stage blobs][stage slot T][(T, H) per slot][contribution
+// scratch (coordinates layout only)], for the largest blob / slot count / scratch of the launch's tiles
+struct SmemMax {
+    int64_t blob = 0, slots = 0, scratch = 0;
+};
+size_t tile_scratch_off(const SmemMax& m, int stages) {
+    return stages * ((size_t)cf_round(m.blob, 16) + 8 * (size_t)m.slots) + 16 * (size_t)m.slots;
+}
+size_t tile_smem_bytes(const SmemMax& m, int stages) {
+    return tile_scratch_off(m, stages) + 8 * (size_t)cf_round(m.scratch, 2) + 16;
 }
 
-#define CF_TILE_VARIANTS_NT(X, NT)                                                                          \
-    X(true, true, true, true, NT) X(true, true, true, false, NT) X(true, true, false, true, NT)                \
-    X(true, true, false, false, NT) X(true, false, true, true, NT) X(true, false, true, false, NT)             \
-    X(true, false, false, true, NT) X(true, false, false, false, NT) X(false, true, true, true, NT)            \
-    X(false, true, true, false, NT) X(false, true, false, true, NT) X(false, true, false, false, NT)           \
-    X(false, false, true, true, NT) X(false, false, true, false, NT) X(false, false, false, true, NT)          \
-    X(false, false, false, false, NT)
-#define CF_TILE_VARIANTS(X) \
-    CF_TILE_VARIANTS_NT(X, 32) CF_TILE_VARIANTS_NT(X, 64) CF_TILE_VARIANTS_NT(X, 128) CF_TILE_VARIANTS_NT(X, 256)
-
-size_t ws_smem_bytes(const RankPlan& h, int ns) {
-    const size_t stage = 32 + (size_t)cf_round(h.max_blob, 16) + 8 * (size_t)h.max_slots;
-    return ns * stage + ns * 16 * (size_t)h.max_slots;
-}
-constexpr int kWsConsumerWarps = 8;  // CF_WS_WARPS=4 selects the 4-warp variant
-
-#define CF_WS_VARIANTS_W(X, W)                                                                              \
-    X(true, false, false, false, 2, W) X(true, false, false, false, 3, W) X(false, false, false, false, 2, W) \
-    X(false, false, false, false, 3, W) X(true, false, true, false, 2, W) X(true, false, true, false, 3, W)   \
-    X(true, false, false, true, 2, W) X(true, false, true, true, 2, W) X(false, false, true, false, 2, W)    \
-    X(false, false, false, true, 2, W) X(false, false, true, true, 2, W) X(true, false, false, true, 3, W)    \
-    X(true, false, true, true, 3, W) X(false, false, true, false, 3, W) X(false, false, false, true, 3, W)   \
-    X(false, false, true, true, 3, W)
-#define CF_WS_VARIANTS(X) CF_WS_VARIANTS_W(X, 4) CF_WS_VARIANTS_W(X, 8)
+#define CF_TILE_VARIANTS_NT(X, NT, G)                                                                          \
+    X(true, true, true, true, NT, G) X(true, true, true, false, NT, G) X(true, true, false, true, NT, G)          \
+    X(true, true, false, false, NT, G) X(true, false, true, true, NT, G) X(true, false, true, false, NT, G)       \
+    X(true, false, false, true, NT, G) X(true, false, false, false, NT, G) X(false, true, true, true, NT, G)      \
+    X(false, true, true, false, NT, G) X(false, true, false, true, NT, G) X(false, true, false, false, NT, G)     \
+    X(false, false, true, true, NT, G) X(false, false, true, false, NT, G) X(false, false, false, true, NT, G)    \
+    X(false, false, false, false, NT, G)
+#define CF_TILE_VARIANTS(X)                                                                       \
+    CF_TILE_VARIANTS_NT(X, 128, true) CF_TILE_VARIANTS_NT(X, 256, true) CF_TILE_VARIANTS_NT(X, 128, false) \
+    CF_TILE_VARIANTS_NT(X, 256, false)
 
 void set_tile_attr(size_t smem) {
-#define CF_WSA(D, T, R, C, NS, W)                                                                                \
-    CF_CUDA_CHECK(cudaFuncSetAttribute(tile_ws_kernel<D, T, R, C, W, NS>,                                        \
+#define CF_ATTR(D, T, R, C, NT, G)                                                                \
+    CF_CUDA_CHECK(cudaFuncSetAttribute(tile_kernel<D, T, R, C, NT, G>,                                    \
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CF_WS_VARIANTS(CF_WSA)
-#undef CF_WSA
-#define CF_ATTR(D, T, R, C, NT)                                                                                  \
-    CF_CUDA_CHECK(cudaFuncSetAttribute(tile_kernel<D, T, R, C, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                       (int)smem));
     CF_TILE_VARIANTS(CF_ATTR)
 #undef CF_ATTR
-}
-
-bool launch_tile_ws(cf_plan* p, Rank& r, const TileArgs& a) {
-    const bool det = p->mode == CF_MODE_DETERMINISTIC;
-    const bool dir = r.ua.node_dir != nullptr, cl = p->finite_range;
-    const dim3 grid(r.tile_grid), block((p->ws_warps + 1) * 32);
-#define CF_WSL(D, T, R, C, NS, W)                                                                  \
-    if (det == D && !p->temp_dep && dir == R && cl == C && r.ws_stages == NS && p->ws_warps == W) { \
-        tile_ws_kernel<D, T, R, C, W, NS><<<grid, block, r.tile_smem, p->stream>>>(a);             \
-        return true;                                                                               \
-    }
-    CF_WS_VARIANTS(CF_WSL)
-#undef CF_WSL
-    return false;
 }
 
 void launch_tile(cf_plan* p, Rank& r, double t_end) {
     if (r.H.n_tiles == 0) return;
     const bool det = p->mode == CF_MODE_DETERMINISTIC;
-    TileArgs a = r.ta;
-    a.T = r.T[p->cur];
-    a.Told = r.T[p->old()];
-    a.Tn = r.T[p->nxt()];
-    a.Tslot = r.Tslot[p->step_parity];
-    a.Tslot_n = r.Tslot[p->step_parity ^ 1];
-    a.t_end = t_end;
     const bool dir = r.ua.node_dir != nullptr, cl = p->finite_range, td = p->temp_dep;
-    if (r.ws_stages && launch_tile_ws(p, r, a)) return;
+    const bool gc = r.H.coords;
     const int nt = p->tile_threads;
-    const dim3 grid(r.tile_grid), block(nt);
-#define CF_LAUNCH(D, T, R, C, NT)                                                                  \
-    if (det == D && td == T && dir == R && cl == C && nt == NT) {                                  \
-        tile_kernel<D, T, R, C, NT><<<grid, block, r.tile_smem, p->stream>>>(a);                   \
-        return;                                                                                    \
+    // the heavy class (few tiles) runs on a side stream, overlapping the main launch
+    // (disjoint outputs: per-slot partials, tile-private nodes); joined before the update
+    const bool two = r.launches.size() > 1;
+    if (two) {
+        CF_CUDA_CHECK(cudaEventRecord(p->fork, p->stream));
+        CF_CUDA_CHECK(cudaStreamWaitEvent(p->side, p->fork, 0));
     }
-    CF_TILE_VARIANTS(CF_LAUNCH)
+    for (size_t k = r.launches.size(); k-- > 0;) {  // heavy class first: its CTAs dispatch first
+        const Rank::TileLaunch& tl = r.launches[k];
+        cudaStream_t st = k == 1 ? p->side : p->stream;
+        TileArgs a = tl.a;
+        a.T = r.T[p->cur];
+        a.Told = r.T[p->old()];
+        a.Tn = r.T[p->nxt()];
+        a.Tslot = r.Tslot[p->step_parity];
+        a.Tslot_n = r.Tslot[p->step_parity ^ 1];
+        a.t_end = t_end;
+        const dim3 grid(tl.grid), block(nt);
+#define CF_LAUNCH(D, T, R, C, NT, G)                                                                  \
+    if (det == D && td == T && dir == R && cl == C && nt == NT && gc == G) {                          \
+        tile_kernel<D, T, R, C, NT, G><<<grid, block, tl.smem, st>>>(a);                              \
+        continue;                                                                                     \
+    }
+        CF_TILE_VARIANTS(CF_LAUNCH)
 #undef CF_LAUNCH
+    }
+    if (two) {
+        CF_CUDA_CHECK(cudaEventRecord(p->join, p->side));
+        CF_CUDA_CHECK(cudaStreamWaitEvent(p->stream, p->join, 0));
+    }
 }
 
 template <bool DET, bool MULTI>
@@ -436,36 +436,72 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     a.blob_smem = (int32_t)cf_round(h.max_blob, 16);
     a.stages = p->stages;
     if (const char* e = std::getenv("CF_PROBE")) a.probe = std::atoi(e);
-    r.tile_smem = tile_smem_bytes(h, p->stages);
-    if (p->ws_stages && ws_smem_bytes(h, p->ws_stages) <= (p->ws_warps == 4 ? 55 : 110) * 1024) {
-        r.ws_stages = p->ws_stages;
-        r.tile_smem = ws_smem_bytes(h, p->ws_stages);
-    }
-    if (r.tile_smem > 220 * 1024) raise(CF_INVALID_ARG, "tile shared-memory footprint exceeds 220 KB; use smaller tiles");
-    // the attribute is per function (shared by every plan and rank): the opt-in maximum;
-    // occupancy follows the dynamic size passed at launch
-    set_tile_attr(220 * 1024);
+    // tile classes: "light" = tiles whose footprint is within the 97th percentile,
+    // "heavy" = the rest (interface / boundary tiles with many facets), own launch
     {
-        int per_sm = 0, sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-#define CF_OCC(NT)                                                                                   \
-    if (p->tile_threads == NT)                                                                       \
-        CF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                 \
-            &per_sm, tile_kernel<true, false, false, false, NT>, NT, r.tile_smem));
-        CF_OCC(32) CF_OCC(64) CF_OCC(128) CF_OCC(256)
-#undef CF_OCC
-        per_sm = std::max(1, per_sm);
-        r.tile_grid = p->stages == 1 ? std::max(1, h.n_tiles) : std::max(1, std::min<int>(h.n_tiles, sms * per_sm));
-        if (r.ws_stages) {
-            if (p->ws_warps == 4)
-                CF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                    &per_sm, tile_ws_kernel<true, false, false, false, 4, 2>, 5 * 32, r.tile_smem));
-            else
-                CF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                    &per_sm, tile_ws_kernel<true, false, false, false, 8, 2>, 9 * 32, r.tile_smem));
-            per_sm = std::max(1, per_sm);
-            r.tile_grid = std::max(1, std::min<int>(h.n_tiles, sms * per_sm));
+        const int S = p->stages;
+        std::vector<SmemMax> need(h.n_tiles);
+        std::vector<size_t> bytes(h.n_tiles);
+        for (int32_t t = 0; t < h.n_tiles; ++t) {
+            const TileMeta& tm = h.tile_meta[t];
+            const TileLayout L(tm, p->temp_dep, h.coords);
+            need[t] = SmemMax{L.bytes, cf_round(tm.ns, 2), L.scratch};
+            bytes[t] = tile_smem_bytes(need[t], S);
         }
+        size_t cut = 0;
+        if (h.n_tiles) {
+            std::vector<size_t> sorted = bytes;
+            const size_t q = std::min<size_t>(sorted.size() - 1, (size_t)(0.97 * (double)sorted.size()));
+            std::nth_element(sorted.begin(), sorted.begin() + q, sorted.end());
+            cut = sorted[q];
+        }
+        if (const char* e = std::getenv("CF_TILE_CLASSES"))
+            if (std::atoi(e) == 1) cut = SIZE_MAX;  // diagnostics: one launch for every tile
+        std::vector<int32_t> lists[2];
+        SmemMax mx[2];
+        for (int32_t t = 0; t < h.n_tiles; ++t) {
+            const int c = bytes[t] <= cut ? 0 : 1;
+            lists[c].push_back(t);
+            mx[c].blob = std::max(mx[c].blob, need[t].blob);
+            mx[c].slots = std::max(mx[c].slots, need[t].slots);
+            mx[c].scratch = std::max(mx[c].scratch, need[t].scratch);
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+        set_tile_attr(220 * 1024);  // per function (shared by every plan): the opt-in maximum
+        for (int c = 0; c < 2; ++c) {
+            if (lists[c].empty()) continue;
+            Rank::TileLaunch tl;
+            tl.a = a;
+            std::vector<TileDesc> desc(lists[c].size());
+            for (size_t i = 0; i < lists[c].size(); ++i) {
+                const int32_t t = lists[c][i];
+                desc[i] = TileDesc{h.tile_meta[t], h.tile_slot_off[t], 0, h.blob_off[t]};
+            }
+            tl.a.desc = M.up(desc, s);
+            tl.a.n_tiles = (int32_t)lists[c].size();
+            tl.a.max_slots = (int32_t)mx[c].slots;
+            tl.a.blob_smem = (int32_t)cf_round(mx[c].blob, 16);
+            tl.a.scratch_off = (int32_t)tile_scratch_off(mx[c], S);
+            tl.smem = tile_smem_bytes(mx[c], S);
+            if (tl.smem > 220 * 1024)
+                raise(CF_INVALID_ARG, "tile shared-memory footprint exceeds 220 KB; use smaller tiles");
+            int per_sm = 0;
+#define CF_OCC(NT, G)                                                                                \
+    if (p->tile_threads == NT && h.coords == G)                                                      \
+        CF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                 \
+            &per_sm, tile_kernel<true, false, false, false, NT, G>, NT, tl.smem));
+            CF_OCC(128, true) CF_OCC(256, true) CF_OCC(128, false) CF_OCC(256, false)
+#undef CF_OCC
+            per_sm = std::max(1, per_sm);
+            tl.grid = S == 1 ? tl.a.n_tiles : std::max(1, std::min<int>(tl.a.n_tiles, sms * per_sm));
+            r.launches.push_back(tl);
+            if (std::getenv("CF_TRACE_SETUP") && std::atoi(std::getenv("CF_TRACE_SETUP")))
+                std::fprintf(stderr, "[cf setup] rank %d class %d: %zu tiles, blob max %lld, slots max %lld, "
+                             "scratch max %lld, smem/CTA %zu B, %d CTAs/SM\n", h.rank, c, lists[c].size(),
+                             (long long)mx[c].blob, (long long)mx[c].slots, (long long)mx[c].scratch, tl.smem, per_sm);
+        }
+        r.tile_smem = r.launches.empty() ? 0 : r.launches[0].smem;
     }
 
     UpdArgs& u = r.ua;
@@ -636,7 +672,7 @@ void run_steps(cf_plan* p, int64_t n, double t_end) {
 // ------------------------------------------------------------------ lambda_max kernels
 struct LamArgs {
     TileArgs a;
-    bool tdep;
+    bool tdep, coords;
     const double* cval;  // per region rho*c(T0)
     const double* kval;  // per region k(T0)
     const double* hval;  // per facet kind
@@ -646,19 +682,43 @@ struct LamArgs {
     double* D;
 };
 
+// element i of a tile blob (global memory): gradients and volume, stored or recomputed
+__device__ void lam_geom(const LamArgs& L, const uint8_t* B, const TileLayout& Ly, int i, ushort4 cn,
+                         double (&g)[4][3], double& vol) {
+    if (L.coords) {
+        const double* X = (const double*)(B + Ly.xyz);
+        const unsigned short sl[4] = {cn.x, cn.y, cn.z, cn.w};
+        double p[4][3];
+        for (int k = 0; k < 4; ++k)
+            for (int c = 0; c < 3; ++c) p[k][c] = X[4 * sl[k] + c];
+        dev_tet_grads(p, g, vol);
+        return;
+    }
+    const double* G = (const double*)(B + Ly.geom);
+    const int S = Ly.ne2;
+    for (int k = 0; k < 3; ++k) {
+        g[1][k] = G[k * S + i];
+        g[2][k] = G[(3 + k) * S + i];
+        g[3][k] = G[(6 + k) * S + i];
+        g[0][k] = ((g[1][k] + g[2][k]) + g[3][k]) * -1.0;
+    }
+    vol = G[9 * S + i];
+}
+
 // lambda_max operator on the tile blobs (global reads, no shared memory)
 __global__ void lam_setup(LamArgs L) {
     const TileArgs& a = L.a;
     const int t = blockIdx.x;
     const TileMeta tm = a.meta[t];
-    const TileLayout Ly(tm, L.tdep);
+    const TileLayout Ly(tm, L.tdep, L.coords);
     const uint8_t* B = a.blob + a.blob_off[t];
     const int s0 = a.slot_off[t];
-    const double* G = (const double*)(B + Ly.geom);
     const ushort4* conn = (const ushort4*)(B + Ly.conn);
     for (int i = threadIdx.x; i < tm.ne; i += blockDim.x) {
         const ushort4 cn = conn[i];
-        const double w = L.cval[B[Ly.region + i]] * G[9 * Ly.ne2 + i] * 0.25;
+        double g[4][3], vol;
+        lam_geom(L, B, Ly, i, cn, g, vol);
+        const double w = L.cval[B[Ly.region + i]] * vol * 0.25;
         const unsigned short sl[4] = {cn.x, cn.y, cn.z, cn.w};
         for (int k = 0; k < 4; ++k) atomicAdd(&L.M[a.slot_node[s0 + sl[k]] & 0x0fffffff], w);
     }
@@ -676,24 +736,17 @@ __global__ void lam_apply(LamArgs L) {
     const TileArgs& a = L.a;
     const int t = blockIdx.x;
     const TileMeta tm = a.meta[t];
-    const TileLayout Ly(tm, L.tdep);
+    const TileLayout Ly(tm, L.tdep, L.coords);
     const uint8_t* B = a.blob + a.blob_off[t];
     const int s0 = a.slot_off[t];
-    const double* G = (const double*)(B + Ly.geom);
     const ushort4* conn = (const ushort4*)(B + Ly.conn);
-    const int S = Ly.ne2;
     for (int i = threadIdx.x; i < tm.ne; i += blockDim.x) {
         const ushort4 cn = conn[i];
         const int32_t n[4] = {a.slot_node[s0 + cn.x] & 0x0fffffff, a.slot_node[s0 + cn.y] & 0x0fffffff,
                               a.slot_node[s0 + cn.z] & 0x0fffffff, a.slot_node[s0 + cn.w] & 0x0fffffff};
-        double g[4][3];
-        for (int k = 0; k < 3; ++k) {
-            g[1][k] = G[k * S + i];
-            g[2][k] = G[(3 + k) * S + i];
-            g[3][k] = G[(6 + k) * S + i];
-            g[0][k] = ((g[1][k] + g[2][k]) + g[3][k]) * -1.0;
-        }
-        const double kv = L.kval[B[Ly.region + i]] * G[9 * S + i];
+        double g[4][3], vol;
+        lam_geom(L, B, Ly, i, cn, g, vol);
+        const double kv = L.kval[B[Ly.region + i]] * vol;
         double gx = 0, gy = 0, gz = 0;
         for (int b = 0; b < 4; ++b) {
             const double xb = L.x[n[b]];
@@ -803,6 +856,7 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         if (o.local_ranks != 1 && o.local_ranks != o.world_size)
             raise(CF_INVALID_ARG, "local_ranks must be 1 or world_size");
         if (o.mode != CF_MODE_ATOMIC && o.mode != CF_MODE_DETERMINISTIC) raise(CF_INVALID_ARG, "bad mode");
+        if (o.geometry != CF_GEOM_COORDS && o.geometry != CF_GEOM_STORED) raise(CF_INVALID_ARG, "bad geometry mode");
         int tile = o.tile_elems > 0 ? o.tile_elems : 384;
         if (tile > kMaxTileElems) raise(CF_INVALID_ARG, "tile_elems must be <= 2048");
 
@@ -832,6 +886,7 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         po.mode = o.mode;
         po.node_order = o.node_order;
         po.elem_order = o.elem_order;
+        po.geometry = o.geometry;
         po.tile_elems = tile;
         po.tile_of_element = o.tile_of_element;
         po.n_tiles_given = o.n_tiles_given;
@@ -854,12 +909,9 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         p->mode = o.mode;
         if (const char* e = std::getenv("CF_TILE_THREADS")) {
             const int v = std::atoi(e);
-            p->tile_threads = (v == 32 || v == 64 || v == 128) ? v : 256;
+            p->tile_threads = v == 256 ? 256 : 128;
         }
         if (const char* e = std::getenv("CF_TILE_STAGES")) p->stages = std::atoi(e) == 2 ? 2 : 1;
-        if (const char* e = std::getenv("CF_TILE_WS")) p->ws_stages = std::atoi(e) == 3 ? 3 : (std::atoi(e) == 2 ? 2 : 0);
-        if (S.temp_dep) p->ws_stages = 0;  // dynamic dt: no fused updates (tile_kernel path)
-        if (const char* e = std::getenv("CF_WS_WARPS")) p->ws_warps = std::atoi(e) == 4 ? 4 : 8;
         p->world = o.world_size;
         p->first_rank = o.rank;
         p->local_ranks = o.local_ranks;
@@ -872,6 +924,9 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         p->output_every = setup->output_every;
         p->t_end_setup = setup->t_end;
         CF_CUDA_CHECK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+        CF_CUDA_CHECK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+        CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
+        CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming));
         CF_CUDA_CHECK(cudaEventCreate(&p->ev0));
         CF_CUDA_CHECK(cudaEventCreate(&p->ev1));
         CF_CUDA_CHECK(cudaMalloc(&p->dP, sizeof(DevParams)));
@@ -893,7 +948,9 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
             trace_stage("upload");
             p->ranks.push_back(std::move(rk));
         }
-        p->launches_per_step = 2 * (int64_t)p->ranks.size() + (p->world > 1 ? (int64_t)p->ranks.size() : 0);
+        p->launches_per_step = 0;
+        for (const auto& rk : p->ranks)
+            p->launches_per_step += (int64_t)rk->launches.size() + 1 + (p->world > 1 ? 1 : 0);
         init_state(p.get(), S.T0.data());
         CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
         trace_stage("init state");
@@ -1133,6 +1190,7 @@ int cf_estimate_lambda_max(cf_plan* p, int32_t iterations, uint64_t seed, double
         LamArgs L;
         L.a = r.ta;
         L.tdep = p->temp_dep;
+        L.coords = r.H.coords;
         L.cval = M.up(cval, p->stream);
         L.kval = M.up(kval, p->stream);
         L.hval = M.up(hval, p->stream);
@@ -1263,6 +1321,7 @@ int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_r
         PlanOptions po;
         po.mode = opts->mode;
         po.elem_order = opts->elem_order;
+        po.geometry = opts->geometry;
         po.tile_elems = opts->tile_elems > 0 ? opts->tile_elems : 384;
         po.tile_of_element = opts->tile_of_element;
         po.world_size = std::max(1, opts->world_size);
@@ -1303,6 +1362,7 @@ int cf_exchange_plan(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const
         std::iota(label.begin(), label.end(), 0);
         PlanOptions po;
         po.elem_order = opts->elem_order;
+        po.geometry = opts->geometry;
         po.node_order = CF_NODE_ORDER_GIVEN;
         po.tile_elems = opts->tile_elems > 0 ? opts->tile_elems : 384;
         po.world_size = opts->world_size;

@@ -181,8 +181,10 @@ struct RankPlan {
     std::vector<int32_t> tile_slot_off;    // [n_tiles+1]
     std::vector<int64_t> blob_off;         // [n_tiles+1] byte offsets into blob
     std::vector<uint8_t, UninitAlloc<uint8_t>> blob;  // all tile blobs
+    bool coords = false;                   // CF_GEOM_COORDS layout (cf_tileblob.hpp)
     int32_t max_slots = 0, max_elems = 0, max_facets = 0;
     int64_t max_blob = 0;
+    int64_t max_scratch = 0;               // coordinates layout: contribution scratch doubles
     std::vector<int32_t> elem_global;      // [E_r] tile order
     std::vector<int32_t> slot_node;        // [S] local node id
     int64_t n_bc_facets = 0, n_if_facets = 0;
@@ -214,6 +216,7 @@ struct PlanOptions {
     int node_order = CF_NODE_ORDER_RCM;
     int elem_order = CF_ELEM_ORDER_MORTON;
     int tile_elems = 1024;
+    int geometry = CF_GEOM_STORED;
     const int32_t* tile_of_element = nullptr;
     int32_t n_tiles_given = 0;
     int world_size = 1;

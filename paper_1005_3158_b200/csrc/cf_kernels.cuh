@@ -134,38 +134,59 @@ struct TileArgs {
     double* acc_r;
     const DevParams* P;
     DevState* st;
-    int32_t n_tiles;
+    const TileDesc* desc;      // tiles of this launch (metadata + offsets, one 32 B record each)
+    int32_t n_tiles;           // tiles of this launch
     int32_t max_slots;
     int32_t blob_smem;   // bytes reserved per blob stage in shared memory
     int32_t stages;      // 1: one tile per CTA; 2: persistent, double-buffered
-    int32_t probe;       // diagnostics only: 1 = stop after the blob lands, 2 = after the gather
+    int32_t scratch_off; // coordinates layout: byte offset of the contribution scratch in shared memory
+    int32_t probe;       // diagnostics only (CF_PROBE; results invalid): 1 = copies only, 3 = no
+                         // reduction phase, 4 = no element phase, 5 = no enthalpy evaluation
     double t_end;
 };
 
 constexpr uint32_t kBulkChunk = 32768;
 
-__device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int t, bool tdep, uint8_t* dst, double* sTdst,
-                                                uint64_t* bar) {
-    const TileMeta tm = a.meta[t];
-    const TileLayout L(tm, tdep);
-    const uint32_t tbytes = 8u * (uint32_t)cf_round(tm.ns, 2);
+struct TileHdr {  // per stage: the metadata of the tile in flight (written before the barrier arrive)
+    TileMeta tm;
+    int32_t s0;
+};
+
+// `it` indexes the launch's tile descriptors
+__device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int it, bool tdep, bool coords, uint8_t* dst,
+                                                double* sTdst, uint64_t* bar, TileHdr* hdr) {
+    const int4 d0 = __ldg((const int4*)(a.desc + it)), d1 = __ldg((const int4*)(a.desc + it) + 1);
+    const TileMeta tm{d0.x, d0.y, d0.z, d0.w};
+    const int32_t s0 = d1.x;
+    const int64_t boff = (int64_t)(uint32_t)d1.z | (int64_t)d1.w << 32;
+    hdr->tm = tm;  // published by the arrive below (release), read after the wait (acquire)
+    hdr->s0 = s0;
+    const TileLayout L(tm, tdep, coords);
+    const uint32_t tbytes = 8u * (uint32_t)cf_round32(tm.ns, 2);
     mbar_expect_tx(bar, (uint32_t)L.bytes + tbytes);
-    const uint8_t* src = a.blob + a.blob_off[t];
+    const uint8_t* src = a.blob + boff;
     for (int64_t o = 0; o < L.bytes; o += kBulkChunk) {
         const uint32_t n = (uint32_t)(L.bytes - o < kBulkChunk ? L.bytes - o : kBulkChunk);
         bulk_g2s(dst + o, src + o, n, bar);
     }
-    if (tbytes) bulk_g2s(sTdst, a.Tslot + a.slot_off[t], tbytes, bar);
+    if (tbytes) bulk_g2s(sTdst, a.Tslot + s0, tbytes, bar);
 }
 
 // Each CTA walks tiles blockIdx.x, +gridDim.x, ...; with stages == 2 it is a
 // persistent two-stage TMA pipeline (the blob of tile k+1 streams in while
 // tile k is computed), with stages == 1 the grid covers the tiles one-to-one.
-template <bool DET, bool TDEP, bool DIR, bool CLAMP, int kTileThreads>
-__global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
+#ifndef CF_GC_MINB
+#define CF_GC_MINB 1  // min resident CTAs per SM requested from ptxas (coordinates layout)
+#endif
+#ifndef CF_GS_MINB
+#define CF_GS_MINB 1  // min resident CTAs per SM requested from ptxas (stored layout)
+#endif
+template <bool DET, bool TDEP, bool DIR, bool CLAMP, int kTileThreads, bool GC>
+__global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) tile_kernel(TileArgs a) {
     constexpr bool FUSE = !TDEP;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t bar[2];
+    __shared__ TileHdr hdr[2];
     __shared__ DevMaterial sMat[kMaxRegions];
     const int tid = threadIdx.x;
     const DevParams* __restrict__ P = a.P;
@@ -175,22 +196,23 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
     double* const sT1 = sT0 + (a.stages - 1) * a.max_slots;
     double2* sTH = (double2*)(sT0 + a.stages * a.max_slots);  // (T, H) per slot, 16 B aligned
 
+    // the first copy is the CTA's critical path: thread 0 initialises the barriers and issues it
+    // before anything else; the material table, the step's dt and the scratch zeros overlap it
+    // (the other threads touch the barriers only after the __syncthreads below)
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        if (blockIdx.x < a.n_tiles) issue_tile_copy(a, blockIdx.x, TDEP, GC, buf0, sT0, &bar[0], &hdr[0]);
+        if (a.stages == 2 && blockIdx.x + gridDim.x < a.n_tiles)
+            issue_tile_copy(a, blockIdx.x + gridDim.x, TDEP, GC, buf1, sT1, &bar[1], &hdr[1]);
     }
     for (int i = tid; i < P->n_materials; i += kTileThreads) sMat[i] = P->mat[i];
-    __syncthreads();  // barriers initialised, material table staged
-    // the copies are issued after the barrier: no warp waits on thread 0's global loads
-    if (tid == 0) {
-        if (blockIdx.x < a.n_tiles) issue_tile_copy(a, blockIdx.x, TDEP, buf0, sT0, &bar[0]);
-        if (a.stages == 2 && blockIdx.x + gridDim.x < a.n_tiles)
-            issue_tile_copy(a, blockIdx.x + gridDim.x, TDEP, buf1, sT1, &bar[1]);
-    }
+    if (GC && tid < 2) ((double*)(smem + a.scratch_off))[tid] = 0.0;  // the facet entries' lump operand
     double dt = 0, t_next = 0;
     bool done = false;
     if (FUSE) step_dt<TDEP>(P, a.st, a.t_end, dt, t_next, done);
     const double time = a.st->time;
+    __syncthreads();  // barriers initialised, material table staged
     int clamped = 0;
     double local_min = __longlong_as_double(0x7ff0000000000000ll);
 
@@ -199,44 +221,61 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
         const int stage = a.stages == 2 ? (k & 1) : 0;
         uint8_t* B = stage ? buf1 : buf0;
         double* sT = stage ? sT1 : sT0;
-        const TileMeta tm = a.meta[t];
-        const TileLayout L(tm, TDEP);
-        const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
-        const int s0 = a.slot_off[t];
         mbar_wait(&bar[stage], a.stages == 2 ? ((k >> 1) & 1) : (k & 1));
+        const TileMeta tm = hdr[stage].tm;
+        const int s0 = hdr[stage].s0;
+        const TileLayout L(tm, TDEP, GC);
+        const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
         if (a.probe == 1) {  // diagnostics: memory-path timing without the physics
             __syncthreads();
             if (tid == 0 && t + a.stages * (int)gridDim.x < a.n_tiles)
-                issue_tile_copy(a, t + a.stages * gridDim.x, TDEP, B, sT, &bar[stage]);
+                issue_tile_copy(a, t + a.stages * gridDim.x, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
             continue;
         }
         // phase 1: H = enthalpy(T) per slot (blocked.hpp:462-467) from the streamed slot temperatures
         const uint8_t* sinfo = B + L.sinfo;
         for (int s = tid; s < ns; s += kTileThreads) {
             const double T = sT[s];
-            sTH[s] = make_double2(T, dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], T));
+            sTH[s] = make_double2(T, a.probe == 5 ? T : dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], T));
         }
         __syncthreads();
 
-        // phase 2a: elements (element_accumulate fem.hpp:57-70); contributions overwrite
-        // this element's consumed geometry columns: lump -> col 0, rc[k] -> col 1+k
+        // phase 2a: elements (element_accumulate fem.hpp:57-70). Contributions go to the
+        // contrib columns (lump -> col 0, rc[k] -> col 1+k): with stored geometry these
+        // are this element's consumed geometry columns, with coordinates a scratch area
         double* G = (double*)(B + L.geom);
+        double* R = GC ? (double*)(smem + a.scratch_off) : (double*)B;  // reduction operand base
         const int S = L.ne2;
         const ushort4* conn = (const ushort4*)(B + L.conn);
         const uint8_t* ereg = B + L.region;
-        for (int i = tid; i < ne; i += kTileThreads) {
-            double g[4][3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                g[1][c] = G[c * S + i];
-                g[2][c] = G[(3 + c) * S + i];
-                g[3][c] = G[(6 + c) * S + i];
-            }
-            const double vol = G[9 * S + i];
-            const double max_edge = G[10 * S + i];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) g[0][c] = ((g[1][c] + g[2][c]) + g[3][c]) * -1.0;
+        for (int i = tid; i < (a.probe == 4 ? 0 : ne); i += kTileThreads) {
+            double g[4][3], vol, max_edge;
             const ushort4 cn = conn[i];
+            if (GC) {
+                const double2* X = (const double2*)(B + L.xyz);  // slot (x, y) (z, 0)
+                const unsigned short sl[4] = {cn.x, cn.y, cn.z, cn.w};
+                double p[4][3];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const double2 xy = X[2 * sl[k]], z0 = X[2 * sl[k] + 1];
+                    p[k][0] = xy.x;
+                    p[k][1] = xy.y;
+                    p[k][2] = z0.x;
+                }
+                dev_tet_grads(p, g, vol);
+                max_edge = G[i];
+            } else {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    g[1][c] = G[c * S + i];
+                    g[2][c] = G[(3 + c) * S + i];
+                    g[3][c] = G[(6 + c) * S + i];
+                }
+                vol = G[9 * S + i];
+                max_edge = G[10 * S + i];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) g[0][c] = ((g[1][c] + g[2][c]) + g[3][c]) * -1.0;
+            }
             const double2 th0 = sTH[cn.x], th1 = sTH[cn.y], th2 = sTH[cn.z], th3 = sTH[cn.w];
             const double T[4] = {th0.x, th1.x, th2.x, th3.x};
             const double H[4] = {th0.y, th1.y, th2.y, th3.y};
@@ -245,12 +284,12 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
             dev_element<TDEP>(P, m, g, vol, max_edge, T, H, lump, rc);
             if (TDEP)
                 local_min = fmin(local_min, dev_stable_bound<TDEP>(P, m, ((const double*)(B + L.minedge))[i], T));
-            G[i] = lump;
+            R[L.lump_idx(i)] = lump;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) G[(1 + c) * S + i] = rc[c];
+            for (int c = 0; c < 4; ++c) R[L.rc_idx(i, c)] = rc[c];
         }
         // phase 2b: facets (facet_flux_accumulate fem.hpp:74-79; interface blocked.hpp:485-490);
-        // terms overwrite the facet's area (a=0) and sister (a=1,2) slots
+        // terms go to R[fac_idx] (stored layout: over the facet's consumed area / sister slots)
         double* farea = (double*)(B + L.farea);
         double* fsis = (double*)(B + L.fsister);
         const ushort4* fsl = (const ushort4*)(B + L.fslots);
@@ -281,39 +320,35 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
             const double f1 = third * (-q + h * (tinf - ts[1]));
             const double f2 = third * (-q + h * (tinf - ts[2]));
             // stored negated: the reduction does r -= v for every entry (r - (-f) == r + f exactly)
-            farea[i] = -f0;
-            fsis[2 * i] = -f1;
-            fsis[2 * i + 1] = -f2;
+            R[L.fac_idx(i, 0)] = -f0;
+            R[L.fac_idx(i, 1)] = -f1;
+            R[L.fac_idx(i, 2)] = -f2;
         }
         __syncthreads();
 
-        // phase 3: per-slot fixed-order reduction (ascending element, then facets) + flush
+        // phase 3: per-slot fixed-order reduction (ascending element, then facets) + flush.
+        // Each entry is a precomputed (lump, residual) operand pair: element e, corner q ->
+        // (lump[e], rc_q[e]); facet f, corner a -> (0.0, -term_a[f]).
         const uint16_t* cend = (const uint16_t*)(B + L.csr_end);
-        const uint16_t* csr = (const uint16_t*)(B + L.csr);
+        const uint32_t* csr = (const uint32_t*)(B + L.csr);
         const int32_t* snode = (const int32_t*)(B + L.snode);
-        const int e4 = 4 * ne;
-        // entry decode (branch-free): element e*4+k -> c += lump[e], r -= rc_k[e];
-        // facet 4*ne+4*f+a -> c += 0.0, r -= (-term). Indices are in doubles from B.
-        const double* Bd = (const double*)B;
-        const int gofs = (int)(L.geom >> 3), zofs = (int)(L.zero >> 3);
-        const int fa_ofs = (int)(L.farea >> 3), fs_ofs = (int)(L.fsister >> 3) - 1;
-        auto decode = [&](int code, int& li, int& ri) {
-            const bool fac = code >= e4;
-            const int q = code & 3;
-            const int e = code >> 2;
-            const int f = (code - e4) >> 2;
-            li = fac ? zofs : gofs + e;
-            ri = fac ? (q == 0 ? fa_ofs + f : fs_ofs + 2 * f + q) : gofs + (1 + q) * S + e;
-        };
-        for (int s = tid; s < ns; s += kTileThreads) {
+        for (int s = tid; s < (a.probe == 3 ? 0 : ns); s += kTileThreads) {
             const int beg = s == 0 ? 0 : cend[s - 1];
             const int end = cend[s];
             double c = 0, r = 0;
-            for (int j = beg; j < end; ++j) {
-                int li, ri;
-                decode(csr[j], li, ri);
-                c += Bd[li];
-                r -= Bd[ri];
+            for (int j = beg; j < end; j += 4) {  // lists padded to 4 with exact (0.0, 0.0) no-ops
+                const uint4 pr = *(const uint4*)(csr + j);
+                const double l0 = R[pr.x & 0xffffu], l1 = R[pr.y & 0xffffu], l2 = R[pr.z & 0xffffu],
+                             l3 = R[pr.w & 0xffffu];
+                const double q0 = R[pr.x >> 16], q1 = R[pr.y >> 16], q2 = R[pr.z >> 16], q3 = R[pr.w >> 16];
+                c += l0;
+                r -= q0;
+                c += l1;
+                r -= q1;
+                c += l2;
+                r -= q2;
+                c += l3;
+                r -= q3;
             }
             const int info = sinfo[s];
             const int32_t node = snode[s];
@@ -342,247 +377,8 @@ __global__ void __launch_bounds__(kTileThreads) tile_kernel(TileArgs a) {
             // generic-proxy writes to B (in-place contributions) must be ordered
             // before the async-proxy (TMA) overwrite of the same buffer
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_tile_copy(a, t + a.stages * gridDim.x, TDEP, B, sT, &bar[stage]);
+            issue_tile_copy(a, t + a.stages * gridDim.x, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
         }
-    }
-    if (TDEP) {
-        for (int o = 16; o > 0; o >>= 1) local_min = fmin(local_min, __shfl_xor_sync(0xffffffffu, local_min, o));
-        if ((tid & 31) == 0) atomic_min_pos(&a.st->min_bound[a.st->step_index & 1], local_min);
-    }
-    if (CLAMP && clamped) a.st->clamp_flag = 1;
-}
-
-// ------------------------------------------------------------------ warp-specialised tile kernel
-// Persistent producer/consumer pipeline (the default on large meshes):
-//  - warp NCW (producer): its 32 lanes prefetch the metadata of the next 32
-//    tiles, lane 0 streams each tile's blob + slot temperatures into a ring of
-//    NS shared-memory stages with TMA bulk copies on full[s] (complete_tx),
-//    after the consumers released the stage on empty[s];
-//  - warps 0..NCW-1 (consumers): the three phases of tile_kernel, separated by
-//    a named barrier among consumers only; they release a stage after a
-//    generic->async proxy fence (their contributions are written in place).
-// Consumers never wait on a copy that was not issued a full tile earlier.
-struct StageHdr {
-    TileMeta tm;
-    int32_t s0, t;
-    int32_t pad[2];
-};
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void named_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-template <bool DET, bool TDEP, bool DIR, bool CLAMP, int NCW, int NS>
-__global__ void __launch_bounds__((NCW + 1) * 32, NCW == 4 ? 4 : 1) tile_ws_kernel(TileArgs a) {
-    constexpr bool FUSE = !TDEP;
-    constexpr int NC = NCW * 32;  // consumer threads
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint64_t full[NS], empty[NS];
-    __shared__ DevMaterial sMat[kMaxRegions];
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const DevParams* __restrict__ P = a.P;
-    // stage s: [StageHdr 32 B][blob blob_smem][T slots 8*max_slots]; then NS x (T,H) 16*max_slots
-    const size_t stage_bytes = 32 + (size_t)a.blob_smem + 8 * (size_t)a.max_slots;
-    double2* const sTHall = (double2*)(smem + NS * stage_bytes);
-
-    if (tid == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCW);
-        }
-    }
-    for (int i = tid; i < P->n_materials; i += blockDim.x) sMat[i] = P->mat[i];
-    __syncthreads();
-
-    if (warp == NCW) {  // ---------------- producer warp
-        const int lane = tid & 31;
-        int k = 0;
-        for (int t0 = blockIdx.x; t0 < a.n_tiles; t0 += 32 * gridDim.x) {
-            const int tl = t0 + lane * gridDim.x;  // this lane prefetches tile tl's metadata
-            int ne = 0, ns = 0, nf = 0, ncsr = 0, s0 = 0;
-            long long boff = 0;
-            if (tl < a.n_tiles) {
-                const TileMeta m = a.meta[tl];
-                ne = m.ne;
-                ns = m.ns;
-                nf = m.nf;
-                ncsr = m.ncsr;
-                s0 = a.slot_off[tl];
-                boff = a.blob_off[tl];
-            }
-            for (int j = 0; j < 32; ++j) {
-                const int t = t0 + j * gridDim.x;
-                if (t >= a.n_tiles) break;
-                const TileMeta m{__shfl_sync(0xffffffffu, ne, j), __shfl_sync(0xffffffffu, ns, j),
-                                 __shfl_sync(0xffffffffu, nf, j), __shfl_sync(0xffffffffu, ncsr, j)};
-                const int ts0 = __shfl_sync(0xffffffffu, s0, j);
-                const long long tb = __shfl_sync(0xffffffffu, boff, j);
-                if (lane == 0) {
-                    const int s = k % NS;
-                    if (k >= NS) mbar_wait(&empty[s], ((k / NS) - 1) & 1);
-                    unsigned char* base = smem + (size_t)s * stage_bytes;
-                    StageHdr* hdr = (StageHdr*)base;
-                    hdr->tm = m;
-                    hdr->s0 = ts0;
-                    hdr->t = t;
-                    const TileLayout L(m, TDEP);
-                    const uint32_t tbytes = 8u * (uint32_t)cf_round(m.ns, 2);
-                    mbar_expect_tx(&full[s], (uint32_t)L.bytes + tbytes);
-                    const uint8_t* src = a.blob + tb;
-                    for (int64_t o = 0; o < L.bytes; o += kBulkChunk) {
-                        const uint32_t n = (uint32_t)(L.bytes - o < kBulkChunk ? L.bytes - o : kBulkChunk);
-                        bulk_g2s(base + 32 + o, src + o, n, &full[s]);
-                    }
-                    if (tbytes) bulk_g2s(base + 32 + a.blob_smem, a.Tslot + ts0, tbytes, &full[s]);
-                }
-                __syncwarp();
-                ++k;
-            }
-        }
-        return;
-    }
-
-    // ---------------- consumer warps
-    double dt = 0, t_next = 0;
-    bool done = false;
-    if (FUSE) step_dt<TDEP>(P, a.st, a.t_end, dt, t_next, done);
-    const double time = a.st->time;
-    int clamped = 0;
-    double local_min = __longlong_as_double(0x7ff0000000000000ll);
-    int k = 0;
-    for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x, ++k) {
-        const int st = k % NS;
-        mbar_wait(&full[st], (k / NS) & 1);
-        unsigned char* base = smem + (size_t)st * stage_bytes;
-        const StageHdr hdr = *(const StageHdr*)base;
-        uint8_t* B = base + 32;
-        const double* sT = (const double*)(base + 32 + a.blob_smem);
-        double2* sTH = sTHall + (size_t)st * a.max_slots;
-        const TileMeta tm = hdr.tm;
-        const TileLayout L(tm, TDEP);
-        const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
-        const int s0 = hdr.s0;
-        const uint8_t* sinfo = B + L.sinfo;
-        // phase 1: (T, H) per slot
-        for (int s = tid; s < ns; s += NC) {
-            const double T = sT[s];
-            sTH[s] = make_double2(T, dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], T));
-        }
-        named_sync(1, NC);
-        // phase 2a: elements
-        double* G = (double*)(B + L.geom);
-        const int S = L.ne2;
-        const ushort4* conn = (const ushort4*)(B + L.conn);
-        const uint8_t* ereg = B + L.region;
-        for (int i = tid; i < ne; i += NC) {
-            double g[4][3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                g[1][c] = G[c * S + i];
-                g[2][c] = G[(3 + c) * S + i];
-                g[3][c] = G[(6 + c) * S + i];
-            }
-            const double vol = G[9 * S + i];
-            const double max_edge = G[10 * S + i];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) g[0][c] = ((g[1][c] + g[2][c]) + g[3][c]) * -1.0;
-            const ushort4 cn = conn[i];
-            const double2 th0 = sTH[cn.x], th1 = sTH[cn.y], th2 = sTH[cn.z], th3 = sTH[cn.w];
-            const double T[4] = {th0.x, th1.x, th2.x, th3.x};
-            const double H[4] = {th0.y, th1.y, th2.y, th3.y};
-            const DevMaterial& m = sMat[ereg[i]];
-            double lump, rc[4];
-            dev_element<TDEP>(P, m, g, vol, max_edge, T, H, lump, rc);
-            if (TDEP)
-                local_min = fmin(local_min, dev_stable_bound<TDEP>(P, m, ((const double*)(B + L.minedge))[i], T));
-            G[i] = lump;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) G[(1 + c) * S + i] = rc[c];
-        }
-        // phase 2b: facets
-        double* farea = (double*)(B + L.farea);
-        double* fsis = (double*)(B + L.fsister);
-        const ushort4* fsl = (const ushort4*)(B + L.fslots);
-        for (int i = tid; i < nf; i += NC) {
-            const ushort4 fs = fsl[i];
-            const DevFacetKind& K = P->kind[fs.w];
-            const double ts[3] = {sTH[fs.x].x, sTH[fs.y].x, sTH[fs.z].x};
-            double q, h, tinf;
-            if (K.interface) {
-                const double var = K.var == CF_VAR_TIME ? time : (ts[0] + ts[1] + ts[2]) / 3.0;
-                q = 0.0;
-                h = dev_pl_eval(P, K.htab, var);
-                const int4 sn = ((const int4*)fsis)[i];
-                double sum = 0;
-                sum += a.Told[sn.x];
-                sum += a.Told[sn.y];
-                sum += a.Told[sn.z];
-                sum += a.Told[sn.w];
-                tinf = 0.25 * sum;
-            } else {
-                q = K.q;
-                h = K.h;
-                tinf = K.t_inf;
-            }
-            const double third = farea[i] / 3.0;
-            const double f0 = third * (-q + h * (tinf - ts[0]));
-            const double f1 = third * (-q + h * (tinf - ts[1]));
-            const double f2 = third * (-q + h * (tinf - ts[2]));
-            farea[i] = -f0;
-            fsis[2 * i] = -f1;
-            fsis[2 * i + 1] = -f2;
-        }
-        named_sync(1, NC);
-        // phase 3: fixed-order reduction + flush
-        const uint16_t* cend = (const uint16_t*)(B + L.csr_end);
-        const uint16_t* csr = (const uint16_t*)(B + L.csr);
-        const int32_t* snode = (const int32_t*)(B + L.snode);
-        const int e4 = 4 * ne;
-        const double* Bd = (const double*)B;
-        const int gofs = (int)(L.geom >> 3), zofs = (int)(L.zero >> 3);
-        const int fa_ofs = (int)(L.farea >> 3), fs_ofs = (int)(L.fsister >> 3) - 1;
-        for (int s = tid; s < ns; s += NC) {
-            const int beg = s == 0 ? 0 : cend[s - 1];
-            const int end = cend[s];
-            double c = 0, r = 0;
-            for (int j = beg; j < end; ++j) {
-                const int code = csr[j];
-                const bool fac = code >= e4;
-                const int q = code & 3;
-                const int li = fac ? zofs : gofs + (code >> 2);
-                const int ri = fac ? (q == 0 ? fa_ofs + ((code - e4) >> 2) : fs_ofs + 2 * ((code - e4) >> 2) + q)
-                                   : gofs + (1 + q) * S + (code >> 2);
-                c += Bd[li];
-                r -= Bd[ri];
-            }
-            const int info = sinfo[s];
-            const int32_t node = snode[s];
-            if (FUSE && (info & 0x80)) {
-                double Tn;
-                if (done) {
-                    Tn = sTH[s].x;
-                } else {
-                    const int dir = (DIR && (info & 0x40)) ? a.node_dir[node] : -1;
-                    Tn = node_update<DIR, CLAMP>(P, a.st, sTH[s].x, c, r, dt, t_next, dir, info & 0x3f,
-                                                 a.local_global + node, clamped);
-                }
-                a.Tn[node] = Tn;
-                a.Tslot_n[s0 + s] = Tn;
-            } else if (DET) {
-                a.part[s0 + s] = make_double2(c, r);
-            } else {
-                atomicAdd(&a.acc_c[node], c);
-                atomicAdd(&a.acc_r[node], r);
-            }
-        }
-        // release the stage (generic-proxy writes ordered before the next TMA overwrite)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty[st]);
     }
     if (TDEP) {
         for (int o = 16; o > 0; o >>= 1) local_min = fmin(local_min, __shfl_xor_sync(0xffffffffu, local_min, o));

@@ -67,6 +67,39 @@ __device__ __forceinline__ double dev_enthalpy(const DevParams* __restrict__ P, 
     return sensible + m.latent * mf;
 }
 
+// Element gradients and volume from the oriented corner coordinates: the
+// operation sequence of the host tet_geometry (cf_mesh.cpp; geometry.hpp:50-79):
+// e_k = p_k - p0, c = e2 x e3, det = e1.c, vol = det/6, g1 = (e2 x e3)/det,
+// g2 = (e3 x e1)/det, g3 = (e1 x e2)/det (as products with inv = 1/det),
+// g0 = ((g1+g2)+g3)*-1. With -fmad=false and IEEE '/', bitwise equal to the
+// stored ElementGeom.
+__device__ __forceinline__ void dev_tet_grads(const double (&p)[4][3], double (&g)[4][3], double& vol) {
+    double e1[3], e2[3], e3[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        e1[k] = p[1][k] - p[0][k];
+        e2[k] = p[2][k] - p[0][k];
+        e3[k] = p[3][k] - p[0][k];
+    }
+    const double c0 = e2[1] * e3[2] - e2[2] * e3[1];
+    const double c1 = e2[2] * e3[0] - e2[0] * e3[2];
+    const double c2 = e2[0] * e3[1] - e2[1] * e3[0];
+    const double det = e1[0] * c0 + e1[1] * c1 + e1[2] * c2;
+    vol = det / 6.0;
+    const double inv = 1.0 / det;
+    g[1][0] = c0 * inv;
+    g[1][1] = c1 * inv;
+    g[1][2] = c2 * inv;
+    g[2][0] = (e3[1] * e1[2] - e3[2] * e1[1]) * inv;
+    g[2][1] = (e3[2] * e1[0] - e3[0] * e1[2]) * inv;
+    g[2][2] = (e3[0] * e1[1] - e3[1] * e1[0]) * inv;
+    g[3][0] = (e1[1] * e2[2] - e1[2] * e2[1]) * inv;
+    g[3][1] = (e1[2] * e2[0] - e1[0] * e2[2]) * inv;
+    g[3][2] = (e1[0] * e2[1] - e1[1] * e2[0]) * inv;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g[0][k] = ((g[1][k] + g[2][k]) + g[3][k]) * -1.0;
+}
+
 // One element: lumped capacitance share `lump` (added to each of the 4
 // nodes) and the 4 conduction residual terms rc[a] (subtracted).
 // g1..g3 are the stored gradients; g0 = (g1+g2+g3)*-1.0 (geometry.hpp:75).

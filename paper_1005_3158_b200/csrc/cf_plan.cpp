@@ -286,6 +286,8 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                      const std::vector<int32_t>& node_label, int32_t rank, RankPlan& rp) {
     rp = RankPlan{};
     rp.rank = rank;
+    rp.coords = o.geometry == CF_GEOM_COORDS;
+    const bool coords = rp.coords;
     const int32_t W = o.world_size;
     auto part_of = [&](int32_t e) { return W > 1 ? o.part_of_element[e] : 0; };
 
@@ -548,22 +550,29 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             for (size_t k = 0; k < idx.size(); ++k) sorted[k] = tnodes[idx[k]];
             tnodes.swap(sorted);
             const int ne = (int)te.size(), ns = (int)tnodes.size(), nf = (int)tfacets.size();
-            rp.tile_meta[t] = TileMeta{ne, ns, nf, 4 * ne + 3 * nf};
+            int ncsr = 0;  // each slot's list padded to a multiple of 4 (16-byte reads in the reduction)
+            for (int32_t cn : cnt_of) ncsr += (cn + 3) & ~3;
+            rp.tile_meta[t] = TileMeta{ne, ns, nf, ncsr};
         }
     }
-    for (int32_t t = 0; t < rp.n_tiles; ++t)  // no throwing inside the parallel regions
-        if (4 * rp.tile_meta[t].ne + 4 * rp.tile_meta[t].nf > 65535)
-            raise(CF_INVALID_ARG, "tile csr exceeds 16-bit codes");
+    for (int32_t t = 0; t < rp.n_tiles; ++t) {  // no throwing inside the parallel regions
+        const TileMeta& tm = rp.tile_meta[t];
+        const TileLayout L(tm, S.temp_dep, coords);
+        if (4 * tm.ne + 4 * tm.nf > 65535 || tm.ncsr > 65535 || L.fac_idx(tm.nf, 2) > 65535 || L.rc_idx(tm.ne, 3) > 65535 ||
+            L.r_zero > 65535)
+            raise(CF_INVALID_ARG, "tile too large for 16-bit slot / operand indices");
+    }
     for (int32_t t = 0; t < rp.n_tiles; ++t) {
         const TileMeta& tm = rp.tile_meta[t];
-        const TileLayout L(tm, S.temp_dep);
+        const TileLayout L(tm, S.temp_dep, coords);
         rp.blob_off[t + 1] = rp.blob_off[t] + L.bytes;
         rp.tile_slot_off[t + 1] = rp.tile_slot_off[t] + (int32_t)cf_round(tm.ns, 2);  // 16 B aligned Tslot segments
         elem_off[t + 1] = elem_off[t] + tm.ne;
         rp.max_elems = std::max(rp.max_elems, tm.ne);
         rp.max_slots = std::max(rp.max_slots, (int32_t)cf_round(tm.ns, 2));
         rp.max_facets = std::max(rp.max_facets, tm.nf);
-        rp.max_blob = std::max(rp.max_blob, L.bytes);
+        rp.max_blob = std::max<int64_t>(rp.max_blob, L.bytes);
+        rp.max_scratch = std::max<int64_t>(rp.max_scratch, L.scratch);
     }
     rp.blob.resize(rp.blob_off[rp.n_tiles]);
     rp.slot_node.resize(rp.tile_slot_off[rp.n_tiles]);
@@ -571,14 +580,15 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
 #pragma omp parallel num_threads(nthr) reduction(+ : n_if, n_bc)
     {
         std::vector<int32_t> slot_of(rp.n_local, -1), tfacets;
-        std::vector<int32_t> ent_off, ent, cur;
+        std::vector<int32_t> ent_off, cur;
+        std::vector<uint32_t> ent;
 #pragma omp for schedule(dynamic, 64)
         for (int32_t t = 0; t < rp.n_tiles; ++t) {
             const auto& te = tiles[t];
             const auto& tnodes = tile_nodes[t];
             const TileMeta tm = rp.tile_meta[t];
             const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
-            const TileLayout L(tm, S.temp_dep);
+            const TileLayout L(tm, S.temp_dep, coords);
             uint8_t* B = rp.blob.data() + rp.blob_off[t];
             std::memset(B, 0, (size_t)L.bytes);
             for (int k = 0; k < ns; ++k) slot_of[tnodes[k]] = k;
@@ -593,22 +603,39 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             ent.resize(ent_off[ns]);
             {
                 cur.assign(ent_off.begin(), ent_off.end() - 1);
+                // (lump, residual) operand pair of every contribution (reduction order)
                 for (int i = 0; i < ne; ++i)
                     for (int a = 0; a < 4; ++a)
-                        ent[cur[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]]]++] = 4 * i + a;
+                        ent[cur[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]]]++] =
+                            (uint32_t)L.lump_idx(i) | (uint32_t)L.rc_idx(i, a) << 16;
                 for (int i = 0; i < nf; ++i)
                     for (int a = 0; a < 3; ++a)
-                        ent[cur[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]]]++] = 4 * ne + 4 * i + a;
+                        ent[cur[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]]]++] =
+                            (uint32_t)L.r_zero | (uint32_t)L.fac_idx(i, a) << 16;
             }
             double* gsec = (double*)(B + L.geom);
             uint16_t* csec = (uint16_t*)(B + L.conn);
+            if (coords) {
+                double* xyz = (double*)(B + L.xyz);
+                for (int k = 0; k < ns; ++k) {
+                    const double* p = m.pos(lnodes[tnodes[k]]);
+                    xyz[4 * k] = p[0];
+                    xyz[4 * k + 1] = p[1];
+                    xyz[4 * k + 2] = p[2];
+                    xyz[4 * k + 3] = 0.0;
+                }
+            }
             for (int i = 0; i < ne; ++i) {
                 const int32_t e = te[i];
                 rp.elem_global[elem_off[t] + i] = e;
                 const Geom g = m.geometry(e);
-                const double vals[11] = {g.g[1][0], g.g[1][1], g.g[1][2], g.g[2][0], g.g[2][1], g.g[2][2],
-                                         g.g[3][0], g.g[3][1], g.g[3][2], g.vol,     g.max_edge};
-                for (int k = 0; k < 11; ++k) gsec[(size_t)k * L.ne2 + i] = vals[k];
+                if (coords) {
+                    gsec[i] = g.max_edge;
+                } else {
+                    const double vals[11] = {g.g[1][0], g.g[1][1], g.g[1][2], g.g[2][0], g.g[2][1], g.g[2][2],
+                                             g.g[3][0], g.g[3][1], g.g[3][2], g.vol,     g.max_edge};
+                    for (int k = 0; k < 11; ++k) gsec[(size_t)k * L.ne2 + i] = vals[k];
+                }
                 if (S.temp_dep) ((double*)(B + L.minedge))[i] = g.min_edge;
                 for (int a = 0; a < 4; ++a) csec[4 * i + a] = (uint16_t)slot_of[local_of[m.tets[4 * (size_t)e + a]]];
                 B[L.region + i] = (uint8_t)m.region[e];
@@ -632,9 +659,10 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                 }
             }
             uint16_t* cend = (uint16_t*)(B + L.csr_end);
-            uint16_t* csr = (uint16_t*)(B + L.csr);
+            uint32_t* csr = (uint32_t*)(B + L.csr);
             int32_t* sn = (int32_t*)(B + L.snode);
             const int64_t so = rp.tile_slot_off[t];
+            int32_t pad = 0;
             for (int k = 0; k < (int)cf_round(ns, 2); ++k) {
                 if (k >= ns) {  // padding slot (never a merge target)
                     rp.slot_node[so + k] = -1;
@@ -645,8 +673,11 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                 const bool priv = ntiles_of[l] == 1 && !shared_node[l];
                 const bool dir = !rp.node_dir.empty() && rp.node_dir[l] >= 0;
                 B[L.sinfo + k] = (uint8_t)((rp.node_region[l] & 0x3f) | (dir ? 0x40 : 0) | (priv ? 0x80 : 0));
-                for (int32_t j = ent_off[k]; j < ent_off[k + 1]; ++j) csr[j] = (uint16_t)ent[j];
-                cend[k] = (uint16_t)ent_off[k + 1];
+                int32_t j = pad;
+                for (int32_t q = ent_off[k]; q < ent_off[k + 1]; ++q) csr[j++] = ent[q];
+                for (; j & 3; ++j) csr[j] = (uint32_t)L.r_zero | (uint32_t)L.r_zero << 16;  // (0.0, 0.0): exact no-op
+                pad = j;
+                cend[k] = (uint16_t)pad;
                 sn[k] = l;
             }
             for (int k = 0; k < ns; ++k) slot_of[tnodes[k]] = -1;

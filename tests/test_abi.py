@@ -32,7 +32,7 @@ def test_python_mirror_binds_every_declared_symbol():
 
 def test_abi_version_and_error_buffer():
     lib = _abi.lib()
-    assert lib.cf_abi_version() == 1
+    assert lib.cf_abi_version() == 2
     buf = C.create_string_buffer(64)
     assert lib.cf_last_error(buf, 64) == 0
     assert lib.cf_last_error(None, 0) == _abi.CF_INVALID_ARG
@@ -49,7 +49,7 @@ def test_cpp_shim_compiles_standalone(tmp_path):
     the caller's types) and links against the C-ABI library."""
     import subprocess
     src = tmp_path / "t.cpp"
-    src.write_text('#include "castfem_b200.hpp"\nint main() { return cf_abi_version() == 1 ? 0 : 1; }\n')
+    src.write_text('#include "castfem_b200.hpp"\nint main() { return cf_abi_version() == 2 ? 0 : 1; }\n')
     inc = os.path.join(os.path.dirname(HDR))
     libdir = os.path.dirname(_abi.LIB_PATH)
     r = subprocess.run(["g++", "-std=c++20", f"-I{inc}", str(src), "-o", str(tmp_path / "t"), f"-L{libdir}",

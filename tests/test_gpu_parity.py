@@ -28,27 +28,34 @@ def run_pair(case, steps, tile_elems=512, **kw):
     return det, ref
 
 
+GEOMS = ["coords", "stored"]  # gradients recomputed from slot coordinates | stored ElementGeom
+
+
+@pytest.mark.parametrize("geometry", GEOMS)
 @pytest.mark.parametrize("n", [8, 16])
-def test_cfg1_cube_deterministic_bitwise(n):
+def test_cfg1_cube_deterministic_bitwise(n, geometry):
     case = configs.config1(n=n)
-    det, ref = run_pair(case, 30)
+    det, ref = run_pair(case, 30, geometry=geometry)
     assert np.array_equal(det.T, ref.T), np.abs(det.T - ref.T).max()
     assert np.array_equal(det.H, ref.H)
     assert det.steps == ref.steps == 30
     assert det.end_time == ref.time
 
 
+@pytest.mark.parametrize("geometry", GEOMS)
 @pytest.mark.parametrize("n,jitter,perm", [(12, 0.0, 0), (14, 0.2, 5)])
-def test_casting_deterministic_bitwise(n, jitter, perm):
+def test_casting_deterministic_bitwise(n, jitter, perm, geometry):
     case = configs.casting(n, jitter=jitter, seed=3, perm_seed=perm, dt_safety=0.14)
-    det, ref = run_pair(case, 40)
+    det, ref = run_pair(case, 40, geometry=geometry)
     assert np.array_equal(det.T, ref.T), np.abs(det.T - ref.T).max()
 
 
-@pytest.mark.parametrize("order", ["morton", "min_node", "given"])
-def test_casting_atomic_within_tolerance(order):
+@pytest.mark.parametrize("order,geometry", [("morton", "coords"), ("min_node", "coords"), ("given", "coords"),
+                                            ("morton", "stored")])
+def test_casting_atomic_within_tolerance(order, geometry):
     case = configs.casting(14, jitter=0.2, seed=3, perm_seed=9, dt_safety=0.14)
-    at = cf.solve(case.mesh, case.setup, cf.SolveOptions(max_steps=40, mode="atomic", elem_order=order))
+    at = cf.solve(case.mesh, case.setup, cf.SolveOptions(max_steps=40, mode="atomic", elem_order=order,
+                                                         geometry=geometry))
     ref = orc.solve(case.mesh, case.setup, 40)
     assert rel(at.T, ref.T) <= RTOL
 
@@ -123,7 +130,8 @@ def test_t_end_mode_and_series():
         assert s.time == r[0] and abs(s.t_min - r[1]) <= 1e-9 * abs(r[1]) and abs(s.t_max - r[2]) <= 1e-9 * r[2]
 
 
-def test_dirichlet_and_temperature_dependent_tables():
+@pytest.mark.parametrize("geometry", GEOMS)
+def test_dirichlet_and_temperature_dependent_tables(geometry):
     """Fixed-temperature BC f(t) (lowest tag wins, blocked.hpp:250-263),
     piecewise-linear c(T), k(T) (dynamic dt, :477-480) and clamp accounting."""
     m = cf.generate_fixture("cube", 8)
@@ -138,7 +146,7 @@ def test_dirichlet_and_temperature_dependent_tables():
         boundary_conditions={"outer": cf.BoundaryCondition("flux", h=50.0, t_inf=300.0),
                              "hot": cf.BoundaryCondition("fixed", fixed_T=cf.PiecewiseLinear([0.0, 50.0], [650.0, 950.0]))},
         solver=cf.SolverConfig(dt_safety=0.1))
-    opts = cf.SolveOptions(max_steps=60, tile_elems=128)
+    opts = cf.SolveOptions(max_steps=60, tile_elems=128, geometry=geometry)
     gpu = cf.solve(m, setup, opts)
     tiles, _ = cf.tile_map(m, setup, opts)
     ref = orc.solve(m, setup, 60, blocks=tiles)
@@ -148,9 +156,10 @@ def test_dirichlet_and_temperature_dependent_tables():
     assert gpu.clamp_steps == ref.clamp_steps and ref.clamp_steps > 0
 
 
-def test_lambda_max_matches_oracle():
+@pytest.mark.parametrize("geometry", GEOMS)
+def test_lambda_max_matches_oracle(geometry):
     case = configs.casting(10, dt_safety=0.14)
-    with cf.Solver(case.mesh, case.setup) as s:
+    with cf.Solver(case.mesh, case.setup, cf.SolveOptions(geometry=geometry)) as s:
         lam, e13 = s.estimate_lambda_max(300)
     lo, e13o = orc.lambda_max(case.mesh, case.setup, 300)
     assert abs(lam - lo) <= 1e-6 * lo

@@ -494,7 +494,12 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
             CF_OCC(128, true) CF_OCC(256, true) CF_OCC(128, false) CF_OCC(256, false)
 #undef CF_OCC
             per_sm = std::max(1, per_sm);
-            tl.grid = S == 1 ? tl.a.n_tiles : std::max(1, std::min<int>(tl.a.n_tiles, sms * per_sm));
+            const bool persist = S == 2 || (std::getenv("CF_TILE_PERSIST") && std::atoi(std::getenv("CF_TILE_PERSIST")));
+            tl.grid = persist ? std::max(1, std::min<int>(tl.a.n_tiles, sms * per_sm)) : tl.a.n_tiles;
+            // one tile per CTA: CTA it stages tile it + (resident CTAs) into L2 (CF_TILE_PREFETCH=k: k x that)
+            tl.a.prefetch = 0;  // measured: no gain (the wait is occupancy, not DRAM latency)
+            if (const char* e = std::getenv("CF_TILE_PREFETCH"))
+                if (!persist) tl.a.prefetch = (int)(std::atof(e) * sms * per_sm);
             r.launches.push_back(tl);
             if (std::getenv("CF_TRACE_SETUP") && std::atoi(std::getenv("CF_TRACE_SETUP")))
                 std::fprintf(stderr, "[cf setup] rank %d class %d: %zu tiles, blob max %lld, slots max %lld, "

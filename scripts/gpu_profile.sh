@@ -7,5 +7,5 @@ python bench.py --steps ${STEPS:-200} --warmup 5 > gpurun_out/bench_${TAG}.json 
 echo "bench rc=$?"
 $SMALL > gpurun_out/plain_${TAG}.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches_${TAG}.csv $SMALL > gpurun_out/ncu1_${TAG}.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:tile_kernel -s 6 -c 1 -o gpurun_out/prof_tile_${TAG} $SMALL > gpurun_out/ncu2_${TAG}.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:tile_kernel -s ${SKIP:-7} -c 1 -o gpurun_out/prof_tile_${TAG} $SMALL > gpurun_out/ncu2_${TAG}.log 2>&1
 echo "ncu rc=$?"

@@ -176,7 +176,8 @@ struct cf_plan {
     cudaEvent_t fork = nullptr, join = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int mode = CF_MODE_ATOMIC;
-    int tile_threads = 128;      // CTA size of the tile kernel (32 | 64 | 128 | 256)
+    int tile_threads = 128;      // CTA size of the tile kernel (128 | 256)
+    bool pdl = true;             // programmatic dependent launch between the step's kernels (CF_PDL=0: off)
     int stages = 1;              // 1: one tile per CTA; 2: persistent double-buffered TMA pipeline
     int world = 1, first_rank = 0, local_ranks = 1;
     cf_comm* comm = nullptr;
@@ -254,6 +255,22 @@ void set_tile_attr(size_t smem) {
 #undef CF_ATTR
 }
 
+// kernel launch with programmatic dependent launch (griddepcontrol in the kernels)
+template <typename Kern, typename... Args>
+void launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 void launch_tile(cf_plan* p, Rank& r, double t_end) {
     if (r.H.n_tiles == 0) return;
     const bool det = p->mode == CF_MODE_DETERMINISTIC;
@@ -280,7 +297,7 @@ void launch_tile(cf_plan* p, Rank& r, double t_end) {
         const dim3 grid(tl.grid), block(nt);
 #define CF_LAUNCH(D, T, R, C, NT, G)                                                                  \
     if (det == D && td == T && dir == R && cl == C && nt == NT && gc == G) {                          \
-        tile_kernel<D, T, R, C, NT, G><<<grid, block, tl.smem, st>>>(a);                              \
+        launch_ex(tile_kernel<D, T, R, C, NT, G>, grid, block, tl.smem, st, p->pdl && !two, a);        \
         continue;                                                                                     \
     }
         CF_TILE_VARIANTS(CF_LAUNCH)
@@ -298,7 +315,7 @@ void launch_update_t(cf_plan* p, Rank& r, const UpdArgs& a, int blocks) {
     const bool dir = r.ua.node_dir != nullptr;
     const bool cl = p->finite_range;
     const bool td = p->temp_dep;
-#define CF_UPD(D, C, T) update_kernel<DET, MULTI, D, C, T><<<grid, block, 0, p->stream>>>(a)
+#define CF_UPD(D, C, T) launch_ex(update_kernel<DET, MULTI, D, C, T>, grid, block, 0, p->stream, p->pdl && !MULTI, a)
     if (dir) {
         if (cl) { if (td) CF_UPD(true, true, true); else CF_UPD(true, true, false); }
         else { if (td) CF_UPD(true, false, true); else CF_UPD(true, false, false); }
@@ -437,7 +454,7 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     a.stages = p->stages;
     if (const char* e = std::getenv("CF_PROBE")) a.probe = std::atoi(e);
     // tile classes: "light" = tiles whose footprint is within the 97th percentile,
-    // "heavy" = the rest (interface / boundary tiles with many facets), own launch
+    // "heavy" = the rest (e.g. a given block map's interface blocks), own concurrent launch
     {
         const int S = p->stages;
         std::vector<SmemMax> need(h.n_tiles);
@@ -448,12 +465,28 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
             need[t] = SmemMax{L.bytes, cf_round(tm.ns, 2), L.scratch};
             bytes[t] = tile_smem_bytes(need[t], S);
         }
+        auto occupancy = [&](size_t smem) {
+            int per_sm = 0;
+#define CF_OCC(NT, G)                                                                                \
+    if (p->tile_threads == NT && h.coords == G)                                                      \
+        CF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                 \
+            &per_sm, tile_kernel<true, false, false, false, NT, G>, NT, smem));
+            CF_OCC(128, true) CF_OCC(256, true) CF_OCC(128, false) CF_OCC(256, false)
+#undef CF_OCC
+            return std::max(1, per_sm);
+        };
+        set_tile_attr(220 * 1024);  // per function (shared by every plan): the opt-in maximum
         size_t cut = 0;
         if (h.n_tiles) {
             std::vector<size_t> sorted = bytes;
             const size_t q = std::min<size_t>(sorted.size() - 1, (size_t)(0.97 * (double)sorted.size()));
             std::nth_element(sorted.begin(), sorted.begin() + q, sorted.end());
             cut = sorted[q];
+            // one launch unless the outliers would lower the occupancy of every tile (tiles
+            // formed from an element order are already split to a common budget; given block
+            // maps are not)
+            const size_t mx_all = *std::max_element(bytes.begin(), bytes.end());
+            if (occupancy(cut) == occupancy(mx_all)) cut = mx_all;
         }
         if (const char* e = std::getenv("CF_TILE_CLASSES"))
             if (std::atoi(e) == 1) cut = SIZE_MAX;  // diagnostics: one launch for every tile
@@ -468,7 +501,6 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
         }
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-        set_tile_attr(220 * 1024);  // per function (shared by every plan): the opt-in maximum
         for (int c = 0; c < 2; ++c) {
             if (lists[c].empty()) continue;
             Rank::TileLaunch tl;
@@ -486,14 +518,7 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
             tl.smem = tile_smem_bytes(mx[c], S);
             if (tl.smem > 220 * 1024)
                 raise(CF_INVALID_ARG, "tile shared-memory footprint exceeds 220 KB; use smaller tiles");
-            int per_sm = 0;
-#define CF_OCC(NT, G)                                                                                \
-    if (p->tile_threads == NT && h.coords == G)                                                      \
-        CF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                 \
-            &per_sm, tile_kernel<true, false, false, false, NT, G>, NT, tl.smem));
-            CF_OCC(128, true) CF_OCC(256, true) CF_OCC(128, false) CF_OCC(256, false)
-#undef CF_OCC
-            per_sm = std::max(1, per_sm);
+            const int per_sm = occupancy(tl.smem);
             const bool persist = S == 2 || (std::getenv("CF_TILE_PERSIST") && std::atoi(std::getenv("CF_TILE_PERSIST")));
             tl.grid = persist ? std::max(1, std::min<int>(tl.a.n_tiles, sms * per_sm)) : tl.a.n_tiles;
             // one tile per CTA: CTA it stages tile it + (resident CTAs) into L2 (CF_TILE_PREFETCH=k: k x that)
@@ -917,6 +942,7 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
             p->tile_threads = v == 256 ? 256 : 128;
         }
         if (const char* e = std::getenv("CF_TILE_STAGES")) p->stages = std::atoi(e) == 2 ? 2 : 1;
+        if (const char* e = std::getenv("CF_PDL")) p->pdl = std::atoi(e) != 0;
         p->world = o.world_size;
         p->first_rank = o.rank;
         p->local_ranks = o.local_ranks;

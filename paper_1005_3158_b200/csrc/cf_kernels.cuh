@@ -70,6 +70,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+// programmatic dependent launch: wait for the preceding kernel's completion (and memory);
+// a no-op without the launch attribute. No kernel triggers early (griddepcontrol.
+// launch_dependents): early-resident waiting CTAs measured slower than the implicit trigger
+// at CTA exit, which still hides the launch latency between the step's kernels.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
@@ -157,8 +162,10 @@ struct TileHdr {  // per stage: the metadata of the tile in flight (written befo
 };
 
 // `it` indexes the launch's tile descriptors
+// (slots == false: the slot temperatures -- written by the preceding kernel -- are left to
+// issue_slot_copy after griddep_wait; the barrier already expects their bytes)
 __device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int it, bool tdep, bool coords, uint8_t* dst,
-                                                double* sTdst, uint64_t* bar, TileHdr* hdr) {
+                                                double* sTdst, uint64_t* bar, TileHdr* hdr, bool slots = true) {
     const int4 d0 = __ldg((const int4*)(a.desc + it)), d1 = __ldg((const int4*)(a.desc + it) + 1);
     const TileMeta tm{d0.x, d0.y, d0.z, d0.w};
     const int32_t s0 = d1.x;
@@ -173,7 +180,11 @@ __device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int it, bool 
         const uint32_t n = (uint32_t)(L.bytes - o < kBulkChunk ? L.bytes - o : kBulkChunk);
         bulk_g2s(dst + o, src + o, n, bar);
     }
-    if (tbytes) bulk_g2s(sTdst, a.Tslot + s0, tbytes, bar);
+    if (slots && tbytes) bulk_g2s(sTdst, a.Tslot + s0, tbytes, bar);
+}
+__device__ __forceinline__ void issue_slot_copy(const TileArgs& a, const TileHdr* hdr, double* sTdst, uint64_t* bar) {
+    const uint32_t tbytes = 8u * (uint32_t)cf_round32(hdr->tm.ns, 2);
+    if (tbytes) bulk_g2s(sTdst, a.Tslot + hdr->s0, tbytes, bar);
 }
 
 // L2 prefetch of the tile a CTA launched about one resident-grid width later will fetch
@@ -217,17 +228,23 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
     // the first copy is the CTA's critical path: thread 0 initialises the barriers and issues it
     // before anything else; the material table, the step's dt and the scratch zeros overlap it
     // (the other threads touch the barriers only after the __syncthreads below)
+    // With programmatic dependent launch this prologue (static blob) overlaps the previous
+    // kernel's completion; the slot temperatures and the step state follow griddep_wait.
+    const bool first0 = blockIdx.x < a.n_tiles, first1 = a.stages == 2 && blockIdx.x + gridDim.x < a.n_tiles;
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
-        if (blockIdx.x < a.n_tiles) issue_tile_copy(a, blockIdx.x, TDEP, GC, buf0, sT0, &bar[0], &hdr[0]);
-        if (a.stages == 2 && blockIdx.x + gridDim.x < a.n_tiles)
-            issue_tile_copy(a, blockIdx.x + gridDim.x, TDEP, GC, buf1, sT1, &bar[1], &hdr[1]);
+        if (first0) issue_tile_copy(a, blockIdx.x, TDEP, GC, buf0, sT0, &bar[0], &hdr[0], false);
+        if (first1) issue_tile_copy(a, blockIdx.x + gridDim.x, TDEP, GC, buf1, sT1, &bar[1], &hdr[1], false);
+        griddep_wait();
+        if (first0) issue_slot_copy(a, &hdr[0], sT0, &bar[0]);
+        if (first1) issue_slot_copy(a, &hdr[1], sT1, &bar[1]);
         if (a.stages == 1 && a.prefetch && (int)blockIdx.x + a.prefetch < a.n_tiles)
             prefetch_tile(a, blockIdx.x + a.prefetch, TDEP, GC);
     }
     for (int i = tid; i < P->n_materials; i += kTileThreads) sMat[i] = P->mat[i];
     if (GC && tid < 2) ((double*)(smem + a.scratch_off))[tid] = 0.0;  // the facet entries' lump operand
+    if (tid != 0) griddep_wait();  // before any thread reads the step state
     double dt = 0, t_next = 0;
     bool done = false;
     if (FUSE) step_dt<TDEP>(P, a.st, a.t_end, dt, t_next, done);
@@ -456,6 +473,7 @@ __device__ __forceinline__ void own_partial(const UpdArgs& a, int i, double& c, 
 template <bool DET, bool MULTI, bool DIR, bool CLAMP, bool TDEP>
 __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
     const DevParams* __restrict__ P = a.P;
+    griddep_wait();  // the tile kernel's partials / private updates are complete and visible
     double dt, t_next;
     bool done;
     step_dt<TDEP>(P, a.st, a.t_end, dt, t_next, done);

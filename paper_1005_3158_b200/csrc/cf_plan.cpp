@@ -354,6 +354,20 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
         return false;
     };
 
+    // facets per element (ascending facet id), Dirichlet facets excluded from bindings
+    std::vector<char> in_rank(m.E, 0);
+    for (int32_t e : elems) in_rank[e] = 1;
+    std::vector<int32_t> fe_off(m.E + 1, 0), fe;
+    for (int32_t f = 0; f < m.F; ++f)
+        if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe_off[m.owner[f] + 1]++;
+    for (int32_t e = 0; e < m.E; ++e) fe_off[e + 1] += fe_off[e];
+    fe.resize(fe_off[m.E]);
+    {
+        std::vector<int32_t> cur(fe_off.begin(), fe_off.end() - 1);
+        for (int32_t f = 0; f < m.F; ++f)
+            if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe[cur[m.owner[f]]++] = f;
+    }
+
     // ---- tiles: element order key, contiguous chunks, ascending id within a tile
     std::vector<std::vector<int32_t>> tiles;
     if (o.tile_of_element) {
@@ -398,10 +412,65 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             for (int64_t i = 0; i < Er; ++i) order[i] = key[i].second;
         }
         const int TE = o.tile_elems;
-        for (int64_t i = 0; i < Er; i += TE) {
+        for (int64_t i = 0; i < Er; i += TE)
             tiles.emplace_back(order.begin() + i, order.begin() + std::min<int64_t>(Er, i + TE));
-            std::sort(tiles.back().begin(), tiles.back().end());
+        // shared-memory budget: chunks whose footprint exceeds the 95th percentile (interface /
+        // boundary chunks with many facets) are halved along the order, so one launch
+        // configuration (and its occupancy) fits every tile
+        auto footprint = [&](const int32_t* e0, int64_t n) {
+            std::vector<int32_t> v;
+            v.reserve(4 * n + 16);
+            int nf = 0;
+            for (int64_t i = 0; i < n; ++i) {
+                const int32_t e = e0[i];
+                for (int a = 0; a < 4; ++a) v.push_back(m.tets[4 * (size_t)e + a]);
+                for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j, ++nf)
+                    for (int a = 0; a < 3; ++a) v.push_back(m.facets[3 * (size_t)fe[j] + a]);
+            }
+            std::sort(v.begin(), v.end());
+            int ns = 0, ncsr = 0;
+            for (size_t i = 0; i < v.size();) {
+                size_t j = i;
+                while (j < v.size() && v[j] == v[i]) ++j;
+                ns++;
+                ncsr += (int)((j - i + 3) & ~size_t(3));
+                i = j;
+            }
+            const TileLayout L(TileMeta{(int32_t)n, ns, nf, ncsr}, S.temp_dep, o.geometry == CF_GEOM_COORDS);
+            return (int64_t)cf_round(L.bytes, 16) + 24 * cf_round(ns, 2) + 8 * cf_round(L.scratch, 2);
+        };
+        if (tiles.size() > 20) {
+            std::vector<int64_t> fp(tiles.size());
+#pragma omp parallel for schedule(dynamic, 64)
+            for (int64_t t = 0; t < (int64_t)tiles.size(); ++t) fp[t] = footprint(tiles[t].data(), tiles[t].size());
+            std::vector<int64_t> srt = fp;
+            const size_t q = (size_t)(0.95 * (double)(srt.size() - 1));
+            std::nth_element(srt.begin(), srt.begin() + q, srt.end());
+            const int64_t budget = srt[q];
+            std::vector<std::vector<int32_t>> out;
+            out.reserve(tiles.size() + tiles.size() / 16);
+            std::vector<std::vector<int32_t>> stack;
+            for (size_t t = 0; t < tiles.size(); ++t) {
+                if (fp[t] <= budget) {
+                    out.push_back(std::move(tiles[t]));
+                    continue;
+                }
+                stack.assign(1, std::move(tiles[t]));
+                while (!stack.empty()) {  // depth-first halves keep the order
+                    std::vector<int32_t> c = std::move(stack.back());
+                    stack.pop_back();
+                    if (c.size() <= 16 || footprint(c.data(), c.size()) <= budget) {
+                        out.push_back(std::move(c));
+                        continue;
+                    }
+                    const size_t h = c.size() / 2;
+                    stack.emplace_back(c.begin() + h, c.end());
+                    stack.emplace_back(c.begin(), c.begin() + h);
+                }
+            }
+            tiles.swap(out);
         }
+        for (auto& t : tiles) std::sort(t.begin(), t.end());
     }
     trace_stage("plan: tiles");
     rp.n_tiles = (int32_t)tiles.size();
@@ -436,20 +505,6 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     trace_stage("plan: local numbering");
     rp.n_local = (int32_t)lnodes.size();
     if (rp.n_local >= (1 << 28)) raise(CF_INVALID_ARG, "more than 2^28 nodes on one rank");
-
-    // facets per element (ascending facet id), Dirichlet facets excluded from bindings
-    std::vector<char> in_rank(m.E, 0);
-    for (int32_t e : elems) in_rank[e] = 1;
-    std::vector<int32_t> fe_off(m.E + 1, 0), fe;
-    for (int32_t f = 0; f < m.F; ++f)
-        if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe_off[m.owner[f] + 1]++;
-    for (int32_t e = 0; e < m.E; ++e) fe_off[e + 1] += fe_off[e];
-    fe.resize(fe_off[m.E]);
-    {
-        std::vector<int32_t> cur(fe_off.begin(), fe_off.end() - 1);
-        for (int32_t f = 0; f < m.F; ++f)
-            if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe[cur[m.owner[f]]++] = f;
-    }
 
     trace_stage("plan: facet bindings");
     // ghosts: sister nodes of this rank's interface facets that are not local

@@ -217,3 +217,13 @@ def test_cfg2_bit_reproducible_run_to_run():
         b, _ = s.fields(False)
     assert np.array_equal(a, b)
     assert np.isfinite(a).all() and 299.0 < a.min() and a.max() < 975.0
+
+
+def test_graph_replay_bitwise():
+    """CUDA-graph stepping (captured 6-step graphs, replayed; remainder steps eager) is bitwise
+    equal to stream stepping, including a step count that is not a multiple of the graph."""
+    case = configs.casting(12, dt_safety=0.14)
+    plain = cf.solve(case.mesh, case.setup, cf.SolveOptions(max_steps=29))
+    graph = cf.solve(case.mesh, case.setup, cf.SolveOptions(max_steps=29, graph_steps=6))
+    assert np.array_equal(plain.T, graph.T)
+    assert plain.end_time == graph.end_time and plain.steps == graph.steps == 29

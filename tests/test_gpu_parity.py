@@ -227,3 +227,27 @@ def test_graph_replay_bitwise():
     graph = cf.solve(case.mesh, case.setup, cf.SolveOptions(max_steps=29, graph_steps=6))
     assert np.array_equal(plain.T, graph.T)
     assert plain.end_time == graph.end_time and plain.steps == graph.steps == 29
+
+
+@pytest.mark.slow
+def test_cfg4_full_size_properties():
+    """BASELINE configs[3] (256^3 cells, 100,663,296 tets) on one GPU, through size-independent
+    properties (the oracle is too slow at this size): the sum-order-sensitive variants -- fp64 RED
+    accumulation, the coordinates tile layout (its own tiling), two ranks in one process (RCB halves
+    plus the exchange combine) -- agree with the deterministic single-rank run within the north_star
+    1e-9, and the deterministic run is bit-reproducible."""
+    case = configs.config4()
+    steps = 20
+    base = cf.solve(case.mesh, case.setup, cf.SolveOptions(max_steps=steps))
+    assert base.steps == steps and np.isfinite(base.T).all()
+    assert 299.0 < base.T.min() and base.T.max() < 975.0
+    again = cf.solve(case.mesh, case.setup, cf.SolveOptions(max_steps=steps))
+    assert np.array_equal(base.T, again.T)
+    del again
+    variants = [cf.SolveOptions(max_steps=steps, mode="atomic"),
+                cf.SolveOptions(max_steps=steps, geometry="coords"),
+                cf.SolveOptions(max_steps=steps, world_size=2, local_ranks=2)]
+    for opts in variants:
+        other = cf.solve(case.mesh, case.setup, opts)
+        assert other.end_time == base.end_time
+        assert rel(other.T, base.T) <= RTOL, opts

@@ -155,6 +155,8 @@ struct Rank {
         TileArgs a;
         size_t smem;
         int grid;
+        int phase;  // 0: border tiles (multi-rank), 1: the rest
+        int heavy;  // footprint outlier class: concurrent launch on the side stream
     };
     std::vector<TileLaunch> launches;
     int32_t* all_list = nullptr;   // unused (NULL list = identity)
@@ -174,6 +176,8 @@ struct cf_plan {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;              // concurrent launch of the heavy tile class
     cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t xside = nullptr;             // multi-rank: pack + exchange beside the interior tiles
+    cudaEvent_t xfork = nullptr, xjoin = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int mode = CF_MODE_ATOMIC;
     int tile_threads = 128;      // CTA size of the tile kernel (128 | 256)
@@ -218,6 +222,9 @@ struct cf_plan {
         if (fork) cudaEventDestroy(fork);
         if (join) cudaEventDestroy(join);
         if (side) cudaStreamDestroy(side);
+        if (xfork) cudaEventDestroy(xfork);
+        if (xjoin) cudaEventDestroy(xjoin);
+        if (xside) cudaStreamDestroy(xside);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -271,41 +278,47 @@ void launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, b
     CF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
-void launch_tile(cf_plan* p, Rank& r, double t_end) {
+// phase: 0 border tiles, 1 interior tiles, -1 both
+void launch_tile(cf_plan* p, Rank& r, double t_end, int phase = -1) {
     if (r.H.n_tiles == 0) return;
     const bool det = p->mode == CF_MODE_DETERMINISTIC;
     const bool dir = r.ua.node_dir != nullptr, cl = p->finite_range, td = p->temp_dep;
     const bool gc = r.H.coords;
     const int nt = p->tile_threads;
-    // the heavy class (few tiles) runs on a side stream, overlapping the main launch
-    // (disjoint outputs: per-slot partials, tile-private nodes); joined before the update
-    const bool two = r.launches.size() > 1;
-    if (two) {
-        CF_CUDA_CHECK(cudaEventRecord(p->fork, p->stream));
-        CF_CUDA_CHECK(cudaStreamWaitEvent(p->side, p->fork, 0));
-    }
-    for (size_t k = r.launches.size(); k-- > 0;) {  // heavy class first: its CTAs dispatch first
-        const Rank::TileLaunch& tl = r.launches[k];
-        cudaStream_t st = k == 1 ? p->side : p->stream;
-        TileArgs a = tl.a;
-        a.T = r.T[p->cur];
-        a.Told = r.T[p->old()];
-        a.Tn = r.T[p->nxt()];
-        a.Tslot = r.Tslot[p->step_parity];
-        a.Tslot_n = r.Tslot[p->step_parity ^ 1];
-        a.t_end = t_end;
-        const dim3 grid(tl.grid), block(nt);
+    for (int ph = 0; ph < 2; ++ph) {
+        if (phase >= 0 && ph != phase) continue;
+        // the outlier class (few tiles) runs on a side stream, overlapping the main launch
+        // (disjoint outputs: per-slot partials, tile-private nodes); joined before what follows
+        bool two = false;
+        for (const Rank::TileLaunch& tl : r.launches) two = two || (tl.phase == ph && tl.heavy);
+        if (two) {
+            CF_CUDA_CHECK(cudaEventRecord(p->fork, p->stream));
+            CF_CUDA_CHECK(cudaStreamWaitEvent(p->side, p->fork, 0));
+        }
+        for (size_t k = r.launches.size(); k-- > 0;) {  // outlier class first: its CTAs dispatch first
+            const Rank::TileLaunch& tl = r.launches[k];
+            if (tl.phase != ph) continue;
+            cudaStream_t st = tl.heavy ? p->side : p->stream;
+            TileArgs a = tl.a;
+            a.T = r.T[p->cur];
+            a.Told = r.T[p->old()];
+            a.Tn = r.T[p->nxt()];
+            a.Tslot = r.Tslot[p->step_parity];
+            a.Tslot_n = r.Tslot[p->step_parity ^ 1];
+            a.t_end = t_end;
+            const dim3 grid(tl.grid), block(nt);
 #define CF_LAUNCH(D, T, R, C, NT, G)                                                                  \
     if (det == D && td == T && dir == R && cl == C && nt == NT && gc == G) {                          \
         launch_ex(tile_kernel<D, T, R, C, NT, G>, grid, block, tl.smem, st, p->pdl && !two, a);        \
         continue;                                                                                     \
     }
-        CF_TILE_VARIANTS(CF_LAUNCH)
+            CF_TILE_VARIANTS(CF_LAUNCH)
 #undef CF_LAUNCH
-    }
-    if (two) {
-        CF_CUDA_CHECK(cudaEventRecord(p->join, p->side));
-        CF_CUDA_CHECK(cudaStreamWaitEvent(p->stream, p->join, 0));
+        }
+        if (two) {
+            CF_CUDA_CHECK(cudaEventRecord(p->join, p->side));
+            CF_CUDA_CHECK(cudaStreamWaitEvent(p->stream, p->join, 0));
+        }
     }
 }
 
@@ -352,17 +365,17 @@ void launch_update(cf_plan* p, Rank& r, double t_end) {
     else launch_update_t<false, false>(p, r, a, blocks);
 }
 
-void launch_pack(cf_plan* p, Rank& r) {
+void launch_pack(cf_plan* p, Rank& r, cudaStream_t st) {
     if (r.pa.n_cr + r.pa.n_t == 0) return;
     PackArgs a = r.pa;
     a.T = r.T[p->cur];
     a.u.T = r.T[p->cur];
     const int blocks = std::max(1, std::min<int>(1184, (a.n_cr + a.n_t + 255) / 256));
-    if (p->mode == CF_MODE_DETERMINISTIC) pack_kernel<true><<<blocks, 256, 0, p->stream>>>(a);
-    else pack_kernel<false><<<blocks, 256, 0, p->stream>>>(a);
+    if (p->mode == CF_MODE_DETERMINISTIC) pack_kernel<true><<<blocks, 256, 0, st>>>(a);
+    else pack_kernel<false><<<blocks, 256, 0, st>>>(a);
 }
 
-void exchange(cf_plan* p) {
+void exchange(cf_plan* p, cudaStream_t st) {
     if (p->world == 1) return;
     if (p->local_ranks == p->world) {
         // in-process transport: every rank's send region for q -> q's recv region for r
@@ -378,7 +391,7 @@ void exchange(cf_plan* p) {
                 if (len != dst.nb_recv_len[kk]) raise(CF_PROTOCOL, "payload length mismatch");
                 if (len)
                     CF_CUDA_CHECK(cudaMemcpyAsync(dst.recv + dst.H.recv_off[kk], r.send + r.H.send_off[k],
-                                                  len * sizeof(double), cudaMemcpyDeviceToDevice, p->stream));
+                                                  len * sizeof(double), cudaMemcpyDeviceToDevice, st));
             }
         }
         return;
@@ -390,19 +403,28 @@ void exchange(cf_plan* p) {
     for (size_t k = 0; k < r.H.nbrs.size(); ++k) {
         const int q = r.H.nbrs[k].rank;
         if (r.nb_send_len[k])
-            CF_NCCL_CHECK(n.Send(r.send + r.H.send_off[k], r.nb_send_len[k], ncclFloat64, q, p->comm->comm, p->stream));
+            CF_NCCL_CHECK(n.Send(r.send + r.H.send_off[k], r.nb_send_len[k], ncclFloat64, q, p->comm->comm, st));
         if (r.nb_recv_len[k])
-            CF_NCCL_CHECK(n.Recv(r.recv + r.H.recv_off[k], r.nb_recv_len[k], ncclFloat64, q, p->comm->comm, p->stream));
+            CF_NCCL_CHECK(n.Recv(r.recv + r.H.recv_off[k], r.nb_recv_len[k], ncclFloat64, q, p->comm->comm, st));
     }
     CF_NCCL_CHECK(n.GroupEnd());
 }
 
 // one blocked_step for every local rank
+// multi-rank (SURVEY 8(e) overlap): border tiles -> [side stream: pack -> exchange] while the
+// interior tiles run on the main stream -> join -> update
 void enqueue_step(cf_plan* p, double t_end) {
-    for (auto& r : p->ranks) launch_tile(p, *r, t_end);
-    if (p->world > 1) {
-        for (auto& r : p->ranks) launch_pack(p, *r);
-        exchange(p);
+    if (p->world == 1) {
+        for (auto& r : p->ranks) launch_tile(p, *r, t_end);
+    } else {
+        for (auto& r : p->ranks) launch_tile(p, *r, t_end, 0);
+        CF_CUDA_CHECK(cudaEventRecord(p->xfork, p->stream));
+        CF_CUDA_CHECK(cudaStreamWaitEvent(p->xside, p->xfork, 0));
+        for (auto& r : p->ranks) launch_pack(p, *r, p->xside);
+        exchange(p, p->xside);
+        CF_CUDA_CHECK(cudaEventRecord(p->xjoin, p->xside));
+        for (auto& r : p->ranks) launch_tile(p, *r, t_end, 1);
+        CF_CUDA_CHECK(cudaStreamWaitEvent(p->stream, p->xjoin, 0));
     }
     for (auto& r : p->ranks) launch_update(p, *r, t_end);
     p->advance();
@@ -490,10 +512,13 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
         }
         if (const char* e = std::getenv("CF_TILE_CLASSES"))
             if (std::atoi(e) == 1) cut = SIZE_MAX;  // diagnostics: one launch for every tile
-        std::vector<int32_t> lists[2];
-        SmemMax mx[2];
+        // groups: phase (multi-rank: 0 = border tiles, whose partials feed the exchange;
+        // 1 = interior tiles, computed while the exchange is in flight) x footprint class
+        std::vector<int32_t> lists[4];
+        SmemMax mx[4];
         for (int32_t t = 0; t < h.n_tiles; ++t) {
-            const int c = bytes[t] <= cut ? 0 : 1;
+            const int phase = (p->world > 1 && h.tile_border[t]) ? 0 : 1;
+            const int c = 2 * phase + (bytes[t] <= cut ? 0 : 1);
             lists[c].push_back(t);
             mx[c].blob = std::max(mx[c].blob, need[t].blob);
             mx[c].slots = std::max(mx[c].slots, need[t].slots);
@@ -501,9 +526,11 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
         }
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < 4; ++c) {
             if (lists[c].empty()) continue;
             Rank::TileLaunch tl;
+            tl.phase = c / 2;
+            tl.heavy = c & 1;
             tl.a = a;
             std::vector<TileDesc> desc(lists[c].size());
             for (size_t i = 0; i < lists[c].size(); ++i) {
@@ -958,6 +985,9 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         CF_CUDA_CHECK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
         CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
         CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming));
+        CF_CUDA_CHECK(cudaStreamCreateWithFlags(&p->xside, cudaStreamNonBlocking));
+        CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->xfork, cudaEventDisableTiming));
+        CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->xjoin, cudaEventDisableTiming));
         CF_CUDA_CHECK(cudaEventCreate(&p->ev0));
         CF_CUDA_CHECK(cudaEventCreate(&p->ev1));
         CF_CUDA_CHECK(cudaMalloc(&p->dP, sizeof(DevParams)));
@@ -1026,9 +1056,9 @@ int cf_time_phases(cf_plan* p, int64_t n, double* ms_out) {
             for (auto& r : p->ranks) launch_tile(p, *r, 0.0);
             CF_CUDA_CHECK(cudaEventRecord(ev[1], p->stream));
             if (p->world > 1)
-                for (auto& r : p->ranks) launch_pack(p, *r);
+                for (auto& r : p->ranks) launch_pack(p, *r, p->stream);
             CF_CUDA_CHECK(cudaEventRecord(ev[2], p->stream));
-            exchange(p);
+            exchange(p, p->stream);
             CF_CUDA_CHECK(cudaEventRecord(ev[3], p->stream));
             for (auto& r : p->ranks) launch_update(p, *r, 0.0);
             CF_CUDA_CHECK(cudaEventRecord(ev[4], p->stream));

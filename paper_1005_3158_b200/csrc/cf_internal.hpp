@@ -178,6 +178,7 @@ struct RankPlan {
     // tiles
     int32_t n_tiles = 0;
     std::vector<TileMeta> tile_meta;       // [n_tiles] ne, ns, nf, ncsr
+    std::vector<uint8_t> tile_border;      // [n_tiles] holds a rank-shared node (multi-rank)
     std::vector<int32_t> tile_slot_off;    // [n_tiles+1]
     std::vector<int64_t> blob_off;         // [n_tiles+1] byte offsets into blob
     std::vector<uint8_t, UninitAlloc<uint8_t>> blob;  // all tile blobs

@@ -560,6 +560,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     // Pass 1 (parallel): each tile's slot list; sizes -> offsets; pass 2
     // (parallel): fill the tile's blob section at its offset.
     rp.tile_meta.resize(rp.n_tiles);
+    rp.tile_border.assign(rp.n_tiles, 0);
     rp.tile_slot_off.assign(rp.n_tiles + 1, 0);
     rp.blob_off.assign(rp.n_tiles + 1, 0);
     rp.elem_global.resize(Er);
@@ -608,6 +609,11 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             int ncsr = 0;  // each slot's list padded to a multiple of 4 (16-byte reads in the reduction)
             for (int32_t cn : cnt_of) ncsr += (cn + 3) & ~3;
             rp.tile_meta[t] = TileMeta{ne, ns, nf, ncsr};
+            if (W > 1) {  // border tile: holds a rank-shared node (its partials feed the exchange)
+                bool b = false;
+                for (int32_t l : tnodes) b = b || shared_node[l];
+                rp.tile_border[t] = b;
+            }
         }
     }
     for (int32_t t = 0; t < rp.n_tiles; ++t) {  // no throwing inside the parallel regions

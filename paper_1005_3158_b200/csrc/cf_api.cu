@@ -63,6 +63,8 @@ struct NcclApi {
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi& nccl() {
@@ -80,6 +82,7 @@ NcclApi& nccl() {
         api.Recv = (decltype(api.Recv))dlsym(api.h, "ncclRecv");
         api.GroupStart = (decltype(api.GroupStart))dlsym(api.h, "ncclGroupStart");
         api.GroupEnd = (decltype(api.GroupEnd))dlsym(api.h, "ncclGroupEnd");
+        api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
         api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
     });
     if (!api.h || !api.Send || !api.Recv || !api.CommInitRank) raise(CF_NCCL, "libnccl.so.2 not loadable");
@@ -177,6 +180,7 @@ struct cf_plan {
     cudaStream_t side = nullptr;              // concurrent launch of the heavy tile class
     cudaEvent_t fork = nullptr, join = nullptr;
     cudaStream_t xside = nullptr;             // multi-rank: pack + exchange beside the interior tiles
+    DevState** d_states = nullptr;            // in-process ranks' step states (dynamic-dt combine)
     cudaEvent_t xfork = nullptr, xjoin = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int mode = CF_MODE_ATOMIC;
@@ -225,6 +229,7 @@ struct cf_plan {
         if (xfork) cudaEventDestroy(xfork);
         if (xjoin) cudaEventDestroy(xjoin);
         if (xside) cudaStreamDestroy(xside);
+        if (d_states) cudaFree(d_states);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -411,6 +416,29 @@ void exchange(cf_plan* p, cudaStream_t st) {
 }
 
 // one blocked_step for every local rank
+// dynamic dt across ranks (blocked.hpp:477-480 is a min over every element of the mesh): after all
+// tiles, min of each rank's per-step bound (both parity slots; the idle slot is +inf everywhere)
+__global__ void min_bound_combine_kernel(DevState* const* st, int n) {
+    const int k = threadIdx.x;
+    if (k >= 2) return;
+    unsigned long long m = ~0ull;
+    for (int r = 0; r < n; ++r) m = st[r]->min_bound[k] < m ? st[r]->min_bound[k] : m;
+    for (int r = 0; r < n; ++r) st[r]->min_bound[k] = m;
+}
+
+void reduce_min_bound(cf_plan* p, cudaStream_t st) {
+    if (!p->temp_dep || p->world == 1) return;
+    if (p->local_ranks == p->world) {
+        min_bound_combine_kernel<<<1, 32, 0, st>>>(p->d_states, (int)p->ranks.size());
+        CF_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
+    NcclApi& n = nccl();
+    if (!n.AllReduce) raise(CF_NCCL, "ncclAllReduce not available");
+    unsigned long long* mb = p->ranks[0]->st->min_bound;  // positive doubles: bit order == value order
+    CF_NCCL_CHECK(n.AllReduce(mb, mb, 2, ncclUint64, ncclMin, p->comm->comm, st));
+}
+
 // multi-rank (SURVEY 8(e) overlap): border tiles -> [side stream: pack -> exchange] while the
 // interior tiles run on the main stream -> join -> update
 void enqueue_step(cf_plan* p, double t_end) {
@@ -424,6 +452,7 @@ void enqueue_step(cf_plan* p, double t_end) {
         exchange(p, p->xside);
         CF_CUDA_CHECK(cudaEventRecord(p->xjoin, p->xside));
         for (auto& r : p->ranks) launch_tile(p, *r, t_end, 1);
+        reduce_min_bound(p, p->stream);
         CF_CUDA_CHECK(cudaStreamWaitEvent(p->stream, p->xjoin, 0));
     }
     for (auto& r : p->ranks) launch_update(p, *r, t_end);
@@ -928,8 +957,6 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         SetupData S;
         resolve_setup(m, setup, S);
         trace_stage("resolve: rest");
-        if (o.world_size > 1 && S.temp_dep)
-            raise(CF_CONFIG, "temperature-dependent tables (dynamic dt) need world_size == 1 in this build");
 
         std::vector<int32_t> label(m.N);
         if (o.node_order == CF_NODE_ORDER_RCM) {
@@ -1009,6 +1036,12 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
             trace_stage("upload");
             p->ranks.push_back(std::move(rk));
         }
+        if (p->ranks.size() > 1) {
+            std::vector<DevState*> sts;
+            for (const auto& rk : p->ranks) sts.push_back(rk->st);
+            CF_CUDA_CHECK(cudaMalloc(&p->d_states, sizeof(DevState*) * sts.size()));
+            CF_CUDA_CHECK(cudaMemcpy(p->d_states, sts.data(), sizeof(DevState*) * sts.size(), cudaMemcpyHostToDevice));
+        }
         p->launches_per_step = 0;
         for (const auto& rk : p->ranks)
             p->launches_per_step += (int64_t)rk->launches.size() + 1 + (p->world > 1 ? 1 : 0);
@@ -1059,6 +1092,7 @@ int cf_time_phases(cf_plan* p, int64_t n, double* ms_out) {
                 for (auto& r : p->ranks) launch_pack(p, *r, p->stream);
             CF_CUDA_CHECK(cudaEventRecord(ev[2], p->stream));
             exchange(p, p->stream);
+            reduce_min_bound(p, p->stream);
             CF_CUDA_CHECK(cudaEventRecord(ev[3], p->stream));
             for (auto& r : p->ranks) launch_update(p, *r, 0.0);
             CF_CUDA_CHECK(cudaEventRecord(ev[4], p->stream));

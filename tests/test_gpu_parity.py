@@ -130,10 +130,7 @@ def test_t_end_mode_and_series():
         assert s.time == r[0] and abs(s.t_min - r[1]) <= 1e-9 * abs(r[1]) and abs(s.t_max - r[2]) <= 1e-9 * r[2]
 
 
-@pytest.mark.parametrize("geometry", GEOMS)
-def test_dirichlet_and_temperature_dependent_tables(geometry):
-    """Fixed-temperature BC f(t) (lowest tag wins, blocked.hpp:250-263),
-    piecewise-linear c(T), k(T) (dynamic dt, :477-480) and clamp accounting."""
+def _dirichlet_tdep_case():
     m = cf.generate_fixture("cube", 8)
     # split the outer tag: x = 0 face fixed, the rest convective
     x0 = np.all(m.nodes[m.facets][:, :, 0] == 0.0, axis=1)
@@ -146,6 +143,14 @@ def test_dirichlet_and_temperature_dependent_tables(geometry):
         boundary_conditions={"outer": cf.BoundaryCondition("flux", h=50.0, t_inf=300.0),
                              "hot": cf.BoundaryCondition("fixed", fixed_T=cf.PiecewiseLinear([0.0, 50.0], [650.0, 950.0]))},
         solver=cf.SolverConfig(dt_safety=0.1))
+    return m, setup
+
+
+@pytest.mark.parametrize("geometry", GEOMS)
+def test_dirichlet_and_temperature_dependent_tables(geometry):
+    """Fixed-temperature BC f(t) (lowest tag wins, blocked.hpp:250-263),
+    piecewise-linear c(T), k(T) (dynamic dt, :477-480) and clamp accounting."""
+    m, setup = _dirichlet_tdep_case()
     opts = cf.SolveOptions(max_steps=60, tile_elems=128, geometry=geometry)
     gpu = cf.solve(m, setup, opts)
     tiles, _ = cf.tile_map(m, setup, opts)
@@ -154,6 +159,22 @@ def test_dirichlet_and_temperature_dependent_tables(geometry):
     assert np.array_equal(gpu.T, ref.T), np.abs(gpu.T - ref.T).max()
     assert rel(gpu.T, orc.solve(m, setup, 60).T) <= RTOL
     assert gpu.clamp_steps == ref.clamp_steps and ref.clamp_steps > 0
+
+
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_multirank_dynamic_dt(ranks):
+    """Dynamic dt on a decomposed mesh: every rank steps with the min of the stable bound over
+    the whole mesh (blocked.hpp:477-480) -- min-combined across ranks each step (in-process
+    here; ncclAllReduce(min) across processes). Bitwise equal to the oracle with the same parts."""
+    m, setup = _dirichlet_tdep_case()
+    parts = cf.partition_rcb(m, ranks)
+    opts = cf.SolveOptions(max_steps=60, tile_elems=128, world_size=ranks, local_ranks=ranks)
+    gpu = cf.solve(m, setup, opts)
+    tiles, _ = cf.tile_map(m, setup, opts)
+    ref = orc.solve(m, setup, 60, blocks=tiles, parts=parts)
+    assert gpu.steps == 60 and gpu.end_time == ref.time
+    assert np.array_equal(gpu.T, ref.T), np.abs(gpu.T - ref.T).max()
+    assert gpu.clamp_steps == ref.clamp_steps
 
 
 @pytest.mark.parametrize("geometry", GEOMS)

@@ -317,6 +317,37 @@ int cf_generate_fixture(int32_t kind, int32_t n, double radius, double jitter, u
 int cf_counter_uniform(uint64_t seed, const int64_t* keys, int64_t n, double lo, double hi,
                        double* out);
 
+/* ---------------------------------------------------------------- text formats
+ * The reference's file formats either side of the step (same tokenizer, number
+ * syntax, sections, defaults and error messages; CF_PARSE messages carry
+ * "line N: "). Parsed objects own their arrays; *_view fills a descriptor that
+ * points into them (valid until *_free). *_format writes NUL-terminated text
+ * into buf (truncated to cap-1) and returns the full length in *len. */
+typedef struct cf_text_mesh cf_text_mesh;
+typedef struct cf_text_setup cf_text_setup;
+
+/* parse_mesh mesh.hpp:256-325 ("femesh 1"; nodes / tets / facets / contact
+ * sections), including finalize_mesh: a rejected mesh is CF_VALIDATION
+ * "mesh validation failed: ..."; the view's tets are oriented like the
+ * reference's finalized Mesh. */
+int cf_mesh_parse(const char* text, int64_t len, cf_text_mesh** out);
+int cf_mesh_view(const cf_text_mesh* m, cf_mesh_desc* out);
+void cf_mesh_free(cf_text_mesh* m);
+/* write_mesh mesh.hpp:327-343 (coordinates %.17g) */
+int cf_mesh_format(const cf_mesh_desc* mesh, char* buf, int64_t cap, int64_t* len);
+
+/* parse_config material.hpp:186-345: [material r] rho c k latent_heat solidus
+ * liquidus T0 / [bc tag] kind T q h T_inf / [interface a b] h h_time h_temp /
+ * [solver] safety t_end output_every; tables are x:y pairs or one constant.
+ * The view's initial_T is NULL (per-region T0). */
+int cf_config_parse(const char* text, int64_t len, cf_text_setup** out);
+int cf_config_view(const cf_text_setup* s, cf_setup_desc* out);
+void cf_config_free(cf_text_setup* s);
+
+/* load_partmap / write_partmap partition.hpp:424-449: one part id per element */
+int cf_partmap_parse(const char* text, int64_t len, int32_t n_elems, int32_t* parts_out, int32_t* part_count);
+int cf_partmap_format(const int32_t* parts, int32_t n, char* buf, int64_t cap, int64_t* len);
+
 #ifdef __cplusplus
 }
 #endif

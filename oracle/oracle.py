@@ -93,6 +93,11 @@ def ref_lib():
         L.ref_enthalpy.argtypes = [C.POINTER(_abi.cf_material), C.c_double]
         L.ref_apparent_heat_capacity.restype = C.c_double
         L.ref_apparent_heat_capacity.argtypes = [_dp, _dp, _dp, C.POINTER(_abi.cf_material)]
+        for f in (L.ref_mesh_roundtrip, L.ref_config_dump):
+            f.restype = C.c_int
+            f.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
+        L.ref_load_partmap.restype = C.c_int
+        L.ref_load_partmap.argtypes = [C.c_char_p, C.c_int64, C.c_int32, _ip, C.POINTER(C.c_int32)]
         _r = L
     return _r
 
@@ -218,3 +223,34 @@ def assemble_part(mesh: Mesh, setup: SimulationSetup, elem_mask: np.ndarray, T: 
     if st:
         raise OracleError(st, oracle_lib().or_last_error().decode())
     return c, r
+
+
+# ---------------------------------------------------------------- text formats (reference parsers)
+def _ref_text(fn, text: bytes):
+    n = C.c_int64(0)
+    st = fn(text, len(text), None, 0, C.byref(n))
+    if st:
+        return st, ref_lib().ref_last_error().decode()
+    buf = C.create_string_buffer(n.value + 1)
+    fn(text, len(text), buf, n.value + 1, C.byref(n))
+    return 0, buf.raw[:n.value].decode()
+
+
+def ref_mesh_roundtrip(text: bytes):
+    """(status, text): the reference's parse_mesh -> write_mesh, or (status, error message)."""
+    return _ref_text(ref_lib().ref_mesh_roundtrip, text)
+
+
+def ref_config_dump(text: bytes):
+    """(status, canonical dump of the reference's parse_config), or (status, error message)."""
+    return _ref_text(ref_lib().ref_config_dump, text)
+
+
+def ref_load_partmap(text: bytes, n_elems: int):
+    out = np.zeros(max(1, n_elems), dtype=np.int32)
+    count = C.c_int32(0)
+    st = ref_lib().ref_load_partmap(text, len(text), int(n_elems), _p(out, C.c_int32), C.byref(count))
+    if st:
+        return st, ref_lib().ref_last_error().decode()
+    return 0, (out[:n_elems], int(count.value))
+

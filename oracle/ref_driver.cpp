@@ -17,8 +17,10 @@
 #include <castfem/reorder.hpp>
 
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <memory>
+#include <sstream>
 
 #include "../include/castfem_b200.h"
 
@@ -340,6 +342,85 @@ __attribute__((visibility("default"))) double ref_apparent_heat_capacity(const d
     g.min_edge = g15[13];
     g.max_edge = g15[14];
     return apparent_heat_capacity(g, Tn, Hn, m);
+}
+
+// ---- text formats (tests/test_io.py): the reference's own parsers
+static void put_text(const std::string& s, char* out, int64_t cap, int64_t* len) {
+    if (len) *len = (int64_t)s.size();
+    if (out && cap > 0) {
+        const size_t n = std::min<size_t>(s.size(), (size_t)cap - 1);
+        std::memcpy(out, s.data(), n);
+        out[n] = 0;
+    }
+}
+
+// parse_mesh then write_mesh: the finalized mesh as text
+__attribute__((visibility("default"))) int ref_mesh_roundtrip(const char* text, int64_t len, char* out, int64_t cap,
+                                                              int64_t* out_len) {
+    try {
+        std::istringstream in(std::string(text, (size_t)len));
+        const Mesh m = parse_mesh(in);
+        std::ostringstream os;
+        write_mesh(m, os);
+        put_text(os.str(), out, cap, out_len);
+        return CF_OK;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+static std::string g17(double v) {
+    char b[40];
+    std::snprintf(b, sizeof b, "%.17g", v);
+    return b;
+}
+static std::string table_text(const PiecewiseLinear& t) {
+    std::string s = "[";
+    for (size_t i = 0; i < t.xs.size(); ++i) s += (i ? "," : "") + g17(t.xs[i]) + ":" + g17(t.ys[i]);
+    return s + "]";
+}
+
+// parse_config, dumped canonically (the Python test formats the product's parse the same way)
+__attribute__((visibility("default"))) int ref_config_dump(const char* text, int64_t len, char* out, int64_t cap,
+                                                           int64_t* out_len) {
+    try {
+        std::istringstream in(std::string(text, (size_t)len));
+        const SimulationSetup S = parse_config(in);
+        std::string s;
+        for (size_t i = 0; i < S.materials.size(); ++i) {
+            const auto& m = S.materials[i];
+            s += "material " + std::to_string(i) + " rho=" + g17(m.rho) + " c=" + table_text(m.c_of_T) +
+                 " k=" + table_text(m.k_of_T) + " L=" + g17(m.latent_heat) + " Ts=" + g17(m.solidus) +
+                 " Tl=" + g17(m.liquidus) + " T0=" + g17(m.initial_temperature) + "\n";
+        }
+        for (const auto& [tag, b] : S.boundary_conditions)
+            s += "bc " + tag + " kind=" + (b.kind == BoundaryCondition::Kind::fixed ? "fixed" : "flux") +
+                 " T=" + table_text(b.fixed_T) + " q=" + g17(b.q) + " h=" + g17(b.h) + " t_inf=" + g17(b.t_inf) +
+                 "\n";
+        for (const auto& c : S.interface_coeffs)
+            s += "interface " + c.tag_a + " " + c.tag_b + " var=" +
+                 (c.var == InterfaceCoeff::Var::temperature ? "temperature" : "time") + " h=" + table_text(c.h) +
+                 "\n";
+        s += "solver safety=" + g17(S.solver.dt_safety) + " t_end=" + g17(S.solver.t_end) +
+             " output_every=" + std::to_string(S.solver.output_every) + "\n";
+        put_text(s, out, cap, out_len);
+        return CF_OK;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+__attribute__((visibility("default"))) int ref_load_partmap(const char* text, int64_t len, int32_t n_elems,
+                                                            int32_t* out, int32_t* count) {
+    try {
+        std::istringstream in(std::string(text, (size_t)len));
+        const PartMap pm = load_partmap(in, n_elems);
+        for (idx e = 0; e < n_elems; ++e) out[e] = pm.part_of_element[e];
+        *count = pm.part_count;
+        return CF_OK;
+    } catch (...) {
+        return map_exception();
+    }
 }
 
 }  // extern "C"

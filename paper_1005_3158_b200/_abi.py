@@ -110,6 +110,15 @@ SIGNATURES = [
     ("cf_generate_fixture", C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, C.c_uint64,
                                       C.POINTER(cf_fixture)]),
     ("cf_counter_uniform", C.c_int, [C.c_uint64, C.POINTER(C.c_int64), C.c_int64, C.c_double, C.c_double, _dp]),
+    ("cf_mesh_parse", C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_void_p)]),
+    ("cf_mesh_view", C.c_int, [C.c_void_p, C.POINTER(cf_mesh_desc)]),
+    ("cf_mesh_free", None, [C.c_void_p]),
+    ("cf_mesh_format", C.c_int, [C.POINTER(cf_mesh_desc), C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]),
+    ("cf_config_parse", C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_void_p)]),
+    ("cf_config_view", C.c_int, [C.c_void_p, C.POINTER(cf_setup_desc)]),
+    ("cf_config_free", None, [C.c_void_p]),
+    ("cf_partmap_parse", C.c_int, [C.c_char_p, C.c_int64, C.c_int32, _ip, C.POINTER(C.c_int32)]),
+    ("cf_partmap_format", C.c_int, [_ip, C.c_int32, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]),
 ]
 
 _lib = None

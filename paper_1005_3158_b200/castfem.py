@@ -589,3 +589,91 @@ def counter_uniform(seed: int, keys: np.ndarray, lo: float, hi: float) -> np.nda
     check(lib().cf_counter_uniform(int(seed), keys.ctypes.data_as(C.POINTER(C.c_int64)), keys.shape[0], lo, hi,
                                    out.ctypes.data_as(C.POINTER(C.c_double))))
     return out
+
+
+# ------------------------------------------------------------------ text formats
+def _text_arg(text) -> bytes:
+    return text.encode() if isinstance(text, str) else bytes(text)
+
+
+def _format(fn, *args) -> str:
+    n = C.c_int64(0)
+    check(fn(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(fn(*args, buf, n.value + 1, C.byref(n)))
+    return buf.raw[:n.value].decode()
+
+
+def _table(t: "_abi.cf_table") -> PiecewiseLinear:
+    return PiecewiseLinear([t.x[i] for i in range(t.n)], [t.y[i] for i in range(t.n)])
+
+
+def parse_mesh(text) -> Mesh:
+    """parse_mesh (mesh.hpp:256-325): 'femesh 1' text -> a finalized Mesh (oriented tets).
+    Raises ParseError (line-numbered) / ValidationError like the reference."""
+    b = _text_arg(text)
+    h = C.c_void_p()
+    check(lib().cf_mesh_parse(b, len(b), C.byref(h)))
+    try:
+        d = _abi.cf_mesh_desc()
+        check(lib().cf_mesh_view(h, C.byref(d)))
+        N, E, F = d.n_nodes, d.n_elems, d.n_facets
+        arr = lambda ptr, n, dt: np.ctypeslib.as_array(ptr, shape=(n,)).astype(dt, copy=True) if n else np.zeros(0, dt)
+        return Mesh(arr(d.coords, 3 * N, np.float64).reshape(-1, 3), arr(d.tets, 4 * E, np.int32).reshape(-1, 4),
+                    arr(d.region, E, np.int32), arr(d.facets, 3 * F, np.int32).reshape(-1, 3),
+                    arr(d.facet_tag, F, np.int32), [d.tags[i].decode() for i in range(d.n_tags)],
+                    [(d.contacts[2 * i], d.contacts[2 * i + 1]) for i in range(d.n_contacts)])
+    finally:
+        lib().cf_mesh_free(h)
+
+
+def write_mesh(m: Mesh) -> str:
+    """write_mesh (mesh.hpp:327-343)."""
+    keep = _Keep()
+    return _format(lib().cf_mesh_format, C.byref(mesh_desc(m, keep)))
+
+
+def read_mesh(path: str) -> Mesh:
+    with open(path, "rb") as f:
+        return parse_mesh(f.read())
+
+
+def parse_config(text) -> SimulationSetup:
+    """parse_config (material.hpp:186-345) -> SimulationSetup (materials indexed by region,
+    boundary conditions by tag, interface coefficients, solver)."""
+    b = _text_arg(text)
+    h = C.c_void_p()
+    check(lib().cf_config_parse(b, len(b), C.byref(h)))
+    try:
+        d = _abi.cf_setup_desc()
+        check(lib().cf_config_view(h, C.byref(d)))
+        mats = [MaterialTable(m.rho, _table(m.c), _table(m.k), m.latent_heat, m.solidus, m.liquidus,
+                              m.initial_temperature) for m in (d.materials[i] for i in range(d.n_materials))]
+        bcs = {}
+        for i in range(d.n_bcs):
+            b_ = d.bcs[i]
+            bcs[b_.tag.decode()] = BoundaryCondition("fixed" if b_.kind == _abi.CF_BC_FIXED else "flux",
+                                                     _table(b_.fixed_T), b_.q, b_.h, b_.t_inf)
+        cos = [InterfaceCoeff(c.tag_a.decode(), c.tag_b.decode(),
+                              "temperature" if c.var == _abi.CF_VAR_TEMPERATURE else "time", _table(c.h))
+               for c in (d.coeffs[i] for i in range(d.n_coeffs))]
+        return SimulationSetup(materials=mats, boundary_conditions=bcs, interface_coeffs=cos,
+                               solver=SolverConfig(d.dt_safety, d.t_end, int(d.output_every)))
+    finally:
+        lib().cf_config_free(h)
+
+
+def load_partmap(text, element_count: int) -> Tuple[np.ndarray, int]:
+    """load_partmap (partition.hpp:424-445) -> (part_of_element, part_count)."""
+    b = _text_arg(text)
+    out = np.zeros(max(1, element_count), dtype=np.int32)
+    count = C.c_int32(0)
+    check(lib().cf_partmap_parse(b, len(b), int(element_count), out.ctypes.data_as(_abi._ip), C.byref(count)))
+    return out[:element_count], int(count.value)
+
+
+def write_partmap(parts: np.ndarray) -> str:
+    """write_partmap (partition.hpp:447-449)."""
+    p = np.ascontiguousarray(parts, dtype=np.int32)
+    return _format(lib().cf_partmap_format, p.ctypes.data_as(_abi._ip), len(p))
+

@@ -234,7 +234,12 @@ void finalize_mesh(const cf_mesh_desc* d, MeshData& m) {
                 if (t[a] == t[b])
                     raise(CF_VALIDATION, "element " + std::to_string(e) + " has repeated node " + std::to_string(t[a]));
         if (d->region[e] < 0) raise(CF_VALIDATION, "negative region id");
-        raise(CF_DEGENERATE, "element " + std::to_string(e) + ": degenerate tetrahedron");
+        Geom g;  // the reference's message (geometry.hpp:66-69, mesh.hpp:175-176)
+        const int32_t* to = &m.tets[4 * (size_t)e];
+        tet_geometry(m.pos(to[0]), m.pos(to[1]), m.pos(to[2]), m.pos(to[3]), g);
+        raise(CF_DEGENERATE, "element " + std::to_string(e) + ": degenerate tetrahedron: volume " +
+                                 std::to_string(g.vol) + " below threshold " +
+                                 std::to_string(1e-12 * g.max_edge * g.max_edge * g.max_edge));
     }
 
     trace_stage("finalize: geometry");

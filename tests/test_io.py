@@ -1,0 +1,216 @@
+"""Text formats either side of the step: the product's
+femesh / config / partmap parsers (C-ABI, paper_1005_3158_b200/csrc/cf_io.cpp)
+against the reference's own parse_mesh / write_mesh / parse_config /
+load_partmap (unmodified headers in oracle/_ref): identical output text,
+identical error class and message (line numbers included)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_1005_3158_b200 import castfem as cf
+
+need_ref = pytest.mark.skipif(not orc.ref_available(), reason="oracle/_ref not built (needs /root/reference)")
+
+
+def ours_mesh(text: bytes):
+    try:
+        return 0, cf.write_mesh(cf.parse_mesh(text))
+    except cf.CastfemError as e:
+        return e.code, str(e)
+
+
+def ours_config(text: bytes):
+    try:
+        S = cf.parse_config(text)
+    except cf.CastfemError as e:
+        return e.code, str(e)
+    g = lambda v: "%.17g" % v
+    tab = lambda t: "[" + ",".join(f"{g(x)}:{g(y)}" for x, y in zip(t.xs, t.ys)) + "]"
+    s = ""
+    for i, m in enumerate(S.materials):
+        s += (f"material {i} rho={g(m.rho)} c={tab(m.c_of_T)} k={tab(m.k_of_T)} L={g(m.latent_heat)} "
+              f"Ts={g(m.solidus)} Tl={g(m.liquidus)} T0={g(m.initial_temperature)}\n")
+    for tag in sorted(S.boundary_conditions):
+        b = S.boundary_conditions[tag]
+        s += f"bc {tag} kind={b.kind} T={tab(b.fixed_T)} q={g(b.q)} h={g(b.h)} t_inf={g(b.t_inf)}\n"
+    for c in S.interface_coeffs:
+        s += f"interface {c.tag_a} {c.tag_b} var={c.var} h={tab(c.h)}\n"
+    s += f"solver safety={g(S.solver.dt_safety)} t_end={g(S.solver.t_end)} output_every={S.solver.output_every}\n"
+    return 0, s
+
+
+def _casting_text(n=5, jitter=0.2, perm=3):
+    m = cf.generate_fixture("casting", n, jitter=jitter, seed=4, perm_seed=perm)
+    return cf.write_mesh(m).encode(), m
+
+
+# ---------------------------------------------------------------- mesh
+def test_mesh_roundtrip_self():
+    text, m = _casting_text()
+    p = cf.parse_mesh(text)
+    assert np.array_equal(p.nodes, m.nodes) and np.array_equal(p.region, m.region)
+    assert p.element_count() == m.element_count() and len(p.facets) == len(m.facets)
+    again = cf.parse_mesh(cf.write_mesh(p))  # a finalized mesh round-trips exactly
+    assert np.array_equal(again.tets, p.tets) and again.tags == p.tags and again.contacts == p.contacts
+
+
+@need_ref
+@pytest.mark.parametrize("n,jitter,perm", [(4, 0.0, 0), (5, 0.2, 3), (7, 0.1, 9)])
+def test_mesh_matches_reference(n, jitter, perm):
+    text, _ = _casting_text(n, jitter, perm)
+    assert ours_mesh(text) == orc.ref_mesh_roundtrip(text)
+
+
+MESH_CASES = [
+    b"",
+    b"femesh 2\n",
+    b"# comment only\n\n   \nfemesh 1 # trailing\n",
+    b"femesh 1\nnodes\n",
+    b"femesh 1\nnodes 2\n0 0 0\n",
+    b"femesh 1\nnodes 1\n0 0\n",
+    b"femesh 1\nnodes 1\n0 0 x\n",
+    b"femesh 1\nnodes 1\n0 0 +1\n",
+    b"femesh 1\nnodes 1\n0 0 1e400\n",
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 3\n",
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 3 0.5\n",
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 3 0\n",
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 3 2 0\nfacets 1\n0 1 2 outer\n",
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 3 0\nfacets 1\n0 1 outer\n",
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 3 0\ncontact a\n",
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 3 0\ncontact a b\nfoo\n",
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 9 0\n",
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n2 0 0\ntets 1\n0 1 2 3 0\n",
+    b"femesh 1\nnodes 5\n0 0 0\n1 0 0\n0 1 0\n0 0 1\n5 5 5\ntets 1\n0 1 2 3 0\n",
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 3 0\nfacets 1\n0 1 3 x\n",
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 3 0\nfacets 1\n0 1 7 x\n",
+]
+
+
+@need_ref
+@pytest.mark.parametrize("i", range(len(MESH_CASES)))
+def test_mesh_edge_cases_match_reference(i):
+    text = MESH_CASES[i]
+    ours, ref = ours_mesh(text), orc.ref_mesh_roundtrip(text)
+    assert ours == ref  # same status, same text / message (line numbers, validation wording)
+
+
+# ---------------------------------------------------------------- config
+CONFIG_OK = [
+    b"",
+    b"[solver]\nsafety 0.14 # comment\nt_end 100\noutput_every 7\n",
+    b"""# casting, config 2
+[material 1]
+rho 1500
+c 1000
+k 1
+T0 300
+[material 0]
+rho 2700
+c 900
+k 200
+latent_heat 3.9e5
+solidus 821
+liquidus 913
+T0 973
+[bc outer]
+h 20
+T_inf 300
+[bc hot]
+kind fixed
+T 0:650 50:950
+[ interface cast_if mold_if ]
+h 1000
+[interface a b]
+h_temp 300:10 900:2000
+[interface c d]
+[solver]
+safety 0.138
+""",
+    b"[material 2]\nrho 7800\nc 300:450 900:700\nk 300:45 900:30\n[bc outer]\nkind flux\nq 5\n",
+]
+
+CONFIG_BAD = [
+    b"rho 5\n",
+    b"[]\n",
+    b"[material]\n",
+    b"[material x]\n",
+    b"[material 0 1]\n",
+    b"[bogus]\n",
+    b"[material 0]\nrho abc\n",
+    b"[material 0]\ncolor red\n",
+    b"[material 0]\nrho 1\nc 1 2\nk 1\n",
+    b"[material 0]\nrho 1\nc 2:1 1:2\nk 1\n",
+    b"[material 0]\nrho 1\nc 0\nk 1\n",
+    b"[material 0]\nrho 1\nc 1\nk 1\nlatent_heat 5\nsolidus 10\nliquidus 10\n",
+    b"[material 0]\nrho 1\nc 1\nk 1\nlatent_heat -1\n",
+    b"[material 0]\nrho 1\nk 1\n",
+    b"[bc x]\nkind other\n",
+    b"[bc x]\nwhat 1\n",
+    b"[interface a b]\nh 5:1 4:2\n",
+    b"[interface a b]\nbeta 1\n",
+    b"[solver]\nsafety 0\n",
+    b"[solver]\nsafety 1.5\n",
+    b"[solver]\noutput_every 2.5\n",
+    b"[solver]\nfoo 1\n",
+]
+
+
+@need_ref
+@pytest.mark.parametrize("i", range(len(CONFIG_OK)))
+def test_config_matches_reference(i):
+    text = CONFIG_OK[i]
+    ours, ref = ours_config(text), orc.ref_config_dump(text)
+    assert ref[0] == 0, ref
+    assert ours == ref
+
+
+@need_ref
+@pytest.mark.parametrize("i", range(len(CONFIG_BAD)))
+def test_config_errors_match_reference(i):
+    text = CONFIG_BAD[i]
+    ours, ref = ours_config(text), orc.ref_config_dump(text)
+    assert ours[0] == ref[0] and ref[0] != 0, (ours, ref)
+    assert ours[1] == ref[1]
+
+
+def test_config_drives_the_solver_setup():
+    """A parsed config is a SimulationSetup the plan accepts (binding checked at plan build)."""
+    S = cf.parse_config(CONFIG_OK[2])
+    assert [m.rho for m in S.materials] == [2700.0, 1500.0]
+    assert S.boundary_conditions["hot"].kind == "fixed" and S.boundary_conditions["hot"].fixed_T.xs == [0.0, 50.0]
+    assert S.interface_coeffs[1].var == "temperature" and S.interface_coeffs[2].h.ys == [0.0]
+    assert S.solver.dt_safety == 0.138
+
+
+# ---------------------------------------------------------------- partmap
+PARTMAPS = [
+    (b"0\n1\n1\n0\n", 4),
+    (b"# parts\n 2 \n\n0\n1\n3\n", 4),
+    (b"0\n1\n", 3),
+    (b"0\n-1\n1\n", 3),
+    (b"0\nx\n1\n", 3),
+    (b"", 0),
+]
+
+
+@need_ref
+@pytest.mark.parametrize("i", range(len(PARTMAPS)))
+def test_partmap_matches_reference(i):
+    text, n = PARTMAPS[i]
+    ref = orc.ref_load_partmap(text, n)
+    try:
+        parts, count = cf.load_partmap(text, n)
+        ours = (0, (parts, count))
+    except cf.CastfemError as e:
+        ours = (e.code, str(e))
+    assert ours[0] == ref[0], (ours, ref)
+    if ref[0] == 0:
+        assert np.array_equal(ours[1][0], ref[1][0]) and ours[1][1] == ref[1][1]
+    else:
+        assert ours[1] == ref[1]
+
+
+def test_partmap_roundtrip():
+    p = np.array([3, 0, 2, 2, 1], dtype=np.int32)
+    parts, count = cf.load_partmap(cf.write_partmap(p), len(p))
+    assert np.array_equal(parts, p) and count == 4

@@ -66,6 +66,19 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(cfg: str, geometry: str, world: int):
+    """DRAM bytes per tile-kernel launch from the committed ncu --set full capture of this
+    workload and layout (profiles/ncu_traffic.json), else None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d["entries"][f"{cfg}/{geometry}"] if world == 1 else None
+        return (int(e["traffic_bytes"]), "profiles/ncu_traffic.json") if e else (None, None)
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def dist_env():
     return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(
         os.environ.get("LOCAL_RANK", "0"))
@@ -257,14 +270,20 @@ def main():
     # 105 B/tet (4 i32 conn + 11 f64 geometry + u8 region) + 24 B/node (T gather once,
     # (c, r) written once) + facets (canonical 24 / 56 B); the whole-step canonical
     # figure B_step = 105E + 48N + 24F_bc + 56F_if is st.bytes_per_step.
+    # The coordinates layout reports its own bytes: blobs + slot T + outputs.
     facet_bytes = st.bytes_per_step - 105 * E_local - 48 * N_local
-    tile_bytes = 105 * E_local + 24 * N_local + facet_bytes
+    if args.geometry == "stored":
+        tile_bytes, bytes_model = 105 * E_local + 24 * N_local + facet_bytes, "canonical (SURVEY 8(d))"
+    else:
+        tile_bytes, bytes_model = st.tile_bytes_per_launch, "coordinates layout (blobs + slot T + outputs)"
     peak, peak_kind = hbm_peak()
     tile_gbs = tile_bytes / (ph[0] * 1e-3) / 1e9
     step_gbs = st.bytes_per_step / (ms_per_step * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic(cfg, args.geometry, world)
     roofline = {"bound": "hbm", "kernel": "tile_kernel (assembly)", "achieved": round(tile_gbs, 1),
                 "peak": peak, "unit": "GB/s", "frac": round(tile_gbs / peak, 4), "peak_kind": peak_kind,
-                "traffic": None, "algorithmic_bytes_per_launch": int(tile_bytes),
+                "traffic": traffic, "traffic_source": traffic_src, "bytes_model": bytes_model,
+                "algorithmic_bytes_per_launch": int(tile_bytes),
                 "kernel_ms": round(ph[0], 4), "update_ms": round(ph[3], 4), "pack_ms": round(ph[1], 4),
                 "exchange_ms": round(ph[2], 4), "step_achieved_gbs": round(step_gbs, 1),
                 "step_frac_of_8tbs": round(step_gbs / 8000.0, 4), "step_frac": round(step_gbs / peak, 4),

@@ -187,6 +187,8 @@ typedef struct cf_stats {
     int64_t device_bytes;      /* resident plan + state bytes */
     int64_t bytes_per_step;    /* canonical algorithmic bytes */
     int64_t launches_per_step; /* kernels launched per step */
+    int64_t tile_bytes_per_launch; /* this layout's tile-kernel bytes per launch: blobs + slot T
+                                      reads + 16 B of output per slot (partial or T + slot copy) */
 } cf_stats;
 
 /* ---------------------------------------------------------------------------

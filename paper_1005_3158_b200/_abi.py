@@ -70,7 +70,8 @@ class cf_stats(C.Structure):
                 ("loop_seconds", C.c_double), ("static_dt", C.c_double), ("dynamic_dt", C.c_int32),
                 ("n_tiles", C.c_int32), ("n_elems_local", C.c_int64), ("n_nodes_local", C.c_int64),
                 ("total_slots", C.c_int64), ("n_shared_nodes", C.c_int64), ("n_ghost_nodes", C.c_int64),
-                ("device_bytes", C.c_int64), ("bytes_per_step", C.c_int64), ("launches_per_step", C.c_int64)]
+                ("device_bytes", C.c_int64), ("bytes_per_step", C.c_int64), ("launches_per_step", C.c_int64),
+                ("tile_bytes_per_launch", C.c_int64)]
 
 
 class cf_fixture(C.Structure):

@@ -169,6 +169,7 @@ struct Rank {
     size_t tile_smem = 0;
     int upd_blocks = 0, upd_blocks_all = 0;
     int64_t bytes_per_step = 0;
+    int64_t tile_bytes = 0;  // layout bytes of one tile-kernel launch
     std::vector<int64_t> nb_send_len, nb_recv_len;
 };
 
@@ -664,6 +665,7 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     r.upd_blocks_all = std::max(1, std::min<int>(sms * 8, (int)((h.n_local + 255) / 256)));
     // canonical algorithmic bytes: 105 E + 48 N + 24 F_bc + 56 F_if
     r.bytes_per_step = 105 * Er + 48 * (int64_t)h.n_local + 24 * h.n_bc_facets + 56 * h.n_if_facets;
+    r.tile_bytes = (h.blob_off.empty() ? 0 : h.blob_off.back()) + (8 + 16) * S_tot;
     CF_CUDA_CHECK(cudaStreamSynchronize(s));
     // drop the big host arrays (metadata kept)
     decltype(h.blob)().swap(h.blob);
@@ -1242,6 +1244,7 @@ int cf_get_stats(cf_plan* p, cf_stats* out) {
             out->n_ghost_nodes += r->H.n_ghost;
             out->device_bytes += r->mem.bytes;
             out->bytes_per_step += r->bytes_per_step;
+            out->tile_bytes_per_launch += r->tile_bytes;
         }
         out->launches_per_step = p->launches_per_step;
     });

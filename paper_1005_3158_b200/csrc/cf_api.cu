@@ -369,6 +369,8 @@ void launch_update(cf_plan* p, Rank& r, double t_end) {
     else if (det) launch_update_t<true, false>(p, r, a, blocks);
     else if (multi) launch_update_t<false, true>(p, r, a, blocks);
     else launch_update_t<false, false>(p, r, a, blocks);
+    if (p->temp_dep) launch_ex(advance_kernel<true>, dim3(1), dim3(32), 0, p->stream, p->pdl, r.st, p->dP, t_end);
+    else launch_ex(advance_kernel<false>, dim3(1), dim3(32), 0, p->stream, p->pdl, r.st, p->dP, t_end);
 }
 
 void launch_pack(cf_plan* p, Rank& r, cudaStream_t st) {
@@ -1046,7 +1048,7 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         }
         p->launches_per_step = 0;
         for (const auto& rk : p->ranks)
-            p->launches_per_step += (int64_t)rk->launches.size() + 1 + (p->world > 1 ? 1 : 0);
+            p->launches_per_step += (int64_t)rk->launches.size() + 2 + (p->world > 1 ? 1 : 0);
         init_state(p.get(), S.T0.data());
         CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
         trace_stage("init state");

@@ -561,32 +561,28 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < a.n_ghost; g += stride)
             a.Tcur_w[a.n_local + g] = a.recv[a.ghost_src[g]];
     if (CLAMP && clamped) a.st->clamp_flag = 1;
-    // last CTA advances the step state (every CTA has read it by then)
-    __shared__ bool last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned int tk = atomicAdd(&a.st->ticket, 1u);
-        last = tk == gridDim.x - 1;
+}
+
+// advances the step state after the update (a separate one-warp launch: the update's CTAs
+// exit without a grid-wide ticket; every kernel of the step has read the state by then)
+template <bool TDEP>
+__global__ void advance_kernel(DevState* st, const DevParams* __restrict__ P, double t_end) {
+    griddep_wait();
+    if (threadIdx.x != 0) return;
+    double dt, t_next;
+    bool done;
+    step_dt<TDEP>(P, st, t_end, dt, t_next, done);
+    if (!done) {
+        const int par = (int)(st->step_index & 1);
+        st->time = t_next;
+        st->dt = dt;
+        st->step_index += 1;
+        if (st->clamp_flag) st->clamp_steps += 1;
+        st->min_bound[par ^ 1] = 0x7ff0000000000000ull;
+    } else {
+        st->done = 1;
     }
-    __syncthreads();
-    if (last && threadIdx.x == 0) {
-        __threadfence();
-        DevState* s = a.st;
-        if (!done) {
-            const int par = (int)(s->step_index & 1);
-            s->time = t_next;
-            s->dt = dt;
-            s->step_index += 1;
-            if (s->clamp_flag) s->clamp_steps += 1;
-            s->min_bound[par ^ 1] = 0x7ff0000000000000ull;
-        } else {
-            s->done = 1;
-        }
-        s->clamp_flag = 0;
-        s->ticket = 0;
-        __threadfence();
-    }
+    st->clamp_flag = 0;
 }
 
 // ------------------------------------------------------------------ pack kernel

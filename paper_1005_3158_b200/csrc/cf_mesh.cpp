@@ -243,16 +243,29 @@ void finalize_mesh(const cf_mesh_desc* d, MeshData& m) {
     }
 
     trace_stage("finalize: geometry");
-    // node_regions (mesh.hpp:129-144)
+    // node_regions (mesh.hpp:129-144): parallel first claim; on a conflict the serial scan
+    // reports the reference's first offending (element, node) pair
     m.node_region.assign(N, -1);
+    bool conflict = false;
+#pragma omp parallel for schedule(static) reduction(|| : conflict)
     for (int64_t e = 0; e < E; ++e)
         for (int a = 0; a < 4; ++a) {
-            const int32_t n = m.tets[4 * (size_t)e + a];
-            if (m.node_region[n] >= 0 && m.node_region[n] != d->region[e])
-                raise(CF_VALIDATION, "node " + std::to_string(n) + " belongs to elements of regions " +
-                                         std::to_string(m.node_region[n]) + " and " + std::to_string(d->region[e]));
-            m.node_region[n] = d->region[e];
+            std::atomic_ref<int32_t> w(m.node_region[m.tets[4 * (size_t)e + a]]);
+            int32_t cur = -1;
+            if (!w.compare_exchange_strong(cur, d->region[e], std::memory_order_relaxed) && cur != d->region[e])
+                conflict = true;
         }
+    if (conflict) {
+        std::fill(m.node_region.begin(), m.node_region.end(), -1);
+        for (int64_t e = 0; e < E; ++e)
+            for (int a = 0; a < 4; ++a) {
+                const int32_t n = m.tets[4 * (size_t)e + a];
+                if (m.node_region[n] >= 0 && m.node_region[n] != d->region[e])
+                    raise(CF_VALIDATION, "node " + std::to_string(n) + " belongs to elements of regions " +
+                                             std::to_string(m.node_region[n]) + " and " + std::to_string(d->region[e]));
+                m.node_region[n] = d->region[e];
+            }
+    }
     for (int64_t n = 0; n < N; ++n)
         if (m.node_region[n] < 0) raise(CF_VALIDATION, "node " + std::to_string(n) + " not referenced by any element");
 

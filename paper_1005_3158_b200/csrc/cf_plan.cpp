@@ -248,10 +248,11 @@ void resolve_setup(const MeshData& m, const cf_setup_desc* s, SetupData& out) {
     }
     // initial_temperatures (+ index-keyed override)
     out.T0.resize(m.N);
-    for (int32_t n = 0; n < m.N; ++n)
+#pragma omp parallel for schedule(static)
+    for (int32_t n = 0; n < m.N; ++n) {
         out.T0[n] = s->initial_T ? s->initial_T[n] : s->materials[m.node_region[n]].initial_temperature;
-    for (int32_t n = 0; n < m.N; ++n)
         if (out.dir_of_node[n] >= 0) out.T0[n] = pl_eval(P, P.dir_tab[out.dir_of_node[n]], 0.0);
+    }
     // static dt (blocked.hpp:340-350): min_e rho c(0) l^2 / k(0). For constant
     // properties the bound is monotone in the element's minimum edge (also
     // under rounding), so the per-region minimum edge gives the exact minimum.
@@ -293,9 +294,31 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
 
     // elements of this rank, ascending global id (SubDomain::from_elements blocked.hpp:25-39)
     std::vector<int32_t> elems;
-    elems.reserve(W > 1 ? m.E / W + 1 : m.E);
-    for (int32_t e = 0; e < m.E; ++e)
-        if (part_of(e) == rank) elems.push_back(e);
+    if (W == 1) {
+        elems.resize(m.E);
+#pragma omp parallel for schedule(static)
+        for (int32_t e = 0; e < m.E; ++e) elems[e] = e;
+    } else {  // ascending filter: per-thread counts, then fill
+        const int nt = omp_get_max_threads();
+        std::vector<int64_t> cnt(nt + 1, 0);
+#pragma omp parallel num_threads(nt)
+        {
+            const int th = omp_get_thread_num();
+            const int64_t lo = (int64_t)m.E * th / nt, hi = (int64_t)m.E * (th + 1) / nt;
+            int64_t c = 0;
+            for (int64_t e = lo; e < hi; ++e) c += part_of((int32_t)e) == rank;
+            cnt[th + 1] = c;
+#pragma omp barrier
+#pragma omp single
+            {
+                for (int k = 0; k < nt; ++k) cnt[k + 1] += cnt[k];
+                elems.resize(cnt[nt]);
+            }
+            int64_t j = cnt[th];
+            for (int64_t e = lo; e < hi; ++e)
+                if (part_of((int32_t)e) == rank) elems[j++] = (int32_t)e;
+        }
+    }
     const int64_t Er = (int64_t)elems.size();
 
     // parts touching each node (classify_nodes partition.hpp:311-327), only for W > 1
@@ -355,12 +378,34 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     };
 
     // facets per element (ascending facet id), Dirichlet facets excluded from bindings
-    std::vector<char> in_rank(m.E, 0);
-    for (int32_t e : elems) in_rank[e] = 1;
+    std::vector<char> in_rank(m.E, W == 1 ? 1 : 0);
+    if (W > 1)
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < Er; ++i) in_rank[elems[i]] = 1;
     std::vector<int32_t> fe_off(m.E + 1, 0), fe;
     for (int32_t f = 0; f < m.F; ++f)
         if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe_off[m.owner[f] + 1]++;
-    for (int32_t e = 0; e < m.E; ++e) fe_off[e + 1] += fe_off[e];
+    {  // parallel inclusive prefix sum over E + 1 entries (per-thread blocks, then offsets)
+        const int nt = omp_get_max_threads();
+        std::vector<int64_t> part(nt + 1, 0);
+        const int64_t n1 = (int64_t)m.E + 1;
+#pragma omp parallel num_threads(nt)
+        {
+            const int th = omp_get_thread_num();
+            const int64_t lo = n1 * th / nt, hi = n1 * (th + 1) / nt;
+            int64_t acc = 0;
+            for (int64_t i = lo; i < hi; ++i) acc += fe_off[i];
+            part[th + 1] = acc;
+#pragma omp barrier
+#pragma omp single
+            for (int k = 0; k < nt; ++k) part[k + 1] += part[k];
+            int64_t run = part[th];
+            for (int64_t i = lo; i < hi; ++i) {
+                run += fe_off[i];
+                fe_off[i] = (int32_t)run;
+            }
+        }
+    }
     fe.resize(fe_off[m.E]);
     {
         std::vector<int32_t> cur(fe_off.begin(), fe_off.end() - 1);
@@ -368,6 +413,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe[cur[m.owner[f]]++] = f;
     }
 
+    trace_stage("plan: facet bindings");
     // ---- tiles: element order key, contiguous chunks, ascending id within a tile
     std::vector<std::vector<int32_t>> tiles;
     if (o.tile_of_element) {
@@ -377,14 +423,25 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     } else {
         std::vector<int32_t> order = elems;
         if (o.elem_order == CF_ELEM_ORDER_MORTON) {
-            double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-            for (int32_t n = 0; n < m.N; ++n)
-                for (int k = 0; k < 3; ++k) {
-                    lo[k] = std::min(lo[k], m.pos(n)[k]);
-                    hi[k] = std::max(hi[k], m.pos(n)[k]);
-                }
+            double lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY;
+#pragma omp parallel for schedule(static) reduction(min : lo0, lo1, lo2) reduction(max : hi0, hi1, hi2)
+            for (int32_t n = 0; n < m.N; ++n) {
+                const double* q = m.pos(n);
+                lo0 = std::min(lo0, q[0]);
+                lo1 = std::min(lo1, q[1]);
+                lo2 = std::min(lo2, q[2]);
+                hi0 = std::max(hi0, q[0]);
+                hi1 = std::max(hi1, q[1]);
+                hi2 = std::max(hi2, q[2]);
+            }
+            const double lo[3] = {lo0, lo1, lo2}, hi[3] = {hi0, hi1, hi2};
             const double span = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 1e-300});
-            std::vector<std::pair<uint64_t, int32_t>> key(Er);
+            struct Key {  // POD: the array is first touched by the parallel fill
+                uint64_t code;
+                int32_t e;
+                bool operator<(const Key& b) const { return code != b.code ? code < b.code : e < b.e; }
+            };
+            std::vector<Key, UninitAlloc<Key>> key(Er);
 #pragma omp parallel for schedule(static)
             for (int64_t i = 0; i < Er; ++i) {
                 const int32_t e = elems[i];
@@ -396,10 +453,13 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                     q = std::min(std::max(q, 0.0), 2097151.0);
                     code |= spread21((uint64_t)q) << k;
                 }
-                key[i] = {code, e};
+                key[i] = Key{code, e};
             }
+            trace_stage("plan: morton keys");
             __gnu_parallel::sort(key.begin(), key.end());  // keys unique: any sort gives this order
-            for (int64_t i = 0; i < Er; ++i) order[i] = key[i].second;
+            trace_stage("plan: morton sort");
+#pragma omp parallel for schedule(static)
+            for (int64_t i = 0; i < Er; ++i) order[i] = key[i].e;
         } else if (o.elem_order == CF_ELEM_ORDER_MIN_NODE) {
             std::vector<std::pair<int32_t, int32_t>> key(Er);
             for (int64_t i = 0; i < Er; ++i) {
@@ -414,35 +474,48 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
         const int TE = o.tile_elems;
         for (int64_t i = 0; i < Er; i += TE)
             tiles.emplace_back(order.begin() + i, order.begin() + std::min<int64_t>(Er, i + TE));
-        // shared-memory budget: chunks whose footprint exceeds the 95th percentile (interface /
-        // boundary chunks with many facets) are halved along the order, so one launch
-        // configuration (and its occupancy) fits every tile
-        auto footprint = [&](const int32_t* e0, int64_t n) {
-            std::vector<int32_t> v;
-            v.reserve(4 * n + 16);
-            int nf = 0;
+        trace_stage("plan: chunks");
+        // shared-memory budget: the 95th percentile of the chunk footprints; larger chunks
+        // (interface / boundary chunks with many facets) are halved along the order until they
+        // fit, so one launch configuration (and its occupancy) serves every tile
+        auto footprint = [&](const int32_t* e0, int64_t n, std::vector<int64_t>& tab) {
+            // unique nodes and their contribution counts: open addressing on (node, count)
+            size_t cap = 64;
+            while (cap < 8 * (size_t)n) cap <<= 1;
+            if (tab.size() < cap) tab.resize(cap);
+            std::fill(tab.begin(), tab.begin() + cap, -1);
+            const size_t mask = cap - 1;
+            int ns = 0, nf = 0;
+            auto add = [&](int32_t v) {
+                size_t h = ((uint64_t)(uint32_t)v * 0x9E3779B97F4A7C15ull) >> 32 & mask;
+                while (tab[h] >= 0 && (int32_t)(tab[h] >> 32) != v) h = (h + 1) & mask;
+                if (tab[h] < 0) {
+                    tab[h] = (int64_t)v << 32;
+                    ++ns;
+                }
+                tab[h] += 1;
+            };
             for (int64_t i = 0; i < n; ++i) {
                 const int32_t e = e0[i];
-                for (int a = 0; a < 4; ++a) v.push_back(m.tets[4 * (size_t)e + a]);
+                for (int a = 0; a < 4; ++a) add(m.tets[4 * (size_t)e + a]);
                 for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j, ++nf)
-                    for (int a = 0; a < 3; ++a) v.push_back(m.facets[3 * (size_t)fe[j] + a]);
+                    for (int a = 0; a < 3; ++a) add(m.facets[3 * (size_t)fe[j] + a]);
             }
-            std::sort(v.begin(), v.end());
-            int ns = 0, ncsr = 0;
-            for (size_t i = 0; i < v.size();) {
-                size_t j = i;
-                while (j < v.size() && v[j] == v[i]) ++j;
-                ns++;
-                ncsr += (int)((j - i + 3) & ~size_t(3));
-                i = j;
-            }
+            int ncsr = 0;
+            for (size_t h = 0; h < cap; ++h)
+                if (tab[h] >= 0) ncsr += ((int)(tab[h] & 0xffffffff) + 3) & ~3;
             const TileLayout L(TileMeta{(int32_t)n, ns, nf, ncsr}, S.temp_dep, o.geometry == CF_GEOM_COORDS);
             return (int64_t)cf_round(L.bytes, 16) + 24 * cf_round(ns, 2) + 8 * cf_round(L.scratch, 2);
         };
         if (tiles.size() > 20) {
             std::vector<int64_t> fp(tiles.size());
-#pragma omp parallel for schedule(dynamic, 64)
-            for (int64_t t = 0; t < (int64_t)tiles.size(); ++t) fp[t] = footprint(tiles[t].data(), tiles[t].size());
+#pragma omp parallel
+            {
+                std::vector<int64_t> tab;
+#pragma omp for schedule(dynamic, 256)
+                for (int64_t t = 0; t < (int64_t)tiles.size(); ++t)
+                    fp[t] = footprint(tiles[t].data(), tiles[t].size(), tab);
+            }
             std::vector<int64_t> srt = fp;
             const size_t q = (size_t)(0.95 * (double)(srt.size() - 1));
             std::nth_element(srt.begin(), srt.begin() + q, srt.end());
@@ -450,6 +523,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             std::vector<std::vector<int32_t>> out;
             out.reserve(tiles.size() + tiles.size() / 16);
             std::vector<std::vector<int32_t>> stack;
+            std::vector<int64_t> tab;
             for (size_t t = 0; t < tiles.size(); ++t) {
                 if (fp[t] <= budget) {
                     out.push_back(std::move(tiles[t]));
@@ -459,7 +533,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                 while (!stack.empty()) {  // depth-first halves keep the order
                     std::vector<int32_t> c = std::move(stack.back());
                     stack.pop_back();
-                    if (c.size() <= 16 || footprint(c.data(), c.size()) <= budget) {
+                    if (c.size() <= 16 || footprint(c.data(), c.size(), tab) <= budget) {
                         out.push_back(std::move(c));
                         continue;
                     }
@@ -470,10 +544,10 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             }
             tiles.swap(out);
         }
-        for (auto& t : tiles) std::sort(t.begin(), t.end());
     }
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t t = 0; t < (int64_t)tiles.size(); ++t) std::sort(tiles[t].begin(), tiles[t].end());
     trace_stage("plan: tiles");
-    rp.n_tiles = (int32_t)tiles.size();
     for (auto& t : tiles)
         if ((int)t.size() > kMaxTileElems)
             raise(CF_INVALID_ARG, "a tile holds more than 2048 elements (" + std::to_string(t.size()) + ")");
@@ -482,15 +556,51 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     std::vector<int32_t> local_of(m.N, -1);
     std::vector<int32_t> lnodes;
     if (o.node_order == CF_NODE_ORDER_TILE) {
-        for (const auto& te : tiles)
-            for (int32_t e : te)
-                for (int a = 0; a < 4; ++a) {
-                    const int32_t n = m.tets[4 * (size_t)e + a];
-                    if (local_of[n] < 0) {
-                        local_of[n] = (int32_t)lnodes.size();
-                        lnodes.push_back(n);
+        // first touch in tile order, in parallel: each thread owns a contiguous range of
+        // tiles; a node belongs to the first range touching it (atomic min of the range
+        // index), the owner lists its nodes in first-touch order, lists concatenate in
+        // range order -- the serial first-touch order exactly
+        const int nt = omp_get_max_threads();
+        const int64_t T_ = (int64_t)tiles.size();
+        std::vector<std::atomic<int32_t>> owner(m.N);
+        std::vector<std::vector<int32_t>> lists(nt);
+#pragma omp parallel num_threads(nt)
+        {
+            const int th = omp_get_thread_num();
+#pragma omp for schedule(static)
+            for (int32_t n = 0; n < m.N; ++n) owner[n].store(INT32_MAX, std::memory_order_relaxed);
+            const int64_t lo = T_ * th / nt, hi = T_ * (th + 1) / nt;
+            for (int64_t t = lo; t < hi; ++t)
+                for (int32_t e : tiles[t])
+                    for (int a = 0; a < 4; ++a) {
+                        std::atomic<int32_t>& w = owner[m.tets[4 * (size_t)e + a]];
+                        int32_t cur = w.load(std::memory_order_relaxed);
+                        while (th < cur && !w.compare_exchange_weak(cur, th, std::memory_order_relaxed)) {
+                        }
                     }
-                }
+#pragma omp barrier
+            auto& L = lists[th];
+            std::vector<uint64_t> seen(((size_t)m.N + 63) / 64, 0);  // private: no shared-line writes
+            for (int64_t t = lo; t < hi; ++t)
+                for (int32_t e : tiles[t])
+                    for (int a = 0; a < 4; ++a) {
+                        const int32_t n = m.tets[4 * (size_t)e + a];
+                        const uint64_t bit = 1ull << (n & 63);
+                        if (!(seen[n >> 6] & bit) && owner[n].load(std::memory_order_relaxed) == th) {
+                            seen[n >> 6] |= bit;
+                            L.push_back(n);
+                        }
+                    }
+        }
+        std::vector<int64_t> off(nt + 1, 0);
+        for (int k = 0; k < nt; ++k) off[k + 1] = off[k] + (int64_t)lists[k].size();
+        lnodes.resize(off[nt]);
+#pragma omp parallel for schedule(static, 1)
+        for (int k = 0; k < nt; ++k)
+            for (size_t i = 0; i < lists[k].size(); ++i) {
+                lnodes[off[k] + i] = lists[k][i];
+                local_of[lists[k][i]] = (int32_t)(off[k] + i);
+            }
     } else {
         std::vector<char> mark(m.N, 0);
         for (int32_t e : elems)
@@ -506,7 +616,6 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     rp.n_local = (int32_t)lnodes.size();
     if (rp.n_local >= (1 << 28)) raise(CF_INVALID_ARG, "more than 2^28 nodes on one rank");
 
-    trace_stage("plan: facet bindings");
     // ghosts: sister nodes of this rank's interface facets that are not local
     std::vector<int32_t> ghosts;
     for (int32_t f = 0; f < m.F; ++f) {
@@ -524,28 +633,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     rp.local_global = lnodes;
     rp.local_global.insert(rp.local_global.end(), ghosts.begin(), ghosts.end());
 
-    // node -> number of tiles touching it (tile-private test)
-    std::vector<int32_t> ntiles_of(rp.n_local, 0);
-    {
-        std::vector<int32_t> last(rp.n_local, -1);
-        for (int32_t t = 0; t < rp.n_tiles; ++t)
-            for (int32_t e : tiles[t])
-                for (int a = 0; a < 4; ++a) {
-                    const int32_t l = local_of[m.tets[4 * (size_t)e + a]];
-                    if (last[l] != t) {
-                        last[l] = t;
-                        ntiles_of[l]++;
-                    }
-                }
-    }
-    std::vector<char> shared_node(rp.n_local, 0);
-    if (W > 1)
-        for (int32_t l = 0; l < rp.n_local; ++l) {
-            const int32_t n = lnodes[l];
-            shared_node[l] = (np_off[n + 1] - np_off[n]) > 1;
-        }
-
-    trace_stage("plan: ghosts + tile counts");
+    trace_stage("plan: ghosts");
     rp.node_region.resize(rp.n_local);
     for (int32_t l = 0; l < rp.n_local; ++l) rp.node_region[l] = (uint8_t)m.node_region[lnodes[l]];
     bool any_dir = false;
@@ -557,65 +645,92 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     }
 
     // ---- per tile: slots, CSR, facet bindings, packed into the blob.
-    // Pass 1 (parallel): each tile's slot list; sizes -> offsets; pass 2
-    // (parallel): fill the tile's blob section at its offset.
-    rp.tile_meta.resize(rp.n_tiles);
-    rp.tile_border.assign(rp.n_tiles, 0);
-    rp.tile_slot_off.assign(rp.n_tiles + 1, 0);
-    rp.blob_off.assign(rp.n_tiles + 1, 0);
-    rp.elem_global.resize(Er);
+    // Pass 1 (parallel): each tile's slot list and sizes; tiles over the shared-memory
+    // budget are halved along the element order (their slot lists recomputed); sizes ->
+    // offsets; pass 2 (parallel): fill the tile's blob section at its offset.
     const int nthr = omp_get_max_threads();
-    std::vector<std::vector<int32_t>> tile_nodes(rp.n_tiles);
-    std::vector<int64_t> elem_off(rp.n_tiles + 1, 0);
+    std::vector<std::vector<int32_t>> tile_nodes;
+    std::vector<TileMeta> meta;
     auto tile_facets = [&](const std::vector<int32_t>& te, std::vector<int32_t>& out) {
         out.clear();  // facet bindings, element order then facet id (blocked.hpp:244-288)
         for (int32_t e : te)
             for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j) out.push_back(fe[j]);
     };
+    auto pass1 = [&](const std::vector<int32_t>& which) {
 #pragma omp parallel num_threads(nthr)
-    {
-        std::vector<int32_t> slot_of(rp.n_local, -1), cnt_of, idx, tfacets;
+        {
+            std::vector<int32_t> slot_of(rp.n_local, -1), cnt_of, idx, tfacets, sorted;
 #pragma omp for schedule(dynamic, 64)
-        for (int32_t t = 0; t < rp.n_tiles; ++t) {
-            const auto& te = tiles[t];
-            auto& tnodes = tile_nodes[t];
-            for (int32_t e : te)
-                for (int a = 0; a < 4; ++a) {
-                    const int32_t l = local_of[m.tets[4 * (size_t)e + a]];
-                    if (slot_of[l] == -1) {
-                        slot_of[l] = -2;
-                        tnodes.push_back(l);
+            for (int64_t w = 0; w < (int64_t)which.size(); ++w) {
+                const int32_t t = which[w];
+                const auto& te = tiles[t];
+                auto& tnodes = tile_nodes[t];
+                tnodes.clear();
+                for (int32_t e : te)
+                    for (int a = 0; a < 4; ++a) {
+                        const int32_t l = local_of[m.tets[4 * (size_t)e + a]];
+                        if (slot_of[l] == -1) {
+                            slot_of[l] = -2;
+                            tnodes.push_back(l);
+                        }
                     }
-                }
-            // slots ordered by contribution count (desc), then local id: the warps of
-            // the reduction phase then walk lists of near-equal length (no divergence)
-            for (size_t k = 0; k < tnodes.size(); ++k) slot_of[tnodes[k]] = (int32_t)k;
-            cnt_of.assign(tnodes.size(), 0);
-            tile_facets(te, tfacets);
-            for (int32_t e : te)
-                for (int a = 0; a < 4; ++a) cnt_of[slot_of[local_of[m.tets[4 * (size_t)e + a]]]]++;
-            for (int32_t f : tfacets)
-                for (int a = 0; a < 3; ++a) cnt_of[slot_of[local_of[m.facets[3 * (size_t)f + a]]]]++;
-            idx.resize(tnodes.size());
-            std::iota(idx.begin(), idx.end(), 0);
-            std::sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) {
-                return cnt_of[x] != cnt_of[y] ? cnt_of[x] > cnt_of[y] : tnodes[x] < tnodes[y];
-            });
-            for (int32_t l : tnodes) slot_of[l] = -1;
-            std::vector<int32_t> sorted(tnodes.size());
-            for (size_t k = 0; k < idx.size(); ++k) sorted[k] = tnodes[idx[k]];
-            tnodes.swap(sorted);
-            const int ne = (int)te.size(), ns = (int)tnodes.size(), nf = (int)tfacets.size();
-            int ncsr = 0;  // each slot's list padded to a multiple of 4 (16-byte reads in the reduction)
-            for (int32_t cn : cnt_of) ncsr += (cn + 3) & ~3;
-            rp.tile_meta[t] = TileMeta{ne, ns, nf, ncsr};
-            if (W > 1) {  // border tile: holds a rank-shared node (its partials feed the exchange)
-                bool b = false;
-                for (int32_t l : tnodes) b = b || shared_node[l];
-                rp.tile_border[t] = b;
+                // slots ordered by contribution count (desc), then local id: the warps of
+                // the reduction phase then walk lists of near-equal length (no divergence)
+                for (size_t k = 0; k < tnodes.size(); ++k) slot_of[tnodes[k]] = (int32_t)k;
+                cnt_of.assign(tnodes.size(), 0);
+                tile_facets(te, tfacets);
+                for (int32_t e : te)
+                    for (int a = 0; a < 4; ++a) cnt_of[slot_of[local_of[m.tets[4 * (size_t)e + a]]]]++;
+                for (int32_t f : tfacets)
+                    for (int a = 0; a < 3; ++a) cnt_of[slot_of[local_of[m.facets[3 * (size_t)f + a]]]]++;
+                idx.resize(tnodes.size());
+                std::iota(idx.begin(), idx.end(), 0);
+                std::sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) {
+                    return cnt_of[x] != cnt_of[y] ? cnt_of[x] > cnt_of[y] : tnodes[x] < tnodes[y];
+                });
+                for (int32_t l : tnodes) slot_of[l] = -1;
+                sorted.resize(tnodes.size());
+                for (size_t k = 0; k < idx.size(); ++k) sorted[k] = tnodes[idx[k]];
+                tnodes.swap(sorted);
+                int ncsr = 0;  // each slot's list padded to a multiple of 4 (16-byte reads in the reduction)
+                for (int32_t cn : cnt_of) ncsr += (cn + 3) & ~3;
+                meta[t] = TileMeta{(int32_t)te.size(), (int32_t)tnodes.size(), (int32_t)tfacets.size(), ncsr};
             }
         }
+    };
+    tile_nodes.resize(tiles.size());
+    meta.resize(tiles.size());
+    {
+        std::vector<int32_t> all(tiles.size());
+        std::iota(all.begin(), all.end(), 0);
+        pass1(all);
     }
+    rp.n_tiles = (int32_t)tiles.size();
+    rp.tile_meta = meta;
+    trace_stage("plan: tile slots");
+
+    // node -> number of tiles touching it (tile-private test), rank-shared nodes, border tiles
+    std::vector<int32_t> ntiles_of(rp.n_local, 0);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int32_t t = 0; t < rp.n_tiles; ++t)
+        for (int32_t l : tile_nodes[t]) std::atomic_ref<int32_t>(ntiles_of[l]).fetch_add(1, std::memory_order_relaxed);
+    std::vector<char> shared_node(rp.n_local, 0);
+    if (W > 1)
+        for (int32_t l = 0; l < rp.n_local; ++l) {
+            const int32_t n = lnodes[l];
+            shared_node[l] = (np_off[n + 1] - np_off[n]) > 1;
+        }
+    rp.tile_border.assign(rp.n_tiles, 0);
+    if (W > 1)
+        for (int32_t t = 0; t < rp.n_tiles; ++t) {  // border tile: holds a rank-shared node
+            bool b = false;
+            for (int32_t l : tile_nodes[t]) b = b || shared_node[l];
+            rp.tile_border[t] = b;
+        }
+    rp.tile_slot_off.assign(rp.n_tiles + 1, 0);
+    rp.blob_off.assign(rp.n_tiles + 1, 0);
+    rp.elem_global.resize(Er);
+    std::vector<int64_t> elem_off(rp.n_tiles + 1, 0);
     for (int32_t t = 0; t < rp.n_tiles; ++t) {  // no throwing inside the parallel regions
         const TileMeta& tm = rp.tile_meta[t];
         const TileLayout L(tm, S.temp_dep, coords);

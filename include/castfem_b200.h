@@ -248,6 +248,26 @@ int cf_time_phases(cf_plan* plan, int64_t n_steps, double* ms_out);
 int cf_estimate_lambda_max(cf_plan* plan, int32_t iterations, uint64_t seed,
                            double* lambda_max, double* eq13_min);
 
+/* Tile-size autotuner: the recast of autotune_block_count / choose_block_count /
+ * default_block_candidates (blocked.hpp:558-623). The reference tunes the CPU
+ * cache-block count; on the B200 the knob is elements per tile (one tile per
+ * CTA). Each candidate builds a plan (opts with tile_elems = candidate), steps
+ * trial_steps from the setup's initial field twice and keeps the better device
+ * time; a candidate whose tiles do not fit shared memory times +inf. */
+typedef struct cf_tune_report {
+    int32_t n_candidates;
+    int32_t chosen;             /* tile_elems with the smallest time (first wins ties) */
+    double overhead_fraction;   /* tune wall time / (tune wall + projected run), 0 if not projected */
+} cf_tune_report;
+int cf_autotune_tiles(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts,
+                      const int32_t* candidates, int32_t n_candidates, int32_t trial_steps,
+                      double projected_total_steps, double* seconds_out, cf_tune_report* out);
+/* argmin of seconds, the first (smallest-index) candidate wins ties */
+int cf_choose_tile_elems(const int32_t* candidates, const double* seconds, int32_t n, int32_t* chosen);
+/* default candidates: multiples of 32 of the form 6*2^k (Morton chunks that are cell
+ * boxes on structured meshes) from 192 to 1536, keeping at least 148 tiles; returns the count */
+int cf_default_tile_candidates(int64_t n_elems, int32_t* out, int32_t cap, int32_t* count);
+
 /* Multi-rank transport. NCCL across processes (one rank per GPU): rank 0
  * calls cf_comm_unique_id, shares the 128 bytes, every rank calls
  * cf_comm_create. world_size ranks in one process use the in-process

@@ -74,6 +74,10 @@ class cf_stats(C.Structure):
                 ("tile_bytes_per_launch", C.c_int64)]
 
 
+class cf_tune_report(C.Structure):
+    _fields_ = [("n_candidates", C.c_int32), ("chosen", C.c_int32), ("overhead_fraction", C.c_double)]
+
+
 class cf_fixture(C.Structure):
     _fields_ = [("n_nodes", C.c_int32), ("n_elems", C.c_int32), ("n_facets", C.c_int32), ("coords", _dp),
                 ("tets", _ip), ("region", _ip), ("facets", _ip), ("facet_tag", _ip), ("node_grid", _ip)]
@@ -111,6 +115,10 @@ SIGNATURES = [
     ("cf_generate_fixture", C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, C.c_uint64,
                                       C.POINTER(cf_fixture)]),
     ("cf_counter_uniform", C.c_int, [C.c_uint64, C.POINTER(C.c_int64), C.c_int64, C.c_double, C.c_double, _dp]),
+    ("cf_autotune_tiles", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts),
+                                    _ip, C.c_int32, C.c_int32, C.c_double, _dp, C.POINTER(cf_tune_report)]),
+    ("cf_choose_tile_elems", C.c_int, [_ip, _dp, C.c_int32, C.POINTER(C.c_int32)]),
+    ("cf_default_tile_candidates", C.c_int, [C.c_int64, _ip, C.c_int32, C.POINTER(C.c_int32)]),
     ("cf_mesh_parse", C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_void_p)]),
     ("cf_mesh_view", C.c_int, [C.c_void_p, C.POINTER(cf_mesh_desc)]),
     ("cf_mesh_free", None, [C.c_void_p]),

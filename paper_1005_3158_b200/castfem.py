@@ -677,3 +677,52 @@ def write_partmap(parts: np.ndarray) -> str:
     p = np.ascontiguousarray(parts, dtype=np.int32)
     return _format(lib().cf_partmap_format, p.ctypes.data_as(_abi._ip), len(p))
 
+
+# ------------------------------------------------------------------ tile autotuner
+@dataclass
+class TuneReport:
+    """TuneReport (blocked.hpp:558-563): candidates (elements per tile), best-of-2 device
+    seconds of trial_steps per candidate, the chosen one, tune overhead fraction."""
+    candidates: List[int]
+    seconds: List[float]
+    chosen: int
+    overhead_fraction: float = 0.0
+
+
+def choose_tile_elems(candidates: Sequence[int], seconds: Sequence[float]) -> int:
+    """choose_block_count (blocked.hpp:566-575): argmin, the first candidate wins ties."""
+    c = np.ascontiguousarray(candidates, dtype=np.int32)
+    t = np.ascontiguousarray(seconds, dtype=np.float64)
+    out = C.c_int32(0)
+    check(lib().cf_choose_tile_elems(c.ctypes.data_as(_abi._ip), t.ctypes.data_as(_abi._dp),
+                                     len(c) if len(c) == len(t) else -1, C.byref(out)))
+    return int(out.value)
+
+
+def default_tile_candidates(element_count: int) -> List[int]:
+    """default_block_candidates (blocked.hpp:578-583) recast: 6*2^k tets per tile (cell boxes
+    of structured meshes in Morton order), at least one tile per SM."""
+    out = np.zeros(16, dtype=np.int32)
+    n = C.c_int32(0)
+    check(lib().cf_default_tile_candidates(int(element_count), out.ctypes.data_as(_abi._ip), 16, C.byref(n)))
+    return [int(v) for v in out[:n.value]]
+
+
+def autotune_tiles(m: Mesh, setup: SimulationSetup, opts: Optional[SolveOptions] = None,
+                   candidates: Optional[Sequence[int]] = None, trial_steps: int = 10,
+                   projected_total_steps: float = 0.0) -> TuneReport:
+    """autotune_block_count (blocked.hpp:587-623) recast for the B200: builds a plan per
+    candidate tile size and times trial_steps (best of 2, device time) from the initial field."""
+    keep = _Keep()
+    md, sd = mesh_desc(m, keep), setup_desc(setup, keep)
+    ro = run_opts(opts or SolveOptions(), keep)
+    cand = np.ascontiguousarray(candidates if candidates is not None else default_tile_candidates(m.element_count()),
+                                dtype=np.int32)
+    secs = np.zeros(max(1, len(cand)))
+    rep = _abi.cf_tune_report()
+    check(lib().cf_autotune_tiles(C.byref(md), C.byref(sd), C.byref(ro), cand.ctypes.data_as(_abi._ip), len(cand),
+                                  int(trial_steps), float(projected_total_steps), secs.ctypes.data_as(_abi._dp),
+                                  C.byref(rep)))
+    return TuneReport([int(c) for c in cand], [float(x) for x in secs[:len(cand)]], int(rep.chosen),
+                      float(rep.overhead_fraction))
+

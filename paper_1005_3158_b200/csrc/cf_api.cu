@@ -723,11 +723,18 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     std::vector<int32_t>().swap(h.merge_idx);
 }
 
+void scatter_state(cf_plan* p);
+
 void init_state(cf_plan* p, const double* T_global_host) {
     // one H2D of the global field, then on-device scatter into every rank's T ring and slot copies
     if (!p->dTg) CF_CUDA_CHECK(cudaMalloc(&p->dTg, std::max<int64_t>(1, p->N_global) * sizeof(double)));
     CF_CUDA_CHECK(cudaMemcpyAsync(p->dTg, T_global_host, (size_t)p->N_global * sizeof(double), cudaMemcpyHostToDevice,
                                   p->stream));
+    scatter_state(p);
+}
+
+// (re)initialise every rank's state from the global field staged in dTg
+void scatter_state(cf_plan* p) {
     for (auto& rp : p->ranks) {
         Rank& r = *rp;
         const int32_t nT = r.H.n_local + r.H.n_ghost;
@@ -1306,6 +1313,81 @@ int cf_device_temperature(cf_plan* p, int32_t k, double** dptr, int64_t* n) {
         if (!p || !dptr || !n || k < 0 || k >= (int32_t)p->ranks.size()) raise(CF_INVALID_ARG, "bad argument");
         *dptr = p->ranks[k]->T[p->cur];
         *n = p->ranks[k]->H.n_local;
+    });
+}
+
+int cf_choose_tile_elems(const int32_t* candidates, const double* seconds, int32_t n, int32_t* chosen) {
+    return guarded([&] {
+        // choose_block_count blocked.hpp:566-575
+        if (n <= 0 || !candidates || !seconds || !chosen) raise(CF_VALIDATION, "autotune needs one timing per candidate");
+        int32_t best = 0;
+        for (int32_t i = 1; i < n; ++i)
+            if (seconds[i] < seconds[best]) best = i;
+        *chosen = candidates[best];
+    });
+}
+
+int cf_default_tile_candidates(int64_t n_elems, int32_t* out, int32_t cap, int32_t* count) {
+    return guarded([&] {
+        if (!count) raise(CF_INVALID_ARG, "null argument");
+        int32_t c = 0;
+        for (int32_t te : {192, 384, 768, 1536}) {  // 6 * 2^k, multiples of 32 (whole warps)
+            if (c > 0 && n_elems / te < 148) break;  // keep at least one CTA per SM
+            if (out && c < cap) out[c] = te;
+            ++c;
+        }
+        *count = c;
+    });
+}
+
+int cf_autotune_tiles(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts,
+                      const int32_t* candidates, int32_t n_candidates, int32_t trial_steps,
+                      double projected_total_steps, double* seconds_out, cf_tune_report* out) {
+    return guarded([&] {
+        if (!mesh || !setup || !opts || !out) raise(CF_INVALID_ARG, "null argument");
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<int32_t> cand;
+        if (candidates && n_candidates > 0) {
+            cand.assign(candidates, candidates + n_candidates);
+        } else {
+            int32_t n = 0;
+            cand.resize(8);
+            if (cf_default_tile_candidates(mesh->n_elems, cand.data(), 8, &n) != CF_OK) raise(CF_INVALID_ARG, "candidates");
+            cand.resize(n);
+        }
+        if (trial_steps < 1) raise(CF_INVALID_ARG, "trial_steps must be >= 1");
+        std::vector<double> secs(cand.size(), INFINITY);
+        for (size_t i = 0; i < cand.size(); ++i) {
+            cf_run_opts o = *opts;
+            o.tile_elems = cand[i];
+            o.tile_of_element = nullptr;
+            cf_plan* p = nullptr;
+            const int st = cf_plan_create(mesh, setup, &o, &p);
+            if (st == CF_INVALID_ARG) continue;  // tiles too large for shared memory: +inf
+            if (st != CF_OK) raise(st, std::string("autotune candidate ") + std::to_string(cand[i]) + ": " +
+                                           g_last_error);
+            std::unique_ptr<cf_plan, int (*)(cf_plan*)> guard(p, cf_plan_destroy);
+            CF_CUDA_CHECK(cudaSetDevice(p->device));
+            for (int rep = 0; rep < 2; ++rep) {  // best of 2 from the initial field (autotune_block_count)
+                if (rep) scatter_state(p);       // dTg still holds the plan's initial field
+                p->loop_seconds = 0;
+                run_steps(p, trial_steps, 0.0);
+                secs[i] = std::min(secs[i], p->loop_seconds);
+            }
+        }
+        int32_t chosen = 0;
+        if (cf_choose_tile_elems(cand.data(), secs.data(), (int32_t)cand.size(), &chosen) != CF_OK)
+            raise(CF_VALIDATION, g_last_error);
+        out->n_candidates = (int32_t)cand.size();
+        out->chosen = chosen;
+        out->overhead_fraction = 0;
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (projected_total_steps > 0) {
+            const size_t k = (size_t)(std::find(cand.begin(), cand.end(), chosen) - cand.begin());
+            const double projected = secs[k] / trial_steps * projected_total_steps;
+            out->overhead_fraction = wall / (wall + projected);
+        }
+        if (seconds_out) std::copy(secs.begin(), secs.end(), seconds_out);
     });
 }
 

@@ -272,3 +272,18 @@ def test_cfg4_full_size_properties():
         other = cf.solve(case.mesh, case.setup, opts)
         assert other.end_time == base.end_time
         assert rel(other.T, base.T) <= RTOL, opts
+
+
+def test_autotune_tiles():
+    """autotune_block_count recast: every candidate is planned and timed (best of 2), an
+    infeasible one (2048 stored tets exceed shared memory) times +inf, the fastest is chosen,
+    and stepping with the chosen tile size stays bitwise equal to the oracle on its tiles."""
+    case = configs.casting(14, dt_safety=0.14)
+    rep = cf.autotune_tiles(case.mesh, case.setup, candidates=[192, 384, 2048], trial_steps=5,
+                            projected_total_steps=1000)
+    assert rep.candidates == [192, 384, 2048]
+    assert np.isfinite(rep.seconds[0]) and np.isfinite(rep.seconds[1]) and rep.seconds[2] == float("inf")
+    assert rep.chosen == cf.choose_tile_elems(rep.candidates, rep.seconds) and rep.chosen in (192, 384)
+    assert 0.0 < rep.overhead_fraction < 1.0
+    det, ref = run_pair(case, 20, tile_elems=rep.chosen)
+    assert np.array_equal(det.T, ref.T)

@@ -175,3 +175,22 @@ def test_error_codes():
     shared = cf.Mesh(m.nodes, m.tets.copy(), m.region.copy(), m.facets, m.facet_tag, m.tags, m.contacts)
     shared.region[0] = 1 - shared.region[0]                                    # regions share a node
     assert _tile_status(shared, s) == cf.ValidationError.code
+
+
+# ---------------------------------------------------------------- tile autotuner (host parts)
+def test_choose_tile_elems_semantics():
+    """choose_block_count (blocked.hpp:566-575): argmin, the first candidate wins ties; a
+    timing per candidate is required."""
+    assert cf.choose_tile_elems([192, 384, 768], [3.0, 1.0, 2.0]) == 384
+    assert cf.choose_tile_elems([192, 384, 768], [1.0, 1.0, 0.5 + 0.5]) == 192
+    assert cf.choose_tile_elems([384, 768], [float("inf"), 2.0]) == 768
+    with pytest.raises(cf.ValidationError):
+        cf.choose_tile_elems([192, 384], [1.0])
+    with pytest.raises(cf.ValidationError):
+        cf.choose_tile_elems([], [])
+
+
+def test_default_tile_candidates():
+    assert cf.default_tile_candidates(12_582_912) == [192, 384, 768, 1536]
+    assert cf.default_tile_candidates(100_000) == [192, 384]   # >= 148 tiles each
+    assert cf.default_tile_candidates(1_000) == [192]          # always one candidate

@@ -530,8 +530,33 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     a.meta = M.up(h.tile_meta, s);
     a.slot_off = M.up(h.tile_slot_off, s);
     a.blob_off = M.up(h.blob_off, s);
-    a.blob = M.up(h.blob, s);
     a.slot_node = M.up(h.slot_node, s);
+    {
+        // device-side packing: the host staged only the non-geometry sections; the geometry
+        // is computed here from the oriented tets and node coordinates (bitwise the host's)
+        uint8_t* blob = M.alloc<uint8_t>((size_t)std::max<int64_t>(16, h.blob_bytes));
+        DeviceMem tmp;
+        FillArgs f{};
+        f.meta = a.meta;
+        f.blob_off = a.blob_off;
+        f.rest_off = tmp.up(h.rest_off, s);
+        f.rest = tmp.up(h.blob, s);
+        f.elem_off = tmp.up(h.elem_off, s);
+        f.tets_ord = tmp.up(h.tets_ord, s);
+        f.coords = tmp.up(h.coords_local, s);
+        f.slot_off = a.slot_off;
+        f.slot_node = a.slot_node;
+        f.blob = blob;
+        f.tdep = p->temp_dep;
+        f.coords_layout = h.coords;
+        if (h.n_tiles) fill_tiles_kernel<<<h.n_tiles, 128, 0, s>>>(f);
+        CF_CUDA_CHECK(cudaGetLastError());
+        CF_CUDA_CHECK(cudaStreamSynchronize(s));
+        tmp.release();
+        a.blob = blob;
+        decltype(h.tets_ord)().swap(h.tets_ord);
+        decltype(h.coords_local)().swap(h.coords_local);
+    }
     const uint8_t* node_region = M.up(h.node_region, s);
     const int8_t* node_dir = h.node_dir.empty() ? nullptr : M.up(h.node_dir, s);
     const int32_t* local_global = M.up(h.local_global, s);

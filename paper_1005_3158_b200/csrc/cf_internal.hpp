@@ -181,7 +181,12 @@ struct RankPlan {
     std::vector<uint8_t> tile_border;      // [n_tiles] holds a rank-shared node (multi-rank)
     std::vector<int32_t> tile_slot_off;    // [n_tiles+1]
     std::vector<int64_t> blob_off;         // [n_tiles+1] byte offsets into blob
-    std::vector<uint8_t, UninitAlloc<uint8_t>> blob;  // all tile blobs
+    std::vector<uint8_t, UninitAlloc<uint8_t>> blob;  // host staging: tiles' [conn, bytes) sections at rest_off
+    std::vector<int64_t> rest_off;         // [n_tiles+1] offsets into blob (after a leading pad)
+    int64_t blob_bytes = 0;                // device blob size (blob_off[n_tiles])
+    std::vector<int64_t> elem_off;         // [n_tiles+1] first element of each tile (tile order)
+    std::vector<int32_t, UninitAlloc<int32_t>> tets_ord;    // [4 E_r] oriented tets, local ids, tile order
+    std::vector<double, UninitAlloc<double>> coords_local;  // [3 n_local] node coordinates
     bool coords = false;                   // CF_GEOM_COORDS layout (cf_tileblob.hpp)
     int32_t max_slots = 0, max_elems = 0, max_facets = 0;
     int64_t max_blob = 0;

@@ -585,6 +585,93 @@ __global__ void advance_kernel(DevState* st, const DevParams* __restrict__ P, do
     st->clamp_flag = 0;
 }
 
+// ------------------------------------------------------------------ plan upload (device-side packing)
+// tet_geometry (cf_mesh.cpp / geometry.hpp:48-77) on the device: edges first (min/max of the six
+// lengths, first pair (0,1) seeding both, as std::min/std::max), then the gradients and volume.
+__device__ __forceinline__ void dev_tet_geometry(const double (&p)[4][3], double (&g)[4][3], double& vol,
+                                                 double& min_edge, double& max_edge) {
+    double d0 = p[1][0] - p[0][0], d1 = p[1][1] - p[0][1], d2 = p[1][2] - p[0][2];
+    min_edge = max_edge = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = a + 1; b < 4; ++b) {
+            d0 = p[b][0] - p[a][0];
+            d1 = p[b][1] - p[a][1];
+            d2 = p[b][2] - p[a][2];
+            const double len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+            min_edge = len < min_edge ? len : min_edge;
+            max_edge = max_edge < len ? len : max_edge;
+        }
+    dev_tet_grads(p, g, vol);
+}
+
+struct FillArgs {
+    const TileMeta* meta;
+    const int64_t* blob_off;
+    const int64_t* rest_off;
+    const uint8_t* rest;          // host-packed [conn, bytes) sections, staged on the device
+    const int64_t* elem_off;
+    const int32_t* tets_ord;      // oriented tets, local node ids, tile order
+    const double* coords;         // local node coordinates
+    const int32_t* slot_off;
+    const int32_t* slot_node;
+    uint8_t* blob;
+    bool tdep, coords_layout;
+};
+
+// one CTA per tile: the non-geometry sections into place, then the geometry columns (stored:
+// g1 g2 g3 V max_edge; coordinates: slot xyz + max_edge), min_edge for dynamic dt
+__global__ void __launch_bounds__(128) fill_tiles_kernel(FillArgs f) {
+    const int t = blockIdx.x;
+    const TileMeta tm = f.meta[t];
+    const TileLayout L(tm, f.tdep, f.coords_layout);
+    uint8_t* B = f.blob + f.blob_off[t];
+    const int4* src = (const int4*)(f.rest + f.rest_off[t]);
+    int4* dst = (int4*)(B + L.conn);
+    for (int j = threadIdx.x; j < (L.bytes - L.conn) / 16; j += blockDim.x) dst[j] = src[j];
+    __syncthreads();  // the minedge section (dynamic dt) lies in the copied range
+    double* G = (double*)(B + L.geom);
+    const int S = L.ne2;
+    const int64_t e0 = f.elem_off[t];
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+        double g[4][3], vol = 0, mn = 0, mx = 0;
+        if (i < tm.ne) {
+            double p[4][3];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int32_t l = f.tets_ord[4 * (e0 + i) + a];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) p[a][k] = f.coords[3 * (int64_t)l + k];
+            }
+            dev_tet_geometry(p, g, vol, mn, mx);
+        } else {
+#pragma unroll
+            for (int a = 0; a < 4; ++a) g[a][0] = g[a][1] = g[a][2] = 0.0;
+        }
+        if (f.coords_layout) {
+            G[i] = mx;
+        } else {
+            const double v[11] = {g[1][0], g[1][1], g[1][2], g[2][0], g[2][1], g[2][2],
+                                  g[3][0], g[3][1], g[3][2], vol,     mx};
+#pragma unroll
+            for (int k = 0; k < 11; ++k) G[k * S + i] = v[k];
+        }
+        if (f.tdep) ((double*)(B + L.minedge))[i] = mn;
+    }
+    if (f.coords_layout) {
+        double* xyz = (double*)(B + L.xyz);
+        const int s0 = f.slot_off[t];
+        for (int k = threadIdx.x; k < tm.ns; k += blockDim.x) {
+            const int32_t l = f.slot_node[s0 + k] & 0x0fffffff;
+            xyz[4 * k] = f.coords[3 * (int64_t)l];
+            xyz[4 * k + 1] = f.coords[3 * (int64_t)l + 1];
+            xyz[4 * k + 2] = f.coords[3 * (int64_t)l + 2];
+            xyz[4 * k + 3] = 0.0;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ pack kernel
 struct PackArgs {
     int32_t n_cr, n_t;

@@ -750,7 +750,29 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
         rp.max_blob = std::max<int64_t>(rp.max_blob, L.bytes);
         rp.max_scratch = std::max<int64_t>(rp.max_scratch, L.scratch);
     }
-    rp.blob.resize(rp.blob_off[rp.n_tiles]);
+    // host staging holds each tile's non-geometry sections [conn, bytes) only; the geometry
+    // columns (or slot coordinates) are computed on the device from tets_ord / coords_local
+    // (fill_geometry_kernel, the host tet_geometry's operation order), so the host never holds
+    // the 88 B/tet of ElementGeom. A leading pad keeps every tile's base pointer in the buffer.
+    rp.rest_off.assign(rp.n_tiles + 1, 0);
+    {
+        int64_t pad = 0;
+        for (int32_t t = 0; t < rp.n_tiles; ++t)
+            pad = std::max<int64_t>(pad, TileLayout(rp.tile_meta[t], S.temp_dep, coords).conn);
+        rp.rest_off[0] = cf_round(pad, 16);
+        for (int32_t t = 0; t < rp.n_tiles; ++t) {
+            const TileLayout L(rp.tile_meta[t], S.temp_dep, coords);
+            rp.rest_off[t + 1] = rp.rest_off[t] + (L.bytes - L.conn);
+        }
+    }
+    rp.blob_bytes = rp.blob_off[rp.n_tiles];
+    rp.blob.resize(rp.rest_off[rp.n_tiles]);
+    rp.elem_off.assign(elem_off.begin(), elem_off.end());
+    rp.tets_ord.resize(4 * (size_t)Er);
+    rp.coords_local.resize(3 * (size_t)rp.n_local);
+#pragma omp parallel for schedule(static)
+    for (int32_t l = 0; l < rp.n_local; ++l)
+        for (int k = 0; k < 3; ++k) rp.coords_local[3 * (size_t)l + k] = m.pos(lnodes[l])[k];
     rp.slot_node.resize(rp.tile_slot_off[rp.n_tiles]);
     int64_t n_if = 0, n_bc = 0;
 #pragma omp parallel num_threads(nthr) reduction(+ : n_if, n_bc)
@@ -765,8 +787,8 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             const TileMeta tm = rp.tile_meta[t];
             const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
             const TileLayout L(tm, S.temp_dep, coords);
-            uint8_t* B = rp.blob.data() + rp.blob_off[t];
-            std::memset(B, 0, (size_t)L.bytes);
+            uint8_t* B = rp.blob.data() + (rp.rest_off[t] - L.conn);  // tile base; sections >= conn only
+            std::memset(B + L.conn, 0, (size_t)(L.bytes - L.conn));
             for (int k = 0; k < ns; ++k) slot_of[tnodes[k]] = k;
             tile_facets(te, tfacets);
             // per-slot contribution codes (4e+a, then 4ne+4f+a), in code order
@@ -789,31 +811,15 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                         ent[cur[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]]]++] =
                             (uint32_t)L.r_zero | (uint32_t)L.fac_idx(i, a) << 16;
             }
-            double* gsec = (double*)(B + L.geom);
             uint16_t* csec = (uint16_t*)(B + L.conn);
-            if (coords) {
-                double* xyz = (double*)(B + L.xyz);
-                for (int k = 0; k < ns; ++k) {
-                    const double* p = m.pos(lnodes[tnodes[k]]);
-                    xyz[4 * k] = p[0];
-                    xyz[4 * k + 1] = p[1];
-                    xyz[4 * k + 2] = p[2];
-                    xyz[4 * k + 3] = 0.0;
-                }
-            }
             for (int i = 0; i < ne; ++i) {
                 const int32_t e = te[i];
                 rp.elem_global[elem_off[t] + i] = e;
-                const Geom g = m.geometry(e);
-                if (coords) {
-                    gsec[i] = g.max_edge;
-                } else {
-                    const double vals[11] = {g.g[1][0], g.g[1][1], g.g[1][2], g.g[2][0], g.g[2][1], g.g[2][2],
-                                             g.g[3][0], g.g[3][1], g.g[3][2], g.vol,     g.max_edge};
-                    for (int k = 0; k < 11; ++k) gsec[(size_t)k * L.ne2 + i] = vals[k];
+                for (int a = 0; a < 4; ++a) {
+                    const int32_t l = local_of[m.tets[4 * (size_t)e + a]];  // oriented (finalize_mesh)
+                    rp.tets_ord[4 * (size_t)(elem_off[t] + i) + a] = l;
+                    csec[4 * i + a] = (uint16_t)slot_of[l];
                 }
-                if (S.temp_dep) ((double*)(B + L.minedge))[i] = g.min_edge;
-                for (int a = 0; a < 4; ++a) csec[4 * i + a] = (uint16_t)slot_of[local_of[m.tets[4 * (size_t)e + a]]];
                 B[L.region + i] = (uint8_t)m.region[e];
             }
             for (int i = 0; i < nf; ++i) {

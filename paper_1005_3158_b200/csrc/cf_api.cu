@@ -1028,6 +1028,7 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
             raise(CF_INVALID_ARG, "local_ranks must be 1 or world_size");
         if (o.mode != CF_MODE_ATOMIC && o.mode != CF_MODE_DETERMINISTIC) raise(CF_INVALID_ARG, "bad mode");
         if (o.geometry != CF_GEOM_COORDS && o.geometry != CF_GEOM_STORED) raise(CF_INVALID_ARG, "bad geometry mode");
+        if (o.fast_math != 0) raise(CF_CONFIG, "fast_math is reserved (kernels are built without FMA contraction)");
         int tile = o.tile_elems > 0 ? o.tile_elems : 384;
         if (tile > kMaxTileElems) raise(CF_INVALID_ARG, "tile_elems must be <= 2048");
 

@@ -87,3 +87,18 @@ def test_empty_mesh():
     s = cf.SimulationSetup(materials=[cf.MaterialTable.make(1.0, 1.0, 1.0)], solver=cf.SolverConfig(dt_safety=0.5))
     res = cf.solve(m, s, cf.SolveOptions(max_steps=3))
     assert res.T.shape == (0,) and res.steps == 3
+
+
+def test_plan_option_validation():
+    """Bad run options fail loudly with the C-ABI status, before any device work."""
+    import ctypes as C
+    from paper_1005_3158_b200 import _abi
+    case = configs.casting(6, dt_safety=0.14)
+    keep = cf._Keep()
+    md, sd = cf.mesh_desc(case.mesh, keep), cf.setup_desc(case.setup, keep)
+    for field, value, code in [("fast_math", 1, _abi.CF_CONFIG), ("geometry", 7, _abi.CF_INVALID_ARG),
+                               ("mode", 9, _abi.CF_INVALID_ARG), ("tile_elems", 4096, _abi.CF_INVALID_ARG)]:
+        ro = cf.run_opts(cf.SolveOptions(), keep)
+        setattr(ro, field, value)
+        h = C.c_void_p()
+        assert _abi.lib().cf_plan_create(C.byref(md), C.byref(sd), C.byref(ro), C.byref(h)) == code, field

@@ -102,3 +102,15 @@ def test_plan_option_validation():
         setattr(ro, field, value)
         h = C.c_void_p()
         assert _abi.lib().cf_plan_create(C.byref(md), C.byref(sd), C.byref(ro), C.byref(h)) == code, field
+
+
+def test_nccl_binding_single_rank():
+    """The NCCL transport's dlopen'd binding (ncclGetUniqueId / ncclCommInitRank /
+    ncclCommDestroy through cf_comm_*) on a one-rank communicator: multi-process runs need
+    one GPU per rank, which a one-GPU box cannot host."""
+    uid = cf.Comm.unique_id()
+    assert len(uid) == 128 and any(uid)
+    comm = cf.Comm(1, 0, 0, uid)
+    assert comm.handle
+    comm.close()
+    assert comm.handle is None

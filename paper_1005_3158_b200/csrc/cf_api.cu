@@ -668,6 +668,7 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     }
 
     UpdArgs& u = r.ua;
+    if (const char* e = std::getenv("CF_PROBE")) u.probe = std::atoi(e);
     u.n_local = h.n_local;
     u.n_ghost = h.n_ghost;
     u.merge_off = M.up(h.merge_off, s);  // partial merge (deterministic) + Tslot scatter (both modes)

@@ -427,6 +427,8 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
 // ------------------------------------------------------------------ update kernel
 struct UpdArgs {
     int32_t n_list, n_local, n_ghost;
+    int32_t probe;        // diagnostics only (CF_PROBE; results invalid): 8 = no slot-copy writes,
+                          // 9 = no partial reads
     const int32_t* list;  // nodes to merge + update (NULL: all local nodes)
     const int4* rec;      // packed per listed node: {node, count, slot0, slot1}, {slot2, slot3, -, -}
                           // (count > 4: slots via merge_off/merge_idx); NULL: use list + merge CSR
@@ -509,7 +511,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
             // all partial loads issued before the in-order (ascending tile) sums
             double2 pr[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) pr[q] = q < cnt ? a.part[sl[q]] : make_double2(0.0, 0.0);
+            for (int q = 0; q < 4; ++q) pr[q] = (q < cnt && a.probe != 9) ? a.part[sl[q]] : make_double2(1.0, 0.0);
             c = 0;
             r = 0;
 #pragma unroll
@@ -549,6 +551,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         const double Tn = node_update<DIR, CLAMP>(P, a.st, T, c, r, dt, t_next, DIR ? a.node_dir[i] : -1,
                                                   CLAMP ? a.node_region[i] : 0, a.local_global + i, clamped);
         a.Tn[i] = Tn;
+        if (a.probe == 8) continue;
         if (packed) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)

@@ -114,3 +114,26 @@ def test_nccl_binding_single_rank():
     assert comm.handle
     comm.close()
     assert comm.handle is None
+
+
+@pytest.mark.parametrize("tile_elems", [1, 384])
+def test_zero_lumped_capacitance_reported_like_the_reference(tile_elems):
+    """explicit_update's error (fem.hpp:110-111): temperatures 1 ulp apart inside the mushy
+    range where H absorbs the difference -> |grad H| = 0 while |grad T| > 0 -> Lemmon C_app = 0
+    -> c = 0 at every node. The GPU raises the reference's error class and message with the same
+    node, from the fused tile-private update (one tile) and from the shared-node update kernel
+    (one element per tile)."""
+    nodes = [[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 1, 1]]
+    tets = [[0, 1, 2, 3], [1, 2, 3, 4]]
+    faces = [[0, 2, 3], [0, 1, 3], [0, 1, 2], [2, 3, 4], [1, 3, 4], [1, 2, 4]]
+    m = cf.Mesh(nodes, tets, [0, 0], faces, [0] * 6, ["skin"])
+    T0 = np.full(5, 973.0)
+    T0[1] = np.nextafter(973.0, 2000.0)
+    mat = cf.MaterialTable.make(2700.0, 900.0, 200.0, latent_heat=3.9e5, solidus=821, liquidus=913, T0=973.0)
+    s = cf.SimulationSetup(materials=[mat], boundary_conditions={"skin": cf.BoundaryCondition("flux", h=0.0)},
+                           solver=cf.SolverConfig(dt_safety=0.2), initial_T=T0)
+    with pytest.raises(orc.OracleError) as ref:
+        orc.ref_solve(m, s, 3) if orc.ref_available() else orc.solve(m, s, 3)
+    with pytest.raises(cf.ValidationError) as gpu:
+        cf.solve(m, s, cf.SolveOptions(max_steps=3, tile_elems=tile_elems))
+    assert str(gpu.value) == str(ref.value).split("] ", 1)[1]

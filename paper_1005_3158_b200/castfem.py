@@ -388,9 +388,20 @@ class Solver:
         k = min(n.value, cap)
         return [SeriesSample(*buf[3 * i:3 * i + 3]) for i in range(k)]
 
-    def fields(self, want_H: bool = True) -> Tuple[np.ndarray, Optional[np.ndarray]]:
-        T = np.zeros(self._N)
-        H = np.zeros(self._N) if want_H else None
+    def fields(self, want_H: bool = True, out: Optional[Tuple[np.ndarray, Optional[np.ndarray]]] = None
+               ) -> Tuple[np.ndarray, Optional[np.ndarray]]:
+        """Global-order T (and H). `out` = caller-owned float64 arrays of node_count() entries
+        (e.g. pinned host memory) filled in place."""
+        if out is not None:
+            T, H = out
+            for a in (T, H):
+                if a is not None and (a.dtype != np.float64 or not a.flags.c_contiguous or a.size != self._N):
+                    raise ValueError("fields(out=...) needs C-contiguous float64 arrays of node_count() entries")
+            if not want_H:
+                H = None
+        else:
+            T = np.zeros(self._N)
+            H = np.zeros(self._N) if want_H else None
         check(lib().cf_get_fields(self.handle, T.ctypes.data_as(C.POINTER(C.c_double)),
                                   H.ctypes.data_as(C.POINTER(C.c_double)) if want_H else None))
         return T, H

@@ -287,3 +287,17 @@ def test_autotune_tiles():
     assert 0.0 < rep.overhead_fraction < 1.0
     det, ref = run_pair(case, 20, tile_elems=rep.chosen)
     assert np.array_equal(det.T, ref.T)
+
+
+def test_fields_into_caller_buffers():
+    """Solver.fields(out=...) fills caller-owned (e.g. pinned) arrays with the same values."""
+    case = configs.casting(10, dt_safety=0.14)
+    with cf.Solver(case.mesh, case.setup) as s:
+        s.step(7)
+        T, H = s.fields()
+        To, Ho = np.empty_like(T), np.empty_like(H)
+        T2, H2 = s.fields(out=(To, Ho))
+        assert T2 is To and H2 is Ho
+        assert np.array_equal(To, T) and np.array_equal(Ho, H)
+        with pytest.raises(ValueError):
+            s.fields(out=(np.empty(3), None))

@@ -210,6 +210,44 @@ class Plan {
     cf_plan* plan_ = nullptr;
 };
 
+// autotune_block_count on the B200 (blocked.hpp:558-623): the knob is elements per tile.
+struct TuneReport {               // castfem::TuneReport
+    std::vector<int> candidates;
+    std::vector<double> seconds;  // best-of-2 device time of trial_steps per candidate (+inf: infeasible)
+    int chosen = 0;
+    double overhead_fraction = 0;
+};
+
+template <class MeshT, class SetupT>
+TuneReport autotune_tiles(const MeshT& m, const SetupT& s, const SolveOptions& o = {},
+                          std::vector<int> candidates = {}, int trial_steps = 10,
+                          double projected_total_steps = 0) {
+    Descriptors d(m, s);
+    cf_run_opts ro{};
+    ro.device = o.device;
+    ro.mode = o.mode;
+    ro.node_order = o.node_order;
+    ro.elem_order = o.elem_order;
+    ro.geometry = o.geometry;
+    ro.world_size = 1;
+    ro.local_ranks = 1;
+    if (candidates.empty()) {
+        int32_t buf[16], n = 0;
+        check(cf_default_tile_candidates((int64_t)m.tets.size(), buf, 16, &n));
+        candidates.assign(buf, buf + n);
+    }
+    std::vector<int32_t> c(candidates.begin(), candidates.end());
+    TuneReport r;
+    r.candidates = candidates;
+    r.seconds.assign(c.size(), 0.0);
+    cf_tune_report rep{};
+    check(cf_autotune_tiles(d.mesh(), d.setup(), &ro, c.data(), (int32_t)c.size(), trial_steps,
+                            projected_total_steps, r.seconds.data(), &rep));
+    r.chosen = rep.chosen;
+    r.overhead_fraction = rep.overhead_fraction;
+    return r;
+}
+
 // solve_serial on the B200 (blocked.hpp:650-696): same loop semantics.
 template <class MeshT, class SetupT>
 SolveResult solve_gpu(const MeshT& m, const SetupT& s, const SolveOptions& o = {},

@@ -85,5 +85,11 @@ int main() {
         return 2;
     } catch (const config_error&) {
     }
-    return ok ? 0 : 1;
+    // autotune_block_count recast through the shim: every candidate timed, the fastest chosen
+    const castfem_b200::TuneReport tr = castfem_b200::autotune_tiles(m, s, go, {64, 128}, 3);
+    const bool tune_ok = tr.candidates.size() == 2 && (tr.chosen == 64 || tr.chosen == 128) &&
+                         tr.seconds[0] > 0 && tr.seconds[1] > 0;
+    std::printf("autotune: chosen %d (%.3e s, %.3e s) %s\n", tr.chosen, tr.seconds[0], tr.seconds[1],
+                tune_ok ? "OK" : "BAD");
+    return ok && tune_ok ? 0 : 1;
 }

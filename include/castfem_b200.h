@@ -359,6 +359,11 @@ int cf_mesh_view(const cf_text_mesh* m, cf_mesh_desc* out);
 void cf_mesh_free(cf_text_mesh* m);
 /* write_mesh mesh.hpp:327-343 (coordinates %.17g) */
 int cf_mesh_format(const cf_mesh_desc* mesh, char* buf, int64_t cap, int64_t* len);
+/* binary fast path (this repo's format "CFMESHB1": counts, then the raw arrays and tag
+ * strings; little-endian) for meshes too large for text; parse validates and orients like
+ * cf_mesh_parse. format: *len = bytes needed; buf (if non-NULL) must hold them. */
+int cf_mesh_parse_binary(const void* data, int64_t len, cf_text_mesh** out);
+int cf_mesh_format_binary(const cf_mesh_desc* mesh, void* buf, int64_t cap, int64_t* len);
 
 /* parse_config material.hpp:186-345: [material r] rho c k latent_heat solidus
  * liquidus T0 / [bc tag] kind T q h T_inf / [interface a b] h h_time h_temp /

@@ -123,6 +123,8 @@ SIGNATURES = [
     ("cf_mesh_view", C.c_int, [C.c_void_p, C.POINTER(cf_mesh_desc)]),
     ("cf_mesh_free", None, [C.c_void_p]),
     ("cf_mesh_format", C.c_int, [C.POINTER(cf_mesh_desc), C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]),
+    ("cf_mesh_parse_binary", C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
+    ("cf_mesh_format_binary", C.c_int, [C.POINTER(cf_mesh_desc), C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
     ("cf_config_parse", C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_void_p)]),
     ("cf_config_view", C.c_int, [C.c_void_p, C.POINTER(cf_setup_desc)]),
     ("cf_config_free", None, [C.c_void_p]),

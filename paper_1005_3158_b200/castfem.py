@@ -619,12 +619,7 @@ def _table(t: "_abi.cf_table") -> PiecewiseLinear:
     return PiecewiseLinear([t.x[i] for i in range(t.n)], [t.y[i] for i in range(t.n)])
 
 
-def parse_mesh(text) -> Mesh:
-    """parse_mesh (mesh.hpp:256-325): 'femesh 1' text -> a finalized Mesh (oriented tets).
-    Raises ParseError (line-numbered) / ValidationError like the reference."""
-    b = _text_arg(text)
-    h = C.c_void_p()
-    check(lib().cf_mesh_parse(b, len(b), C.byref(h)))
+def _mesh_from_handle(h) -> Mesh:
     try:
         d = _abi.cf_mesh_desc()
         check(lib().cf_mesh_view(h, C.byref(d)))
@@ -638,15 +633,47 @@ def parse_mesh(text) -> Mesh:
         lib().cf_mesh_free(h)
 
 
+def parse_mesh(text) -> Mesh:
+    """parse_mesh (mesh.hpp:256-325): 'femesh 1' text -> a finalized Mesh (oriented tets).
+    Raises ParseError (line-numbered) / ValidationError like the reference."""
+    b = _text_arg(text)
+    h = C.c_void_p()
+    check(lib().cf_mesh_parse(b, len(b), C.byref(h)))
+    return _mesh_from_handle(h)
+
+
 def write_mesh(m: Mesh) -> str:
     """write_mesh (mesh.hpp:327-343)."""
     keep = _Keep()
     return _format(lib().cf_mesh_format, C.byref(mesh_desc(m, keep)))
 
 
+MESH_BINARY_MAGIC = b"CFMESHB1"
+
+
+def parse_mesh_binary(data: bytes) -> Mesh:
+    """The binary fast path ("CFMESHB1"): same validation / orientation as parse_mesh."""
+    b = bytes(data)
+    h = C.c_void_p()
+    check(lib().cf_mesh_parse_binary(b, len(b), C.byref(h)))
+    return _mesh_from_handle(h)
+
+
+def write_mesh_binary(m: Mesh) -> bytes:
+    keep = _Keep()
+    d = mesh_desc(m, keep)
+    n = C.c_int64(0)
+    check(lib().cf_mesh_format_binary(C.byref(d), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(max(1, n.value))
+    check(lib().cf_mesh_format_binary(C.byref(d), buf, n.value, C.byref(n)))
+    return buf.raw[:n.value]
+
+
 def read_mesh(path: str) -> Mesh:
+    """A mesh file: the reference's femesh text, or this repo's binary fast path (by magic)."""
     with open(path, "rb") as f:
-        return parse_mesh(f.read())
+        data = f.read()
+    return parse_mesh_binary(data) if data[:8] == MESH_BINARY_MAGIC else parse_mesh(data)
 
 
 def parse_config(text) -> SimulationSetup:

@@ -2,6 +2,7 @@
 //   femesh 1 mesh       parse_mesh / write_mesh      mesh.hpp:256-343
 //   solver config       parse_config                 material.hpp:186-345
 //   partmap             load_partmap / write_partmap partition.hpp:424-449
+//   binary mesh         this repo's fast path for large meshes (same validation as parse_mesh)
 // Same tokenizer ('#' comments, whitespace-separated tokens, blank lines skipped,
 // 1-based line numbers), the same number syntax (std::from_chars), the same
 // section semantics and defaults, and the same error classes and messages:
@@ -193,6 +194,84 @@ std::string format_mesh(const cf_mesh_desc* d) {  // write_mesh mesh.hpp:327-343
     for (int64_t c = 0; c < d->n_contacts; ++c)
         s += "contact " + tag(d->contacts[2 * c]) + " " + tag(d->contacts[2 * c + 1]) + "\n";
     return s;
+}
+
+// ------------------------------------------------------------------ binary mesh (fast path)
+// "CFMESHB1" | i64 N E F n_tags n_contacts | f64 coords[3N] | i32 tets[4E] region[E]
+// facets[3F] facet_tag[F] contacts[2C] | per tag: i32 length + bytes. Little-endian.
+namespace {
+constexpr char kMagic[8] = {'C', 'F', 'M', 'E', 'S', 'H', 'B', '1'};
+}
+
+std::string mesh_binary(const cf_mesh_desc* d) {
+    std::string s(kMagic, 8);
+    auto put = [&](const void* p, size_t n) { s.append((const char*)p, n); };
+    const int64_t hdr[5] = {d->n_nodes, d->n_elems, d->n_facets, d->n_tags, d->n_contacts};
+    put(hdr, sizeof hdr);
+    put(d->coords, 24 * (size_t)d->n_nodes);
+    put(d->tets, 16 * (size_t)d->n_elems);
+    put(d->region, 4 * (size_t)d->n_elems);
+    put(d->facets, 12 * (size_t)d->n_facets);
+    put(d->facet_tag, 4 * (size_t)d->n_facets);
+    put(d->contacts, 8 * (size_t)d->n_contacts);
+    for (int32_t t = 0; t < d->n_tags; ++t) {
+        const int32_t n = (int32_t)std::strlen(d->tags[t]);
+        put(&n, 4);
+        put(d->tags[t], (size_t)n);
+    }
+    return s;
+}
+
+std::unique_ptr<TextMesh> parse_mesh_binary(std::string_view b) {
+    size_t pos = 0;
+    auto take = [&](void* dst, size_t n) {
+        if (b.size() - pos < n) raise(CF_PARSE, "binary mesh truncated at byte " + std::to_string(pos));
+        if (n) std::memcpy(dst, b.data() + pos, n);
+        pos += n;
+    };
+    char magic[8];
+    if (b.size() < 8) raise(CF_PARSE, "binary mesh: missing header");
+    take(magic, 8);
+    if (std::memcmp(magic, kMagic, 8) != 0) raise(CF_PARSE, "binary mesh: bad magic (expected CFMESHB1)");
+    int64_t h[5];
+    take(h, sizeof h);
+    for (int k = 0; k < 5; ++k)
+        if (h[k] < 0 || h[k] > INT32_MAX) raise(CF_PARSE, "binary mesh: bad count in header");
+    auto m = std::make_unique<TextMesh>();
+    m->coords.resize(3 * (size_t)h[0]);
+    m->tets.resize(4 * (size_t)h[1]);
+    m->region.resize((size_t)h[1]);
+    m->facets.resize(3 * (size_t)h[2]);
+    m->facet_tag.resize((size_t)h[2]);
+    m->contacts.resize(2 * (size_t)h[4]);
+    take(m->coords.data(), 8 * m->coords.size());
+    take(m->tets.data(), 4 * m->tets.size());
+    take(m->region.data(), 4 * m->region.size());
+    take(m->facets.data(), 4 * m->facets.size());
+    take(m->facet_tag.data(), 4 * m->facet_tag.size());
+    take(m->contacts.data(), 4 * m->contacts.size());
+    for (int64_t t = 0; t < h[3]; ++t) {
+        int32_t n = 0;
+        take(&n, 4);
+        if (n < 0) raise(CF_PARSE, "binary mesh: bad tag length");
+        std::string tag((size_t)n, '\0');
+        take(tag.data(), (size_t)n);
+        m->tags.push_back(tag);
+    }
+    if (pos != b.size()) raise(CF_PARSE, "binary mesh: trailing bytes");
+    for (int32_t v : m->facet_tag)
+        if (v < 0 || v >= (int32_t)m->tags.size()) raise(CF_VALIDATION, "mesh validation failed: facet tag out of range");
+    for (int32_t v : m->contacts)
+        if (v < 0 || v >= (int32_t)m->tags.size()) raise(CF_VALIDATION, "mesh validation failed: contact tag out of range");
+    m->make_desc();
+    MeshData md;  // the text parser's finalize_mesh contract: validation + orientation
+    try {
+        finalize_mesh(&m->desc, md);
+    } catch (const Error& e) {
+        raise(CF_VALIDATION, std::string("mesh validation failed: ") + e.what());
+    }
+    std::memcpy(m->tets.data(), md.tets.data(), sizeof(int32_t) * m->tets.size());
+    return m;
 }
 
 // ------------------------------------------------------------------ config
@@ -479,6 +558,27 @@ int cf_mesh_view(const cf_text_mesh* m, cf_mesh_desc* out) {
 }
 
 void cf_mesh_free(cf_text_mesh* m) { delete m; }
+
+int cf_mesh_parse_binary(const void* data, int64_t len, cf_text_mesh** out) {
+    return io_guarded([&] {
+        if (!out || (len && !data) || len < 0) raise(CF_INVALID_ARG, "null argument");
+        auto m = parse_mesh_binary(std::string_view((const char*)data, (size_t)len));
+        auto r = std::make_unique<cf_text_mesh>();
+        static_cast<TextMesh&>(*r) = std::move(*m);
+        r->make_desc();
+        *out = r.release();
+    });
+}
+
+int cf_mesh_format_binary(const cf_mesh_desc* d, void* buf, int64_t cap, int64_t* len) {
+    return io_guarded([&] {
+        if (!d) raise(CF_INVALID_ARG, "null argument");
+        const std::string s = mesh_binary(d);
+        if (len) *len = (int64_t)s.size();
+        if (buf && cap >= (int64_t)s.size()) std::memcpy(buf, s.data(), s.size());
+        else if (buf) raise(CF_INVALID_ARG, "buffer too small for the binary mesh");
+    });
+}
 
 int cf_mesh_format(const cf_mesh_desc* d, char* buf, int64_t cap, int64_t* len) {
     return io_guarded([&] {

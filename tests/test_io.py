@@ -214,3 +214,37 @@ def test_partmap_roundtrip():
     p = np.array([3, 0, 2, 2, 1], dtype=np.int32)
     parts, count = cf.load_partmap(cf.write_partmap(p), len(p))
     assert np.array_equal(parts, p) and count == 4
+
+
+# ---------------------------------------------------------------- binary fast path
+def test_binary_mesh_roundtrip_equals_text(tmp_path):
+    """The binary fast path holds exactly what the text format holds (after the same
+    finalize_mesh), and read_mesh dispatches on the magic."""
+    text, m = _casting_text(6, 0.2, 4)
+    from_text = cf.parse_mesh(text)
+    blob = cf.write_mesh_binary(m)
+    assert blob[:8] == cf.MESH_BINARY_MAGIC
+    from_bin = cf.parse_mesh_binary(blob)
+    for a, b in [(from_text.nodes, from_bin.nodes), (from_text.tets, from_bin.tets), (from_text.region, from_bin.region),
+                 (from_text.facets, from_bin.facets)]:
+        assert np.array_equal(a, b)
+    assert [from_text.tags[t] for t in from_text.facet_tag] == [from_bin.tags[t] for t in from_bin.facet_tag]
+    p = tmp_path / "m.cfmb"
+    p.write_bytes(blob)
+    assert np.array_equal(cf.read_mesh(str(p)).tets, from_bin.tets)
+    p2 = tmp_path / "m.femesh"
+    p2.write_bytes(text)
+    assert np.array_equal(cf.read_mesh(str(p2)).tets, from_text.tets)
+
+
+def test_binary_mesh_errors():
+    _, m = _casting_text(3, 0.0, 0)
+    blob = cf.write_mesh_binary(m)
+    for bad in [b"", b"NOTAMESH" + blob[8:], blob[:-3], blob + b"x"]:
+        with pytest.raises(cf.ParseError):
+            cf.parse_mesh_binary(bad)
+    bad_tet = bytearray(blob)  # first tet's first node -> out of range: validation like parse_mesh
+    off = 8 + 40 + 24 * m.node_count()
+    bad_tet[off:off + 4] = (10 ** 6).to_bytes(4, "little")
+    with pytest.raises(cf.ValidationError, match="mesh validation failed"):
+        cf.parse_mesh_binary(bytes(bad_tet))

@@ -300,6 +300,11 @@ def main():
         pin = lambda: torch.empty(mesh.node_count(), dtype=torch.float64, pin_memory=True).numpy()
         T0, Tout, Hout = pin(), pin(), pin()
         T0[:] = T0src
+        # one untimed pass warms the path (first launches of the scatter / gather kernels load
+        # them lazily; first transfers through freshly pinned pages)
+        solver.set_temperature(T0)
+        solver.step(1)
+        solver.fields(out=(Tout, Hout))
         barrier()
         t1 = time.perf_counter()
         solver.set_temperature(T0)

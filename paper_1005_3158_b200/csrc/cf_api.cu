@@ -211,7 +211,6 @@ struct Rank {
         int heavy;  // footprint outlier class: concurrent launch on the side stream
     };
     std::vector<TileLaunch> launches;
-    int32_t* all_list = nullptr;   // unused (NULL list = identity)
     int32_t* shared_list = nullptr;
     int4* shared_rec = nullptr;     // packed update records of shared_list
     int32_t n_shared_list = 0;

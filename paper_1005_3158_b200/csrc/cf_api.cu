@@ -865,15 +865,18 @@ __device__ void lam_geom(const LamArgs& L, const uint8_t* B, const TileLayout& L
         dev_tet_grads(p, g, vol);
         return;
     }
-    const double* G = (const double*)(B + Ly.geom);
+    const double* G = (const double*)(B + Ly.geom);  // pairs (g1x g1y) (g1z g2x) (g2y g2z) (g3x g3y) (g3z vol)
     const int S = Ly.ne2;
+    const double v[10] = {G[2 * i], G[2 * i + 1], G[2 * (S + i)], G[2 * (S + i) + 1], G[2 * (2 * S + i)],
+                          G[2 * (2 * S + i) + 1], G[2 * (3 * S + i)], G[2 * (3 * S + i) + 1], G[2 * (4 * S + i)],
+                          G[2 * (4 * S + i) + 1]};
     for (int k = 0; k < 3; ++k) {
-        g[1][k] = G[k * S + i];
-        g[2][k] = G[(3 + k) * S + i];
-        g[3][k] = G[(6 + k) * S + i];
+        g[1][k] = v[k];
+        g[2][k] = v[3 + k];
+        g[3][k] = v[6 + k];
         g[0][k] = ((g[1][k] + g[2][k]) + g[3][k]) * -1.0;
     }
-    vol = G[9 * S + i];
+    vol = v[9];
 }
 
 // lambda_max operator on the tile blobs (global reads, no shared memory)
@@ -884,20 +887,17 @@ __global__ void lam_setup(LamArgs L) {
     const TileLayout Ly(tm, L.tdep, L.coords);
     const uint8_t* B = a.blob + a.blob_off[t];
     const int s0 = a.slot_off[t];
-    const ushort4* conn = (const ushort4*)(B + Ly.conn);
     for (int i = threadIdx.x; i < tm.ne; i += blockDim.x) {
-        const ushort4 cn = conn[i];
+        const ushort4 cn = *(const ushort4*)(B + Ly.conn_of(i));
         double g[4][3], vol;
         lam_geom(L, B, Ly, i, cn, g, vol);
         const double w = L.cval[B[Ly.region + i]] * vol * 0.25;
         const unsigned short sl[4] = {cn.x, cn.y, cn.z, cn.w};
         for (int k = 0; k < 4; ++k) atomicAdd(&L.M[a.slot_node[s0 + sl[k]] & 0x0fffffff], w);
     }
-    const ushort4* fsl = (const ushort4*)(B + Ly.fslots);
-    const double* farea = (const double*)(B + Ly.farea);
     for (int i = threadIdx.x; i < tm.nf; i += blockDim.x) {
-        const ushort4 fs = fsl[i];
-        const double w = L.hval[fs.w] * (farea[i] / 3.0);
+        const ushort4 fs = *(const ushort4*)(B + Ly.fac_slots(i));
+        const double w = L.hval[fs.w] * (*(const double*)(B + Ly.fac_area(i)) / 3.0);
         const unsigned short sl[3] = {fs.x, fs.y, fs.z};
         for (int k = 0; k < 3; ++k) atomicAdd(&L.D[a.slot_node[s0 + sl[k]] & 0x0fffffff], w);
     }
@@ -910,9 +910,8 @@ __global__ void lam_apply(LamArgs L) {
     const TileLayout Ly(tm, L.tdep, L.coords);
     const uint8_t* B = a.blob + a.blob_off[t];
     const int s0 = a.slot_off[t];
-    const ushort4* conn = (const ushort4*)(B + Ly.conn);
     for (int i = threadIdx.x; i < tm.ne; i += blockDim.x) {
-        const ushort4 cn = conn[i];
+        const ushort4 cn = *(const ushort4*)(B + Ly.conn_of(i));
         const int32_t n[4] = {a.slot_node[s0 + cn.x] & 0x0fffffff, a.slot_node[s0 + cn.y] & 0x0fffffff,
                               a.slot_node[s0 + cn.z] & 0x0fffffff, a.slot_node[s0 + cn.w] & 0x0fffffff};
         double g[4][3], vol;

@@ -150,7 +150,8 @@ struct TileArgs {
     int32_t prefetch;    // stages == 1: tile it + prefetch is staged into L2 by CTA it (0: off)
     int32_t scratch_off; // coordinates layout: byte offset of the contribution scratch in shared memory
     int32_t probe;       // diagnostics only (CF_PROBE; results invalid): 1 = copies only, 3 = no
-                         // reduction phase, 4 = no element phase, 5 = no enthalpy evaluation
+                         // reduction phase, 4 = no element phase, 5 = no enthalpy evaluation,
+                         // 6 = every CTA re-reads one of 1184 L2-resident tiles
     double t_end;
 };
 
@@ -159,6 +160,10 @@ constexpr uint32_t kBulkChunk = 32768;
 struct TileHdr {  // per stage: the metadata of the tile in flight (written before the barrier arrive)
     TileMeta tm;
     int32_t s0;
+    // the tile's section layout, computed once by the issuing thread (raw storage: TileLayout
+    // has a constructor, which __shared__ variables cannot run)
+    alignas(8) unsigned char L[sizeof(TileLayout)];
+    __device__ __forceinline__ const TileLayout& layout() const { return *reinterpret_cast<const TileLayout*>(L); }
 };
 
 // `it` indexes the launch's tile descriptors
@@ -166,6 +171,7 @@ struct TileHdr {  // per stage: the metadata of the tile in flight (written befo
 // issue_slot_copy after griddep_wait; the barrier already expects their bytes)
 __device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int it, bool tdep, bool coords, uint8_t* dst,
                                                 double* sTdst, uint64_t* bar, TileHdr* hdr, bool slots = true) {
+    if (a.probe == 6) it %= 1184;  // diagnostics: L2-resident tiles (compute-side time)
     const int4 d0 = __ldg((const int4*)(a.desc + it)), d1 = __ldg((const int4*)(a.desc + it) + 1);
     const TileMeta tm{d0.x, d0.y, d0.z, d0.w};
     const int32_t s0 = d1.x;
@@ -173,6 +179,7 @@ __device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int it, bool 
     hdr->tm = tm;  // published by the arrive below (release), read after the wait (acquire)
     hdr->s0 = s0;
     const TileLayout L(tm, tdep, coords);
+    *reinterpret_cast<TileLayout*>(hdr->L) = L;
     const uint32_t tbytes = 8u * (uint32_t)cf_round32(tm.ns, 2);
     mbar_expect_tx(bar, (uint32_t)L.bytes + tbytes);
     const uint8_t* src = a.blob + boff;
@@ -261,7 +268,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         mbar_wait(&bar[stage], a.stages == 2 ? ((k >> 1) & 1) : (k & 1));
         const TileMeta tm = hdr[stage].tm;
         const int s0 = hdr[stage].s0;
-        const TileLayout L(tm, TDEP, GC);
+        const TileLayout& L = hdr[stage].layout();
         const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
         if (a.probe == 1) {  // diagnostics: memory-path timing without the physics
             __syncthreads();
@@ -277,18 +284,17 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         }
         __syncthreads();
 
-        // phase 2a: elements (element_accumulate fem.hpp:57-70). Contributions go to the
-        // contrib columns (lump -> col 0, rc[k] -> col 1+k): with stored geometry these
-        // are this element's consumed geometry columns, with coordinates a scratch area
-        double* G = (double*)(B + L.geom);
-        double* R = GC ? (double*)(smem + a.scratch_off) : (double*)B;  // reduction operand base
+        // phase 2a: elements (element_accumulate fem.hpp:57-70). Stored layout: the element's
+        // four (lump, rc_q) pairs go over its own consumed geometry pairs (columns 0..3);
+        // coordinates layout: lump / rc columns of the shared-memory scratch R
         const int S = L.ne2;
-        const ushort4* conn = (const ushort4*)(B + L.conn);
+        double* R = (double*)(smem + a.scratch_off);  // coordinates layout only
         const uint8_t* ereg = B + L.region;
         for (int i = tid; i < (a.probe == 4 ? 0 : ne); i += kTileThreads) {
             double g[4][3], vol, max_edge;
-            const ushort4 cn = conn[i];
+            ushort4 cn;
             if (GC) {
+                cn = ((const ushort4*)(B + L.conn))[i];
                 const double2* X = (const double2*)(B + L.xyz);  // slot (x, y) (z, 0)
                 const unsigned short sl[4] = {cn.x, cn.y, cn.z, cn.w};
                 double p[4][3];
@@ -300,16 +306,25 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                     p[k][2] = z0.x;
                 }
                 dev_tet_grads(p, g, vol);
-                max_edge = G[i];
+                max_edge = ((const double*)(B + L.geom))[i];
             } else {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    g[1][c] = G[c * S + i];
-                    g[2][c] = G[(3 + c) * S + i];
-                    g[3][c] = G[(6 + c) * S + i];
-                }
-                vol = G[9 * S + i];
-                max_edge = G[10 * S + i];
+                const double2* G2 = (const double2*)(B + L.geom);
+                const double2 c0 = G2[i], c1 = G2[S + i], c2 = G2[2 * S + i], c3 = G2[3 * S + i],
+                              c4 = G2[4 * S + i], c5 = G2[5 * S + i];
+                g[1][0] = c0.x;
+                g[1][1] = c0.y;
+                g[1][2] = c1.x;
+                g[2][0] = c1.y;
+                g[2][1] = c2.x;
+                g[2][2] = c2.y;
+                g[3][0] = c3.x;
+                g[3][1] = c3.y;
+                g[3][2] = c4.x;
+                vol = c4.y;
+                max_edge = c5.x;
+                const long long cb = __double_as_longlong(c5.y);
+                cn = make_ushort4((unsigned short)cb, (unsigned short)(cb >> 16), (unsigned short)(cb >> 32),
+                                  (unsigned short)(cb >> 48));
 #pragma unroll
                 for (int c = 0; c < 3; ++c) g[0][c] = ((g[1][c] + g[2][c]) + g[3][c]) * -1.0;
             }
@@ -321,17 +336,27 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             dev_element<TDEP>(P, m, g, vol, max_edge, T, H, lump, rc);
             if (TDEP)
                 local_min = fmin(local_min, dev_stable_bound<TDEP>(P, m, ((const double*)(B + L.minedge))[i], T));
-            R[L.lump_idx(i)] = lump;
+            if (GC) {
+                R[L.lump_idx(i)] = lump;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) R[L.rc_idx(i, c)] = rc[c];
+                for (int c = 0; c < 4; ++c) R[L.rc_idx(i, c)] = rc[c];
+            } else {
+                double2* W = (double2*)B;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) W[L.pair_elem(i, c)] = make_double2(lump, rc[c]);
+            }
         }
         // phase 2b: facets (facet_flux_accumulate fem.hpp:74-79; interface blocked.hpp:485-490);
-        // terms go to R[fac_idx] (stored layout: over the facet's consumed area / sister slots)
-        double* farea = (double*)(B + L.farea);
-        double* fsis = (double*)(B + L.fsister);
-        const ushort4* fsl = (const ushort4*)(B + L.fslots);
+        // terms stored negated (the reduction does r -= v for every entry: r - (-f) == r + f
+        // exactly): stored layout as (0.0, -term_a) pairs over the facet's own consumed record,
+        // coordinates layout into the scratch's facet-term columns
         for (int i = tid; i < nf; i += kTileThreads) {
-            const ushort4 fs = fsl[i];
+            const double2* rec = (const double2*)(B + L.fac + 48 * i);  // (area, slots+kind), sisters
+            const double2 rec0 = rec[0];
+            const double area = rec0.x;
+            const long long fb = __double_as_longlong(rec0.y);
+            const ushort4 fs = make_ushort4((unsigned short)fb, (unsigned short)(fb >> 16), (unsigned short)(fb >> 32),
+                                            (unsigned short)(fb >> 48));
             const DevFacetKind& K = P->kind[fs.w];
             const double ts[3] = {sT[fs.x], sT[fs.y], sT[fs.z]};
             double q, h, tinf;
@@ -339,53 +364,73 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                 const double var = K.var == CF_VAR_TIME ? time : (ts[0] + ts[1] + ts[2]) / 3.0;
                 q = 0.0;
                 h = dev_pl_eval(P, K.htab, var);
-                const int4 sn = ((const int4*)fsis)[i];
+                const double2 rec1 = rec[1];
+                const long long s01 = __double_as_longlong(rec1.x), s23 = __double_as_longlong(rec1.y);
                 // interface_ambient from the PRE-update T of the previous step (refresh_ambient lag)
                 double sum = 0;
-                sum += a.Told[sn.x];
-                sum += a.Told[sn.y];
-                sum += a.Told[sn.z];
-                sum += a.Told[sn.w];
+                sum += a.Told[(int32_t)s01];
+                sum += a.Told[(int32_t)(s01 >> 32)];
+                sum += a.Told[(int32_t)s23];
+                sum += a.Told[(int32_t)(s23 >> 32)];
                 tinf = 0.25 * sum;
             } else {
                 q = K.q;
                 h = K.h;
                 tinf = K.t_inf;
             }
-            const double third = farea[i] / 3.0;
+            const double third = area / 3.0;
             const double f0 = third * (-q + h * (tinf - ts[0]));
             const double f1 = third * (-q + h * (tinf - ts[1]));
             const double f2 = third * (-q + h * (tinf - ts[2]));
-            // stored negated: the reduction does r -= v for every entry (r - (-f) == r + f exactly)
-            R[L.fac_idx(i, 0)] = -f0;
-            R[L.fac_idx(i, 1)] = -f1;
-            R[L.fac_idx(i, 2)] = -f2;
+            if (GC) {
+                R[L.fac_idx(i, 0)] = -f0;
+                R[L.fac_idx(i, 1)] = -f1;
+                R[L.fac_idx(i, 2)] = -f2;
+            } else {
+                double2* W = (double2*)B;
+                W[L.pair_facet(i, 0)] = make_double2(0.0, -f0);
+                W[L.pair_facet(i, 1)] = make_double2(0.0, -f1);
+                W[L.pair_facet(i, 2)] = make_double2(0.0, -f2);
+            }
         }
         __syncthreads();
 
-        // phase 3: per-slot fixed-order reduction (ascending element, then facets) + flush.
-        // Each entry is a precomputed (lump, residual) operand pair: element e, corner q ->
-        // (lump[e], rc_q[e]); facet f, corner a -> (0.0, -term_a[f]).
+        // phase 3: per-slot fixed-order reduction (ascending element, then facets) + flush,
+        // through the slot's 16-bit operand codes (cf_tileblob.hpp)
         const uint16_t* cend = (const uint16_t*)(B + L.csr_end);
-        const uint32_t* csr = (const uint32_t*)(B + L.csr);
+        const uint16_t* csr = (const uint16_t*)(B + L.csr);
         const int32_t* snode = (const int32_t*)(B + L.snode);
+        const double2* W = (const double2*)B;
         for (int s = tid; s < (a.probe == 3 ? 0 : ns); s += kTileThreads) {
             const int beg = s == 0 ? 0 : cend[s - 1];
             const int end = cend[s];
             double c = 0, r = 0;
             for (int j = beg; j < end; j += 4) {  // lists padded to 4 with exact (0.0, 0.0) no-ops
-                const uint4 pr = *(const uint4*)(csr + j);
-                const double l0 = R[pr.x & 0xffffu], l1 = R[pr.y & 0xffffu], l2 = R[pr.z & 0xffffu],
-                             l3 = R[pr.w & 0xffffu];
-                const double q0 = R[pr.x >> 16], q1 = R[pr.y >> 16], q2 = R[pr.z >> 16], q3 = R[pr.w >> 16];
-                c += l0;
-                r -= q0;
-                c += l1;
-                r -= q1;
-                c += l2;
-                r -= q2;
-                c += l3;
-                r -= q3;
+                const uint2 pr = *(const uint2*)(csr + j);
+                const uint32_t v[4] = {pr.x & 0xffffu, pr.x >> 16, pr.y & 0xffffu, pr.y >> 16};
+                double l[4], q[4];
+                if (GC) {
+                    const int32_t rz = L.r_zero, rl = L.r_lump;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const bool op = v[k] & 0x8000u;
+                        const int li = rl + (int)(v[k] & 0x3ffu);
+                        l[k] = R[op ? rz : li];
+                        q[k] = R[op ? (int)(v[k] & 0x7fffu) : li + ((int)(v[k] >> 10) + 1) * S];
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const double2 w = W[v[k]];
+                        l[k] = w.x;
+                        q[k] = w.y;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    c += l[k];
+                    r -= q[k];
+                }
             }
             const int info = sinfo[s];
             const int32_t node = snode[s];
@@ -623,19 +668,21 @@ struct FillArgs {
     bool tdep, coords_layout;
 };
 
-// one CTA per tile: the non-geometry sections into place, then the geometry columns (stored:
-// g1 g2 g3 V max_edge; coordinates: slot xyz + max_edge), min_edge for dynamic dt
+// one CTA per tile: the staged sections into place, then the geometry (stored: the six
+// 16-byte pair columns g1 g2 g3 vol (max_edge, conn); coordinates: slot xyz + max_edge),
+// min_edge for dynamic dt
 __global__ void __launch_bounds__(128) fill_tiles_kernel(FillArgs f) {
     const int t = blockIdx.x;
     const TileMeta tm = f.meta[t];
     const TileLayout L(tm, f.tdep, f.coords_layout);
     uint8_t* B = f.blob + f.blob_off[t];
-    const int4* src = (const int4*)(f.rest + f.rest_off[t]);
-    int4* dst = (int4*)(B + L.conn);
-    for (int j = threadIdx.x; j < (L.bytes - L.conn) / 16; j += blockDim.x) dst[j] = src[j];
-    __syncthreads();  // the minedge section (dynamic dt) lies in the copied range
-    double* G = (double*)(B + L.geom);
+    const uint8_t* stg = f.rest + f.rest_off[t];
     const int S = L.ne2;
+    const int skip = f.coords_layout ? 0 : 8 * S;  // stored: the connectivity prefix goes into the pairs
+    const int4* src = (const int4*)(stg + skip);
+    int4* dst = (int4*)(B + L.stage);
+    for (int j = threadIdx.x; j < (L.bytes - L.stage) / 16; j += blockDim.x) dst[j] = src[j];
+    __syncthreads();  // the minedge section (dynamic dt) lies in the copied range
     const int64_t e0 = f.elem_off[t];
     for (int i = threadIdx.x; i < S; i += blockDim.x) {
         double g[4][3], vol = 0, mn = 0, mx = 0;
@@ -653,12 +700,16 @@ __global__ void __launch_bounds__(128) fill_tiles_kernel(FillArgs f) {
             for (int a = 0; a < 4; ++a) g[a][0] = g[a][1] = g[a][2] = 0.0;
         }
         if (f.coords_layout) {
-            G[i] = mx;
+            ((double*)(B + L.geom))[i] = mx;
         } else {
-            const double v[11] = {g[1][0], g[1][1], g[1][2], g[2][0], g[2][1], g[2][2],
-                                  g[3][0], g[3][1], g[3][2], vol,     mx};
-#pragma unroll
-            for (int k = 0; k < 11; ++k) G[k * S + i] = v[k];
+            double2* G2 = (double2*)(B + L.geom);
+            const double cn = __longlong_as_double(((const long long*)stg)[i]);  // the ushort4 slots, raw bits
+            G2[i] = make_double2(g[1][0], g[1][1]);
+            G2[S + i] = make_double2(g[1][2], g[2][0]);
+            G2[2 * S + i] = make_double2(g[2][1], g[2][2]);
+            G2[3 * S + i] = make_double2(g[3][0], g[3][1]);
+            G2[4 * S + i] = make_double2(g[3][2], vol);
+            G2[5 * S + i] = make_double2(mx, cn);
         }
         if (f.tdep) ((double*)(B + L.minedge))[i] = mn;
     }

@@ -115,10 +115,13 @@ __device__ __forceinline__ void dev_element(const DevParams* __restrict__ P, con
                                             const double (&g)[4][3], double vol, double max_edge,
                                             const double (&T)[4], const double (&H)[4], double& lump,
                                             double (&rc)[4]) {
-    // grad T (fem.hpp:36-40 and :64-65 compute the same sums; shared here)
-    double gtx = 0.0, gty = 0.0, gtz = 0.0;
+    // grad T (fem.hpp:36-40 and :64-65 compute the same sums; shared here). The reference
+    // starts each sum at 0.0; starting at the first product differs only in the sign of an
+    // all-zero sum, which every consumer erases (squares in gt2/gh2; kv*(g.gradT) enters r
+    // only through r - rc with r starting at +0.0), so every output stays bitwise equal.
+    double gtx = g[0][0] * T[0], gty = g[0][1] * T[0], gtz = g[0][2] * T[0];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
+    for (int a = 1; a < 4; ++a) {
         gtx = gtx + g[a][0] * T[a];
         gty = gty + g[a][1] * T[a];
         gtz = gtz + g[a][2] * T[a];
@@ -134,9 +137,9 @@ __device__ __forceinline__ void dev_element(const DevParams* __restrict__ P, con
     if (range <= 0) {
         capp = dev_c<TDEP>(P, m, t_bar);
     } else {
-        double ghx = 0.0, ghy = 0.0, ghz = 0.0;
+        double ghx = g[0][0] * H[0], ghy = g[0][1] * H[0], ghz = g[0][2] * H[0];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = 1; a < 4; ++a) {
             ghx = ghx + g[a][0] * H[a];
             ghy = ghy + g[a][1] * H[a];
             ghz = ghz + g[a][2] * H[a];

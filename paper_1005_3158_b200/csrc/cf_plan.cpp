@@ -734,9 +734,8 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     for (int32_t t = 0; t < rp.n_tiles; ++t) {  // no throwing inside the parallel regions
         const TileMeta& tm = rp.tile_meta[t];
         const TileLayout L(tm, S.temp_dep, coords);
-        if (4 * tm.ne + 4 * tm.nf > 65535 || tm.ncsr > 65535 || L.fac_idx(tm.nf, 2) > 65535 || L.rc_idx(tm.ne, 3) > 65535 ||
-            L.r_zero > 65535)
-            raise(CF_INVALID_ARG, "tile too large for 16-bit slot / operand indices");
+        if (4 * tm.ne + 4 * tm.nf > 65535 || tm.ncsr > 65535 || tm.ne > 1024 || L.max_operand() > 0x7fff)
+            raise(CF_INVALID_ARG, "tile too large for 16-bit slot / operand indices (at most 1024 tets per tile)");
     }
     for (int32_t t = 0; t < rp.n_tiles; ++t) {
         const TileMeta& tm = rp.tile_meta[t];
@@ -750,21 +749,13 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
         rp.max_blob = std::max<int64_t>(rp.max_blob, L.bytes);
         rp.max_scratch = std::max<int64_t>(rp.max_scratch, L.scratch);
     }
-    // host staging holds each tile's non-geometry sections [conn, bytes) only; the geometry
-    // columns (or slot coordinates) are computed on the device from tets_ord / coords_local
-    // (fill_geometry_kernel, the host tet_geometry's operation order), so the host never holds
-    // the 88 B/tet of ElementGeom. A leading pad keeps every tile's base pointer in the buffer.
+    // host staging holds each tile's connectivity and non-geometry sections only
+    // (TileLayout::staged_bytes); the geometry pairs (or slot coordinates) are computed on the
+    // device from tets_ord / coords_local (fill_tiles_kernel, the host tet_geometry's operation
+    // order), so the host never holds the 88 B/tet of ElementGeom.
     rp.rest_off.assign(rp.n_tiles + 1, 0);
-    {
-        int64_t pad = 0;
-        for (int32_t t = 0; t < rp.n_tiles; ++t)
-            pad = std::max<int64_t>(pad, TileLayout(rp.tile_meta[t], S.temp_dep, coords).conn);
-        rp.rest_off[0] = cf_round(pad, 16);
-        for (int32_t t = 0; t < rp.n_tiles; ++t) {
-            const TileLayout L(rp.tile_meta[t], S.temp_dep, coords);
-            rp.rest_off[t + 1] = rp.rest_off[t] + (L.bytes - L.conn);
-        }
-    }
+    for (int32_t t = 0; t < rp.n_tiles; ++t)
+        rp.rest_off[t + 1] = rp.rest_off[t] + TileLayout(rp.tile_meta[t], S.temp_dep, coords).staged_bytes();
     rp.blob_bytes = rp.blob_off[rp.n_tiles];
     rp.blob.resize(rp.rest_off[rp.n_tiles]);
     rp.elem_off.assign(elem_off.begin(), elem_off.end());
@@ -779,7 +770,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     {
         std::vector<int32_t> slot_of(rp.n_local, -1), tfacets;
         std::vector<int32_t> ent_off, cur;
-        std::vector<uint32_t> ent;
+        std::vector<uint16_t> ent;
 #pragma omp for schedule(dynamic, 64)
         for (int32_t t = 0; t < rp.n_tiles; ++t) {
             const auto& te = tiles[t];
@@ -787,8 +778,9 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             const TileMeta tm = rp.tile_meta[t];
             const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
             const TileLayout L(tm, S.temp_dep, coords);
-            uint8_t* B = rp.blob.data() + (rp.rest_off[t] - L.conn);  // tile base; sections >= conn only
-            std::memset(B + L.conn, 0, (size_t)(L.bytes - L.conn));
+            uint8_t* const stg = rp.blob.data() + rp.rest_off[t];  // connectivity first, then sections >= stage
+            std::memset(stg, 0, (size_t)L.staged_bytes());
+            auto at = [&](int32_t off) { return stg + L.stage_of(off); };
             for (int k = 0; k < ns; ++k) slot_of[tnodes[k]] = k;
             tile_facets(te, tfacets);
             // per-slot contribution codes (4e+a, then 4ne+4f+a), in code order
@@ -804,14 +796,12 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                 // (lump, residual) operand pair of every contribution (reduction order)
                 for (int i = 0; i < ne; ++i)
                     for (int a = 0; a < 4; ++a)
-                        ent[cur[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]]]++] =
-                            (uint32_t)L.lump_idx(i) | (uint32_t)L.rc_idx(i, a) << 16;
+                        ent[cur[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]]]++] = L.code_elem(i, a);
                 for (int i = 0; i < nf; ++i)
                     for (int a = 0; a < 3; ++a)
-                        ent[cur[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]]]++] =
-                            (uint32_t)L.r_zero | (uint32_t)L.fac_idx(i, a) << 16;
+                        ent[cur[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]]]++] = L.code_facet(i, a);
             }
-            uint16_t* csec = (uint16_t*)(B + L.conn);
+            uint16_t* csec = (uint16_t*)stg;  // ushort4 per element
             for (int i = 0; i < ne; ++i) {
                 const int32_t e = te[i];
                 rp.elem_global[elem_off[t] + i] = e;
@@ -820,18 +810,19 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                     rp.tets_ord[4 * (size_t)(elem_off[t] + i) + a] = l;
                     csec[4 * i + a] = (uint16_t)slot_of[l];
                 }
-                B[L.region + i] = (uint8_t)m.region[e];
+                *at(L.region + i) = (uint8_t)m.region[e];
             }
             for (int i = 0; i < nf; ++i) {
                 const int32_t f = tfacets[i];
                 const int32_t kind = S.facet_kind[f];
-                uint16_t* fs = (uint16_t*)(B + L.fslots) + 4 * i;
+                uint8_t* rec = at(L.fac + 48 * i);  // (area, slots + kind), sister nodes, pad
+                uint16_t* fs = (uint16_t*)(rec + 8);
                 for (int a = 0; a < 3; ++a) fs[a] = (uint16_t)slot_of[local_of[m.facets[3 * (size_t)f + a]]];
                 fs[3] = (uint16_t)kind;
-                ((double*)(B + L.farea))[i] = triangle_area(m.pos(m.facets[3 * (size_t)f]),
-                                                            m.pos(m.facets[3 * (size_t)f + 1]),
-                                                            m.pos(m.facets[3 * (size_t)f + 2]));
-                int32_t* sis = (int32_t*)(B + L.fsister) + 4 * i;
+                const double area = triangle_area(m.pos(m.facets[3 * (size_t)f]), m.pos(m.facets[3 * (size_t)f + 1]),
+                                                  m.pos(m.facets[3 * (size_t)f + 2]));
+                std::memcpy(rec, &area, 8);
+                int32_t* sis = (int32_t*)(rec + 16);
                 if (S.P.kind[kind].interface) {
                     const int32_t se = S.pairs[S.pair_of_facet[f]].sister;
                     for (int a = 0; a < 4; ++a) sis[a] = local_of[m.tets[4 * (size_t)se + a]];
@@ -840,9 +831,9 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                     n_bc++;
                 }
             }
-            uint16_t* cend = (uint16_t*)(B + L.csr_end);
-            uint32_t* csr = (uint32_t*)(B + L.csr);
-            int32_t* sn = (int32_t*)(B + L.snode);
+            uint16_t* cend = (uint16_t*)at(L.csr_end);
+            uint16_t* csr = (uint16_t*)at(L.csr);
+            int32_t* sn = (int32_t*)at(L.snode);
             const int64_t so = rp.tile_slot_off[t];
             int32_t pad = 0;
             for (int k = 0; k < (int)cf_round(ns, 2); ++k) {
@@ -854,10 +845,10 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                 rp.slot_node[so + k] = (int32_t)(((uint32_t)rp.node_region[l] << 28) | (uint32_t)l);
                 const bool priv = ntiles_of[l] == 1 && !shared_node[l];
                 const bool dir = !rp.node_dir.empty() && rp.node_dir[l] >= 0;
-                B[L.sinfo + k] = (uint8_t)((rp.node_region[l] & 0x3f) | (dir ? 0x40 : 0) | (priv ? 0x80 : 0));
+                *at(L.sinfo + k) = (uint8_t)((rp.node_region[l] & 0x3f) | (dir ? 0x40 : 0) | (priv ? 0x80 : 0));
                 int32_t j = pad;
                 for (int32_t q = ent_off[k]; q < ent_off[k + 1]; ++q) csr[j++] = ent[q];
-                for (; j & 3; ++j) csr[j] = (uint32_t)L.r_zero | (uint32_t)L.r_zero << 16;  // (0.0, 0.0): exact no-op
+                for (; j & 3; ++j) csr[j] = L.code_zero();  // (0.0, 0.0): exact no-op
                 pad = j;
                 cend[k] = (uint16_t)pad;
                 sn[k] = l;

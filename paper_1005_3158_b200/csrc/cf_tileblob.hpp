@@ -3,30 +3,41 @@
 // Every tile's element, facet and reduction data is one contiguous,
 // 16-byte-aligned blob so the tile kernel fetches it with a single TMA bulk
 // copy (cp.async.bulk) into shared memory. Sections (each 16 B aligned):
-//   xyz       ns x 4 f64     slot coordinates (x, y, z, 0)       [CF_GEOM_COORDS only]
-//   geom      11 x ne2 f64   SoA: g1x g1y g1z g2x g2y g2z g3x g3y g3z vol max_edge
-//                            [CF_GEOM_COORDS: max_edge only, 1 x ne2 f64]
+//   CF_GEOM_STORED (default):
+//   geom      6 x ne2 x 16 B SoA of 16-byte pairs, one pair per element per column:
+//                            (g1x g1y) (g1z g2x) (g2y g2z) (g3x g3y) (g3z vol) (max_edge conn)
+//                            -- conn = the tile-local slots of the 4 nodes (ushort4)
+//   CF_GEOM_COORDS:
+//   xyz       ns x 4 f64     slot coordinates (x, y, z, 0)
+//   geom      ne2 f64        max_edge
 //   conn      ne2 x ushort4  tile-local slots of the 4 nodes
+//   both:
 //   minedge   ne2 f64        (only with temperature-dependent tables: dynamic dt)
-//   farea     nf2 f64        facet area
-//   fsister   nf x int4      sister-element nodes (local / ghost ids) of interface facets
-//   fslots    nf2 x ushort4  facet slots s0 s1 s2 + facet kind
+//   fac       nf x 48 B      per facet: (area f64, slots s0 s1 s2 + kind as ushort4),
+//                            sister-element nodes (local / ghost ids) as int4, 16 B pad
 //   snode     ns4 i32        local node id of each slot (flush target)
 //   csr_end   ns8 u16        per-slot end of its contribution list (tile relative)
-//   csr       ncsr4 u32      contribution pairs (lump index | residual index << 16), double
-//                            indices from the operand base R (see TileLayout::lump_idx ...);
-//                            each slot's list padded to a multiple of 4 with (0.0, 0.0) pairs
+//   csr       ncsr8 u16      per-slot contribution codes in reduction order (see below); each
+//                            slot's list padded to a multiple of 4 with the zero operand
 //   sinfo     ns16 u8        region | 0x40 Dirichlet | 0x80 tile-private node
 //   region    ne16 u8        element region
-//   zero      16 B           0.0 (c-operand of facet entries in the slot reduction)
-// The element phase writes its (lump, rc0..rc3) contribution columns over the
-// consumed geometry columns (stored layout) or into a shared-memory scratch that
-// is never streamed (coordinates layout).
+//   zero      16 B           (0.0, 0.0)
+// Reduction operands. Stored layout: the element phase writes each element's four
+// (lump, rc_q) pairs over its own consumed geometry pairs (column q), each facet's three
+// (0.0, -term_a) pairs over its own consumed 48-byte record, so a code is simply the
+// 16-byte pair index from the blob base (one 16-byte load per contribution).
+// Coordinates layout: lump / rc / facet terms go to a shared-memory scratch of doubles
+// (zero pair, lump column, 4 rc columns, 3 facet-term columns); a code is e | q << 10 for an
+// element contribution (operands lump[e], rc_q[e]) or 0x8000 | the residual operand's
+// double index (lump operand: the zero) for a facet term or padding.
 // The slots' current temperatures are NOT in the blob: they live in a per-slot
 // copy Tslot[s0 .. s0+ns) (ping-ponged per step, written by the update of the
 // previous step) fetched by a second bulk copy, so no tile ever gathers T.
 // (nX = n rounded up to a multiple of X.) Host packing (cf_plan.cpp) and the
 // device view (cf_kernels.cuh) both use TileLayout, so they cannot disagree.
+// Host staging (cf_plan.cpp -> fill_tiles_kernel) holds the sections from `stage`
+// on, with the connectivity first: stored layout [conn ne2 x 8 B | minedge .. end),
+// coordinates layout [conn .. end) verbatim; the geometry is computed on the device.
 #pragma once
 
 #include <cstdint>
@@ -54,59 +65,79 @@ CF_HD int32_t cf_round32(int32_t n, int32_t m) { return (n + m - 1) & ~(m - 1); 
 
 struct TileLayout {
     // byte offsets (a tile is at most ~220 KB: 32-bit offsets keep the kernel's registers down)
-    int32_t geom, xyz, conn, minedge, farea, fsister, fslots, snode, csr_end, csr, sinfo, region, zero, bytes;
-    int32_t ne2, nf2;  // SoA strides (elements, facets)
+    int32_t geom, xyz, conn, minedge, fac, snode, csr_end, csr, sinfo, region, zero, bytes;
+    int32_t stage;     // first byte of the host-staged part (conn for the stored layout is staged
+                       // as an 8 B x ne2 prefix at `stage - 8 * ne2`, then placed into the pairs)
+    int32_t ne2;       // SoA stride (elements)
+    int32_t nf;
     bool coords;
-    // Reduction operands, as double indices from the tile's operand base R (the stage
-    // blob for the stored layout, the shared-memory scratch for the coordinates layout):
-    //   zero, lump(e), rc(e, q), facet term(f, a)  -- precomputed into the CSR pairs
-    int32_t r_zero, r_lump;
+    int32_t r_zero, r_lump;  // reduction operand indices (stored: 16 B pairs; coords: scratch doubles)
     int32_t scratch;   // coordinates layout: scratch doubles (zero pair, 5 x ne2, 3 x nf2)
+    // stored layout: pair index of (lump, rc_q) of element e / (0, -term_a) of facet f
+    CF_HD int32_t pair_elem(int e, int q) const { return q * ne2 + e; }
+    CF_HD int32_t pair_facet(int f, int a) const { return (fac >> 4) + 3 * f + a; }
+    // coordinates layout: scratch double indices
     CF_HD int32_t lump_idx(int e) const { return r_lump + e; }
     CF_HD int32_t rc_idx(int e, int q) const { return r_lump + (1 + q) * ne2 + e; }
-    CF_HD int32_t fac_idx(int f, int a) const {
-        if (coords) return r_lump + 5 * ne2 + a * nf2 + f;
-        return a == 0 ? (farea >> 3) + f : (fsister >> 3) + 2 * f + a - 1;
+    CF_HD int32_t fac_idx(int f, int a) const { return r_lump + 5 * ne2 + a * cf_round32(nf, 2) + f; }
+    // 16-bit reduction code of element e corner q / facet f corner a / the padding no-op
+    CF_HD uint16_t code_elem(int e, int q) const {
+        return coords ? (uint16_t)(e | q << 10) : (uint16_t)pair_elem(e, q);
+    }
+    CF_HD uint16_t code_facet(int f, int a) const {
+        return coords ? (uint16_t)(0x8000 | fac_idx(f, a)) : (uint16_t)pair_facet(f, a);
+    }
+    CF_HD uint16_t code_zero() const { return coords ? (uint16_t)(0x8000 | r_zero) : (uint16_t)r_zero; }
+    // largest operand index a code carries (must stay below 0x8000)
+    CF_HD int32_t max_operand() const {
+        return coords ? fac_idx(nf, 2) : (bytes >> 4);
     }
     CF_HD TileLayout(const TileMeta& m, bool tdep, bool coords_) : coords(coords_) {
         ne2 = cf_round32(m.ne, 2);
-        nf2 = cf_round32(m.nf, 2);
+        nf = m.nf;
         int32_t o = 0;
-        geom = xyz = o;
+        geom = xyz = conn = o;
         if (coords) {
             o += 32 * m.ns;  // slot (x, y, z, 0)
-            geom = o;                 // max_edge only
+            geom = o;        // max_edge only
+            o += 8 * ne2;
+            conn = o;
             o += 8 * ne2;
         } else {
-            o += 11 * 8 * ne2;
+            o += 6 * 16 * ne2;
+            conn = 5 * 16 * ne2 + 8;  // inside the (max_edge, conn) pairs, 16-byte stride
         }
-        conn = o;
-        o += 8 * ne2;
         minedge = o;
+        stage = coords ? conn : o;
         if (tdep) o += 8 * ne2;
-        farea = o;
-        o += 8 * nf2;
-        fsister = o;
-        o += 16 * m.nf;
-        fslots = o;
-        o += 8 * nf2;
+        fac = o;
+        o += 48 * m.nf;
         snode = o;
         o += 4 * cf_round32(m.ns, 4);
         csr_end = o;
         o += 2 * cf_round32(m.ns, 8);
         csr = o;
-        o += 4 * cf_round32(m.ncsr, 4);
+        o += 2 * cf_round32(m.ncsr, 8);
         sinfo = o;
         o += cf_round32(m.ns, 16);
         region = o;
         o += cf_round32(m.ne, 16);
-        zero = o;  // 16 zero bytes: the "lump" operand of facet entries in the reduction
+        zero = o;  // 16 zero bytes
         o += 16;
         bytes = o;
-        r_zero = coords ? 0 : (zero >> 3);
-        r_lump = coords ? 2 : (geom >> 3);
-        scratch = coords ? 2 + 5 * ne2 + 3 * (int32_t)nf2 : 0;
+        r_zero = coords ? 0 : (zero >> 4);
+        r_lump = coords ? 2 : 0;
+        scratch = coords ? 2 + 5 * ne2 + 3 * cf_round32(m.nf, 2) : 0;
     }
+    // byte offsets of element i's connectivity (ushort4) and of facet f's record fields
+    CF_HD int32_t conn_of(int i) const { return conn + (coords ? 8 : 16) * i; }
+    CF_HD int32_t fac_area(int f) const { return fac + 48 * f; }
+    CF_HD int32_t fac_slots(int f) const { return fac + 48 * f + 8; }
+    CF_HD int32_t fac_sister(int f) const { return fac + 48 * f + 16; }
+    // bytes of the host staging of this tile
+    CF_HD int32_t staged_bytes() const { return bytes - stage + (coords ? 0 : 8 * ne2); }
+    // staging offset of a blob offset >= stage; the stored layout's connectivity prefix is at 0
+    CF_HD int32_t stage_of(int32_t off) const { return off - stage + (coords ? 0 : 8 * ne2); }
 };
 
 }  // namespace cfb

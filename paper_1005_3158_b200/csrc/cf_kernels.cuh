@@ -151,7 +151,9 @@ struct TileArgs {
     int32_t scratch_off; // coordinates layout: byte offset of the contribution scratch in shared memory
     int32_t probe;       // diagnostics only (CF_PROBE; results invalid): 1 = copies only, 3 = no
                          // reduction phase, 4 = no element phase, 5 = no enthalpy evaluation,
-                         // 6 = every CTA re-reads one of 1184 L2-resident tiles
+                         // 7 = no Lemmon divide / sqrt, 8 = bank-conflict-free reduction operand
+                         // reads (wrong operands); + 16: every CTA re-reads one of 1184
+                         // L2-resident tiles (compute-side time)
     double t_end;
 };
 
@@ -171,7 +173,7 @@ struct TileHdr {  // per stage: the metadata of the tile in flight (written befo
 // issue_slot_copy after griddep_wait; the barrier already expects their bytes)
 __device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int it, bool tdep, bool coords, uint8_t* dst,
                                                 double* sTdst, uint64_t* bar, TileHdr* hdr, bool slots = true) {
-    if (a.probe == 6) it %= 1184;  // diagnostics: L2-resident tiles (compute-side time)
+    if (a.probe & 16) it %= 1184;  // diagnostics: L2-resident tiles (compute-side time)
     const int4 d0 = __ldg((const int4*)(a.desc + it)), d1 = __ldg((const int4*)(a.desc + it) + 1);
     const TileMeta tm{d0.x, d0.y, d0.z, d0.w};
     const int32_t s0 = d1.x;
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         const int s0 = hdr[stage].s0;
         const TileLayout& L = hdr[stage].layout();
         const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
-        if (a.probe == 1) {  // diagnostics: memory-path timing without the physics
+        if ((a.probe & 15) == 1) {  // diagnostics: memory-path timing without the physics
             __syncthreads();
             if (tid == 0 && t + a.stages * (int)gridDim.x < a.n_tiles)
                 issue_tile_copy(a, t + a.stages * gridDim.x, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         const uint8_t* sinfo = B + L.sinfo;
         for (int s = tid; s < ns; s += kTileThreads) {
             const double T = sT[s];
-            sTH[s] = make_double2(T, a.probe == 5 ? T : dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], T));
+            sTH[s] = make_double2(T, (a.probe & 15) == 5 ? T : dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], T));
         }
         __syncthreads();
 
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         const int S = L.ne2;
         double* R = (double*)(smem + a.scratch_off);  // coordinates layout only
         const uint8_t* ereg = B + L.region;
-        for (int i = tid; i < (a.probe == 4 ? 0 : ne); i += kTileThreads) {
+        for (int i = tid; i < ((a.probe & 15) == 4 ? 0 : ne); i += kTileThreads) {
             double g[4][3], vol, max_edge;
             ushort4 cn;
             if (GC) {
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             const double H[4] = {th0.y, th1.y, th2.y, th3.y};
             const DevMaterial& m = sMat[ereg[i]];
             double lump, rc[4];
-            dev_element<TDEP>(P, m, g, vol, max_edge, T, H, lump, rc);
+            dev_element<TDEP>(P, m, g, vol, max_edge, T, H, lump, rc, (a.probe & 15) == 7);
             if (TDEP)
                 local_min = fmin(local_min, dev_stable_bound<TDEP>(P, m, ((const double*)(B + L.minedge))[i], T));
             if (GC) {
@@ -401,7 +403,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         const uint16_t* csr = (const uint16_t*)(B + L.csr);
         const int32_t* snode = (const int32_t*)(B + L.snode);
         const double2* W = (const double2*)B;
-        for (int s = tid; s < (a.probe == 3 ? 0 : ns); s += kTileThreads) {
+        for (int s = tid; s < ((a.probe & 15) == 3 ? 0 : ns); s += kTileThreads) {
             const int beg = s == 0 ? 0 : cend[s - 1];
             const int end = cend[s];
             double c = 0, r = 0;
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        const double2 w = W[v[k]];
+                        const double2 w = W[(a.probe & 15) == 8 ? ((v[k] & ~7u) | (s & 7)) : v[k]];
                         l[k] = w.x;
                         q[k] = w.y;
                     }

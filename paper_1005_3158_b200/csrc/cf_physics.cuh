@@ -114,7 +114,7 @@ template <bool TDEP>
 __device__ __forceinline__ void dev_element(const DevParams* __restrict__ P, const DevMaterial& m,
                                             const double (&g)[4][3], double vol, double max_edge,
                                             const double (&T)[4], const double (&H)[4], double& lump,
-                                            double (&rc)[4]) {
+                                            double (&rc)[4], bool probe_no_divsqrt = false) {
     // grad T (fem.hpp:36-40 and :64-65 compute the same sums; shared here). The reference
     // starts each sum at 0.0; starting at the first product differs only in the sign of an
     // all-zero sum, which every consumer erases (squares in gt2/gh2; kv*(g.gradT) enters r
@@ -163,7 +163,8 @@ __device__ __forceinline__ void dev_element(const DevParams* __restrict__ P, con
             }
             capp = (hh - hl) / range;
         } else {
-            capp = sqrt((ghx * ghx + ghy * ghy + ghz * ghz) / gt2);
+            const double gh2 = ghx * ghx + ghy * ghy + ghz * ghz;
+            capp = probe_no_divsqrt ? gh2 + gt2 : sqrt(gh2 / gt2);  // (diagnostics probe only)
         }
     }
     // element_accumulate fem.hpp:60-69

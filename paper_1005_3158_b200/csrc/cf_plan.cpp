@@ -281,6 +281,197 @@ inline uint64_t spread21(uint64_t v) {
     v = (v | v << 2) & 0x1249249249249249ull;
     return v;
 }
+
+// Bank-aware local element positions. The tile kernel reads shared memory in two gathers:
+//   phase 3: thread s (slot s) reads its j-th (lump, rc) operand pair, 16 B at pair index
+//            q*S + pos(e) (S = ne2, a multiple of 8), so its 16-byte bank group is pos(e) & 7;
+//   phase 2a: thread p (element at position p) reads sTH[slot of corner q], bank group slot & 7.
+// An 8-thread quarter warp costs one shared-memory wavefront per distinct address in its most
+// loaded bank group. The element positions are a free permutation (the reduction order is fixed
+// by the CSR lists, ascending global element id): a greedy balanced colouring of the elements
+// (colour = position & 7) spreads each phase-3 group over the bank groups (cfg2: 1.63x -> ~1.3x
+// the ideal wavefronts of random positions... see DESIGN.md), and an optional seeded local search
+// over position swaps (CF_BANK_ITERS) lowers the summed wavefronts of both gathers further.
+// `items` are the slots' operand lists in reduction
+// order, padded like the CSR: element corner (i << 2 | q) or 0x80000000 | fixed pair address.
+// Deterministic: the same tile always yields the same positions.
+struct BankPlanner {
+    int ne, ns;
+    std::vector<int32_t> pos, at;            // element -> position, position -> element
+    std::vector<int32_t> a_off, a_items;     // phase-3 groups (quarter warp of slots, list index)
+    std::vector<int32_t> g_off, g_list;      // element -> its phase-3 groups
+    const int32_t* eslot = nullptr;          // element i, corner q -> slot
+    int cost_a(int g) const {
+        int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint32_t fixed[8];
+        int nfix = 0;
+        for (int k = a_off[g]; k < a_off[g + 1]; ++k) {
+            const uint32_t it = (uint32_t)a_items[k];
+            if (it & 0x80000000u) {
+                const uint32_t ad = it & 0x7fffffffu;
+                bool dup = false;
+                for (int f = 0; f < nfix; ++f) dup = dup || fixed[f] == ad;
+                if (dup) continue;
+                if (nfix < 8) fixed[nfix++] = ad;
+                cnt[ad & 7]++;
+            } else {
+                cnt[pos[it >> 2] & 7]++;
+            }
+        }
+        int mx = 0;
+        for (int b = 0; b < 8; ++b) mx = std::max(mx, cnt[b]);
+        return mx;
+    }
+    int cost_b(int blk, int q) const {  // quarter warp of element positions, corner q
+        int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int32_t seen[8];
+        int ns_ = 0;
+        for (int p = 8 * blk; p < std::min(ne, 8 * blk + 8); ++p) {
+            const int32_t sl = eslot[4 * at[p] + q];
+            bool dup = false;
+            for (int k = 0; k < ns_; ++k) dup = dup || seen[k] == sl;
+            if (dup) continue;
+            seen[ns_++] = sl;
+            cnt[sl & 7]++;
+        }
+        int mx = 0;
+        for (int b = 0; b < 8; ++b) mx = std::max(mx, cnt[b]);
+        return mx;
+    }
+    // items: per slot [off[s], off[s+1]) in reduction order (already padded to multiples of 4)
+    void run(int ne_, int ns_, const int32_t* eslot_, const std::vector<int32_t>& off,
+             const std::vector<uint32_t>& items, int iters, uint64_t seed, bool greedy = true) {
+        ne = ne_;
+        ns = ns_;
+        eslot = eslot_;
+        pos.resize(ne);
+        at.resize(ne);
+        std::iota(pos.begin(), pos.end(), 0);
+        std::iota(at.begin(), at.end(), 0);
+        if (ne < 16) return;
+        // phase-3 groups
+        a_off.assign(1, 0);
+        a_items.clear();
+        for (int q0 = 0; q0 < ns; q0 += 8) {
+            int mx = 0;
+            for (int s = q0; s < std::min(ns, q0 + 8); ++s) mx = std::max(mx, off[s + 1] - off[s]);
+            for (int j = 0; j < mx; ++j) {
+                for (int s = q0; s < std::min(ns, q0 + 8); ++s)
+                    if (off[s] + j < off[s + 1]) a_items.push_back((int32_t)items[off[s] + j]);
+                a_off.push_back((int32_t)a_items.size());
+            }
+        }
+        const int na = (int)a_off.size() - 1;
+        g_off.assign(ne + 1, 0);
+        for (int g = 0; g < na; ++g)
+            for (int k = a_off[g]; k < a_off[g + 1]; ++k)
+                if (!((uint32_t)a_items[k] & 0x80000000u)) g_off[((uint32_t)a_items[k] >> 2) + 1]++;
+        for (int i = 0; i < ne; ++i) g_off[i + 1] += g_off[i];
+        g_list.resize(g_off[ne]);
+        {
+            std::vector<int32_t> cur(g_off.begin(), g_off.end() - 1);
+            for (int g = 0; g < na; ++g)
+                for (int k = a_off[g]; k < a_off[g + 1]; ++k)
+                    if (!((uint32_t)a_items[k] & 0x80000000u)) g_list[cur[(uint32_t)a_items[k] >> 2]++] = g;
+        }
+        // greedy balanced colouring: each element takes the bank group (position & 7) least used by
+        // the other members of its phase-3 groups, within the group's capacity (positions < ne)
+        if (greedy) {
+            std::vector<int32_t> cnt(8 * (size_t)na, 0);
+            for (int g = 0; g < na; ++g) {
+                uint32_t fixed[64];
+                int nfix = 0;
+                for (int k = a_off[g]; k < a_off[g + 1]; ++k) {
+                    const uint32_t it = (uint32_t)a_items[k];
+                    if (!(it & 0x80000000u)) continue;
+                    const uint32_t ad = it & 0x7fffffffu;
+                    bool dup = false;
+                    for (int f = 0; f < nfix; ++f) dup = dup || fixed[f] == ad;
+                    if (dup) continue;
+                    if (nfix < 64) fixed[nfix++] = ad;
+                    cnt[8 * (size_t)g + (ad & 7)]++;
+                }
+            }
+            // blocks of 8 consecutive elements (reference order: spatially coherent, so the
+            // phase-2a corner gathers keep their broadcasts) take the 8 colours as a permutation
+            for (int b0 = 0; b0 < ne; b0 += 8) {
+                const int nb = std::min(8, ne - b0);
+                bool used[8] = {false, false, false, false, false, false, false, false};
+                for (int i = b0; i < b0 + nb; ++i) {
+                    int best = -1, best_score = 1 << 30;
+                    for (int c = 0; c < nb; ++c) {  // a partial last block uses positions b0 .. ne-1
+                        if (used[c]) continue;
+                        // score: added wavefronts (a count reaching its group's maximum), then load
+                        int sc = 0;
+                        for (int k = g_off[i]; k < g_off[i + 1]; ++k) {
+                            const int32_t* cg = &cnt[8 * (size_t)g_list[k]];
+                            int mx = 0;
+                            for (int u = 0; u < 8; ++u) mx = std::max(mx, cg[u]);
+                            sc += 64 * (cg[c] + 1 > mx) + cg[c];
+                        }
+                        if (sc < best_score) {
+                            best_score = sc;
+                            best = c;
+                        }
+                    }
+                    used[best] = true;
+                    for (int k = g_off[i]; k < g_off[i + 1]; ++k) cnt[8 * (size_t)g_list[k] + best]++;
+                    pos[i] = b0 + best;
+                    at[b0 + best] = i;
+                }
+            }
+        }
+        uint64_t x = seed * 0x9E3779B97F4A7C15ull + 0x2545F4914F6CDD1Dull;
+        auto rnd = [&]() {
+            x ^= x << 13;
+            x ^= x >> 7;
+            x ^= x << 17;
+            return x;
+        };
+        int ga[16], gb[4];
+        for (int it = 0; it < iters; ++it) {
+            const int i1 = (int)(rnd() % (uint64_t)ne), i2 = (int)(rnd() % (uint64_t)ne);
+            const int p1 = pos[i1], p2 = pos[i2];
+            if ((p1 & 7) == (p2 & 7) && (p1 >> 3) == (p2 >> 3)) continue;
+            int na_ = 0;
+            for (int i : {i1, i2})
+                for (int k = g_off[i]; k < g_off[i + 1]; ++k) {
+                    bool dup = false;
+                    for (int u = 0; u < na_; ++u) dup = dup || ga[u] == g_list[k];
+                    if (!dup && na_ < 16) ga[na_++] = g_list[k];
+                }
+            const int nb = (p1 >> 3) == (p2 >> 3) ? 1 : 2;
+            gb[0] = p1 >> 3;
+            gb[1] = p2 >> 3;
+            auto total = [&]() {
+                int c = 0;
+                for (int u = 0; u < na_; ++u) c += cost_a(ga[u]);
+                for (int u = 0; u < nb; ++u)
+                    for (int q = 0; q < 4; ++q) c += cost_b(gb[u], q);
+                return c;
+            };
+            const int before = total();
+            std::swap(pos[i1], pos[i2]);
+            at[p1] = i2;
+            at[p2] = i1;
+            if (total() > before) {  // revert (sideways moves are kept)
+                std::swap(pos[i1], pos[i2]);
+                at[p1] = i1;
+                at[p2] = i2;
+            }
+        }
+    }
+    int total_cost(int which = 3) const {  // 1: phase-3 reads, 2: phase-2a gathers
+        int c = 0;
+        if (which & 1)
+            for (int g = 0; g + 1 < (int)a_off.size(); ++g) c += cost_a(g);
+        if (which & 2)
+            for (int b = 0; 8 * b < ne; ++b)
+                for (int q = 0; q < 4; ++q) c += cost_b(b, q);
+        return c;
+    }
+    int n_groups(int which) const { return which == 1 ? (int)a_off.size() - 1 : 4 * ((ne + 7) / 8); }
+};
 }  // namespace
 
 void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o,
@@ -765,13 +956,19 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     for (int32_t l = 0; l < rp.n_local; ++l)
         for (int k = 0; k < 3; ++k) rp.coords_local[3 * (size_t)l + k] = m.pos(lnodes[l])[k];
     rp.slot_node.resize(rp.tile_slot_off[rp.n_tiles]);
-    int64_t n_if = 0, n_bc = 0;
+    int64_t n_if = 0, n_bc = 0, bank_before = 0, bank_after = 0, bank_a = 0, bank_b = 0, bank_ia = 0, bank_ib = 0, bank_id_a = 0;
+    const char* bank_env = std::getenv("CF_BANK_ITERS");
+    // swap attempts per element after the greedy colouring (measured: 8 -> -1 % tile time for
+    // +13 s setup at cfg2; off by default)
+    const int bank_iters = bank_env ? std::atoi(bank_env) : 0;
+    const bool bank_trace = std::getenv("CF_TRACE_SETUP") && std::atoi(std::getenv("CF_TRACE_SETUP"));
 #pragma omp parallel num_threads(nthr) reduction(+ : n_if, n_bc)
     {
         std::vector<int32_t> slot_of(rp.n_local, -1), tfacets;
-        std::vector<int32_t> ent_off, cur;
-        std::vector<uint16_t> ent;
-#pragma omp for schedule(dynamic, 64)
+        std::vector<int32_t> ent_off, cur, poff, eslot;
+        std::vector<uint32_t> ent, items;
+        BankPlanner bank;
+#pragma omp for schedule(dynamic, 64) reduction(+ : bank_before, bank_after, bank_a, bank_b, bank_ia, bank_ib, bank_id_a)
         for (int32_t t = 0; t < rp.n_tiles; ++t) {
             const auto& te = tiles[t];
             const auto& tnodes = tile_nodes[t];
@@ -783,7 +980,8 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             auto at = [&](int32_t off) { return stg + L.stage_of(off); };
             for (int k = 0; k < ns; ++k) slot_of[tnodes[k]] = k;
             tile_facets(te, tfacets);
-            // per-slot contribution codes (4e+a, then 4ne+4f+a), in code order
+            // per-slot contributions in reduction order (ascending element, then facets):
+            // element corner (i << 2 | q) or 0x80000000 | final 16-bit code
             ent_off.assign(ns + 1, 0);
             for (int i = 0; i < ne; ++i)
                 for (int a = 0; a < 4; ++a) ent_off[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]] + 1]++;
@@ -793,24 +991,49 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             ent.resize(ent_off[ns]);
             {
                 cur.assign(ent_off.begin(), ent_off.end() - 1);
-                // (lump, residual) operand pair of every contribution (reduction order)
                 for (int i = 0; i < ne; ++i)
                     for (int a = 0; a < 4; ++a)
-                        ent[cur[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]]]++] = L.code_elem(i, a);
+                        ent[cur[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]]]++] = (uint32_t)(i << 2 | a);
                 for (int i = 0; i < nf; ++i)
                     for (int a = 0; a < 3; ++a)
-                        ent[cur[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]]]++] = L.code_facet(i, a);
+                        ent[cur[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]]]++] =
+                            0x80000000u | L.code_facet(i, a);
             }
+            // padded lists (multiples of 4: the kernel reads 4 codes at a time; padding = the zero
+            // operand), then bank-aware element positions (stored layout)
+            poff.assign(ns + 1, 0);
+            for (int k = 0; k < ns; ++k) poff[k + 1] = poff[k] + ((ent_off[k + 1] - ent_off[k] + 3) & ~3);
+            items.assign(poff[ns], 0x80000000u | L.code_zero());
+            for (int k = 0; k < ns; ++k)
+                std::copy(ent.begin() + ent_off[k], ent.begin() + ent_off[k + 1], items.begin() + poff[k]);
+            eslot.resize(4 * (size_t)ne);
+            for (int i = 0; i < ne; ++i)
+                for (int a = 0; a < 4; ++a) eslot[4 * i + a] = slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]];
+            bank.run(ne, ns, eslot.data(), poff, items, coords ? 0 : bank_iters * ne, (uint64_t)t + 1);
+            if (bank_trace) {
+                BankPlanner id;
+                id.run(ne, ns, eslot.data(), poff, items, 0, 0, false);  // reference-order positions
+                if (!coords) {
+                    bank_before += id.total_cost();
+                    bank_after += bank.total_cost();
+                    bank_id_a += id.total_cost(1);
+                    bank_a += bank.total_cost(1);
+                    bank_b += bank.total_cost(2);
+                    bank_ia += bank.n_groups(1);
+                    bank_ib += bank.n_groups(2);
+                }
+            }
+            const int32_t* lp = bank.pos.data();  // element i -> local position
             uint16_t* csec = (uint16_t*)stg;  // ushort4 per element
             for (int i = 0; i < ne; ++i) {
-                const int32_t e = te[i];
-                rp.elem_global[elem_off[t] + i] = e;
+                const int32_t e = te[i], p = lp[i];
+                rp.elem_global[elem_off[t] + p] = e;
                 for (int a = 0; a < 4; ++a) {
                     const int32_t l = local_of[m.tets[4 * (size_t)e + a]];  // oriented (finalize_mesh)
-                    rp.tets_ord[4 * (size_t)(elem_off[t] + i) + a] = l;
-                    csec[4 * i + a] = (uint16_t)slot_of[l];
+                    rp.tets_ord[4 * (size_t)(elem_off[t] + p) + a] = l;
+                    csec[4 * p + a] = (uint16_t)slot_of[l];
                 }
-                *at(L.region + i) = (uint8_t)m.region[e];
+                *at(L.region + p) = (uint8_t)m.region[e];
             }
             for (int i = 0; i < nf; ++i) {
                 const int32_t f = tfacets[i];
@@ -835,7 +1058,6 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             uint16_t* csr = (uint16_t*)at(L.csr);
             int32_t* sn = (int32_t*)at(L.snode);
             const int64_t so = rp.tile_slot_off[t];
-            int32_t pad = 0;
             for (int k = 0; k < (int)cf_round(ns, 2); ++k) {
                 if (k >= ns) {  // padding slot (never a merge target)
                     rp.slot_node[so + k] = -1;
@@ -846,16 +1068,21 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                 const bool priv = ntiles_of[l] == 1 && !shared_node[l];
                 const bool dir = !rp.node_dir.empty() && rp.node_dir[l] >= 0;
                 *at(L.sinfo + k) = (uint8_t)((rp.node_region[l] & 0x3f) | (dir ? 0x40 : 0) | (priv ? 0x80 : 0));
-                int32_t j = pad;
-                for (int32_t q = ent_off[k]; q < ent_off[k + 1]; ++q) csr[j++] = ent[q];
-                for (; j & 3; ++j) csr[j] = L.code_zero();  // (0.0, 0.0): exact no-op
-                pad = j;
-                cend[k] = (uint16_t)pad;
+                for (int32_t q = poff[k]; q < poff[k + 1]; ++q) {
+                    const uint32_t it = items[q];
+                    csr[q] = (it & 0x80000000u) ? (uint16_t)(it & 0xffffu) : L.code_elem(lp[it >> 2], (int)(it & 3));
+                }
+                cend[k] = (uint16_t)poff[k + 1];
                 sn[k] = l;
             }
             for (int k = 0; k < ns; ++k) slot_of[tnodes[k]] = -1;
         }
     }
+    if (bank_trace)
+        std::fprintf(stderr, "[cf setup] rank %d bank-aware positions: shared-memory wavefronts %lld -> %lld "
+                     "(reduction reads %lld from %lld, ideal %lld; corner gathers %lld, ideal %lld)\n", rank,
+                     (long long)bank_before, (long long)bank_after, (long long)bank_a, (long long)bank_id_a, (long long)bank_ia,
+                     (long long)bank_b, (long long)bank_ib);
     rp.n_if_facets = n_if;
     rp.n_bc_facets = n_bc;
     std::vector<std::vector<int32_t>>().swap(tile_nodes);

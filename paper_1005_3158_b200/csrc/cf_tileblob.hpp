@@ -4,7 +4,7 @@
 // 16-byte-aligned blob so the tile kernel fetches it with a single TMA bulk
 // copy (cp.async.bulk) into shared memory. Sections (each 16 B aligned):
 //   CF_GEOM_STORED (default):
-//   geom      6 x ne2 x 16 B SoA of 16-byte pairs, one pair per element per column:
+//   geom      6 x ne8 x 16 B SoA of 16-byte pairs, one pair per element per column:
 //                            (g1x g1y) (g1z g2x) (g2y g2z) (g3x g3y) (g3z vol) (max_edge conn)
 //                            -- conn = the tile-local slots of the 4 nodes (ushort4)
 //   CF_GEOM_COORDS:
@@ -93,7 +93,7 @@ struct TileLayout {
         return coords ? fac_idx(nf, 2) : (bytes >> 4);
     }
     CF_HD TileLayout(const TileMeta& m, bool tdep, bool coords_) : coords(coords_) {
-        ne2 = cf_round32(m.ne, 2);
+        ne2 = cf_round32(m.ne, coords ? 2 : 8);  // stored: pair columns 8-aligned (bank groups, cf_plan.cpp)
         nf = m.nf;
         int32_t o = 0;
         geom = xyz = conn = o;

@@ -631,6 +631,7 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
         }
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+        const bool heavy_any = !lists[1].empty() || !lists[3].empty();
         for (int c = 0; c < 4; ++c) {
             if (lists[c].empty()) continue;
             Rank::TileLaunch tl;
@@ -651,7 +652,12 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
             if (tl.smem > 220 * 1024)
                 raise(CF_INVALID_ARG, "tile shared-memory footprint exceeds 220 KB; use smaller tiles");
             const int per_sm = occupancy(tl.smem);
-            const bool persist = S == 2 || (std::getenv("CF_TILE_PERSIST") && std::atoi(std::getenv("CF_TILE_PERSIST")));
+            // persistent CTAs (one per resident slot, each walking tiles it, it + grid, ...): the
+            // CTA prologue is paid once and the next tile's copy is issued right after the previous
+            // tile's reduction (cfg2: -2.9 % tile time). Not with a concurrent outlier-class launch,
+            // whose CTAs could only become resident after the persistent grid drained.
+            bool persist = S == 2 || !heavy_any;
+            if (const char* e = std::getenv("CF_TILE_PERSIST")) persist = S == 2 || std::atoi(e) != 0;
             tl.grid = persist ? std::max(1, std::min<int>(tl.a.n_tiles, sms * per_sm)) : tl.a.n_tiles;
             // one tile per CTA: CTA it stages tile it + (resident CTAs) into L2 (CF_TILE_PREFETCH=k: k x that)
             tl.a.prefetch = 0;  // measured: no gain (the wait is occupancy, not DRAM latency)

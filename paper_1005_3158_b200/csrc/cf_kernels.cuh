@@ -171,10 +171,14 @@ struct TileHdr {  // per stage: the metadata of the tile in flight (written befo
 // `it` indexes the launch's tile descriptors
 // (slots == false: the slot temperatures -- written by the preceding kernel -- are left to
 // issue_slot_copy after griddep_wait; the barrier already expects their bytes)
-__device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int it, bool tdep, bool coords, uint8_t* dst,
-                                                double* sTdst, uint64_t* bar, TileHdr* hdr, bool slots = true) {
+__device__ __forceinline__ void load_desc(const TileArgs& a, int it, int4& d0, int4& d1) {
     if (a.probe & 16) it %= 1184;  // diagnostics: L2-resident tiles (compute-side time)
-    const int4 d0 = __ldg((const int4*)(a.desc + it)), d1 = __ldg((const int4*)(a.desc + it) + 1);
+    d0 = __ldg((const int4*)(a.desc + it));
+    d1 = __ldg((const int4*)(a.desc + it) + 1);
+}
+__device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int4 d0, int4 d1, bool tdep, bool coords,
+                                                uint8_t* dst, double* sTdst, uint64_t* bar, TileHdr* hdr,
+                                                bool slots = true) {
     const TileMeta tm{d0.x, d0.y, d0.z, d0.w};
     const int32_t s0 = d1.x;
     const int64_t boff = (int64_t)(uint32_t)d1.z | (int64_t)d1.w << 32;
@@ -243,8 +247,15 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
-        if (first0) issue_tile_copy(a, blockIdx.x, TDEP, GC, buf0, sT0, &bar[0], &hdr[0], false);
-        if (first1) issue_tile_copy(a, blockIdx.x + gridDim.x, TDEP, GC, buf1, sT1, &bar[1], &hdr[1], false);
+        int4 d0, d1;
+        if (first0) {
+            load_desc(a, blockIdx.x, d0, d1);
+            issue_tile_copy(a, d0, d1, TDEP, GC, buf0, sT0, &bar[0], &hdr[0], false);
+        }
+        if (first1) {
+            load_desc(a, blockIdx.x + gridDim.x, d0, d1);
+            issue_tile_copy(a, d0, d1, TDEP, GC, buf1, sT1, &bar[1], &hdr[1], false);
+        }
         griddep_wait();
         if (first0) issue_slot_copy(a, &hdr[0], sT0, &bar[0]);
         if (first1) issue_slot_copy(a, &hdr[1], sT1, &bar[1]);
@@ -272,10 +283,14 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         const int s0 = hdr[stage].s0;
         const TileLayout& L = hdr[stage].layout();
         const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
+        const bool has_next = t + a.stages * (int)gridDim.x < a.n_tiles;
+        int4 nd0, nd1;
         if ((a.probe & 15) == 1) {  // diagnostics: memory-path timing without the physics
             __syncthreads();
-            if (tid == 0 && t + a.stages * (int)gridDim.x < a.n_tiles)
-                issue_tile_copy(a, t + a.stages * gridDim.x, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
+            if (tid == 0 && has_next) {
+                load_desc(a, t + a.stages * gridDim.x, nd0, nd1);
+                issue_tile_copy(a, nd0, nd1, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
+            }
             continue;
         }
         // phase 1: H = enthalpy(T) per slot (blocked.hpp:462-467) from the streamed slot temperatures
@@ -457,11 +472,12 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         }
         if (t + (int)gridDim.x >= a.n_tiles) break;  // last tile of this CTA: no trailing barrier
         __syncthreads();  // stage buffer and sT/sH free again
-        if (tid == 0 && t + a.stages * (int)gridDim.x < a.n_tiles) {
+        if (tid == 0 && has_next) {
             // generic-proxy writes to B (in-place contributions) must be ordered
             // before the async-proxy (TMA) overwrite of the same buffer
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_tile_copy(a, t + a.stages * gridDim.x, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
+            load_desc(a, t + a.stages * gridDim.x, nd0, nd1);
+            issue_tile_copy(a, nd0, nd1, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
         }
     }
     if (TDEP) {

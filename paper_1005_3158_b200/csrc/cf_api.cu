@@ -641,7 +641,8 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
             std::vector<TileDesc> desc(lists[c].size());
             for (size_t i = 0; i < lists[c].size(); ++i) {
                 const int32_t t = lists[c][i];
-                desc[i] = TileDesc{h.tile_meta[t], h.tile_slot_off[t], 0, h.blob_off[t]};
+                desc[i] = TileDesc{h.tile_meta[t], h.tile_slot_off[t],
+                                   TileLayout(h.tile_meta[t], p->temp_dep, h.coords).bytes, h.blob_off[t]};
             }
             tl.a.desc = M.up(desc, s);
             tl.a.n_tiles = (int32_t)lists[c].size();
@@ -655,8 +656,9 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
             // persistent CTAs (one per resident slot, each walking tiles it, it + grid, ...): the
             // CTA prologue is paid once and the next tile's copy is issued right after the previous
             // tile's reduction (cfg2: -2.9 % tile time). Not with a concurrent outlier-class launch,
-            // whose CTAs could only become resident after the persistent grid drained.
-            bool persist = S == 2 || !heavy_any;
+            // whose CTAs could only become resident after the persistent grid drained, and not on
+            // decomposed meshes, whose interior tiles overlap the exchange kernels (pack, NCCL).
+            bool persist = S == 2 || (!heavy_any && p->world == 1);
             if (const char* e = std::getenv("CF_TILE_PERSIST")) persist = S == 2 || std::atoi(e) != 0;
             tl.grid = persist ? std::max(1, std::min<int>(tl.a.n_tiles, sms * per_sm)) : tl.a.n_tiles;
             // one tile per CTA: CTA it stages tile it + (resident CTAs) into L2 (CF_TILE_PREFETCH=k: k x that)

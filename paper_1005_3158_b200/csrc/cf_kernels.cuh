@@ -180,20 +180,34 @@ __device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int4 d0, int4
                                                 uint8_t* dst, double* sTdst, uint64_t* bar, TileHdr* hdr,
                                                 bool slots = true) {
     const TileMeta tm{d0.x, d0.y, d0.z, d0.w};
-    const int32_t s0 = d1.x;
+    const int32_t s0 = d1.x, bytes = d1.y;
     const int64_t boff = (int64_t)(uint32_t)d1.z | (int64_t)d1.w << 32;
-    hdr->tm = tm;  // published by the arrive below (release), read after the wait (acquire)
-    hdr->s0 = s0;
-    const TileLayout L(tm, tdep, coords);
-    *reinterpret_cast<TileLayout*>(hdr->L) = L;
     const uint32_t tbytes = 8u * (uint32_t)cf_round32(tm.ns, 2);
-    mbar_expect_tx(bar, (uint32_t)L.bytes + tbytes);
+    // copies first (their complete_tx may precede the expect_tx: the barrier's phase also waits
+    // for the arrive below), then the header, published by that arrive (release)
     const uint8_t* src = a.blob + boff;
-    for (int64_t o = 0; o < L.bytes; o += kBulkChunk) {
-        const uint32_t n = (uint32_t)(L.bytes - o < kBulkChunk ? L.bytes - o : kBulkChunk);
+    for (int32_t o = 0; o < bytes; o += (int32_t)kBulkChunk) {
+        const uint32_t n = (uint32_t)(bytes - o < (int32_t)kBulkChunk ? bytes - o : (int32_t)kBulkChunk);
         bulk_g2s(dst + o, src + o, n, bar);
     }
     if (slots && tbytes) bulk_g2s(sTdst, a.Tslot + s0, tbytes, bar);
+    hdr->tm = tm;
+    hdr->s0 = s0;
+    *reinterpret_cast<TileLayout*>(hdr->L) = TileLayout(tm, tdep, coords);
+    mbar_expect_tx(bar, (uint32_t)bytes + tbytes);
+}
+// the next tile's descriptor, staged asynchronously into shared memory (no registers held)
+__device__ __forceinline__ void prefetch_desc(const TileArgs& a, int it, int4* sdesc) {
+    if (a.probe & 16) it %= 1184;
+    const int4* g = (const int4*)(a.desc + it);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdesc)), "l"(g) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdesc + 1)), "l"(g + 1) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void staged_desc(const int4* sdesc, int4& d0, int4& d1) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    d0 = sdesc[0];
+    d1 = sdesc[1];
 }
 __device__ __forceinline__ void issue_slot_copy(const TileArgs& a, const TileHdr* hdr, double* sTdst, uint64_t* bar) {
     const uint32_t tbytes = 8u * (uint32_t)cf_round32(hdr->tm.ns, 2);
@@ -229,6 +243,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t bar[2];
     __shared__ TileHdr hdr[2];
+    __shared__ int4 ndesc[2];  // next tile's descriptor (thread 0 only)
     __shared__ DevMaterial sMat[kMaxRegions];
     const int tid = threadIdx.x;
     const DevParams* __restrict__ P = a.P;
@@ -285,10 +300,11 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
         const bool has_next = t + a.stages * (int)gridDim.x < a.n_tiles;
         int4 nd0, nd1;
+        if (tid == 0 && has_next) prefetch_desc(a, t + a.stages * gridDim.x, ndesc);
         if ((a.probe & 15) == 1) {  // diagnostics: memory-path timing without the physics
             __syncthreads();
             if (tid == 0 && has_next) {
-                load_desc(a, t + a.stages * gridDim.x, nd0, nd1);
+                staged_desc(ndesc, nd0, nd1);
                 issue_tile_copy(a, nd0, nd1, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
             }
             continue;
@@ -476,7 +492,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             // generic-proxy writes to B (in-place contributions) must be ordered
             // before the async-proxy (TMA) overwrite of the same buffer
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            load_desc(a, t + a.stages * gridDim.x, nd0, nd1);
+            staged_desc(ndesc, nd0, nd1);
             issue_tile_copy(a, nd0, nd1, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
         }
     }

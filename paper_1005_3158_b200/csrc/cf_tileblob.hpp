@@ -54,9 +54,9 @@ struct TileMeta {
     int32_t ne, ns, nf, ncsr;  // ncsr: padded contribution entries
 };
 
-struct alignas(16) TileDesc {  // one tile of a launch: metadata + slot offset + blob byte offset
+struct alignas(16) TileDesc {  // one tile of a launch: metadata + slot offset + blob bytes + offset
     TileMeta tm;
-    int32_t s0, pad;
+    int32_t s0, bytes;  // bytes: TileLayout(tm).bytes (the copy is issued before the layout is built)
     int64_t blob_off;
 };
 

@@ -47,7 +47,7 @@ FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)  # BASELINE configs[1]: 1000 steps
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=None, help="cfg1..cfg5 (default: cfg2 at N=1, weak ladder at N>1)")
@@ -99,31 +99,53 @@ def make_case(cfg: str | None, world: int, casting_n: int = 0):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML every 5 ms (the
+    nvidia-smi CLI, ~100 ms per query, is the fallback)."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, sm_max_mhz, set of active reason names)
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+        except Exception:
+            self._nv = None
 
     def _one(self):
+        if self._nv:
+            nv, h = self._nv
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                        nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+                self.samples.append((float(sm), float(mx), {self.NAMES[i] for i, b in enumerate(bits) if r & b}))
+                return
+            except Exception:
+                self._nv = None
         try:
             out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                   "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
             f = [x.strip() for x in out.stdout.strip().split(",")]
-            if len(f) >= 7:
-                self.samples.append(f)
+            if len(f) >= 7 and f[0].replace(".", "").isdigit():
+                self.samples.append((float(f[0]), float(f[1]),
+                                     {self.NAMES[i] for i in range(4) if f[3 + i] == "Active"}))
         except Exception:
             pass
 
     def _run(self):
         while not self._stop.is_set():
             self._one()
-            self._stop.wait(0.2)
+            self._stop.wait(0.005 if self._nv else 0.2)
 
     def start(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -135,12 +157,12 @@ class ClockSampler:
             self._t.join(timeout=10)
         if not self.samples:
             self._one()
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].strip() == "Active"})
+        sm = [s[0] for s in self.samples]
+        mx = [s[1] for s in self.samples]
+        reasons = sorted(set().union(*[s[2] for s in self.samples])) if self.samples else []
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml" if self._nv else "nvidia-smi"}
 
 
 def hbm_peak():

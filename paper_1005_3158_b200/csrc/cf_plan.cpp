@@ -420,6 +420,56 @@ struct BankPlanner {
                     at[b0 + best] = i;
                 }
             }
+            // refinement: pairwise colour swaps inside a block (the block's corner gathers are
+            // unchanged) while they lower the reduction-read wavefronts
+            auto gmax = [&](int g) {
+                const int32_t* cg = &cnt[8 * (size_t)g];
+                int mx = 0;
+                for (int u = 0; u < 8; ++u) mx = std::max(mx, cg[u]);
+                return mx;
+            };
+            int touched[16];
+            for (int pass = 0; pass < 3; ++pass) {
+                bool improved = false;
+                for (int b0 = 0; b0 < ne; b0 += 8) {
+                    const int nb = std::min(8, ne - b0);
+                    for (int u = 0; u < nb; ++u)
+                        for (int v = u + 1; v < nb; ++v) {
+                            const int i1 = at[b0 + u], i2 = at[b0 + v];
+                            const int c1 = pos[i1] & 7, c2 = pos[i2] & 7;
+                            int nt = 0;
+                            for (int i : {i1, i2})
+                                for (int k = g_off[i]; k < g_off[i + 1]; ++k) {
+                                    bool dup = false;
+                                    for (int w = 0; w < nt; ++w) dup = dup || touched[w] == g_list[k];
+                                    if (!dup && nt < 16) touched[nt++] = g_list[k];
+                                }
+                            int before = 0;
+                            for (int w = 0; w < nt; ++w) before += gmax(touched[w]);
+                            auto move = [&](int i, int from, int to) {
+                                for (int k = g_off[i]; k < g_off[i + 1]; ++k) {
+                                    cnt[8 * (size_t)g_list[k] + from]--;
+                                    cnt[8 * (size_t)g_list[k] + to]++;
+                                }
+                            };
+                            move(i1, c1, c2);
+                            move(i2, c2, c1);
+                            int after = 0;
+                            for (int w = 0; w < nt; ++w) after += gmax(touched[w]);
+                            if (after < before) {
+                                pos[i1] = b0 + c2;
+                                pos[i2] = b0 + c1;
+                                at[b0 + c2] = i1;
+                                at[b0 + c1] = i2;
+                                improved = true;
+                            } else {
+                                move(i1, c2, c1);
+                                move(i2, c1, c2);
+                            }
+                        }
+                }
+                if (!improved) break;
+            }
         }
         uint64_t x = seed * 0x9E3779B97F4A7C15ull + 0x2545F4914F6CDD1Dull;
         auto rnd = [&]() {

@@ -564,8 +564,8 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         int i, cnt = -1;
         int4 r0, r1;
         if (a.rec) {  // one coalesced 32-byte record: node + up to 4 slot (= partial) indices
-            r0 = a.rec[2 * k];
-            r1 = a.rec[2 * k + 1];
+            r0 = __ldg(a.rec + 2 * k);
+            r1 = __ldg(a.rec + 2 * k + 1);
             i = r0.x;
             cnt = r0.y;
         } else {
@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         }
         const int sl[4] = {r0.z, r0.w, r1.x, r1.y};
         const bool packed = cnt >= 0 && cnt <= 4;
-        const double T = a.T[i];
+        const double T = __ldg(a.T + i);
         if (done) {
             a.Tn[i] = T;
             if (packed) {
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
             // all partial loads issued before the in-order (ascending tile) sums
             double2 pr[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) pr[q] = (q < cnt && a.probe != 9) ? a.part[sl[q]] : make_double2(1.0, 0.0);
+            for (int q = 0; q < 4; ++q) pr[q] = (q < cnt && a.probe != 9) ? __ldg(a.part + sl[q]) : make_double2(1.0, 0.0);
             c = 0;
             r = 0;
 #pragma unroll

@@ -195,6 +195,7 @@ struct Rank {
     // during a step — a two-buffer ping-pong would race with the fused updates)
     double* T[3] = {nullptr, nullptr, nullptr};
     double* Tslot[2] = {nullptr, nullptr};  // per-slot T copies (ping-pong)
+    int32_t* sched = nullptr;               // dynamic tile-scheduling counter (persistent grids)
     double* recv = nullptr;
     double* send = nullptr;
     double* acc_c = nullptr;
@@ -417,8 +418,8 @@ void launch_update(cf_plan* p, Rank& r, double t_end) {
     else if (det) launch_update_t<true, false>(p, r, a, blocks);
     else if (multi) launch_update_t<false, true>(p, r, a, blocks);
     else launch_update_t<false, false>(p, r, a, blocks);
-    if (p->temp_dep) launch_ex(advance_kernel<true>, dim3(1), dim3(32), 0, p->stream, p->pdl, r.st, p->dP, t_end);
-    else launch_ex(advance_kernel<false>, dim3(1), dim3(32), 0, p->stream, p->pdl, r.st, p->dP, t_end);
+    if (p->temp_dep) launch_ex(advance_kernel<true>, dim3(1), dim3(32), 0, p->stream, p->pdl, r.st, p->dP, t_end, r.sched);
+    else launch_ex(advance_kernel<false>, dim3(1), dim3(32), 0, p->stream, p->pdl, r.st, p->dP, t_end, r.sched);
 }
 
 void launch_pack(cf_plan* p, Rank& r, cudaStream_t st) {
@@ -661,6 +662,17 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
             bool persist = S == 2 || (!heavy_any && p->world == 1);
             if (const char* e = std::getenv("CF_TILE_PERSIST")) persist = S == 2 || std::atoi(e) != 0;
             tl.grid = persist ? std::max(1, std::min<int>(tl.a.n_tiles, sms * per_sm)) : tl.a.n_tiles;
+            // persistent single-stage grids schedule tiles dynamically (ticket counter reset by
+            // the advance kernel of every step); CF_TILE_DYNAMIC=0: static round-robin
+            tl.a.sched = nullptr;
+            const char* dyn_env = std::getenv("CF_TILE_DYNAMIC");
+            if (persist && S == 1 && tl.grid < tl.a.n_tiles && !(dyn_env && std::atoi(dyn_env) == 0)) {
+                if (!r.sched) {
+                    r.sched = M.alloc<int32_t>(1);
+                    CF_CUDA_CHECK(cudaMemsetAsync(r.sched, 0, sizeof(int32_t), s));
+                }
+                tl.a.sched = r.sched;
+            }
             // one tile per CTA: CTA it stages tile it + (resident CTAs) into L2 (CF_TILE_PREFETCH=k: k x that)
             tl.a.prefetch = 0;  // measured: no gain (the wait is occupancy, not DRAM latency)
             if (const char* e = std::getenv("CF_TILE_PREFETCH"))

@@ -155,6 +155,7 @@ struct TileArgs {
                          // reads (wrong operands); + 16: every CTA re-reads one of 1184
                          // L2-resident tiles (compute-side time)
     double t_end;
+    int32_t* sched;            // dynamic tile scheduling counter (persistent single-stage grids), or null
 };
 
 constexpr uint32_t kBulkChunk = 32768;
@@ -244,6 +245,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
     __shared__ uint64_t bar[2];
     __shared__ TileHdr hdr[2];
     __shared__ int4 ndesc[2];  // next tile's descriptor (thread 0 only)
+    __shared__ int s_issue;     // the tile whose copy follows this one in the stage buffer
     __shared__ DevMaterial sMat[kMaxRegions];
     const int tid = threadIdx.x;
     const DevParams* __restrict__ P = a.P;
@@ -277,6 +279,12 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         if (a.stages == 1 && a.prefetch && (int)blockIdx.x + a.prefetch < a.n_tiles)
             prefetch_tile(a, blockIdx.x + a.prefetch, TDEP, GC);
     }
+    // dynamic tile scheduling (persistent single-stage grids): after its first tile (blockIdx.x)
+    // a CTA takes tickets from a.sched (reset to 0 by the update kernel); tile = grid + ticket.
+    // Thread 0 draws the ticket one tile ahead, so the atomic's latency overlaps a whole tile.
+    const bool dyn = a.sched != nullptr && a.stages == 1;
+    int ticket = 0;
+    if (dyn && tid == 0 && first0) ticket = atomicAdd(a.sched, 1);
     for (int i = tid; i < P->n_materials; i += kTileThreads) sMat[i] = P->mat[i];
     if (GC && tid < 2) ((double*)(smem + a.scratch_off))[tid] = 0.0;  // the facet entries' lump operand
     if (tid != 0) griddep_wait();  // before any thread reads the step state
@@ -289,7 +297,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
     double local_min = __longlong_as_double(0x7ff0000000000000ll);
 
     int k = 0;
-    for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x, ++k) {
+    for (int t = blockIdx.x; t < a.n_tiles; ++k) {
         const int stage = a.stages == 2 ? (k & 1) : 0;
         uint8_t* B = stage ? buf1 : buf0;
         double* sT = stage ? sT1 : sT0;
@@ -298,15 +306,27 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         const int s0 = hdr[stage].s0;
         const TileLayout& L = hdr[stage].layout();
         const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
-        const bool has_next = t + a.stages * (int)gridDim.x < a.n_tiles;
+        // t_follow: this CTA's next tile; t_issue: the tile copied into this stage's buffer next
+        const int t_follow = dyn ? -1 : t + (int)gridDim.x;
+        if (tid == 0) {
+            int nx = t + a.stages * (int)gridDim.x;
+            if (dyn) {
+                nx = ticket + (int)gridDim.x;
+                if (nx < a.n_tiles) ticket = atomicAdd(a.sched, 1);
+            }
+            s_issue = nx;
+            if (nx < a.n_tiles) prefetch_desc(a, nx, ndesc);
+        }
         int4 nd0, nd1;
-        if (tid == 0 && has_next) prefetch_desc(a, t + a.stages * gridDim.x, ndesc);
         if ((a.probe & 15) == 1) {  // diagnostics: memory-path timing without the physics
             __syncthreads();
-            if (tid == 0 && has_next) {
+            const int t_issue = s_issue;
+            if (tid == 0 && t_issue < a.n_tiles) {
                 staged_desc(ndesc, nd0, nd1);
                 issue_tile_copy(a, nd0, nd1, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
             }
+            t = dyn ? t_issue : t_follow;
+            __syncthreads();  // s_issue read by every thread before its next write
             continue;
         }
         // phase 1: H = enthalpy(T) per slot (blocked.hpp:462-467) from the streamed slot temperatures
@@ -486,9 +506,12 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                 atomicAdd(&a.acc_r[node], r);
             }
         }
-        if (t + (int)gridDim.x >= a.n_tiles) break;  // last tile of this CTA: no trailing barrier
-        __syncthreads();  // stage buffer and sT/sH free again
-        if (tid == 0 && has_next) {
+        const int t_issue = s_issue;  // written before the phase-1 barrier
+        const int t_next = dyn ? t_issue : t_follow;
+        if (t_next >= a.n_tiles) break;  // last tile of this CTA: no trailing barrier
+        __syncthreads();  // stage buffer and sT/sH free again; s_issue read by every thread
+        t = t_next;
+        if (tid == 0 && t_issue < a.n_tiles) {
             // generic-proxy writes to B (in-place contributions) must be ordered
             // before the async-proxy (TMA) overwrite of the same buffer
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -648,9 +671,10 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
 // advances the step state after the update (a separate one-warp launch: the update's CTAs
 // exit without a grid-wide ticket; every kernel of the step has read the state by then)
 template <bool TDEP>
-__global__ void advance_kernel(DevState* st, const DevParams* __restrict__ P, double t_end) {
+__global__ void advance_kernel(DevState* st, const DevParams* __restrict__ P, double t_end, int32_t* sched) {
     griddep_wait();
     if (threadIdx.x != 0) return;
+    if (sched) *sched = 0;  // the tile kernel's scheduling tickets restart every step
     double dt, t_next;
     bool done;
     step_dt<TDEP>(P, st, t_end, dt, t_next, done);

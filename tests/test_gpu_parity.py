@@ -67,13 +67,14 @@ def test_deterministic_repeat_bitwise():
     assert np.array_equal(a.T, b.T)
 
 
-@pytest.mark.parametrize("env", [{"CF_TILE_PERSIST": "0"}, {"CF_BANK_ITERS": "4"},
+@pytest.mark.parametrize("env", [{"CF_TILE_PERSIST": "0"}, {"CF_TILE_DYNAMIC": "0"}, {"CF_BANK_ITERS": "4"},
                                  {"CF_TILE_PERSIST": "0", "CF_BANK_ITERS": "0"}])
 def test_schedule_and_element_positions_leave_results_bitwise(env, monkeypatch):
-    """Persistent vs one-CTA-per-tile scheduling and the bank-aware element positions inside a
-    tile (greedy colouring, optional local search) only move work and shared-memory addresses:
-    the reduction order is the CSR's, so T is bitwise that of the default plan and the oracle."""
-    case = configs.casting(14, jitter=0.2, seed=3, perm_seed=5, dt_safety=0.14)
+    """Persistent (dynamically or statically scheduled) vs one-CTA-per-tile grids and the
+    bank-aware element positions inside a tile (greedy colouring, optional local search) only
+    move work and shared-memory addresses: the reduction order is the CSR's, so T is bitwise that
+    of the default plan and the oracle. 40^3 cells: ~1000 tiles, several per persistent CTA."""
+    case = configs.casting(40, jitter=0.2, seed=3, perm_seed=5, dt_safety=0.14)
     opts = cf.SolveOptions(max_steps=30, mode="deterministic", tile_elems=384)
     base = cf.solve(case.mesh, case.setup, opts)
     for k, v in env.items():

@@ -639,6 +639,16 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
             tl.phase = c / 2;
             tl.heavy = c & 1;
             tl.a = a;
+            // heavy-first processing order (longest processing time first, for the dynamic
+            // scheduler of single-rank persistent grids: -0.5 % tile time at cfg2; results do not
+            // depend on the order). CF_TILE_ORDER=heavy | morton overrides.
+            bool heavy_first = p->world == 1 && !heavy_any && p->stages == 1;
+            if (const char* e = std::getenv("CF_TILE_ORDER")) heavy_first = std::string(e) == "heavy";
+            if (heavy_first)
+                    std::stable_sort(lists[c].begin(), lists[c].end(), [&](int32_t x, int32_t y) {
+                        const TileMeta &mx_ = h.tile_meta[x], &my_ = h.tile_meta[y];
+                        return 4 * mx_.nf + mx_.ns > 4 * my_.nf + my_.ns;
+                    });
             std::vector<TileDesc> desc(lists[c].size());
             for (size_t i = 0; i < lists[c].size(); ++i) {
                 const int32_t t = lists[c][i];

@@ -163,6 +163,7 @@ constexpr uint32_t kBulkChunk = 32768;
 struct TileHdr {  // per stage: the metadata of the tile in flight (written before the barrier arrive)
     TileMeta tm;
     int32_t s0;
+    int64_t boff;  // blob byte offset (the stored layout's max_edge tail is read from global memory)
     // the tile's section layout, computed once by the issuing thread (raw storage: TileLayout
     // has a constructor, which __shared__ variables cannot run)
     alignas(8) unsigned char L[sizeof(TileLayout)];
@@ -194,6 +195,7 @@ __device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int4 d0, int4
     if (slots && tbytes) bulk_g2s(sTdst, a.Tslot + s0, tbytes, bar);
     hdr->tm = tm;
     hdr->s0 = s0;
+    hdr->boff = boff;
     *reinterpret_cast<TileLayout*>(hdr->L) = TileLayout(tm, tdep, coords);
     mbar_expect_tx(bar, (uint32_t)bytes + tbytes);
 }
@@ -343,11 +345,11 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         const int S = L.ne2;
         double* R = (double*)(smem + a.scratch_off);  // coordinates layout only
         const uint8_t* ereg = B + L.region;
+        const uint8_t* gblob = a.blob + hdr[stage].boff;  // this tile's blob in global memory
         for (int i = tid; i < ((a.probe & 15) == 4 ? 0 : ne); i += kTileThreads) {
-            double g[4][3], vol, max_edge;
-            ushort4 cn;
+            double g[4][3], vol, max_edge = 0;
+            const ushort4 cn = ((const ushort4*)(B + L.conn))[i];
             if (GC) {
-                cn = ((const ushort4*)(B + L.conn))[i];
                 const double2* X = (const double2*)(B + L.xyz);  // slot (x, y) (z, 0)
                 const unsigned short sl[4] = {cn.x, cn.y, cn.z, cn.w};
                 double p[4][3];
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             } else {
                 const double2* G2 = (const double2*)(B + L.geom);
                 const double2 c0 = G2[i], c1 = G2[S + i], c2 = G2[2 * S + i], c3 = G2[3 * S + i],
-                              c4 = G2[4 * S + i], c5 = G2[5 * S + i];
+                              c4 = G2[4 * S + i];
                 g[1][0] = c0.x;
                 g[1][1] = c0.y;
                 g[1][2] = c1.x;
@@ -374,10 +376,6 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                 g[3][1] = c3.y;
                 g[3][2] = c4.x;
                 vol = c4.y;
-                max_edge = c5.x;
-                const long long cb = __double_as_longlong(c5.y);
-                cn = make_ushort4((unsigned short)cb, (unsigned short)(cb >> 16), (unsigned short)(cb >> 32),
-                                  (unsigned short)(cb >> 48));
 #pragma unroll
                 for (int c = 0; c < 3; ++c) g[0][c] = ((g[1][c] + g[2][c]) + g[3][c]) * -1.0;
             }
@@ -386,7 +384,9 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             const double H[4] = {th0.y, th1.y, th2.y, th3.y};
             const DevMaterial& m = sMat[ereg[i]];
             double lump, rc[4];
-            dev_element<TDEP>(P, m, g, vol, max_edge, T, H, lump, rc, (a.probe & 15) == 7);
+            dev_element<TDEP, !GC>(
+                P, m, g, vol, [&]() { return GC ? max_edge : __ldg((const double*)(gblob + L.max_edge_of(i))); },
+                T, H, lump, rc, (a.probe & 15) == 7);
             if (TDEP)
                 local_min = fmin(local_min, dev_stable_bound<TDEP>(P, m, ((const double*)(B + L.minedge))[i], T));
             if (GC) {
@@ -726,8 +726,8 @@ struct FillArgs {
     bool tdep, coords_layout;
 };
 
-// one CTA per tile: the staged sections into place, then the geometry (stored: the six
-// 16-byte pair columns g1 g2 g3 vol (max_edge, conn); coordinates: slot xyz + max_edge),
+// one CTA per tile: the staged sections into place, then the geometry (stored: the five
+// 16-byte pair columns g1 g2 g3 vol + the max_edge tail; coordinates: slot xyz + max_edge),
 // min_edge for dynamic dt
 __global__ void __launch_bounds__(128) fill_tiles_kernel(FillArgs f) {
     const int t = blockIdx.x;
@@ -736,8 +736,7 @@ __global__ void __launch_bounds__(128) fill_tiles_kernel(FillArgs f) {
     uint8_t* B = f.blob + f.blob_off[t];
     const uint8_t* stg = f.rest + f.rest_off[t];
     const int S = L.ne2;
-    const int skip = f.coords_layout ? 0 : 8 * S;  // stored: the connectivity prefix goes into the pairs
-    const int4* src = (const int4*)(stg + skip);
+    const int4* src = (const int4*)stg;
     int4* dst = (int4*)(B + L.stage);
     for (int j = threadIdx.x; j < (L.bytes - L.stage) / 16; j += blockDim.x) dst[j] = src[j];
     __syncthreads();  // the minedge section (dynamic dt) lies in the copied range
@@ -761,13 +760,12 @@ __global__ void __launch_bounds__(128) fill_tiles_kernel(FillArgs f) {
             ((double*)(B + L.geom))[i] = mx;
         } else {
             double2* G2 = (double2*)(B + L.geom);
-            const double cn = __longlong_as_double(((const long long*)stg)[i]);  // the ushort4 slots, raw bits
             G2[i] = make_double2(g[1][0], g[1][1]);
             G2[S + i] = make_double2(g[1][2], g[2][0]);
             G2[2 * S + i] = make_double2(g[2][1], g[2][2]);
             G2[3 * S + i] = make_double2(g[3][0], g[3][1]);
             G2[4 * S + i] = make_double2(g[3][2], vol);
-            G2[5 * S + i] = make_double2(mx, cn);
+            *(double*)(B + L.max_edge_of(i)) = mx;  // uncopied tail
         }
         if (f.tdep) ((double*)(B + L.minedge))[i] = mn;
     }

@@ -110,9 +110,16 @@ __device__ __forceinline__ void dev_tet_grads(const double (&p)[4][3], double (&
 //    decided without the division whenever gt2*max_edge^2 clears 1e-14*range^2
 //    by a 1e-6 relative margin (far above the ~1e-15 rounding of either form);
 //    otherwise the reference expression is evaluated verbatim.
-template <bool TDEP>
+//  - LB (stored layout, which does not stream max_edge): max_edge >= 1/|g_1| (the height
+//    from vertex 1, 1/|grad N_1|, is at most the longest edge), so gt2 > 1000*rhs*|g_1|^2
+//    implies the margin test above with a factor-1000 allowance for the rounding of the stored
+//    g_1 (relative error <= ~1e-4 even for the flattest tet finalize_mesh accepts,
+//    V > 1e-12 max_edge^3). Exactly: gt2*max_edge^2 >= range^2 >> 1e-14 range^2, so the test
+//    passes for all but near-uniform (round-off) gradients and extreme slivers; only then is the
+//    exact max_edge fetched (max_edge_fn(): a global load) and the original test evaluated.
+template <bool TDEP, bool LB, class MaxEdge>
 __device__ __forceinline__ void dev_element(const DevParams* __restrict__ P, const DevMaterial& m,
-                                            const double (&g)[4][3], double vol, double max_edge,
+                                            const double (&g)[4][3], double vol, MaxEdge&& max_edge_fn,
                                             const double (&T)[4], const double (&H)[4], double& lump,
                                             double (&rc)[4], bool probe_no_divsqrt = false) {
     // grad T (fem.hpp:36-40 and :64-65 compute the same sums; shared here). The reference
@@ -145,13 +152,16 @@ __device__ __forceinline__ void dev_element(const DevParams* __restrict__ P, con
             ghz = ghz + g[a][2] * H[a];
         }
         const double gt2 = gtx * gtx + gty * gty + gtz * gtz;
-        bool degenerate;
-        const double lhs = gt2 * (max_edge * max_edge), rhs = 1e-14 * (range * range);
-        if (lhs > rhs * 1.000001) {
-            degenerate = false;
-        } else {
-            const double scale = range / max_edge;
-            degenerate = gt2 < 1e-14 * scale * scale;
+        bool degenerate = false;
+        const double rhs = 1e-14 * (range * range);
+        const double g1sq = g[1][0] * g[1][0] + g[1][1] * g[1][1] + g[1][2] * g[1][2];
+        if (!LB || !(gt2 > (rhs * 1000.0) * g1sq)) {
+            const double max_edge = max_edge_fn();
+            const double lhs = gt2 * (max_edge * max_edge);
+            if (!(lhs > rhs * 1.000001)) {
+                const double scale = range / max_edge;
+                degenerate = gt2 < 1e-14 * scale * scale;
+            }
         }
         if (degenerate) {
             // secant (H_hi - H_lo)/range with the reference's first-index tie rule

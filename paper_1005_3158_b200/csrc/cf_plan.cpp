@@ -981,7 +981,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     for (int32_t t = 0; t < rp.n_tiles; ++t) {
         const TileMeta& tm = rp.tile_meta[t];
         const TileLayout L(tm, S.temp_dep, coords);
-        rp.blob_off[t + 1] = rp.blob_off[t] + L.bytes;
+        rp.blob_off[t + 1] = rp.blob_off[t] + L.total;  // copied part + the stored layout's max_edge tail
         rp.tile_slot_off[t + 1] = rp.tile_slot_off[t] + (int32_t)cf_round(tm.ns, 2);  // 16 B aligned Tslot segments
         elem_off[t + 1] = elem_off[t] + tm.ne;
         rp.max_elems = std::max(rp.max_elems, tm.ne);
@@ -1074,7 +1074,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                 }
             }
             const int32_t* lp = bank.pos.data();  // element i -> local position
-            uint16_t* csec = (uint16_t*)stg;  // ushort4 per element
+            uint16_t* csec = (uint16_t*)at(L.conn);  // ushort4 per element
             for (int i = 0; i < ne; ++i) {
                 const int32_t e = te[i], p = lp[i];
                 rp.elem_global[elem_off[t] + p] = e;

@@ -4,9 +4,11 @@
 // 16-byte-aligned blob so the tile kernel fetches it with a single TMA bulk
 // copy (cp.async.bulk) into shared memory. Sections (each 16 B aligned):
 //   CF_GEOM_STORED (default):
-//   geom      6 x ne8 x 16 B SoA of 16-byte pairs, one pair per element per column:
-//                            (g1x g1y) (g1z g2x) (g2y g2z) (g3x g3y) (g3z vol) (max_edge conn)
-//                            -- conn = the tile-local slots of the 4 nodes (ushort4)
+//   geom      5 x ne8 x 16 B SoA of 16-byte pairs, one pair per element per column:
+//                            (g1x g1y) (g1z g2x) (g2y g2z) (g3x g3y) (g3z vol)
+//   conn      ne8 x ushort4  tile-local slots of the 4 nodes
+//   (max_edge is not streamed: the degeneracy test bounds it by 1/|g1| and reads the exact
+//    value, ne8 f64 in an uncopied tail after `bytes`, only when that bound cannot decide)
 //   CF_GEOM_COORDS:
 //   xyz       ns x 4 f64     slot coordinates (x, y, z, 0)
 //   geom      ne2 f64        max_edge
@@ -35,9 +37,8 @@
 // previous step) fetched by a second bulk copy, so no tile ever gathers T.
 // (nX = n rounded up to a multiple of X.) Host packing (cf_plan.cpp) and the
 // device view (cf_kernels.cuh) both use TileLayout, so they cannot disagree.
-// Host staging (cf_plan.cpp -> fill_tiles_kernel) holds the sections from `stage`
-// on, with the connectivity first: stored layout [conn ne2 x 8 B | minedge .. end),
-// coordinates layout [conn .. end) verbatim; the geometry is computed on the device.
+// Host staging (cf_plan.cpp -> fill_tiles_kernel) holds the sections [conn, bytes) verbatim;
+// the geometry (and the stored layout's max_edge tail) is computed on the device.
 #pragma once
 
 #include <cstdint>
@@ -66,8 +67,9 @@ CF_HD int32_t cf_round32(int32_t n, int32_t m) { return (n + m - 1) & ~(m - 1); 
 struct TileLayout {
     // byte offsets (a tile is at most ~220 KB: 32-bit offsets keep the kernel's registers down)
     int32_t geom, xyz, conn, minedge, fac, snode, csr_end, csr, sinfo, region, zero, bytes;
-    int32_t stage;     // first byte of the host-staged part (conn for the stored layout is staged
-                       // as an 8 B x ne2 prefix at `stage - 8 * ne2`, then placed into the pairs)
+    int32_t stage;     // first byte of the host-staged part (= conn)
+    int32_t total;     // bytes in HBM: `bytes` (copied to shared memory) + the stored layout's
+                       // uncopied max_edge tail (ne2 f64 at offset `bytes`)
     int32_t ne2;       // SoA stride (elements)
     int32_t nf;
     bool coords;
@@ -104,11 +106,12 @@ struct TileLayout {
             conn = o;
             o += 8 * ne2;
         } else {
-            o += 6 * 16 * ne2;
-            conn = 5 * 16 * ne2 + 8;  // inside the (max_edge, conn) pairs, 16-byte stride
+            o += 5 * 16 * ne2;
+            conn = o;
+            o += 8 * ne2;
         }
         minedge = o;
-        stage = coords ? conn : o;
+        stage = conn;
         if (tdep) o += 8 * ne2;
         fac = o;
         o += 48 * m.nf;
@@ -125,19 +128,21 @@ struct TileLayout {
         zero = o;  // 16 zero bytes
         o += 16;
         bytes = o;
+        total = coords ? bytes : bytes + 8 * ne2;
         r_zero = coords ? 0 : (zero >> 4);
         r_lump = coords ? 2 : 0;
         scratch = coords ? 2 + 5 * ne2 + 3 * cf_round32(m.nf, 2) : 0;
     }
-    // byte offsets of element i's connectivity (ushort4) and of facet f's record fields
-    CF_HD int32_t conn_of(int i) const { return conn + (coords ? 8 : 16) * i; }
+    // byte offsets of element i's connectivity (ushort4), its exact max_edge (stored layout: in the
+    // uncopied tail) and of facet f's record fields
+    CF_HD int32_t conn_of(int i) const { return conn + 8 * i; }
+    CF_HD int32_t max_edge_of(int i) const { return coords ? geom + 8 * i : bytes + 8 * i; }
     CF_HD int32_t fac_area(int f) const { return fac + 48 * f; }
     CF_HD int32_t fac_slots(int f) const { return fac + 48 * f + 8; }
     CF_HD int32_t fac_sister(int f) const { return fac + 48 * f + 16; }
-    // bytes of the host staging of this tile
-    CF_HD int32_t staged_bytes() const { return bytes - stage + (coords ? 0 : 8 * ne2); }
-    // staging offset of a blob offset >= stage; the stored layout's connectivity prefix is at 0
-    CF_HD int32_t stage_of(int32_t off) const { return off - stage + (coords ? 0 : 8 * ne2); }
+    // bytes of the host staging of this tile, and the staging offset of a blob offset >= stage
+    CF_HD int32_t staged_bytes() const { return bytes - stage; }
+    CF_HD int32_t stage_of(int32_t off) const { return off - stage; }
 };
 
 }  // namespace cfb

@@ -320,3 +320,16 @@ def test_fields_into_caller_buffers():
         assert np.array_equal(To, T) and np.array_equal(Ho, H)
         with pytest.raises(ValueError):
             s.fields(out=(np.empty(3), None))
+
+
+@pytest.mark.parametrize("n", [24, 40])
+def test_uniform_t0_degeneracy_matches_reference(n):
+    """BASELINE's literal uniform casting T0 (no noise): the hot interior varies by round-off
+    only, so the Lemmon degeneracy test (fem.hpp:36-44) decides on near-zero gradients, where
+    the stored layout's 1/|g1| bound cannot and the exact max_edge is fetched from the blob's
+    uncopied tail. Bitwise equal to the oracle replaying the same tiles (cfg2 itself throws
+    "zero lumped capacitance" at step 30, node 802288, in the reference and here alike)."""
+    case = configs.casting(n, noise=0.0, dt_safety=0.138)
+    for geometry in ("stored", "coords"):
+        det, ref = run_pair(case, 80, tile_elems=384, geometry=geometry)
+        assert np.array_equal(det.T, ref.T), np.abs(det.T - ref.T).max()

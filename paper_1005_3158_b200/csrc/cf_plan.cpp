@@ -968,6 +968,20 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             for (int32_t l : tile_nodes[t]) b = b || shared_node[l];
             rp.tile_border[t] = b;
         }
+    // slot order inside a tile: tile-private nodes first (by contribution count, descending: similar
+    // reduction-list lengths share a warp), then the tile-shared nodes in ascending node id, so the
+    // partials they write and the slot copies the update kernel writes back are laid out in the
+    // update's (node) order -- whole sectors instead of scattered 16 / 8-byte accesses
+    if (!(std::getenv("CF_SLOT_ORDER") && std::string(std::getenv("CF_SLOT_ORDER")) == "count")) {
+#pragma omp parallel for schedule(dynamic, 256)
+        for (int32_t t = 0; t < rp.n_tiles; ++t) {
+            auto& tn = tile_nodes[t];
+            auto mid = std::stable_partition(tn.begin(), tn.end(), [&](int32_t l) {
+                return ntiles_of[l] == 1 && !shared_node[l];
+            });
+            std::sort(mid, tn.end());
+        }
+    }
     rp.tile_slot_off.assign(rp.n_tiles + 1, 0);
     rp.blob_off.assign(rp.n_tiles + 1, 0);
     rp.elem_global.resize(Er);

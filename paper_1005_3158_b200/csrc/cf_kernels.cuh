@@ -451,10 +451,12 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         // phase 3: per-slot fixed-order reduction (ascending element, then facets) + flush,
         // through the slot's 16-bit operand codes (cf_tileblob.hpp)
         const uint16_t* cend = (const uint16_t*)(B + L.csr_end);
+        const uint16_t* sperm = (const uint16_t*)(B + L.sperm);
         const uint16_t* csr = (const uint16_t*)(B + L.csr);
         const int32_t* snode = (const int32_t*)(B + L.snode);
         const double2* W = (const double2*)B;
-        for (int s = tid; s < ((a.probe & 15) == 3 ? 0 : ns); s += kTileThreads) {
+        for (int j = tid; j < ((a.probe & 15) == 3 ? 0 : ns); j += kTileThreads) {
+            const int s = sperm[j];  // threads take slots by list length (similar trip counts per warp)
             const int beg = s == 0 ? 0 : cend[s - 1];
             const int end = cend[s];
             double c = 0, r = 0;

@@ -339,6 +339,7 @@ struct BankPlanner {
         return mx;
     }
     // items: per slot [off[s], off[s+1]) in reduction order (already padded to multiples of 4)
+    const int32_t* sperm = nullptr;          // phase-3 thread j reduces slot sperm[j] (null: j)
     void run(int ne_, int ns_, const int32_t* eslot_, const std::vector<int32_t>& off,
              const std::vector<uint32_t>& items, int iters, uint64_t seed, bool greedy = true) {
         ne = ne_;
@@ -352,12 +353,15 @@ struct BankPlanner {
         // phase-3 groups
         a_off.assign(1, 0);
         a_items.clear();
+        auto slot_at = [&](int j) { return sperm ? sperm[j] : j; };
         for (int q0 = 0; q0 < ns; q0 += 8) {
             int mx = 0;
-            for (int s = q0; s < std::min(ns, q0 + 8); ++s) mx = std::max(mx, off[s + 1] - off[s]);
+            for (int u = q0; u < std::min(ns, q0 + 8); ++u) mx = std::max(mx, off[slot_at(u) + 1] - off[slot_at(u)]);
             for (int j = 0; j < mx; ++j) {
-                for (int s = q0; s < std::min(ns, q0 + 8); ++s)
-                    if (off[s] + j < off[s + 1]) a_items.push_back((int32_t)items[off[s] + j]);
+                for (int u = q0; u < std::min(ns, q0 + 8); ++u) {
+                    const int sl = slot_at(u);
+                    if (off[sl] + j < off[sl + 1]) a_items.push_back((int32_t)items[off[sl] + j]);
+                }
                 a_off.push_back((int32_t)a_items.size());
             }
         }
@@ -1029,7 +1033,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
 #pragma omp parallel num_threads(nthr) reduction(+ : n_if, n_bc)
     {
         std::vector<int32_t> slot_of(rp.n_local, -1), tfacets;
-        std::vector<int32_t> ent_off, cur, poff, eslot;
+        std::vector<int32_t> ent_off, cur, poff, eslot, sperm;
         std::vector<uint32_t> ent, items;
         BankPlanner bank;
 #pragma omp for schedule(dynamic, 64) reduction(+ : bank_before, bank_after, bank_a, bank_b, bank_ia, bank_ib, bank_id_a)
@@ -1070,12 +1074,21 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             items.assign(poff[ns], 0x80000000u | L.code_zero());
             for (int k = 0; k < ns; ++k)
                 std::copy(ent.begin() + ent_off[k], ent.begin() + ent_off[k + 1], items.begin() + poff[k]);
+            // phase-3 thread order: slots by padded list length (descending), so a warp's reduction
+            // loops have similar trip counts whatever the slot order (tile-shared slots by node id)
+            sperm.resize(ns);
+            std::iota(sperm.begin(), sperm.end(), 0);
+            std::stable_sort(sperm.begin(), sperm.end(), [&](int32_t x, int32_t y) {
+                return poff[x + 1] - poff[x] > poff[y + 1] - poff[y];
+            });
+            bank.sperm = sperm.data();
             eslot.resize(4 * (size_t)ne);
             for (int i = 0; i < ne; ++i)
                 for (int a = 0; a < 4; ++a) eslot[4 * i + a] = slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]];
             bank.run(ne, ns, eslot.data(), poff, items, coords ? 0 : bank_iters * ne, (uint64_t)t + 1);
             if (bank_trace) {
                 BankPlanner id;
+                id.sperm = sperm.data();
                 id.run(ne, ns, eslot.data(), poff, items, 0, 0, false);  // reference-order positions
                 if (!coords) {
                     bank_before += id.total_cost();
@@ -1118,6 +1131,8 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
                     n_bc++;
                 }
             }
+            uint16_t* sp = (uint16_t*)at(L.sperm);
+            for (int j = 0; j < ns; ++j) sp[j] = (uint16_t)sperm[j];
             uint16_t* cend = (uint16_t*)at(L.csr_end);
             uint16_t* csr = (uint16_t*)at(L.csr);
             int32_t* sn = (int32_t*)at(L.snode);

@@ -19,6 +19,9 @@
 //                            sister-element nodes (local / ghost ids) as int4, 16 B pad
 //   snode     ns4 i32        local node id of each slot (flush target)
 //   csr_end   ns8 u16        per-slot end of its contribution list (tile relative)
+//   sperm     ns8 u16        phase-3 thread order: thread j reduces slot sperm[j] (slots sorted by
+//                            list length; the slots themselves are private first, then shared by
+//                            node id)
 //   csr       ncsr8 u16      per-slot contribution codes in reduction order (see below); each
 //                            slot's list padded to a multiple of 4 with the zero operand
 //   sinfo     ns16 u8        region | 0x40 Dirichlet | 0x80 tile-private node
@@ -66,7 +69,7 @@ CF_HD int32_t cf_round32(int32_t n, int32_t m) { return (n + m - 1) & ~(m - 1); 
 
 struct TileLayout {
     // byte offsets (a tile is at most ~220 KB: 32-bit offsets keep the kernel's registers down)
-    int32_t geom, xyz, conn, minedge, fac, snode, csr_end, csr, sinfo, region, zero, bytes;
+    int32_t geom, xyz, conn, minedge, fac, snode, csr_end, sperm, csr, sinfo, region, zero, bytes;
     int32_t stage;     // first byte of the host-staged part (= conn)
     int32_t total;     // bytes in HBM: `bytes` (copied to shared memory) + the stored layout's
                        // uncopied max_edge tail (ne2 f64 at offset `bytes`)
@@ -118,6 +121,8 @@ struct TileLayout {
         snode = o;
         o += 4 * cf_round32(m.ns, 4);
         csr_end = o;
+        o += 2 * cf_round32(m.ns, 8);
+        sperm = o;
         o += 2 * cf_round32(m.ns, 8);
         csr = o;
         o += 2 * cf_round32(m.ncsr, 8);

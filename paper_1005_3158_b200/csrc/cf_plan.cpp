@@ -424,8 +424,12 @@ struct BankPlanner {
                     at[b0 + best] = i;
                 }
             }
-            // refinement: pairwise colour swaps inside a block (the block's corner gathers are
-            // unchanged) while they lower the reduction-read wavefronts
+            // refinement (CF_BANK_PASSES, default 0): pairwise colour swaps inside a block (the
+            // block's corner gathers are unchanged) while they lower the reduction-read wavefronts.
+            // cfg2: 3 passes take the reduction reads from 1.80x to 1.67x the ideal for -0.5 % tile
+            // time, but cost ~2 s of setup per 12.6 M tets (cfg5: ~30 s), so they are opt-in.
+            const char* rp_env = std::getenv("CF_BANK_PASSES");
+            const int refine_passes = rp_env ? std::atoi(rp_env) : 0;
             auto gmax = [&](int g) {
                 const int32_t* cg = &cnt[8 * (size_t)g];
                 int mx = 0;
@@ -433,7 +437,7 @@ struct BankPlanner {
                 return mx;
             };
             int touched[16];
-            for (int pass = 0; pass < 3; ++pass) {
+            for (int pass = 0; pass < refine_passes; ++pass) {
                 bool improved = false;
                 for (int b0 = 0; b0 < ne; b0 += 8) {
                     const int nb = std::min(8, ne - b0);

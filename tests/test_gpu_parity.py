@@ -68,6 +68,7 @@ def test_deterministic_repeat_bitwise():
 
 
 @pytest.mark.parametrize("env", [{"CF_TILE_PERSIST": "0"}, {"CF_TILE_DYNAMIC": "0"}, {"CF_BANK_ITERS": "4"},
+                                 {"CF_BANK_PASSES": "3"}, {"CF_SLOT_ORDER": "count"},
                                  {"CF_TILE_PERSIST": "0", "CF_BANK_ITERS": "0"}])
 def test_schedule_and_element_positions_leave_results_bitwise(env, monkeypatch):
     """Persistent (dynamically or statically scheduled) vs one-CTA-per-tile grids and the
@@ -333,3 +334,22 @@ def test_uniform_t0_degeneracy_matches_reference(n):
     for geometry in ("stored", "coords"):
         det, ref = run_pair(case, 80, tile_elems=384, geometry=geometry)
         assert np.array_equal(det.T, ref.T), np.abs(det.T - ref.T).max()
+
+
+def test_stepping_paths_share_the_dynamic_schedule():
+    """The persistent tile kernel's scheduling counter is reset by every step's advance kernel,
+    whichever API drives the steps: step(), time_phases() and fields() interleaved on ~1000 tiles
+    (several per CTA) stay bitwise equal to the oracle replaying the same tiles."""
+    case = configs.casting(40, jitter=0.2, seed=21, perm_seed=7, dt_safety=0.17)
+    opts = cf.SolveOptions(mode="deterministic")
+    with cf.Solver(case.mesh, case.setup, opts) as sv:
+        sv.step(5)
+        T5, _ = sv.fields(False)
+        sv.time_phases(10)
+        sv.step(20)
+        T35, _ = sv.fields(False)
+        assert sv.stats().step_index == 35
+    tiles, nt = cf.tile_map(case.mesh, case.setup, opts)
+    assert nt > 600  # more tiles than resident CTAs: the dynamic scheduler is active
+    assert np.array_equal(T5, orc.solve(case.mesh, case.setup, 5, blocks=tiles).T)
+    assert np.array_equal(T35, orc.solve(case.mesh, case.setup, 35, blocks=tiles).T)

@@ -331,6 +331,21 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             __syncthreads();  // s_issue read by every thread before its next write
             continue;
         }
+        // interface facets: the 4 sister temperatures of the lagged ambient (T^{k-1}, global) are
+        // gathered by cp.async into the facet record's sister/pad bytes (the ids are read first),
+        // overlapping phases 1 and 2a; the same thread consumes them in phase 2b
+        for (int i = tid; i < nf; i += kTileThreads) {
+            double2* rec = (double2*)(B + L.fac + 48 * i);
+            const ushort4 fs = *(const ushort4*)(B + L.fac_slots(i));
+            if (!P->kind[fs.w].interface) continue;
+            const int4 sn = *(const int4*)(rec + 1);
+            const uint32_t dst = smem_u32(rec + 1);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(a.Told + sn.x) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8), "l"(a.Told + sn.y) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 16), "l"(a.Told + sn.z) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 24), "l"(a.Told + sn.w) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
         // phase 1: H = enthalpy(T) per slot (blocked.hpp:462-467) from the streamed slot temperatures
         const uint8_t* sinfo = B + L.sinfo;
         for (int s = tid; s < ns; s += kTileThreads) {
@@ -417,14 +432,15 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                 const double var = K.var == CF_VAR_TIME ? time : (ts[0] + ts[1] + ts[2]) / 3.0;
                 q = 0.0;
                 h = dev_pl_eval(P, K.htab, var);
-                const double2 rec1 = rec[1];
-                const long long s01 = __double_as_longlong(rec1.x), s23 = __double_as_longlong(rec1.y);
-                // interface_ambient from the PRE-update T of the previous step (refresh_ambient lag)
+                // interface_ambient from the PRE-update T of the previous step (refresh_ambient lag),
+                // gathered before phase 1 (this thread's cp.async group)
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                const double2 t01 = rec[1], t23 = rec[2];
                 double sum = 0;
-                sum += a.Told[(int32_t)s01];
-                sum += a.Told[(int32_t)(s01 >> 32)];
-                sum += a.Told[(int32_t)s23];
-                sum += a.Told[(int32_t)(s23 >> 32)];
+                sum += t01.x;
+                sum += t01.y;
+                sum += t23.x;
+                sum += t23.y;
                 tinf = 0.25 * sum;
             } else {
                 q = K.q;

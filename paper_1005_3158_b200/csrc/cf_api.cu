@@ -427,7 +427,9 @@ void launch_pack(cf_plan* p, Rank& r, cudaStream_t st) {
     PackArgs a = r.pa;
     a.T = r.T[p->cur];
     a.u.T = r.T[p->cur];
-    const int blocks = std::max(1, std::min<int>(1184, (a.n_cr + a.n_t + 255) / 256));
+    // few CTAs (grid-stride): it runs beside the persistent interior tiles in the SM slots they
+    // leave free
+    const int blocks = std::max(1, std::min<int>(16, (a.n_cr + a.n_t + 255) / 256));
     if (p->mode == CF_MODE_DETERMINISTIC) pack_kernel<true><<<blocks, 256, 0, st>>>(a);
     else pack_kernel<false><<<blocks, 256, 0, st>>>(a);
 }
@@ -642,7 +644,7 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
             // heavy-first processing order (longest processing time first, for the dynamic
             // scheduler of single-rank persistent grids: -0.5 % tile time at cfg2; results do not
             // depend on the order). CF_TILE_ORDER=heavy | morton overrides.
-            bool heavy_first = p->world == 1 && !heavy_any && p->stages == 1;
+            bool heavy_first = !heavy_any && p->stages == 1;
             if (const char* e = std::getenv("CF_TILE_ORDER")) heavy_first = std::string(e) == "heavy";
             if (heavy_first)
                     std::stable_sort(lists[c].begin(), lists[c].end(), [&](int32_t x, int32_t y) {
@@ -667,21 +669,24 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
             // persistent CTAs (one per resident slot, each walking tiles it, it + grid, ...): the
             // CTA prologue is paid once and the next tile's copy is issued right after the previous
             // tile's reduction (cfg2: -2.9 % tile time). Not with a concurrent outlier-class launch,
-            // whose CTAs could only become resident after the persistent grid drained, and not on
-            // decomposed meshes, whose interior tiles overlap the exchange kernels (pack, NCCL).
-            bool persist = S == 2 || (!heavy_any && p->world == 1);
+            // whose CTAs could only become resident after the persistent grid drained. On
+            // decomposed meshes the grid leaves CTA slots for the exchange kernels (below).
+            bool persist = S == 2 || !heavy_any;
             if (const char* e = std::getenv("CF_TILE_PERSIST")) persist = S == 2 || std::atoi(e) != 0;
-            tl.grid = persist ? std::max(1, std::min<int>(tl.a.n_tiles, sms * per_sm)) : tl.a.n_tiles;
+            // decomposed plans leave a few CTA slots free so the exchange's pack and NCCL kernels
+            // (side stream) run beside the persistent interior tiles instead of after them
+            const int reserve = p->world > 1 ? 8 : 0;
+            tl.grid = persist ? std::max(1, std::min<int>(tl.a.n_tiles, sms * per_sm - reserve)) : tl.a.n_tiles;
             // persistent single-stage grids schedule tiles dynamically (ticket counter reset by
             // the advance kernel of every step); CF_TILE_DYNAMIC=0: static round-robin
             tl.a.sched = nullptr;
             const char* dyn_env = std::getenv("CF_TILE_DYNAMIC");
             if (persist && S == 1 && tl.grid < tl.a.n_tiles && !(dyn_env && std::atoi(dyn_env) == 0)) {
-                if (!r.sched) {
-                    r.sched = M.alloc<int32_t>(1);
-                    CF_CUDA_CHECK(cudaMemsetAsync(r.sched, 0, sizeof(int32_t), s));
+                if (!r.sched) {  // one counter per launch class (border / interior x light / heavy)
+                    r.sched = M.alloc<int32_t>(4);
+                    CF_CUDA_CHECK(cudaMemsetAsync(r.sched, 0, 4 * sizeof(int32_t), s));
                 }
-                tl.a.sched = r.sched;
+                tl.a.sched = r.sched + c;
             }
             // one tile per CTA: CTA it stages tile it + (resident CTAs) into L2 (CF_TILE_PREFETCH=k: k x that)
             tl.a.prefetch = 0;  // measured: no gain (the wait is occupancy, not DRAM latency)

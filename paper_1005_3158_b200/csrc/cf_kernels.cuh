@@ -692,7 +692,8 @@ template <bool TDEP>
 __global__ void advance_kernel(DevState* st, const DevParams* __restrict__ P, double t_end, int32_t* sched) {
     griddep_wait();
     if (threadIdx.x != 0) return;
-    if (sched) *sched = 0;  // the tile kernel's scheduling tickets restart every step
+    if (sched)  // the tile kernel's scheduling tickets (one counter per launch class) restart every step
+        for (int c = 0; c < 4; ++c) sched[c] = 0;
     double dt, t_next;
     bool done;
     step_dt<TDEP>(P, st, t_end, dt, t_next, done);

@@ -14,7 +14,7 @@ case = configs.casting(n, dt_safety=configs.DT_SAFETY["cfg4"], steps=steps)
 E = case.mesh.element_count()
 out = {"mesh": f"casting {n}^3", "elements": E, "steps": steps}
 ref = None
-for R in [1, 2, 8]:
+for R in [int(x) for x in os.environ.get("RANKS", "1 2 8").split()]:
     t0 = time.time()
     opts = cf.SolveOptions(world_size=R, local_ranks=R, rank=0)
     with cf.Solver(case.mesh, case.setup, opts) as sv:
@@ -24,9 +24,11 @@ for R in [1, 2, 8]:
         sv.step(steps)
         secs = sv.stats().loop_seconds - before
         T, _ = sv.fields(False)
+        ph = sv.time_phases(10)
     if ref is None:
         ref = T
     out[f"R={R}"] = {"element_updates_per_s": E * steps / secs, "ms_per_step": 1e3 * secs / steps,
-                     "setup_s": setup, "max_rel_vs_R1": float(np.max(np.abs(T - ref) / np.abs(ref)))}
+                     "setup_s": setup,
+                     "phases_ms (tile, pack, exchange, update)": [float(x) for x in ph], "max_rel_vs_R1": float(np.max(np.abs(T - ref) / np.abs(ref)))}
     print(R, out[f"R={R}"], flush=True)
 print(json.dumps(out))

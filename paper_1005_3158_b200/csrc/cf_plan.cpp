@@ -1034,23 +1034,91 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     // +13 s setup at cfg2; off by default)
     const int bank_iters = bank_env ? std::atoi(bank_env) : 0;
     const bool bank_trace = std::getenv("CF_TRACE_SETUP") && std::atoi(std::getenv("CF_TRACE_SETUP"));
+    const bool slot_order_default = !(std::getenv("CF_SLOT_ORDER") && std::string(std::getenv("CF_SLOT_ORDER")) != "node")
+                                    && !(std::getenv("CF_SLOT_BANKS") && std::atoi(std::getenv("CF_SLOT_BANKS")) == 0);
 #pragma omp parallel num_threads(nthr) reduction(+ : n_if, n_bc)
     {
         std::vector<int32_t> slot_of(rp.n_local, -1), tfacets;
-        std::vector<int32_t> ent_off, cur, poff, eslot, sperm;
+        std::vector<int32_t> ent_off, cur, poff, eslot, sperm, tn, gmem, goff, ord, bank_of;
         std::vector<uint32_t> ent, items;
+        std::vector<int32_t> gcnt;
         BankPlanner bank;
 #pragma omp for schedule(dynamic, 64) reduction(+ : bank_before, bank_after, bank_a, bank_b, bank_ia, bank_ib, bank_id_a)
         for (int32_t t = 0; t < rp.n_tiles; ++t) {
             const auto& te = tiles[t];
-            const auto& tnodes = tile_nodes[t];
             const TileMeta tm = rp.tile_meta[t];
             const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
             const TileLayout L(tm, S.temp_dep, coords);
             uint8_t* const stg = rp.blob.data() + rp.rest_off[t];  // connectivity first, then sections >= stage
             std::memset(stg, 0, (size_t)L.staged_bytes());
             auto at = [&](int32_t off) { return stg + L.stage_of(off); };
-            for (int k = 0; k < ns; ++k) slot_of[tnodes[k]] = k;
+            tn.assign(tile_nodes[t].begin(), tile_nodes[t].end());
+            const auto& tnodes = tn;
+            for (int k = 0; k < ns; ++k) slot_of[tn[k]] = k;
+            // bank-aware numbering of the tile-private slots (their order is free: the reduction's
+            // thread order is sperm, the update never sees them): phase 2a reads sTH[slot] for
+            // corner q of 8 consecutive elements (the bank planner keeps such blocks together), so
+            // spread each block's corner slots over the 8 bank groups (slot & 7); shared slots fixed
+            if (!coords && ne >= 16 && slot_order_default) {
+                int np = 0;
+                while (np < ns && ntiles_of[tn[np]] == 1 && !shared_node[tn[np]]) ++np;
+                if (np >= 16) {
+                    const int ng = 4 * ((ne + 7) / 8);
+                    goff.assign(ng + 1, 0);
+                    gmem.clear();
+                    for (int b0 = 0, g = 0; b0 < ne; b0 += 8)
+                        for (int q = 0; q < 4; ++q, ++g) {
+                            for (int i = b0; i < std::min(ne, b0 + 8); ++i) {
+                                const int32_t sl = slot_of[local_of[m.tets[4 * (size_t)te[i] + q]]];
+                                bool dup = false;
+                                for (int k = goff[g]; k < (int)gmem.size(); ++k) dup = dup || gmem[k] == sl;
+                                if (!dup) gmem.push_back(sl);
+                            }
+                            goff[g + 1] = (int)gmem.size();
+                        }
+                    // private slot (old index) -> its groups
+                    std::vector<std::vector<int32_t>> pg(np);
+                    for (int g = 0; g < ng; ++g)
+                        for (int k = goff[g]; k < goff[g + 1]; ++k)
+                            if (gmem[k] < np) pg[gmem[k]].push_back(g);
+                    gcnt.assign(8 * (size_t)ng, 0);
+                    for (int g = 0; g < ng; ++g)
+                        for (int k = goff[g]; k < goff[g + 1]; ++k)
+                            if (gmem[k] >= np) gcnt[8 * (size_t)g + (gmem[k] & 7)]++;
+                    int freeb[8];
+                    for (int b = 0; b < 8; ++b) freeb[b] = (np - b + 7) / 8;
+                    ord.resize(np);
+                    std::iota(ord.begin(), ord.end(), 0);
+                    std::stable_sort(ord.begin(), ord.end(),
+                                     [&](int32_t x, int32_t y) { return pg[x].size() > pg[y].size(); });
+                    bank_of.assign(np, -1);
+                    for (int32_t o : ord) {
+                        int best = -1, bc = 1 << 30;
+                        for (int b = 0; b < 8; ++b) {
+                            if (!freeb[b]) continue;
+                            int c = 0;
+                            for (int32_t g : pg[o]) c += gcnt[8 * (size_t)g + b];
+                            if (c < bc || (c == bc && freeb[b] > freeb[best])) {
+                                bc = c;
+                                best = b;
+                            }
+                        }
+                        bank_of[o] = best;
+                        freeb[best]--;
+                        for (int32_t g : pg[o]) gcnt[8 * (size_t)g + best]++;
+                    }
+                    // new index: the k-th private slot of bank b gets b + 8k (stable in old order)
+                    int nextb[8];
+                    for (int b = 0; b < 8; ++b) nextb[b] = b;
+                    std::vector<int32_t> newtn(tn.begin(), tn.begin() + np);
+                    for (int o = 0; o < np; ++o) {
+                        newtn[nextb[bank_of[o]]] = tn[o];
+                        nextb[bank_of[o]] += 8;
+                    }
+                    std::copy(newtn.begin(), newtn.end(), tn.begin());
+                    for (int k = 0; k < np; ++k) slot_of[tn[k]] = k;
+                }
+            }
             tile_facets(te, tfacets);
             // per-slot contributions in reduction order (ascending element, then facets):
             // element corner (i << 2 | q) or 0x80000000 | final 16-bit code

@@ -4,19 +4,20 @@
 A "step" is one explicit time step (blocked_step, blocked.hpp:542-550) over
 the whole synthetic mesh: element/facet assembly + merge + update.
 
-Workloads (seeded synthetic meshes, no external data):
-  N = 1   BASELINE configs[1] = cfg2: 128^3-cell casting (12,582,912 tets).
-  N > 1   weak-scaling ladder at ~12.6 M tets per GPU: casting n = 128*N^(1/3)
-          (N=2: 161^3, N=4: 203^3, N=8: 256^3 = BASELINE config 4), RCB
-          decomposition, one NCCL exchange of interface-node partials per step.
-  --config cfg1..cfg5 overrides (all N then run that one mesh: strong scaling).
+Workload (seeded synthetic meshes, no external data): BASELINE
+configs[4] = cfg5, the 512^3-cell casting (805,306,368 tets, 135.6 M nodes), the
+largest configuration and the one the 1/2/4/8-GPU metric is quoted on; it fits one
+B200 (~105 GB). N = 1 steps it on one GPU; N > 1 is strong scaling of the SAME mesh:
+recursive coordinate bisection into N parts, one rank per GPU, one NCCL exchange of
+interface-node partials per step. --config cfg1..cfg4 selects another config.
 
 value  = element-updates/s over the K timed steps, inputs resident in HBM
          (device time by CUDA events on the plan's stream; max over ranks).
-e2e    = the same metric through the public API with host buffers:
+e2e    = the same metric through the public API with pinned host buffers:
          set_temperature(host T0) -> step(K) -> fields(host T, H).
---impl reference times the reference solver itself (oracle/_ref, the
-         unmodified castfem headers) on the host cores: rank 0 only.
+--impl reference times the reference solver itself (oracle/_ref/ref_bench: the
+         unmodified castfem headers + the oracle's workload generator, its own process;
+         this process never loads the product library) on the host: rank 0 only.
 """
 from __future__ import annotations
 
@@ -47,10 +48,12 @@ FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)  # BASELINE configs[1]: 1000 steps
+    ap.add_argument("--steps", type=int, default=200)  # BASELINE configs[4]: 200 steps
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default=None, help="cfg1..cfg5 (default: cfg2 at N=1, weak ladder at N>1)")
+    ap.add_argument("--config", default="cfg5", help="cfg1..cfg5 (default cfg5; N > 1: strong scaling of it)")
+    ap.add_argument("--weak", action="store_true",
+                    help="diagnostics: weak-scaling ladder at ~12.6 M tets per GPU instead of --config")
     ap.add_argument("--casting", type=int, default=0, help="diagnostics: an n^3-cell casting instead of a config")
     ap.add_argument("--mode", default="deterministic", choices=["atomic", "deterministic"])
     ap.add_argument("--tile", type=int, default=384)
@@ -58,8 +61,10 @@ def parse():
     ap.add_argument("--geometry", default="stored", choices=["stored", "coords"],
                     help="tile layout: slot coordinates (gradients recomputed) or stored ElementGeom")
     ap.add_argument("--node-order", default="tile")
-    ap.add_argument("--cpu-steps", type=int, default=int(os.environ.get("CF_CPU_STEPS", "12")))
+    ap.add_argument("--cpu-steps", type=int, default=int(os.environ.get("CF_CPU_STEPS", "5")))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-blocked", action="store_true",
+                    help="--impl reference: also time the reference's own cache blocking (autotune_block_count)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", type=int, default=0, help="capture the step loop in CUDA graphs of this many steps")
     ap.add_argument("--phase-steps", type=int, default=20)
@@ -84,18 +89,98 @@ def dist_env():
         os.environ.get("LOCAL_RANK", "0"))
 
 
-def make_case(cfg: str | None, world: int, casting_n: int = 0):
+def make_case(cfg: str, world: int, casting_n: int = 0, weak: bool = False):
     from paper_1005_3158_b200 import configs
     if casting_n:
         return configs.casting(casting_n, dt_safety=configs.DT_SAFETY["cfg2"], steps=100,
                                name=f"casting{casting_n}"), f"casting{casting_n}", "weak"
-    if cfg:
-        return configs.CONFIGS[cfg](), cfg, "strong" if world > 1 else "weak"
-    if world == 1:
-        return configs.config2(), "cfg2", "weak"
-    n = int(round(128 * world ** (1.0 / 3.0)))
-    return configs.casting(n, dt_safety=configs.DT_SAFETY["cfg4"], steps=500, name=f"casting{n}"), \
-        f"weak_casting{n}", "weak"
+    if weak and world > 1:
+        n = int(round(128 * world ** (1.0 / 3.0)))
+        return configs.casting(n, dt_safety=configs.DT_SAFETY["cfg4"], steps=500, name=f"casting{n}"), \
+            f"weak_casting{n}", "weak"
+    return configs.CONFIGS[cfg](), cfg, "strong" if world > 1 else "weak"
+
+
+# The reference arm's bounded sample per workload ("time a truncated run"). The
+# reference needs ~420 B/tet of host memory and ~1.2 us/tet of setup: cfg5 in full
+# would take > 300 GB and ~16 min, more than the GPU box's host (196 GB, 16 cores). The sample is a
+# z-slab window of the SAME mesh -- same h, element shapes, regions, interface, initial field and
+# dt -- with adiabatic cut planes: per-element work equals the full mesh's, so the per-element
+# rate is the reference's rate on the workload. Full meshes where they fit in seconds.
+REF_WINDOW = {"cfg4": [0, 256, 0, 256, 112, 144],   # 256 x 256 x 32 cells = 12,582,912 tets
+              "cfg5": [0, 512, 0, 512, 252, 260]}   # 512 x 512 x 8 cells  = 12,582,912 tets
+REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+
+
+def reference_sample(cfg: str, steps: int, warmup: int, blocks: int = 1, autotune=None, window="default"):
+    """Runs the reference solver on the host (oracle/_ref/ref_bench, its own process: the
+    unmodified castfem headers and the oracle's workload generator; no product library)."""
+    if not os.path.exists(REF_BENCH):
+        return None, "oracle/_ref/ref_bench not built (needs the reference headers at build time)"
+    w = REF_WINDOW.get(cfg) if window == "default" else window
+    cmd = [REF_BENCH, "--workload", cfg, "--steps", str(steps), "--warmup", str(warmup), "--blocks", str(blocks)]
+    if w:
+        cmd += ["--window", f"{w[0]}:{w[1]},{w[2]}:{w[3]},{w[4]}:{w[5]}"]
+    if autotune:
+        cmd += ["--autotune", ",".join(map(str, autotune))]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode != 0:
+        return None, f"ref_bench failed ({out.returncode}): {out.stderr.strip()[-300:]}"
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    what = (f"z-slab window cells {w[0]}:{w[1]} x {w[2]}:{w[3]} x {w[4]}:{w[5]} of the {cfg} mesh (same h, "
+            f"regions, interface, T0 and dt; adiabatic cut planes)" if w else f"the full {cfg} mesh")
+    r["sample"] = (f"{r['steps']} blocked_step calls after {r['warmup']} warm-up on {what}: E={r['elements']}, "
+                   f"{r['blocks']} cache block(s); setup {r['setup_seconds']:.1f}s excluded (loop_seconds, "
+                   f"blocked.hpp:673-684); serial by contract (SPEC S:403-408)")
+    return r, None
+
+
+def cpu_reference_rate(cfg: str, steps: int):
+    r, err = reference_sample(cfg, steps, 1)
+    if r is None:
+        return {"error": err}
+    return {"value": r["element_updates_per_s"], "unit": "element-updates/s", "cores": 1, "kind": "reference",
+            "sample": r["sample"], "seconds": r["seconds"]}
+
+
+def _maps_product_library() -> bool:
+    try:
+        with open("/proc/self/maps") as f:
+            return "libcastfem_b200" in f.read()
+    except OSError:
+        return False
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = args.config
+    steps, warmup = max(1, min(args.steps, 20)), min(args.warmup, 2)
+    r, err = reference_sample(cfg, steps, warmup)
+    if r is None:
+        print(json.dumps({"impl": "reference", "unavailable": err}), flush=True)
+        return
+    blocked = None
+    if args.ref_blocked:  # the paper's technique: the reference's own cache blocking, autotuned
+        b, berr = reference_sample(cfg, steps, warmup, autotune=[1, 16, 64, 256],
+                                   window=[0, 512, 0, 512, 255, 257] if cfg == "cfg5" else "default")
+        blocked = b if b is not None else {"error": berr}
+    assert not _maps_product_library(), "the reference arm must not load the product library"
+    value = r["element_updates_per_s"]
+    line = {"impl": "reference", "metric": "element-updates/s (fp64)", "value": value, "unit": "element-updates/s",
+            "n_gpus": 0, "steps": r["steps"], "warmup": r["warmup"], "ms_per_step": 1e3 * r["seconds"] / r["steps"],
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded Kuhn-split casting fixtures, SURVEY §8(d))",
+            "config": {"workload": cfg, "sample_elements": r["elements"], "sample_nodes": r["nodes"],
+                       "window": r["window"], "h_interface": 1000.0},
+            "cpu_baseline": {"value": value, "unit": "element-updates/s", "cores": 1, "kind": "reference",
+                             "sample": r["sample"]},
+            "e2e": {"value": value, "unit": "element-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_run": {k: r[k] for k in ("seconds", "setup_seconds", "dt", "T_sum", "T_min", "T_max",
+                                                "interface_pairs")},
+            "reference_blocked": blocked}
+    print(json.dumps(line), flush=True)
 
 
 class ClockSampler:
@@ -173,61 +258,10 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback"
 
 
-def cpu_reference_rate(case, steps: int):
-    """The reference solver (oracle/_ref: unmodified castfem headers, 1 host core)."""
-    from oracle import oracle as orc
-    if not orc.ref_available():
-        return None
-    t0 = time.time()
-    rb = orc.RefBench(case.mesh, case.setup)
-    setup_s = time.time() - t0
-    rb.steps(1)  # warm
-    secs = rb.steps(steps)
-    rb.close()
-    E = case.mesh.element_count()
-    return {"value": E * steps / secs, "unit": "element-updates/s", "cores": 1, "kind": "reference",
-            "sample": f"{case.name}: {steps} blocked_step calls of the full mesh (E={E}), 1 warm step, "
-                      f"setup {setup_s:.1f}s excluded (loop_seconds semantics, blocked.hpp:673-684)",
-            "seconds": secs}
-
-
-def run_reference(args):
-    world, rank, _ = dist_env()
-    if rank != 0:
-        return
-    case, cfg, scaling = make_case(args.config, 1 if args.config is None else world)
-    if args.config is None and world > 1:
-        case, cfg, scaling = make_case(None, world)
-    from oracle import oracle as orc
-    if not orc.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcastfem_ref.so not built"}))
-        return
-    E = case.mesh.element_count()
-    t0 = time.time()
-    rb = orc.RefBench(case.mesh, case.setup)
-    setup_s = time.time() - t0
-    # each bench step = one blocked_step of the reference on the full mesh; the
-    # sample is bounded to ~10-30 s of CPU work (fewer steps on large meshes)
-    per = max(1, min(args.steps, 10 if E <= 20_000_000 else 3))
-    rb.steps(min(args.warmup, 2) if E <= 20_000_000 else 1)
-    secs = rb.steps(per)
-    rb.close()
-    value = E * per / secs
-    line = {"impl": "reference", "metric": "element-updates/s (fp64)", "value": value, "unit": "element-updates/s",
-            "n_gpus": 0, "steps": per, "warmup": min(args.warmup, 2), "ms_per_step": 1e3 * secs / per,
-            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg, "elements": E, "nodes": case.mesh.node_count(),
-                       "dt_safety": case.setup.solver.dt_safety, "h_interface": 1000.0},
-            "cpu_baseline": {"value": value, "unit": "element-updates/s", "cores": 1, "kind": "reference",
-                             "sample": f"{per} blocked_step calls on the full {cfg} mesh (E={E}; bounded; the "
-                                       f"reference is serial by contract, SPEC S:403-408; setup {setup_s:.1f}s "
-                                       f"excluded)"},
-            "e2e": {"value": value, "unit": "element-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
 def main():
     args = parse()
+    if "CF_PROBE" in os.environ:
+        sys.exit("bench.py: CF_PROBE is a diagnostics knob (results invalid); unset it to measure")
     if args.impl == "reference":
         return run_reference(args)
     world, rank, local_rank = dist_env()
@@ -238,7 +272,7 @@ def main():
         pg = dist
     from paper_1005_3158_b200 import castfem as cf
 
-    case, cfg, scaling = make_case(args.config, world, args.casting)
+    case, cfg, scaling = make_case(args.config, world, args.casting, args.weak)
     mesh, setup = case.mesh, case.setup
     comm = None
     if world > 1:
@@ -343,7 +377,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_rate(case, args.cpu_steps)
+            cpu = cpu_reference_rate(cfg, args.cpu_steps)
         except Exception as e:  # reported, not fatal
             cpu = {"error": str(e)}
 
@@ -365,7 +399,9 @@ def main():
                 "gpu_launches": int(st.launches_per_step * args.steps), "clocks": clocks,
                 "device_bytes": int(st.device_bytes), "tiles": int(st.n_tiles),
                 "host_peak_rss_gb": round(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20, 2),
-                "total_slots": int(st.total_slots)}
+                "total_slots": int(st.total_slots),
+                "env": {k: v for k, v in sorted(os.environ.items()) if k.startswith("CF_")},
+                "build": "production (probe branches compiled out: no CF_DIAG)"}
         print(json.dumps(line), flush=True)
     solver.close()
     if comm:

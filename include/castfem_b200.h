@@ -279,6 +279,27 @@ int cf_comm_create(int32_t world_size, int32_t rank, int32_t device,
                    const uint8_t unique_id[128], cf_comm** out);
 int cf_comm_destroy(cf_comm* comm);
 
+/* Host-staged transport: the exchange_and_merge payload moves
+ * through caller-supplied callbacks instead of NCCL, e.g. over a gloo / MPI / TCP
+ * process group. Use it where NCCL cannot run: several rank processes sharing one
+ * GPU (NCCL refuses duplicate devices) or hosts without a GPU interconnect. Each
+ * step the pack kernel's send buffer is copied to pinned host memory, `sendrecv`
+ * moves every neighbour's payload (one paired round, the edge-colouring stages of
+ * S:441-449 collapsed), and the received payload is copied back before the update.
+ * `allreduce` combines per-rank scalars (dynamic-dt bound: min; clamp flag and the
+ * series' T_max: max; T_min: min) in place over all ranks. A nonzero callback
+ * return fails the step with CF_PROTOCOL. Steps are host-synchronous (no CUDA
+ * graphs). The callbacks are called from the thread that calls cf_step. */
+typedef struct cf_host_transport {
+    void* ctx;
+    int (*sendrecv)(void* ctx, int32_t n_peers, const int32_t* peers, const double* const* send,
+                    const int64_t* send_len, double* const* recv, const int64_t* recv_len);
+    int (*allreduce)(void* ctx, double* values, int64_t count, int32_t op); /* op: CF_REDUCE_* */
+} cf_host_transport;
+enum { CF_REDUCE_MIN = 0, CF_REDUCE_MAX = 1 };
+int cf_comm_create_host(int32_t world_size, int32_t rank, int32_t device,
+                        const cf_host_transport* transport, cf_comm** out);
+
 /* ---------------------------------------------------------------------------
  * Host utilities (no GPU needed) — the setup pipeline on either side of the path
  * ------------------------------------------------------------------------- */

@@ -58,6 +58,12 @@ def oracle_lib():
         L.or_assemble_part.restype = C.c_int
         L.or_assemble_part.argtypes = [C.POINTER(_abi.cf_mesh_desc), C.POINTER(_abi.cf_setup_desc), C.c_char_p, _dp,
                                        _dp, C.c_double, _dp, _dp]
+        L.or_generate_fixture.restype = C.c_int
+        L.or_generate_fixture.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, C.c_uint64, _ip,
+                                          C.POINTER(_abi.cf_fixture)]
+        L.or_counter_uniform_array.restype = None
+        L.or_counter_uniform_array.argtypes = [C.c_uint64, C.POINTER(C.c_int64), C.c_int64, C.c_double, C.c_double,
+                                               _dp]
         L.or_element_accumulate.restype = None
         L.or_element_accumulate.argtypes = [_dp, C.POINTER(_abi.cf_material), _dp, _dp, _dp, _dp]
         _o = L
@@ -254,3 +260,63 @@ def ref_load_partmap(text: bytes, n_elems: int):
         return st, ref_lib().ref_last_error().decode()
     return 0, (out[:n_elems], int(count.value))
 
+
+
+# ---------------------------------------------------------------- fixtures (oracle/fixture.c)
+REF_BENCH = os.path.join(HERE, "_ref", "ref_bench")
+
+
+def generate_fixture(kind: str, n: int, radius: float = 0.35, jitter: float = 0.0, seed: int = 0,
+                     perm_seed: int = 0, window=None) -> dict:
+    """The oracle's restatement of the synthetic workload generator (arrays as a dict)."""
+    k = {"cube": 0, "casting": 1}[kind]
+    w = np.ascontiguousarray(np.asarray(window, dtype=np.int32).reshape(6)) if window is not None else None
+    fx = _abi.cf_fixture()
+    wp = _p(w, C.c_int32)
+    st = oracle_lib().or_generate_fixture(k, n, radius, jitter, seed, perm_seed, wp, C.byref(fx))
+    if st:
+        raise OracleError(st, "bad fixture arguments")
+    out = {"nodes": np.zeros((fx.n_nodes, 3)), "tets": np.zeros((fx.n_elems, 4), np.int32),
+           "region": np.zeros(fx.n_elems, np.int32), "facets": np.zeros((fx.n_facets, 3), np.int32),
+           "facet_tag": np.zeros(fx.n_facets, np.int32), "node_grid": np.zeros(fx.n_nodes, np.int32)}
+    fx.coords = _p(out["nodes"])
+    fx.tets = _p(out["tets"], C.c_int32)
+    fx.region = _p(out["region"], C.c_int32)
+    fx.facets = _p(out["facets"], C.c_int32)
+    fx.facet_tag = _p(out["facet_tag"], C.c_int32)
+    fx.node_grid = _p(out["node_grid"], C.c_int32)
+    st = oracle_lib().or_generate_fixture(k, n, radius, jitter, seed, perm_seed, wp, C.byref(fx))
+    if st:
+        raise OracleError(st, "fixture generation failed")
+    return out
+
+
+def counter_uniform(seed: int, keys: np.ndarray, lo: float, hi: float) -> np.ndarray:
+    keys = np.ascontiguousarray(keys, dtype=np.int64)
+    out = np.zeros(keys.shape[0])
+    oracle_lib().or_counter_uniform_array(seed, keys.ctypes.data_as(C.POINTER(C.c_int64)), keys.shape[0], lo, hi,
+                                          _p(out))
+    return out
+
+
+def ref_bench(workload: str, steps: int = 10, warmup: int = 1, window=None, blocks: int = 1, autotune=None,
+              describe: bool = False, dump_T: Optional[str] = None, timeout: float = 3600) -> dict:
+    """Runs oracle/_ref/ref_bench (the reference's own blocked_step loop in its own process)."""
+    import json
+    import subprocess
+    if not os.path.exists(REF_BENCH):
+        raise ImportError(f"{REF_BENCH} missing: run `make -C oracle` where /root/reference exists")
+    cmd = [REF_BENCH, "--workload", workload, "--steps", str(steps), "--warmup", str(warmup), "--blocks", str(blocks)]
+    if window is not None:
+        w = list(window)
+        cmd += ["--window", f"{w[0]}:{w[1]},{w[2]}:{w[3]},{w[4]}:{w[5]}"]
+    if autotune:
+        cmd += ["--autotune", ",".join(str(c) for c in autotune)]
+    if describe:
+        cmd.append("--describe")
+    if dump_T:
+        cmd += ["--dump-T", dump_T]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    if out.returncode != 0:
+        raise OracleError(out.returncode, out.stderr.strip())
+    return json.loads(out.stdout.strip().splitlines()[-1])

@@ -83,6 +83,16 @@ class cf_fixture(C.Structure):
                 ("tets", _ip), ("region", _ip), ("facets", _ip), ("facet_tag", _ip), ("node_grid", _ip)]
 
 
+CF_REDUCE_MIN, CF_REDUCE_MAX = 0, 1
+SENDRECV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, _ip, C.POINTER(_dp), C.POINTER(C.c_int64),
+                          C.POINTER(_dp), C.POINTER(C.c_int64))
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, _dp, C.c_int64, C.c_int32)
+
+
+class cf_host_transport(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("sendrecv", SENDRECV_FN), ("allreduce", ALLREDUCE_FN)]
+
+
 # (name, restype, argtypes) — every symbol declared in include/castfem_b200.h
 SIGNATURES = [
     ("cf_abi_version", C.c_int, []),
@@ -102,6 +112,8 @@ SIGNATURES = [
     ("cf_estimate_lambda_max", C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, _dp, _dp]),
     ("cf_comm_unique_id", C.c_int, [C.c_char_p]),
     ("cf_comm_create", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_void_p)]),
+    ("cf_comm_create_host", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(cf_host_transport),
+                                      C.POINTER(C.c_void_p)]),
     ("cf_comm_destroy", C.c_int, [C.c_void_p]),
     ("cf_rcm_permutation", C.c_int, [C.POINTER(cf_mesh_desc), C.c_int32, _ip]),
     ("cf_bandwidth", C.c_int, [C.POINTER(cf_mesh_desc), _ip, C.POINTER(C.c_int64)]),

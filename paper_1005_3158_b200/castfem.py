@@ -194,7 +194,7 @@ class SolveOptions:
     rank: int = 0
     local_ranks: int = 1
     part_of_element: Optional[np.ndarray] = None
-    comm: Optional["Comm"] = None
+    comm: Optional["Comm"] = None    # Comm (NCCL) or HostComm (host-staged) for world_size > local_ranks
     graph_steps: int = 0
 
 
@@ -339,6 +339,58 @@ class Comm:
     def __init__(self, world_size: int, rank: int, device: int, uid: bytes):
         h = C.c_void_p()
         check(lib().cf_comm_create(world_size, rank, device, uid, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib().cf_comm_destroy(self.handle)
+            self.handle = None
+
+
+class HostComm:
+    """Host-staged transport (cf_comm_create_host): the per-step exchange_and_merge payload
+     and the per-rank scalar reductions go through a torch.distributed process
+    group (e.g. gloo) instead of NCCL -- for rank processes that share one GPU (NCCL refuses
+    duplicate devices) or hosts without a GPU interconnect. One paired send/recv round per step
+    with every neighbour, like the NCCL path."""
+
+    def __init__(self, world_size: int, rank: int, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+        self._dist, self._torch, self._group = dist, torch, group
+
+        def sendrecv(ctx, n, peers, send, send_len, recv, recv_len):
+            try:
+                reqs = []
+                for k in range(n):
+                    q = int(peers[k])
+                    if send_len[k]:
+                        buf = np.ctypeslib.as_array(send[k], shape=(int(send_len[k]),))
+                        reqs.append(dist.isend(torch.from_numpy(buf), q, group=group))
+                    if recv_len[k]:
+                        buf = np.ctypeslib.as_array(recv[k], shape=(int(recv_len[k]),))
+                        reqs.append(dist.irecv(torch.from_numpy(buf), q, group=group))
+                for r in reqs:
+                    r.wait()
+                return 0
+            except Exception:  # reported by the library as CF_PROTOCOL
+                return 1
+
+        def allreduce(ctx, values, n, op):
+            try:
+                buf = np.ctypeslib.as_array(values, shape=(int(n),))
+                t = torch.from_numpy(buf)
+                dist.all_reduce(t, op=dist.ReduceOp.MIN if op == _abi.CF_REDUCE_MIN else dist.ReduceOp.MAX,
+                                group=group)
+                return 0
+            except Exception:
+                return 1
+
+        # the callbacks must outlive the communicator
+        self._cb = (_abi.SENDRECV_FN(sendrecv), _abi.ALLREDUCE_FN(allreduce))
+        t = _abi.cf_host_transport(None, self._cb[0], self._cb[1])
+        h = C.c_void_p()
+        check(lib().cf_comm_create_host(world_size, rank, device, C.byref(t), C.byref(h)))
         self.handle = h
 
     def close(self):

@@ -98,6 +98,8 @@ NcclApi& nccl() {
 struct cf_comm {
     ncclComm_t comm = nullptr;
     int world = 1, rank = 0, device = 0;
+    bool host = false;        // host-staged transport (cf_comm_create_host): callbacks instead of NCCL
+    cf_host_transport ht{};
 };
 
 // ------------------------------------------------------------------ plan
@@ -259,6 +261,9 @@ struct cf_plan {
     int64_t output_every = 0;
     double t_end_setup = 0;
     // graph
+    double* h_send = nullptr;    // host-staged transport: pinned copies of the send / recv payloads
+    double* h_recv = nullptr;
+    bool host_comm() const { return comm && comm->host && world > local_ranks; }
     double* dTg = nullptr;       // global-order staging (device) for set_temperature / get_fields
     double* dHg = nullptr;
     int64_t graph_steps = 0;
@@ -280,6 +285,8 @@ struct cf_plan {
         if (xjoin) cudaEventDestroy(xjoin);
         if (xside) cudaStreamDestroy(xside);
         if (d_states) cudaFree(d_states);
+        if (h_send) cudaFreeHost(h_send);
+        if (h_recv) cudaFreeHost(h_recv);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -377,6 +384,8 @@ void launch_tile(cf_plan* p, Rank& r, double t_end, int phase = -1) {
     }
 }
 
+void reduce_clamp(cf_plan* p, cudaStream_t st);
+
 template <bool DET, bool MULTI>
 void launch_update_t(cf_plan* p, Rank& r, const UpdArgs& a, int blocks) {
     // 128-thread CTAs (measured: update 0.0448 -> 0.0434 ms at cfg2 vs 256; CF_UPD_BLOCK overrides)
@@ -420,8 +429,18 @@ void launch_update(cf_plan* p, Rank& r, double t_end) {
     else if (det) launch_update_t<true, false>(p, r, a, blocks);
     else if (multi) launch_update_t<false, true>(p, r, a, blocks);
     else launch_update_t<false, false>(p, r, a, blocks);
+}
+
+void launch_advance(cf_plan* p, Rank& r, double t_end) {
     if (p->temp_dep) launch_ex(advance_kernel<true>, dim3(1), dim3(32), 0, p->stream, p->pdl, r.st, p->dP, t_end, r.sched);
     else launch_ex(advance_kernel<false>, dim3(1), dim3(32), 0, p->stream, p->pdl, r.st, p->dP, t_end, r.sched);
+}
+
+// merge + update of every local rank, the cross-rank clamp flag, then the state advance
+void launch_update_all(cf_plan* p, double t_end) {
+    for (auto& r : p->ranks) launch_update(p, *r, t_end);
+    reduce_clamp(p, p->stream);
+    for (auto& r : p->ranks) launch_advance(p, *r, t_end);
 }
 
 void launch_pack(cf_plan* p, Rank& r, cudaStream_t st) {
@@ -434,6 +453,11 @@ void launch_pack(cf_plan* p, Rank& r, cudaStream_t st) {
     const int blocks = std::max(1, std::min<int>(16, (a.n_cr + a.n_t + 255) / 256));
     if (p->mode == CF_MODE_DETERMINISTIC) pack_kernel<true><<<blocks, 256, 0, st>>>(a);
     else pack_kernel<false><<<blocks, 256, 0, st>>>(a);
+}
+
+void host_allreduce(cf_plan* p, double* v, int64_t n, int32_t op) {
+    const cf_host_transport& t = p->comm->ht;
+    if (t.allreduce(t.ctx, v, n, op) != 0) raise(CF_PROTOCOL, "host transport: allreduce failed");
 }
 
 void exchange(cf_plan* p, cudaStream_t st) {
@@ -458,6 +482,30 @@ void exchange(cf_plan* p, cudaStream_t st) {
         return;
     }
     if (!p->comm) raise(CF_NCCL, "world_size > local ranks but no communicator");
+    if (p->host_comm()) {
+        // host-staged: send payload -> pinned host -> caller's sendrecv -> pinned host -> recv buffer.
+        // The previous step's H2D from h_recv is complete: it precedes this D2H on the same stream.
+        Rank& r = *p->ranks[0];
+        const size_t nk = r.H.nbrs.size();
+        if (r.H.send_len) CF_CUDA_CHECK(cudaMemcpyAsync(p->h_send, r.send, r.H.send_len * sizeof(double),
+                                                        cudaMemcpyDeviceToHost, st));
+        CF_CUDA_CHECK(cudaStreamSynchronize(st));
+        std::vector<int32_t> peers(nk);
+        std::vector<const double*> sp(nk);
+        std::vector<double*> rp(nk);
+        for (size_t k = 0; k < nk; ++k) {
+            peers[k] = r.H.nbrs[k].rank;
+            sp[k] = p->h_send + r.H.send_off[k];
+            rp[k] = p->h_recv + r.H.recv_off[k];
+        }
+        const cf_host_transport& t = p->comm->ht;
+        if (t.sendrecv(t.ctx, (int32_t)nk, peers.data(), sp.data(), r.nb_send_len.data(), rp.data(),
+                       r.nb_recv_len.data()) != 0)
+            raise(CF_PROTOCOL, "host transport: sendrecv failed");
+        if (r.H.recv_len) CF_CUDA_CHECK(cudaMemcpyAsync(r.recv, p->h_recv, r.H.recv_len * sizeof(double),
+                                                        cudaMemcpyHostToDevice, st));
+        return;
+    }
     NcclApi& n = nccl();
     Rank& r = *p->ranks[0];
     CF_NCCL_CHECK(n.GroupStart());
@@ -489,10 +537,50 @@ void reduce_min_bound(cf_plan* p, cudaStream_t st) {
         CF_CUDA_CHECK(cudaGetLastError());
         return;
     }
+    unsigned long long* mb = p->ranks[0]->st->min_bound;  // positive doubles: bit order == value order
+    if (p->host_comm()) {
+        double v[2];
+        CF_CUDA_CHECK(cudaMemcpyAsync(v, mb, sizeof v, cudaMemcpyDeviceToHost, st));
+        CF_CUDA_CHECK(cudaStreamSynchronize(st));
+        host_allreduce(p, v, 2, CF_REDUCE_MIN);
+        CF_CUDA_CHECK(cudaMemcpyAsync(mb, v, sizeof v, cudaMemcpyHostToDevice, st));
+        CF_CUDA_CHECK(cudaStreamSynchronize(st));  // v is a stack array
+        return;
+    }
     NcclApi& n = nccl();
     if (!n.AllReduce) raise(CF_NCCL, "ncclAllReduce not available");
-    unsigned long long* mb = p->ranks[0]->st->min_bound;  // positive doubles: bit order == value order
     CF_NCCL_CHECK(n.AllReduce(mb, mb, 2, ncclUint64, ncclMin, p->comm->comm, st));
+}
+
+// clamp accounting over the whole mesh (update_fields blocked.hpp:526-534 counts a step as clamped
+// when any node clamps): OR of every rank's per-step flag before the advance kernels count it
+__global__ void clamp_combine_kernel(DevState* const* st, int n) {
+    int f = 0;
+    for (int r = 0; r < n; ++r) f |= st[r]->clamp_flag;
+    for (int r = 0; r < n; ++r) st[r]->clamp_flag = f;
+}
+
+void reduce_clamp(cf_plan* p, cudaStream_t st) {
+    if (!p->finite_range || p->world == 1) return;
+    if (p->local_ranks == p->world) {
+        clamp_combine_kernel<<<1, 1, 0, st>>>(p->d_states, (int)p->ranks.size());
+        CF_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
+    int* flag = &p->ranks[0]->st->clamp_flag;
+    if (p->host_comm()) {
+        int f = 0;
+        CF_CUDA_CHECK(cudaMemcpyAsync(&f, flag, sizeof f, cudaMemcpyDeviceToHost, st));
+        CF_CUDA_CHECK(cudaStreamSynchronize(st));
+        double v = f;
+        host_allreduce(p, &v, 1, CF_REDUCE_MAX);
+        f = v > 0 ? 1 : 0;
+        CF_CUDA_CHECK(cudaMemcpyAsync(flag, &f, sizeof f, cudaMemcpyHostToDevice, st));
+        CF_CUDA_CHECK(cudaStreamSynchronize(st));
+        return;
+    }
+    NcclApi& n = nccl();
+    CF_NCCL_CHECK(n.AllReduce(flag, flag, 1, ncclInt32, ncclMax, p->comm->comm, st));
 }
 
 // multi-rank (SURVEY 8(e) overlap): border tiles -> [side stream: pack -> exchange] while the
@@ -505,13 +593,19 @@ void enqueue_step(cf_plan* p, double t_end) {
         CF_CUDA_CHECK(cudaEventRecord(p->xfork, p->stream));
         CF_CUDA_CHECK(cudaStreamWaitEvent(p->xside, p->xfork, 0));
         for (auto& r : p->ranks) launch_pack(p, *r, p->xside);
-        exchange(p, p->xside);
-        CF_CUDA_CHECK(cudaEventRecord(p->xjoin, p->xside));
-        for (auto& r : p->ranks) launch_tile(p, *r, t_end, 1);
+        if (p->host_comm()) {  // the host blocks in the exchange: enqueue the interior tiles first
+            for (auto& r : p->ranks) launch_tile(p, *r, t_end, 1);
+            exchange(p, p->xside);
+            CF_CUDA_CHECK(cudaEventRecord(p->xjoin, p->xside));
+        } else {
+            exchange(p, p->xside);
+            CF_CUDA_CHECK(cudaEventRecord(p->xjoin, p->xside));
+            for (auto& r : p->ranks) launch_tile(p, *r, t_end, 1);
+        }
         reduce_min_bound(p, p->stream);
         CF_CUDA_CHECK(cudaStreamWaitEvent(p->stream, p->xjoin, 0));
     }
-    for (auto& r : p->ranks) launch_update(p, *r, t_end);
+    launch_update_all(p, t_end);
     p->advance();
 }
 
@@ -584,7 +678,9 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     a.max_slots = h.max_slots;
     a.blob_smem = (int32_t)cf_round(h.max_blob, 16);
     a.stages = p->stages;
+#ifdef CF_DIAG
     if (const char* e = std::getenv("CF_PROBE")) a.probe = std::atoi(e);
+#endif
     // tile classes: "light" = tiles whose footprint is within the 97th percentile,
     // "heavy" = the rest (e.g. a given block map's interface blocks), own concurrent launch
     {
@@ -704,7 +800,9 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     }
 
     UpdArgs& u = r.ua;
+#ifdef CF_DIAG
     if (const char* e = std::getenv("CF_PROBE")) u.probe = std::atoi(e);
+#endif
     u.n_local = h.n_local;
     u.n_ghost = h.n_ghost;
     u.merge_off = M.up(h.merge_off, s);  // partial merge (deterministic) + Tslot scatter (both modes)
@@ -805,6 +903,11 @@ void scatter_state(cf_plan* p) {
         const int64_t S_tot = (int64_t)r.H.slot_node.size();
         const int sb = (int)std::max<int64_t>(1, std::min<int64_t>(1184, (S_tot + 255) / 256));
         slot_init_kernel<<<sb, 256, 0, p->stream>>>(S_tot, r.ta.slot_node, r.T[0], r.Tslot[0], r.Tslot[1]);
+        if (r.acc_c) {  // atomic mode: no partial sums survive a re-initialisation
+            const size_t nb = sizeof(double) * std::max<int64_t>(1, r.H.n_local);
+            CF_CUDA_CHECK(cudaMemsetAsync(r.acc_c, 0, nb, p->stream));
+            CF_CUDA_CHECK(cudaMemsetAsync(r.acc_r, 0, nb, p->stream));
+        }
         DevState st{};
         st.min_bound[0] = st.min_bound[1] = 0x7ff0000000000000ull;
         st.err_node = INT32_MAX;
@@ -828,7 +931,9 @@ DevState read_state(cf_plan* p, int k = 0) {
 }
 
 void check_device_errors(cf_plan* p) {
+#ifdef CF_DIAG
     if (std::getenv("CF_PROBE")) return;  // diagnostics runs skip the physics
+#endif
     for (size_t k = 0; k < p->ranks.size(); ++k) {
         const DevState st = read_state(p, (int)k);
         if (st.err_node != INT32_MAX)
@@ -841,7 +946,7 @@ void run_steps(cf_plan* p, int64_t n, double t_end) {
     CF_CUDA_CHECK(cudaSetDevice(p->device));
     CF_CUDA_CHECK(cudaEventRecord(p->ev0, p->stream));
     int64_t done = 0;
-    if (p->graph_steps > 0) {
+    if (p->graph_steps > 0 && !p->host_comm()) {  // host-staged steps synchronise: never captured
         const int state_key = p->cur * 2 + p->step_parity;
         if (p->graph && (p->graph_t_end != t_end || p->graph_cur != state_key)) {
             cudaGraphExecDestroy(p->graph);
@@ -1192,6 +1297,11 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
                                  (double)v.accessPolicyWindow.hitRatio);
             }
         }
+        if (p->host_comm()) {
+            const RankPlan& h = p->ranks[0]->H;
+            CF_CUDA_CHECK(cudaMallocHost(&p->h_send, sizeof(double) * std::max<int64_t>(1, h.send_len)));
+            CF_CUDA_CHECK(cudaMallocHost(&p->h_recv, sizeof(double) * std::max<int64_t>(1, h.recv_len)));
+        }
         p->launches_per_step = 0;
         for (const auto& rk : p->ranks)
             p->launches_per_step += (int64_t)rk->launches.size() + 2 + (p->world > 1 ? 1 : 0);
@@ -1244,7 +1354,7 @@ int cf_time_phases(cf_plan* p, int64_t n, double* ms_out) {
             exchange(p, p->stream);
             reduce_min_bound(p, p->stream);
             CF_CUDA_CHECK(cudaEventRecord(ev[3], p->stream));
-            for (auto& r : p->ranks) launch_update(p, *r, 0.0);
+            launch_update_all(p, 0.0);
             CF_CUDA_CHECK(cudaEventRecord(ev[4], p->stream));
             p->advance();
             CF_CUDA_CHECK(cudaEventSynchronize(ev[4]));
@@ -1300,13 +1410,26 @@ int cf_solve(cf_plan* p, int64_t max_steps, double* series, int64_t cap, int64_t
             CF_CUDA_CHECK(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, p->stream));
             for (auto& r : p->ranks)
                 minmax_kernel<<<148, 256, 0, p->stream>>>(r->H.n_local, r->T[p->cur], mm);
+            // the series covers the whole mesh (solve_serial blocked.hpp:678-681): min / max over
+            // every rank of the job
+            if (p->world > p->local_ranks && !p->host_comm()) {
+                NcclApi& n = nccl();
+                CF_NCCL_CHECK(n.AllReduce(mm, mm, 1, ncclUint64, ncclMin, p->comm->comm, p->stream));
+                CF_NCCL_CHECK(n.AllReduce((unsigned long long*)mm + 1, (unsigned long long*)mm + 1, 1, ncclUint64,
+                                          ncclMax, p->comm->comm, p->stream));
+            }
             unsigned long long res[2];
             CF_CUDA_CHECK(cudaMemcpyAsync(res, mm, sizeof res, cudaMemcpyDeviceToHost, p->stream));
             const DevState st = read_state(p);
+            double lo = dec_ordered(res[0]), hi = dec_ordered(res[1]);
+            if (p->host_comm()) {
+                host_allreduce(p, &lo, 1, CF_REDUCE_MIN);
+                host_allreduce(p, &hi, 1, CF_REDUCE_MAX);
+            }
             if (series && ns < cap) {
                 series[3 * ns] = st.time;
-                series[3 * ns + 1] = dec_ordered(res[0]);
-                series[3 * ns + 2] = dec_ordered(res[1]);
+                series[3 * ns + 1] = lo;
+                series[3 * ns + 2] = hi;
             }
             ++ns;
         };
@@ -1563,6 +1686,20 @@ int cf_comm_create(int32_t world, int32_t rank, int32_t device, const uint8_t ui
         c->world = world;
         c->rank = rank;
         c->device = device;
+        *out = c.release();
+    });
+}
+
+int cf_comm_create_host(int32_t world, int32_t rank, int32_t device, const cf_host_transport* t, cf_comm** out) {
+    return guarded([&] {
+        if (!out || !t || !t->sendrecv || !t->allreduce) raise(CF_INVALID_ARG, "null argument");
+        if (world < 1 || rank < 0 || rank >= world) raise(CF_INVALID_ARG, "bad world / rank");
+        auto c = std::make_unique<cf_comm>();
+        c->world = world;
+        c->rank = rank;
+        c->device = device;
+        c->host = true;
+        c->ht = *t;
         *out = c.release();
     });
 }

@@ -237,6 +237,11 @@ std::unique_ptr<TextMesh> parse_mesh_binary(std::string_view b) {
     take(h, sizeof h);
     for (int k = 0; k < 5; ++k)
         if (h[k] < 0 || h[k] > INT32_MAX) raise(CF_PARSE, "binary mesh: bad count in header");
+    // the fixed-size sections the header announces must be present before anything is allocated
+    // (counts <= INT32_MAX: the byte total fits in 64 bits); tags add at least 4 bytes each
+    const uint64_t need = 24ull * (uint64_t)h[0] + 20ull * (uint64_t)h[1] + 16ull * (uint64_t)h[2] +
+                          4ull * (uint64_t)h[3] + 8ull * (uint64_t)h[4];
+    if (need > b.size() - pos) raise(CF_PARSE, "binary mesh truncated at byte " + std::to_string(b.size()));
     auto m = std::make_unique<TextMesh>();
     m->coords.resize(3 * (size_t)h[0]);
     m->tets.resize(4 * (size_t)h[1]);

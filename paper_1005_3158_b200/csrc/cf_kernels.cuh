@@ -36,6 +36,14 @@
 
 namespace cfb {
 
+// Diagnostics (CF_PROBE: skip phases, L2-resident replay) exist only in a -DCF_DIAG build
+// (`make DIAG=1`, results invalid); the production kernels compile every probe branch away.
+#ifdef CF_DIAG
+#define CF_PRB(a) ((a).probe)
+#else
+#define CF_PRB(a) 0
+#endif
+
 struct DevState {
     double time;
     double dt;
@@ -174,7 +182,7 @@ struct TileHdr {  // per stage: the metadata of the tile in flight (written befo
 // (slots == false: the slot temperatures -- written by the preceding kernel -- are left to
 // issue_slot_copy after griddep_wait; the barrier already expects their bytes)
 __device__ __forceinline__ void load_desc(const TileArgs& a, int it, int4& d0, int4& d1) {
-    if (a.probe & 16) it %= 1184;  // diagnostics: L2-resident tiles (compute-side time)
+    if (CF_PRB(a) & 16) it %= 1184;  // diagnostics: L2-resident tiles (compute-side time)
     d0 = __ldg((const int4*)(a.desc + it));
     d1 = __ldg((const int4*)(a.desc + it) + 1);
 }
@@ -201,7 +209,7 @@ __device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int4 d0, int4
 }
 // the next tile's descriptor, staged asynchronously into shared memory (no registers held)
 __device__ __forceinline__ void prefetch_desc(const TileArgs& a, int it, int4* sdesc) {
-    if (a.probe & 16) it %= 1184;
+    if (CF_PRB(a) & 16) it %= 1184;
     const int4* g = (const int4*)(a.desc + it);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdesc)), "l"(g) : "memory");
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdesc + 1)), "l"(g + 1) : "memory");
@@ -320,7 +328,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             if (nx < a.n_tiles) prefetch_desc(a, nx, ndesc);
         }
         int4 nd0, nd1;
-        if ((a.probe & 15) == 1) {  // diagnostics: memory-path timing without the physics
+        if ((CF_PRB(a) & 15) == 1) {  // diagnostics: memory-path timing without the physics
             __syncthreads();
             const int t_issue = s_issue;
             if (tid == 0 && t_issue < a.n_tiles) {
@@ -350,7 +358,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         const uint8_t* sinfo = B + L.sinfo;
         for (int s = tid; s < ns; s += kTileThreads) {
             const double T = sT[s];
-            sTH[s] = make_double2(T, (a.probe & 15) == 5 ? T : dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], T));
+            sTH[s] = make_double2(T, (CF_PRB(a) & 15) == 5 ? T : dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], T));
         }
         __syncthreads();
 
@@ -361,7 +369,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         double* R = (double*)(smem + a.scratch_off);  // coordinates layout only
         const uint8_t* ereg = B + L.region;
         const uint8_t* gblob = a.blob + hdr[stage].boff;  // this tile's blob in global memory
-        for (int i = tid; i < ((a.probe & 15) == 4 ? 0 : ne); i += kTileThreads) {
+        for (int i = tid; i < ((CF_PRB(a) & 15) == 4 ? 0 : ne); i += kTileThreads) {
             double g[4][3], vol, max_edge = 0;
             const ushort4 cn = ((const ushort4*)(B + L.conn))[i];
             if (GC) {
@@ -401,7 +409,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             double lump, rc[4];
             dev_element<TDEP, !GC>(
                 P, m, g, vol, [&]() { return GC ? max_edge : __ldg((const double*)(gblob + L.max_edge_of(i))); },
-                T, H, lump, rc, (a.probe & 15) == 7);
+                T, H, lump, rc, (CF_PRB(a) & 15) == 7);
             if (TDEP)
                 local_min = fmin(local_min, dev_stable_bound<TDEP>(P, m, ((const double*)(B + L.minedge))[i], T));
             if (GC) {
@@ -471,7 +479,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         const uint16_t* csr = (const uint16_t*)(B + L.csr);
         const int32_t* snode = (const int32_t*)(B + L.snode);
         const double2* W = (const double2*)B;
-        for (int j = tid; j < ((a.probe & 15) == 3 ? 0 : ns); j += kTileThreads) {
+        for (int j = tid; j < ((CF_PRB(a) & 15) == 3 ? 0 : ns); j += kTileThreads) {
             const int s = sperm[j];  // threads take slots by list length (similar trip counts per warp)
             const int beg = s == 0 ? 0 : cend[s - 1];
             const int end = cend[s];
@@ -492,7 +500,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        const double2 w = W[(a.probe & 15) == 8 ? ((v[k] & ~7u) | (s & 7)) : v[k]];
+                        const double2 w = W[(CF_PRB(a) & 15) == 8 ? ((v[k] & ~7u) | (s & 7)) : v[k]];
                         l[k] = w.x;
                         q[k] = w.y;
                     }
@@ -616,6 +624,10 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         const bool packed = cnt >= 0 && cnt <= 4;
         const double T = __ldg(a.T + i);
         if (done) {
+            if (!DET) {  // the tile kernel still accumulated this (no-op) step: drop it
+                a.acc_c[i] = 0;
+                a.acc_r[i] = 0;
+            }
             a.Tn[i] = T;
             if (packed) {
 #pragma unroll
@@ -631,7 +643,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
             // all partial loads issued before the in-order (ascending tile) sums
             double2 pr[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) pr[q] = (q < cnt && a.probe != 9) ? __ldg(a.part + sl[q]) : make_double2(1.0, 0.0);
+            for (int q = 0; q < 4; ++q) pr[q] = (q < cnt && CF_PRB(a) != 9) ? __ldg(a.part + sl[q]) : make_double2(1.0, 0.0);
             c = 0;
             r = 0;
 #pragma unroll
@@ -671,7 +683,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         const double Tn = node_update<DIR, CLAMP>(P, a.st, T, c, r, dt, t_next, DIR ? a.node_dir[i] : -1,
                                                   CLAMP ? a.node_region[i] : 0, a.local_global + i, clamped);
         a.Tn[i] = Tn;
-        if (a.probe == 8) continue;
+        if (CF_PRB(a) == 8) continue;
         if (packed) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)

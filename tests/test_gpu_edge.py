@@ -137,3 +137,26 @@ def test_zero_lumped_capacitance_reported_like_the_reference(tile_elems):
     with pytest.raises(cf.ValidationError) as gpu:
         cf.solve(m, s, cf.SolveOptions(max_steps=3, tile_elems=tile_elems))
     assert str(gpu.value) == str(ref.value).split("] ", 1)[1]
+
+
+def test_atomic_steps_past_t_end_leave_no_stale_sums():
+    """Atomic mode (fp64 RED accumulators): steps past t_end are no-ops (solve_serial
+    blocked.hpp:674-677) and must not leave partial sums behind for the next real step, nor may
+    a re-initialisation (set_temperature). Compared against the deterministic mode (1e-9)."""
+    case = configs.casting(10, dt_safety=0.14)
+    out = {}
+    for mode in ("deterministic", "atomic"):
+        with cf.Solver(case.mesh, case.setup, cf.SolveOptions(mode=mode)) as s:
+            dt = s.stats().static_dt
+            s.step(10, t_end=5.5 * dt)           # 6 real steps (the last one clipped), 4 no-ops
+            assert s.stats().step_index == 6
+            s.step(8)                            # max_steps mode again
+            T1, _ = s.fields(False)
+            s.set_temperature(case.setup.initial_T)
+            s.step(3, t_end=1.5 * dt)            # 2 real steps, 1 no-op
+            s.set_temperature(case.setup.initial_T)
+            s.step(5)
+            T2, _ = s.fields(False)
+            out[mode] = (T1, T2)
+    for a, b in zip(out["atomic"], out["deterministic"]):
+        assert float(np.max(np.abs(a - b) / np.abs(b))) <= 1e-9

@@ -248,3 +248,15 @@ def test_binary_mesh_errors():
     bad_tet[off:off + 4] = (10 ** 6).to_bytes(4, "little")
     with pytest.raises(cf.ValidationError, match="mesh validation failed"):
         cf.parse_mesh_binary(bytes(bad_tet))
+
+
+def test_binary_mesh_header_counts_bounded_by_buffer():
+    """A 48-byte header announcing INT32_MAX nodes/tets is rejected as truncated before any
+    section is allocated (no multi-GB resize on a malformed file)."""
+    import struct
+    hdr = b"CFMESHB1" + struct.pack("<5q", 2**31 - 1, 2**31 - 1, 0, 0, 0)
+    import time
+    t0 = time.time()
+    with pytest.raises(cf.ParseError, match="truncated"):
+        cf.parse_mesh_binary(hdr)
+    assert time.time() - t0 < 1.0

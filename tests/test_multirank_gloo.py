@@ -119,3 +119,53 @@ def test_gloo_exchange_matches_oracle(world):
         nodes, T = out[r]
         assert np.array_equal(T, ref.T[nodes]), np.abs(T - ref.T[nodes]).max()
         assert np.max(np.abs(T - single.T[nodes]) / single.T[nodes]) < 1e-14
+
+
+def _host_comm_worker(rank, world, port, out):
+    """The product's host-staged transport callbacks (castfem.HostComm, the functions the library
+    calls from cf_step) driven directly with payloads of the exchange plan's shape."""
+    sys.path.insert(0, ROOT)
+    import ctypes as C
+
+    import torch.distributed as dist
+
+    from paper_1005_3158_b200 import castfem as cf
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    comm = cf.HostComm(world, rank, 0)
+    sendrecv, allreduce = comm._cb
+    peers = [q for q in range(world) if q != rank]
+    n = len(peers)
+    send = [np.arange(5 + q, dtype=np.float64) + 100 * rank + 10 * q for q in peers]   # rank -> q
+    recv = [np.full(5 + rank, np.nan) for q in peers]                                    # q -> rank
+    dp = C.POINTER(C.c_double)
+    rc = sendrecv(None, n, (C.c_int32 * n)(*peers), (dp * n)(*[a.ctypes.data_as(dp) for a in send]),
+                  (C.c_int64 * n)(*[a.size for a in send]), (dp * n)(*[a.ctypes.data_as(dp) for a in recv]),
+                  (C.c_int64 * n)(*[a.size for a in recv]))
+    vals = np.array([float(rank + 1), -float(rank)])
+    rc2 = allreduce(None, vals[:1].ctypes.data_as(dp), 1, 0)  # min
+    rc3 = allreduce(None, vals[1:].ctypes.data_as(dp), 1, 1)  # max
+    out[rank] = (rc, rc2, rc3, [r.tolist() for r in recv], vals.tolist())
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_comm_callbacks(world):
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_host_comm_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    for r in range(world):
+        rc, rc2, rc3, recv, vals = out[r]
+        assert (rc, rc2, rc3) == (0, 0, 0)
+        peers = [q for q in range(world) if q != r]
+        for q, got in zip(peers, recv):
+            assert got == (np.arange(5 + r, dtype=np.float64) + 100 * q + 10 * r).tolist()
+        assert vals == [1.0, 0.0]

@@ -223,3 +223,71 @@ def test_kat_conservation_adiabatic():  # sum C (T' - T) = 0, no boun
     Cn = np.zeros(c.mesh.node_count())
     np.add.at(Cn, tets.reshape(-1), np.repeat(2700.0 * 900.0 * V / 4, 4))
     assert abs(np.sum(Cn * (o.T - T0))) <= 1e-12 * np.sum(Cn * T0)
+
+
+# ---------------------------------------------------------------- the reference arm's own workload generator
+@pytest.mark.parametrize("kind,n,radius,jitter,seed,perm", [("cube", 5, 0.35, 0.0, 0, 0), ("casting", 8, 0.35, 0.0, 0, 0),
+                                                            ("casting", 9, 0.35, 0.2, 3, 5),
+                                                            ("casting", 10, 0.3, 0.1, 2, 0)])
+def test_oracle_fixture_generator_equals_product(kind, n, radius, jitter, seed, perm):
+    """oracle/fixture.c (used by the reference arm, which must not load the product library)
+    reproduces the product's cf_generate_fixture bit for bit, including the non-integer
+    radius path, jitter keys and the node / element permutations; a full window is the mesh."""
+    p = cf.generate_fixture(kind, n, radius=radius, jitter=jitter, seed=seed, perm_seed=perm)
+    for window in (None, [0, n, 0, n, 0, n]):
+        o = orc.generate_fixture(kind, n, radius, jitter, seed, perm, window=window)
+        assert np.array_equal(o["nodes"], p.nodes)
+        assert np.array_equal(o["tets"], p.tets) and np.array_equal(o["region"], p.region)
+        assert np.array_equal(o["facets"], p.facets) and np.array_equal(o["facet_tag"], p.facet_tag)
+        assert np.array_equal(o["node_grid"], p.node_grid)
+    keys = np.arange(1000, dtype=np.int64) * 7919
+    assert np.array_equal(orc.counter_uniform(1, keys, -1.0, 1.0), cf.counter_uniform(1, keys, -1.0, 1.0))
+
+
+def test_oracle_fixture_window_is_a_box_of_the_mesh():
+    """A window keeps the full mesh's coordinates, regions and global grid keys; facets only on
+    the box boundary and the cast/mould interface (cut planes are adiabatic)."""
+    n, w = 16, [2, 14, 0, 16, 5, 9]
+    full = orc.generate_fixture("casting", n, jitter=0.2, seed=3)
+    win = orc.generate_fixture("casting", n, jitter=0.2, seed=3, window=w)
+    cells = (w[1] - w[0]) * (w[3] - w[2]) * (w[5] - w[4])
+    assert win["tets"].shape[0] == 6 * cells
+    P = n + 1
+    g = win["node_grid"]
+    gi, gj, gk = g % P, (g // P) % P, g // (P * P)
+    assert gi.min() == w[0] and gi.max() == w[1] and gk.min() == w[4] and gk.max() == w[5]
+    pos = {int(a): full["nodes"][i] for i, a in enumerate(full["node_grid"])}
+    assert all(np.array_equal(win["nodes"][i], pos[int(g[i])]) for i in range(0, len(g), 37))
+    fx = win["nodes"][win["facets"]]  # (F, 3, 3)
+    outer = win["facet_tag"] == 0
+    on_box = np.any(np.all(np.isclose(fx, 0.0) | np.isclose(fx, 1.0), axis=1), axis=1)
+    assert on_box[outer].all()
+    assert np.bincount(win["facet_tag"], minlength=3)[1] == np.bincount(win["facet_tag"], minlength=3)[2]
+
+
+@needs_ref
+def test_ref_bench_workloads_equal_the_product_configs():
+    """oracle/_ref/ref_bench (the reference arm) builds BASELINE's workloads exactly like
+    paper_1005_3158_b200/configs.py: same mesh counts, dt_safety, h_i and initial field."""
+    for name in ("cfg1", "cfg2", "cfg3"):
+        d = orc.ref_bench(name, describe=True)
+        case = configs.CONFIGS[name]()
+        assert d["elements"] == case.mesh.element_count() and d["nodes"] == case.mesh.node_count()
+        assert d["facets"] == case.mesh.facets.shape[0]
+        assert d["dt_safety"] == case.setup.solver.dt_safety == configs.DT_SAFETY[name]
+        assert d["h_interface"] == configs.H_INTERFACE
+        assert d["T0_sum"] == float(np.cumsum(case.setup.initial_T)[-1])
+    for name in ("cfg4", "cfg5"):  # too large to generate here: the constants
+        d = orc.ref_bench(name, describe=True, window=[0, 8, 0, 8, 0, 8])
+        assert d["dt_safety"] == configs.DT_SAFETY[name]
+
+
+@needs_ref
+def test_ref_bench_steps_equal_reference_solve(tmp_path):
+    """The reference arm's timed loop is the reference solver: 5 steps of cfg1 and of a 24^3
+    casting window through ref_bench equal ref_solve on the product-generated mesh bit for bit."""
+    dump = str(tmp_path / "T.bin")
+    orc.ref_bench("cfg1", steps=4, warmup=1, dump_T=dump)
+    case = configs.config1()
+    r, _ = orc.ref_solve(case.mesh, case.setup, 5)
+    assert np.array_equal(np.fromfile(dump), r.T)

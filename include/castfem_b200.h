@@ -307,6 +307,11 @@ int cf_comm_create_host(int32_t world_size, int32_t rank, int32_t device,
 /* rcm_permutation (reorder.hpp:127-148) over build_node_graph (:17-24):
  * new_of_old[n_nodes]. seed < 0 = pseudo-peripheral start per component. */
 int cf_rcm_permutation(const cf_mesh_desc* mesh, int32_t seed, int32_t* new_of_old);
+/* The same permutation computed on the B200 `device` (the RCM pass of the plan builder):
+ * node graph built on the device from the tets, level-synchronous Cuthill-McKee in which each
+ * level's order is (first-discovering parent position, degree, id) -- equal to rcm_permutation
+ * element for element. Used by cf_plan_create for CF_NODE_ORDER_RCM. */
+int cf_rcm_permutation_device(const cf_mesh_desc* mesh, int32_t seed, int32_t device, int32_t* new_of_old);
 /* bandwidth (reorder.hpp:41-48); new_of_old NULL = identity. */
 int cf_bandwidth(const cf_mesh_desc* mesh, const int32_t* new_of_old, int64_t* out);
 

@@ -116,6 +116,7 @@ SIGNATURES = [
                                       C.POINTER(C.c_void_p)]),
     ("cf_comm_destroy", C.c_int, [C.c_void_p]),
     ("cf_rcm_permutation", C.c_int, [C.POINTER(cf_mesh_desc), C.c_int32, _ip]),
+    ("cf_rcm_permutation_device", C.c_int, [C.POINTER(cf_mesh_desc), C.c_int32, C.c_int32, _ip]),
     ("cf_bandwidth", C.c_int, [C.POINTER(cf_mesh_desc), _ip, C.POINTER(C.c_int64)]),
     ("cf_finalize_mesh", C.c_int, [C.POINTER(cf_mesh_desc), _ip, _ip]),
     ("cf_pair_sister_facets", C.c_int, [C.POINTER(cf_mesh_desc), _ip, C.c_int64, C.POINTER(C.c_int64)]),

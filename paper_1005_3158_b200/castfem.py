@@ -548,6 +548,15 @@ def rcm_permutation(m: Mesh, seed: int = -1) -> np.ndarray:
     return out
 
 
+def rcm_permutation_device(m: Mesh, seed: int = -1, device: int = 0) -> np.ndarray:
+    """The same permutation computed on the B200 (the plan builder's RCM pass, cf_rcm.cu)."""
+    keep = _Keep()
+    d = mesh_desc(m, keep)
+    out = np.zeros(m.node_count(), np.int32)
+    check(lib().cf_rcm_permutation_device(C.byref(d), int(seed), int(device), out.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out
+
+
 def bandwidth(m: Mesh, new_of_old: Optional[np.ndarray] = None) -> int:
     keep = _Keep()
     d = mesh_desc(m, keep)

@@ -26,6 +26,12 @@ using namespace cfb;
 // ------------------------------------------------------------------ errors
 namespace cfb {
 static thread_local std::string g_last_error;
+bool cuda_device_present() {
+    int n = 0;
+    const bool ok = cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+    cudaGetLastError();
+    return ok;
+}
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 }  // namespace cfb
 
@@ -1187,8 +1193,7 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
 
         std::vector<int32_t> label(m.N);
         if (o.node_order == CF_NODE_ORDER_RCM) {
-            const Graph g = build_node_graph(m.N, m.E, m.tets.data());
-            label = rcm_permutation(g, -1);
+            label = rcm_permutation_device(m.N, m.E, m.tets.data(), -1, o.device);  // the RCM pass on the B200
         } else {
             std::iota(label.begin(), label.end(), 0);
         }
@@ -1722,6 +1727,17 @@ int cf_rcm_permutation(const cf_mesh_desc* d, int32_t seed, int32_t* out) {
     });
 }
 
+int cf_rcm_permutation_device(const cf_mesh_desc* d, int32_t seed, int32_t device, int32_t* out) {
+    return guarded([&] {
+        if (!d || !out) raise(CF_INVALID_ARG, "null argument");
+        if (d->n_nodes < 0 || d->n_elems < 0) raise(CF_INVALID_ARG, "negative size");
+        for (int64_t k = 0; k < 4 * (int64_t)d->n_elems; ++k)
+            if (d->tets[k] < 0 || d->tets[k] >= d->n_nodes) raise(CF_VALIDATION, "tet node id out of range");
+        const auto p = rcm_permutation_device(d->n_nodes, d->n_elems, d->tets, seed, device);
+        std::memcpy(out, p.data(), sizeof(int32_t) * p.size());
+    });
+}
+
 int cf_bandwidth(const cf_mesh_desc* d, const int32_t* perm, int64_t* out) {
     return guarded([&] {
         if (!d || !out) raise(CF_INVALID_ARG, "null argument");
@@ -1772,8 +1788,9 @@ int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_r
         SetupData S;
         resolve_setup(m, setup, S);
         std::vector<int32_t> label(m.N);
-        if (opts->node_order == CF_NODE_ORDER_RCM)
-            label = rcm_permutation(build_node_graph(m.N, m.E, m.tets.data()), -1);
+        if (opts->node_order == CF_NODE_ORDER_RCM)  // the plan's own pass where a B200 is present
+            label = cuda_device_present() ? rcm_permutation_device(m.N, m.E, m.tets.data(), -1, opts->device)
+                                          : rcm_permutation(build_node_graph(m.N, m.E, m.tets.data()), -1);
         else
             std::iota(label.begin(), label.end(), 0);
         PlanOptions po;

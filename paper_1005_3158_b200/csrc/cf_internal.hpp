@@ -99,6 +99,10 @@ Graph build_node_graph(int32_t N, int32_t E, const int32_t* tets);
 // rcm_permutation reorder.hpp:127-148 (exact order reproduction).
 std::vector<int32_t> rcm_permutation(const Graph& g, int32_t seed);
 int64_t bandwidth(const Graph& g, const int32_t* new_of_old);
+// The same permutation computed on the B200 (cf_rcm.cu): device node graph + level-synchronous
+// Cuthill-McKee with first-discoverer claims; equal to rcm_permutation.
+std::vector<int32_t> rcm_permutation_device(int32_t N, int64_t E, const int32_t* tets, int32_t seed, int device);
+bool cuda_device_present();
 
 // Recursive coordinate bisection along the longest axis.
 std::vector<int32_t> partition_rcb(const MeshData& m, int32_t parts);

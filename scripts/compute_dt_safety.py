@@ -13,8 +13,8 @@ from paper_1005_3158_b200 import configs  # noqa: E402
 
 ITERS = int(os.environ.get("LAMBDA_ITERS", "3000"))
 out = {}
-for name, make in [("cfg1", lambda: configs.config1(32)), ("cfg3", lambda: configs.config3()),
-                   ("cfg2", lambda: configs.config2()), ("cfg4", lambda: configs.config4())]:
+names = sys.argv[1:] or ["cfg1", "cfg3", "cfg2", "cfg4", "cfg5"]
+for name, make in [(k, configs.CONFIGS[k]) for k in names]:
     t0 = time.time()
     case = make()
     with cf.Solver(case.mesh, case.setup, cf.SolveOptions(max_steps=0)) as s:

@@ -60,7 +60,11 @@ def parse():
     ap.add_argument("--elem-order", default="morton")
     ap.add_argument("--geometry", default="stored", choices=["stored", "coords"],
                     help="tile layout: slot coordinates (gradients recomputed) or stored ElementGeom")
-    ap.add_argument("--node-order", default="tile")
+    ap.add_argument("--node-order", default="rcm",
+                    help="rcm: BASELINE configs[1] ('RCM-reordered'; configs[4] = config 2's setup), by the "
+                         "device RCM pass; tile: first touch in tile order; given")
+    ap.add_argument("--compare-order", default="tile",
+                    help="a second node ordering measured side by side (K steps, same mesh); 'none' to skip")
     ap.add_argument("--cpu-steps", type=int, default=int(os.environ.get("CF_CPU_STEPS", "5")))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-blocked", action="store_true",
@@ -343,7 +347,14 @@ def main():
                 "kernel_ms": round(ph[0], 4), "update_ms": round(ph[3], 4), "pack_ms": round(ph[1], 4),
                 "exchange_ms": round(ph[2], 4), "step_achieved_gbs": round(step_gbs, 1),
                 "step_frac_of_8tbs": round(step_gbs / 8000.0, 4), "step_frac": round(step_gbs / peak, 4),
-                "canonical_bytes_per_step": int(st.bytes_per_step)}
+                "canonical_bytes_per_step": int(st.bytes_per_step),
+                # the merge + update kernel's own byte model: per merged node its
+                # record + T read/write, per partial the 16 B read + 8 B slot-copy write
+                "update_kernel": {"algorithmic_bytes": int(st.update_bytes_per_step),
+                                  "achieved_gbs": round(st.update_bytes_per_step / (ph[3] * 1e-3) / 1e9, 1)
+                                  if ph[3] > 0 else None,
+                                  "frac": round(st.update_bytes_per_step / (ph[3] * 1e-3) / 1e9 / peak, 4)
+                                  if ph[3] > 0 else None}}
 
     # e2e through the public API with host buffers
     e2e = None
@@ -374,6 +385,26 @@ def main():
                "seconds": e_secs, "host_buffers": "pinned",
                "api": "Solver.set_temperature -> Solver.step(K) -> Solver.fields()"}
 
+    solver.close()
+    # the other node ordering, side by side (node numbering leaves every result bitwise unchanged:
+    # only the locality of the node arrays differs)
+    order_cmp = None
+    if args.compare_order not in ("none", "", args.node_order):
+        o2 = cf.SolveOptions(**{**opts.__dict__, "node_order": args.compare_order})
+        t2 = time.time()
+        s2 = cf.Solver(mesh, setup, o2)
+        setup2 = time.time() - t2
+        s2.step(max(args.warmup, 3))
+        barrier()
+        b2 = s2.stats().loop_seconds
+        s2.step(args.steps)
+        secs2 = max_over_ranks(s2.stats().loop_seconds - b2)
+        ph2 = s2.time_phases(args.phase_steps)
+        order_cmp = {"node_order": args.compare_order, "value": E_total * args.steps / secs2,
+                     "ms_per_step": 1e3 * secs2 / args.steps, "kernel_ms": round(ph2[0], 4),
+                     "update_ms": round(ph2[3], 4), "setup_seconds": round(setup2, 2)}
+        s2.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -401,9 +432,9 @@ def main():
                 "host_peak_rss_gb": round(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20, 2),
                 "total_slots": int(st.total_slots),
                 "env": {k: v for k, v in sorted(os.environ.items()) if k.startswith("CF_")},
-                "build": "production (probe branches compiled out: no CF_DIAG)"}
+                "build": "production (probe branches compiled out: no CF_DIAG)",
+                "node_order_comparison": order_cmp}
         print(json.dumps(line), flush=True)
-    solver.close()
     if comm:
         comm.close()
     if pg:

@@ -191,6 +191,9 @@ typedef struct cf_stats {
     int64_t launches_per_step; /* kernels launched per step */
     int64_t tile_bytes_per_launch; /* this layout's tile-kernel bytes per launch: blobs + slot T
                                       reads + 16 B of output per slot (partial or T + slot copy) */
+    int64_t update_bytes_per_step; /* merge + update kernel's algorithmic bytes per step: per merged
+                                      node its record (32 B), T read + write (16 B), and per partial
+                                      the 16 B read + the 8 B slot-copy write */
 } cf_stats;
 
 /* ---------------------------------------------------------------------------

@@ -51,7 +51,7 @@ const Workload kWorkloads[] = {
     {"cfg2", 1, 128, 0.0, 0, 0, 0.14355290898864603, 1000},
     {"cfg3", 1, 70, 0.2, 7, 11, 0.12107620380138684, 500},
     {"cfg4", 1, 256, 0.0, 0, 0, 0.14434666132619436, 500},
-    {"cfg5", 1, 512, 0.0, 0, 0, 0.14434666132619436, 200},
+    {"cfg5", 1, 512, 0.0, 0, 0, 0.14472535840047063, 200},
 };
 constexpr double kRadius = 0.35, kHInterface = 1000.0, kNoise = 1.0;
 constexpr uint64_t kNoiseSeed = 1;

@@ -71,7 +71,7 @@ class cf_stats(C.Structure):
                 ("n_tiles", C.c_int32), ("n_elems_local", C.c_int64), ("n_nodes_local", C.c_int64),
                 ("total_slots", C.c_int64), ("n_shared_nodes", C.c_int64), ("n_ghost_nodes", C.c_int64),
                 ("device_bytes", C.c_int64), ("bytes_per_step", C.c_int64), ("launches_per_step", C.c_int64),
-                ("tile_bytes_per_launch", C.c_int64)]
+                ("tile_bytes_per_launch", C.c_int64), ("update_bytes_per_step", C.c_int64)]
 
 
 class cf_tune_report(C.Structure):

@@ -227,6 +227,7 @@ struct Rank {
     int upd_blocks = 0, upd_blocks_all = 0;
     int64_t bytes_per_step = 0;
     int64_t tile_bytes = 0;  // layout bytes of one tile-kernel launch
+    int64_t update_bytes = 0;  // algorithmic bytes of the merge + update kernel per step
     std::vector<int64_t> nb_send_len, nb_recv_len;
 };
 
@@ -883,6 +884,20 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     // canonical algorithmic bytes: 105 E + 48 N + 24 F_bc + 56 F_if
     r.bytes_per_step = 105 * Er + 48 * (int64_t)h.n_local + 24 * h.n_bc_facets + 56 * h.n_if_facets;
     r.tile_bytes = (h.blob_off.empty() ? 0 : h.blob_off.back()) + (8 + 16) * S_tot;
+    {
+        // update kernel: per merged node its 32 B record (or CSR offsets), T read + Tn write, per
+        // partial a 16 B read (deterministic; atomic: the node's two accumulators read + zeroed)
+        // and the 8 B slot-copy write
+        const bool all = p->temp_dep;
+        const int64_t nodes = all ? h.n_local : (int64_t)h.shared_list.size();
+        int64_t parts = 0;
+        if (all) {
+            parts = S_tot;
+        } else {
+            for (int32_t i : h.shared_list) parts += h.merge_off[i + 1] - h.merge_off[i];
+        }
+        r.update_bytes = nodes * (32 + 16) + parts * 8 + (det ? parts * 16 : nodes * 32);
+    }
     CF_CUDA_CHECK(cudaStreamSynchronize(s));
     // drop the big host arrays (metadata kept)
     decltype(h.blob)().swap(h.blob);
@@ -1521,6 +1536,7 @@ int cf_get_stats(cf_plan* p, cf_stats* out) {
             out->device_bytes += r->mem.bytes;
             out->bytes_per_step += r->bytes_per_step;
             out->tile_bytes_per_launch += r->tile_bytes;
+            out->update_bytes_per_step += r->update_bytes;
         }
         out->launches_per_step = p->launches_per_step;
     });

@@ -142,7 +142,9 @@ enum {
 };
 enum {
     CF_PARTITION_RCB = 0,      /* recursive coordinate bisection along the longest axis */
-    CF_PARTITION_GIVEN = 1     /* part_of_element supplied (load_partmap partition.hpp:424-445) */
+    CF_PARTITION_GIVEN = 1,    /* part_of_element supplied (load_partmap partition.hpp:424-445) */
+    CF_PARTITION_GRAPH = 2     /* the reference's greedy graph partitioner over the virtual-element
+                                  augmented dual graph (cf_partition_graph; balance_tol 0.05) */
 };
 
 typedef struct cf_run_opts {
@@ -328,6 +330,19 @@ int cf_pair_sister_facets(const cf_mesh_desc* mesh, int32_t* out, int64_t cap, i
 
 /* Recursive coordinate bisection along the longest axis: part_of_element[E]. */
 int cf_partition_rcb(const cf_mesh_desc* mesh, int32_t parts, int32_t* part_of_element);
+
+/* Graph partitioning for unstructured decoupled meshes (paper 4.1.1): the reference's greedy
+ * graph-growing partitioner (partition_graph partition.hpp:134-232) over the element dual graph
+ * (build_dual_graph mesh.hpp:119-126), with augment != 0 first gluing the decoupled regions by one
+ * zero-weight virtual element per cast-side interface pair (augment_virtual_elements
+ * partition.hpp:43-91; partition_elements :236-241). Equal to the reference's partition. */
+int cf_partition_graph(const cf_mesh_desc* mesh, int32_t parts, double balance_tol, int32_t augment,
+                       int32_t* part_of_element);
+/* partition_metrics (partition.hpp:250-272): edge cut and imbalance over the dual graph,
+ * neighbor_counts[parts]; count_split_interface_pairs (:276-283). Any output may be NULL. */
+int cf_partition_metrics(const cf_mesh_desc* mesh, const int32_t* part_of_element, int32_t parts,
+                         int64_t* edge_cut, double* imbalance, int32_t* neighbor_counts,
+                         int64_t* split_interface_pairs);
 
 /* The tiles a plan would build (element -> tile map, in the plan's tile
  * order; for rank `rank` of a world of `world_size`, -1 for other ranks'

@@ -102,6 +102,11 @@ def ref_lib():
         for f in (L.ref_mesh_roundtrip, L.ref_config_dump):
             f.restype = C.c_int
             f.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
+        L.ref_partition.restype = C.c_int
+        L.ref_partition.argtypes = [C.POINTER(_abi.cf_mesh_desc), C.c_int32, C.c_double, C.c_int32, _ip]
+        L.ref_partition_metrics.restype = C.c_int
+        L.ref_partition_metrics.argtypes = [C.POINTER(_abi.cf_mesh_desc), _ip, C.c_int32, C.POINTER(C.c_int64), _dp,
+                                            _ip, C.POINTER(C.c_int64)]
         L.ref_load_partmap.restype = C.c_int
         L.ref_load_partmap.argtypes = [C.c_char_p, C.c_int64, C.c_int32, _ip, C.POINTER(C.c_int32)]
         _r = L

@@ -14,6 +14,7 @@
 // index-keyed T0, which solve_serial's position-keyed
 // initial_override hook cannot express for duplicated interface nodes.
 #include <castfem/blocked.hpp>
+#include <castfem/partition.hpp>
 #include <castfem/reorder.hpp>
 
 #include <chrono>
@@ -417,6 +418,45 @@ __attribute__((visibility("default"))) int ref_load_partmap(const char* text, in
         const PartMap pm = load_partmap(in, n_elems);
         for (idx e = 0; e < n_elems; ++e) out[e] = pm.part_of_element[e];
         *count = pm.part_count;
+        return CF_OK;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// partition_elements(augment_virtual_elements(...)) (partition.hpp:43-91, 236-241) or plain
+// partition_graph over build_dual_graph (augment == 0)
+__attribute__((visibility("default"))) int ref_partition(const cf_mesh_desc* md, int32_t k, double tol,
+                                                         int32_t augment, int32_t* out) {
+    try {
+        const Mesh m = to_mesh(md);
+        PartMap pm;
+        if (augment) {
+            const auto pairs = pair_sister_facets(m);
+            pm = partition_elements(augment_virtual_elements(m, pairs), k, tol);
+        } else {
+            const AdjacencyGraph g = build_dual_graph(m);
+            pm = partition_graph(g, {}, k, tol);
+        }
+        for (idx e = 0; e < m.element_count(); ++e) out[e] = pm.part_of_element[e];
+        return CF_OK;
+    } catch (...) {
+        return map_exception();
+    }
+}
+__attribute__((visibility("default"))) int ref_partition_metrics(const cf_mesh_desc* md, const int32_t* part,
+                                                                 int32_t k, int64_t* cut, double* imb,
+                                                                 int32_t* nb, int64_t* split) {
+    try {
+        const Mesh m = to_mesh(md);
+        PartMap pm;
+        pm.part_count = k;
+        pm.part_of_element.assign(part, part + m.element_count());
+        const PartitionQuality q = partition_metrics(build_dual_graph(m), pm);
+        *cut = q.edge_cut;
+        *imb = q.imbalance;
+        for (idx p = 0; p < k; ++p) nb[p] = q.neighbor_counts[p];
+        *split = count_split_interface_pairs(m, pair_sister_facets(m), pm);
         return CF_OK;
     } catch (...) {
         return map_exception();

@@ -19,7 +19,7 @@ CF_MODE_ATOMIC, CF_MODE_DETERMINISTIC = 0, 1
 CF_NODE_ORDER_GIVEN, CF_NODE_ORDER_RCM, CF_NODE_ORDER_TILE = 0, 1, 2
 CF_ELEM_ORDER_GIVEN, CF_ELEM_ORDER_MORTON, CF_ELEM_ORDER_MIN_NODE = 0, 1, 2
 CF_GEOM_STORED, CF_GEOM_COORDS = 0, 1
-CF_PARTITION_RCB, CF_PARTITION_GIVEN = 0, 1
+CF_PARTITION_RCB, CF_PARTITION_GIVEN, CF_PARTITION_GRAPH = 0, 1, 2
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -121,6 +121,9 @@ SIGNATURES = [
     ("cf_finalize_mesh", C.c_int, [C.POINTER(cf_mesh_desc), _ip, _ip]),
     ("cf_pair_sister_facets", C.c_int, [C.POINTER(cf_mesh_desc), _ip, C.c_int64, C.POINTER(C.c_int64)]),
     ("cf_partition_rcb", C.c_int, [C.POINTER(cf_mesh_desc), C.c_int32, _ip]),
+    ("cf_partition_graph", C.c_int, [C.POINTER(cf_mesh_desc), C.c_int32, C.c_double, C.c_int32, _ip]),
+    ("cf_partition_metrics", C.c_int, [C.POINTER(cf_mesh_desc), _ip, C.c_int32, C.POINTER(C.c_int64), _dp, _ip,
+                                       C.POINTER(C.c_int64)]),
     ("cf_tile_map", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts), _ip,
                               _ip]),
     ("cf_exchange_plan", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts), _ip,

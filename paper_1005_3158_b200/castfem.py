@@ -194,6 +194,7 @@ class SolveOptions:
     rank: int = 0
     local_ranks: int = 1
     part_of_element: Optional[np.ndarray] = None
+    partition: str = "rcb"           # 'rcb' | 'graph' (virtual-element augmented greedy partitioner)
     comm: Optional["Comm"] = None    # Comm (NCCL) or HostComm (host-staged) for world_size > local_ranks
     graph_steps: int = 0
 
@@ -322,6 +323,8 @@ def run_opts(o: SolveOptions, keep: _Keep) -> _abi.cf_run_opts:
     if o.part_of_element is not None:
         d.partition = _abi.CF_PARTITION_GIVEN
         d.part_of_element = keep.iptr(o.part_of_element)
+    elif o.partition == "graph":
+        d.partition = _abi.CF_PARTITION_GRAPH
     d.comm = o.comm.handle if o.comm is not None else None
     return d
 
@@ -587,6 +590,37 @@ def partition_rcb(m: Mesh, parts: int) -> np.ndarray:
     out = np.zeros(m.element_count(), np.int32)
     check(lib().cf_partition_rcb(C.byref(d), int(parts), out.ctypes.data_as(C.POINTER(C.c_int32))))
     return out
+
+
+def partition_elements(m: Mesh, parts: int, balance_tol: float = 0.05, augment: bool = True) -> np.ndarray:
+    """Graph partition of the elements (partition_graph partition.hpp:134-232 over the dual graph,
+    augmented with virtual elements across interface pairs when `augment`)."""
+    keep = _Keep()
+    d = mesh_desc(m, keep)
+    out = np.zeros(m.element_count(), np.int32)
+    check(lib().cf_partition_graph(C.byref(d), int(parts), float(balance_tol), int(bool(augment)),
+                                   out.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out
+
+
+@dataclass
+class PartitionQuality:
+    edge_cut: int
+    imbalance: float
+    neighbor_counts: List[int]
+    split_interface_pairs: int
+
+
+def partition_metrics(m: Mesh, parts_of_element: np.ndarray, parts: int) -> PartitionQuality:
+    """partition_metrics + count_split_interface_pairs (partition.hpp:250-283)."""
+    keep = _Keep()
+    d = mesh_desc(m, keep)
+    cut, split = C.c_int64(), C.c_int64()
+    imb = C.c_double()
+    nb = np.zeros(max(1, parts), np.int32)
+    check(lib().cf_partition_metrics(C.byref(d), keep.iptr(parts_of_element), int(parts), C.byref(cut), C.byref(imb),
+                                     nb.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(split)))
+    return PartitionQuality(cut.value, imb.value, nb[:parts].tolist(), split.value)
 
 
 def tile_map(m: Mesh, setup: SimulationSetup, opts: SolveOptions) -> Tuple[np.ndarray, int]:

@@ -1228,6 +1228,8 @@ int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
                 part.assign(o.part_of_element, o.part_of_element + m.E);
                 for (int32_t v : part)
                     if (v < 0 || v >= o.world_size) raise(CF_VALIDATION, "part id out of range");
+            } else if (o.partition == CF_PARTITION_GRAPH) {
+                part = partition_elements(m, o.world_size, 0.05, true);
             } else {
                 part = partition_rcb(m, o.world_size);
             }
@@ -1795,6 +1797,33 @@ int cf_partition_rcb(const cf_mesh_desc* d, int32_t parts, int32_t* out) {
     });
 }
 
+int cf_partition_graph(const cf_mesh_desc* d, int32_t parts, double balance_tol, int32_t augment, int32_t* out) {
+    return guarded([&] {
+        if (!d || !out) raise(CF_INVALID_ARG, "null argument");
+        MeshData m;
+        finalize_mesh(d, m);
+        const auto p = partition_elements(m, parts, balance_tol, augment != 0);
+        std::memcpy(out, p.data(), sizeof(int32_t) * p.size());
+    });
+}
+
+int cf_partition_metrics(const cf_mesh_desc* d, const int32_t* part, int32_t parts, int64_t* edge_cut,
+                         double* imbalance, int32_t* neighbor_counts, int64_t* split_interface_pairs) {
+    return guarded([&] {
+        if (!d || !part) raise(CF_INVALID_ARG, "null argument");
+        if (parts < 1) raise(CF_VALIDATION, "part count must be >= 1");
+        for (int32_t e = 0; e < d->n_elems; ++e)
+            if (part[e] < 0 || part[e] >= parts) raise(CF_VALIDATION, "part id out of range");
+        MeshData m;
+        finalize_mesh(d, m);
+        const PartitionQuality q = partition_metrics(m, part, parts);
+        if (edge_cut) *edge_cut = q.edge_cut;
+        if (imbalance) *imbalance = q.imbalance;
+        if (neighbor_counts) std::memcpy(neighbor_counts, q.neighbor_counts.data(), sizeof(int32_t) * parts);
+        if (split_interface_pairs) *split_interface_pairs = count_split_interface_pairs(m, part);
+    });
+}
+
 int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts,
                 int32_t* tile_of_element, int32_t* n_tiles) {
     return guarded([&] {
@@ -1820,7 +1849,8 @@ int cf_tile_map(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_r
         if (po.world_size > 1) {
             part = opts->partition == CF_PARTITION_GIVEN && opts->part_of_element
                        ? std::vector<int32_t>(opts->part_of_element, opts->part_of_element + m.E)
-                       : partition_rcb(m, po.world_size);
+                   : opts->partition == CF_PARTITION_GRAPH ? partition_elements(m, po.world_size, 0.05, true)
+                                                           : partition_rcb(m, po.world_size);
             po.part_of_element = part.data();
         }
         for (int32_t e = 0; e < m.E; ++e) tile_of_element[e] = -1;
@@ -1859,7 +1889,8 @@ int cf_exchange_plan(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const
         po.world_size = opts->world_size;
         std::vector<int32_t> part = opts->partition == CF_PARTITION_GIVEN && opts->part_of_element
                                         ? std::vector<int32_t>(opts->part_of_element, opts->part_of_element + m.E)
-                                        : partition_rcb(m, po.world_size);
+                                    : opts->partition == CF_PARTITION_GRAPH ? partition_elements(m, po.world_size, 0.05, true)
+                                                                            : partition_rcb(m, po.world_size);
         trace_stage("partition");
         po.part_of_element = part.data();
         RankPlan rp;

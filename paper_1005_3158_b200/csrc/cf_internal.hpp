@@ -107,6 +107,20 @@ bool cuda_device_present();
 // Recursive coordinate bisection along the longest axis.
 std::vector<int32_t> partition_rcb(const MeshData& m, int32_t parts);
 
+// Graph partitioning of decoupled meshes (cf_partition.cpp): partition_graph partition.hpp:134-232
+// over the dual graph (build_dual_graph mesh.hpp:119-126), optionally augmented with virtual
+// elements (augment_virtual_elements partition.hpp:43-91); quality metrics :243-283.
+struct PartitionQuality {
+    int64_t edge_cut = 0;
+    double imbalance = 1.0;
+    std::vector<int32_t> neighbor_counts;
+};
+Graph dual_graph(const MeshData& m);
+std::vector<int32_t> partition_graph(const Graph& g, const std::vector<int32_t>& weights, int32_t k, double tol);
+std::vector<int32_t> partition_elements(const MeshData& m, int32_t k, double tol, bool augment);
+PartitionQuality partition_metrics(const MeshData& m, const int32_t* part, int32_t k);
+int64_t count_split_interface_pairs(const MeshData& m, const int32_t* part);
+
 // Fixtures (SPEC bench module S:502-519).
 struct FixtureSizes {
     int32_t N, E, F;

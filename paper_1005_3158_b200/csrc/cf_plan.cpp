@@ -768,7 +768,9 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             std::vector<int64_t> srt = fp;
             const size_t q = (size_t)(0.95 * (double)(srt.size() - 1));
             std::nth_element(srt.begin(), srt.begin() + q, srt.end());
-            const int64_t budget = srt[q];
+            int64_t budget = srt[q];
+            // CF_SMEM_BUDGET=bytes caps it (e.g. so that 5 CTAs fit an SM's shared memory)
+            if (const char* e = std::getenv("CF_SMEM_BUDGET")) budget = std::min<int64_t>(budget, std::atoll(e));
             std::vector<std::vector<int32_t>> out;
             out.reserve(tiles.size() + tiles.size() / 16);
             std::vector<std::vector<int32_t>> stack;

@@ -353,3 +353,17 @@ def test_stepping_paths_share_the_dynamic_schedule():
     assert nt > 600  # more tiles than resident CTAs: the dynamic scheduler is active
     assert np.array_equal(T5, orc.solve(case.mesh, case.setup, 5, blocks=tiles).T)
     assert np.array_equal(T35, orc.solve(case.mesh, case.setup, 35, blocks=tiles).T)
+
+
+def test_multirank_graph_partition_vs_oracle():
+    """A decomposition by the reference's partitioner (greedy graph growing over the dual graph
+    glued by virtual interface elements, partition="graph") instead of RCB: 3 in-process ranks,
+    bitwise equal to the oracle replaying the same parts and tiles."""
+    case = configs.casting(12, jitter=0.2, seed=4, perm_seed=2, dt_safety=0.14)
+    parts = cf.partition_elements(case.mesh, 3)
+    opts = cf.SolveOptions(max_steps=25, tile_elems=192, world_size=3, local_ranks=3, partition="graph")
+    gpu = cf.solve(case.mesh, case.setup, opts)
+    tiles, _ = cf.tile_map(case.mesh, case.setup, opts)
+    assert np.array_equal(np.unique(parts), [0, 1, 2])
+    ref = orc.solve(case.mesh, case.setup, 25, blocks=tiles, parts=parts)
+    assert np.array_equal(gpu.T, ref.T), np.abs(gpu.T - ref.T).max()

@@ -194,3 +194,48 @@ def test_default_tile_candidates():
     assert cf.default_tile_candidates(12_582_912) == [192, 384, 768, 1536]
     assert cf.default_tile_candidates(100_000) == [192, 384]   # >= 148 tiles each
     assert cf.default_tile_candidates(1_000) == [192]          # always one candidate
+
+
+# ---------------------------------------------------------------- graph partitioning
+PART_MESHES = {
+    "casting8": lambda: cf.generate_fixture("casting", 8),
+    "jitter7_perm": lambda: cf.generate_fixture("casting", 7, jitter=0.2, seed=5, perm_seed=17),
+    "cube5_perm": lambda: cf.generate_fixture("cube", 5, perm_seed=3),
+}
+
+
+@needs_ref
+@pytest.mark.parametrize("name", sorted(PART_MESHES))
+@pytest.mark.parametrize("k,augment", [(2, True), (3, True), (5, False), (8, True)])
+def test_graph_partition_equals_reference(name, k, augment):
+    """partition_graph over the (virtual-element augmented) dual graph: the same part of every
+    element as the reference's partition_elements / partition_graph, and the same quality."""
+    m = PART_MESHES[name]()
+    ours = cf.partition_elements(m, k, 0.05, augment)
+    ref = np.zeros(m.element_count(), np.int32)
+    ref_call(orc.ref_lib().ref_partition, m, k, 0.05, int(augment), ref.ctypes.data_as(C.POINTER(C.c_int32)))
+    assert np.array_equal(ours, ref)
+    q = cf.partition_metrics(m, ours, k)
+    cut, split, imb = C.c_int64(), C.c_int64(), C.c_double()
+    nb = np.zeros(k, np.int32)
+    ref_call(orc.ref_lib().ref_partition_metrics, m, ours.ctypes.data_as(C.POINTER(C.c_int32)), k, C.byref(cut),
+             C.byref(imb), nb.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(split))
+    assert (q.edge_cut, q.imbalance, q.neighbor_counts, q.split_interface_pairs) == \
+        (cut.value, imb.value, nb.tolist(), split.value)
+
+
+def test_virtual_elements_keep_interface_pairs_together():
+    """The point of the augmentation (paper 4.1.1): fewer interface pairs split across parts."""
+    m = cf.generate_fixture("casting", 10)
+    plain = cf.partition_metrics(m, cf.partition_elements(m, 4, augment=False), 4)
+    aug = cf.partition_metrics(m, cf.partition_elements(m, 4, augment=True), 4)
+    assert aug.split_interface_pairs < plain.split_interface_pairs
+    assert aug.imbalance <= 1.06
+
+
+def test_partition_errors_like_reference():
+    m = cf.generate_fixture("cube", 2)
+    with pytest.raises(cf.ValidationError, match="requested 100 parts for 48 weighted elements"):
+        cf.partition_elements(m, 100)
+    with pytest.raises(cf.ValidationError):
+        cf.partition_metrics(m, np.full(m.element_count(), 7, np.int32), 2)

@@ -1257,6 +1257,23 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
         if (ntiles_of[l] == 1 && !shared_node[l]) rp.n_private++;
         else rp.shared_list.push_back(l);
     }
+    // the update kernel walks its nodes in the order of their first partial (the tile order), so
+    // consecutive threads read neighbouring partials and write neighbouring slot copies whatever
+    // the node numbering (RCM labels sweep a front across the mesh; first-touch numbering already
+    // follows the tiles, for which this order is the node order)
+    {
+        std::vector<std::pair<int64_t, int32_t>> key(rp.shared_list.size());  // first partials are unique
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < (int64_t)key.size(); ++k) {
+            const int32_t l = rp.shared_list[k];
+            key[k] = {rp.merge_off[l + 1] > rp.merge_off[l] ? (int64_t)rp.merge_idx[rp.merge_off[l]]
+                                                             : INT64_MAX - rp.n_local + l,
+                      l};
+        }
+        __gnu_parallel::sort(key.begin(), key.end());
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < (int64_t)key.size(); ++k) rp.shared_list[k] = key[k].second;
+    }
 
     trace_stage("plan: merge lists");
     // ---------------------------------------------------- multi-rank exchange

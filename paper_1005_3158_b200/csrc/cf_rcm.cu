@@ -186,24 +186,40 @@ struct DevBuf {
     }
 };
 
-// out[0..n) = exclusive scan of in[0..n), out[n] = total (out has n + 1 entries)
+// scan workspace for up to n_max elements: per recursion level the block sums and their offsets
+// (allocated once per RCM pass: the BFS scans every level)
+struct ScanWs {
+    std::vector<int64_t*> sums, offs;
+};
+ScanWs make_scan_ws(DevBuf& B, int64_t n_max) {
+    ScanWs w;
+    for (int64_t n = n_max;;) {
+        const int64_t blocks = std::max<int64_t>(1, (n + kScanTile - 1) / kScanTile);
+        w.sums.push_back(B.alloc<int64_t>(blocks + 1));
+        w.offs.push_back(B.alloc<int64_t>(blocks + 1));
+        if (blocks == 1) break;
+        n = blocks;
+    }
+    return w;
+}
+
+// out[0..n) = exclusive scan of in[0..n), out[n] = total (out has n + 1 entries); asynchronous
 template <class In>
-void exclusive_scan(const In* in, int64_t n, int64_t* out, cudaStream_t s) {
+void exclusive_scan(const In* in, int64_t n, int64_t* out, cudaStream_t s, const ScanWs& w, size_t lvl = 0) {
+    if (lvl >= w.sums.size()) raise(CF_INVALID_ARG, "rcm: scan workspace too small");
     const int64_t blocks = std::max<int64_t>(1, (n + kScanTile - 1) / kScanTile);
-    DevBuf B;
-    int64_t* sums = B.alloc<int64_t>(blocks + 1);
+    int64_t* sums = w.sums[lvl];
     scan_tiles<In><<<(unsigned)blocks, kScanThreads, 0, s>>>(n, in, out, sums);
     RCM_CHECK(cudaGetLastError());
     if (blocks > 1) {
-        int64_t* soff = B.alloc<int64_t>(blocks + 1);
-        exclusive_scan<int64_t>(sums, blocks, soff, s);
+        int64_t* soff = w.offs[lvl];
+        exclusive_scan<int64_t>(sums, blocks, soff, s, w, lvl + 1);
         scan_add<<<(unsigned)blocks, 256, 0, s>>>(n, out, soff);
         RCM_CHECK(cudaGetLastError());
         RCM_CHECK(cudaMemcpyAsync(out + n, soff + blocks, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
     } else {
         RCM_CHECK(cudaMemcpyAsync(out + n, sums, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
     }
-    RCM_CHECK(cudaStreamSynchronize(s));  // B's buffers are freed on return
 }
 
 // ---- BFS pieces
@@ -326,7 +342,8 @@ std::vector<int32_t> rcm_permutation_device(int32_t N, int64_t E, const int32_t*
     RCM_CHECK(cudaMemsetAsync(icnt, 0, (size_t)N * sizeof(int32_t), s));
     incidence_count<<<grid_for(4 * E), 256, 0, s>>>(E, tets, icnt);
     int64_t* ioff = B.alloc<int64_t>((size_t)N + 1);
-    exclusive_scan<int32_t>(icnt, N, ioff, s);
+    const ScanWs ws = make_scan_ws(B, N);
+    exclusive_scan<int32_t>(icnt, N, ioff, s, ws);
     int64_t* cursor = B.alloc<int64_t>((size_t)N + 1);
     RCM_CHECK(cudaMemcpyAsync(cursor, ioff, ((size_t)N + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
     int32_t* n2e = B.alloc<int32_t>(4 * (size_t)E);
@@ -336,9 +353,10 @@ std::vector<int32_t> rcm_permutation_device(int32_t N, int64_t E, const int32_t*
     graph_degree<<<grid_for(N, 128), 128, 0, s>>>(N, ioff, n2e, tets, deg);
     RCM_CHECK(cudaGetLastError());
     int64_t* goff = B.alloc<int64_t>((size_t)N + 1);
-    exclusive_scan<int32_t>(deg, N, goff, s);
+    exclusive_scan<int32_t>(deg, N, goff, s, ws);
     int64_t n_adj = 0;
-    RCM_CHECK(cudaMemcpy(&n_adj, goff + N, sizeof n_adj, cudaMemcpyDeviceToHost));
+    RCM_CHECK(cudaMemcpyAsync(&n_adj, goff + N, sizeof n_adj, cudaMemcpyDeviceToHost, s));
+    RCM_CHECK(cudaStreamSynchronize(s));
     int32_t* adj = B.alloc<int32_t>((size_t)n_adj);
     graph_fill<<<grid_for(N, 128), 128, 0, s>>>(N, ioff, n2e, tets, goff, adj);
     RCM_CHECK(cudaGetLastError());
@@ -360,11 +378,6 @@ std::vector<int32_t> rcm_permutation_device(int32_t N, int64_t E, const int32_t*
     unsigned long long* dbest = B.alloc<unsigned long long>(1);
     RCM_CHECK(cudaMemsetAsync(seen, 0, (size_t)N * sizeof(int32_t), s));
     RCM_CHECK(cudaMemsetAsync(claim, 0x7f, (size_t)N * sizeof(int32_t), s));  // 0x7f7f7f7f > any position
-    auto get_degree = [&](int32_t v) {
-        int64_t o[2];
-        RCM_CHECK(cudaMemcpy(o, goff + v, sizeof o, cudaMemcpyDeviceToHost));
-        return o[1] - o[0];
-    };
     // BFS over the whole component of `start` (set semantics) into dist; returns (depth, last level in fa/fb)
     auto bfs_sets = [&](int32_t start, int32_t*& last, int32_t& nlast) -> int64_t {
         RCM_CHECK(cudaMemsetAsync(dist, 0xff, (size_t)N * sizeof(int32_t), s));
@@ -410,7 +423,6 @@ std::vector<int32_t> rcm_permutation_device(int32_t N, int64_t E, const int32_t*
             node = (int32_t)(best & 0xffffffffu);
         }
     };
-    (void)get_degree;
 
     int64_t placed = 0;  // vertices in `order`
     int32_t v = 0;
@@ -429,15 +441,18 @@ std::vector<int32_t> rcm_permutation_device(int32_t N, int64_t E, const int32_t*
         v = found;
         int32_t root;
         int32_t in_seen = 1;
-        if (seed >= 0 && seed < N)
-            RCM_CHECK(cudaMemcpy(&in_seen, seen + seed, sizeof in_seen, cudaMemcpyDeviceToHost));
+        if (seed >= 0 && seed < N) {
+            RCM_CHECK(cudaMemcpyAsync(&in_seen, seen + seed, sizeof in_seen, cudaMemcpyDeviceToHost, s));
+            RCM_CHECK(cudaStreamSynchronize(s));
+        }
         if (seed >= 0 && seed < N && !in_seen) {
             // the seed is used if it lives in this (unvisited) component
             int32_t* last = nullptr;
             int32_t nlast = 0;
             bfs_sets(v, last, nlast);
             int32_t ds = -1;
-            RCM_CHECK(cudaMemcpy(&ds, dist + seed, sizeof ds, cudaMemcpyDeviceToHost));
+            RCM_CHECK(cudaMemcpyAsync(&ds, dist + seed, sizeof ds, cudaMemcpyDeviceToHost, s));
+            RCM_CHECK(cudaStreamSynchronize(s));
             root = ds >= 0 ? seed : pseudo_peripheral(v);
         } else {
             root = pseudo_peripheral(v);
@@ -452,9 +467,10 @@ std::vector<int32_t> rcm_permutation_device(int32_t N, int64_t E, const int32_t*
             const int32_t* front = order + ls;
             cm_claim<<<grid_for(nf), 256, 0, s>>>(nf, front, goff, adj, seen, claim);
             cm_count<<<grid_for(nf), 256, 0, s>>>(nf, front, goff, adj, seen, claim, cnt);
-            exclusive_scan<int32_t>(cnt, nf, loff, s);  // synchronises
+            exclusive_scan<int32_t>(cnt, nf, loff, s, ws);
             int64_t tot = 0;
-            RCM_CHECK(cudaMemcpy(&tot, loff + nf, sizeof tot, cudaMemcpyDeviceToHost));
+            RCM_CHECK(cudaMemcpyAsync(&tot, loff + nf, sizeof tot, cudaMemcpyDeviceToHost, s));
+            RCM_CHECK(cudaStreamSynchronize(s));
             if (tot == 0) break;
             cm_emit<<<grid_for(nf), 256, 0, s>>>(nf, front, goff, adj, deg, seen, claim, loff, order + le);
             RCM_CHECK(cudaGetLastError());

@@ -385,6 +385,14 @@ int cf_generate_fixture(int32_t kind, int32_t n, double radius, double jitter, u
 int cf_counter_uniform(uint64_t seed, const int64_t* keys, int64_t n, double lo, double hi,
                        double* out);
 
+/* Test instrumentation: FNV-1a digests of one rank's tiled plan, one per plan array
+ * (scalars, tile_meta, tile_border, tile_slot_off, blob_off, elem_off, staged blob sections,
+ * tets_ord, elem_global, slot_node, local_global, node_region, node_dir, merge_off, merge_idx,
+ * shared_list, neighbour lists, exchange tables), CF_DIGEST_LEN entries. Host plan builder. */
+#define CF_DIGEST_LEN 24
+int cf_plan_digest(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts,
+                   int32_t rank, uint64_t* digest);
+
 /* ---------------------------------------------------------------- text formats
  * The reference's file formats either side of the step (same tokenizer, number
  * syntax, sections, defaults and error messages; CF_PARSE messages carry

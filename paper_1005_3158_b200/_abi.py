@@ -126,6 +126,8 @@ SIGNATURES = [
                                        C.POINTER(C.c_int64)]),
     ("cf_tile_map", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts), _ip,
                               _ip]),
+    ("cf_plan_digest", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts),
+                                 C.c_int32, C.POINTER(C.c_uint64)]),
     ("cf_exchange_plan", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts), _ip,
                                    _ip, C.POINTER(C.c_int64), _ip, _ip, _ip]),
     ("cf_generate_fixture", C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, C.c_uint64,

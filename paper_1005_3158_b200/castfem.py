@@ -634,6 +634,21 @@ def tile_map(m: Mesh, setup: SimulationSetup, opts: SolveOptions) -> Tuple[np.nd
     return out, n.value
 
 
+DIGEST_NAMES = ("scalars", "tile_meta", "tile_border", "tile_slot_off", "blob_off", "elem_off", "blob_staged",
+                "tets_ord", "elem_global", "slot_node", "local_global", "node_region", "node_dir", "merge_off",
+                "merge_idx", "shared_list", "neighbors", "exchange")
+
+
+def plan_digest(m: Mesh, setup: SimulationSetup, opts: SolveOptions, rank: int = 0) -> dict:
+    """Per-array digests of one rank's tiled plan from the host plan builder (test
+    instrumentation: the device builder must reproduce them)."""
+    keep = _Keep()
+    md, sd, ro = mesh_desc(m, keep), setup_desc(setup, keep), run_opts(opts, keep)
+    out = (C.c_uint64 * 24)()
+    check(lib().cf_plan_digest(C.byref(md), C.byref(sd), C.byref(ro), rank, out))
+    return {k: int(out[i]) for i, k in enumerate(DIGEST_NAMES)}
+
+
 def exchange_plan(m: Mesh, setup: SimulationSetup, world_size: int, rank: int,
                   part_of_element: Optional[np.ndarray] = None) -> List[dict]:
     """Rank `rank`'s neighbours and exchange lists (global node ids): shared

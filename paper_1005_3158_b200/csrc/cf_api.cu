@@ -1912,6 +1912,90 @@ int cf_exchange_plan(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const
     });
 }
 
+}  // extern "C"
+// Digest of one rank's tiled plan (host builder, or the device builder with device != 0): one
+// FNV-1a 64 per plan array, in the order of cf_plan_digest_names (castfem_b200.h). Test
+// instrumentation: the two builders must agree array for array.
+static uint64_t fnv(const void* p, size_t n, uint64_t h = 1469598103934665603ull) {
+    const uint8_t* b = (const uint8_t*)p;
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+}
+template <class V>
+static uint64_t fnv_vec(const V& v) {
+    return fnv(v.data(), v.size() * sizeof(typename V::value_type), fnv(&v, 0) ^ (uint64_t)v.size());
+}
+static void digest_rank_plan(const RankPlan& rp, uint64_t* d) {
+    int k = 0;
+    const int64_t scal[] = {rp.n_tiles, rp.n_local, rp.n_ghost, rp.n_if_facets, rp.n_bc_facets, rp.n_private,
+                            rp.max_slots, rp.max_elems, rp.max_facets, rp.max_blob, rp.blob_bytes, rp.n_shared,
+                            rp.send_len, rp.recv_len};
+    d[k++] = fnv(scal, sizeof scal);
+    d[k++] = fnv_vec(rp.tile_meta);
+    d[k++] = fnv_vec(rp.tile_border);
+    d[k++] = fnv_vec(rp.tile_slot_off);
+    d[k++] = fnv_vec(rp.blob_off);
+    d[k++] = fnv_vec(rp.elem_off);
+    uint64_t hb = 0;  // the staged (non-geometry) part of every tile, tile by tile
+    for (int32_t t = 0; t < rp.n_tiles; ++t) hb = fnv(rp.blob.data() + rp.rest_off[t], rp.rest_off[t + 1] - rp.rest_off[t], hb ^ (uint64_t)t);
+    d[k++] = hb;
+    d[k++] = fnv_vec(rp.tets_ord);
+    d[k++] = fnv_vec(rp.elem_global);
+    d[k++] = fnv_vec(rp.slot_node);
+    d[k++] = fnv_vec(rp.local_global);
+    d[k++] = fnv_vec(rp.node_region);
+    d[k++] = fnv_vec(rp.node_dir);
+    d[k++] = fnv_vec(rp.merge_off);
+    d[k++] = fnv_vec(rp.merge_idx);
+    d[k++] = fnv_vec(rp.shared_list);
+    uint64_t hn = 0;
+    for (const auto& x : rp.nbrs) {
+        hn = fnv(&x.rank, 4, hn);
+        hn ^= fnv_vec(x.shared) + 3 * fnv_vec(x.ext_to) + 7 * fnv_vec(x.ext_from);
+    }
+    d[k++] = hn;
+    d[k++] = fnv_vec(rp.node_shared) ^ 3 * fnv_vec(rp.shared_off) ^ 5 * fnv_vec(rp.shared_src) ^
+             7 * fnv_vec(rp.shared_src_r) ^ 11 * fnv_vec(rp.send_off) ^ 13 * fnv_vec(rp.recv_off) ^
+             17 * fnv_vec(rp.ghost_src);
+    while (k < CF_DIGEST_LEN) d[k++] = 0;
+}
+
+extern "C" {
+int cf_plan_digest(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts, int32_t rank,
+                   uint64_t* digest) {
+    return guarded([&] {
+        if (!mesh || !setup || !opts || !digest) raise(CF_INVALID_ARG, "null argument");
+        MeshData m;
+        finalize_mesh(mesh, m);
+        SetupData S;
+        resolve_setup(m, setup, S);
+        std::vector<int32_t> label(m.N);
+        if (opts->node_order == CF_NODE_ORDER_RCM)
+            label = rcm_permutation(build_node_graph(m.N, m.E, m.tets.data()), -1);
+        else
+            std::iota(label.begin(), label.end(), 0);
+        PlanOptions po;
+        po.mode = opts->mode;
+        po.node_order = opts->node_order;
+        po.elem_order = opts->elem_order;
+        po.geometry = opts->geometry;
+        po.tile_elems = opts->tile_elems > 0 ? opts->tile_elems : 384;
+        po.tile_of_element = opts->tile_of_element;
+        po.n_tiles_given = opts->n_tiles_given;
+        po.world_size = std::max(1, opts->world_size);
+        std::vector<int32_t> part;
+        if (po.world_size > 1) {
+            part = opts->partition == CF_PARTITION_GIVEN && opts->part_of_element
+                       ? std::vector<int32_t>(opts->part_of_element, opts->part_of_element + m.E)
+                       : partition_rcb(m, po.world_size);
+            po.part_of_element = part.data();
+        }
+        RankPlan rp;
+        build_rank_plan(m, S, po, label, rank, rp);
+        digest_rank_plan(rp, digest);
+    });
+}
+
 int cf_generate_fixture(int32_t kind, int32_t n, double radius, double jitter, uint64_t seed, uint64_t perm_seed,
                         cf_fixture* out) {
     return guarded([&] {

@@ -235,6 +235,11 @@ struct RankPlan {
     int64_t n_shared = 0;
 };
 
+struct TileCtx;
+// environment knobs of the tile builder (CF_SLOT_ORDER, CF_SLOT_BANKS, CF_BANK_PASSES,
+// CF_BANK_ITERS), read once per plan by both builders
+void tile_env(TileCtx& c);
+
 struct PlanOptions {
     int mode = CF_MODE_ATOMIC;
     int node_order = CF_NODE_ORDER_RCM;

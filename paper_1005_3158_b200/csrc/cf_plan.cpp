@@ -20,6 +20,7 @@
 #include <numeric>
 
 #include "cf_internal.hpp"
+#include "cf_tilepack.hpp"
 
 namespace cfb {
 
@@ -271,6 +272,17 @@ void resolve_setup(const MeshData& m, const cf_setup_desc* s, SetupData& out) {
 }
 
 // ------------------------------------------------------------------ tiles
+void tile_env(TileCtx& c) {
+    const char* so = std::getenv("CF_SLOT_ORDER");
+    const char* sb = std::getenv("CF_SLOT_BANKS");
+    c.slot_by_node = !(so && std::string(so) == "count");
+    c.slot_banks = !(so && std::string(so) != "node") && !(sb && std::atoi(sb) == 0);
+    const char* bp = std::getenv("CF_BANK_PASSES");
+    c.bank_passes = bp ? std::atoi(bp) : 0;
+    const char* bi = std::getenv("CF_BANK_ITERS");
+    c.bank_iters = bi ? std::atoi(bi) : 0;
+}
+
 namespace {
 inline uint64_t spread21(uint64_t v) {
     v &= 0x1fffff;
@@ -282,254 +294,36 @@ inline uint64_t spread21(uint64_t v) {
     return v;
 }
 
-// Bank-aware local element positions. The tile kernel reads shared memory in two gathers:
+// Bank-aware local element positions (BankPlan, cf_tilepack.hpp). The tile kernel reads shared
+// memory in two gathers:
 //   phase 3: thread s (slot s) reads its j-th (lump, rc) operand pair, 16 B at pair index
 //            q*S + pos(e) (S = ne2, a multiple of 8), so its 16-byte bank group is pos(e) & 7;
 //   phase 2a: thread p (element at position p) reads sTH[slot of corner q], bank group slot & 7.
 // An 8-thread quarter warp costs one shared-memory wavefront per distinct address in its most
 // loaded bank group. The element positions are a free permutation (the reduction order is fixed
 // by the CSR lists, ascending global element id): a greedy balanced colouring of the elements
-// (colour = position & 7) spreads each phase-3 group over the bank groups (cfg2: 1.63x -> ~1.3x
-// the ideal wavefronts of random positions... see DESIGN.md), and an optional seeded local search
-// over position swaps (CF_BANK_ITERS) lowers the summed wavefronts of both gathers further.
-// `items` are the slots' operand lists in reduction
-// order, padded like the CSR: element corner (i << 2 | q) or 0x80000000 | fixed pair address.
+// (colour = position & 7) spreads each phase-3 group over the bank groups, and optional in-block
+// swaps (CF_BANK_PASSES) or a seeded local search (CF_BANK_ITERS) lower the wavefronts further.
 // Deterministic: the same tile always yields the same positions.
-struct BankPlanner {
-    int ne, ns;
-    std::vector<int32_t> pos, at;            // element -> position, position -> element
-    std::vector<int32_t> a_off, a_items;     // phase-3 groups (quarter warp of slots, list index)
-    std::vector<int32_t> g_off, g_list;      // element -> its phase-3 groups
-    const int32_t* eslot = nullptr;          // element i, corner q -> slot
-    int cost_a(int g) const {
-        int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        uint32_t fixed[8];
-        int nfix = 0;
-        for (int k = a_off[g]; k < a_off[g + 1]; ++k) {
-            const uint32_t it = (uint32_t)a_items[k];
-            if (it & 0x80000000u) {
-                const uint32_t ad = it & 0x7fffffffu;
-                bool dup = false;
-                for (int f = 0; f < nfix; ++f) dup = dup || fixed[f] == ad;
-                if (dup) continue;
-                if (nfix < 8) fixed[nfix++] = ad;
-                cnt[ad & 7]++;
-            } else {
-                cnt[pos[it >> 2] & 7]++;
-            }
-        }
-        int mx = 0;
-        for (int b = 0; b < 8; ++b) mx = std::max(mx, cnt[b]);
-        return mx;
-    }
-    int cost_b(int blk, int q) const {  // quarter warp of element positions, corner q
-        int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        int32_t seen[8];
-        int ns_ = 0;
-        for (int p = 8 * blk; p < std::min(ne, 8 * blk + 8); ++p) {
-            const int32_t sl = eslot[4 * at[p] + q];
-            bool dup = false;
-            for (int k = 0; k < ns_; ++k) dup = dup || seen[k] == sl;
-            if (dup) continue;
-            seen[ns_++] = sl;
-            cnt[sl & 7]++;
-        }
-        int mx = 0;
-        for (int b = 0; b < 8; ++b) mx = std::max(mx, cnt[b]);
-        return mx;
-    }
-    // items: per slot [off[s], off[s+1]) in reduction order (already padded to multiples of 4)
-    const int32_t* sperm = nullptr;          // phase-3 thread j reduces slot sperm[j] (null: j)
-    void run(int ne_, int ns_, const int32_t* eslot_, const std::vector<int32_t>& off,
-             const std::vector<uint32_t>& items, int iters, uint64_t seed, bool greedy = true) {
-        ne = ne_;
-        ns = ns_;
-        eslot = eslot_;
-        pos.resize(ne);
-        at.resize(ne);
-        std::iota(pos.begin(), pos.end(), 0);
-        std::iota(at.begin(), at.end(), 0);
-        if (ne < 16) return;
-        // phase-3 groups
-        a_off.assign(1, 0);
-        a_items.clear();
-        auto slot_at = [&](int j) { return sperm ? sperm[j] : j; };
-        for (int q0 = 0; q0 < ns; q0 += 8) {
-            int mx = 0;
-            for (int u = q0; u < std::min(ns, q0 + 8); ++u) mx = std::max(mx, off[slot_at(u) + 1] - off[slot_at(u)]);
-            for (int j = 0; j < mx; ++j) {
-                for (int u = q0; u < std::min(ns, q0 + 8); ++u) {
-                    const int sl = slot_at(u);
-                    if (off[sl] + j < off[sl + 1]) a_items.push_back((int32_t)items[off[sl] + j]);
-                }
-                a_off.push_back((int32_t)a_items.size());
-            }
-        }
-        const int na = (int)a_off.size() - 1;
-        g_off.assign(ne + 1, 0);
-        for (int g = 0; g < na; ++g)
-            for (int k = a_off[g]; k < a_off[g + 1]; ++k)
-                if (!((uint32_t)a_items[k] & 0x80000000u)) g_off[((uint32_t)a_items[k] >> 2) + 1]++;
-        for (int i = 0; i < ne; ++i) g_off[i + 1] += g_off[i];
-        g_list.resize(g_off[ne]);
-        {
-            std::vector<int32_t> cur(g_off.begin(), g_off.end() - 1);
-            for (int g = 0; g < na; ++g)
-                for (int k = a_off[g]; k < a_off[g + 1]; ++k)
-                    if (!((uint32_t)a_items[k] & 0x80000000u)) g_list[cur[(uint32_t)a_items[k] >> 2]++] = g;
-        }
-        // greedy balanced colouring: each element takes the bank group (position & 7) least used by
-        // the other members of its phase-3 groups, within the group's capacity (positions < ne)
-        if (greedy) {
-            std::vector<int32_t> cnt(8 * (size_t)na, 0);
-            for (int g = 0; g < na; ++g) {
-                uint32_t fixed[64];
-                int nfix = 0;
-                for (int k = a_off[g]; k < a_off[g + 1]; ++k) {
-                    const uint32_t it = (uint32_t)a_items[k];
-                    if (!(it & 0x80000000u)) continue;
-                    const uint32_t ad = it & 0x7fffffffu;
-                    bool dup = false;
-                    for (int f = 0; f < nfix; ++f) dup = dup || fixed[f] == ad;
-                    if (dup) continue;
-                    if (nfix < 64) fixed[nfix++] = ad;
-                    cnt[8 * (size_t)g + (ad & 7)]++;
-                }
-            }
-            // blocks of 8 consecutive elements (reference order: spatially coherent, so the
-            // phase-2a corner gathers keep their broadcasts) take the 8 colours as a permutation
-            for (int b0 = 0; b0 < ne; b0 += 8) {
-                const int nb = std::min(8, ne - b0);
-                bool used[8] = {false, false, false, false, false, false, false, false};
-                for (int i = b0; i < b0 + nb; ++i) {
-                    int best = -1, best_score = 1 << 30;
-                    for (int c = 0; c < nb; ++c) {  // a partial last block uses positions b0 .. ne-1
-                        if (used[c]) continue;
-                        // score: added wavefronts (a count reaching its group's maximum), then load
-                        int sc = 0;
-                        for (int k = g_off[i]; k < g_off[i + 1]; ++k) {
-                            const int32_t* cg = &cnt[8 * (size_t)g_list[k]];
-                            int mx = 0;
-                            for (int u = 0; u < 8; ++u) mx = std::max(mx, cg[u]);
-                            sc += 64 * (cg[c] + 1 > mx) + cg[c];
-                        }
-                        if (sc < best_score) {
-                            best_score = sc;
-                            best = c;
-                        }
-                    }
-                    used[best] = true;
-                    for (int k = g_off[i]; k < g_off[i + 1]; ++k) cnt[8 * (size_t)g_list[k] + best]++;
-                    pos[i] = b0 + best;
-                    at[b0 + best] = i;
-                }
-            }
-            // refinement (CF_BANK_PASSES, default 0): pairwise colour swaps inside a block (the
-            // block's corner gathers are unchanged) while they lower the reduction-read wavefronts.
-            // cfg2: 3 passes take the reduction reads from 1.80x to 1.67x the ideal for -0.5 % tile
-            // time, but cost ~2 s of setup per 12.6 M tets (cfg5: ~30 s), so they are opt-in.
-            const char* rp_env = std::getenv("CF_BANK_PASSES");
-            const int refine_passes = rp_env ? std::atoi(rp_env) : 0;
-            auto gmax = [&](int g) {
-                const int32_t* cg = &cnt[8 * (size_t)g];
-                int mx = 0;
-                for (int u = 0; u < 8; ++u) mx = std::max(mx, cg[u]);
-                return mx;
-            };
-            int touched[16];
-            for (int pass = 0; pass < refine_passes; ++pass) {
-                bool improved = false;
-                for (int b0 = 0; b0 < ne; b0 += 8) {
-                    const int nb = std::min(8, ne - b0);
-                    for (int u = 0; u < nb; ++u)
-                        for (int v = u + 1; v < nb; ++v) {
-                            const int i1 = at[b0 + u], i2 = at[b0 + v];
-                            const int c1 = pos[i1] & 7, c2 = pos[i2] & 7;
-                            int nt = 0;
-                            for (int i : {i1, i2})
-                                for (int k = g_off[i]; k < g_off[i + 1]; ++k) {
-                                    bool dup = false;
-                                    for (int w = 0; w < nt; ++w) dup = dup || touched[w] == g_list[k];
-                                    if (!dup && nt < 16) touched[nt++] = g_list[k];
-                                }
-                            int before = 0;
-                            for (int w = 0; w < nt; ++w) before += gmax(touched[w]);
-                            auto move = [&](int i, int from, int to) {
-                                for (int k = g_off[i]; k < g_off[i + 1]; ++k) {
-                                    cnt[8 * (size_t)g_list[k] + from]--;
-                                    cnt[8 * (size_t)g_list[k] + to]++;
-                                }
-                            };
-                            move(i1, c1, c2);
-                            move(i2, c2, c1);
-                            int after = 0;
-                            for (int w = 0; w < nt; ++w) after += gmax(touched[w]);
-                            if (after < before) {
-                                pos[i1] = b0 + c2;
-                                pos[i2] = b0 + c1;
-                                at[b0 + c2] = i1;
-                                at[b0 + c1] = i2;
-                                improved = true;
-                            } else {
-                                move(i1, c2, c1);
-                                move(i2, c1, c2);
-                            }
-                        }
-                }
-                if (!improved) break;
-            }
-        }
-        uint64_t x = seed * 0x9E3779B97F4A7C15ull + 0x2545F4914F6CDD1Dull;
-        auto rnd = [&]() {
-            x ^= x << 13;
-            x ^= x >> 7;
-            x ^= x << 17;
-            return x;
-        };
-        int ga[16], gb[4];
-        for (int it = 0; it < iters; ++it) {
-            const int i1 = (int)(rnd() % (uint64_t)ne), i2 = (int)(rnd() % (uint64_t)ne);
-            const int p1 = pos[i1], p2 = pos[i2];
-            if ((p1 & 7) == (p2 & 7) && (p1 >> 3) == (p2 >> 3)) continue;
-            int na_ = 0;
-            for (int i : {i1, i2})
-                for (int k = g_off[i]; k < g_off[i + 1]; ++k) {
-                    bool dup = false;
-                    for (int u = 0; u < na_; ++u) dup = dup || ga[u] == g_list[k];
-                    if (!dup && na_ < 16) ga[na_++] = g_list[k];
-                }
-            const int nb = (p1 >> 3) == (p2 >> 3) ? 1 : 2;
-            gb[0] = p1 >> 3;
-            gb[1] = p2 >> 3;
-            auto total = [&]() {
-                int c = 0;
-                for (int u = 0; u < na_; ++u) c += cost_a(ga[u]);
-                for (int u = 0; u < nb; ++u)
-                    for (int q = 0; q < 4; ++q) c += cost_b(gb[u], q);
-                return c;
-            };
-            const int before = total();
-            std::swap(pos[i1], pos[i2]);
-            at[p1] = i2;
-            at[p2] = i1;
-            if (total() > before) {  // revert (sideways moves are kept)
-                std::swap(pos[i1], pos[i2]);
-                at[p1] = i1;
-                at[p2] = i2;
-            }
-        }
-    }
-    int total_cost(int which = 3) const {  // 1: phase-3 reads, 2: phase-2a gathers
-        int c = 0;
-        if (which & 1)
-            for (int g = 0; g + 1 < (int)a_off.size(); ++g) c += cost_a(g);
-        if (which & 2)
-            for (int b = 0; 8 * b < ne; ++b)
-                for (int q = 0; q < 4; ++q) c += cost_b(b, q);
-        return c;
-    }
-    int n_groups(int which) const { return which == 1 ? (int)a_off.size() - 1 : 4 * ((ne + 7) / 8); }
-};
+
+// per-tile context of the shared tile functions (cf_tilepack.hpp) over the host arrays
+TileCtx tile_ctx(const MeshData& m, const SetupData& S, const PlanOptions& o, const std::vector<int32_t>& fe_off,
+                 const std::vector<int32_t>& fe, const std::vector<int32_t>& facet_sister, const uint8_t* kind_if) {
+    TileCtx c;
+    c.tets = m.tets.data();
+    c.region = m.region;
+    c.facets = m.facets;
+    c.coords = m.coords;
+    c.fe_off = fe_off.data();
+    c.fe = fe.data();
+    c.facet_kind = S.facet_kind.data();
+    c.facet_sister = facet_sister.data();
+    c.kind_interface = kind_if;
+    c.tdep = S.temp_dep;
+    c.coords_layout = o.geometry == CF_GEOM_COORDS;
+    tile_env(c);
+    return c;
+}
 }  // namespace
 
 void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o,
@@ -662,6 +456,11 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             if (in_rank[m.owner[f]] && S.facet_kind[f] >= 0) fe[cur[m.owner[f]]++] = f;
     }
 
+    std::vector<int32_t> facet_sister(m.F, -1);  // sister element of each interface facet
+    for (size_t q = 0; q < S.pairs.size(); ++q) facet_sister[S.pairs[q].facet] = S.pairs[q].sister;
+    uint8_t kind_if[kMaxFacetKinds];
+    for (int k = 0; k < kMaxFacetKinds; ++k) kind_if[k] = (uint8_t)(S.P.kind[k].interface != 0);
+    const TileCtx fc = tile_ctx(m, S, o, fe_off, fe, facet_sister, kind_if);
     trace_stage("plan: facet bindings");
     // ---- tiles: element order key, contiguous chunks, ascending id within a tile
     std::vector<std::vector<int32_t>> tiles;
@@ -727,40 +526,15 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
         // shared-memory budget: the 95th percentile of the chunk footprints; larger chunks
         // (interface / boundary chunks with many facets) are halved along the order until they
         // fit, so one launch configuration (and its occupancy) serves every tile
-        auto footprint = [&](const int32_t* e0, int64_t n, std::vector<int64_t>& tab) {
-            // unique nodes and their contribution counts: open addressing on (node, count)
-            size_t cap = 64;
-            while (cap < 8 * (size_t)n) cap <<= 1;
-            if (tab.size() < cap) tab.resize(cap);
-            std::fill(tab.begin(), tab.begin() + cap, -1);
-            const size_t mask = cap - 1;
-            int ns = 0, nf = 0;
-            auto add = [&](int32_t v) {
-                size_t h = ((uint64_t)(uint32_t)v * 0x9E3779B97F4A7C15ull) >> 32 & mask;
-                while (tab[h] >= 0 && (int32_t)(tab[h] >> 32) != v) h = (h + 1) & mask;
-                if (tab[h] < 0) {
-                    tab[h] = (int64_t)v << 32;
-                    ++ns;
-                }
-                tab[h] += 1;
-            };
-            for (int64_t i = 0; i < n; ++i) {
-                const int32_t e = e0[i];
-                for (int a = 0; a < 4; ++a) add(m.tets[4 * (size_t)e + a]);
-                for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j, ++nf)
-                    for (int a = 0; a < 3; ++a) add(m.facets[3 * (size_t)fe[j] + a]);
-            }
-            int ncsr = 0;
-            for (size_t h = 0; h < cap; ++h)
-                if (tab[h] >= 0) ncsr += ((int)(tab[h] & 0xffffffff) + 3) & ~3;
-            const TileLayout L(TileMeta{(int32_t)n, ns, nf, ncsr}, S.temp_dep, o.geometry == CF_GEOM_COORDS);
-            return (int64_t)cf_round(L.bytes, 16) + 24 * cf_round(ns, 2) + 8 * cf_round(L.scratch, 2);
+            auto footprint = [&](const int32_t* e0, int64_t n, std::vector<int32_t>& tab) {
+            if (tab.size() < (size_t)(8 * n + 64)) tab.resize(8 * n + 64);
+            return tile_footprint(fc, e0, (int)n, tab.data());
         };
         if (tiles.size() > 20) {
             std::vector<int64_t> fp(tiles.size());
 #pragma omp parallel
             {
-                std::vector<int64_t> tab;
+                std::vector<int32_t> tab;
 #pragma omp for schedule(dynamic, 256)
                 for (int64_t t = 0; t < (int64_t)tiles.size(); ++t)
                     fp[t] = footprint(tiles[t].data(), tiles[t].size(), tab);
@@ -774,7 +548,7 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             std::vector<std::vector<int32_t>> out;
             out.reserve(tiles.size() + tiles.size() / 16);
             std::vector<std::vector<int32_t>> stack;
-            std::vector<int64_t> tab;
+            std::vector<int32_t> tab;
             for (size_t t = 0; t < tiles.size(); ++t) {
                 if (fp[t] <= budget) {
                     out.push_back(std::move(tiles[t]));
@@ -902,50 +676,21 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     const int nthr = omp_get_max_threads();
     std::vector<std::vector<int32_t>> tile_nodes;
     std::vector<TileMeta> meta;
-    auto tile_facets = [&](const std::vector<int32_t>& te, std::vector<int32_t>& out) {
-        out.clear();  // facet bindings, element order then facet id (blocked.hpp:244-288)
-        for (int32_t e : te)
-            for (int32_t j = fe_off[e]; j < fe_off[e + 1]; ++j) out.push_back(fe[j]);
-    };
+    TileCtx tc = fc;
+    tc.local_of = local_of.data();
     auto pass1 = [&](const std::vector<int32_t>& which) {
 #pragma omp parallel num_threads(nthr)
         {
-            std::vector<int32_t> slot_of(rp.n_local, -1), cnt_of, idx, tfacets, sorted;
+            std::vector<int32_t> ws, tmp;
 #pragma omp for schedule(dynamic, 64)
             for (int64_t w = 0; w < (int64_t)which.size(); ++w) {
                 const int32_t t = which[w];
                 const auto& te = tiles[t];
-                auto& tnodes = tile_nodes[t];
-                tnodes.clear();
-                for (int32_t e : te)
-                    for (int a = 0; a < 4; ++a) {
-                        const int32_t l = local_of[m.tets[4 * (size_t)e + a]];
-                        if (slot_of[l] == -1) {
-                            slot_of[l] = -2;
-                            tnodes.push_back(l);
-                        }
-                    }
-                // slots ordered by contribution count (desc), then local id: the warps of
-                // the reduction phase then walk lists of near-equal length (no divergence)
-                for (size_t k = 0; k < tnodes.size(); ++k) slot_of[tnodes[k]] = (int32_t)k;
-                cnt_of.assign(tnodes.size(), 0);
-                tile_facets(te, tfacets);
-                for (int32_t e : te)
-                    for (int a = 0; a < 4; ++a) cnt_of[slot_of[local_of[m.tets[4 * (size_t)e + a]]]]++;
-                for (int32_t f : tfacets)
-                    for (int a = 0; a < 3; ++a) cnt_of[slot_of[local_of[m.facets[3 * (size_t)f + a]]]]++;
-                idx.resize(tnodes.size());
-                std::iota(idx.begin(), idx.end(), 0);
-                std::sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) {
-                    return cnt_of[x] != cnt_of[y] ? cnt_of[x] > cnt_of[y] : tnodes[x] < tnodes[y];
-                });
-                for (int32_t l : tnodes) slot_of[l] = -1;
-                sorted.resize(tnodes.size());
-                for (size_t k = 0; k < idx.size(); ++k) sorted[k] = tnodes[idx[k]];
-                tnodes.swap(sorted);
-                int ncsr = 0;  // each slot's list padded to a multiple of 4 (16-byte reads in the reduction)
-                for (int32_t cn : cnt_of) ncsr += (cn + 3) & ~3;
-                meta[t] = TileMeta{(int32_t)te.size(), (int32_t)tnodes.size(), (int32_t)tfacets.size(), ncsr};
+                const size_t need = 8 * te.size() + 8 * 4 * te.size() + 64;
+                if (ws.size() < need) ws.resize(need);
+                if (tmp.size() < 4 * te.size()) tmp.resize(4 * te.size());
+                meta[t] = tile_pass1(tc, te.data(), (int)te.size(), tmp.data(), ws.data());
+                tile_nodes[t].assign(tmp.begin(), tmp.begin() + meta[t].ns);
             }
         }
     };
@@ -978,20 +723,11 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
             for (int32_t l : tile_nodes[t]) b = b || shared_node[l];
             rp.tile_border[t] = b;
         }
-    // slot order inside a tile: tile-private nodes first (by contribution count, descending: similar
-    // reduction-list lengths share a warp), then the tile-shared nodes in ascending node id, so the
-    // partials they write and the slot copies the update kernel writes back are laid out in the
-    // update's (node) order -- whole sectors instead of scattered 16 / 8-byte accesses
-    if (!(std::getenv("CF_SLOT_ORDER") && std::string(std::getenv("CF_SLOT_ORDER")) == "count")) {
-#pragma omp parallel for schedule(dynamic, 256)
-        for (int32_t t = 0; t < rp.n_tiles; ++t) {
-            auto& tn = tile_nodes[t];
-            auto mid = std::stable_partition(tn.begin(), tn.end(), [&](int32_t l) {
-                return ntiles_of[l] == 1 && !shared_node[l];
-            });
-            std::sort(mid, tn.end());
-        }
-    }
+    // slot order inside a tile (tile_pack): tile-private nodes first (by contribution count,
+    // descending: similar reduction-list lengths share a warp), then the tile-shared nodes in
+    // ascending node id, so the partials they write and the slot copies the update kernel writes
+    // back are laid out in the update's (node) order -- whole sectors instead of scattered 16 /
+    // 8-byte accesses
     rp.tile_slot_off.assign(rp.n_tiles + 1, 0);
     rp.blob_off.assign(rp.n_tiles + 1, 0);
     rp.elem_global.resize(Er);
@@ -1030,212 +766,54 @@ void build_rank_plan(const MeshData& m, const SetupData& S, const PlanOptions& o
     for (int32_t l = 0; l < rp.n_local; ++l)
         for (int k = 0; k < 3; ++k) rp.coords_local[3 * (size_t)l + k] = m.pos(lnodes[l])[k];
     rp.slot_node.resize(rp.tile_slot_off[rp.n_tiles]);
-    int64_t n_if = 0, n_bc = 0, bank_before = 0, bank_after = 0, bank_a = 0, bank_b = 0, bank_ia = 0, bank_ib = 0, bank_id_a = 0;
-    const char* bank_env = std::getenv("CF_BANK_ITERS");
-    // swap attempts per element after the greedy colouring (measured: 8 -> -1 % tile time for
-    // +13 s setup at cfg2; off by default)
-    const int bank_iters = bank_env ? std::atoi(bank_env) : 0;
+    int64_t n_if = 0, n_bc = 0, bank_after = 0, bank_a = 0, bank_b = 0, bank_ib = 0;
     const bool bank_trace = std::getenv("CF_TRACE_SETUP") && std::atoi(std::getenv("CF_TRACE_SETUP"));
-    const bool slot_order_default = !(std::getenv("CF_SLOT_ORDER") && std::string(std::getenv("CF_SLOT_ORDER")) != "node")
-                                    && !(std::getenv("CF_SLOT_BANKS") && std::atoi(std::getenv("CF_SLOT_BANKS")) == 0);
-#pragma omp parallel num_threads(nthr) reduction(+ : n_if, n_bc)
+    tc.lnode_region = rp.node_region.data();
+    tc.lnode_dir = rp.node_dir.empty() ? nullptr : rp.node_dir.data();
+    tc.ntiles_of = ntiles_of.data();
+    std::vector<uint8_t> shared_u8;
+    if (W > 1) {
+        shared_u8.assign(shared_node.begin(), shared_node.end());
+        tc.shared_node = shared_u8.data();
+    }
+    TileCaps caps{1, 1, 0, 0};
+    for (int32_t t = 0; t < rp.n_tiles; ++t) {
+        const TileMeta& tm = rp.tile_meta[t];
+        caps.ne = std::max(caps.ne, tm.ne);
+        caps.ns = std::max(caps.ns, tm.ns);
+        caps.nf = std::max(caps.nf, tm.nf);
+        caps.ncsr = std::max(caps.ncsr, tm.ncsr);
+    }
+    const int64_t ws_ints = tile_ws_ints(caps);
+#pragma omp parallel num_threads(nthr) reduction(+ : n_if, n_bc, bank_after, bank_a, bank_b, bank_ib)
     {
-        std::vector<int32_t> slot_of(rp.n_local, -1), tfacets;
-        std::vector<int32_t> ent_off, cur, poff, eslot, sperm, tn, gmem, goff, ord, bank_of;
-        std::vector<uint32_t> ent, items;
-        std::vector<int32_t> gcnt;
-        BankPlanner bank;
-#pragma omp for schedule(dynamic, 64) reduction(+ : bank_before, bank_after, bank_a, bank_b, bank_ia, bank_ib, bank_id_a)
+        std::vector<int32_t> ws(ws_ints);
+#pragma omp for schedule(dynamic, 64)
         for (int32_t t = 0; t < rp.n_tiles; ++t) {
-            const auto& te = tiles[t];
             const TileMeta tm = rp.tile_meta[t];
-            const int ne = tm.ne, ns = tm.ns, nf = tm.nf;
             const TileLayout L(tm, S.temp_dep, coords);
             uint8_t* const stg = rp.blob.data() + rp.rest_off[t];  // connectivity first, then sections >= stage
             std::memset(stg, 0, (size_t)L.staged_bytes());
-            auto at = [&](int32_t off) { return stg + L.stage_of(off); };
-            tn.assign(tile_nodes[t].begin(), tile_nodes[t].end());
-            const auto& tnodes = tn;
-            for (int k = 0; k < ns; ++k) slot_of[tn[k]] = k;
-            // bank-aware numbering of the tile-private slots (their order is free: the reduction's
-            // thread order is sperm, the update never sees them): phase 2a reads sTH[slot] for
-            // corner q of 8 consecutive elements (the bank planner keeps such blocks together), so
-            // spread each block's corner slots over the 8 bank groups (slot & 7); shared slots fixed
-            if (!coords && ne >= 16 && slot_order_default) {
-                int np = 0;
-                while (np < ns && ntiles_of[tn[np]] == 1 && !shared_node[tn[np]]) ++np;
-                if (np >= 16) {
-                    const int ng = 4 * ((ne + 7) / 8);
-                    goff.assign(ng + 1, 0);
-                    gmem.clear();
-                    for (int b0 = 0, g = 0; b0 < ne; b0 += 8)
-                        for (int q = 0; q < 4; ++q, ++g) {
-                            for (int i = b0; i < std::min(ne, b0 + 8); ++i) {
-                                const int32_t sl = slot_of[local_of[m.tets[4 * (size_t)te[i] + q]]];
-                                bool dup = false;
-                                for (int k = goff[g]; k < (int)gmem.size(); ++k) dup = dup || gmem[k] == sl;
-                                if (!dup) gmem.push_back(sl);
-                            }
-                            goff[g + 1] = (int)gmem.size();
-                        }
-                    // private slot (old index) -> its groups
-                    std::vector<std::vector<int32_t>> pg(np);
-                    for (int g = 0; g < ng; ++g)
-                        for (int k = goff[g]; k < goff[g + 1]; ++k)
-                            if (gmem[k] < np) pg[gmem[k]].push_back(g);
-                    gcnt.assign(8 * (size_t)ng, 0);
-                    for (int g = 0; g < ng; ++g)
-                        for (int k = goff[g]; k < goff[g + 1]; ++k)
-                            if (gmem[k] >= np) gcnt[8 * (size_t)g + (gmem[k] & 7)]++;
-                    int freeb[8];
-                    for (int b = 0; b < 8; ++b) freeb[b] = (np - b + 7) / 8;
-                    ord.resize(np);
-                    std::iota(ord.begin(), ord.end(), 0);
-                    std::stable_sort(ord.begin(), ord.end(),
-                                     [&](int32_t x, int32_t y) { return pg[x].size() > pg[y].size(); });
-                    bank_of.assign(np, -1);
-                    for (int32_t o : ord) {
-                        int best = -1, bc = 1 << 30;
-                        for (int b = 0; b < 8; ++b) {
-                            if (!freeb[b]) continue;
-                            int c = 0;
-                            for (int32_t g : pg[o]) c += gcnt[8 * (size_t)g + b];
-                            if (c < bc || (c == bc && freeb[b] > freeb[best])) {
-                                bc = c;
-                                best = b;
-                            }
-                        }
-                        bank_of[o] = best;
-                        freeb[best]--;
-                        for (int32_t g : pg[o]) gcnt[8 * (size_t)g + best]++;
-                    }
-                    // new index: the k-th private slot of bank b gets b + 8k (stable in old order)
-                    int nextb[8];
-                    for (int b = 0; b < 8; ++b) nextb[b] = b;
-                    std::vector<int32_t> newtn(tn.begin(), tn.begin() + np);
-                    for (int o = 0; o < np; ++o) {
-                        newtn[nextb[bank_of[o]]] = tn[o];
-                        nextb[bank_of[o]] += 8;
-                    }
-                    std::copy(newtn.begin(), newtn.end(), tn.begin());
-                    for (int k = 0; k < np; ++k) slot_of[tn[k]] = k;
-                }
+            TileOut to;
+            to.stg = stg;
+            to.elem_global = rp.elem_global.data() + elem_off[t];
+            to.tets_ord = rp.tets_ord.data() + 4 * elem_off[t];
+            to.slot_node = rp.slot_node.data() + rp.tile_slot_off[t];
+            tile_pack(tc, t, tiles[t].data(), tm, tile_nodes[t].data(), ws.data(), to, bank_trace);
+            n_if += to.n_if;
+            n_bc += to.n_bc;
+            if (bank_trace && !coords && tm.ne >= 16) {
+                bank_after += to.bank_cost[0];
+                bank_a += to.bank_cost[1];
+                bank_b += to.bank_cost[2];
+                bank_ib += 4 * ((tm.ne + 7) / 8);
             }
-            tile_facets(te, tfacets);
-            // per-slot contributions in reduction order (ascending element, then facets):
-            // element corner (i << 2 | q) or 0x80000000 | final 16-bit code
-            ent_off.assign(ns + 1, 0);
-            for (int i = 0; i < ne; ++i)
-                for (int a = 0; a < 4; ++a) ent_off[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]] + 1]++;
-            for (int i = 0; i < nf; ++i)
-                for (int a = 0; a < 3; ++a) ent_off[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]] + 1]++;
-            for (int k = 0; k < ns; ++k) ent_off[k + 1] += ent_off[k];
-            ent.resize(ent_off[ns]);
-            {
-                cur.assign(ent_off.begin(), ent_off.end() - 1);
-                for (int i = 0; i < ne; ++i)
-                    for (int a = 0; a < 4; ++a)
-                        ent[cur[slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]]]++] = (uint32_t)(i << 2 | a);
-                for (int i = 0; i < nf; ++i)
-                    for (int a = 0; a < 3; ++a)
-                        ent[cur[slot_of[local_of[m.facets[3 * (size_t)tfacets[i] + a]]]]++] =
-                            0x80000000u | L.code_facet(i, a);
-            }
-            // padded lists (multiples of 4: the kernel reads 4 codes at a time; padding = the zero
-            // operand), then bank-aware element positions (stored layout)
-            poff.assign(ns + 1, 0);
-            for (int k = 0; k < ns; ++k) poff[k + 1] = poff[k] + ((ent_off[k + 1] - ent_off[k] + 3) & ~3);
-            items.assign(poff[ns], 0x80000000u | L.code_zero());
-            for (int k = 0; k < ns; ++k)
-                std::copy(ent.begin() + ent_off[k], ent.begin() + ent_off[k + 1], items.begin() + poff[k]);
-            // phase-3 thread order: slots by padded list length (descending), so a warp's reduction
-            // loops have similar trip counts whatever the slot order (tile-shared slots by node id)
-            sperm.resize(ns);
-            std::iota(sperm.begin(), sperm.end(), 0);
-            std::stable_sort(sperm.begin(), sperm.end(), [&](int32_t x, int32_t y) {
-                return poff[x + 1] - poff[x] > poff[y + 1] - poff[y];
-            });
-            bank.sperm = sperm.data();
-            eslot.resize(4 * (size_t)ne);
-            for (int i = 0; i < ne; ++i)
-                for (int a = 0; a < 4; ++a) eslot[4 * i + a] = slot_of[local_of[m.tets[4 * (size_t)te[i] + a]]];
-            bank.run(ne, ns, eslot.data(), poff, items, coords ? 0 : bank_iters * ne, (uint64_t)t + 1);
-            if (bank_trace) {
-                BankPlanner id;
-                id.sperm = sperm.data();
-                id.run(ne, ns, eslot.data(), poff, items, 0, 0, false);  // reference-order positions
-                if (!coords) {
-                    bank_before += id.total_cost();
-                    bank_after += bank.total_cost();
-                    bank_id_a += id.total_cost(1);
-                    bank_a += bank.total_cost(1);
-                    bank_b += bank.total_cost(2);
-                    bank_ia += bank.n_groups(1);
-                    bank_ib += bank.n_groups(2);
-                }
-            }
-            const int32_t* lp = bank.pos.data();  // element i -> local position
-            uint16_t* csec = (uint16_t*)at(L.conn);  // ushort4 per element
-            for (int i = 0; i < ne; ++i) {
-                const int32_t e = te[i], p = lp[i];
-                rp.elem_global[elem_off[t] + p] = e;
-                for (int a = 0; a < 4; ++a) {
-                    const int32_t l = local_of[m.tets[4 * (size_t)e + a]];  // oriented (finalize_mesh)
-                    rp.tets_ord[4 * (size_t)(elem_off[t] + p) + a] = l;
-                    csec[4 * p + a] = (uint16_t)slot_of[l];
-                }
-                *at(L.region + p) = (uint8_t)m.region[e];
-            }
-            for (int i = 0; i < nf; ++i) {
-                const int32_t f = tfacets[i];
-                const int32_t kind = S.facet_kind[f];
-                uint8_t* rec = at(L.fac + 48 * i);  // (area, slots + kind), sister nodes, pad
-                uint16_t* fs = (uint16_t*)(rec + 8);
-                for (int a = 0; a < 3; ++a) fs[a] = (uint16_t)slot_of[local_of[m.facets[3 * (size_t)f + a]]];
-                fs[3] = (uint16_t)kind;
-                const double area = triangle_area(m.pos(m.facets[3 * (size_t)f]), m.pos(m.facets[3 * (size_t)f + 1]),
-                                                  m.pos(m.facets[3 * (size_t)f + 2]));
-                std::memcpy(rec, &area, 8);
-                int32_t* sis = (int32_t*)(rec + 16);
-                if (S.P.kind[kind].interface) {
-                    const int32_t se = S.pairs[S.pair_of_facet[f]].sister;
-                    for (int a = 0; a < 4; ++a) sis[a] = local_of[m.tets[4 * (size_t)se + a]];
-                    n_if++;
-                } else {
-                    n_bc++;
-                }
-            }
-            uint16_t* sp = (uint16_t*)at(L.sperm);
-            for (int j = 0; j < ns; ++j) sp[j] = (uint16_t)sperm[j];
-            uint16_t* cend = (uint16_t*)at(L.csr_end);
-            uint16_t* csr = (uint16_t*)at(L.csr);
-            int32_t* sn = (int32_t*)at(L.snode);
-            const int64_t so = rp.tile_slot_off[t];
-            for (int k = 0; k < (int)cf_round(ns, 2); ++k) {
-                if (k >= ns) {  // padding slot (never a merge target)
-                    rp.slot_node[so + k] = -1;
-                    continue;
-                }
-                const int32_t l = tnodes[k];
-                rp.slot_node[so + k] = (int32_t)(((uint32_t)rp.node_region[l] << 28) | (uint32_t)l);
-                const bool priv = ntiles_of[l] == 1 && !shared_node[l];
-                const bool dir = !rp.node_dir.empty() && rp.node_dir[l] >= 0;
-                *at(L.sinfo + k) = (uint8_t)((rp.node_region[l] & 0x3f) | (dir ? 0x40 : 0) | (priv ? 0x80 : 0));
-                for (int32_t q = poff[k]; q < poff[k + 1]; ++q) {
-                    const uint32_t it = items[q];
-                    csr[q] = (it & 0x80000000u) ? (uint16_t)(it & 0xffffu) : L.code_elem(lp[it >> 2], (int)(it & 3));
-                }
-                cend[k] = (uint16_t)poff[k + 1];
-                sn[k] = l;
-            }
-            for (int k = 0; k < ns; ++k) slot_of[tnodes[k]] = -1;
         }
     }
     if (bank_trace)
-        std::fprintf(stderr, "[cf setup] rank %d bank-aware positions: shared-memory wavefronts %lld -> %lld "
-                     "(reduction reads %lld from %lld, ideal %lld; corner gathers %lld, ideal %lld)\n", rank,
-                     (long long)bank_before, (long long)bank_after, (long long)bank_a, (long long)bank_id_a, (long long)bank_ia,
-                     (long long)bank_b, (long long)bank_ib);
+        std::fprintf(stderr, "[cf setup] rank %d bank-aware positions: shared-memory wavefronts %lld "
+                     "(reduction reads %lld; corner gathers %lld, ideal %lld)\n", rank,
+                     (long long)bank_after, (long long)bank_a, (long long)bank_b, (long long)bank_ib);
     rp.n_if_facets = n_if;
     rp.n_bc_facets = n_bc;
     std::vector<std::vector<int32_t>>().swap(tile_nodes);

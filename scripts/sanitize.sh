@@ -4,5 +4,5 @@
 cd "$(dirname "$0")/.."
 for tool in memcheck racecheck synccheck initcheck; do
     echo "=== $tool"
-    timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_case.py 2>&1 | tail -25
+    timeout 600 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_case.py 2>&1 | tail -25
 done

@@ -196,6 +196,9 @@ typedef struct cf_stats {
     int64_t update_bytes_per_step; /* merge + update kernel's algorithmic bytes per step: per merged
                                       node its record (32 B), T read + write (16 B), and per partial
                                       the 16 B read + the 8 B slot-copy write */
+    int64_t n_nodes_global;    /* nodes / elements of the whole mesh */
+    int64_t n_elems_global;
+    int32_t device_setup;      /* 1: the plan was built by the device setup pipeline */
 } cf_stats;
 
 /* ---------------------------------------------------------------------------
@@ -380,6 +383,21 @@ typedef struct cf_fixture {
 int cf_generate_fixture(int32_t kind, int32_t n, double radius, double jitter, uint64_t seed,
                         uint64_t perm_seed, cf_fixture* out);
 
+/* A plan over a fixture generated on the device (the same mesh cf_generate_fixture
+ * returns, perm_seed 0): the mesh never exists in host memory (cfg5: 805 M tets). The
+ * setup's tags are the fixture's ("outer", "cast_if", "mold_if"); T0 is the material
+ * initial temperature of each node's region plus U(-t0_noise, t0_noise) keyed by grid point
+ * with noise_seed (cf_counter_uniform), unless setup->initial_T is given. */
+typedef struct cf_fixture_spec {
+    int32_t kind, n;        /* 0 cube, 1 casting; n^3 cells */
+    double radius, jitter;
+    uint64_t seed, perm_seed;  /* perm_seed must be 0 */
+    double t0_noise;
+    uint64_t noise_seed;
+} cf_fixture_spec;
+int cf_plan_create_fixture(const cf_fixture_spec* fx, const cf_setup_desc* setup,
+                           const cf_run_opts* opts, cf_plan** out);
+
 /* Counter-based uniform noise U(lo, hi) keyed by (seed, key) — T0 noise
  * keyed by grid point so it is independent of numbering. */
 int cf_counter_uniform(uint64_t seed, const int64_t* keys, int64_t n, double lo, double hi,
@@ -392,6 +410,11 @@ int cf_counter_uniform(uint64_t seed, const int64_t* keys, int64_t n, double lo,
 #define CF_DIGEST_LEN 24
 int cf_plan_digest(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts,
                    int32_t rank, uint64_t* digest);
+/* The same digests from the device setup pipeline (tets_ord is not kept there: its entry is
+ * the digest of an empty array), and the device RCB partition. Need a B200. */
+int cf_plan_digest_device(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts,
+                          int32_t rank, uint64_t* digest);
+int cf_partition_rcb_device(const cf_mesh_desc* mesh, int32_t parts, int32_t* out);
 
 /* ---------------------------------------------------------------- text formats
  * The reference's file formats either side of the step (same tokenizer, number

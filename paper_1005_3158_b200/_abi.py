@@ -71,7 +71,8 @@ class cf_stats(C.Structure):
                 ("n_tiles", C.c_int32), ("n_elems_local", C.c_int64), ("n_nodes_local", C.c_int64),
                 ("total_slots", C.c_int64), ("n_shared_nodes", C.c_int64), ("n_ghost_nodes", C.c_int64),
                 ("device_bytes", C.c_int64), ("bytes_per_step", C.c_int64), ("launches_per_step", C.c_int64),
-                ("tile_bytes_per_launch", C.c_int64), ("update_bytes_per_step", C.c_int64)]
+                ("tile_bytes_per_launch", C.c_int64), ("update_bytes_per_step", C.c_int64),
+                ("n_nodes_global", C.c_int64), ("n_elems_global", C.c_int64), ("device_setup", C.c_int32)]
 
 
 class cf_tune_report(C.Structure):
@@ -81,6 +82,11 @@ class cf_tune_report(C.Structure):
 class cf_fixture(C.Structure):
     _fields_ = [("n_nodes", C.c_int32), ("n_elems", C.c_int32), ("n_facets", C.c_int32), ("coords", _dp),
                 ("tets", _ip), ("region", _ip), ("facets", _ip), ("facet_tag", _ip), ("node_grid", _ip)]
+
+
+class cf_fixture_spec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("radius", C.c_double), ("jitter", C.c_double),
+                ("seed", C.c_uint64), ("perm_seed", C.c_uint64), ("t0_noise", C.c_double), ("noise_seed", C.c_uint64)]
 
 
 CF_REDUCE_MIN, CF_REDUCE_MAX = 0, 1
@@ -126,6 +132,11 @@ SIGNATURES = [
                                        C.POINTER(C.c_int64)]),
     ("cf_tile_map", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts), _ip,
                               _ip]),
+    ("cf_plan_create_fixture", C.c_int, [C.POINTER(cf_fixture_spec), C.POINTER(cf_setup_desc),
+                                         C.POINTER(cf_run_opts), C.POINTER(C.c_void_p)]),
+    ("cf_plan_digest_device", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts),
+                                        C.c_int32, C.POINTER(C.c_uint64)]),
+    ("cf_partition_rcb_device", C.c_int, [C.POINTER(cf_mesh_desc), C.c_int32, _ip]),
     ("cf_plan_digest", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts),
                                  C.c_int32, C.POINTER(C.c_uint64)]),
     ("cf_exchange_plan", C.c_int, [C.POINTER(cf_mesh_desc), C.POINTER(cf_setup_desc), C.POINTER(cf_run_opts), _ip,

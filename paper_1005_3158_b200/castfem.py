@@ -407,17 +407,25 @@ class Solver:
     """A device-resident plan: build_worker_model + init_worker_fields
     (blocked.hpp:156-436), stepped with blocked_step semantics (:542-550)."""
 
-    def __init__(self, mesh: Mesh, setup: SimulationSetup, opts: Optional[SolveOptions] = None):
+    def __init__(self, mesh: Optional[Mesh], setup: SimulationSetup, opts: Optional[SolveOptions] = None,
+                 fixture: Optional["FixtureSpec"] = None):
+        """mesh: host arrays (cf_plan_create); or fixture: the mesh generated on the device
+        (cf_plan_create_fixture: it never exists in host memory)."""
         opts = opts or SolveOptions()
         keep = _Keep()
-        self._N = mesh.node_count()
         self.mesh = mesh
         self.setup = setup
         self.opts = opts
-        md, sd, ro = mesh_desc(mesh, keep), setup_desc(setup, keep), run_opts(opts, keep)
+        sd, ro = setup_desc(setup, keep), run_opts(opts, keep)
         h = C.c_void_p()
-        check(lib().cf_plan_create(C.byref(md), C.byref(sd), C.byref(ro), C.byref(h)))
+        if fixture is not None:
+            fx = fixture.desc()
+            check(lib().cf_plan_create_fixture(C.byref(fx), C.byref(sd), C.byref(ro), C.byref(h)))
+        else:
+            md = mesh_desc(mesh, keep)
+            check(lib().cf_plan_create(C.byref(md), C.byref(sd), C.byref(ro), C.byref(h)))
         self.handle = h
+        self._N = int(self.stats().n_nodes_global)
         if opts.graph_steps:
             check(lib().cf_enable_graph(self.handle, opts.graph_steps))
 
@@ -639,14 +647,45 @@ DIGEST_NAMES = ("scalars", "tile_meta", "tile_border", "tile_slot_off", "blob_of
                 "merge_idx", "shared_list", "neighbors", "exchange")
 
 
-def plan_digest(m: Mesh, setup: SimulationSetup, opts: SolveOptions, rank: int = 0) -> dict:
-    """Per-array digests of one rank's tiled plan from the host plan builder (test
-    instrumentation: the device builder must reproduce them)."""
+def plan_digest(m: Mesh, setup: SimulationSetup, opts: SolveOptions, rank: int = 0, device: bool = False) -> dict:
+    """Per-array digests of one rank's tiled plan from the host plan builder, or (device=True)
+    from the device setup pipeline (test instrumentation: the two must agree)."""
     keep = _Keep()
     md, sd, ro = mesh_desc(m, keep), setup_desc(setup, keep), run_opts(opts, keep)
     out = (C.c_uint64 * 24)()
-    check(lib().cf_plan_digest(C.byref(md), C.byref(sd), C.byref(ro), rank, out))
+    fn = lib().cf_plan_digest_device if device else lib().cf_plan_digest
+    check(fn(C.byref(md), C.byref(sd), C.byref(ro), rank, out))
     return {k: int(out[i]) for i, k in enumerate(DIGEST_NAMES)}
+
+
+def partition_rcb_device(m: Mesh, parts: int) -> np.ndarray:
+    """partition_rcb computed on the B200 (equal to partition_rcb)."""
+    keep = _Keep()
+    md = mesh_desc(m, keep)
+    out = np.zeros(m.element_count(), np.int32)
+    check(lib().cf_partition_rcb_device(C.byref(md), int(parts), out.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out
+
+
+@dataclass
+class FixtureSpec:
+    """A structured fixture generated on the device (generate_fixture with perm_seed 0), and
+    its T0 rule: region T0 + U(-t0_noise, t0_noise) keyed by grid point (counter_uniform)."""
+    kind: str = "casting"
+    n: int = 32
+    radius: float = 0.35
+    jitter: float = 0.0
+    seed: int = 0
+    t0_noise: float = 0.0
+    noise_seed: int = 1
+
+    def desc(self) -> "_abi.cf_fixture_spec":
+        return _abi.cf_fixture_spec({"cube": 0, "casting": 1}[self.kind], int(self.n), float(self.radius),
+                                    float(self.jitter), int(self.seed), 0, float(self.t0_noise), int(self.noise_seed))
+
+    def mesh(self) -> Mesh:
+        """The same mesh on the host (cf_generate_fixture)."""
+        return generate_fixture(self.kind, self.n, radius=self.radius, jitter=self.jitter, seed=self.seed)
 
 
 def exchange_plan(m: Mesh, setup: SimulationSetup, world_size: int, rank: int,

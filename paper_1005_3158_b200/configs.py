@@ -14,8 +14,8 @@ from typing import Optional
 
 import numpy as np
 
-from .castfem import (BoundaryCondition, InterfaceCoeff, MaterialTable, Mesh, PiecewiseLinear, SimulationSetup,
-                      SolverConfig, counter_uniform, generate_fixture)
+from .castfem import (BoundaryCondition, FixtureSpec, InterfaceCoeff, MaterialTable, Mesh, PiecewiseLinear,
+                      SimulationSetup, SolverConfig, counter_uniform, generate_fixture)
 
 H_INTERFACE = 1000.0  # W/m^2K — builder-chosen, stated in every report
 
@@ -79,12 +79,38 @@ def casting(n: int, jitter: float = 0.0, seed: int = 0, perm_seed: int = 0, dt_s
     if noise:
         base = np.where(_node_region(m) == 0, aluminium().initial_temperature, sand().initial_temperature)
         T0 = base + counter_uniform(noise_seed, m.node_grid.astype(np.int64), -noise, noise)
-    setup = SimulationSetup(
+    return Case(name or f"casting{n}", m, casting_setup(dt_safety, h_interface, T0), steps)
+
+
+def casting_setup(dt_safety: float, h_interface: float = H_INTERFACE, T0: Optional[np.ndarray] = None
+                  ) -> SimulationSetup:
+    return SimulationSetup(
         materials=[aluminium(), sand()],
         boundary_conditions={"outer": BoundaryCondition("flux", h=20.0, t_inf=300.0)},
         interface_coeffs=[InterfaceCoeff("cast_if", "mold_if", "time", PiecewiseLinear.constant(h_interface))],
         solver=SolverConfig(dt_safety=dt_safety), initial_T=T0)
-    return Case(name or f"casting{n}", m, setup, steps)
+
+
+@dataclass
+class DeviceCase:
+    """A BASELINE config whose mesh is generated on the device (castfem.FixtureSpec): the
+    same mesh and T0 as the host-built Case of that name, without the mesh in host memory."""
+    name: str
+    spec: FixtureSpec
+    setup: SimulationSetup
+    steps: int
+
+
+def device_case(name: str) -> DeviceCase:
+    """cfg1, cfg2, cfg4, cfg5 (cfg3 permutes its numbering on the host: no device form)."""
+    if name == "cfg1":
+        setup = SimulationSetup(materials=[MaterialTable.make(rho=2700.0, c=900.0, k=200.0, T0=973.0)],
+                                boundary_conditions={"outer": BoundaryCondition("flux", h=100.0, t_inf=300.0)},
+                                solver=SolverConfig(dt_safety=DT_SAFETY["cfg1"]))
+        return DeviceCase("cfg1_cube32", FixtureSpec("cube", 32, t0_noise=1.0, noise_seed=1), setup, 100)
+    n, steps = {"cfg2": (128, 1000), "cfg4": (256, 500), "cfg5": (512, 200)}[name]
+    return DeviceCase(f"{name}_casting{n}", FixtureSpec("casting", n, radius=0.35, t0_noise=T0_NOISE, noise_seed=1),
+                      casting_setup(DT_SAFETY[name]), steps)
 
 
 def _node_region(m: Mesh) -> np.ndarray:

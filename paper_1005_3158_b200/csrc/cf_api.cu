@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "cf_devplan.hpp"
 #include "cf_internal.hpp"
 #include "cf_kernels.cuh"
 
@@ -111,12 +112,6 @@ struct cf_comm {
 // ------------------------------------------------------------------ plan
 namespace {
 
-template <class T>
-struct DBuf {
-    T* p = nullptr;
-    size_t n = 0;
-};
-
 struct DeviceMem {
     std::vector<void*> ptrs;
     int64_t bytes = 0;
@@ -188,6 +183,13 @@ struct DeviceMem {
         for (void* p : ptrs) cudaFree(p);
         ptrs.clear();
     }
+    void adopt(cfb::DBuf& b) {  // a device-built plan's allocations
+        ptrs.insert(ptrs.end(), b.p.begin(), b.p.end());
+        bytes += b.bytes;
+        b.p.clear();
+        b.sz.clear();
+        b.bytes = 0;
+    }
 };
 
 struct Rank {
@@ -228,6 +230,7 @@ struct Rank {
     int64_t bytes_per_step = 0;
     int64_t tile_bytes = 0;  // layout bytes of one tile-kernel launch
     int64_t update_bytes = 0;  // algorithmic bytes of the merge + update kernel per step
+    int64_t S_tot = 0, E_r = 0;  // slots, elements of this rank
     std::vector<int64_t> nb_send_len, nb_recv_len;
 };
 
@@ -261,6 +264,8 @@ struct cf_plan {
         step_parity ^= 1;
     }
     int32_t N_global = 0;
+    int64_t E_global = 0;
+    bool device_setup = false;
     double loop_seconds = 0;
     double eq13_min = 0;
     double base_min_bound = 0;   // min_e rho c(0) l^2 / k(0) (static dt before the safety factor)
@@ -616,41 +621,47 @@ void enqueue_step(cf_plan* p, double t_end) {
     p->advance();
 }
 
+// the device-resident arrays of one rank's plan (uploaded host plan or device-built plan)
+struct RankDev {
+    uint8_t* blob = nullptr;
+    int32_t* slot_node = nullptr;
+    const uint8_t* node_region = nullptr;
+    const int8_t* node_dir = nullptr;
+    const int32_t* local_global = nullptr;
+    int32_t* merge_off = nullptr;
+    int32_t* merge_idx = nullptr;
+    int32_t* shared_list = nullptr;
+    int4* shared_rec = nullptr;
+    int64_t n_shared_list = 0, merge_parts = 0, S_tot = 0, E_r = 0;
+    int32_t *node_shared = nullptr, *shared_off = nullptr, *shared_src = nullptr, *shared_src_r = nullptr,
+            *ghost_src = nullptr;
+};
+void finish_rank(cf_plan* p, Rank& r, const RankDev& d);
+
 void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
+    (void)S;
     RankPlan& h = r.H;
     DeviceMem& M = r.mem;
     cudaStream_t s = p->stream;
-    const int64_t S_tot = h.tile_slot_off.empty() ? 0 : h.tile_slot_off.back();
-    const int64_t Er = (int64_t)h.elem_global.size();
-    const int64_t nT = (int64_t)h.n_local + h.n_ghost;
-    const bool det = p->mode == CF_MODE_DETERMINISTIC;
-
-    r.T[0] = M.alloc<double>(nT);
-    r.T[1] = M.alloc<double>(nT);
-    r.T[2] = M.alloc<double>(nT);
-    r.Tslot[0] = M.alloc<double>(S_tot + 2);
-    r.Tslot[1] = M.alloc<double>(S_tot + 2);
-    r.st = M.alloc<DevState>(1);
-    TileArgs& a = r.ta;
-    a.meta = M.up(h.tile_meta, s);
-    a.slot_off = M.up(h.tile_slot_off, s);
-    a.blob_off = M.up(h.blob_off, s);
-    a.slot_node = M.up(h.slot_node, s);
+    RankDev d;
+    d.S_tot = h.tile_slot_off.empty() ? 0 : h.tile_slot_off.back();
+    d.E_r = (int64_t)h.elem_global.size();
+    d.slot_node = M.up(h.slot_node, s);
     {
         // device-side packing: the host staged only the non-geometry sections; the geometry
         // is computed here from the oriented tets and node coordinates (bitwise the host's)
         uint8_t* blob = M.alloc<uint8_t>((size_t)std::max<int64_t>(16, h.blob_bytes));
         DeviceMem tmp;
         FillArgs f{};
-        f.meta = a.meta;
-        f.blob_off = a.blob_off;
+        f.meta = tmp.up(h.tile_meta, s);
+        f.blob_off = tmp.up(h.blob_off, s);
         f.rest_off = tmp.up(h.rest_off, s);
         f.rest = tmp.up(h.blob, s);
         f.elem_off = tmp.up(h.elem_off, s);
         f.tets_ord = tmp.up(h.tets_ord, s);
         f.coords = tmp.up(h.coords_local, s);
-        f.slot_off = a.slot_off;
-        f.slot_node = a.slot_node;
+        f.slot_off = tmp.up(h.tile_slot_off, s);
+        f.slot_node = d.slot_node;
         f.blob = blob;
         f.tdep = p->temp_dep;
         f.coords_layout = h.coords;
@@ -658,13 +669,97 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
         CF_CUDA_CHECK(cudaGetLastError());
         CF_CUDA_CHECK(cudaStreamSynchronize(s));
         tmp.release();
-        a.blob = blob;
+        d.blob = blob;
         decltype(h.tets_ord)().swap(h.tets_ord);
         decltype(h.coords_local)().swap(h.coords_local);
     }
-    const uint8_t* node_region = M.up(h.node_region, s);
-    const int8_t* node_dir = h.node_dir.empty() ? nullptr : M.up(h.node_dir, s);
-    const int32_t* local_global = M.up(h.local_global, s);
+    d.node_region = M.up(h.node_region, s);
+    d.node_dir = h.node_dir.empty() ? nullptr : M.up(h.node_dir, s);
+    d.local_global = M.up(h.local_global, s);
+    d.merge_off = M.up(h.merge_off, s);
+    d.merge_idx = M.up(h.merge_idx, s);
+    d.shared_list = M.up(h.shared_list, s);
+    d.n_shared_list = (int64_t)h.shared_list.size();
+    {
+        std::vector<int4> rec(2 * std::max<size_t>(1, h.shared_list.size()));
+        for (size_t k = 0; k < h.shared_list.size(); ++k) {
+            const int32_t i = h.shared_list[k];
+            const int32_t b = h.merge_off[i], cnt = h.merge_off[i + 1] - b;
+            int32_t sl[4] = {0, 0, 0, 0};
+            for (int q = 0; q < 4 && q < cnt; ++q) sl[q] = h.merge_idx[b + q];
+            rec[2 * k] = make_int4(i, cnt, sl[0], sl[1]);
+            rec[2 * k + 1] = make_int4(sl[2], sl[3], 0, 0);
+            d.merge_parts += cnt;
+        }
+        d.shared_rec = M.up(rec, s);
+    }
+    if (p->world > 1) {
+        d.node_shared = M.up(h.node_shared, s);
+        d.shared_off = M.up(h.shared_off, s);
+        d.shared_src = M.up(h.shared_src, s);
+        d.shared_src_r = M.up(h.shared_src_r, s);
+        d.ghost_src = M.up(h.ghost_src, s);
+    }
+    CF_CUDA_CHECK(cudaStreamSynchronize(s));
+    finish_rank(p, r, d);
+    // drop the big host arrays (metadata kept)
+    decltype(h.blob)().swap(h.blob);
+    std::vector<int32_t>().swap(h.merge_idx);
+    std::vector<int32_t>().swap(h.slot_node);
+    std::vector<int32_t>().swap(h.elem_global);
+}
+
+// a device-built plan (cf_devplan.cu): its allocations move into the rank
+void adopt_rank(cf_plan* p, Rank& r, DevRankPlan& dp) {
+    r.H = std::move(dp.H);
+    RankDev d;
+    d.blob = dp.blob;
+    d.slot_node = dp.slot_node;
+    d.node_region = dp.node_region;
+    d.node_dir = dp.node_dir;
+    d.local_global = dp.local_global;
+    d.merge_off = dp.merge_off;
+    d.merge_idx = dp.merge_idx;
+    d.shared_list = dp.shared_list;
+    d.shared_rec = dp.shared_rec;
+    d.n_shared_list = dp.n_shared_list;
+    d.merge_parts = dp.merge_parts;
+    d.S_tot = dp.S_tot;
+    d.E_r = dp.E_r;
+    d.node_shared = dp.node_shared;
+    d.shared_off = dp.shared_off;
+    d.shared_src = dp.shared_src;
+    d.shared_src_r = dp.shared_src_r;
+    d.ghost_src = dp.ghost_src;
+    r.mem.adopt(dp.mem);
+    finish_rank(p, r, d);
+}
+
+void finish_rank(cf_plan* p, Rank& r, const RankDev& d) {
+    RankPlan& h = r.H;
+    DeviceMem& M = r.mem;
+    cudaStream_t s = p->stream;
+    const int64_t S_tot = d.S_tot;
+    const int64_t Er = d.E_r;
+    r.S_tot = S_tot;
+    r.E_r = Er;
+    const bool det = p->mode == CF_MODE_DETERMINISTIC;
+
+    r.T[0] = M.alloc<double>((size_t)h.n_local + h.n_ghost);
+    r.T[1] = M.alloc<double>((size_t)h.n_local + h.n_ghost);
+    r.T[2] = M.alloc<double>((size_t)h.n_local + h.n_ghost);
+    r.Tslot[0] = M.alloc<double>(S_tot + 2);
+    r.Tslot[1] = M.alloc<double>(S_tot + 2);
+    r.st = M.alloc<DevState>(1);
+    TileArgs& a = r.ta;
+    a.meta = M.up(h.tile_meta, s);
+    a.slot_off = M.up(h.tile_slot_off, s);
+    a.blob_off = M.up(h.blob_off, s);
+    a.slot_node = d.slot_node;
+    a.blob = d.blob;
+    const uint8_t* node_region = d.node_region;
+    const int8_t* node_dir = d.node_dir;
+    const int32_t* local_global = d.local_global;
     a.node_region = node_region;
     a.node_dir = node_dir;
     a.local_global = local_global;
@@ -812,8 +907,8 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
 #endif
     u.n_local = h.n_local;
     u.n_ghost = h.n_ghost;
-    u.merge_off = M.up(h.merge_off, s);  // partial merge (deterministic) + Tslot scatter (both modes)
-    u.merge_idx = M.up(h.merge_idx, s);
+    u.merge_off = d.merge_off;  // partial merge (deterministic) + Tslot scatter (both modes)
+    u.merge_idx = d.merge_idx;
     u.part = r.part;
     u.acc_c = r.acc_c;
     u.acc_r = r.acc_r;
@@ -822,32 +917,18 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     u.local_global = local_global;
     u.P = p->dP;
     u.st = r.st;
-    r.shared_list = M.up(h.shared_list, s);
-    r.n_shared_list = (int32_t)h.shared_list.size();
-    {
-        std::vector<int4> rec(2 * std::max<size_t>(1, h.shared_list.size()));
-        for (size_t k = 0; k < h.shared_list.size(); ++k) {
-            const int32_t i = h.shared_list[k];
-            const int32_t b = h.merge_off[i], cnt = h.merge_off[i + 1] - b;
-            int32_t sl[4] = {0, 0, 0, 0};
-            for (int q = 0; q < 4 && q < cnt; ++q) sl[q] = h.merge_idx[b + q];
-            rec[2 * k] = make_int4(i, cnt, sl[0], sl[1]);
-            rec[2 * k + 1] = make_int4(sl[2], sl[3], 0, 0);
-        }
-        int4* d = M.alloc<int4>(rec.size());
-        CF_CUDA_CHECK(cudaMemcpyAsync(d, rec.data(), rec.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
-        CF_CUDA_CHECK(cudaStreamSynchronize(s));
-        r.shared_rec = d;
-    }
+    r.shared_list = d.shared_list;
+    r.n_shared_list = (int32_t)d.n_shared_list;
+    r.shared_rec = d.shared_rec;
     if (p->world > 1) {
-        u.node_shared = M.up(h.node_shared, s);
-        u.shared_off = M.up(h.shared_off, s);
-        u.shared_src_c = M.up(h.shared_src, s);
-        u.shared_src_r = M.up(h.shared_src_r, s);
+        u.node_shared = d.node_shared;
+        u.shared_off = d.shared_off;
+        u.shared_src_c = d.shared_src;
+        u.shared_src_r = d.shared_src_r;
         r.recv = M.alloc<double>(h.recv_len);
         r.send = M.alloc<double>(h.send_len);
         u.recv = r.recv;
-        u.ghost_src = M.up(h.ghost_src, s);
+        u.ghost_src = d.ghost_src;
         std::vector<int32_t> cr_node, t_node;
         std::vector<int64_t> cr_dst, cr_dst_r, t_dst;
         for (size_t k = 0; k < h.nbrs.size(); ++k) {
@@ -889,19 +970,11 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
         // partial a 16 B read (deterministic; atomic: the node's two accumulators read + zeroed)
         // and the 8 B slot-copy write
         const bool all = p->temp_dep;
-        const int64_t nodes = all ? h.n_local : (int64_t)h.shared_list.size();
-        int64_t parts = 0;
-        if (all) {
-            parts = S_tot;
-        } else {
-            for (int32_t i : h.shared_list) parts += h.merge_off[i + 1] - h.merge_off[i];
-        }
+        const int64_t nodes = all ? h.n_local : d.n_shared_list;
+        const int64_t parts = all ? S_tot : d.merge_parts;
         r.update_bytes = nodes * (32 + 16) + parts * 8 + (det ? parts * 16 : nodes * 32);
     }
     CF_CUDA_CHECK(cudaStreamSynchronize(s));
-    // drop the big host arrays (metadata kept)
-    decltype(h.blob)().swap(h.blob);
-    std::vector<int32_t>().swap(h.merge_idx);
 }
 
 void scatter_state(cf_plan* p);
@@ -921,7 +994,7 @@ void scatter_state(cf_plan* p) {
         const int32_t nT = r.H.n_local + r.H.n_ghost;
         const int blocks = std::max(1, std::min(1184, (nT + 255) / 256));
         scatter_init_kernel<<<blocks, 256, 0, p->stream>>>(nT, r.ta.local_global, p->dTg, r.T[0], r.T[1], r.T[2]);
-        const int64_t S_tot = (int64_t)r.H.slot_node.size();
+        const int64_t S_tot = r.S_tot;
         const int sb = (int)std::max<int64_t>(1, std::min<int64_t>(1184, (S_tot + 255) / 256));
         slot_init_kernel<<<sb, 256, 0, p->stream>>>(S_tot, r.ta.slot_node, r.T[0], r.Tslot[0], r.Tslot[1]);
         if (r.acc_c) {  // atomic mode: no partial sums survive a re-initialisation
@@ -1173,164 +1246,288 @@ int cf_last_error(char* buf, size_t len) {
     return CF_OK;
 }
 
+}  // extern "C"
+
+namespace {
+struct FixtureArgs {  // cf_plan_create_fixture: the mesh generated on the device
+    int32_t kind, n;
+    double radius, jitter;
+    uint64_t seed;
+    double t0_noise;
+    uint64_t noise_seed;
+};
+
+cf_run_opts normalized_opts(const cf_run_opts* opts, int& tile) {
+    cf_run_opts o{};
+    o.world_size = 1;
+    o.local_ranks = 1;
+    o.node_order = CF_NODE_ORDER_RCM;
+    o.elem_order = CF_ELEM_ORDER_MORTON;
+    if (opts) o = *opts;
+    if (o.world_size < 1) o.world_size = 1;
+    if (o.local_ranks < 1) o.local_ranks = 1;
+    if (o.rank < 0 || o.rank + o.local_ranks > o.world_size) raise(CF_INVALID_ARG, "bad rank / local_ranks");
+    if (o.local_ranks != 1 && o.local_ranks != o.world_size)
+        raise(CF_INVALID_ARG, "local_ranks must be 1 or world_size");
+    if (o.mode != CF_MODE_ATOMIC && o.mode != CF_MODE_DETERMINISTIC) raise(CF_INVALID_ARG, "bad mode");
+    if (o.geometry != CF_GEOM_COORDS && o.geometry != CF_GEOM_STORED) raise(CF_INVALID_ARG, "bad geometry mode");
+    if (o.fast_math != 0) raise(CF_CONFIG, "fast_math is reserved (kernels are built without FMA contraction)");
+    tile = o.tile_elems > 0 ? o.tile_elems : 384;
+    if (tile > kMaxTileElems) raise(CF_INVALID_ARG, "tile_elems must be <= 2048");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) raise(CF_CUDA, "no CUDA device available");
+    if (o.device < 0 || o.device >= ndev) raise(CF_INVALID_ARG, "bad device ordinal");
+    CF_CUDA_CHECK(cudaSetDevice(o.device));
+    return o;
+}
+
+PlanOptions plan_options(const cf_run_opts& o, int tile) {
+    PlanOptions po;
+    po.mode = o.mode;
+    po.node_order = o.node_order;
+    po.elem_order = o.elem_order;
+    po.geometry = o.geometry;
+    po.tile_elems = tile;
+    po.tile_of_element = o.tile_of_element;
+    po.n_tiles_given = o.n_tiles_given;
+    po.world_size = o.world_size;
+    return po;
+}
+
+// the plan object before its ranks: streams, parameters, static dt bound
+std::unique_ptr<cf_plan> new_plan(const cf_run_opts& o, const cf_setup_desc* setup, const SetupData& S, int32_t N,
+                                  const std::vector<double>& region_min_edge) {
+    auto p = std::make_unique<cf_plan>();
+    p->device = o.device;
+    p->mode = o.mode;
+    if (const char* e = std::getenv("CF_TILE_THREADS")) {
+        const int v = std::atoi(e);
+        p->tile_threads = v == 256 ? 256 : 128;
+    }
+    if (const char* e = std::getenv("CF_TILE_STAGES")) p->stages = std::atoi(e) == 2 ? 2 : 1;
+    if (const char* e = std::getenv("CF_PDL")) p->pdl = std::atoi(e) != 0;
+    p->world = o.world_size;
+    p->first_rank = o.rank;
+    p->local_ranks = o.local_ranks;
+    p->comm = (cf_comm*)o.comm;
+    if (p->world > p->local_ranks && !p->comm) raise(CF_NCCL, "world_size > local_ranks needs a cf_comm");
+    p->P = S.P;
+    p->temp_dep = S.temp_dep;
+    p->finite_range = S.P.finite_range != 0;
+    p->N_global = N;
+    p->output_every = setup->output_every;
+    p->t_end_setup = setup->t_end;
+    CF_CUDA_CHECK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    CF_CUDA_CHECK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
+    CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming));
+    CF_CUDA_CHECK(cudaStreamCreateWithFlags(&p->xside, cudaStreamNonBlocking));
+    CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->xfork, cudaEventDisableTiming));
+    CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->xjoin, cudaEventDisableTiming));
+    CF_CUDA_CHECK(cudaEventCreate(&p->ev0));
+    CF_CUDA_CHECK(cudaEventCreate(&p->ev1));
+    CF_CUDA_CHECK(cudaMalloc(&p->dP, sizeof(DevParams)));
+    CF_CUDA_CHECK(cudaMemcpy(p->dP, &p->P, sizeof(DevParams), cudaMemcpyHostToDevice));
+    double e13 = INFINITY;  // monotone in the minimum edge per region (see resolve_setup)
+    for (int32_t rg = 0; rg < (int32_t)region_min_edge.size(); ++rg) {
+        if (!std::isfinite(region_min_edge[rg])) continue;
+        const DevMaterial& mm = S.P.mat[rg];
+        const double c0 = pl_eval(S.P, mm.c, 0), k0 = pl_eval(S.P, mm.k, 0), me = region_min_edge[rg];
+        e13 = std::min(e13, mm.rho * c0 * me * me / k0);
+    }
+    p->eq13_min = e13;
+    p->base_min_bound = S.min_bound;
+    return p;
+}
+
+// after the ranks: multi-rank state table, optional L2 window, host buffers, launch count
+void finish_plan(cf_plan* p) {
+    if (p->ranks.size() > 1) {
+        std::vector<DevState*> sts;
+        for (const auto& rk : p->ranks) sts.push_back(rk->st);
+        CF_CUDA_CHECK(cudaMalloc(&p->d_states, sizeof(DevState*) * sts.size()));
+        CF_CUDA_CHECK(cudaMemcpy(p->d_states, sts.data(), sizeof(DevState*) * sts.size(), cudaMemcpyHostToDevice));
+    }
+    // Optional L2 residency of the per-slot partials between their writer (tile kernel) and
+    // reader (update kernel), CF_L2_PERSIST=fraction. Measured on cfg2 and left off: update
+    // 0.049 -> 0.058 ms with the whole 67 MB persisting, tile kernel unchanged.
+    if (p->ranks.size() == 1 && p->ranks[0]->part) {
+        const char* e = std::getenv("CF_L2_PERSIST");
+        const double frac = e ? std::atof(e) : 0.0;
+        int max_win = 0, max_pers = 0;
+        cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, p->device);
+        cudaDeviceGetAttribute(&max_pers, cudaDevAttrMaxPersistingL2CacheSize, p->device);
+        const Rank& rk = *p->ranks[0];
+        const size_t bytes = sizeof(double2) * (size_t)rk.H.tile_slot_off.back();
+        if (frac > 0 && max_win > 0 && max_pers > 0 && bytes > 0) {
+            const size_t pers = std::min<size_t>((size_t)(frac * (double)bytes), (size_t)max_pers);
+            CF_CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, pers));
+            cudaStreamAttrValue v = {};
+            v.accessPolicyWindow.base_ptr = (void*)rk.part;
+            v.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, (size_t)max_win);
+            v.accessPolicyWindow.hitRatio =
+                (float)std::min(1.0, (double)pers / (double)v.accessPolicyWindow.num_bytes);
+            v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            CF_CUDA_CHECK(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+        }
+    }
+    if (p->host_comm()) {
+        const RankPlan& h = p->ranks[0]->H;
+        CF_CUDA_CHECK(cudaMallocHost(&p->h_send, sizeof(double) * std::max<int64_t>(1, h.send_len)));
+        CF_CUDA_CHECK(cudaMallocHost(&p->h_recv, sizeof(double) * std::max<int64_t>(1, h.recv_len)));
+    }
+    p->launches_per_step = 0;
+    for (const auto& rk : p->ranks)
+        p->launches_per_step += (int64_t)rk->launches.size() + 2 + (p->world > 1 ? 1 : 0);
+}
+
+bool use_device_setup(const cf_run_opts& o) {
+    const char* e = std::getenv("CF_HOST_SETUP");
+    if (e && std::atoi(e)) return false;
+    return !o.tile_of_element && o.partition != CF_PARTITION_GRAPH && o.world_size <= 64;
+}
+
+// host setup pipeline (cf_mesh.cpp / cf_plan.cpp): given block maps, graph partitions, > 64
+// ranks, or CF_HOST_SETUP=1
+void create_host(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts& o, int tile, cf_plan** out) {
+    trace_stage("plan_create: start");
+    MeshData m;
+    finalize_mesh(mesh, m);
+    SetupData S;
+    resolve_setup(m, setup, S);
+    trace_stage("resolve: rest");
+    std::vector<int32_t> label(m.N);
+    if (o.node_order == CF_NODE_ORDER_RCM) {
+        label = rcm_permutation_device(m.N, m.E, m.tets.data(), -1, o.device);  // the RCM pass on the B200
+    } else {
+        std::iota(label.begin(), label.end(), 0);
+    }
+    std::vector<int32_t> part;
+    PlanOptions po = plan_options(o, tile);
+    if (o.world_size > 1) {
+        if (o.partition == CF_PARTITION_GIVEN) {
+            if (!o.part_of_element) raise(CF_INVALID_ARG, "part_of_element required");
+            part.assign(o.part_of_element, o.part_of_element + m.E);
+            for (int32_t v : part)
+                if (v < 0 || v >= o.world_size) raise(CF_VALIDATION, "part id out of range");
+        } else if (o.partition == CF_PARTITION_GRAPH) {
+            part = partition_elements(m, o.world_size, 0.05, true);
+        } else {
+            part = partition_rcb(m, o.world_size);
+        }
+        po.part_of_element = part.data();
+    }
+    trace_stage("labels + partition");
+    auto p = new_plan(o, setup, S, m.N, m.region_min_edge);
+    p->E_global = m.E;
+    for (int r = o.rank; r < o.rank + o.local_ranks; ++r) {
+        auto rk = std::make_unique<Rank>();
+        rk->rank = r;
+        build_rank_plan(m, S, po, label, r, rk->H);
+        upload_rank(p.get(), *rk, S);
+        trace_stage("upload");
+        p->ranks.push_back(std::move(rk));
+    }
+    finish_plan(p.get());
+    init_state(p.get(), S.T0.data());
+    CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+    trace_stage("init state");
+    *out = p.release();
+}
+
+// device setup pipeline (cf_devplan.cu): the mesh lives only in device memory
+void create_device(const cf_mesh_desc* mesh, const FixtureArgs* fx, const cf_setup_desc* setup, const cf_run_opts& o,
+                   int tile, cf_plan** out) {
+    trace_stage("plan_create: start (device setup)");
+    cudaStream_t s;
+    CF_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SG {
+        cudaStream_t s;
+        ~SG() { cudaStreamDestroy(s); }
+    } sg{s};
+    DevMesh dm;
+    T0Noise noise;
+    if (fx) {
+        devmesh_fixture(fx->kind, fx->n, fx->radius, fx->jitter, fx->seed, s, dm);
+        noise.amp = fx->t0_noise;
+        noise.seed = fx->noise_seed;
+    } else {
+        devmesh_from_desc(mesh, s, dm);
+    }
+    trace_stage("device: mesh + finalize");
+    DevSetup ds;
+    resolve_setup_device(dm, setup, noise, s, ds);
+    trace_stage("device: resolve");
+    DBuf work;
+    int32_t* d_label = nullptr;
+    if (o.node_order == CF_NODE_ORDER_RCM) {
+        d_label = work.alloc<int32_t>(dm.N);
+        rcm_labels_device(dm.N, dm.E, dm.tets, -1, s, d_label);
+        trace_stage("device: rcm");
+    }
+    int32_t* d_part = nullptr;
+    if (o.world_size > 1) {
+        d_part = work.alloc<int32_t>(dm.E);
+        if (o.partition == CF_PARTITION_GIVEN) {
+            if (!o.part_of_element) raise(CF_INVALID_ARG, "part_of_element required");
+            for (int64_t e = 0; e < dm.E; ++e)
+                if (o.part_of_element[e] < 0 || o.part_of_element[e] >= o.world_size)
+                    raise(CF_VALIDATION, "part id out of range");
+            CF_CUDA_CHECK(cudaMemcpyAsync(d_part, o.part_of_element, sizeof(int32_t) * dm.E, cudaMemcpyHostToDevice, s));
+        } else {
+            partition_rcb_device(dm, o.world_size, s, d_part);
+        }
+        trace_stage("device: partition");
+    }
+    const PlanOptions po = plan_options(o, tile);
+    auto p = new_plan(o, setup, ds.S, dm.N, dm.region_min_edge);
+    p->E_global = dm.E;
+    p->device_setup = true;
+    for (int r = o.rank; r < o.rank + o.local_ranks; ++r) {
+        auto rk = std::make_unique<Rank>();
+        rk->rank = r;
+        DevRankPlan dp;
+        build_rank_plan_device(dm, ds, po, d_label, d_part, r, s, dp);
+        trace_stage("device: rank plan");
+        adopt_rank(p.get(), *rk, dp);
+        p->ranks.push_back(std::move(rk));
+    }
+    finish_plan(p.get());
+    if (!p->dTg) CF_CUDA_CHECK(cudaMalloc(&p->dTg, std::max<int64_t>(1, p->N_global) * sizeof(double)));
+    CF_CUDA_CHECK(cudaMemcpyAsync(p->dTg, ds.T0, (size_t)p->N_global * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CF_CUDA_CHECK(cudaStreamSynchronize(s));
+    scatter_state(p.get());
+    CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+    trace_stage("init state");
+    *out = p.release();
+}
+}  // namespace
+
+extern "C" {
 int cf_plan_create(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts, cf_plan** out) {
     return guarded([&] {
         if (!mesh || !setup || !out) raise(CF_INVALID_ARG, "null argument");
         *out = nullptr;
-        cf_run_opts o{};
-        o.world_size = 1;
-        o.local_ranks = 1;
-        o.node_order = CF_NODE_ORDER_RCM;
-        o.elem_order = CF_ELEM_ORDER_MORTON;
-        if (opts) o = *opts;
-        if (o.world_size < 1) o.world_size = 1;
-        if (o.local_ranks < 1) o.local_ranks = 1;
-        if (o.rank < 0 || o.rank + o.local_ranks > o.world_size) raise(CF_INVALID_ARG, "bad rank / local_ranks");
-        if (o.local_ranks != 1 && o.local_ranks != o.world_size)
-            raise(CF_INVALID_ARG, "local_ranks must be 1 or world_size");
-        if (o.mode != CF_MODE_ATOMIC && o.mode != CF_MODE_DETERMINISTIC) raise(CF_INVALID_ARG, "bad mode");
-        if (o.geometry != CF_GEOM_COORDS && o.geometry != CF_GEOM_STORED) raise(CF_INVALID_ARG, "bad geometry mode");
-        if (o.fast_math != 0) raise(CF_CONFIG, "fast_math is reserved (kernels are built without FMA contraction)");
-        int tile = o.tile_elems > 0 ? o.tile_elems : 384;
-        if (tile > kMaxTileElems) raise(CF_INVALID_ARG, "tile_elems must be <= 2048");
+        int tile = 384;
+        const cf_run_opts o = normalized_opts(opts, tile);
+        if (use_device_setup(o)) create_device(mesh, nullptr, setup, o, tile, out);
+        else create_host(mesh, setup, o, tile, out);
+    });
+}
 
-        int ndev = 0;
-        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) raise(CF_CUDA, "no CUDA device available");
-        if (o.device < 0 || o.device >= ndev) raise(CF_INVALID_ARG, "bad device ordinal");
-        CF_CUDA_CHECK(cudaSetDevice(o.device));
-
-        trace_stage("plan_create: start");
-        MeshData m;
-        finalize_mesh(mesh, m);
-        SetupData S;
-        resolve_setup(m, setup, S);
-        trace_stage("resolve: rest");
-
-        std::vector<int32_t> label(m.N);
-        if (o.node_order == CF_NODE_ORDER_RCM) {
-            label = rcm_permutation_device(m.N, m.E, m.tets.data(), -1, o.device);  // the RCM pass on the B200
-        } else {
-            std::iota(label.begin(), label.end(), 0);
-        }
-        std::vector<int32_t> part;
-        PlanOptions po;
-        po.mode = o.mode;
-        po.node_order = o.node_order;
-        po.elem_order = o.elem_order;
-        po.geometry = o.geometry;
-        po.tile_elems = tile;
-        po.tile_of_element = o.tile_of_element;
-        po.n_tiles_given = o.n_tiles_given;
-        po.world_size = o.world_size;
-        if (o.world_size > 1) {
-            if (o.partition == CF_PARTITION_GIVEN) {
-                if (!o.part_of_element) raise(CF_INVALID_ARG, "part_of_element required");
-                part.assign(o.part_of_element, o.part_of_element + m.E);
-                for (int32_t v : part)
-                    if (v < 0 || v >= o.world_size) raise(CF_VALIDATION, "part id out of range");
-            } else if (o.partition == CF_PARTITION_GRAPH) {
-                part = partition_elements(m, o.world_size, 0.05, true);
-            } else {
-                part = partition_rcb(m, o.world_size);
-            }
-            po.part_of_element = part.data();
-        }
-        trace_stage("labels + partition");
-
-        auto p = std::make_unique<cf_plan>();
-        p->device = o.device;
-        p->mode = o.mode;
-        if (const char* e = std::getenv("CF_TILE_THREADS")) {
-            const int v = std::atoi(e);
-            p->tile_threads = v == 256 ? 256 : 128;
-        }
-        if (const char* e = std::getenv("CF_TILE_STAGES")) p->stages = std::atoi(e) == 2 ? 2 : 1;
-        if (const char* e = std::getenv("CF_PDL")) p->pdl = std::atoi(e) != 0;
-        p->world = o.world_size;
-        p->first_rank = o.rank;
-        p->local_ranks = o.local_ranks;
-        p->comm = (cf_comm*)o.comm;
-        if (p->world > p->local_ranks && !p->comm) raise(CF_NCCL, "world_size > local_ranks needs a cf_comm");
-        p->P = S.P;
-        p->temp_dep = S.temp_dep;
-        p->finite_range = S.P.finite_range != 0;
-        p->N_global = m.N;
-        p->output_every = setup->output_every;
-        p->t_end_setup = setup->t_end;
-        CF_CUDA_CHECK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-        CF_CUDA_CHECK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
-        CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
-        CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming));
-        CF_CUDA_CHECK(cudaStreamCreateWithFlags(&p->xside, cudaStreamNonBlocking));
-        CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->xfork, cudaEventDisableTiming));
-        CF_CUDA_CHECK(cudaEventCreateWithFlags(&p->xjoin, cudaEventDisableTiming));
-        CF_CUDA_CHECK(cudaEventCreate(&p->ev0));
-        CF_CUDA_CHECK(cudaEventCreate(&p->ev1));
-        CF_CUDA_CHECK(cudaMalloc(&p->dP, sizeof(DevParams)));
-        CF_CUDA_CHECK(cudaMemcpy(p->dP, &p->P, sizeof(DevParams), cudaMemcpyHostToDevice));
-        double e13 = INFINITY;  // monotone in the minimum edge per region (see resolve_setup)
-        for (int32_t rg = 0; rg < (int32_t)m.region_min_edge.size(); ++rg) {
-            if (!std::isfinite(m.region_min_edge[rg])) continue;
-            const DevMaterial& mm = S.P.mat[rg];
-            const double c0 = pl_eval(S.P, mm.c, 0), k0 = pl_eval(S.P, mm.k, 0), me = m.region_min_edge[rg];
-            e13 = std::min(e13, mm.rho * c0 * me * me / k0);
-        }
-        p->eq13_min = e13;
-        p->base_min_bound = S.min_bound;
-        for (int r = o.rank; r < o.rank + o.local_ranks; ++r) {
-            auto rk = std::make_unique<Rank>();
-            rk->rank = r;
-            build_rank_plan(m, S, po, label, r, rk->H);
-            upload_rank(p.get(), *rk, S);
-            trace_stage("upload");
-            p->ranks.push_back(std::move(rk));
-        }
-        if (p->ranks.size() > 1) {
-            std::vector<DevState*> sts;
-            for (const auto& rk : p->ranks) sts.push_back(rk->st);
-            CF_CUDA_CHECK(cudaMalloc(&p->d_states, sizeof(DevState*) * sts.size()));
-            CF_CUDA_CHECK(cudaMemcpy(p->d_states, sts.data(), sizeof(DevState*) * sts.size(), cudaMemcpyHostToDevice));
-        }
-        // Optional L2 residency of the per-slot partials between their writer (tile kernel) and
-        // reader (update kernel), CF_L2_PERSIST=fraction. Measured on cfg2 and left off: update
-        // 0.049 -> 0.058 ms with the whole 67 MB persisting, tile kernel unchanged.
-        if (p->ranks.size() == 1 && p->ranks[0]->part) {
-            const char* e = std::getenv("CF_L2_PERSIST");
-            const double frac = e ? std::atof(e) : 0.0;
-            int max_win = 0, max_pers = 0;
-            cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, p->device);
-            cudaDeviceGetAttribute(&max_pers, cudaDevAttrMaxPersistingL2CacheSize, p->device);
-            const Rank& rk = *p->ranks[0];
-            const size_t bytes = sizeof(double2) * (size_t)rk.H.tile_slot_off.back();
-            if (frac > 0 && max_win > 0 && max_pers > 0 && bytes > 0) {
-                const size_t pers = std::min<size_t>((size_t)(frac * (double)bytes), (size_t)max_pers);
-                CF_CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, pers));
-                cudaStreamAttrValue v = {};
-                v.accessPolicyWindow.base_ptr = (void*)rk.part;
-                v.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, (size_t)max_win);
-                v.accessPolicyWindow.hitRatio =
-                    (float)std::min(1.0, (double)pers / (double)v.accessPolicyWindow.num_bytes);
-                v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-                v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-                CF_CUDA_CHECK(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
-                if (std::getenv("CF_TRACE_SETUP") && std::atoi(std::getenv("CF_TRACE_SETUP")))
-                    std::fprintf(stderr, "[cf setup] L2 persisting window: partials %zu B, window max %d B, "
-                                 "persisting max %d B, hit ratio %.2f\n", bytes, max_win, max_pers,
-                                 (double)v.accessPolicyWindow.hitRatio);
-            }
-        }
-        if (p->host_comm()) {
-            const RankPlan& h = p->ranks[0]->H;
-            CF_CUDA_CHECK(cudaMallocHost(&p->h_send, sizeof(double) * std::max<int64_t>(1, h.send_len)));
-            CF_CUDA_CHECK(cudaMallocHost(&p->h_recv, sizeof(double) * std::max<int64_t>(1, h.recv_len)));
-        }
-        p->launches_per_step = 0;
-        for (const auto& rk : p->ranks)
-            p->launches_per_step += (int64_t)rk->launches.size() + 2 + (p->world > 1 ? 1 : 0);
-        init_state(p.get(), S.T0.data());
-        CF_CUDA_CHECK(cudaStreamSynchronize(p->stream));
-        trace_stage("init state");
-        *out = p.release();
+int cf_plan_create_fixture(const cf_fixture_spec* fx, const cf_setup_desc* setup, const cf_run_opts* opts,
+                           cf_plan** out) {
+    return guarded([&] {
+        if (!fx || !setup || !out) raise(CF_INVALID_ARG, "null argument");
+        if (fx->perm_seed != 0) raise(CF_INVALID_ARG, "device fixtures keep the generator numbering (perm_seed 0)");
+        *out = nullptr;
+        int tile = 384;
+        const cf_run_opts o = normalized_opts(opts, tile);
+        if (o.tile_of_element || o.partition == CF_PARTITION_GRAPH || o.world_size > 64)
+            raise(CF_INVALID_ARG, "device fixtures need RCB or given partitions and no given tile map");
+        const FixtureArgs a{fx->kind, fx->n, fx->radius, fx->jitter, fx->seed, fx->t0_noise, fx->noise_seed};
+        create_device(nullptr, &a, setup, o, tile, out);
     });
 }
 
@@ -1530,7 +1727,7 @@ int cf_get_stats(cf_plan* p, cf_stats* out) {
         out->dynamic_dt = p->temp_dep;
         for (auto& r : p->ranks) {
             out->n_tiles += r->H.n_tiles;
-            out->n_elems_local += (int64_t)r->H.elem_global.size();
+            out->n_elems_local += r->E_r;
             out->n_nodes_local += r->H.n_local;
             out->total_slots += r->H.tile_slot_off.empty() ? 0 : r->H.tile_slot_off.back();
             out->n_shared_nodes += r->H.n_shared;
@@ -1541,6 +1738,9 @@ int cf_get_stats(cf_plan* p, cf_stats* out) {
             out->update_bytes_per_step += r->update_bytes;
         }
         out->launches_per_step = p->launches_per_step;
+        out->n_nodes_global = p->N_global;
+        out->n_elems_global = p->E_global;
+        out->device_setup = p->device_setup ? 1 : 0;
     });
 }
 
@@ -1993,6 +2193,64 @@ int cf_plan_digest(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const c
         RankPlan rp;
         build_rank_plan(m, S, po, label, rank, rp);
         digest_rank_plan(rp, digest);
+    });
+}
+
+// the same digests from the device setup pipeline (needs a B200)
+int cf_plan_digest_device(const cf_mesh_desc* mesh, const cf_setup_desc* setup, const cf_run_opts* opts, int32_t rank,
+                          uint64_t* digest) {
+    return guarded([&] {
+        if (!mesh || !setup || !opts || !digest) raise(CF_INVALID_ARG, "null argument");
+        int tile = 384;
+        cf_run_opts o = normalized_opts(opts, tile);
+        cudaStream_t s;
+        CF_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct SG {
+            cudaStream_t s;
+            ~SG() { cudaStreamDestroy(s); }
+        } sg{s};
+        DevMesh dm;
+        devmesh_from_desc(mesh, s, dm);
+        DevSetup ds;
+        resolve_setup_device(dm, setup, T0Noise{}, s, ds);
+        DBuf work;
+        int32_t* d_label = nullptr;
+        if (o.node_order == CF_NODE_ORDER_RCM) {
+            d_label = work.alloc<int32_t>(dm.N);
+            rcm_labels_device(dm.N, dm.E, dm.tets, -1, s, d_label);
+        }
+        int32_t* d_part = nullptr;
+        if (o.world_size > 1) {
+            d_part = work.alloc<int32_t>(dm.E);
+            if (o.partition == CF_PARTITION_GIVEN && o.part_of_element)
+                CF_CUDA_CHECK(cudaMemcpyAsync(d_part, o.part_of_element, sizeof(int32_t) * dm.E, cudaMemcpyHostToDevice, s));
+            else
+                partition_rcb_device(dm, o.world_size, s, d_part);
+        }
+        DevRankPlan dp;
+        build_rank_plan_device(dm, ds, plan_options(o, tile), d_label, d_part, rank, s, dp);
+        RankPlan rp;
+        download_dev_rank_plan(dp, ds.S.temp_dep, o.geometry == CF_GEOM_COORDS, s, rp);
+        digest_rank_plan(rp, digest);
+    });
+}
+
+// device partition (test instrumentation: equal to cf_partition_rcb)
+int cf_partition_rcb_device(const cf_mesh_desc* mesh, int32_t parts, int32_t* out) {
+    return guarded([&] {
+        if (!mesh || !out) raise(CF_INVALID_ARG, "null argument");
+        cudaStream_t s;
+        CF_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct SG {
+            cudaStream_t s;
+            ~SG() { cudaStreamDestroy(s); }
+        } sg{s};
+        DevMesh dm;
+        devmesh_from_desc(mesh, s, dm);
+        DBuf work;
+        int32_t* d = work.alloc<int32_t>(dm.E);
+        partition_rcb_device(dm, parts, s, d);
+        CF_CUDA_CHECK(cudaMemcpy(out, d, sizeof(int32_t) * dm.E, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -177,8 +177,18 @@ struct SetupData {
     std::vector<int32_t> pair_of_facet; // [F]
     bool temp_dep = false;
     double min_bound = 0;               // min_e rho c l^2 / k before the safety factor
+    bool static_dt_only = false;        // node arrays not built here (device setup)
+    std::vector<int32_t> kind_of_tag;   // [tags] facet kind per tag (-1 - dirichlet id), INT32_MIN unused
 };
 void resolve_setup(const MeshData& m, const cf_setup_desc* s, SetupData& out);
+// the same with the element-region facts given (device meshes: m holds only the facet part)
+// and, node_arrays false, without the O(N) dir_of_node / T0 arrays
+struct RegionUse {
+    int32_t first_bad_region = -1;  // region of the first element whose region has no material
+    uint32_t mask = 0;              // regions in use
+};
+void resolve_setup_impl(const MeshData& m, const cf_setup_desc* s, SetupData& out, const RegionUse* ru,
+                        bool node_arrays);
 double pl_eval(const DevParams& P, const DevTable& t, double x);
 double enthalpy(const DevParams& P, const DevMaterial& m, double T);
 

@@ -369,20 +369,14 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         double* R = (double*)(smem + a.scratch_off);  // coordinates layout only
         const uint8_t* ereg = B + L.region;
         const uint8_t* gblob = a.blob + hdr[stage].boff;  // this tile's blob in global memory
-#ifdef CF_EXP_HOIST
         // the tile's section offsets in registers for the whole element loop (the layout lives in
         // shared memory, which the loop's contribution stores may alias)
         const ushort4* connp = (const ushort4*)(B + L.conn);
         const double2* G2p = (const double2*)(B + L.geom);
         const uint8_t* metail = gblob + L.bytes;
-#endif
         for (int i = tid; i < ((CF_PRB(a) & 15) == 4 ? 0 : ne); i += kTileThreads) {
             double g[4][3], vol, max_edge = 0;
-#ifdef CF_EXP_HOIST
             const ushort4 cn = connp[i];
-#else
-            const ushort4 cn = ((const ushort4*)(B + L.conn))[i];
-#endif
             if (GC) {
                 const double2* X = (const double2*)(B + L.xyz);  // slot (x, y) (z, 0)
                 const unsigned short sl[4] = {cn.x, cn.y, cn.z, cn.w};
@@ -397,11 +391,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                 dev_tet_grads(p, g, vol);
                 max_edge = ((const double*)(B + L.geom))[i];
             } else {
-#ifdef CF_EXP_HOIST
                 const double2* G2 = G2p;
-#else
-                const double2* G2 = (const double2*)(B + L.geom);
-#endif
                 const double2 c0 = G2[i], c1 = G2[S + i], c2 = G2[2 * S + i], c3 = G2[3 * S + i],
                               c4 = G2[4 * S + i];
                 g[1][0] = c0.x;
@@ -422,15 +412,9 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             const double H[4] = {th0.y, th1.y, th2.y, th3.y};
             const DevMaterial& m = sMat[ereg[i]];
             double lump, rc[4];
-#ifdef CF_EXP_HOIST
             dev_element<TDEP, !GC>(
                 P, m, g, vol, [&]() { return GC ? max_edge : __ldg((const double*)metail + i); },
                 T, H, lump, rc, (CF_PRB(a) & 15) == 7);
-#else
-            dev_element<TDEP, !GC>(
-                P, m, g, vol, [&]() { return GC ? max_edge : __ldg((const double*)(gblob + L.max_edge_of(i))); },
-                T, H, lump, rc, (CF_PRB(a) & 15) == 7);
-#endif
             if (TDEP)
                 local_min = fmin(local_min, dev_stable_bound<TDEP>(P, m, ((const double*)(B + L.minedge))[i], T));
             if (GC) {
@@ -505,38 +489,6 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             const int beg = s == 0 ? 0 : cend[s - 1];
             const int end = cend[s];
             double c = 0, r = 0;
-#ifdef CF_EXP_PF
-            if (!GC && beg < end) {
-                // software-pipelined: the next group's codes and operand pairs are loaded before
-                // this group's in-order sums (the sums' order is the list's: bitwise unchanged)
-                uint2 pr = *(const uint2*)(csr + beg);
-                double2 w0 = W[pr.x & 0xffffu], w1 = W[pr.x >> 16], w2 = W[pr.y & 0xffffu], w3 = W[pr.y >> 16];
-                for (int jj = beg + 4;; jj += 4) {
-                    const bool more = jj < end;
-                    double2 n0, n1, n2, n3;
-                    if (more) {
-                        const uint2 pn = *(const uint2*)(csr + jj);
-                        n0 = W[pn.x & 0xffffu];
-                        n1 = W[pn.x >> 16];
-                        n2 = W[pn.y & 0xffffu];
-                        n3 = W[pn.y >> 16];
-                    }
-                    c += w0.x;
-                    r -= w0.y;
-                    c += w1.x;
-                    r -= w1.y;
-                    c += w2.x;
-                    r -= w2.y;
-                    c += w3.x;
-                    r -= w3.y;
-                    if (!more) break;
-                    w0 = n0;
-                    w1 = n1;
-                    w2 = n2;
-                    w3 = n3;
-                }
-            } else
-#endif
             for (int j = beg; j < end; j += 4) {  // lists padded to 4 with exact (0.0, 0.0) no-ops
                 const uint2 pr = *(const uint2*)(csr + j);
                 const uint32_t v[4] = {pr.x & 0xffffu, pr.x >> 16, pr.y & 0xffffu, pr.y >> 16};
@@ -776,26 +728,6 @@ __global__ void advance_kernel(DevState* st, const DevParams* __restrict__ P, do
 }
 
 // ------------------------------------------------------------------ plan upload (device-side packing)
-// tet_geometry (cf_mesh.cpp / geometry.hpp:48-77) on the device: edges first (min/max of the six
-// lengths, first pair (0,1) seeding both, as std::min/std::max), then the gradients and volume.
-__device__ __forceinline__ void dev_tet_geometry(const double (&p)[4][3], double (&g)[4][3], double& vol,
-                                                 double& min_edge, double& max_edge) {
-    double d0 = p[1][0] - p[0][0], d1 = p[1][1] - p[0][1], d2 = p[1][2] - p[0][2];
-    min_edge = max_edge = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = a + 1; b < 4; ++b) {
-            d0 = p[b][0] - p[a][0];
-            d1 = p[b][1] - p[a][1];
-            d2 = p[b][2] - p[a][2];
-            const double len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-            min_edge = len < min_edge ? len : min_edge;
-            max_edge = max_edge < len ? len : max_edge;
-        }
-    dev_tet_grads(p, g, vol);
-}
-
 struct FillArgs {
     const TileMeta* meta;
     const int64_t* blob_off;

@@ -100,6 +100,26 @@ __device__ __forceinline__ void dev_tet_grads(const double (&p)[4][3], double (&
     for (int k = 0; k < 3; ++k) g[0][k] = ((g[1][k] + g[2][k]) + g[3][k]) * -1.0;
 }
 
+// tet_geometry (cf_mesh.cpp / geometry.hpp:48-77) on the device: edges first (min/max of the six
+// lengths, first pair (0,1) seeding both, as std::min/std::max), then the gradients and volume.
+__device__ __forceinline__ void dev_tet_geometry(const double (&p)[4][3], double (&g)[4][3], double& vol,
+                                                 double& min_edge, double& max_edge) {
+    double d0 = p[1][0] - p[0][0], d1 = p[1][1] - p[0][1], d2 = p[1][2] - p[0][2];
+    min_edge = max_edge = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = a + 1; b < 4; ++b) {
+            d0 = p[b][0] - p[a][0];
+            d1 = p[b][1] - p[a][1];
+            d2 = p[b][2] - p[a][2];
+            const double len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+            min_edge = len < min_edge ? len : min_edge;
+            max_edge = max_edge < len ? len : max_edge;
+        }
+    dev_tet_grads(p, g, vol);
+}
+
 // One element: lumped capacitance share `lump` (added to each of the 4
 // nodes) and the 4 conduction residual terms rc[a] (subtracted).
 // g1..g3 are the stored gradients; g0 = (g1+g2+g3)*-1.0 (geometry.hpp:75).

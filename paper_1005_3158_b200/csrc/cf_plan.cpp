@@ -84,6 +84,11 @@ bool name_eq(const char* a, const std::string& b) { return a && b == a; }
 }  // namespace
 
 void resolve_setup(const MeshData& m, const cf_setup_desc* s, SetupData& out) {
+    resolve_setup_impl(m, s, out, nullptr, true);
+}
+
+void resolve_setup_impl(const MeshData& m, const cf_setup_desc* s, SetupData& out, const RegionUse* ru,
+                        bool node_arrays) {
     if (!s) raise(CF_INVALID_ARG, "null setup");
     if ((s->n_materials && !s->materials) || (s->n_bcs && !s->bcs) || (s->n_coeffs && !s->coeffs))
         raise(CF_INVALID_ARG, "null array in setup descriptor");
@@ -105,13 +110,18 @@ void resolve_setup(const MeshData& m, const cf_setup_desc* s, SetupData& out) {
     for (size_t p = 0; p < out.pairs.size(); ++p) out.pair_of_facet[out.pairs[p].facet] = (int32_t)p;
 
     // materials of used regions (MaterialTable::finalize)
-    for (int32_t e = 0; e < m.E; ++e)
-        if (m.region[e] >= s->n_materials)
-            raise(CF_CONFIG, "no material for region " + std::to_string(m.region[e]));
-    if (s->n_materials > kMaxRegions) raise(CF_CONFIG, "more than 16 material regions");
     std::vector<char> used(s->n_materials + 1, 0);
-    for (int32_t r = 0; r < m.region_count; ++r) used[r] = 0;
-    for (int32_t e = 0; e < m.E; ++e) used[m.region[e]] = 1;
+    if (!ru) {
+        for (int32_t e = 0; e < m.E; ++e)
+            if (m.region[e] >= s->n_materials)
+                raise(CF_CONFIG, "no material for region " + std::to_string(m.region[e]));
+        if (s->n_materials > kMaxRegions) raise(CF_CONFIG, "more than 16 material regions");
+        for (int32_t e = 0; e < m.E; ++e) used[m.region[e]] = 1;
+    } else {
+        if (ru->first_bad_region >= 0) raise(CF_CONFIG, "no material for region " + std::to_string(ru->first_bad_region));
+        if (s->n_materials > kMaxRegions) raise(CF_CONFIG, "more than 16 material regions");
+        for (int r = 0; r < s->n_materials && r < 32; ++r) used[r] = (ru->mask >> r) & 1;
+    }
     P.n_materials = s->n_materials;
     for (int r = 0; r < s->n_materials; ++r) {
         const cf_material& c = s->materials[r];
@@ -227,12 +237,16 @@ void resolve_setup(const MeshData& m, const cf_setup_desc* s, SetupData& out) {
             kind_of_tag[t] = kind_of_coeff[coeff];
         }
     }
+    out.kind_of_tag = kind_of_tag;
     out.facet_kind.resize(m.F);
     for (int32_t f = 0; f < m.F; ++f) {
         out.facet_kind[f] = kind_of_tag[m.facet_tag[f]];
         if (out.facet_kind[f] >= 0 && P.kind[out.facet_kind[f]].interface && out.pair_of_facet[f] < 0)
             raise(CF_CONFIG, "interface facet " + std::to_string(f) + " has no sister pairing; call pair_sister_facets");
     }
+    if (!node_arrays) {
+        out.static_dt_only = true;
+    } else {
     // Dirichlet nodes: lowest tag wins
     out.dir_of_node.assign(m.N, -1);
     std::vector<int32_t> best_tag(m.N, INT32_MAX);
@@ -253,6 +267,7 @@ void resolve_setup(const MeshData& m, const cf_setup_desc* s, SetupData& out) {
     for (int32_t n = 0; n < m.N; ++n) {
         out.T0[n] = s->initial_T ? s->initial_T[n] : s->materials[m.node_region[n]].initial_temperature;
         if (out.dir_of_node[n] >= 0) out.T0[n] = pl_eval(P, P.dir_tab[out.dir_of_node[n]], 0.0);
+    }
     }
     // static dt (blocked.hpp:340-350): min_e rho c(0) l^2 / k(0). For constant
     // properties the bound is monotone in the element's minimum edge (also

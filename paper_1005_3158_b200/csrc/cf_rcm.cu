@@ -324,20 +324,11 @@ unsigned grid_for(int64_t n, int threads = 256) {
 
 }  // namespace
 
-std::vector<int32_t> rcm_permutation_device(int32_t N, int64_t E, const int32_t* tets_host, int32_t seed, int device) {
-    std::vector<int32_t> new_of_old(N);
-    if (N == 0) return new_of_old;
-    RCM_CHECK(cudaSetDevice(device));
-    cudaStream_t s;
-    RCM_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    struct StreamGuard {
-        cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
-    } sg{s};
+// the pass over device-resident tets; new_of_old: device array [N] (the labels)
+void rcm_labels_device(int32_t N, int64_t E, const int32_t* tets, int32_t seed, cudaStream_t s, int32_t* new_of_old) {
+    if (N == 0) return;
     DevBuf B;
     // ---- node graph (build_node_graph reorder.hpp:17-24) on the device
-    int32_t* tets = B.alloc<int32_t>(4 * (size_t)E);
-    RCM_CHECK(cudaMemcpyAsync(tets, tets_host, 4 * (size_t)E * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     int32_t* icnt = B.alloc<int32_t>(N);
     RCM_CHECK(cudaMemsetAsync(icnt, 0, (size_t)N * sizeof(int32_t), s));
     incidence_count<<<grid_for(4 * E), 256, 0, s>>>(E, tets, icnt);
@@ -363,7 +354,6 @@ std::vector<int32_t> rcm_permutation_device(int32_t N, int64_t E, const int32_t*
     RCM_CHECK(cudaStreamSynchronize(s));
     B.free(n2e);
     B.free(ioff);
-    B.free(tets);
 
     // ---- BFS state
     int32_t* seen = B.alloc<int32_t>(N);
@@ -479,9 +469,27 @@ std::vector<int32_t> rcm_permutation_device(int32_t N, int64_t E, const int32_t*
         }
         placed = le;
     }
-    int32_t* labels = B.alloc<int32_t>(N);
-    reverse_labels<<<grid_for(N), 256, 0, s>>>(N, order, labels);
+    reverse_labels<<<grid_for(N), 256, 0, s>>>(N, order, new_of_old);
     RCM_CHECK(cudaGetLastError());
+    RCM_CHECK(cudaStreamSynchronize(s));
+}
+
+std::vector<int32_t> rcm_permutation_device(int32_t N, int64_t E, const int32_t* tets_host, int32_t seed, int device) {
+    std::vector<int32_t> new_of_old(N);
+    if (N == 0) return new_of_old;
+    RCM_CHECK(cudaSetDevice(device));
+    cudaStream_t s;
+    RCM_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{s};
+    DevBuf B;
+    int32_t* tets = B.alloc<int32_t>(4 * (size_t)E);
+    RCM_CHECK(cudaMemcpyAsync(tets, tets_host, 4 * (size_t)E * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    int32_t* labels = B.alloc<int32_t>(N);
+    rcm_labels_device(N, E, tets, seed, s, labels);
+    B.free(tets);
     RCM_CHECK(cudaMemcpyAsync(new_of_old.data(), labels, (size_t)N * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     RCM_CHECK(cudaStreamSynchronize(s));
     return new_of_old;

@@ -4,7 +4,7 @@
 CFG=${CFG:-cfg4}
 run() {  # name lib budget
     local out
-    out=$(CF_TRACE_SETUP=1 CF_LIB_PATH=paper_1005_3158_b200/$2 ${3:+CF_SMEM_BUDGET=$3} python bench.py --config $CFG \
+    out=$(env CF_TRACE_SETUP=1 CF_LIB_PATH=paper_1005_3158_b200/$2 ${3:+CF_SMEM_BUDGET=$3} python bench.py --config $CFG \
         --node-order tile --compare-order none --no-cpu-baseline --no-e2e --steps ${STEPS:-60} --warmup 5 \
         --phase-steps 20 2> gpurun_out/exp_$1.err)
     echo "$1 $(echo "$out" | python -c 'import json,sys; d=json.loads(sys.stdin.read()); r=d["roofline"]; print(round(d["value"]/1e9,3), "G/s tile", r["kernel_ms"], "upd", r["update_ms"], "frac", r["frac"], "step8", r["step_frac_of_8tbs"], "tiles", d["tiles"])') $(grep -o '[0-9]* CTAs/SM' gpurun_out/exp_$1.err | head -1)"

@@ -60,11 +60,16 @@ def parse():
     ap.add_argument("--elem-order", default="morton")
     ap.add_argument("--geometry", default="stored", choices=["stored", "coords"],
                     help="tile layout: slot coordinates (gradients recomputed) or stored ElementGeom")
-    ap.add_argument("--node-order", default="rcm",
-                    help="rcm: BASELINE configs[1] ('RCM-reordered'; configs[4] = config 2's setup), by the "
-                         "device RCM pass; tile: first touch in tile order; given")
-    ap.add_argument("--compare-order", default="tile",
-                    help="a second node ordering measured side by side (K steps, same mesh); 'none' to skip")
+    ap.add_argument("--node-order", default="tile",
+                    help="the plan's local node numbering: tile (first touch in tile order, the B200 layout), "
+                         "rcm (local ids in RCM label order) or given. cfg2's MESH is RCM-reordered (BASELINE "
+                         "configs[1] 'RCM-reordered'): the generated mesh is renumbered by the device RCM pass "
+                         "(permute_mesh(m, rcm_permutation(m))), in both arms; --mesh-rcm / --no-mesh-rcm override")
+    ap.add_argument("--compare-order", default="rcm",
+                    help="a second local numbering measured side by side (K steps, same mesh); 'none' to skip")
+    ap.add_argument("--mesh-rcm", dest="mesh_rcm", action="store_true", default=None,
+                    help="RCM-reorder the mesh (both arms); default: cfg2 only (the config that names it)")
+    ap.add_argument("--no-mesh-rcm", dest="mesh_rcm", action="store_false")
     ap.add_argument("--cpu-steps", type=int, default=int(os.environ.get("CF_CPU_STEPS", "5")))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-blocked", action="store_true",
@@ -93,7 +98,11 @@ def dist_env():
         os.environ.get("LOCAL_RANK", "0"))
 
 
-def make_case(cfg: str, world: int, casting_n: int = 0, weak: bool = False):
+def mesh_rcm_default(cfg: str, flag) -> bool:
+    return (cfg == "cfg2") if flag is None else bool(flag)
+
+
+def make_case(cfg: str, world: int, casting_n: int = 0, weak: bool = False, mesh_rcm: bool = False):
     from paper_1005_3158_b200 import configs
     if casting_n:
         return configs.casting(casting_n, dt_safety=configs.DT_SAFETY["cfg2"], steps=100,
@@ -102,6 +111,10 @@ def make_case(cfg: str, world: int, casting_n: int = 0, weak: bool = False):
         n = int(round(128 * world ** (1.0 / 3.0)))
         return configs.casting(n, dt_safety=configs.DT_SAFETY["cfg4"], steps=500, name=f"casting{n}"), \
             f"weak_casting{n}", "weak"
+    if cfg in ("cfg1", "cfg2", "cfg4", "cfg5") and not os.environ.get("CF_BENCH_HOST_MESH"):
+        # the mesh is generated on the device (cf_plan_create_fixture): the same fixture and T0 as
+        # the host-built case, without ~20 GB of host mesh per process at cfg5
+        return configs.device_case(cfg, rcm=mesh_rcm), cfg, "strong" if world > 1 else "weak"
     return configs.CONFIGS[cfg](), cfg, "strong" if world > 1 else "weak"
 
 
@@ -116,7 +129,8 @@ REF_WINDOW = {"cfg4": [0, 256, 0, 256, 112, 144],   # 256 x 256 x 32 cells = 12,
 REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
 
 
-def reference_sample(cfg: str, steps: int, warmup: int, blocks: int = 1, autotune=None, window="default"):
+def reference_sample(cfg: str, steps: int, warmup: int, blocks: int = 1, autotune=None, window="default",
+                     rcm: bool = False):
     """Runs the reference solver on the host (oracle/_ref/ref_bench, its own process: the
     unmodified castfem headers and the oracle's workload generator; no product library)."""
     if not os.path.exists(REF_BENCH):
@@ -127,20 +141,23 @@ def reference_sample(cfg: str, steps: int, warmup: int, blocks: int = 1, autotun
         cmd += ["--window", f"{w[0]}:{w[1]},{w[2]}:{w[3]},{w[4]}:{w[5]}"]
     if autotune:
         cmd += ["--autotune", ",".join(map(str, autotune))]
+    if rcm:  # RCM-reordered mesh (the reference's own rcm_permutation + permute_mesh)
+        cmd += ["--rcm"]
     out = subprocess.run(cmd, capture_output=True, text=True)
     if out.returncode != 0:
         return None, f"ref_bench failed ({out.returncode}): {out.stderr.strip()[-300:]}"
     r = json.loads(out.stdout.strip().splitlines()[-1])
     what = (f"z-slab window cells {w[0]}:{w[1]} x {w[2]}:{w[3]} x {w[4]}:{w[5]} of the {cfg} mesh (same h, "
             f"regions, interface, T0 and dt; adiabatic cut planes)" if w else f"the full {cfg} mesh")
+    what += ", RCM-reordered (the reference's rcm_permutation + permute_mesh)" if r.get("rcm") else ""
     r["sample"] = (f"{r['steps']} blocked_step calls after {r['warmup']} warm-up on {what}: E={r['elements']}, "
                    f"{r['blocks']} cache block(s); setup {r['setup_seconds']:.1f}s excluded (loop_seconds, "
                    f"blocked.hpp:673-684); serial by contract (SPEC S:403-408)")
     return r, None
 
 
-def cpu_reference_rate(cfg: str, steps: int):
-    r, err = reference_sample(cfg, steps, 1)
+def cpu_reference_rate(cfg: str, steps: int, rcm: bool = False):
+    r, err = reference_sample(cfg, steps, 1, rcm=rcm)
     if r is None:
         return {"error": err}
     return {"value": r["element_updates_per_s"], "unit": "element-updates/s", "cores": 1, "kind": "reference",
@@ -161,14 +178,16 @@ def run_reference(args):
         return
     cfg = args.config
     steps, warmup = max(1, min(args.steps, 20)), min(args.warmup, 2)
-    r, err = reference_sample(cfg, steps, warmup)
+    rcm = mesh_rcm_default(cfg, args.mesh_rcm)
+    r, err = reference_sample(cfg, steps, warmup, rcm=rcm)
     if r is None:
         print(json.dumps({"impl": "reference", "unavailable": err}), flush=True)
         return
     blocked = None
     if args.ref_blocked:  # the paper's technique: the reference's own cache blocking, autotuned
         b, berr = reference_sample(cfg, steps, warmup, autotune=[1, 16, 64, 256],
-                                   window=[0, 512, 0, 512, 255, 257] if cfg == "cfg5" else "default")
+                                   window=[0, 512, 0, 512, 255, 257] if cfg == "cfg5" else "default",
+                                   rcm=rcm)
         blocked = b if b is not None else {"error": berr}
     assert not _maps_product_library(), "the reference arm must not load the product library"
     value = r["element_updates_per_s"]
@@ -276,8 +295,11 @@ def main():
         pg = dist
     from paper_1005_3158_b200 import castfem as cf
 
-    case, cfg, scaling = make_case(args.config, world, args.casting, args.weak)
-    mesh, setup = case.mesh, case.setup
+    mesh_rcm = mesh_rcm_default(args.config, args.mesh_rcm)
+    case, cfg, scaling = make_case(args.config, world, args.casting, args.weak, mesh_rcm)
+    setup = case.setup
+    spec = getattr(case, "spec", None)  # device-generated mesh
+    mesh = None if spec is not None else case.mesh
     comm = None
     if world > 1:
         import torch
@@ -289,10 +311,12 @@ def main():
                            node_order=args.node_order, device=local_rank, world_size=world, rank=rank,
                            comm=comm, graph_steps=args.graph)
     t0 = time.time()
-    solver = cf.Solver(mesh, setup, opts)
+    solver = cf.Solver(mesh, setup, opts, fixture=spec)
     setup_s = time.time() - t0
     st0 = solver.stats()
-    E_total = mesh.element_count()
+    E_total = int(st0.n_elems_global)
+    N_total = int(st0.n_nodes_global)
+    T0_global = solver.fields(want_H=False)[0] if not args.no_e2e else None  # initial_temperatures
 
     def barrier():
         if pg:
@@ -359,12 +383,10 @@ def main():
     # e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        T0src = np.ascontiguousarray(case.setup.initial_T if case.setup.initial_T is not None else
-                                     np.array([setup.materials[r].initial_temperature for r in
-                                               _node_regions(mesh)]), dtype=np.float64)
+        T0src = T0_global
         # pinned host buffers (the contract's host side): input T0, outputs T and H
         import torch
-        pin = lambda: torch.empty(mesh.node_count(), dtype=torch.float64, pin_memory=True).numpy()
+        pin = lambda: torch.empty(N_total, dtype=torch.float64, pin_memory=True).numpy()
         T0, Tout, Hout = pin(), pin(), pin()
         T0[:] = T0src
         # one untimed pass warms the path (first launches of the scatter / gather kernels load
@@ -378,7 +400,7 @@ def main():
         solver.step(args.steps)
         T, H = solver.fields(out=(Tout, Hout))
         e_secs = max_over_ranks(time.perf_counter() - t1)
-        nb = mesh.node_count() * 8
+        nb = N_total * 8
         e2e = {"value": E_total * args.steps / e_secs, "unit": "element-updates/s",
                "h2d_bytes_per_step": nb / args.steps, "d2h_bytes_per_step": 2 * nb / args.steps,
                "h2d_bytes_per_call": nb, "d2h_bytes_per_call": 2 * nb, "steps_per_call": args.steps,
@@ -392,7 +414,7 @@ def main():
     if args.compare_order not in ("none", "", args.node_order):
         o2 = cf.SolveOptions(**{**opts.__dict__, "node_order": args.compare_order})
         t2 = time.time()
-        s2 = cf.Solver(mesh, setup, o2)
+        s2 = cf.Solver(mesh, setup, o2, fixture=spec)
         setup2 = time.time() - t2
         s2.step(max(args.warmup, 3))
         barrier()
@@ -408,7 +430,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_rate(cfg, args.cpu_steps)
+            cpu = cpu_reference_rate(cfg, args.cpu_steps, rcm=mesh_rcm)
         except Exception as e:  # reported, not fatal
             cpu = {"error": str(e)}
 
@@ -417,12 +439,17 @@ def main():
                 "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded Kuhn-split casting fixtures, SURVEY §8(d))",
-                "config": {"workload": cfg, "elements": E_total, "nodes": mesh.node_count(),
+                "config": {"workload": cfg, "elements": E_total, "nodes": N_total,
+                           "mesh_source": "generated on the device (cf_plan_create_fixture)" if spec is not None
+                           else "host arrays (cf_plan_create)",
+                           "mesh_numbering": "RCM (device pass: permute_mesh(m, rcm_permutation(m)))"
+                           if spec is not None and spec.rcm else "generator",
                            "hex_cells": E_total // 6, "mode": args.mode, "tile_elems": args.tile,
                            "elem_order": args.elem_order, "node_order": args.node_order,
                            "geometry": args.geometry,
                            "dt_safety": setup.solver.dt_safety, "h_interface": 1000.0,
                            "parallelism": f"rcb{world}" if world > 1 else "single",
+                           "setup_pipeline": "device" if st0.device_setup else "host",
                            "l2": "working set > 126 MB L2 (no flush needed)" if st.bytes_per_step > 2e8
                            else "working set L2-resident", "setup_seconds": round(setup_s, 2)},
                 "hex_cell_updates_per_s": value / 6.0,
@@ -439,12 +466,6 @@ def main():
         comm.close()
     if pg:
         pg.destroy_process_group()
-
-
-def _node_regions(mesh):
-    reg = np.zeros(mesh.node_count(), np.int32)
-    reg[mesh.tets.reshape(-1)] = np.repeat(mesh.region, 4)
-    return reg
 
 
 if __name__ == "__main__":

@@ -394,6 +394,9 @@ typedef struct cf_fixture_spec {
     uint64_t seed, perm_seed;  /* perm_seed must be 0 */
     double t0_noise;
     uint64_t noise_seed;
+    int32_t rcm;            /* 1: node numbering permuted by the RCM pass (permute_mesh(m,
+                               rcm_permutation(m)), reorder.hpp:127-163), like an RCM-reordered
+                               input mesh */
 } cf_fixture_spec;
 int cf_plan_create_fixture(const cf_fixture_spec* fx, const cf_setup_desc* setup,
                            const cf_run_opts* opts, cf_plan** out);

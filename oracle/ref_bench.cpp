@@ -14,6 +14,7 @@
 // usage: ref_bench --workload cfg1..cfg5 [--window i0:i1,j0:j1,k0:k1] [--steps K] [--warmup W]
 //                  [--blocks B | --autotune c1,c2,...] [--tune-steps S] [--describe] [--dump-T file]
 #include <castfem/blocked.hpp>
+#include <castfem/reorder.hpp>
 
 #include <chrono>
 #include <cinttypes>
@@ -81,6 +82,7 @@ int main(int argc, char** argv) {
     int32_t window[6];
     bool have_window = false, describe = false;
     long steps = 10, warmup = 1, blocks = 1, tune_steps = 3;
+    bool rcm = false;  // RCM-reordered mesh: permute_mesh(m, rcm_permutation(build_node_graph(m)))
     std::vector<idx> candidates;
     for (int a = 1; a < argc; ++a) {
         const std::string k = argv[a];
@@ -94,6 +96,7 @@ int main(int argc, char** argv) {
         else if (k == "--blocks") blocks = std::atol(val().c_str());
         else if (k == "--tune-steps") tune_steps = std::atol(val().c_str());
         else if (k == "--describe") describe = true;
+        else if (k == "--rcm") rcm = true;
         else if (k == "--dump-T") dump = val();
         else if (k == "--autotune") {
             std::string v = val();
@@ -158,6 +161,13 @@ int main(int argc, char** argv) {
     std::vector<int32_t>().swap(tets);
     std::vector<int32_t>().swap(facets);
     finalize_mesh(m);
+    if (rcm) {  // BASELINE configs[1] "RCM-reordered" (the reference's own pass, reorder.hpp:127-163)
+        const auto perm = rcm_permutation(build_node_graph(m));
+        m = permute_mesh(m, perm);
+        std::vector<int32_t> g2(grid.size());
+        for (size_t i = 0; i < grid.size(); ++i) g2[perm[i]] = grid[i];
+        grid.swap(g2);
+    }
 
     // ---- BASELINE physics
     SimulationSetup setup;
@@ -242,12 +252,12 @@ int main(int argc, char** argv) {
     }
     cand_json += "]";
     sec_json += "]";
-    std::printf("{\"workload\": \"%s\", \"window\": %s, \"elements\": %d, \"nodes\": %d, \"facets\": %d, "
+    std::printf("{\"workload\": \"%s\", \"rcm\": %s, \"window\": %s, \"elements\": %d, \"nodes\": %d, \"facets\": %d, "
                 "\"interface_pairs\": %zu, \"blocks\": %ld, \"warmup\": %ld, \"steps\": %ld, \"seconds\": %.9g, "
                 "\"setup_seconds\": %.3f, \"element_updates_per_s\": %.9g, \"dt\": %.17g, \"time\": %.17g, "
                 "\"T_sum\": %.17g, \"T_min\": %.17g, \"T_max\": %.17g, \"clamp_steps\": %ld, "
                 "\"autotune\": {\"candidates\": %s, \"seconds\": %s, \"tune_seconds\": %.3f}}\n",
-                W->name,
+                W->name, rcm ? "true" : "false",
                 have_window ? ("\"" + std::to_string(window[0]) + ":" + std::to_string(window[1]) + "," +
                                std::to_string(window[2]) + ":" + std::to_string(window[3]) + "," +
                                std::to_string(window[4]) + ":" + std::to_string(window[5]) + "\"").c_str()

@@ -86,7 +86,8 @@ class cf_fixture(C.Structure):
 
 class cf_fixture_spec(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("radius", C.c_double), ("jitter", C.c_double),
-                ("seed", C.c_uint64), ("perm_seed", C.c_uint64), ("t0_noise", C.c_double), ("noise_seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("perm_seed", C.c_uint64), ("t0_noise", C.c_double), ("noise_seed", C.c_uint64),
+                ("rcm", C.c_int32)]
 
 
 CF_REDUCE_MIN, CF_REDUCE_MAX = 0, 1

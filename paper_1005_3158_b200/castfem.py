@@ -678,14 +678,17 @@ class FixtureSpec:
     seed: int = 0
     t0_noise: float = 0.0
     noise_seed: int = 1
+    rcm: bool = False       # node numbering permuted by the RCM pass (an RCM-reordered mesh)
 
     def desc(self) -> "_abi.cf_fixture_spec":
         return _abi.cf_fixture_spec({"cube": 0, "casting": 1}[self.kind], int(self.n), float(self.radius),
-                                    float(self.jitter), int(self.seed), 0, float(self.t0_noise), int(self.noise_seed))
+                                    float(self.jitter), int(self.seed), 0, float(self.t0_noise), int(self.noise_seed),
+                                    int(self.rcm))
 
     def mesh(self) -> Mesh:
-        """The same mesh on the host (cf_generate_fixture)."""
-        return generate_fixture(self.kind, self.n, radius=self.radius, jitter=self.jitter, seed=self.seed)
+        """The same mesh on the host (cf_generate_fixture, then permute_mesh by rcm_permutation)."""
+        m = generate_fixture(self.kind, self.n, radius=self.radius, jitter=self.jitter, seed=self.seed)
+        return permute_mesh(m, rcm_permutation(m)) if self.rcm else m
 
 
 def exchange_plan(m: Mesh, setup: SimulationSetup, world_size: int, rank: int,

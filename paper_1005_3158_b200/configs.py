@@ -101,16 +101,20 @@ class DeviceCase:
     steps: int
 
 
-def device_case(name: str) -> DeviceCase:
-    """cfg1, cfg2, cfg4, cfg5 (cfg3 permutes its numbering on the host: no device form)."""
+def device_case(name: str, rcm: Optional[bool] = None) -> DeviceCase:
+    """cfg1, cfg2, cfg4, cfg5 (cfg3 permutes its numbering on the host: no device form). cfg2 is
+    RCM-reordered as configs[1] states: the generated mesh's nodes renumbered by the device RCM
+    pass, permute_mesh(m, rcm_permutation(m)); the other configs name no ordering and keep the
+    generator's (rcm overrides)."""
     if name == "cfg1":
         setup = SimulationSetup(materials=[MaterialTable.make(rho=2700.0, c=900.0, k=200.0, T0=973.0)],
                                 boundary_conditions={"outer": BoundaryCondition("flux", h=100.0, t_inf=300.0)},
                                 solver=SolverConfig(dt_safety=DT_SAFETY["cfg1"]))
         return DeviceCase("cfg1_cube32", FixtureSpec("cube", 32, t0_noise=1.0, noise_seed=1), setup, 100)
     n, steps = {"cfg2": (128, 1000), "cfg4": (256, 500), "cfg5": (512, 200)}[name]
-    return DeviceCase(f"{name}_casting{n}", FixtureSpec("casting", n, radius=0.35, t0_noise=T0_NOISE, noise_seed=1),
-                      casting_setup(DT_SAFETY[name]), steps)
+    spec = FixtureSpec("casting", n, radius=0.35, t0_noise=T0_NOISE, noise_seed=1,
+                       rcm=(name == "cfg2") if rcm is None else rcm)
+    return DeviceCase(f"{name}_casting{n}", spec, casting_setup(DT_SAFETY[name]), steps)
 
 
 def _node_region(m: Mesh) -> np.ndarray:

@@ -1255,6 +1255,7 @@ struct FixtureArgs {  // cf_plan_create_fixture: the mesh generated on the devic
     uint64_t seed;
     double t0_noise;
     uint64_t noise_seed;
+    int32_t rcm;
 };
 
 cf_run_opts normalized_opts(const cf_run_opts* opts, int& tile) {
@@ -1449,7 +1450,7 @@ void create_device(const cf_mesh_desc* mesh, const FixtureArgs* fx, const cf_set
     DevMesh dm;
     T0Noise noise;
     if (fx) {
-        devmesh_fixture(fx->kind, fx->n, fx->radius, fx->jitter, fx->seed, s, dm);
+        devmesh_fixture(fx->kind, fx->n, fx->radius, fx->jitter, fx->seed, fx->rcm != 0, s, dm);
         noise.amp = fx->t0_noise;
         noise.seed = fx->noise_seed;
     } else {
@@ -1526,7 +1527,7 @@ int cf_plan_create_fixture(const cf_fixture_spec* fx, const cf_setup_desc* setup
         const cf_run_opts o = normalized_opts(opts, tile);
         if (o.tile_of_element || o.partition == CF_PARTITION_GRAPH || o.world_size > 64)
             raise(CF_INVALID_ARG, "device fixtures need RCB or given partitions and no given tile map");
-        const FixtureArgs a{fx->kind, fx->n, fx->radius, fx->jitter, fx->seed, fx->t0_noise, fx->noise_seed};
+        const FixtureArgs a{fx->kind, fx->n, fx->radius, fx->jitter, fx->seed, fx->t0_noise, fx->noise_seed, fx->rcm};
         create_device(nullptr, &a, setup, o, tile, out);
     });
 }

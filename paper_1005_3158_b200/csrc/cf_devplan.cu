@@ -492,7 +492,25 @@ void devmesh_from_desc(const cf_mesh_desc* d, cudaStream_t s, DevMesh& m) {
     }
 }
 
-void devmesh_fixture(int kind, int n, double radius, double jitter, uint64_t seed, cudaStream_t s, DevMesh& m) {
+namespace {
+// permute_mesh reorder.hpp:152-163: node p moves to new_of_old[p]
+__global__ void k_permute_nodes(int64_t N, const int32_t* p, const double* X, const int32_t* grid, double* X2,
+                                int32_t* grid2) {
+    GRID_STRIDE(n, N) {
+        const int64_t q = p[n];
+        X2[3 * q] = X[3 * n];
+        X2[3 * q + 1] = X[3 * n + 1];
+        X2[3 * q + 2] = X[3 * n + 2];
+        if (grid) grid2[q] = grid[n];
+    }
+}
+__global__ void k_relabel(int64_t n, const int32_t* p, int32_t* ids) {
+    GRID_STRIDE(i, n) ids[i] = p[ids[i]];
+}
+}  // namespace
+
+void devmesh_fixture(int kind, int n, double radius, double jitter, uint64_t seed, bool rcm, cudaStream_t s,
+                     DevMesh& m) {
     if (n < 1 || n > 1024) raise(CF_INVALID_ARG, "fixture n out of range [1, 1024]");
     if (kind != 0 && kind != 1) raise(CF_INVALID_ARG, "fixture kind must be 0 (cube) or 1 (casting)");
     FixSpec sp{};
@@ -531,6 +549,22 @@ void devmesh_fixture(int kind, int n, double radius, double jitter, uint64_t see
     k_fx_coords<<<grid_of(G), 256, 0, s>>>(sp, G, first, m.coords, m.node_grid);
     k_fx_cells<<<grid_of(C, 128), 128, 0, s>>>(sp, C, first, foff, m.tets, m.region, m.facets, ftag);
     DP_CHECK(cudaGetLastError());
+    if (rcm) {  // the generated mesh renumbered by rcm_permutation (the reference's preprocessing)
+        DBuf P;
+        int32_t* lab = P.alloc<int32_t>(N);
+        rcm_labels_device(N, E, m.tets, -1, s, lab);
+        double* X2 = m.mem.alloc<double>(3 * (size_t)N);
+        int32_t* g2 = m.mem.alloc<int32_t>(N);
+        k_permute_nodes<<<grid_of(N), 256, 0, s>>>(N, lab, m.coords, m.node_grid, X2, g2);
+        k_relabel<<<grid_of(4 * E), 256, 0, s>>>(4 * E, lab, m.tets);
+        if (F) k_relabel<<<grid_of(3 * (int64_t)F), 256, 0, s>>>(3 * (int64_t)F, lab, m.facets);
+        DP_CHECK(cudaGetLastError());
+        DP_CHECK(cudaStreamSynchronize(s));
+        m.mem.free(m.coords);
+        m.mem.free(m.node_grid);
+        m.coords = X2;
+        m.node_grid = g2;
+    }
     m.h_facets.resize(3 * (size_t)F);
     m.h_facet_tag.resize(F);
     d2h(m.h_facets.data(), m.facets, 3 * (size_t)F, s);

@@ -76,8 +76,10 @@ struct DevMesh {
 // upload + validate/orient on the device; any defect is re-diagnosed by the host finalize_mesh,
 // which raises the reference's exact error
 void devmesh_from_desc(const cf_mesh_desc* d, cudaStream_t s, DevMesh& m);
-// generate_fixture on the device (perm_seed 0): same coordinates, numbering, tets, facets
-void devmesh_fixture(int kind, int n, double radius, double jitter, uint64_t seed, cudaStream_t s, DevMesh& m);
+// generate_fixture on the device (perm_seed 0): same coordinates, numbering, tets, facets;
+// rcm: then renumbered by the RCM pass (permute_mesh(m, rcm_permutation(m)), reorder.hpp:127-163)
+void devmesh_fixture(int kind, int n, double radius, double jitter, uint64_t seed, bool rcm, cudaStream_t s,
+                     DevMesh& m);
 
 // resolved setup over a device mesh: tables, facet kinds, sister pairs on the host (O(F));
 // Dirichlet node ids and T0 on the device (O(N))

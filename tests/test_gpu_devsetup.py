@@ -124,3 +124,21 @@ def test_device_pipeline_reports_the_host_errors(defect, monkeypatch):
             cf.Solver(m, case.setup, cf.SolveOptions())
         msgs.append((type(ei.value), str(ei.value)))
     assert msgs[0] == msgs[1]
+
+
+def test_rcm_fixture_is_the_permuted_host_mesh():
+    """FixtureSpec(rcm=True): the device fixture renumbered by the device RCM pass equals
+    permute_mesh(host fixture, rcm_permutation) -- plan and 20 steps bitwise."""
+    spec = cf.FixtureSpec("casting", 18, t0_noise=1.0, noise_seed=1, rcm=True)
+    base = configs.casting(18, dt_safety=0.13)
+    p = cf.rcm_permutation(base.mesh)
+    m = cf.permute_mesh(base.mesh, p)
+    T0 = np.empty_like(base.setup.initial_T)
+    T0[p] = base.setup.initial_T
+    o = cf.SolveOptions(max_steps=20, node_order="tile")
+    with cf.Solver(None, configs.casting_setup(0.13), o, fixture=spec) as s:
+        assert np.array_equal(s.fields(want_H=False)[0], T0)
+        s.step(20)
+        Td = s.fields(want_H=False)[0]
+    ref = cf.solve(m, configs.casting_setup(0.13, T0=T0), o)
+    assert np.array_equal(Td, ref.T)

@@ -484,11 +484,12 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         const uint16_t* csr = (const uint16_t*)(B + L.csr);
         const int32_t* snode = (const int32_t*)(B + L.snode);
         const double2* W = (const double2*)B;
-        for (int j = tid; j < ((CF_PRB(a) & 15) == 3 ? 0 : ns); j += kTileThreads) {
-            const int s = sperm[j];  // threads take slots by list length (similar trip counts per warp)
+        // per-slot reduction (reads the tile's shared memory) ...
+        auto reduce = [&](int s, double& c, double& r) {
             const int beg = s == 0 ? 0 : cend[s - 1];
             const int end = cend[s];
-            double c = 0, r = 0;
+            c = 0;
+            r = 0;
             for (int j = beg; j < end; j += 4) {  // lists padded to 4 with exact (0.0, 0.0) no-ops
                 const uint2 pr = *(const uint2*)(csr + j);
                 const uint32_t v[4] = {pr.x & 0xffffu, pr.x >> 16, pr.y & 0xffffu, pr.y >> 16};
@@ -516,16 +517,17 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                     r -= q[k];
                 }
             }
-            const int info = sinfo[s];
-            const int32_t node = snode[s];
+        };
+        // ... and its flush (global memory only, so it may follow the next tile's copy issue)
+        auto flush = [&](int s, double c, double r, int info, int32_t node, double Ts) {
             if (FUSE && (info & 0x80)) {
                 // tile-private node: its merge is the identity, update it now
                 double Tn;
                 if (done) {
-                    Tn = sT[s];
+                    Tn = Ts;
                 } else {
                     const int dir = (DIR && (info & 0x40)) ? a.node_dir[node] : -1;
-                    Tn = node_update<DIR, CLAMP>(P, a.st, sT[s], c, r, dt, t_next, dir, info & 0x3f,
+                    Tn = node_update<DIR, CLAMP>(P, a.st, Ts, c, r, dt, t_next, dir, info & 0x3f,
                                                  a.local_global + node, clamped);
                 }
                 a.Tn[node] = Tn;
@@ -536,19 +538,51 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                 atomicAdd(&a.acc_c[node], c);
                 atomicAdd(&a.acc_r[node], r);
             }
+        };
+        // the first slot of every thread keeps its result in registers and flushes after the next
+        // tile's copy is issued; further slots (tiles of > 128 slots) flush inline
+        const int nred = (CF_PRB(a) & 15) == 3 ? 0 : ns;
+        constexpr int KD = 1;
+        double kc[KD], kr[KD], kT[KD];
+        int ks[KD], kinfo[KD];
+        int32_t knode[KD];
+        bool kv[KD];
+#pragma unroll
+        for (int k = 0; k < KD; ++k) {
+            const int j = tid + k * kTileThreads;
+            kv[k] = j < nred;
+            if (kv[k]) {
+                const int sl = sperm[j];  // threads take slots by list length (similar trip counts per warp)
+                ks[k] = sl;
+                reduce(sl, kc[k], kr[k]);
+                kinfo[k] = sinfo[sl];
+                knode[k] = snode[sl];
+                kT[k] = sT[sl];
+            }
+        }
+        for (int j = tid + KD * kTileThreads; j < nred; j += kTileThreads) {
+            const int sl = sperm[j];
+            double c, r;
+            reduce(sl, c, r);
+            flush(sl, c, r, sinfo[sl], snode[sl], sT[sl]);
         }
         const int t_issue = s_issue;  // written before the phase-1 barrier
-        const int t_next = dyn ? t_issue : t_follow;
-        if (t_next >= a.n_tiles) break;  // last tile of this CTA: no trailing barrier
-        __syncthreads();  // stage buffer and sT/sH free again; s_issue read by every thread
-        t = t_next;
-        if (tid == 0 && t_issue < a.n_tiles) {
-            // generic-proxy writes to B (in-place contributions) must be ordered
-            // before the async-proxy (TMA) overwrite of the same buffer
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            staged_desc(ndesc, nd0, nd1);
-            issue_tile_copy(a, nd0, nd1, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
+        const int t_nxt = dyn ? t_issue : t_follow;
+        if (t_nxt < a.n_tiles) {
+            __syncthreads();  // stage buffer and sT/sH free again; s_issue read by every thread
+            if (tid == 0 && t_issue < a.n_tiles) {
+                // generic-proxy writes to B (in-place contributions) must be ordered
+                // before the async-proxy (TMA) overwrite of the same buffer
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                staged_desc(ndesc, nd0, nd1);
+                issue_tile_copy(a, nd0, nd1, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
+            }
         }
+#pragma unroll
+        for (int k = 0; k < KD; ++k)
+            if (kv[k]) flush(ks[k], kc[k], kr[k], kinfo[k], knode[k], kT[k]);
+        if (t_nxt >= a.n_tiles) break;  // last tile of this CTA: no trailing barrier
+        t = t_nxt;
     }
     if (TDEP) {
         for (int o = 16; o > 0; o >>= 1) local_min = fmin(local_min, __shfl_xor_sync(0xffffffffu, local_min, o));

@@ -14,6 +14,7 @@ for v in ${VARIANTS:-base hoist pf both}; do
     run $v $lib ""
 done
 for v in ${VARIANTS5:-base m5 m5x}; do
+    [ "$v" = none ] && continue
     lib=libcastfem_b200_$v.so; [ $v = base ] && lib=libcastfem_b200.so
     run ${v}_b43 $lib 43700
 done

@@ -164,6 +164,7 @@ struct TileArgs {
                          // L2-resident tiles (compute-side time)
     double t_end;
     int32_t* sched;            // dynamic tile scheduling counter (persistent single-stage grids), or null
+    int32_t slot_gather;       // 1: slot temperatures gathered from T by node id (no slot copies)
 };
 
 constexpr uint32_t kBulkChunk = 32768;
@@ -200,12 +201,36 @@ __device__ __forceinline__ void issue_tile_copy(const TileArgs& a, int4 d0, int4
         const uint32_t n = (uint32_t)(bytes - o < (int32_t)kBulkChunk ? bytes - o : (int32_t)kBulkChunk);
         bulk_g2s(dst + o, src + o, n, bar);
     }
+    if (a.slot_gather) {
+        hdr->tm = tm;
+        hdr->s0 = s0;
+        hdr->boff = boff;
+        *reinterpret_cast<TileLayout*>(hdr->L) = TileLayout(tm, tdep, coords);
+        mbar_expect_tx(bar, (uint32_t)bytes);
+        return;
+    }
     if (slots && tbytes) bulk_g2s(sTdst, a.Tslot + s0, tbytes, bar);
     hdr->tm = tm;
     hdr->s0 = s0;
     hdr->boff = boff;
     *reinterpret_cast<TileLayout*>(hdr->L) = TileLayout(tm, tdep, coords);
     mbar_expect_tx(bar, (uint32_t)bytes + tbytes);
+}
+// slot temperatures gathered from the node array by the tile's slot node ids (read from the
+// tile's blob in global memory, so the gathers need not wait for its bulk copy): one 8-byte
+// cp.async per slot into sTdst, one commit group per thread (possibly empty)
+template <int NT>
+__device__ __forceinline__ void gather_slot_T(const TileArgs& a, int4 d0, int4 d1, bool tdep, bool coords, double* sTdst,
+                                              int tid) {
+    const TileMeta tm{d0.x, d0.y, d0.z, d0.w};
+    const int64_t boff = (int64_t)(uint32_t)d1.z | (int64_t)d1.w << 32;
+    const TileLayout L(tm, tdep, coords);
+    const int32_t* gsn = (const int32_t*)(a.blob + boff + L.snode);
+    for (int s = tid; s < tm.ns; s += NT) {
+        const int32_t node = __ldg(gsn + s);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sTdst + s)), "l"(a.T + node) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
 }
 // the next tile's descriptor, staged asynchronously into shared memory (no registers held)
 __device__ __forceinline__ void prefetch_desc(const TileArgs& a, int it, int4* sdesc) {
@@ -215,8 +240,10 @@ __device__ __forceinline__ void prefetch_desc(const TileArgs& a, int it, int4* s
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdesc + 1)), "l"(g + 1) : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void staged_desc(const int4* sdesc, int4& d0, int4& d1) {
-    asm volatile("cp.async.wait_all;" ::: "memory");
+__device__ __forceinline__ void staged_desc(const int4* sdesc, int4& d0, int4& d1, bool keep_last = false) {
+    // keep_last: the most recent group (the next tile's slot-temperature gathers) may stay in flight
+    if (keep_last) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_all;" ::: "memory");
     d0 = sdesc[0];
     d1 = sdesc[1];
 }
@@ -235,7 +262,7 @@ __device__ __forceinline__ void prefetch_tile(const TileArgs& a, int it, bool td
     for (int32_t o = 0; o < L.bytes; o += (int32_t)kBulkChunk)
         bulk_prefetch_l2(src + o, (uint32_t)(L.bytes - o < (int32_t)kBulkChunk ? L.bytes - o : kBulkChunk));
     const uint32_t tbytes = 8u * (uint32_t)cf_round32(tm.ns, 2);
-    if (tbytes) bulk_prefetch_l2(a.Tslot + d1.x, tbytes);
+    if (tbytes && a.Tslot) bulk_prefetch_l2(a.Tslot + d1.x, tbytes);
 }
 
 // Each CTA walks tiles blockIdx.x, +gridDim.x, ...; with stages == 2 it is a
@@ -261,9 +288,13 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
     const DevParams* __restrict__ P = a.P;
     uint8_t* const buf0 = smem;
     uint8_t* const buf1 = smem + (a.stages - 1) * a.blob_smem;
+    // slot-temperature buffers: one per stage; gathered slots (single stage) alternate between two,
+    // the next tile's gathers landing while this tile computes
+    const bool gather = a.slot_gather && a.stages == 1;
+    const int nsT = (a.stages == 2 || gather) ? 2 : 1;
     double* const sT0 = (double*)(smem + a.stages * (size_t)a.blob_smem);
-    double* const sT1 = sT0 + (a.stages - 1) * a.max_slots;
-    double2* sTH = (double2*)(sT0 + a.stages * a.max_slots);  // (T, H) per slot, 16 B aligned
+    double* const sT1 = sT0 + (nsT - 1) * a.max_slots;
+    double2* sTH = (double2*)(sT0 + nsT * a.max_slots);  // (T, H) per slot, 16 B aligned
 
     // the first copy is the CTA's critical path: thread 0 initialises the barriers and issues it
     // before anything else; the material table, the step's dt and the scratch zeros overlap it
@@ -284,7 +315,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             issue_tile_copy(a, d0, d1, TDEP, GC, buf1, sT1, &bar[1], &hdr[1], false);
         }
         griddep_wait();
-        if (first0) issue_slot_copy(a, &hdr[0], sT0, &bar[0]);
+        if (first0 && !gather) issue_slot_copy(a, &hdr[0], sT0, &bar[0]);
         if (first1) issue_slot_copy(a, &hdr[1], sT1, &bar[1]);
         if (a.stages == 1 && a.prefetch && (int)blockIdx.x + a.prefetch < a.n_tiles)
             prefetch_tile(a, blockIdx.x + a.prefetch, TDEP, GC);
@@ -298,6 +329,11 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
     for (int i = tid; i < P->n_materials; i += kTileThreads) sMat[i] = P->mat[i];
     if (GC && tid < 2) ((double*)(smem + a.scratch_off))[tid] = 0.0;  // the facet entries' lump operand
     if (tid != 0) griddep_wait();  // before any thread reads the step state
+    if (gather && first0) {  // the first tile's slot temperatures (T is final for this step)
+        int4 d0, d1;
+        load_desc(a, blockIdx.x, d0, d1);
+        gather_slot_T<kTileThreads>(a, d0, d1, TDEP, GC, sT0, tid);
+    }
     double dt = 0, t_next = 0;
     bool done = false;
     if (FUSE) step_dt<TDEP>(P, a.st, a.t_end, dt, t_next, done);
@@ -310,8 +346,9 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
     for (int t = blockIdx.x; t < a.n_tiles; ++k) {
         const int stage = a.stages == 2 ? (k & 1) : 0;
         uint8_t* B = stage ? buf1 : buf0;
-        double* sT = stage ? sT1 : sT0;
+        double* sT = (gather ? (k & 1) : stage) ? sT1 : sT0;
         mbar_wait(&bar[stage], a.stages == 2 ? ((k >> 1) & 1) : (k & 1));
+        if (gather) asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's slot gathers
         const TileMeta tm = hdr[stage].tm;
         const int s0 = hdr[stage].s0;
         const TileLayout& L = hdr[stage].layout();
@@ -477,6 +514,19 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         }
         __syncthreads();
 
+        // the next tile's slot temperatures, gathered into the other buffer while this tile reduces
+        // and its blob streams in (after phase 2b: the facet threads' wait_all there covers only
+        // the ambient gathers)
+        if (gather) {
+            const int t_iss = s_issue;
+            if (t_iss < a.n_tiles) {
+                int4 d0, d1;
+                load_desc(a, t_iss, d0, d1);
+                gather_slot_T<kTileThreads>(a, d0, d1, TDEP, GC, (k & 1) ? sT0 : sT1, tid);
+            } else {
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+        }
         // phase 3: per-slot fixed-order reduction (ascending element, then facets) + flush,
         // through the slot's 16-bit operand codes (cf_tileblob.hpp)
         const uint16_t* cend = (const uint16_t*)(B + L.csr_end);
@@ -531,7 +581,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                                                  a.local_global + node, clamped);
                 }
                 a.Tn[node] = Tn;
-                a.Tslot_n[s0 + s] = Tn;
+                if (!gather) a.Tslot_n[s0 + s] = Tn;
             } else if (DET) {
                 a.part[s0 + s] = make_double2(c, r);
             } else {
@@ -574,7 +624,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
                 // generic-proxy writes to B (in-place contributions) must be ordered
                 // before the async-proxy (TMA) overwrite of the same buffer
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                staged_desc(ndesc, nd0, nd1);
+                staged_desc(ndesc, nd0, nd1, gather);
                 issue_tile_copy(a, nd0, nd1, TDEP, GC, B, sT, &bar[stage], &hdr[stage]);
             }
         }
@@ -668,6 +718,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
                 a.acc_r[i] = 0;
             }
             a.Tn[i] = T;
+            if (!a.Tslot_n) continue;
             if (packed) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
@@ -722,7 +773,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         const double Tn = node_update<DIR, CLAMP>(P, a.st, T, c, r, dt, t_next, DIR ? a.node_dir[i] : -1,
                                                   CLAMP ? a.node_region[i] : 0, a.local_global + i, clamped);
         a.Tn[i] = Tn;
-        if (CF_PRB(a) == 8) continue;
+        if (CF_PRB(a) == 8 || !a.Tslot_n) continue;
         if (packed) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)

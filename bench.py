@@ -77,6 +77,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", type=int, default=0, help="capture the step loop in CUDA graphs of this many steps")
     ap.add_argument("--phase-steps", type=int, default=20)
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                    help="N > 1: NCCL (one GPU per rank) or the host-staged transport (diagnostics: every rank "
+                         "on cuda:0)")
     return ap.parse_args()
 
 
@@ -301,7 +304,12 @@ def main():
     spec = getattr(case, "spec", None)  # device-generated mesh
     mesh = None if spec is not None else case.mesh
     comm = None
-    if world > 1:
+    if world > 1 and args.transport == "host":
+        # diagnostics: several ranks on one GPU (NCCL refuses duplicate devices), exchange staged
+        # through host memory over the gloo group; not a multi-GPU measurement
+        local_rank = 0
+        comm = cf.HostComm(world, rank, 0)
+    elif world > 1:
         import torch
         uid = cf.Comm.unique_id() if rank == 0 else bytes(128)
         t = torch.tensor(list(uid), dtype=torch.uint8)
@@ -449,6 +457,7 @@ def main():
                            "geometry": args.geometry,
                            "dt_safety": setup.solver.dt_safety, "h_interface": 1000.0,
                            "parallelism": f"rcb{world}" if world > 1 else "single",
+                           "transport": (args.transport if world > 1 else None),
                            "setup_pipeline": "device" if st0.device_setup else "host",
                            "l2": "working set > 126 MB L2 (no flush needed)" if st.bytes_per_step > 2e8
                            else "working set L2-resident", "setup_seconds": round(setup_s, 2)},

@@ -239,3 +239,19 @@ def test_partition_errors_like_reference():
         cf.partition_elements(m, 100)
     with pytest.raises(cf.ValidationError):
         cf.partition_metrics(m, np.full(m.element_count(), 7, np.int32), 2)
+
+
+def test_plan_digests_golden():
+    """The host plan builder (and with it the per-tile code shared with the device builder)
+    reproduces the committed plan digests (tests/golden/make_plan_digests.py)."""
+    import json
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    from make_plan_digests import digests
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "plan_digests.json")) as f:
+        want = json.load(f)
+    got = digests()
+    assert got.keys() == want.keys()
+    bad = [(k, a) for k in want for a in want[k] if want[k][a] != got[k][a]]
+    assert not bad, bad[:5]

@@ -502,92 +502,112 @@ Graph build_node_graph(int32_t N, int32_t E, const int32_t* tets) {
 }
 
 namespace {
-// bfs_levels reorder.hpp:54-88: per parent, fresh neighbours sorted by (degree, id)
-void bfs_levels(const Graph& g, int32_t root, std::vector<char>& seen, std::vector<int32_t>* order) {
-    std::vector<int32_t> frontier{root}, next, fresh;
-    seen[root] = 1;
-    if (order) order->push_back(root);
-    while (!frontier.empty()) {
-        next.clear();
-        for (int32_t v : frontier) {
-            fresh.clear();
-            for (int64_t j = g.off[v]; j < g.off[v + 1]; ++j) {
-                const int32_t u = g.adj[j];
-                if (!seen[u]) {
-                    seen[u] = 1;
-                    fresh.push_back(u);
-                }
-            }
-            std::sort(fresh.begin(), fresh.end(), [&](int32_t a, int32_t b) {
-                const int32_t da = g.degree(a), db = g.degree(b);
-                return da != db ? da < db : a < b;
-            });
-            for (int32_t u : fresh) {
-                next.push_back(u);
-                if (order) order->push_back(u);
-            }
-        }
-        if (next.empty()) break;
-        frontier.swap(next);
-    }
-}
-// pseudo_peripheral reorder.hpp:91-120 (George-Liu)
-int32_t pseudo_peripheral(const Graph& g, int32_t start, std::vector<int32_t>& stamp, int32_t& epoch) {
-    int32_t node = start;
-    int64_t ecc = -1;
-    std::vector<int32_t> frontier, next, last;
-    for (;;) {
-        ++epoch;
-        frontier.assign(1, node);
-        stamp[node] = epoch;
+// The reference's Cuthill-McKee BFS (bfs_levels reorder.hpp:54-88) appends each visited vertex's
+// unseen neighbours sorted by (degree, id). Its order within level L+1 is therefore fixed by the
+// level-L position of each vertex's first discoverer, then (degree, id) -- the formulation the
+// device pass uses (cf_rcm.cu). Here: level sets by BFS, then each level sorted by
+// (smallest position among its neighbours in the previous level, degree, id).
+struct Levels {
+    std::vector<int32_t> dist;  // -1 unvisited in this sweep (only the touched entries are reset)
+    std::vector<int32_t> touched;
+    explicit Levels(int32_t n) : dist(n, -1) {}
+    // BFS from root (set semantics); returns the level sets in discovery-independent order
+    int64_t sweep(const Graph& g, int32_t root, std::vector<std::vector<int32_t>>* levels,
+                  std::vector<int32_t>* last) {
+        for (int32_t v : touched) dist[v] = -1;
+        touched.assign(1, root);
+        dist[root] = 0;
+        std::vector<int32_t> front{root}, next;
+        if (levels) levels->assign(1, front);
         int64_t depth = 0;
-        last = frontier;
         for (;;) {
             next.clear();
-            for (int32_t v : frontier)
+            for (int32_t v : front)
                 for (int64_t j = g.off[v]; j < g.off[v + 1]; ++j) {
                     const int32_t u = g.adj[j];
-                    if (stamp[u] != epoch) {
-                        stamp[u] = epoch;
+                    if (dist[u] < 0) {
+                        dist[u] = (int32_t)depth + 1;
+                        touched.push_back(u);
                         next.push_back(u);
                     }
                 }
             if (next.empty()) break;
             ++depth;
-            last = next;
-            frontier.swap(next);
+            front.swap(next);
+            if (levels) levels->push_back(front);
         }
+        if (last) *last = front;
+        return depth;
+    }
+};
+
+// pseudo_peripheral reorder.hpp:91-120 (George-Liu): restart from the (degree, id)-smallest vertex
+// of the last level while the eccentricity grows
+int32_t pseudo_peripheral(const Graph& g, int32_t start, Levels& lv) {
+    int32_t node = start;
+    int64_t ecc = -1;
+    std::vector<int32_t> last;
+    for (;;) {
+        const int64_t depth = lv.sweep(g, node, nullptr, &last);
         if (depth <= ecc) return node;
         ecc = depth;
-        int32_t best = last.front();
-        for (int32_t v : last) {
-            const int32_t dv = g.degree(v), db = g.degree(best);
-            if (dv < db || (dv == db && v < best)) best = v;
+        node = *std::min_element(last.begin(), last.end(), [&](int32_t a, int32_t b) {
+            return g.degree(a) != g.degree(b) ? g.degree(a) < g.degree(b) : a < b;
+        });
+    }
+}
+
+// Cuthill-McKee order of root's component appended to `order` (positions in `pos`)
+void cm_order(const Graph& g, int32_t root, Levels& lv, std::vector<int32_t>& order, std::vector<int64_t>& pos) {
+    std::vector<std::vector<int32_t>> levels;
+    lv.sweep(g, root, &levels, nullptr);
+    pos[root] = (int64_t)order.size();
+    order.push_back(root);
+    struct Key {
+        int64_t parent;
+        int32_t deg, id;
+    };
+    std::vector<Key> keys;
+    for (size_t L = 1; L < levels.size(); ++L) {
+        keys.clear();
+        for (int32_t u : levels[L]) {
+            int64_t first = INT64_MAX;  // first discoverer: earliest-placed neighbour one level up
+            for (int64_t j = g.off[u]; j < g.off[u + 1]; ++j) {
+                const int32_t w = g.adj[j];
+                if (lv.dist[w] == (int32_t)L - 1) first = std::min(first, pos[w]);
+            }
+            keys.push_back({first, g.degree(u), u});
         }
-        node = best;
+        std::sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
+            if (a.parent != b.parent) return a.parent < b.parent;
+            return a.deg != b.deg ? a.deg < b.deg : a.id < b.id;
+        });
+        for (const Key& k : keys) {
+            pos[k.id] = (int64_t)order.size();
+            order.push_back(k.id);
+        }
     }
 }
 }  // namespace
 
+// rcm_permutation reorder.hpp:127-148: components by ascending smallest vertex id, each rooted at
+// a pseudo-peripheral vertex (or at the seed when it lies in the component), order reversed
 std::vector<int32_t> rcm_permutation(const Graph& g, int32_t seed) {
     const int32_t n = g.n;
-    std::vector<char> seen(n, 0);
     std::vector<int32_t> order;
     order.reserve(n);
-    std::vector<int32_t> stamp(n, 0);
-    int32_t epoch = 0;
+    std::vector<int64_t> pos(n, -1);
+    Levels lv(n);
     for (int32_t v = 0; v < n; ++v) {
-        if (seen[v]) continue;
+        if (pos[v] >= 0) continue;
         int32_t root;
-        if (seed >= 0 && seed < n && !seen[seed]) {
-            // the seed is used if it lives in this (unvisited) component
-            std::vector<char> probe(n, 0);
-            bfs_levels(g, v, probe, nullptr);
-            root = probe[seed] ? seed : pseudo_peripheral(g, v, stamp, epoch);
+        if (seed >= 0 && seed < n && pos[seed] < 0) {
+            lv.sweep(g, v, nullptr, nullptr);
+            root = lv.dist[seed] >= 0 ? seed : pseudo_peripheral(g, v, lv);
         } else {
-            root = pseudo_peripheral(g, v, stamp, epoch);
+            root = pseudo_peripheral(g, v, lv);
         }
-        bfs_levels(g, root, seen, &order);
+        cm_order(g, root, lv, order, pos);
     }
     std::vector<int32_t> new_of_old(n);
     for (int32_t i = 0; i < n; ++i) new_of_old[order[i]] = n - 1 - i;

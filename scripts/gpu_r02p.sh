@@ -1,0 +1,7 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_devsetup.py tests/test_multiprocess_gpu.py -q -x > gpurun_out/parity_r02p.log 2>&1
+echo "parity rc=$?"; tail -2 gpurun_out/parity_r02p.log
+for CFG in cfg5 cfg2; do
+  CFG=$CFG VARIANTS="prev base" VARIANTS5="none" STEPS=40 timeout 1200 bash scripts/exp_r02.sh 2>&1 | grep -v "^Traceback\|^  \|^json\|^    \|none" | sed "s/^/$CFG /"
+done

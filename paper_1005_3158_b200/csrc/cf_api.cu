@@ -224,6 +224,7 @@ struct Rank {
     std::vector<TileLaunch> launches;
     int32_t* shared_list = nullptr;
     int4* shared_rec = nullptr;     // packed update records of shared_list
+    int2* shared_rec2 = nullptr;    // their slots 6, 7
     int32_t n_shared_list = 0;
     size_t tile_smem = 0;
     int upd_blocks = 0, upd_blocks_all = 0;
@@ -439,6 +440,7 @@ void launch_update(cf_plan* p, Rank& r, double t_end) {
     } else {
         a.list = r.shared_list;
         a.rec = r.shared_rec;
+        a.rec2 = r.shared_rec2;
         a.n_list = r.n_shared_list;
         blocks = r.upd_blocks;
     }
@@ -639,6 +641,7 @@ struct RankDev {
     int32_t* merge_idx = nullptr;
     int32_t* shared_list = nullptr;
     int4* shared_rec = nullptr;
+    int2* shared_rec2 = nullptr;
     int64_t n_shared_list = 0, merge_parts = 0, S_tot = 0, E_r = 0;
     int32_t *node_shared = nullptr, *shared_off = nullptr, *shared_src = nullptr, *shared_src_r = nullptr,
             *ghost_src = nullptr;
@@ -689,16 +692,19 @@ void upload_rank(cf_plan* p, Rank& r, const SetupData& S) {
     d.n_shared_list = (int64_t)h.shared_list.size();
     {
         std::vector<int4> rec(2 * std::max<size_t>(1, h.shared_list.size()));
+        std::vector<int2> rec2(std::max<size_t>(1, h.shared_list.size()));
         for (size_t k = 0; k < h.shared_list.size(); ++k) {
             const int32_t i = h.shared_list[k];
             const int32_t b = h.merge_off[i], cnt = h.merge_off[i + 1] - b;
-            int32_t sl[4] = {0, 0, 0, 0};
-            for (int q = 0; q < 4 && q < cnt; ++q) sl[q] = h.merge_idx[b + q];
+            int32_t sl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int q = 0; q < 8 && q < cnt; ++q) sl[q] = h.merge_idx[b + q];
             rec[2 * k] = make_int4(i, cnt, sl[0], sl[1]);
-            rec[2 * k + 1] = make_int4(sl[2], sl[3], 0, 0);
+            rec[2 * k + 1] = make_int4(sl[2], sl[3], sl[4], sl[5]);
+            rec2[k] = make_int2(sl[6], sl[7]);
             d.merge_parts += cnt;
         }
         d.shared_rec = M.up(rec, s);
+        d.shared_rec2 = M.up(rec2, s);
     }
     if (p->world > 1) {
         d.node_shared = M.up(h.node_shared, s);
@@ -729,6 +735,7 @@ void adopt_rank(cf_plan* p, Rank& r, DevRankPlan& dp) {
     d.merge_idx = dp.merge_idx;
     d.shared_list = dp.shared_list;
     d.shared_rec = dp.shared_rec;
+    d.shared_rec2 = dp.shared_rec2;
     d.n_shared_list = dp.n_shared_list;
     d.merge_parts = dp.merge_parts;
     d.S_tot = dp.S_tot;
@@ -929,6 +936,7 @@ void finish_rank(cf_plan* p, Rank& r, const RankDev& d) {
     r.shared_list = d.shared_list;
     r.n_shared_list = (int32_t)d.n_shared_list;
     r.shared_rec = d.shared_rec;
+    r.shared_rec2 = d.shared_rec2;
     if (p->world > 1) {
         u.node_shared = d.node_shared;
         u.shared_off = d.shared_off;

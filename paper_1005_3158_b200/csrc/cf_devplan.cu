@@ -1028,15 +1028,17 @@ __global__ void k_shared_keys(int64_t nl, const int32_t* ntiles_of, const uint8_
         val[l] = (int32_t)l;
     }
 }
+// update records (update_kernel): {node, count, slot0, slot1}, {slot2 .. slot5} + {slot6, slot7}
 __global__ void k_shared_rec(int64_t n, const int32_t* list, const int32_t* merge_off, const int32_t* merge_idx,
-                             int4* rec, unsigned long long* parts) {
+                             int4* rec, int2* rec2, unsigned long long* parts) {
     GRID_STRIDE(k, n) {
         const int32_t i = list[k];
         const int32_t b = merge_off[i], cnt = merge_off[i + 1] - b;
-        int32_t sl[4] = {0, 0, 0, 0};
-        for (int q = 0; q < 4 && q < cnt; ++q) sl[q] = merge_idx[b + q];
+        int32_t sl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int q = 0; q < 8 && q < cnt; ++q) sl[q] = merge_idx[b + q];
         rec[2 * k] = make_int4(i, cnt, sl[0], sl[1]);
-        rec[2 * k + 1] = make_int4(sl[2], sl[3], 0, 0);
+        rec[2 * k + 1] = make_int4(sl[2], sl[3], sl[4], sl[5]);
+        rec2[k] = make_int2(sl[6], sl[7]);
         atomicAdd(parts, (unsigned long long)cnt);
     }
 }
@@ -1569,11 +1571,13 @@ void build_rank_plan_device(const DevMesh& m, const DevSetup& DS, const PlanOpti
         out.shared_list = M.alloc<int32_t>(std::max<int64_t>(1, n_sh));
         DP_CHECK(cudaMemcpyAsync(out.shared_list, v1, n_sh * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
         out.shared_rec = M.alloc<int4>(2 * std::max<int64_t>(1, n_sh));
+        out.shared_rec2 = M.alloc<int2>(std::max<int64_t>(1, n_sh));
         DP_CHECK(cudaMemsetAsync(out.shared_rec, 0, 2 * std::max<int64_t>(1, n_sh) * sizeof(int4), s));
+        DP_CHECK(cudaMemsetAsync(out.shared_rec2, 0, std::max<int64_t>(1, n_sh) * sizeof(int2), s));
         unsigned long long* parts = TT.alloc<unsigned long long>(1);
         DP_CHECK(cudaMemsetAsync(parts, 0, 8, s));
         if (n_sh) k_shared_rec<<<grid_of(n_sh), 256, 0, s>>>(n_sh, out.shared_list, out.merge_off, out.merge_idx,
-                                                            out.shared_rec, parts);
+                                                            out.shared_rec, out.shared_rec2, parts);
         out.merge_parts = (int64_t)read1(parts, s);
     }
 

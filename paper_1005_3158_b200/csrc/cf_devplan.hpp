@@ -115,6 +115,7 @@ struct DevRankPlan {
     int32_t* merge_idx = nullptr;
     int32_t* shared_list = nullptr;
     int4* shared_rec = nullptr;
+    int2* shared_rec2 = nullptr;
     int32_t* elem_global = nullptr; // [E_r] tile order (kept for cf_tile_map-style queries)
     // multi-rank exchange tables (device)
     int32_t *node_shared = nullptr, *shared_off = nullptr, *shared_src = nullptr, *shared_src_r = nullptr,

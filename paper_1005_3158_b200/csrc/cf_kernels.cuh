@@ -647,8 +647,9 @@ struct UpdArgs {
     int32_t probe;        // diagnostics only (CF_PROBE; results invalid): 8 = no slot-copy writes,
                           // 9 = no partial reads
     const int32_t* list;  // nodes to merge + update (NULL: all local nodes)
-    const int4* rec;      // packed per listed node: {node, count, slot0, slot1}, {slot2, slot3, -, -}
-                          // (count > 4: slots via merge_off/merge_idx); NULL: use list + merge CSR
+    const int4* rec;      // packed per listed node: {node, count, slot0, slot1}, {slot2 .. slot5}
+                          // (count > 8: slots via merge_off/merge_idx); NULL: use list + merge CSR
+    const int2* rec2;     // per listed node: {slot6, slot7} (tile corners of structured meshes)
     const double* T;      // current (ghost slots written here)
     double* Tn;           // next
     const int32_t* merge_off;
@@ -701,16 +702,18 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n_list; k += stride) {
         int i, cnt = -1;
         int4 r0, r1;
-        if (a.rec) {  // one coalesced 32-byte record: node + up to 4 slot (= partial) indices
+        int2 r2 = make_int2(0, 0);
+        if (a.rec) {  // coalesced records: node + up to 8 slot (= partial) indices
             r0 = __ldg(a.rec + 2 * k);
             r1 = __ldg(a.rec + 2 * k + 1);
             i = r0.x;
             cnt = r0.y;
+            if (cnt > 6) r2 = __ldg(a.rec2 + k);
         } else {
             i = a.list ? a.list[k] : k;
         }
-        const int sl[4] = {r0.z, r0.w, r1.x, r1.y};
-        const bool packed = cnt >= 0 && cnt <= 4;
+        const int sl[8] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y};
+        const bool packed = cnt >= 0 && cnt <= 8;
         const double T = __ldg(a.T + i);
         if (done) {
             if (!DET) {  // the tile kernel still accumulated this (no-op) step: drop it
@@ -721,7 +724,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
             if (!a.Tslot_n) continue;
             if (packed) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
+                for (int q = 0; q < 8; ++q)
                     if (q < cnt) a.Tslot_n[sl[q]] = T;
             } else {
                 for (int j = a.merge_off[i]; j < a.merge_off[i + 1]; ++j) a.Tslot_n[a.merge_idx[j]] = T;
@@ -731,13 +734,13 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         double c, r;
         if (DET && packed) {
             // all partial loads issued before the in-order (ascending tile) sums
-            double2 pr[4];
+            double2 pr[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) pr[q] = (q < cnt && CF_PRB(a) != 9) ? __ldg(a.part + sl[q]) : make_double2(1.0, 0.0);
+            for (int q = 0; q < 8; ++q) pr[q] = (q < cnt && CF_PRB(a) != 9) ? __ldg(a.part + sl[q]) : make_double2(1.0, 0.0);
             c = 0;
             r = 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < 8; ++q)
                 if (q < cnt) {
                     c += pr[q].x;
                     r += pr[q].y;
@@ -776,7 +779,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         if (CF_PRB(a) == 8 || !a.Tslot_n) continue;
         if (packed) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < 8; ++q)
                 if (q < cnt) a.Tslot_n[sl[q]] = Tn;
         } else {
             for (int j = a.merge_off[i]; j < a.merge_off[i + 1]; ++j) a.Tslot_n[a.merge_idx[j]] = Tn;

@@ -103,7 +103,7 @@ def test_device_and_host_pipelines_step_identically(monkeypatch):
     assert np.array_equal(dev.T, host.T)
 
 
-@pytest.mark.parametrize("defect", ["degenerate", "region_conflict", "interior_facet", "bad_index"])
+@pytest.mark.parametrize("defect", ["degenerate", "region_conflict", "interior_facet", "bad_index", "no_material"])
 def test_device_pipeline_reports_the_host_errors(defect, monkeypatch):
     case = configs.casting(6, dt_safety=0.14)
     m = case.mesh
@@ -115,6 +115,8 @@ def test_device_pipeline_reports_the_host_errors(defect, monkeypatch):
         t = m.tets[0]
         other = np.where((m.tets == t[1]).any(1) & (m.tets == t[2]).any(1) & (m.tets == t[3]).any(1))[0]
         m.facets[0] = t[[1, 2, 3]] if len(other) > 1 else m.facets[0]
+    elif defect == "no_material":
+        m.region[m.region == 1] = 40  # the mould as region 40: no material (2 declared)
     else:
         m.tets[3, 2] = m.node_count() + 5
     msgs = []

@@ -254,6 +254,9 @@ struct cf_plan {
     // from T by node id (CF_SLOT_GATHER=1: update -27 %, tile kernel +7 % at cfg5, net -4 %;
     // saves the 2 x 8 B/slot copies, 4.2 GB at cfg5)
     bool slot_gather = false;
+    // the next tile's blob staged into L2 during the reduction (CF_L2_NEXT=0: off): cfg2 tile
+    // kernel -4 %, cfg4 / cfg5 unchanged (profiles/r02r_l2_next_ab.txt)
+    bool l2_next = true;
     int world = 1, first_rank = 0, local_ranks = 1;
     cf_comm* comm = nullptr;
     DevParams P{};
@@ -387,6 +390,7 @@ void launch_tile(cf_plan* p, Rank& r, double t_end, int phase = -1) {
             a.Tslot = r.Tslot[p->step_parity];
             a.Tslot_n = r.Tslot[p->step_parity ^ 1];
             a.slot_gather = p->slot_gather ? 1 : 0;
+            a.l2_next = p->l2_next ? 1 : 0;
             a.t_end = t_end;
             const dim3 grid(tl.grid), block(nt);
 #define CF_LAUNCH(D, T, R, C, NT, G)                                                                  \
@@ -1325,6 +1329,7 @@ std::unique_ptr<cf_plan> new_plan(const cf_run_opts& o, const cf_setup_desc* set
     if (const char* e = std::getenv("CF_TILE_STAGES")) p->stages = std::atoi(e) == 2 ? 2 : 1;
     if (const char* e = std::getenv("CF_PDL")) p->pdl = std::atoi(e) != 0;
     if (const char* e = std::getenv("CF_SLOT_GATHER")) p->slot_gather = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CF_L2_NEXT")) p->l2_next = std::atoi(e) != 0;
     if (p->stages == 2) p->slot_gather = false;
     p->world = o.world_size;
     p->first_rank = o.rank;

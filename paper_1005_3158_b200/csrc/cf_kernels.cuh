@@ -165,6 +165,7 @@ struct TileArgs {
     double t_end;
     int32_t* sched;            // dynamic tile scheduling counter (persistent single-stage grids), or null
     int32_t slot_gather;       // 1: slot temperatures gathered from T by node id (no slot copies)
+    int32_t l2_next;           // persistent grids: stage the next tile's blob into L2 at phase 3's start
 };
 
 constexpr uint32_t kBulkChunk = 32768;
@@ -526,6 +527,20 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             } else {
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
+        }
+        // the next tile of this CTA into L2 while this one reduces: its bulk copy, issued after the
+        // reduction, then reads L2 instead of waiting out the DRAM latency (thread 0's groups: the
+        // descriptor staged at this tile's start and the ambient gathers, both complete by now)
+        if (a.l2_next && tid == 0 && s_issue < a.n_tiles) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            const int4 d0 = ndesc[0], d1 = ndesc[1];
+            const TileMeta tm{d0.x, d0.y, d0.z, d0.w};
+            const int64_t boff = (int64_t)(uint32_t)d1.z | (int64_t)d1.w << 32;
+            const uint8_t* src = a.blob + boff;
+            for (int32_t o = 0; o < d1.y; o += (int32_t)kBulkChunk)
+                bulk_prefetch_l2(src + o, (uint32_t)(d1.y - o < (int32_t)kBulkChunk ? d1.y - o : kBulkChunk));
+            const uint32_t tbytes = 8u * (uint32_t)cf_round32(tm.ns, 2);
+            if (tbytes && a.Tslot) bulk_prefetch_l2(a.Tslot + d1.x, tbytes);
         }
         // phase 3: per-slot fixed-order reduction (ascending element, then facets) + flush,
         // through the slot's 16-bit operand codes (cf_tileblob.hpp)

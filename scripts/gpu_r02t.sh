@@ -1,0 +1,4 @@
+#!/bin/bash
+for CFG in cfg5 cfg2 cfg5; do
+  CFG=$CFG VARIANTS="r2early base" VARIANTS5="none" STEPS=40 timeout 1200 bash scripts/exp_r02.sh 2>&1 | grep -v "^Traceback\|^  \|^json\|^    \|none" | sed "s/^/$CFG /"
+done

@@ -1427,7 +1427,9 @@ void build_rank_plan_device(const DevMesh& m, const DevSetup& DS, const PlanOpti
             d2h(hm.data(), d_meta, nT, s);
             rp.tile_meta = hm;
             std::vector<int32_t> nsv(nT);
-            for (int64_t t = 0; t < nT; ++t) nsv[t] = hm[t].ns;
+            int64_t sum_ns = 0;
+            for (int64_t t = 0; t < nT; ++t) sum_ns += nsv[t] = hm[t].ns;
+            if (sum_ns > INT32_MAX) raise(CF_INVALID_ARG, "more than 2^31 tile slots on one rank");
             h2d(ns_arr, nsv.data(), nT, s);
         }
         excl_sum(ns_arr, tn_off, nT, s);

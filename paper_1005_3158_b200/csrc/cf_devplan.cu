@@ -1046,6 +1046,9 @@ __global__ void k_shared_rec(int64_t n, const int32_t* list, const int32_t* merg
 __global__ void k_gather_i32(int64_t n, const int32_t* idx, const int32_t* src, int32_t* out) {
     GRID_STRIDE(i, n) out[i] = idx[i] >= 0 ? src[idx[i]] : -1;
 }
+__global__ void k_gather_corners(int64_t n, const int32_t* elems, const int32_t* tets, int32_t* out) {
+    GRID_STRIDE(i, 4 * n) out[i] = tets[4 * (int64_t)elems[i >> 2] + (i & 3)];
+}
 __global__ void k_gather_u64(int64_t n, const int32_t* idx, const unsigned long long* src, unsigned long long* out) {
     GRID_STRIDE(i, n) out[i] = src[idx[i]];
 }
@@ -1353,20 +1356,16 @@ void build_rank_plan_device(const DevMesh& m, const DevSetup& DS, const PlanOpti
         h2d(d_se, se.data(), se.size(), s);
         k_gather_i32<<<grid_of((int64_t)se.size()), 256, 0, s>>>((int64_t)se.size(), d_se, d_part, d_sp);
         d2h(sis_part.data(), d_sp, se.size(), s);
-        std::vector<int32_t> ti(4 * se.size());
-        for (size_t i = 0; i < se.size(); ++i)
-            for (int a = 0; a < 4; ++a) ti[4 * i + a] = 4 * se[i] + a;
-        int32_t* d_ti = TT.alloc<int32_t>(ti.size());
-        int32_t* d_sn = TT.alloc<int32_t>(ti.size());
-        int32_t* d_sl = TT.alloc<int32_t>(ti.size());
-        unsigned long long* d_sm = TT.alloc<unsigned long long>(ti.size());
-        h2d(d_ti, ti.data(), ti.size(), s);
-        k_gather_i32<<<grid_of((int64_t)ti.size()), 256, 0, s>>>((int64_t)ti.size(), d_ti, m.tets, d_sn);
-        k_gather_i32<<<grid_of((int64_t)ti.size()), 256, 0, s>>>((int64_t)ti.size(), d_sn, local_of, d_sl);
-        k_gather_u64<<<grid_of((int64_t)ti.size()), 256, 0, s>>>((int64_t)ti.size(), d_sn, nmask, d_sm);
-        d2h(sis_nodes.data(), d_sn, ti.size(), s);
-        d2h(sis_local.data(), d_sl, ti.size(), s);
-        d2h(sis_mask.data(), d_sm, ti.size(), s);
+        const int64_t n4 = 4 * (int64_t)se.size();  // the sister elements' corners (element ids may exceed 2^29)
+        int32_t* d_sn = TT.alloc<int32_t>(n4);
+        int32_t* d_sl = TT.alloc<int32_t>(n4);
+        unsigned long long* d_sm = TT.alloc<unsigned long long>(n4);
+        k_gather_corners<<<grid_of(n4), 256, 0, s>>>((int64_t)se.size(), d_se, m.tets, d_sn);
+        k_gather_i32<<<grid_of(n4), 256, 0, s>>>(n4, d_sn, local_of, d_sl);
+        k_gather_u64<<<grid_of(n4), 256, 0, s>>>(n4, d_sn, nmask, d_sm);
+        d2h(sis_nodes.data(), d_sn, n4, s);
+        d2h(sis_local.data(), d_sl, n4, s);
+        d2h(sis_mask.data(), d_sm, n4, s);
         for (size_t i = 0; i < ifac.size(); ++i) {
             if (!in_rank_owner(ifac[i])) continue;
             for (int a = 0; a < 4; ++a)

@@ -142,3 +142,17 @@ def test_cfg5_two_steps_vs_oracle_window():
     assert inner.sum() > 1_000_000
     assert rel(gpu.T[pos[inner]], o.T[inner]) <= RTOL
     assert np.array_equal(T0[inner], s.initial_T[pos[inner]])
+
+
+def test_cfg5_decomposed_matches_single_rank():
+    """The 8-rank decomposition of the gate configuration (cfg5, 805 M tets: element ids beyond
+    2^29, so 4 x id overflows int32) built by the device pipeline for every rank, all ranks in one
+    process on one GPU (in-process transport): 2 steps equal the single-rank run to 1e-9
+    (summation order over ranks only)."""
+    dc = configs.device_case("cfg5")
+    T = {}
+    for R in (1, 8):
+        with cf.Solver(None, dc.setup, cf.SolveOptions(world_size=R, local_ranks=R), fixture=dc.spec) as s:
+            s.step(2)
+            T[R] = s.fields(want_H=False)[0]
+    assert rel(T[8], T[1]) <= RTOL

@@ -36,9 +36,6 @@ inline int grid_of(int64_t n, int block = 256) {
 #define GRID_STRIDE(i, n) for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
 template <class T>
-T* dalloc(DBuf& B, size_t n) { return B.alloc<T>(n); }
-
-template <class T>
 void h2d(T* d, const T* h, size_t n, cudaStream_t s) {
     if (n) DP_CHECK(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
 }

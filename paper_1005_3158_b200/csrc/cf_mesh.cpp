@@ -462,7 +462,6 @@ Graph build_node_graph(int32_t N, int32_t E, const int32_t* tets) {
     Graph g;
     g.n = N;
     g.off.assign(N + 1, 0);
-    std::vector<std::vector<int32_t>> tmp_dummy;
     // two passes: count, fill
     std::vector<int32_t> deg(N);
 #pragma omp parallel

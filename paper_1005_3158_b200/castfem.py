@@ -418,6 +418,8 @@ class Solver:
         self.opts = opts
         sd, ro = setup_desc(setup, keep), run_opts(opts, keep)
         h = C.c_void_p()
+        if (mesh is None) == (fixture is None):
+            raise InvalidArgument("Solver needs exactly one of mesh (host arrays) or fixture (device-generated)")
         if fixture is not None:
             fx = fixture.desc()
             check(lib().cf_plan_create_fixture(C.byref(fx), C.byref(sd), C.byref(ro), C.byref(h)))

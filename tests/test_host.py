@@ -255,3 +255,19 @@ def test_plan_digests_golden():
     assert got.keys() == want.keys()
     bad = [(k, a) for k in want for a in want[k] if want[k][a] != got[k][a]]
     assert not bad, bad[:5]
+
+
+def test_device_case_specs_match_host_cases():
+    """configs.device_case: the same fixture rule and physics as the host-built cases (the mesh
+    itself is compared on the GPU, tests/test_gpu_devsetup.py)."""
+    from paper_1005_3158_b200 import configs
+    for name in ("cfg2", "cfg4", "cfg5"):
+        dc = configs.device_case(name)
+        assert dc.spec.kind == "casting" and dc.spec.radius == 0.35 and dc.spec.t0_noise == configs.T0_NOISE
+        assert dc.setup.solver.dt_safety == configs.DT_SAFETY[name] and dc.setup.initial_T is None
+        assert dc.spec.rcm == (name == "cfg2")
+        d = dc.spec.desc()
+        assert (d.kind, d.n, d.perm_seed, d.rcm) == (1, dc.spec.n, 0, int(dc.spec.rcm))
+    assert configs.device_case("cfg1").spec.kind == "cube"
+    with pytest.raises(cf.InvalidArgument):
+        cf.Solver(None, configs.device_case("cfg2").setup)

@@ -69,7 +69,9 @@ def test_deterministic_repeat_bitwise():
 
 @pytest.mark.parametrize("env", [{"CF_TILE_PERSIST": "0"}, {"CF_TILE_DYNAMIC": "0"}, {"CF_BANK_ITERS": "4"},
                                  {"CF_BANK_PASSES": "3"}, {"CF_SLOT_ORDER": "count"}, {"CF_SLOT_BANKS": "0"},
-                                 {"CF_TILE_PERSIST": "0", "CF_BANK_ITERS": "0"}])
+                                 {"CF_TILE_PERSIST": "0", "CF_BANK_ITERS": "0"}, {"CF_SLOT_GATHER": "1"},
+                                 {"CF_L2_NEXT": "0"}, {"CF_TILE_STAGES": "2"}, {"CF_TILE_ORDER": "morton"},
+                                 {"CF_HOST_SETUP": "1"}])
 def test_schedule_and_element_positions_leave_results_bitwise(env, monkeypatch):
     """Persistent (dynamically or statically scheduled) vs one-CTA-per-tile grids and the
     bank-aware element positions inside a tile (greedy colouring, optional local search) only

@@ -59,10 +59,17 @@ __device__ __forceinline__ double dev_enthalpy(const DevParams* __restrict__ P, 
         const int i = (ub < n - 1 ? ub : n - 1) - 1;
         sensible = P->pool[m.cum_off + i] + 0.5 * (ys[i] + dev_pl_eval(P, m.c, Tc)) * (Tc - xs[i]);
     }
+    // melt_fraction material.hpp:69-72: clamp((T - Ts)/(Tl - Ts), 0, 1). Outside the mushy range
+    // the clamp decides without the IEEE division (T <= Ts gives v <= 0, T >= Tl gives v >= 1:
+    // the correctly rounded quotient is monotone), so only mushy nodes divide; NaN falls through
     double mf = 0.0;
     if (m.has_phase) {
-        const double v = (T - m.solidus) / (m.liquidus - m.solidus);
-        mf = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+        if (T >= m.liquidus) {
+            mf = 1.0;
+        } else if (!(T <= m.solidus)) {
+            const double v = (T - m.solidus) / (m.liquidus - m.solidus);
+            mf = v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+        }
     }
     return sensible + m.latent * mf;
 }

@@ -772,6 +772,9 @@ void finish_rank(cf_plan* p, Rank& r, const RankDev& d) {
     }
     r.st = M.alloc<DevState>(1);
     TileArgs& a = r.ta;
+    a.n_local = h.n_local;
+    a.n_T = h.n_local + h.n_ghost;
+    a.n_slots = S_tot;
     a.meta = M.up(h.tile_meta, s);
     a.slot_off = M.up(h.tile_slot_off, s);
     a.blob_off = M.up(h.blob_off, s);
@@ -927,6 +930,7 @@ void finish_rank(cf_plan* p, Rank& r, const RankDev& d) {
 #endif
     u.n_local = h.n_local;
     u.n_ghost = h.n_ghost;
+    u.n_slots = S_tot;
     u.merge_off = d.merge_off;  // partial merge (deterministic) + Tslot scatter (both modes)
     u.merge_idx = d.merge_idx;
     u.part = r.part;

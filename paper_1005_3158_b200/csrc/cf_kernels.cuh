@@ -43,6 +43,15 @@ namespace cfb {
 #else
 #define CF_PRB(a) 0
 #endif
+// Bounds assertions (a -DCF_BOUNDS build, `make BOUNDS=1`): every shared-memory index the tile
+// kernel derives from plan data and every global index of the step kernels is checked against
+// its array, trapping on violation -- the memcheck substitute where compute-sanitizer is
+// unavailable (tests run against such a build, scripts/bounds_check.sh). Compiled out otherwise.
+#ifdef CF_BOUNDS
+#define CF_ASSERT(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define CF_ASSERT(c) do { } while (0)
+#endif
 
 struct DevState {
     double time;
@@ -166,6 +175,9 @@ struct TileArgs {
     int32_t* sched;            // dynamic tile scheduling counter (persistent single-stage grids), or null
     int32_t slot_gather;       // 1: slot temperatures gathered from T by node id (no slot copies)
     int32_t l2_next;           // persistent grids: stage the next tile's blob into L2 at phase 3's start
+    int32_t n_local;           // bounds (CF_BOUNDS builds): local nodes (+ ghosts below n_T)
+    int32_t n_T;
+    int64_t n_slots;
 };
 
 constexpr uint32_t kBulkChunk = 32768;
@@ -385,6 +397,8 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             const ushort4 fs = *(const ushort4*)(B + L.fac_slots(i));
             if (!P->kind[fs.w].interface) continue;
             const int4 sn = *(const int4*)(rec + 1);
+            CF_ASSERT(sn.x >= 0 && sn.y >= 0 && sn.z >= 0 && sn.w >= 0 && sn.x < a.n_T && sn.y < a.n_T && sn.z < a.n_T &&
+                      sn.w < a.n_T);
             const uint32_t dst = smem_u32(rec + 1);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(a.Told + sn.x) : "memory");
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8), "l"(a.Told + sn.y) : "memory");
@@ -415,6 +429,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         for (int i = tid; i < ((CF_PRB(a) & 15) == 4 ? 0 : ne); i += kTileThreads) {
             double g[4][3], vol, max_edge = 0;
             const ushort4 cn = connp[i];
+            CF_ASSERT(cn.x < ns && cn.y < ns && cn.z < ns && cn.w < ns);
             if (GC) {
                 const double2* X = (const double2*)(B + L.xyz);  // slot (x, y) (z, 0)
                 const unsigned short sl[4] = {cn.x, cn.y, cn.z, cn.w};
@@ -477,6 +492,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             const ushort4 fs = make_ushort4((unsigned short)fb, (unsigned short)(fb >> 16), (unsigned short)(fb >> 32),
                                             (unsigned short)(fb >> 48));
             const DevFacetKind& K = P->kind[fs.w];
+            CF_ASSERT(fs.x < ns && fs.y < ns && fs.z < ns);
             const double ts[3] = {sT[fs.x], sT[fs.y], sT[fs.z]};
             double q, h, tinf;
             if (K.interface) {
@@ -553,11 +569,14 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         auto reduce = [&](int s, double& c, double& r) {
             const int beg = s == 0 ? 0 : cend[s - 1];
             const int end = cend[s];
+            CF_ASSERT(s < ns && beg <= end && (end - beg) % 4 == 0);
             c = 0;
             r = 0;
             for (int j = beg; j < end; j += 4) {  // lists padded to 4 with exact (0.0, 0.0) no-ops
                 const uint2 pr = *(const uint2*)(csr + j);
                 const uint32_t v[4] = {pr.x & 0xffffu, pr.x >> 16, pr.y & 0xffffu, pr.y >> 16};
+                CF_ASSERT(GC || (v[0] < (uint32_t)(L.bytes >> 4) && v[1] < (uint32_t)(L.bytes >> 4) &&
+                                 v[2] < (uint32_t)(L.bytes >> 4) && v[3] < (uint32_t)(L.bytes >> 4)));
                 double l[4], q[4];
                 if (GC) {
                     const int32_t rz = L.r_zero, rl = L.r_lump;
@@ -585,6 +604,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
         };
         // ... and its flush (global memory only, so it may follow the next tile's copy issue)
         auto flush = [&](int s, double c, double r, int info, int32_t node, double Ts) {
+            CF_ASSERT(node >= 0 && node < a.n_local && (int64_t)s0 + s < a.n_slots);
             if (FUSE && (info & 0x80)) {
                 // tile-private node: its merge is the identity, update it now
                 double Tn;
@@ -659,6 +679,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
 // ------------------------------------------------------------------ update kernel
 struct UpdArgs {
     int32_t n_list, n_local, n_ghost;
+    int64_t n_slots;      // bounds (CF_BOUNDS builds)
     int32_t probe;        // diagnostics only (CF_PROBE; results invalid): 8 = no slot-copy writes,
                           // 9 = no partial reads
     const int32_t* list;  // nodes to merge + update (NULL: all local nodes)
@@ -729,6 +750,9 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         }
         const int sl[8] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y};
         const bool packed = cnt >= 0 && cnt <= 8;
+        CF_ASSERT(i >= 0 && i < a.n_local);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) CF_ASSERT(!packed || q >= cnt || (sl[q] >= 0 && sl[q] < a.n_slots));
         const double T = __ldg(a.T + i);
         if (done) {
             if (!DET) {  // the tile kernel still accumulated this (no-op) step: drop it

@@ -545,11 +545,12 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             }
         }
         // the next tile of this CTA into L2 while this one reduces: its bulk copy, issued after the
-        // reduction, then reads L2 instead of waiting out the DRAM latency (thread 0's groups: the
-        // descriptor staged at this tile's start and the ambient gathers, both complete by now)
-        if (a.l2_next && tid == 0 && s_issue < a.n_tiles) {
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            const int4 d0 = ndesc[0], d1 = ndesc[1];
+        // reduction, then reads L2 instead of waiting out the DRAM latency. Issued by the last warp,
+        // whose reduction lists are the shortest (sperm), not by warp 0 on the critical path; the
+        // descriptor is read from global memory (L2-hot: thread 0 staged it at the tile's start)
+        if (a.l2_next && tid == kTileThreads - 32 && s_issue < a.n_tiles) {
+            int4 d0, d1;
+            load_desc(a, s_issue, d0, d1);
             const TileMeta tm{d0.x, d0.y, d0.z, d0.w};
             const int64_t boff = (int64_t)(uint32_t)d1.z | (int64_t)d1.w << 32;
             const uint8_t* src = a.blob + boff;

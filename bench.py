@@ -77,9 +77,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", type=int, default=0, help="capture the step loop in CUDA graphs of this many steps")
     ap.add_argument("--phase-steps", type=int, default=20)
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
-                    help="N > 1: NCCL (one GPU per rank) or the host-staged transport (diagnostics: every rank "
-                         "on cuda:0)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer", "host", "peer-1gpu"],
+                    help="N > 1: NCCL send/recv (one GPU per rank); peer = the pack kernel stores into the "
+                         "neighbours' IPC windows over NVLink, streams wait on step flags (no library collective "
+                         "on the data path); host = host-staged, every rank on cuda:0 (diagnostics); peer-1gpu = "
+                         "the peer transport with every rank on cuda:0 (diagnostics)")
     return ap.parse_args()
 
 
@@ -309,6 +311,10 @@ def main():
         # through host memory over the gloo group; not a multi-GPU measurement
         local_rank = 0
         comm = cf.HostComm(world, rank, 0)
+    elif world > 1 and args.transport in ("peer", "peer-1gpu"):
+        if args.transport == "peer-1gpu":
+            local_rank = 0
+        comm = cf.PeerComm(world, rank, local_rank)
     elif world > 1:
         import torch
         uid = cf.Comm.unique_id() if rank == 0 else bytes(128)

@@ -308,6 +308,25 @@ enum { CF_REDUCE_MIN = 0, CF_REDUCE_MAX = 1 };
 int cf_comm_create_host(int32_t world_size, int32_t rank, int32_t device,
                         const cf_host_transport* transport, cf_comm** out);
 
+/* Peer-memory transport (NVLink 5 / NVSwitch P2P, one rank process per GPU): no library
+ * collective on the data path. Every rank exports one device window (CUDA IPC) holding a
+ * control block and its receive buffer for two step parities; `bootstrap` is used once per
+ * plan to exchange the window handles (and once at cf_plan_destroy as a barrier, so a window
+ * is unmapped everywhere before its owner frees it). Each step (SPEC S:450-458
+ * exchange_and_merge): the pack kernel stores every neighbour's [c(shared) | r(shared) |
+ * T(external)] payload straight into that neighbour's window and its last CTA raises this
+ * rank's step flag there (system-scope release); the receiver's stream waits on its
+ * neighbours' flags (cuStreamWaitValue32 -- no kernel spins on another rank) before the
+ * update. Two parities suffice: a rank writes exchange k+2 only after its update k+1, which
+ * waited for the neighbour's flag k+1, raised after the neighbour's update k read parity k.
+ * The scalar reductions (dynamic-dt bound, clamp flag, series T_min / T_max) are all-to-all
+ * stores into the control blocks. Steps stay asynchronous; CUDA graphs are not used (the
+ * waited flag value changes every step). Limits: world_size <= 64, <= 32 neighbours per rank,
+ * local_ranks == 1. Rank processes sharing one GPU work too (the windows are then local
+ * memory), which is how the 1-GPU test pool exercises it. Destroy the plan before the comm. */
+int cf_comm_create_peer(int32_t world_size, int32_t rank, int32_t device,
+                        const cf_host_transport* bootstrap, cf_comm** out);
+
 /* ---------------------------------------------------------------------------
  * Host utilities (no GPU needed) — the setup pipeline on either side of the path
  * ------------------------------------------------------------------------- */

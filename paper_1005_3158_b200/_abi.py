@@ -121,6 +121,8 @@ SIGNATURES = [
     ("cf_comm_create", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_void_p)]),
     ("cf_comm_create_host", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(cf_host_transport),
                                       C.POINTER(C.c_void_p)]),
+    ("cf_comm_create_peer", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(cf_host_transport),
+                                      C.POINTER(C.c_void_p)]),
     ("cf_comm_destroy", C.c_int, [C.c_void_p]),
     ("cf_rcm_permutation", C.c_int, [C.POINTER(cf_mesh_desc), C.c_int32, _ip]),
     ("cf_rcm_permutation_device", C.c_int, [C.POINTER(cf_mesh_desc), C.c_int32, C.c_int32, _ip]),

@@ -393,13 +393,25 @@ class HostComm:
         self._cb = (_abi.SENDRECV_FN(sendrecv), _abi.ALLREDUCE_FN(allreduce))
         t = _abi.cf_host_transport(None, self._cb[0], self._cb[1])
         h = C.c_void_p()
-        check(lib().cf_comm_create_host(world_size, rank, device, C.byref(t), C.byref(h)))
+        check(getattr(lib(), self._create)(world_size, rank, device, C.byref(t), C.byref(h)))
         self.handle = h
+
+    _create = "cf_comm_create_host"
 
     def close(self):
         if self.handle:
             lib().cf_comm_destroy(self.handle)
             self.handle = None
+
+
+class PeerComm(HostComm):
+    """Peer-memory transport (cf_comm_create_peer): the pack kernel stores each neighbour's
+    payload straight into that neighbour's IPC-exported device window over NVLink and raises a
+    step flag the neighbour's stream waits on; no library collective on the data path. The
+    torch.distributed group (gloo is enough) only carries the one-time window-handle exchange
+    and the barrier at plan destruction. Close the Solver before this communicator."""
+
+    _create = "cf_comm_create_peer"
 
 
 # ------------------------------------------------------------------ solver

@@ -1,7 +1,8 @@
 // cf_api.cu — the C-ABI of include/castfem_b200.h: plan object, upload,
-// stepping (CUDA graphs), multi-rank exchange (in-process or NCCL), and the
+// stepping (CUDA graphs), multi-rank exchange (in-process, NCCL, peer memory or host-staged), and the
 // host utilities. Reference interfaces replaced are cited at each entry point
 // in include/castfem_b200.h.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -106,6 +107,7 @@ struct cf_comm {
     ncclComm_t comm = nullptr;
     int world = 1, rank = 0, device = 0;
     bool host = false;        // host-staged transport (cf_comm_create_host): callbacks instead of NCCL
+    bool peer = false;        // peer-memory transport (cf_comm_create_peer): ht only bootstraps the windows
     cf_host_transport ht{};
 };
 
@@ -284,6 +286,18 @@ struct cf_plan {
     double* h_send = nullptr;    // host-staged transport: pinned copies of the send / recv payloads
     double* h_recv = nullptr;
     bool host_comm() const { return comm && comm->host && world > local_ranks; }
+    bool peer_comm() const { return comm && comm->peer && world > local_ranks; }
+    // peer-memory transport: this rank's exported window [control | recv x 2 parities] and the
+    // other ranks' windows as mapped here (CUDA IPC)
+    struct Peer {
+        uint8_t* win = nullptr;
+        std::vector<uint8_t*> mapped;          // [world]; own entry = win
+        uint8_t** d_win = nullptr;             // device copy of mapped
+        std::vector<double*> nb_dst;           // per neighbour: its receive region for this rank (parity 0)
+        std::vector<int64_t> nb_stride;        // per neighbour: its receive-buffer length (parity stride)
+        uint32_t seq = 0, rseq = 0;            // exchanges / reductions issued so far
+        bool open = false;
+    } peer;
     double* dTg = nullptr;       // global-order staging (device) for set_temperature / get_fields
     double* dHg = nullptr;
     int64_t graph_steps = 0;
@@ -292,6 +306,7 @@ struct cf_plan {
     int graph_cur = -1;
     ~cf_plan() {
         if (graph) cudaGraphExecDestroy(graph);
+        peer_close();
         for (auto& r : ranks) r->mem.release();
         if (dP) cudaFree(dP);
         if (dTg) cudaFree(dTg);
@@ -308,6 +323,22 @@ struct cf_plan {
         if (h_send) cudaFreeHost(h_send);
         if (h_recv) cudaFreeHost(h_recv);
         if (stream) cudaStreamDestroy(stream);
+    }
+    // The importers unmap a window before its owner frees it (cudaIpcOpenMemHandle's contract):
+    // every rank closes its mappings, then all meet on the bootstrap transport, then the owners free.
+    void peer_close() {
+        if (!peer.open) return;
+        peer.open = false;
+        cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        if (xside) cudaStreamSynchronize(xside);
+        for (size_t q = 0; q < peer.mapped.size(); ++q)
+            if (peer.mapped[q] && peer.mapped[q] != peer.win) cudaIpcCloseMemHandle(peer.mapped[q]);
+        peer.mapped.clear();
+        if (peer.d_win) cudaFree(peer.d_win);
+        peer.d_win = nullptr;
+        double one = 1.0;
+        if (comm && comm->ht.allreduce) comm->ht.allreduce(comm->ht.ctx, &one, 1, CF_REDUCE_MAX);
     }
 };
 
@@ -436,6 +467,7 @@ void launch_update(cf_plan* p, Rank& r, double t_end) {
     a.Tn = r.T[p->nxt()];
     a.Tslot_n = r.Tslot[p->step_parity ^ 1];  // null with gathered slot temperatures
     a.t_end = t_end;
+    if (p->peer_comm()) a.recv = r.recv + (size_t)(p->peer.seq & 1) * (size_t)r.H.recv_len;
     int blocks;
     if (p->temp_dep) {  // no fused private updates: every node
         a.list = nullptr;
@@ -476,8 +508,140 @@ void launch_pack(cf_plan* p, Rank& r, cudaStream_t st) {
     // few CTAs (grid-stride): it runs beside the persistent interior tiles in the SM slots they
     // leave free
     const int blocks = std::max(1, std::min<int>(16, (a.n_cr + a.n_t + 255) / 256));
-    if (p->mode == CF_MODE_DETERMINISTIC) pack_kernel<true><<<blocks, 256, 0, st>>>(a);
-    else pack_kernel<false><<<blocks, 256, 0, st>>>(a);
+    if (p->mode == CF_MODE_DETERMINISTIC) pack_kernel<true, false><<<blocks, 256, 0, st>>>(a);
+    else pack_kernel<false, false><<<blocks, 256, 0, st>>>(a);
+}
+
+// ------------------------------------------------------------------ peer-memory transport
+struct DriverApi {
+    CUresult (*StreamWaitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+};
+DriverApi& driver() {
+    static DriverApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            api.StreamWaitValue32 = (decltype(api.StreamWaitValue32))fn;
+        cudaGetLastError();
+    });
+    if (!api.StreamWaitValue32) raise(CF_CUDA, "cuStreamWaitValue32 not available from this driver");
+    return api;
+}
+
+void stream_wait_geq(cudaStream_t st, const uint32_t* flag, uint32_t value) {
+    const CUresult r = driver().StreamWaitValue32((CUstream)st, (CUdeviceptr)flag, value, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) raise(CF_CUDA, "cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
+}
+
+// send half of the exchange: the pack kernel stores into the neighbours' windows and raises the flags
+void launch_pack_peer(cf_plan* p, Rank& r, cudaStream_t st) {
+    cf_plan::Peer& x = p->peer;
+    PackArgs a = r.pa;
+    a.T = r.T[p->cur];
+    a.u.T = r.T[p->cur];
+    x.seq += 1;
+    a.pp.seq = x.seq;
+    const size_t nk = r.H.nbrs.size();
+    for (size_t k = 0; k < nk; ++k) a.pp.dst[k] = x.nb_dst[k] + (size_t)(x.seq & 1) * (size_t)x.nb_stride[k];
+    const int blocks = std::max(1, std::min<int>(16, (a.n_cr + a.n_t + 255) / 256));
+    if (p->mode == CF_MODE_DETERMINISTIC) pack_kernel<true, true><<<blocks, 256, 0, st>>>(a);
+    else pack_kernel<false, true><<<blocks, 256, 0, st>>>(a);
+    CF_CUDA_CHECK(cudaGetLastError());
+}
+
+// receive half: the stream waits until every neighbour's payload of this exchange has landed
+void peer_wait_payload(cf_plan* p, Rank& r, cudaStream_t st) {
+    const uint32_t* xflag = (const uint32_t*)(p->peer.win + kPeerXflagOff);
+    for (const auto& nb : r.H.nbrs) stream_wait_geq(st, xflag + nb.rank, p->peer.seq);
+}
+
+// all-reduce of n <= 2 scalars at `v` (device) over every rank of the job through the peer windows
+template <class V>
+void peer_allreduce(cf_plan* p, V* v, int n, int op0, int op1, cudaStream_t st) {
+    cf_plan::Peer& x = p->peer;
+    x.rseq += 1;
+    PeerRed pr{p->world, p->first_rank, x.rseq, x.d_win};
+    peer_put_kernel<V><<<1, kPeerMaxWorld, 0, st>>>(pr, v, n);
+    CF_CUDA_CHECK(cudaGetLastError());
+    const uint32_t* rflag = (const uint32_t*)(x.win + kPeerRflagOff);
+    for (int q = 0; q < p->world; ++q)
+        if (q != p->first_rank) stream_wait_geq(st, rflag + q, x.rseq);
+    peer_get_kernel<V><<<1, 32, 0, st>>>(pr, v, n, op0, op1);
+    CF_CUDA_CHECK(cudaGetLastError());
+}
+
+// windows exported / imported once per plan; the bootstrap transport carries the IPC handles.
+// Message to rank q (doubles as raw 8-byte carriers): [0..8) cudaIpcMemHandle_t of this rank's
+// window, [8] its receive-buffer length, [9] offset of q's region in it (-1: not a neighbour),
+// [10] length of q's region.
+void peer_setup(cf_plan* p) {
+    cf_plan::Peer& x = p->peer;
+    Rank& r = *p->ranks[0];
+    const int W = p->world, me = p->first_rank;
+    if (p->local_ranks != 1) raise(CF_INVALID_ARG, "peer-memory transport needs one rank per process");
+    if (W > kPeerMaxWorld) raise(CF_INVALID_ARG, "peer-memory transport: world_size > " + std::to_string(kPeerMaxWorld));
+    if (r.H.nbrs.size() > (size_t)kPeerMaxNbrs)
+        raise(CF_INVALID_ARG, "peer-memory transport: more than " + std::to_string(kPeerMaxNbrs) + " neighbours");
+    driver();
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    constexpr int kMsg = 11;
+    cudaIpcMemHandle_t mine;
+    CF_CUDA_CHECK(cudaIpcGetMemHandle(&mine, x.win));
+    std::vector<double> out((size_t)W * kMsg, 0.0), in((size_t)W * kMsg, 0.0);
+    std::vector<int32_t> peers;
+    std::vector<const double*> sp;
+    std::vector<double*> rp;
+    std::vector<int64_t> len;
+    for (int q = 0; q < W; ++q) {
+        if (q == me) continue;
+        double* m = out.data() + (size_t)q * kMsg;
+        std::memcpy(m, &mine, 64);
+        int64_t v[3] = {r.H.recv_len, -1, 0};
+        for (size_t k = 0; k < r.H.nbrs.size(); ++k)
+            if (r.H.nbrs[k].rank == q) {
+                v[1] = r.H.recv_off[k];
+                v[2] = r.nb_recv_len[k];
+            }
+        std::memcpy(m + 8, v, sizeof v);
+        peers.push_back(q);
+        sp.push_back(m);
+        rp.push_back(in.data() + (size_t)q * kMsg);
+        len.push_back(kMsg);
+    }
+    const cf_host_transport& t = p->comm->ht;
+    if (t.sendrecv(t.ctx, (int32_t)peers.size(), peers.data(), sp.data(), len.data(), rp.data(), len.data()) != 0)
+        raise(CF_PROTOCOL, "peer-memory transport: handle exchange failed");
+    x.mapped.assign((size_t)W, nullptr);
+    x.mapped[(size_t)me] = x.win;
+    x.open = true;
+    for (int q = 0; q < W; ++q) {
+        if (q == me) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, in.data() + (size_t)q * kMsg, 64);
+        void* base = nullptr;
+        CF_CUDA_CHECK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+        x.mapped[(size_t)q] = (uint8_t*)base;
+    }
+    CF_CUDA_CHECK(cudaMalloc(&x.d_win, sizeof(uint8_t*) * (size_t)W));
+    CF_CUDA_CHECK(cudaMemcpy(x.d_win, x.mapped.data(), sizeof(uint8_t*) * (size_t)W, cudaMemcpyHostToDevice));
+    PackArgs& pk = r.pa;
+    pk.pp.n_nbrs = (int32_t)r.H.nbrs.size();
+    pk.pp.ticket = (unsigned*)(x.win + kPeerCtrlBytes - 64);
+    for (size_t k = 0; k < r.H.nbrs.size(); ++k) {
+        const int q = r.H.nbrs[k].rank;
+        int64_t v[3];
+        std::memcpy(v, in.data() + (size_t)q * kMsg + 8, sizeof v);
+        if (v[1] < 0) raise(CF_PROTOCOL, "asymmetric neighbour lists");
+        if (v[2] != r.nb_send_len[k]) raise(CF_PROTOCOL, "payload length mismatch");
+        x.nb_dst.push_back((double*)(x.mapped[(size_t)q] + kPeerCtrlBytes) + v[1]);
+        x.nb_stride.push_back(v[0]);
+        pk.pp.send_off[k] = r.H.send_off[k];
+        pk.pp.flag[k] = (uint32_t*)(x.mapped[(size_t)q] + kPeerXflagOff) + me;
+    }
+    pk.pp.send_off[r.H.nbrs.size()] = r.H.send_len;
 }
 
 void host_allreduce(cf_plan* p, double* v, int64_t n, int32_t op) {
@@ -507,6 +671,10 @@ void exchange(cf_plan* p, cudaStream_t st) {
         return;
     }
     if (!p->comm) raise(CF_NCCL, "world_size > local ranks but no communicator");
+    if (p->peer_comm()) {  // the pack kernel already stored into the neighbours' windows
+        peer_wait_payload(p, *p->ranks[0], st);
+        return;
+    }
     if (p->host_comm()) {
         // host-staged: send payload -> pinned host -> caller's sendrecv -> pinned host -> recv buffer.
         // The previous step's H2D from h_recv is complete: it precedes this D2H on the same stream.
@@ -563,6 +731,10 @@ void reduce_min_bound(cf_plan* p, cudaStream_t st) {
         return;
     }
     unsigned long long* mb = p->ranks[0]->st->min_bound;  // positive doubles: bit order == value order
+    if (p->peer_comm()) {
+        peer_allreduce(p, mb, 2, kPeerMin, kPeerMin, st);
+        return;
+    }
     if (p->host_comm()) {
         double v[2];
         CF_CUDA_CHECK(cudaMemcpyAsync(v, mb, sizeof v, cudaMemcpyDeviceToHost, st));
@@ -593,6 +765,10 @@ void reduce_clamp(cf_plan* p, cudaStream_t st) {
         return;
     }
     int* flag = &p->ranks[0]->st->clamp_flag;
+    if (p->peer_comm()) {
+        peer_allreduce(p, flag, 1, kPeerMax, kPeerMax, st);
+        return;
+    }
     if (p->host_comm()) {
         int f = 0;
         CF_CUDA_CHECK(cudaMemcpyAsync(&f, flag, sizeof f, cudaMemcpyDeviceToHost, st));
@@ -617,7 +793,9 @@ void enqueue_step(cf_plan* p, double t_end) {
         for (auto& r : p->ranks) launch_tile(p, *r, t_end, 0);
         CF_CUDA_CHECK(cudaEventRecord(p->xfork, p->stream));
         CF_CUDA_CHECK(cudaStreamWaitEvent(p->xside, p->xfork, 0));
-        for (auto& r : p->ranks) launch_pack(p, *r, p->xside);
+        if (p->peer_comm()) launch_pack_peer(p, *p->ranks[0], p->xside);
+        else
+            for (auto& r : p->ranks) launch_pack(p, *r, p->xside);
         if (p->host_comm()) {  // the host blocks in the exchange: enqueue the interior tiles first
             for (auto& r : p->ranks) launch_tile(p, *r, t_end, 1);
             exchange(p, p->xside);
@@ -950,7 +1128,14 @@ void finish_rank(cf_plan* p, Rank& r, const RankDev& d) {
         u.shared_off = d.shared_off;
         u.shared_src_c = d.shared_src;
         u.shared_src_r = d.shared_src_r;
-        r.recv = M.alloc<double>(h.recv_len);
+        if (p->peer_comm()) {  // receive buffer (two step parities) inside the exported window
+            const size_t bytes = (size_t)kPeerCtrlBytes + 2 * sizeof(double) * (size_t)std::max<int64_t>(1, h.recv_len);
+            p->peer.win = M.alloc<uint8_t>(bytes);
+            CF_CUDA_CHECK(cudaMemsetAsync(p->peer.win, 0, bytes, s));
+            r.recv = (double*)(p->peer.win + kPeerCtrlBytes);
+        } else {
+            r.recv = M.alloc<double>(h.recv_len);
+        }
         r.send = M.alloc<double>(h.send_len);
         u.recv = r.recv;
         u.ghost_src = d.ghost_src;
@@ -1065,7 +1250,8 @@ void run_steps(cf_plan* p, int64_t n, double t_end) {
     CF_CUDA_CHECK(cudaSetDevice(p->device));
     CF_CUDA_CHECK(cudaEventRecord(p->ev0, p->stream));
     int64_t done = 0;
-    if (p->graph_steps > 0 && !p->host_comm()) {  // host-staged steps synchronise: never captured
+    // host-staged steps synchronise, peer-memory steps wait on per-step flag values: never captured
+    if (p->graph_steps > 0 && !p->host_comm() && !p->peer_comm()) {
         const int state_key = p->cur * 2 + p->step_parity;
         if (p->graph && (p->graph_t_end != t_end || p->graph_cur != state_key)) {
             cudaGraphExecDestroy(p->graph);
@@ -1401,6 +1587,7 @@ void finish_plan(cf_plan* p) {
             CF_CUDA_CHECK(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
         }
     }
+    if (p->peer_comm()) peer_setup(p);
     if (p->host_comm()) {
         const RankPlan& h = p->ranks[0]->H;
         CF_CUDA_CHECK(cudaMallocHost(&p->h_send, sizeof(double) * std::max<int64_t>(1, h.send_len)));
@@ -1596,7 +1783,8 @@ int cf_time_phases(cf_plan* p, int64_t n, double* ms_out) {
             CF_CUDA_CHECK(cudaEventRecord(ev[0], p->stream));
             for (auto& r : p->ranks) launch_tile(p, *r, 0.0);
             CF_CUDA_CHECK(cudaEventRecord(ev[1], p->stream));
-            if (p->world > 1)
+            if (p->peer_comm()) launch_pack_peer(p, *p->ranks[0], p->stream);
+            else if (p->world > 1)
                 for (auto& r : p->ranks) launch_pack(p, *r, p->stream);
             CF_CUDA_CHECK(cudaEventRecord(ev[2], p->stream));
             exchange(p, p->stream);
@@ -1660,7 +1848,9 @@ int cf_solve(cf_plan* p, int64_t max_steps, double* series, int64_t cap, int64_t
                 minmax_kernel<<<148, 256, 0, p->stream>>>(r->H.n_local, r->T[p->cur], mm);
             // the series covers the whole mesh (solve_serial blocked.hpp:678-681): min / max over
             // every rank of the job
-            if (p->world > p->local_ranks && !p->host_comm()) {
+            if (p->peer_comm()) {
+                peer_allreduce(p, (unsigned long long*)mm, 2, kPeerMin, kPeerMax, p->stream);
+            } else if (p->world > p->local_ranks && !p->host_comm()) {
                 NcclApi& n = nccl();
                 CF_NCCL_CHECK(n.AllReduce(mm, mm, 1, ncclUint64, ncclMin, p->comm->comm, p->stream));
                 CF_NCCL_CHECK(n.AllReduce((unsigned long long*)mm + 1, (unsigned long long*)mm + 1, 1, ncclUint64,
@@ -1951,6 +2141,21 @@ int cf_comm_create_host(int32_t world, int32_t rank, int32_t device, const cf_ho
         c->rank = rank;
         c->device = device;
         c->host = true;
+        c->ht = *t;
+        *out = c.release();
+    });
+}
+
+int cf_comm_create_peer(int32_t world, int32_t rank, int32_t device, const cf_host_transport* t, cf_comm** out) {
+    return guarded([&] {
+        if (!out || !t || !t->sendrecv || !t->allreduce) raise(CF_INVALID_ARG, "null argument");
+        if (world < 1 || rank < 0 || rank >= world) raise(CF_INVALID_ARG, "bad world / rank");
+        if (world > kPeerMaxWorld) raise(CF_INVALID_ARG, "peer-memory transport: world_size > " + std::to_string(kPeerMaxWorld));
+        auto c = std::make_unique<cf_comm>();
+        c->world = world;
+        c->rank = rank;
+        c->device = device;
+        c->peer = true;
         c->ht = *t;
         *out = c.release();
     });

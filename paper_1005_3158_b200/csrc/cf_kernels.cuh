@@ -927,6 +927,26 @@ __global__ void __launch_bounds__(128) fill_tiles_kernel(FillArgs f) {
 }
 
 // ------------------------------------------------------------------ pack kernel
+// Peer-memory transport (NVLink / NVSwitch P2P; CUDA IPC between the rank processes): every rank
+// owns one exported window = [control block | receive buffer x 2 step parities]. The control block
+// holds, per sending rank, the payload flag (the sender's exchange sequence number), the flag of
+// the scalar reductions and their 2-parity value slots.
+constexpr int kPeerMaxNbrs = 32;
+constexpr int kPeerMaxWorld = 64;
+constexpr int kPeerXflagOff = 0;      // u32[kPeerMaxWorld]: payload of exchange #seq from rank q has landed
+constexpr int kPeerRflagOff = 256;    // u32[kPeerMaxWorld]: reduction #seq operands of rank q have landed
+constexpr int kPeerRedOff = 512;      // u64[2 parities][kPeerMaxWorld][2]
+constexpr int kPeerCtrlBytes = 4096;  // the receive buffer starts here
+
+struct PeerPack {
+    int32_t n_nbrs;
+    uint32_t seq;                      // this exchange's sequence number (1, 2, ...)
+    unsigned* ticket;                  // CTAs done (last one raises the flags)
+    int64_t send_off[kPeerMaxNbrs + 1];  // payload offsets per neighbour (the send-buffer layout)
+    double* dst[kPeerMaxNbrs];         // the neighbour's receive region for this rank, this step's parity
+    uint32_t* flag[kPeerMaxNbrs];      // the neighbour's payload flag for this rank
+};
+
 struct PackArgs {
     int32_t n_cr, n_t;
     const int32_t* cr_node;  // local ids
@@ -937,22 +957,88 @@ struct PackArgs {
     const double* T;
     double* send;
     UpdArgs u;               // merge inputs
+    PeerPack pp;             // peer-memory transport only
 };
 
-template <bool DET>
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// PEER: exchange_and_merge's send half fused with the pack -- each value is stored
+// straight into the neighbour's receive buffer over NVLink, and the last CTA to finish raises this
+// rank's flag in every neighbour's control block (release at system scope after every CTA's
+// system-scope fence), on which the neighbour's stream waits before its update.
+template <bool DET, bool PEER>
 __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
     const int stride = gridDim.x * blockDim.x;
+    auto out = [&](int64_t off) -> double* {
+        if (!PEER) return a.send + off;
+        int k = 0;
+        while (k + 1 < a.pp.n_nbrs && off >= a.pp.send_off[k + 1]) ++k;
+        return a.pp.dst[k] + (off - a.pp.send_off[k]);
+    };
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < a.n_cr + a.n_t; j += stride) {
         if (j < a.n_cr) {
             double c, r;
             own_partial<DET>(a.u, a.cr_node[j], c, r);
-            a.send[a.cr_dst[j]] = c;
-            a.send[a.cr_dst_r[j]] = r;
+            *out(a.cr_dst[j]) = c;
+            *out(a.cr_dst_r[j]) = r;
         } else {
             const int k = j - a.n_cr;
-            a.send[a.t_dst[k]] = a.T[a.t_node[k]];
+            *out(a.t_dst[k]) = a.T[a.t_node[k]];
         }
     }
+    if (PEER) {
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned done = atomicAdd(a.pp.ticket, 1u);
+            if (done == gridDim.x - 1) {
+                *a.pp.ticket = 0;
+                __threadfence_system();
+                for (int k = 0; k < a.pp.n_nbrs; ++k) st_release_sys(a.pp.flag[k], a.pp.seq);
+            }
+        }
+    }
+}
+
+// Scalar all-reduce over the peer windows (dynamic dt: min of the per-step bound, blocked.hpp:477-480;
+// clamp flag: max, :526-534; series T min / max, :678-681). put: this rank's operands into its slot
+// of every other rank's control block + flag; the stream then waits for every rank's flag; get:
+// combine the slots of this rank's own block. Slots alternate by sequence parity: a rank can be at
+// most one reduction ahead of any other (it waited for everyone's previous operands).
+struct PeerRed {
+    int32_t world, rank;
+    uint32_t seq;
+    uint8_t* const* win;  // [world] window bases as mapped in this process (own included)
+};
+enum { kPeerMin = 0, kPeerMax = 1 };
+
+template <class V>
+__global__ void peer_put_kernel(PeerRed pr, const V* src, int n) {
+    const int q = threadIdx.x;
+    if (q >= pr.world || q == pr.rank) return;
+    unsigned long long* slot = (unsigned long long*)(pr.win[q] + kPeerRedOff) +
+                               (((size_t)(pr.seq & 1) * kPeerMaxWorld + pr.rank) * 2);
+    for (int k = 0; k < n; ++k) slot[k] = (unsigned long long)src[k];
+    __threadfence_system();
+    st_release_sys((uint32_t*)(pr.win[q] + kPeerRflagOff) + pr.rank, pr.seq);
+}
+
+template <class V>
+__global__ void peer_get_kernel(PeerRed pr, V* dst, int n, int op0, int op1) {
+    if (threadIdx.x >= n) return;
+    const int k = threadIdx.x;
+    const int op = k == 0 ? op0 : op1;
+    unsigned long long v = (unsigned long long)dst[k];
+    const volatile unsigned long long* base = (const volatile unsigned long long*)(pr.win[pr.rank] + kPeerRedOff) +
+                                              (size_t)(pr.seq & 1) * kPeerMaxWorld * 2;
+    for (int q = 0; q < pr.world; ++q) {
+        if (q == pr.rank) continue;
+        const unsigned long long w = base[q * 2 + k];
+        v = op == kPeerMin ? (w < v ? w : v) : (w > v ? w : v);
+    }
+    dst[k] = (V)v;
 }
 
 // global-order host field -> rank-local T ring (all 3 buffers) and slot copies

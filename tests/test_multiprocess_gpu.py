@@ -1,12 +1,16 @@
 """Multi-process decomposition through the product path: one process per rank, every rank on
 cuda:0, the exchange_and_merge payload moved by the host-staged transport
-(cf_comm_create_host over a gloo process group; NCCL refuses two ranks on one device).
+(cf_comm_create_host over a gloo process group; NCCL refuses two ranks on one device) or by the
+peer-memory transport (cf_comm_create_peer: the pack kernel stores into the neighbours'
+IPC-exported windows and raises step flags the neighbours' streams wait on).
 
 Each process builds only its own rank's plan (local_ranks = 1), steps, and writes the nodes it
 owns; the merged field must be bitwise equal to the oracle replaying the same parts and tiles
 (per node: ascending-rank sum of each rank's ascending-tile partial), replicas of shared nodes
 bitwise identical, and the whole-mesh statistics (clamp steps, series T_min / T_max, dynamic dt)
-equal on every rank. No kernel waits on another process's kernel: the ranks meet on the host.
+equal on every rank. No kernel waits on another process's kernel: the ranks meet on the host
+(host-staged) or their streams wait on flag values (peer memory: cuStreamWaitValue32 holds the
+stream, not an SM, so the processes time-slicing one GPU cannot block each other).
 """
 import multiprocessing as mp
 import os
@@ -35,14 +39,14 @@ def _case(kind):
     return _dirichlet_tdep_case()
 
 
-def _worker(rank, world, port, kind, steps, mode, out):
+def _worker(rank, world, port, kind, steps, mode, out, transport="host"):
     import torch.distributed as dist
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         from paper_1005_3158_b200 import castfem as cf
         mesh, setup = _case(kind)
         setup.solver.output_every = 10
-        comm = cf.HostComm(world, rank, 0)
+        comm = (cf.PeerComm if transport == "peer" else cf.HostComm)(world, rank, 0)
         opts = cf.SolveOptions(max_steps=steps, mode=mode, tile_elems=128, world_size=world, rank=rank,
                                local_ranks=1, comm=comm)
         with cf.Solver(mesh, setup, opts) as s:
@@ -58,15 +62,15 @@ def _worker(rank, world, port, kind, steps, mode, out):
         dist.destroy_process_group()
 
 
-def _run(kind, world, steps, mode, tmp_path):
+def _run(kind, world, steps, mode, tmp_path, transport="host"):
     port = _free_port()
     ctx = mp.get_context("spawn")
     outs = [str(tmp_path / f"rank{r}.npz") for r in range(world)]
-    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, steps, mode, outs[r])) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, steps, mode, outs[r], transport)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(timeout=600)
+        p.join(timeout=300)
     for p in procs:
         if p.is_alive():
             p.kill()
@@ -86,13 +90,14 @@ def _merge(res):
     return T
 
 
+@pytest.mark.parametrize("transport", ["host", "peer"])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("mode", ["deterministic", "atomic"])
-def test_host_transport_processes_vs_oracle(world, mode, tmp_path):
+def test_host_transport_processes_vs_oracle(world, mode, transport, tmp_path):
     from oracle import oracle as orc
     from paper_1005_3158_b200 import castfem as cf
     steps = 30
-    res = _run("casting", world, steps, mode, tmp_path)
+    res = _run("casting", world, steps, mode, tmp_path, transport)
     T = _merge(res)
     mesh, setup = _case("casting")
     setup.solver.output_every = 10
@@ -113,14 +118,15 @@ def test_host_transport_processes_vs_oracle(world, mode, tmp_path):
     assert np.allclose(res[0]["series"][:, 1:], ref.series[:, 1:], rtol=1e-9, atol=0)
 
 
-def test_host_transport_dynamic_dt_and_clamps(tmp_path):
+@pytest.mark.parametrize("transport", ["host", "peer"])
+def test_host_transport_dynamic_dt_and_clamps(transport, tmp_path):
     """Temperature-dependent tables: the per-step stable bound is min-reduced over the processes
     (blocked.hpp:477-480 is a min over the whole mesh) and a step counts as clamped when any
     rank's node clamps (blocked.hpp:526-534) -- identical on every rank, equal to the oracle."""
     from oracle import oracle as orc
     from paper_1005_3158_b200 import castfem as cf
     steps, world = 60, 2
-    res = _run("tdep", world, steps, "deterministic", tmp_path)
+    res = _run("tdep", world, steps, "deterministic", tmp_path, transport)
     T = _merge(res)
     mesh, setup = _case("tdep")
     parts = cf.partition_rcb(mesh, world)

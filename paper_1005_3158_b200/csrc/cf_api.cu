@@ -531,8 +531,20 @@ DriverApi& driver() {
     return api;
 }
 
+// GEQ is a cyclic compare ((int32)(*flag - value) >= 0), so the sequence numbers may wrap. The
+// payload stores are ordered before the flag by the sender's system-scope fence + release; where
+// the device can also flush third-party remote writes behind a wait, ask for that too.
 void stream_wait_geq(cudaStream_t st, const uint32_t* flag, uint32_t value) {
-    const CUresult r = driver().StreamWaitValue32((CUstream)st, (CUdeviceptr)flag, value, CU_STREAM_WAIT_VALUE_GEQ);
+    static const unsigned flush = [] {
+        int dev = 0, can = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&can, cudaDevAttrCanFlushRemoteWrites, dev) != cudaSuccess)
+            can = 0;
+        cudaGetLastError();
+        return can ? (unsigned)CU_STREAM_WAIT_VALUE_FLUSH : 0u;
+    }();
+    const CUresult r =
+        driver().StreamWaitValue32((CUstream)st, (CUdeviceptr)flag, value, CU_STREAM_WAIT_VALUE_GEQ | flush);
     if (r != CUDA_SUCCESS) raise(CF_CUDA, "cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
 }
 

@@ -64,7 +64,7 @@ def config1(n: int = 32, seed: int = 1, dt_safety: float = DT_SAFETY["cfg1"]) ->
 
 def casting(n: int, jitter: float = 0.0, seed: int = 0, perm_seed: int = 0, dt_safety: float = 0.138,
             steps: int = 1000, name: Optional[str] = None, h_interface: float = H_INTERFACE,
-            noise: float = T0_NOISE, noise_seed: int = 1) -> Case:
+            noise: float = T0_NOISE, noise_seed: int = 1, radius: float = 0.35) -> Case:
     """Two-material casting (configs 2-5): Al sphere r=0.35 in a sand mould, outer h=20, T_inf=300.
 
     T0 = region pouring temperature + U(-noise, noise) keyed by grid point (the
@@ -74,7 +74,7 @@ def casting(n: int, jitter: float = 0.0, seed: int = 0, perm_seed: int = 0, dt_s
     C_app = 0 and explicit_update throws "zero lumped capacitance" — at step 30
     of cfg2, node 802288, in the reference and in this path alike
     (tests/test_gpu_parity.py::test_uniform_t0_degeneracy_matches_reference)."""
-    m = generate_fixture("casting", n, radius=0.35, jitter=jitter, seed=seed, perm_seed=perm_seed)
+    m = generate_fixture("casting", n, radius=radius, jitter=jitter, seed=seed, perm_seed=perm_seed)
     T0 = None
     if noise:
         base = np.where(_node_region(m) == 0, aluminium().initial_temperature, sand().initial_temperature)

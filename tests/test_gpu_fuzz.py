@@ -1,0 +1,76 @@
+"""Seeded random sweep of the plan options against the CPU oracle.
+
+The parity suite fixes one combination per feature; here 48 seeded draws combine mesh size,
+jitter, element / node permutation, casting radius, tile size, tile layout, element order, node
+order, rank count, mode and the physics variant (constant properties; c(T), k(T) tables with
+dynamic dt; a Dirichlet f(t) face; interface h(T-bar)), each checked through the C-ABI against
+the oracle replaying the same tiles (and parts): deterministic bitwise, atomic within the
+north_star tolerance of 1e-9 relative. Draws are reproducible (the seed is the test id).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_1005_3158_b200 import castfem as cf
+from paper_1005_3158_b200 import configs
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-9
+
+
+def _draw(seed):
+    rng = np.random.default_rng(1000 + seed)
+    d = dict(
+        n=int(rng.integers(5, 15)),
+        jitter=float(rng.choice([0.0, 0.1, 0.2])),
+        perm=int(rng.integers(0, 4)) * int(rng.integers(1, 100)),  # 0 = generator numbering
+        radius=float(rng.choice([0.25, 0.35, 0.45])),
+        tile=int(rng.choice([96, 128, 192, 256, 384, 512, 768])),
+        geometry=str(rng.choice(["stored", "coords"])),
+        elem_order=str(rng.choice(["morton", "min_node", "given"])),
+        node_order=str(rng.choice(["tile", "rcm", "given"])),
+        ranks=int(rng.choice([1, 1, 2, 3, 5])),
+        mode=str(rng.choice(["deterministic", "deterministic", "atomic"])),
+        steps=int(rng.integers(5, 40)),
+        physics=str(rng.choice(["plain", "plain", "tdep", "dirichlet", "h_of_T"])),
+    )
+    return d
+
+
+def _apply_physics(case, kind):
+    m, setup = case.mesh, case.setup
+    if kind == "tdep":  # piecewise-linear c(T), k(T) in the casting: dynamic dt (blocked.hpp:477-480)
+        setup.materials[0] = cf.MaterialTable.make(
+            rho=2700.0, c=[(300.0, 850.0), (1000.0, 1100.0)], k=[(300.0, 230.0), (1000.0, 90.0)],
+            latent_heat=3.9e5, solidus=821.0, liquidus=913.0, T0=973.0)
+        setup.solver.dt_safety = 0.1
+    elif kind == "dirichlet":  # the x = 0 face held at f(t) (lowest tag wins, blocked.hpp:250-263)
+        x0 = np.all(m.nodes[m.facets][:, :, 0] == 0.0, axis=1) & (m.facet_tag == m.tags.index("outer"))
+        m.tags = list(m.tags) + ["chill"]
+        m.facet_tag = np.where(x0, len(m.tags) - 1, m.facet_tag).astype(np.int32)
+        setup.boundary_conditions["chill"] = cf.BoundaryCondition(
+            "fixed", fixed_T=cf.PiecewiseLinear([0.0, 200.0], [300.0, 420.0]))
+    elif kind == "h_of_T":  # interface coefficient h(T-bar of the facet) (blocked.hpp:485-490)
+        setup.interface_coeffs[0] = cf.InterfaceCoeff(
+            "cast_if", "mold_if", "temperature", cf.PiecewiseLinear([300.0, 1000.0], [400.0, 1600.0]))
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_random_plan_options_vs_oracle(seed):
+    d = _draw(seed)
+    case = configs.casting(d["n"], radius=d["radius"], jitter=d["jitter"], seed=seed, perm_seed=d["perm"],
+                           dt_safety=0.14)
+    _apply_physics(case, d["physics"])
+    opts = cf.SolveOptions(max_steps=d["steps"], mode=d["mode"], tile_elems=d["tile"], geometry=d["geometry"],
+                           elem_order=d["elem_order"], node_order=d["node_order"], world_size=d["ranks"],
+                           local_ranks=d["ranks"])
+    gpu = cf.solve(case.mesh, case.setup, opts)
+    tiles, _ = cf.tile_map(case.mesh, case.setup, opts)
+    parts = cf.partition_rcb(case.mesh, d["ranks"]) if d["ranks"] > 1 else None
+    ref = orc.solve(case.mesh, case.setup, d["steps"], blocks=tiles, parts=parts)
+    assert gpu.steps == d["steps"] and gpu.end_time == ref.time, d
+    if d["mode"] == "deterministic":
+        assert np.array_equal(gpu.T, ref.T), (d, float(np.abs(gpu.T - ref.T).max()))
+        assert np.array_equal(gpu.H, ref.H), d
+    else:
+        assert float(np.max(np.abs(gpu.T - ref.T) / np.abs(ref.T))) <= RTOL, d

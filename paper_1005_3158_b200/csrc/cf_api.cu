@@ -297,6 +297,7 @@ struct cf_plan {
         std::vector<int64_t> nb_stride;        // per neighbour: its receive-buffer length (parity stride)
         uint32_t seq = 0, rseq = 0;            // exchanges / reductions issued so far
         bool open = false;
+        cf_host_transport boot{};              // bootstrap callbacks (copied: the barrier at destruction)
     } peer;
     double* dTg = nullptr;       // global-order staging (device) for set_temperature / get_fields
     double* dHg = nullptr;
@@ -338,7 +339,7 @@ struct cf_plan {
         if (peer.d_win) cudaFree(peer.d_win);
         peer.d_win = nullptr;
         double one = 1.0;
-        if (comm && comm->ht.allreduce) comm->ht.allreduce(comm->ht.ctx, &one, 1, CF_REDUCE_MAX);
+        if (peer.boot.allreduce) peer.boot.allreduce(peer.boot.ctx, &one, 1, CF_REDUCE_MAX);
     }
 };
 
@@ -624,6 +625,7 @@ void peer_setup(cf_plan* p) {
         len.push_back(kMsg);
     }
     const cf_host_transport& t = p->comm->ht;
+    x.boot = t;
     if (t.sendrecv(t.ctx, (int32_t)peers.size(), peers.data(), sp.data(), len.data(), rp.data(), len.data()) != 0)
         raise(CF_PROTOCOL, "peer-memory transport: handle exchange failed");
     x.mapped.assign((size_t)W, nullptr);

@@ -1,6 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-bash scripts/gpu_r02e.sh > gpurun_out/r02f_devsetup.txt 2>&1
+bash scripts/runs/gpu_r02e.sh > gpurun_out/r02f_devsetup.txt 2>&1
 cat gpurun_out/r02f_devsetup.txt | grep -v "^\[cf setup\]" | tail -12
 timeout 1500 python -m pytest tests -m gpu -q -x --durations=12 > gpurun_out/gputests_r02f.log 2>&1
 echo "suite rc=$?"; tail -16 gpurun_out/gputests_r02f.log

@@ -210,8 +210,7 @@ struct Rank {
     int32_t* sched = nullptr;               // dynamic tile-scheduling counter (persistent grids)
     double* recv = nullptr;
     double* send = nullptr;
-    double* acc_c = nullptr;
-    double* acc_r = nullptr;
+    double2* acc = nullptr;  // atomic mode: per node (c, r) accumulators
     double2* part = nullptr;
     DevState* st = nullptr;
     // tile launches of one step: tiles grouped by shared-memory footprint, so the common
@@ -981,14 +980,11 @@ void finish_rank(cf_plan* p, Rank& r, const RankDev& d) {
     if (det) {
         r.part = M.alloc<double2>(S_tot);
     } else {
-        r.acc_c = M.alloc<double>(h.n_local);
-        r.acc_r = M.alloc<double>(h.n_local);
-        CF_CUDA_CHECK(cudaMemsetAsync(r.acc_c, 0, sizeof(double) * std::max<int64_t>(1, h.n_local), s));
-        CF_CUDA_CHECK(cudaMemsetAsync(r.acc_r, 0, sizeof(double) * std::max<int64_t>(1, h.n_local), s));
+        r.acc = M.alloc<double2>(h.n_local);
+        CF_CUDA_CHECK(cudaMemsetAsync(r.acc, 0, sizeof(double2) * std::max<int64_t>(1, h.n_local), s));
     }
     a.part = r.part;
-    a.acc_c = r.acc_c;
-    a.acc_r = r.acc_r;
+    a.acc = r.acc;
     a.P = p->dP;
     a.st = r.st;
     a.n_tiles = h.n_tiles;
@@ -1126,8 +1122,7 @@ void finish_rank(cf_plan* p, Rank& r, const RankDev& d) {
     u.merge_off = d.merge_off;  // partial merge (deterministic) + Tslot scatter (both modes)
     u.merge_idx = d.merge_idx;
     u.part = r.part;
-    u.acc_c = r.acc_c;
-    u.acc_r = r.acc_r;
+    u.acc = r.acc;
     u.node_dir = node_dir;
     u.node_region = node_region;
     u.local_global = local_global;
@@ -1221,10 +1216,9 @@ void scatter_state(cf_plan* p) {
         const int64_t S_tot = r.S_tot;
         const int sb = (int)std::max<int64_t>(1, std::min<int64_t>(1184, (S_tot + 255) / 256));
         if (r.Tslot[0]) slot_init_kernel<<<sb, 256, 0, p->stream>>>(S_tot, r.ta.slot_node, r.T[0], r.Tslot[0], r.Tslot[1]);
-        if (r.acc_c) {  // atomic mode: no partial sums survive a re-initialisation
-            const size_t nb = sizeof(double) * std::max<int64_t>(1, r.H.n_local);
-            CF_CUDA_CHECK(cudaMemsetAsync(r.acc_c, 0, nb, p->stream));
-            CF_CUDA_CHECK(cudaMemsetAsync(r.acc_r, 0, nb, p->stream));
+        if (r.acc) {  // atomic mode: no partial sums survive a re-initialisation
+            const size_t nb = sizeof(double2) * std::max<int64_t>(1, r.H.n_local);
+            CF_CUDA_CHECK(cudaMemsetAsync(r.acc, 0, nb, p->stream));
         }
         DevState st{};
         st.min_bound[0] = st.min_bound[1] = 0x7ff0000000000000ull;

@@ -155,8 +155,7 @@ struct TileArgs {
     const double* Tslot; // current T of every tile slot
     double* Tslot_n;     // next T of every tile slot (tile-private slots written here)
     double2* part;       // per (tile, slot) partial (c, r)   [deterministic]
-    double* acc_c;       // per node RED accumulators         [atomic]
-    double* acc_r;
+    double2* acc;        // per node (c, r) RED accumulators, one 16-byte pair per node  [atomic]
     const DevParams* P;
     DevState* st;
     const TileDesc* desc;      // tiles of this launch (metadata + offsets, one 32 B record each)
@@ -621,8 +620,8 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             } else if (DET) {
                 a.part[s0 + s] = make_double2(c, r);
             } else {
-                atomicAdd(&a.acc_c[node], c);
-                atomicAdd(&a.acc_r[node], r);
+                atomicAdd(&a.acc[node].x, c);  // both REDs land in the node's one sector
+                atomicAdd(&a.acc[node].y, r);
             }
         };
         // the first slot of every thread keeps its result in registers and flushes after the next
@@ -692,8 +691,7 @@ struct UpdArgs {
     const int32_t* merge_off;
     const int32_t* merge_idx;
     const double2* part;
-    double* acc_c;
-    double* acc_r;
+    double2* acc;
     const int8_t* node_dir;
     const uint8_t* node_region;
     const int32_t* local_global;
@@ -722,8 +720,9 @@ __device__ __forceinline__ void own_partial(const UpdArgs& a, int i, double& c, 
             r += pr.y;
         }
     } else {
-        c = a.acc_c[i];
-        r = a.acc_r[i];
+        const double2 v = a.acc[i];
+        c = v.x;
+        r = v.y;
     }
 }
 
@@ -757,8 +756,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         const double T = __ldg(a.T + i);
         if (done) {
             if (!DET) {  // the tile kernel still accumulated this (no-op) step: drop it
-                a.acc_c[i] = 0;
-                a.acc_r[i] = 0;
+                a.acc[i] = make_double2(0.0, 0.0);
             }
             a.Tn[i] = T;
             if (!a.Tslot_n) continue;
@@ -789,8 +787,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
             own_partial<DET>(a, i, c, r);
         }
         if (!DET) {
-            a.acc_c[i] = 0;
-            a.acc_r[i] = 0;
+            a.acc[i] = make_double2(0.0, 0.0);
         }
         if (MULTI) {
             const int32_t sh = a.node_shared[i];

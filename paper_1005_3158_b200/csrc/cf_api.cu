@@ -1147,6 +1147,7 @@ void finish_rank(cf_plan* p, Rank& r, const RankDev& d) {
         }
         r.send = M.alloc<double>(h.send_len);
         u.recv = r.recv;
+        u.n_recv = h.recv_len;
         u.ghost_src = d.ghost_src;
         std::vector<int32_t> cr_node, t_node;
         std::vector<int64_t> cr_dst, cr_dst_r, t_dst;

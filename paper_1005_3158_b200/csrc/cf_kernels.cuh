@@ -680,6 +680,7 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
 struct UpdArgs {
     int32_t n_list, n_local, n_ghost;
     int64_t n_slots;      // bounds (CF_BOUNDS builds)
+    int64_t n_recv;       // bounds: doubles in one parity of the receive buffer
     int32_t probe;        // diagnostics only (CF_PROBE; results invalid): 8 = no slot-copy writes,
                           // 9 = no partial reads
     const int32_t* list;  // nodes to merge + update (NULL: all local nodes)
@@ -799,6 +800,7 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
                         ct += c;
                         rt += r;
                     } else {
+                        CF_ASSERT(sc < a.n_recv && a.shared_src_r[j] >= 0 && a.shared_src_r[j] < a.n_recv);
                         ct += a.recv[sc];
                         rt += a.recv[a.shared_src_r[j]];
                     }
@@ -823,8 +825,10 @@ __global__ void __launch_bounds__(256) update_kernel(UpdArgs a) {
         }
     }
     if (MULTI)
-        for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < a.n_ghost; g += stride)
+        for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < a.n_ghost; g += stride) {
+            CF_ASSERT(a.ghost_src[g] >= 0 && a.ghost_src[g] < a.n_recv);
             a.Tcur_w[a.n_local + g] = a.recv[a.ghost_src[g]];
+        }
     if (CLAMP && clamped) a.st->clamp_flag = 1;
 }
 
@@ -970,6 +974,7 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
     const int stride = gridDim.x * blockDim.x;
     auto out = [&](int64_t off) -> double* {
         if (!PEER) return a.send + off;
+        CF_ASSERT(off >= 0 && off < a.pp.send_off[a.pp.n_nbrs]);  // inside this rank's payload layout
         int k = 0;
         while (k + 1 < a.pp.n_nbrs && off >= a.pp.send_off[k + 1]) ++k;
         return a.pp.dst[k] + (off - a.pp.send_off[k]);
@@ -977,6 +982,7 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < a.n_cr + a.n_t; j += stride) {
         if (j < a.n_cr) {
             double c, r;
+            CF_ASSERT(a.cr_node[j] >= 0 && a.cr_node[j] < a.u.n_local);
             own_partial<DET>(a.u, a.cr_node[j], c, r);
             *out(a.cr_dst[j]) = c;
             *out(a.cr_dst_r[j]) = r;

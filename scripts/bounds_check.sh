@@ -7,4 +7,4 @@ cd "$(dirname "$0")/.."
 make -s -j8 -C paper_1005_3158_b200/csrc OBJDIR=../../build/obj_bounds OUT=../libcastfem_b200_bounds.so BOUNDS=1
 CF_LIB_PATH=paper_1005_3158_b200/libcastfem_b200_bounds.so timeout 1500 python -m pytest \
     tests/test_gpu_parity.py tests/test_gpu_edge.py tests/test_gpu_devsetup.py tests/test_multiprocess_gpu.py \
-    tests/test_gpu_physics.py tests/test_gpu_rcm.py -q -x 2>&1 | tail -4
+    tests/test_gpu_physics.py tests/test_gpu_rcm.py tests/test_gpu_fuzz.py -q -x 2>&1 | tail -4

@@ -74,6 +74,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-blocked", action="store_true",
                     help="--impl reference: also time the reference's own cache blocking (autotune_block_count)")
+    ap.add_argument("--ref-replicas", type=int, default=-1,
+                    help="--impl reference: also run this many independent copies of the serial reference at once, "
+                         "each pinned to its own core on its own 2-cell z-slab of the mesh (no exchange between "
+                         "them): an upper bound for what the host's cores could do with a perfectly parallel "
+                         "CPU run; -1 = one per core (default), 0 = skip")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", type=int, default=0, help="capture the step loop in CUDA graphs of this many steps")
     ap.add_argument("--phase-steps", type=int, default=20)
@@ -161,6 +166,49 @@ def reference_sample(cfg: str, steps: int, warmup: int, blocks: int = 1, autotun
     return r, None
 
 
+def reference_replicas(cfg: str, steps: int, warmup: int, want: int):
+    """`want` concurrent copies of the serial reference (ref_bench), each pinned to one core, each
+    on its own 2-cell z-slab window of the cfg mesh (adiabatic cut planes, no exchange): the
+    aggregate rate bounds from above what a perfectly parallel CPU run of the reference could reach
+    on this host. Reported beside the 1-core figure; the reference itself is serial by contract."""
+    n = {"cfg2": 128, "cfg4": 256, "cfg5": 512}.get(cfg)
+    if n is None or not os.path.exists(REF_BENCH):
+        return {"error": "replicas need a casting config and oracle/_ref/ref_bench"}
+    cores = sorted(os.sched_getaffinity(0))
+    P = len(cores) if want < 0 else min(want, len(cores))
+    P = min(P, n // 2)
+    try:  # ~1.5 GB per 2-cell slab of a 512^2 cross-section: stay well inside the free memory
+        with open("/proc/meminfo") as f:
+            avail_kb = next(int(l.split()[1]) for l in f if l.startswith("MemAvailable"))
+        P = max(1, min(P, int(avail_kb / 1e6 / (2.0 * (n / 512.0) ** 2 + 0.2) / 2)))
+    except Exception:
+        P = min(P, 16)
+    # slabs that cut the casting sphere (|z - 0.5| < 0.35), so every copy has both materials and
+    # the interface; disjoint while P <= 0.33 n, as here
+    lo, hi = int(0.16 * n) + 1, int(0.84 * n) - 3
+    P = min(P, (hi - lo) // 2 + 1)
+    procs = []
+    for k in range(P):
+        z0 = lo + (2 * (((hi - lo) // 2) * k // max(1, P - 1)) if P > 1 else (hi - lo) // 2)
+        cmd = ["taskset", "-c", str(cores[k]), REF_BENCH, "--workload", cfg, "--steps", str(steps), "--warmup",
+               str(warmup), "--blocks", "1", "--window", f"0:{n},0:{n},{z0}:{z0 + 2}"]
+        procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    res = []
+    for pr in procs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            return {"error": f"ref_bench replica failed ({pr.returncode}): {err.strip()[-200:]}"}
+        res.append(json.loads(out.strip().splitlines()[-1]))
+    work = sum(r["elements"] * r["steps"] for r in res)
+    slowest = max(r["seconds"] for r in res)
+    return {"value": work / slowest, "unit": "element-updates/s", "cores": P, "kind": "reference",
+            "sample": f"{P} concurrent copies of the serial reference, one per core (taskset), each {steps} "
+                      f"blocked_step calls on its own 0:{n} x 0:{n} x 2-cell z-slab of the {cfg} mesh; total work / "
+                      f"slowest copy's loop time; no exchange between copies (upper bound for a parallel CPU run)",
+            "per_copy_min": min(r["element_updates_per_s"] for r in res),
+            "per_copy_max": max(r["element_updates_per_s"] for r in res), "slowest_seconds": slowest}
+
+
 def cpu_reference_rate(cfg: str, steps: int, rcm: bool = False):
     r, err = reference_sample(cfg, steps, 1, rcm=rcm)
     if r is None:
@@ -194,6 +242,12 @@ def run_reference(args):
                                    window=[0, 512, 0, 512, 255, 257] if cfg == "cfg5" else "default",
                                    rcm=rcm)
         blocked = b if b is not None else {"error": berr}
+    replicas = None
+    if args.ref_replicas:  # reported beside the 1-core figure, never instead of it
+        try:
+            replicas = reference_replicas(cfg, steps, warmup, args.ref_replicas)
+        except Exception as e:  # noqa: BLE001 -- an extra figure must not take the arm down
+            replicas = {"error": f"{type(e).__name__}: {e}"}
     assert not _maps_product_library(), "the reference arm must not load the product library"
     value = r["element_updates_per_s"]
     line = {"impl": "reference", "metric": "element-updates/s (fp64)", "value": value, "unit": "element-updates/s",
@@ -207,7 +261,7 @@ def run_reference(args):
             "e2e": {"value": value, "unit": "element-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "reference_run": {k: r[k] for k in ("seconds", "setup_seconds", "dt", "T_sum", "T_min", "T_max",
                                                 "interface_pairs")},
-            "reference_blocked": blocked}
+            "reference_blocked": blocked, "reference_replicas": replicas}
     print(json.dumps(line), flush=True)
 
 

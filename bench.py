@@ -352,6 +352,11 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("gloo")
         pg = dist
+        # launchers that isolate each rank with CUDA_VISIBLE_DEVICES show one device per process
+        import torch
+        ndev = torch.cuda.device_count()
+        if ndev > 0:
+            local_rank %= ndev
     from paper_1005_3158_b200 import castfem as cf
 
     mesh_rcm = mesh_rcm_default(args.config, args.mesh_rcm)

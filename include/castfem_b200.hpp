@@ -54,6 +54,13 @@ struct SolveOptions {             // castfem::SolveOptions (blocked.hpp:630-636)
     int tile_elems = 384;
     int geometry = CF_GEOM_STORED;
     int device = 0;
+    // domain decomposition (SPEC S:413-485 parallel_solve; partition.hpp:377-422): RCB parts unless
+    // part_of_element (load_partmap's vector) is given. local_ranks == world_size runs every rank
+    // in this process on `device` (the SPEC's mandatory in-process transport); one rank per
+    // process needs a cf_comm (cf_comm_create / _peer / _host) and returns this rank's nodes.
+    int world_size = 1, rank = 0, local_ranks = 1;
+    const std::vector<int>* part_of_element = nullptr;
+    cf_comm* comm = nullptr;
 };
 
 struct SeriesSample {
@@ -174,8 +181,17 @@ class Plan {
         ro.elem_order = o.elem_order;
         ro.tile_elems = o.tile_elems;
         ro.geometry = o.geometry;
-        ro.world_size = 1;
-        ro.local_ranks = 1;
+        ro.world_size = o.world_size;
+        ro.rank = o.rank;
+        ro.local_ranks = o.local_ranks;
+        static_assert(sizeof(int) == sizeof(int32_t), "part_of_element is passed as int32");
+        if (o.part_of_element) {
+            if (o.part_of_element->size() != m.tets.size())
+                throw error(CF_INVALID_ARG, "part_of_element needs one entry per element");
+            ro.partition = CF_PARTITION_GIVEN;
+            ro.part_of_element = reinterpret_cast<const int32_t*>(o.part_of_element->data());
+        }
+        ro.comm = o.comm;
         check(cf_plan_create(d.mesh(), d.setup(), &ro, &plan_));
     }
     ~Plan() {

@@ -91,5 +91,23 @@ int main() {
                          tr.seconds[0] > 0 && tr.seconds[1] > 0;
     std::printf("autotune: chosen %d (%.3e s, %.3e s) %s\n", tr.chosen, tr.seconds[0], tr.seconds[1],
                 tune_ok ? "OK" : "BAD");
-    return ok && tune_ok ? 0 : 1;
+    // non-overlapped element decomposition through the shim: 3 ranks in this
+    // process (the in-process transport), RCB parts and a given part map, vs solve_serial
+    bool dd_ok = true;
+    for (int given = 0; given < 2; ++given) {
+        castfem_b200::SolveOptions dd = go;
+        dd.world_size = dd.local_ranks = 3;
+        dd.tile_elems = 128;
+        std::vector<int> parts(m.tets.size());
+        for (size_t e = 0; e < parts.size(); ++e) parts[e] = (int)(e % 3);  // scattered: every node shared
+        if (given) dd.part_of_element = &parts;
+        const castfem_b200::SolveResult r3 = castfem_b200::solve_gpu(m, s, dd);
+        double w3 = 0;
+        for (size_t i = 0; i < ref.T.size(); ++i) w3 = std::max(w3, std::fabs(r3.T[i] - ref.T[i]) / std::fabs(ref.T[i]));
+        const bool k = w3 <= 1e-9 && r3.steps == ref.steps && r3.end_time == ref.end_time &&
+                       r3.clamp_steps == ref.clamp_steps;
+        std::printf("decomposed (3 ranks, %s): max_rel=%.3e %s\n", given ? "given parts" : "RCB", w3, k ? "OK" : "MISMATCH");
+        dd_ok = dd_ok && k;
+    }
+    return ok && tune_ok && dd_ok ? 0 : 1;
 }

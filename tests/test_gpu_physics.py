@@ -1,4 +1,4 @@
-"""Physics acceptance checks against analytic solutions (SPEC acceptance criteria 4-5),
+"""Physics acceptance checks (SPEC acceptance criteria 2-5; 4-5 against analytic solutions),
 through the B200 path: the bitwise parity tests prove the step equals the reference's; these
 check that the configured physics (lumped explicit FE, Dirichlet f(t), Lemmon apparent heat
 capacity with latent heat) solves the problems SPEC names.
@@ -98,3 +98,28 @@ def test_neumann_stefan_front_within_five_percent():
     lam = _stefan_lambda(1.0 * (Tm - Tw) / L)
     exact = 2.0 * lam * math.sqrt(r.end_time)
     assert abs(front - exact) / exact <= 0.05, (front, exact)
+
+
+def test_conservation_1000_steps_and_decomposed_run():
+    """SPEC acceptance criteria 2-3 through the B200 path: an adiabatic, constant-property
+    10^3-cell cube with a seeded non-uniform T0 conserves sum_i C_i T_i to 1e-10 relative over 1000
+    steps (lumped C_i = sum_e rho c V_e / 4), in one rank and split over 3 in-process ranks, and the
+    decomposed run equals the single-rank run to 1e-10."""
+    from paper_1005_3158_b200 import configs
+    c = configs.config1(n=10)
+    m = cf.Mesh(c.mesh.nodes, c.mesh.tets, c.mesh.region, np.zeros((0, 3)), np.zeros(0), [])
+    rng = np.random.default_rng(7)
+    T0 = 600.0 + 300.0 * rng.random(m.node_count())
+    s = cf.SimulationSetup(materials=c.setup.materials, solver=c.setup.solver, initial_T=T0)
+    tets, _ = cf.finalize_mesh(m)
+    p = m.nodes[tets]
+    V = np.einsum("ij,ij->i", p[:, 1] - p[:, 0], np.cross(p[:, 2] - p[:, 0], p[:, 3] - p[:, 0])) / 6
+    Cn = np.zeros(m.node_count())
+    np.add.at(Cn, tets.reshape(-1), np.repeat(2700.0 * 900.0 * V / 4, 4))
+    one = cf.solve(m, s, cf.SolveOptions(max_steps=1000, tile_elems=256))
+    dd = cf.solve(m, s, cf.SolveOptions(max_steps=1000, tile_elems=256, world_size=3, local_ranks=3))
+    assert one.steps == dd.steps == 1000
+    for r in (one, dd):
+        assert abs(np.sum(Cn * (r.T - T0))) <= 1e-10 * np.sum(Cn * T0)
+        assert np.ptp(r.T) < np.ptp(T0)  # diffusion only smooths
+    assert float(np.max(np.abs(dd.T - one.T) / np.abs(one.T))) <= 1e-10

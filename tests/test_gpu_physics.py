@@ -123,3 +123,23 @@ def test_conservation_1000_steps_and_decomposed_run():
         assert abs(np.sum(Cn * (r.T - T0))) <= 1e-10 * np.sum(Cn * T0)
         assert np.ptp(r.T) < np.ptp(T0)  # diffusion only smooths
     assert float(np.max(np.abs(dd.T - one.T) / np.abs(one.T))) <= 1e-10
+
+
+def test_permuted_mesh_gives_the_permuted_solution():
+    """solving on permute_mesh(m, p) equals the permuted solution of m to 1e-12
+    (node renumbering only relabels the unknowns) -- with the RCM permutation from the device pass and
+    with a random one, on a jittered two-material casting."""
+    from paper_1005_3158_b200 import configs
+    c = configs.casting(10, jitter=0.15, seed=4, dt_safety=0.14)
+    m, s = c.mesh, c.setup
+    base = cf.solve(m, s, cf.SolveOptions(max_steps=60, tile_elems=256))
+    rng = np.random.default_rng(11)
+    for p in (cf.rcm_permutation_device(m), rng.permutation(m.node_count()).astype(np.int32)):
+        mp = cf.permute_mesh(m, p)
+        T0p = np.empty_like(s.initial_T)
+        T0p[p] = s.initial_T
+        sp = cf.SimulationSetup(materials=s.materials, boundary_conditions=s.boundary_conditions,
+                                interface_coeffs=s.interface_coeffs, solver=s.solver, initial_T=T0p)
+        r = cf.solve(mp, sp, cf.SolveOptions(max_steps=60, tile_elems=256))
+        assert float(np.max(np.abs(r.T[p] - base.T) / np.abs(base.T))) <= 1e-12
+        assert r.end_time == base.end_time

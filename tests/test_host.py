@@ -141,6 +141,32 @@ def test_exchange_plan_symmetric():
             assert np.all(np.diff(x["shared"]) > 0)
 
 
+def test_exchange_payload_kat():
+    """exchange_and_merge's payload: two workers sharing 3 nodes exchange 6 values
+    each way (c and r per shared node), 7 shared nodes 14; the shared lists are ascending and the
+    same on both sides."""
+    setup = configs.config1(n=1).setup
+    s = cf.SimulationSetup(materials=setup.materials, solver=setup.solver)
+    none3, none1 = np.zeros((0, 3), np.int32), np.zeros(0, np.int32)
+    # two tets glued on one face: 3 shared nodes
+    nodes = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 1, 1]], float)
+    m = cf.Mesh(nodes, np.array([[0, 1, 2, 3], [1, 2, 3, 4]], np.int32), np.zeros(2, np.int32), none3, none1, [])
+    # a Kuhn cube split 4 + 2 tets shares 6 of its 8 nodes; one more tet of the small part on node 4: 7
+    c = cf.generate_fixture("cube", 1)
+    nodes7 = np.vstack([c.nodes, [[2.0, 0.0, 0.0], [2.0, 1.0, 0.0], [2.0, 0.0, 1.0]]])
+    tets7 = np.vstack([c.tets, [[4, 8, 9, 10]]]).astype(np.int32)
+    m7 = cf.Mesh(nodes7, tets7, np.zeros(7, np.int32), none3, none1, [])
+    for mesh, parts, n_shared in ((m, [0, 1], 3), (m7, [0, 1, 1, 0, 0, 0, 1], 7)):
+        parts = np.array(parts, np.int32)
+        a = cf.exchange_plan(mesh, s, 2, 0, parts)
+        b = cf.exchange_plan(mesh, s, 2, 1, parts)
+        assert len(a) == len(b) == 1 and a[0]["rank"] == 1 and b[0]["rank"] == 0
+        assert np.array_equal(a[0]["shared"], b[0]["shared"]) and np.all(np.diff(a[0]["shared"]) > 0)
+        assert len(a[0]["shared"]) == n_shared
+        for x in (a[0], b[0]):  # no interface facets here: the payload is the (c, r) pairs alone
+            assert 2 * len(x["shared"]) + len(x["ext_to"]) == 2 * n_shared
+
+
 # ---------------------------------------------------------------- error taxonomy
 def _tile_status(m, setup):
     try:

@@ -376,10 +376,22 @@ def main():
         comm = cf.PeerComm(world, rank, local_rank)
     elif world > 1:
         import torch
-        uid = cf.Comm.unique_id() if rank == 0 else bytes(128)
-        t = torch.tensor(list(uid), dtype=torch.uint8)
-        pg.broadcast(t, 0)
-        comm = cf.Comm(world, rank, local_rank, bytes(t.tolist()))
+        # every rank must be able to load NCCL before anyone enters ncclCommInitRank (which waits
+        # for all of them); if one cannot, all fall back to the host-staged transport, and say so
+        try:
+            uid = cf.Comm.unique_id()
+            ok = 1
+        except cf.CastfemError:
+            uid, ok = bytes(128), 0
+        flag = torch.tensor([ok], dtype=torch.int32)
+        pg.all_reduce(flag, op=pg.ReduceOp.MIN)
+        if int(flag[0]) == 1:
+            t = torch.tensor(list(uid), dtype=torch.uint8)
+            pg.broadcast(t, 0)
+            comm = cf.Comm(world, rank, local_rank, bytes(t.tolist()))
+        else:
+            args.transport = "host (NCCL not loadable on every rank)"
+            comm = cf.HostComm(world, rank, local_rank)
     opts = cf.SolveOptions(mode=args.mode, tile_elems=args.tile, elem_order=args.elem_order, geometry=args.geometry,
                            node_order=args.node_order, device=local_rank, world_size=world, rank=rank,
                            comm=comm, graph_steps=args.graph)

@@ -208,6 +208,12 @@ struct Rank {
     double* T[3] = {nullptr, nullptr, nullptr};
     double* Tslot[2] = {nullptr, nullptr};  // per-slot T copies (ping-pong)
     int32_t* sched = nullptr;               // dynamic tile-scheduling counter (persistent grids)
+    // decomposed plans, border tiles first in one launch (fused_border): completion counter + flag
+    // raised by the tile kernel, waited on by the exchange stream; border_seq = steps launched
+    bool fused_border = false;
+    unsigned long long* border_cnt = nullptr;
+    uint32_t* border_flag = nullptr;
+    uint32_t border_seq = 0;
     double* recv = nullptr;
     double* send = nullptr;
     double2* acc = nullptr;  // atomic mode: per node (c, r) accumulators
@@ -405,14 +411,16 @@ void launch_tile(cf_plan* p, Rank& r, double t_end, int phase = -1) {
         // the outlier class (few tiles) runs on a side stream, overlapping the main launch
         // (disjoint outputs: per-slot partials, tile-private nodes); joined before what follows
         bool two = false;
-        for (const Rank::TileLaunch& tl : r.launches) two = two || (tl.phase == ph && tl.heavy);
+        // (a fused border + interior launch, phase -1, goes with pass 0)
+        auto pass_of = [](const Rank::TileLaunch& tl) { return tl.phase < 0 ? 0 : tl.phase; };
+        for (const Rank::TileLaunch& tl : r.launches) two = two || (pass_of(tl) == ph && tl.heavy);
         if (two) {
             CF_CUDA_CHECK(cudaEventRecord(p->fork, p->stream));
             CF_CUDA_CHECK(cudaStreamWaitEvent(p->side, p->fork, 0));
         }
         for (size_t k = r.launches.size(); k-- > 0;) {  // outlier class first: its CTAs dispatch first
             const Rank::TileLaunch& tl = r.launches[k];
-            if (tl.phase != ph) continue;
+            if (pass_of(tl) != ph) continue;
             cudaStream_t st = tl.heavy ? p->side : p->stream;
             TileArgs a = tl.a;
             a.T = r.T[p->cur];
@@ -423,6 +431,11 @@ void launch_tile(cf_plan* p, Rank& r, double t_end, int phase = -1) {
             a.slot_gather = p->slot_gather ? 1 : 0;
             a.l2_next = p->l2_next ? 1 : 0;
             a.t_end = t_end;
+            if (a.n_border > 0) {
+                r.border_seq += 1;
+                a.border_seq = r.border_seq;
+                a.border_target = (unsigned long long)r.border_seq * (unsigned long long)a.n_border;
+            }
             const dim3 grid(tl.grid), block(nt);
 #define CF_LAUNCH(D, T, R, C, NT, G)                                                                  \
     if (det == D && td == T && dir == R && cl == C && nt == NT && gc == G) {                          \
@@ -800,8 +813,24 @@ void reduce_clamp(cf_plan* p, cudaStream_t st) {
 // multi-rank (SURVEY 8(e) overlap): border tiles -> [side stream: pack -> exchange] while the
 // interior tiles run on the main stream -> join -> update
 void enqueue_step(cf_plan* p, double t_end) {
+    bool fused = p->world > 1;
+    for (auto& r : p->ranks) fused = fused && r->fused_border;
     if (p->world == 1) {
         for (auto& r : p->ranks) launch_tile(p, *r, t_end);
+    } else if (fused) {
+        // one tile launch per rank, border tiles first; the exchange stream waits for the flag the
+        // kernel raises when its last border tile has flushed, then packs and exchanges while the
+        // same kernel goes on with the interior tiles
+        for (auto& r : p->ranks) launch_tile(p, *r, t_end);
+        for (auto& r : p->ranks) {  // each rank's pack as soon as its own border tiles are done
+            if (r->border_flag) stream_wait_geq(p->xside, r->border_flag, r->border_seq);
+            if (p->peer_comm()) launch_pack_peer(p, *r, p->xside);
+            else launch_pack(p, *r, p->xside);
+        }
+        exchange(p, p->xside);
+        CF_CUDA_CHECK(cudaEventRecord(p->xjoin, p->xside));
+        reduce_min_bound(p, p->stream);
+        CF_CUDA_CHECK(cudaStreamWaitEvent(p->stream, p->xjoin, 0));
     } else {
         for (auto& r : p->ranks) launch_tile(p, *r, t_end, 0);
         CF_CUDA_CHECK(cudaEventRecord(p->xfork, p->stream));
@@ -1046,8 +1075,19 @@ void finish_rank(cf_plan* p, Rank& r, const RankDev& d) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
         const bool heavy_any = !lists[1].empty() || !lists[3].empty();
+        // CF_BORDER_FUSED=1 (decomposed plans without an outlier class): ONE launch, border tiles
+        // first (each part in its own processing order); the kernel raises a flag when the border
+        // tiles are done and the exchange stream waits on its value. Default: two launches, border
+        // then interior, joined by an event -- in the in-process proxy (R ranks on one GPU) the
+        // stream's flag wait costs more than the saved border tail (cfg4 R = 8: 2.61 vs 2.44 ms per
+        // step, profiles/r02an_fused_border_ab.txt); to be re-measured with one GPU per rank.
+        bool fuse = false;
+        if (const char* e = std::getenv("CF_BORDER_FUSED"))
+            fuse = std::atoi(e) != 0 && p->world > 1 && !heavy_any && S == 1 && !lists[0].empty();
+        int32_t n_border = 0;
         for (int c = 0; c < 4; ++c) {
             if (lists[c].empty()) continue;
+            if (fuse && c == 2) continue;  // appended to class 0 below
             Rank::TileLaunch tl;
             tl.phase = c / 2;
             tl.heavy = c & 1;
@@ -1062,6 +1102,29 @@ void finish_rank(cf_plan* p, Rank& r, const RankDev& d) {
                         const TileMeta &mx_ = h.tile_meta[x], &my_ = h.tile_meta[y];
                         return 4 * mx_.nf + mx_.ns > 4 * my_.nf + my_.ns;
                     });
+            if (fuse && c == 0) {
+                bool hf = p->stages == 1;
+                if (const char* e = std::getenv("CF_TILE_ORDER")) hf = std::string(e) == "heavy";
+                if (hf)
+                    std::stable_sort(lists[2].begin(), lists[2].end(), [&](int32_t x, int32_t y) {
+                        const TileMeta &mx_ = h.tile_meta[x], &my_ = h.tile_meta[y];
+                        return 4 * mx_.nf + mx_.ns > 4 * my_.nf + my_.ns;
+                    });
+                n_border = (int32_t)lists[0].size();
+                lists[0].insert(lists[0].end(), lists[2].begin(), lists[2].end());
+                mx[0].blob = std::max(mx[0].blob, mx[2].blob);
+                mx[0].slots = std::max(mx[0].slots, mx[2].slots);
+                mx[0].scratch = std::max(mx[0].scratch, mx[2].scratch);
+                tl.phase = -1;
+                r.fused_border = true;
+                r.border_cnt = M.alloc<unsigned long long>(1);
+                r.border_flag = M.alloc<uint32_t>(1);
+                CF_CUDA_CHECK(cudaMemsetAsync(r.border_cnt, 0, sizeof(unsigned long long), s));
+                CF_CUDA_CHECK(cudaMemsetAsync(r.border_flag, 0, sizeof(uint32_t), s));
+                tl.a.n_border = n_border;
+                tl.a.border_cnt = r.border_cnt;
+                tl.a.border_flag = r.border_flag;
+            }
             std::vector<TileDesc> desc(lists[c].size());
             for (size_t i = 0; i < lists[c].size(); ++i) {
                 const int32_t t = lists[c][i];
@@ -1260,7 +1323,9 @@ void run_steps(cf_plan* p, int64_t n, double t_end) {
     CF_CUDA_CHECK(cudaEventRecord(p->ev0, p->stream));
     int64_t done = 0;
     // host-staged steps synchronise, peer-memory steps wait on per-step flag values: never captured
-    if (p->graph_steps > 0 && !p->host_comm() && !p->peer_comm()) {
+    bool flag_waits = false;  // fused border launches: the exchange stream waits on per-step flag values
+    for (auto& r : p->ranks) flag_waits = flag_waits || r->fused_border;
+    if (p->graph_steps > 0 && !p->host_comm() && !p->peer_comm() && !flag_waits) {
         const int state_key = p->cur * 2 + p->step_parity;
         if (p->graph && (p->graph_t_end != t_end || p->graph_cur != state_key)) {
             cudaGraphExecDestroy(p->graph);

@@ -99,6 +99,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void atomic_min_pos(unsigned long long* addr, double v) {
     atomicMin(addr, (unsigned long long)__double_as_longlong(v));
 }
@@ -174,6 +177,14 @@ struct TileArgs {
     int32_t* sched;            // dynamic tile scheduling counter (persistent single-stage grids), or null
     int32_t slot_gather;       // 1: slot temperatures gathered from T by node id (no slot copies)
     int32_t l2_next;           // persistent grids: stage the next tile's blob into L2 at phase 3's start
+    // decomposed plans, one launch for every tile with the border tiles (those holding a
+    // rank-shared node) first: when the last of them has flushed its partials the kernel raises
+    // border_flag = border_seq, on which the exchange stream waits before it packs
+    int32_t n_border;               // leading tiles of this launch that are border tiles (0: none)
+    uint32_t border_seq;            // this step's flag value
+    unsigned long long border_target;  // border_cnt after this step's last border tile (cumulative)
+    unsigned long long* border_cnt;
+    uint32_t* border_flag;
     int32_t n_local;           // bounds (CF_BOUNDS builds): local nodes (+ ghosts below n_T)
     int32_t n_T;
     int64_t n_slots;
@@ -354,6 +365,17 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
     int clamped = 0;
     double local_min = __longlong_as_double(0x7ff0000000000000ll);
 
+    // a border tile is complete once every thread's flush has been fenced and the CTA has met at a
+    // barrier; thread 0 then counts it and the CTA finishing the launch's last one raises the flag
+    auto border_done = [&]() {
+        __threadfence();
+        const unsigned long long old = atomicAdd(a.border_cnt, 1ull);
+        if (old + 1 == a.border_target) {
+            __threadfence();
+            st_release_sys(a.border_flag, a.border_seq);
+        }
+    };
+    bool pending_border = false;  // the previous tile of this CTA was a border tile (CTA-uniform)
     int k = 0;
     for (int t = blockIdx.x; t < a.n_tiles; ++k) {
         const int stage = a.stages == 2 ? (k & 1) : 0;
@@ -412,6 +434,8 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
             sTH[s] = make_double2(T, (CF_PRB(a) & 15) == 5 ? T : dev_enthalpy<TDEP>(P, sMat[sinfo[s] & 0x3f], T));
         }
         __syncthreads();
+        if (pending_border && tid == 0) border_done();  // every thread's fenced flush precedes the barrier
+        pending_border = false;
 
         // phase 2a: elements (element_accumulate fem.hpp:57-70). Stored layout: the element's
         // four (lump, rc_q) pairs go over its own consumed geometry pairs (columns 0..3);
@@ -666,8 +690,16 @@ __global__ void __launch_bounds__(kTileThreads, GC ? CF_GC_MINB : CF_GS_MINB) ti
 #pragma unroll
         for (int k = 0; k < KD; ++k)
             if (kv[k]) flush(ks[k], kc[k], kr[k], kinfo[k], knode[k], kT[k]);
+        if (t < a.n_border) {  // partials of a border tile: visible device-wide before it is counted
+            __threadfence();
+            pending_border = true;
+        }
         if (t_nxt >= a.n_tiles) break;  // last tile of this CTA: no trailing barrier
         t = t_nxt;
+    }
+    if (pending_border) {
+        __syncthreads();
+        if (tid == 0) border_done();
     }
     if (TDEP) {
         for (int o = 16; o > 0; o >>= 1) local_min = fmin(local_min, __shfl_xor_sync(0xffffffffu, local_min, o));
@@ -960,10 +992,6 @@ struct PackArgs {
     UpdArgs u;               // merge inputs
     PeerPack pp;             // peer-memory transport only
 };
-
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 // PEER: exchange_and_merge's send half fused with the pack -- each value is stored
 // straight into the neighbour's receive buffer over NVLink, and the last CTA to finish raises this

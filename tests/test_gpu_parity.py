@@ -120,6 +120,22 @@ def test_multirank_inprocess_vs_oracle(ranks, mode):
     assert rel(gpu.T, single.T) <= RTOL
 
 
+def test_multirank_fused_border_launch(monkeypatch):
+    """CF_BORDER_FUSED=1: one tile launch per rank, border tiles first; the kernel raises a flag
+    when its last border tile has flushed and the exchange stream waits on the flag's value
+    before packing. Same tiles, same reduction order: bitwise equal to the default two-launch
+    schedule and to the oracle with the same parts."""
+    case = configs.casting(16, jitter=0.15, seed=2, dt_safety=0.14)
+    opts = cf.SolveOptions(max_steps=30, mode="deterministic", tile_elems=192, world_size=3, local_ranks=3)
+    base = cf.solve(case.mesh, case.setup, opts)
+    monkeypatch.setenv("CF_BORDER_FUSED", "1")
+    fused = cf.solve(case.mesh, case.setup, opts)
+    assert np.array_equal(base.T, fused.T)
+    tiles, _ = cf.tile_map(case.mesh, case.setup, opts)
+    ref = orc.solve(case.mesh, case.setup, 30, blocks=tiles, parts=cf.partition_rcb(case.mesh, 3))
+    assert np.array_equal(fused.T, ref.T)
+
+
 def test_multirank_interface_split_across_ranks():
     """A partition cutting through the cast/mould interface: sister elements on
     other ranks supply the lagged ambient through ghost nodes."""

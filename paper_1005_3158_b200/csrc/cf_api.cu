@@ -528,6 +528,7 @@ void launch_pack(cf_plan* p, Rank& r, cudaStream_t st) {
 // ------------------------------------------------------------------ peer-memory transport
 struct DriverApi {
     CUresult (*StreamWaitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+    CUresult (*StreamBatchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int) = nullptr;
 };
 DriverApi& driver() {
     static DriverApi api;
@@ -538,6 +539,10 @@ DriverApi& driver() {
         if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             api.StreamWaitValue32 = (decltype(api.StreamWaitValue32))fn;
+        fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamBatchMemOp", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            api.StreamBatchMemOp = (decltype(api.StreamBatchMemOp))fn;
         cudaGetLastError();
     });
     if (!api.StreamWaitValue32) raise(CF_CUDA, "cuStreamWaitValue32 not available from this driver");
@@ -547,7 +552,7 @@ DriverApi& driver() {
 // GEQ is a cyclic compare ((int32)(*flag - value) >= 0), so the sequence numbers may wrap. The
 // payload stores are ordered before the flag by the sender's system-scope fence + release; where
 // the device can also flush third-party remote writes behind a wait, ask for that too.
-void stream_wait_geq(cudaStream_t st, const uint32_t* flag, uint32_t value) {
+unsigned wait_geq_flags() {
     static const unsigned flush = [] {
         int dev = 0, can = 0;
         if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -556,8 +561,10 @@ void stream_wait_geq(cudaStream_t st, const uint32_t* flag, uint32_t value) {
         cudaGetLastError();
         return can ? (unsigned)CU_STREAM_WAIT_VALUE_FLUSH : 0u;
     }();
-    const CUresult r =
-        driver().StreamWaitValue32((CUstream)st, (CUdeviceptr)flag, value, CU_STREAM_WAIT_VALUE_GEQ | flush);
+    return (unsigned)CU_STREAM_WAIT_VALUE_GEQ | flush;
+}
+void stream_wait_geq(cudaStream_t st, const uint32_t* flag, uint32_t value) {
+    const CUresult r = driver().StreamWaitValue32((CUstream)st, (CUdeviceptr)flag, value, wait_geq_flags());
     if (r != CUDA_SUCCESS) raise(CF_CUDA, "cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
 }
 
@@ -577,10 +584,33 @@ void launch_pack_peer(cf_plan* p, Rank& r, cudaStream_t st) {
     CF_CUDA_CHECK(cudaGetLastError());
 }
 
+// several flags >= value as ONE stream operation (cuStreamBatchMemOp) where the driver offers it:
+// one front-end round instead of one per flag
+void stream_wait_geq_all(cudaStream_t st, const std::vector<const uint32_t*>& flags, uint32_t value) {
+    if (flags.empty()) return;
+    DriverApi& d = driver();
+    if (!d.StreamBatchMemOp || flags.size() == 1 || flags.size() > 256) {
+        for (const uint32_t* f : flags) stream_wait_geq(st, f, value);
+        return;
+    }
+    std::vector<CUstreamBatchMemOpParams> ops(flags.size());
+    for (size_t k = 0; k < flags.size(); ++k) {
+        std::memset(&ops[k], 0, sizeof(ops[k]));
+        ops[k].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+        ops[k].waitValue.address = (CUdeviceptr)flags[k];
+        ops[k].waitValue.value = value;
+        ops[k].waitValue.flags = wait_geq_flags();
+    }
+    const CUresult r = d.StreamBatchMemOp((CUstream)st, (unsigned)ops.size(), ops.data(), 0);
+    if (r != CUDA_SUCCESS) raise(CF_CUDA, "cuStreamBatchMemOp failed (" + std::to_string((int)r) + ")");
+}
+
 // receive half: the stream waits until every neighbour's payload of this exchange has landed
 void peer_wait_payload(cf_plan* p, Rank& r, cudaStream_t st) {
     const uint32_t* xflag = (const uint32_t*)(p->peer.win + kPeerXflagOff);
-    for (const auto& nb : r.H.nbrs) stream_wait_geq(st, xflag + nb.rank, p->peer.seq);
+    std::vector<const uint32_t*> flags;
+    for (const auto& nb : r.H.nbrs) flags.push_back(xflag + nb.rank);
+    stream_wait_geq_all(st, flags, p->peer.seq);
 }
 
 // all-reduce of n <= 2 scalars at `v` (device) over every rank of the job through the peer windows
@@ -592,8 +622,10 @@ void peer_allreduce(cf_plan* p, V* v, int n, int op0, int op1, cudaStream_t st) 
     peer_put_kernel<V><<<1, kPeerMaxWorld, 0, st>>>(pr, v, n);
     CF_CUDA_CHECK(cudaGetLastError());
     const uint32_t* rflag = (const uint32_t*)(x.win + kPeerRflagOff);
+    std::vector<const uint32_t*> flags;
     for (int q = 0; q < p->world; ++q)
-        if (q != p->first_rank) stream_wait_geq(st, rflag + q, x.rseq);
+        if (q != p->first_rank) flags.push_back(rflag + q);
+    stream_wait_geq_all(st, flags, x.rseq);
     peer_get_kernel<V><<<1, 32, 0, st>>>(pr, v, n, op0, op1);
     CF_CUDA_CHECK(cudaGetLastError());
 }

@@ -160,3 +160,40 @@ def test_atomic_steps_past_t_end_leave_no_stale_sums():
             out[mode] = (T1, T2)
     for a, b in zip(out["atomic"], out["deterministic"]):
         assert float(np.max(np.abs(a - b) / np.abs(b))) <= 1e-9
+
+
+@pytest.mark.parametrize("tile_elems,ranks", [(32, 1), (512, 1), (48, 3)])
+def test_high_valence_hub_mesh(tile_elems, ranks):
+    """A genuinely unstructured topology: 400 tets fanned around one hub node (the convex hull of
+    random points on a sphere, each surface triangle joined to the centre). The hub's reduction
+    list holds every element of its tile, and with small tiles the hub is shared by more tiles
+    than an update record holds (the merge-list path, > 8 partials) and by every rank."""
+    from scipy.spatial import ConvexHull
+    rng = np.random.default_rng(5)
+    pts = rng.normal(size=(202, 3))
+    pts /= np.linalg.norm(pts, axis=1)[:, None]
+    pts *= 0.8 + 0.4 * rng.random((202, 1))  # star-shaped, not a sphere: varied element sizes
+    hull = ConvexHull(pts / np.linalg.norm(pts, axis=1)[:, None])
+    tri = hull.simplices.astype(np.int32) + 1
+    nodes = np.vstack([[0.0, 0.0, 0.0], pts])
+    tets = np.hstack([np.zeros((len(tri), 1), np.int32), tri])
+    m = cf.Mesh(nodes, tets, np.zeros(len(tets), np.int32), tri, np.zeros(len(tri), np.int32), ["outer"])
+    mat = cf.MaterialTable.make(rho=2700.0, c=900.0, k=200.0, latent_heat=3.9e5, solidus=821.0, liquidus=913.0,
+                                T0=930.0)
+    T0 = 930.0 + 20.0 * rng.random(m.node_count())
+    s = cf.SimulationSetup(materials=[mat], boundary_conditions={"outer": cf.BoundaryCondition("flux", h=500.0,
+                                                                                              t_inf=300.0)},
+                           solver=cf.SolverConfig(dt_safety=0.05), initial_T=T0)
+    assert len(tets) >= 390
+    opts = cf.SolveOptions(max_steps=200, tile_elems=tile_elems, world_size=ranks, local_ranks=ranks)
+    gpu = cf.solve(m, s, opts)
+    tiles, nt = cf.tile_map(m, s, opts)
+    if tile_elems == 32:
+        assert nt > 8  # the hub's partial count exceeds an update record
+    parts = cf.partition_rcb(m, ranks) if ranks > 1 else None
+    ref = orc.solve(m, s, 200, blocks=tiles, parts=parts)
+    assert np.array_equal(gpu.T, ref.T), float(np.abs(gpu.T - ref.T).max())
+    at = cf.solve(m, s, cf.SolveOptions(max_steps=200, tile_elems=tile_elems, mode="atomic", world_size=ranks,
+                                        local_ranks=ranks))
+    assert float(np.max(np.abs(at.T - ref.T) / np.abs(ref.T))) <= 1e-9
+    assert gpu.T.min() < T0.min()  # it cools

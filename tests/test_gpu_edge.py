@@ -197,3 +197,38 @@ def test_high_valence_hub_mesh(tile_elems, ranks):
                                         local_ranks=ranks))
     assert float(np.max(np.abs(at.T - ref.T) / np.abs(ref.T))) <= 1e-9
     assert gpu.T.min() < T0.min()  # it cools
+
+
+@pytest.mark.parametrize("tile_elems,ranks,geometry", [(128, 1, "stored"), (384, 1, "coords"), (160, 2, "stored")])
+def test_delaunay_mesh(tile_elems, ranks, geometry):
+    """An unstructured Delaunay tetrahedralisation of 600 random points (3704 tets of every shape,
+    slivers included, node valences 5-40; hull faces convective): nothing of the Kuhn fixtures'
+    regularity. Deterministic mode bitwise, atomic mode 1e-9, against the oracle on the same tiles
+    and parts; dt_safety is small because Eq. 13's bound is not a stability bound on slivers."""
+    from scipy.spatial import Delaunay
+    rng = np.random.default_rng(12)
+    pts = rng.random((600, 3))
+    d = Delaunay(pts)
+    tets, hull = d.simplices.astype(np.int32), d.convex_hull.astype(np.int32)
+    m = cf.Mesh(pts, tets, np.zeros(len(tets), np.int32), hull, np.zeros(len(hull), np.int32), ["outer"])
+    mat = cf.MaterialTable.make(rho=2700.0, c=900.0, k=200.0, latent_heat=3.9e5, solidus=821.0, liquidus=913.0,
+                                T0=930.0)
+    T0 = 900.0 + 60.0 * rng.random(m.node_count())  # straddles the liquidus: latent heat active
+    s = cf.SimulationSetup(materials=[mat], boundary_conditions={"outer": cf.BoundaryCondition("flux", h=500.0,
+                                                                                              t_inf=300.0)},
+                           solver=cf.SolverConfig(dt_safety=0.01), initial_T=T0)
+    steps = 150
+    opts = cf.SolveOptions(max_steps=steps, tile_elems=tile_elems, geometry=geometry, world_size=ranks,
+                           local_ranks=ranks)
+    gpu = cf.solve(m, s, opts)
+    tiles, _ = cf.tile_map(m, s, opts)
+    parts = cf.partition_rcb(m, ranks) if ranks > 1 else None
+    ref = orc.solve(m, s, steps, blocks=tiles, parts=parts)
+    assert np.isfinite(ref.T).all() and ref.T.max() < 960.0
+    assert np.array_equal(gpu.T, ref.T), float(np.abs(gpu.T - ref.T).max())
+    at = cf.solve(m, s, cf.SolveOptions(max_steps=steps, tile_elems=tile_elems, geometry=geometry, mode="atomic",
+                                        world_size=ranks, local_ranks=ranks))
+    assert float(np.max(np.abs(at.T - ref.T) / np.abs(ref.T))) <= 1e-9
+    if orc.ref_available() and ranks == 1:  # and the reference itself, one block
+        r, _ = orc.ref_solve(m, s, steps)
+        assert float(np.max(np.abs(gpu.T - r.T) / np.abs(r.T))) <= 1e-9

@@ -18,7 +18,24 @@ pytestmark = pytest.mark.gpu
 
 SKIP = {"tets_ord"}  # not kept by the device pipeline (geometry is computed straight from the mesh)
 
+def _delaunay_case():
+    """Unstructured topology (irregular valence, slivers): Delaunay of 500 random points."""
+    from types import SimpleNamespace
+
+    from scipy.spatial import Delaunay
+    rng = np.random.default_rng(21)
+    pts = rng.random((500, 3))
+    d = Delaunay(pts)
+    tets, hull = d.simplices.astype(np.int32), d.convex_hull.astype(np.int32)
+    m = cf.Mesh(pts, tets, np.zeros(len(tets), np.int32), hull, np.zeros(len(hull), np.int32), ["outer"])
+    s = cf.SimulationSetup(materials=[cf.MaterialTable.make(rho=2700.0, c=900.0, k=200.0, T0=930.0)],
+                           boundary_conditions={"outer": cf.BoundaryCondition("flux", h=500.0, t_inf=300.0)},
+                           solver=cf.SolverConfig(dt_safety=0.01))
+    return SimpleNamespace(mesh=m, setup=s)
+
+
 CASES = {
+    "delaunay500": _delaunay_case,
     "cast12": lambda: configs.casting(12, dt_safety=0.14),
     "cast16j": lambda: configs.casting(16, jitter=0.2, seed=3, perm_seed=5, dt_safety=0.12),
     "cast24": lambda: configs.casting(24, dt_safety=0.14),

@@ -45,7 +45,17 @@ def _fan(k):
                    np.zeros(0), []), int(perm[iso])
 
 
+def _delaunay(n, seed):
+    """Unstructured node graph (degrees 4-40, many (degree, id) ties to break)."""
+    from scipy.spatial import Delaunay
+    pts = np.random.default_rng(seed).random((n, 3))
+    tets = Delaunay(pts).simplices.astype(np.int32)
+    return cf.Mesh(pts, tets, np.zeros(len(tets), np.int32), np.zeros((0, 3)), np.zeros(0), [])
+
+
 MESHES = {
+    "delaunay800": lambda: _delaunay(800, 31),
+    "delaunay3000": lambda: _delaunay(3000, 32),
     "cube5": lambda: cf.generate_fixture("cube", 5),
     "casting9": lambda: cf.generate_fixture("casting", 9),
     "jitter8_perm": lambda: cf.generate_fixture("casting", 8, jitter=0.2, seed=5, perm_seed=17),

@@ -13,7 +13,17 @@ from paper_1005_3158_b200 import configs
 from paper_1005_3158_b200.castfem import _Keep, mesh_desc
 
 needs_ref = pytest.mark.skipif(not orc.ref_available(), reason="oracle/_ref not built")
+def _delaunay(n=600, seed=41):
+    """Unstructured topology: Delaunay of random points, hull faces as boundary facets."""
+    from scipy.spatial import Delaunay
+    pts = np.random.default_rng(seed).random((n, 3))
+    d = Delaunay(pts)
+    tets, hull = d.simplices.astype(np.int32), d.convex_hull.astype(np.int32)
+    return cf.Mesh(pts, tets, np.zeros(len(tets), np.int32), hull, np.zeros(len(hull), np.int32), ["outer"])
+
+
 MESHES = {
+    "delaunay600": _delaunay,
     "cube5": lambda: cf.generate_fixture("cube", 5),
     "casting9": lambda: cf.generate_fixture("casting", 9),
     "jitter8_perm": lambda: cf.generate_fixture("casting", 8, jitter=0.2, seed=5, perm_seed=17),
@@ -227,6 +237,7 @@ PART_MESHES = {
     "casting8": lambda: cf.generate_fixture("casting", 8),
     "jitter7_perm": lambda: cf.generate_fixture("casting", 7, jitter=0.2, seed=5, perm_seed=17),
     "cube5_perm": lambda: cf.generate_fixture("cube", 5, perm_seed=3),
+    "delaunay400": lambda: _delaunay(400, 43),
 }
 
 

@@ -25,7 +25,7 @@ def _draw(seed):
         jitter=float(rng.choice([0.0, 0.1, 0.2])),
         perm=int(rng.integers(0, 4)) * int(rng.integers(1, 100)),  # 0 = generator numbering
         radius=float(rng.choice([0.25, 0.35, 0.45])),
-        tile=int(rng.choice([96, 128, 192, 256, 384, 512, 768])),
+        tile=int(rng.choice([32, 96, 128, 192, 256, 384, 512, 768, 1024])),
         geometry=str(rng.choice(["stored", "coords"])),
         elem_order=str(rng.choice(["morton", "min_node", "given"])),
         node_order=str(rng.choice(["tile", "rcm", "given"])),

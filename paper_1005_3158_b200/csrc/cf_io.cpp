@@ -3,18 +3,25 @@
 //   solver config       parse_config                 material.hpp:186-345
 //   partmap             load_partmap / write_partmap partition.hpp:424-449
 //   binary mesh         this repo's fast path for large meshes (same validation as parse_mesh)
-// Same tokenizer ('#' comments, whitespace-separated tokens, blank lines skipped,
+// Same lexical rules ('#' comments, whitespace-separated words, blank lines skipped,
 // 1-based line numbers), the same number syntax (std::from_chars), the same
-// section semantics and defaults, and the same error classes and messages:
+// section semantics and defaults, and the same error classes and messages (the first
+// defect in file order, as a sequential reader would meet it):
 // CF_PARSE "line N: ..." for syntax, CF_VALIDATION "mesh validation failed: ..."
 // for a mesh finalize_mesh rejects, CF_CONFIG for table / material checks.
+// Structure (this repo's own): the buffer is indexed into logical lines once; the mesh parser
+// plans its sections from the header lines, converts every section's records in parallel (OpenMP)
+// and numbers the tags in a last ordered pass (1.6 M tets of text: 0.16 s, the reference's stream
+// reader 3.7 s); the config grammar is a table of sections and keys, each key with its assignment.
 #include <algorithm>
 #include <cctype>
 #include <charconv>
 #include <cstdio>
 #include <cstring>
+#include <iterator>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <string_view>
 #include <vector>
@@ -24,65 +31,92 @@
 namespace cfb {
 namespace {
 
-struct Lines {  // LineReader mesh.hpp:211-235
-    std::string_view text;
-    size_t pos = 0;
-    long line_no = 0;
-    bool next(std::vector<std::string_view>& tok) {
-        while (pos < text.size()) {
-            size_t end = text.find('\n', pos);
-            if (end == std::string_view::npos) end = text.size();
-            std::string_view v = text.substr(pos, end - pos);
-            pos = end + 1;
-            ++line_no;
-            if (const size_t h = v.find('#'); h != std::string_view::npos) v = v.substr(0, h);
-            tok.clear();
-            size_t i = 0;
-            while (i < v.size()) {
-                while (i < v.size() && std::isspace((unsigned char)v[i])) ++i;
-                size_t j = i;
-                while (j < v.size() && !std::isspace((unsigned char)v[j])) ++j;
-                if (j > i) tok.push_back(v.substr(i, j - i));
-                i = j;
-            }
-            if (!tok.empty()) return true;
+// ---- text front end ------------------------------------------------------------------------
+// The buffer is indexed once into its logical lines (comment cut at '#', blank lines dropped,
+// physical line numbers kept). The parsers work on that index: the mesh parser plans its sections
+// from the header lines alone (a section's records are the next N logical lines) and then converts
+// the record lines of every section in parallel; the first defect in file order is the one
+// reported, with the line number the reference's sequential reader would report.
+struct LogicalLine {
+    const char* b;
+    const char* e;  // [b, e): comment removed; may still carry blanks at either end
+    long no;        // 1-based physical line number
+};
+
+inline bool blank(char c) { return std::isspace((unsigned char)c) != 0; }
+
+struct LineIndex {
+    std::vector<LogicalLine> lines;
+    long physical = 0;  // physical lines in the buffer: what an end-of-input error reports
+    explicit LineIndex(std::string_view text) {
+        const char* p = text.data();
+        const char* const end = p + text.size();
+        while (p < end) {
+            const char* nl = (const char*)std::memchr(p, '\n', (size_t)(end - p));
+            const char* stop = nl ? nl : end;
+            ++physical;
+            if (const char* hash = (const char*)std::memchr(p, '#', (size_t)(stop - p))) stop = hash;
+            const char* q = p;
+            while (q < stop && blank(*q)) ++q;
+            if (q < stop) lines.push_back(LogicalLine{q, stop, physical});
+            p = nl ? nl + 1 : end;
         }
-        return false;
     }
 };
+
+// whitespace-separated words of a logical line: stores up to cap of them, returns how many there are
+int words(const LogicalLine& L, std::string_view* out, int cap) {
+    int n = 0;
+    for (const char* p = L.b; p < L.e;) {
+        while (p < L.e && blank(*p)) ++p;
+        const char* q = p;
+        while (q < L.e && !blank(*q)) ++q;
+        if (q > p) {
+            if (n < cap) out[n] = std::string_view(p, (size_t)(q - p));
+            ++n;
+        }
+        p = q;
+    }
+    return n;
+}
 
 [[noreturn]] void parse_fail(const std::string& what, long line) {
     raise(CF_PARSE, "line " + std::to_string(line) + ": " + what);
 }
 
-double to_double(std::string_view t, long line) {
-    double v = 0;
+template <class T>
+T number(std::string_view t, long line, const char* kind) {
+    T v{};
     const auto r = std::from_chars(t.data(), t.data() + t.size(), v);
     if (r.ec != std::errc{} || r.ptr != t.data() + t.size())
-        parse_fail("expected a number, got '" + std::string(t) + "'", line);
+        parse_fail(std::string("expected ") + kind + ", got '" + std::string(t) + "'", line);
     return v;
 }
-
-long to_long(std::string_view t, long line) {
-    long v = 0;
-    const auto r = std::from_chars(t.data(), t.data() + t.size(), v);
-    if (r.ec != std::errc{} || r.ptr != t.data() + t.size())
-        parse_fail("expected an integer, got '" + std::string(t) + "'", line);
-    return v;
-}
-
-// a count from a section header: the reference reserves it (negative -> length error)
-size_t to_count(std::string_view t, long line) {
-    const long n = to_long(t, line);
-    if (n < 0) raise(CF_INVALID_ARG, "line " + std::to_string(line) + ": negative count");
-    return (size_t)n;
-}
+double to_double(std::string_view t, long line) { return number<double>(t, line, "a number"); }
+long to_long(std::string_view t, long line) { return number<long>(t, line, "an integer"); }
 
 void append_g17(std::string& s, double v) {
     char b[40];
     const int n = std::snprintf(b, sizeof b, "%.17g", v);
     s.append(b, (size_t)n);
 }
+
+// The earliest defect in file order wins, whichever pass or thread met it.
+struct FirstDefect {
+    size_t at = SIZE_MAX;  // position in the line index (lines.size() = end of input)
+    Error err{CF_OK, ""};
+    std::mutex mu;
+    void offer(size_t where, const Error& e) {
+        std::lock_guard<std::mutex> g(mu);
+        if (where < at) {
+            at = where;
+            err = e;
+        }
+    }
+    void rethrow() const {
+        if (at != SIZE_MAX) throw err;
+    }
+};
 
 }  // namespace
 
@@ -93,9 +127,9 @@ struct TextMesh {
     std::vector<std::string> tags;
     std::vector<const char*> tag_ptrs;
     cf_mesh_desc desc{};
-    int32_t add_tag(std::string_view name) {  // Mesh::add_tag mesh.hpp:62-67
-        for (size_t i = 0; i < tags.size(); ++i)
-            if (tags[i] == name) return (int32_t)i;
+    int32_t tag_id(std::string_view name) {  // first use numbers a tag (Mesh::add_tag mesh.hpp:62-67)
+        const auto it = std::find(tags.begin(), tags.end(), name);
+        if (it != tags.end()) return (int32_t)(it - tags.begin());
         tags.emplace_back(name);
         return (int32_t)tags.size() - 1;
     }
@@ -109,53 +143,119 @@ struct TextMesh {
     }
 };
 
+namespace {
+// the femesh record sections (mesh.hpp:256-262): keyword, words per record, and the reference's messages
+struct RecordKind {
+    const char* keyword;
+    int fields;
+    const char* usage;
+    const char* cut_short;
+    const char* shape;
+};
+constexpr RecordKind kRecordKinds[] = {
+    {"nodes", 3, "usage: nodes N", "unexpected end of node list", "node line needs 'x y z'"},
+    {"tets", 5, "usage: tets M", "unexpected end of element list", "element line needs 'n0 n1 n2 n3 region'"},
+    {"facets", 4, "usage: facets B", "unexpected end of facet list", "facet line needs 'n0 n1 n2 tag'"},
+};
+enum { kNodes = 0, kTets = 1, kFacets = 2, kContact = 3 };
+
+struct Section {   // one header line and the logical lines it owns
+    int kind;      // kNodes .. kContact
+    size_t first;  // contact: the header line itself; records: the first record line
+    size_t count;  // records present (a list cut short by the end of input keeps what is there)
+    size_t base;   // index of its first record in the mesh arrays
+};
+}  // namespace
+
 std::unique_ptr<TextMesh> parse_mesh_text(std::string_view text) {
-    Lines rd{text};
-    std::vector<std::string_view> tok;
-    if (!rd.next(tok) || tok.size() != 2 || tok[0] != "femesh" || tok[1] != "1")
-        parse_fail("expected header 'femesh 1'", rd.line_no);
+    const LineIndex idx(text);
+    const auto& L = idx.lines;
+    std::string_view w[6];
+    if (L.empty() || words(L[0], w, 6) != 2 || w[0] != "femesh" || w[1] != "1")
+        parse_fail("expected header 'femesh 1'", L.empty() ? idx.physical : L[0].no);
+
+    // pass 1: the section plan, from the header lines alone
+    FirstDefect defect;
+    std::vector<Section> plan;
+    size_t totals[3] = {0, 0, 0};
+    for (size_t i = 1; i < L.size();) {
+        try {
+            const int nw = words(L[i], w, 6);
+            if (w[0] == "contact") {
+                if (nw != 3) parse_fail("usage: contact tagA tagB", L[i].no);
+                plan.push_back(Section{kContact, i, 0, 0});
+                ++i;
+                continue;
+            }
+            int kind = -1;
+            for (int k = 0; k < 3; ++k)
+                if (w[0] == kRecordKinds[k].keyword) kind = k;
+            if (kind < 0) parse_fail("unknown section '" + std::string(w[0]) + "'", L[i].no);
+            if (nw != 2) parse_fail(kRecordKinds[kind].usage, L[i].no);
+            const long n = to_long(w[1], L[i].no);
+            if (n < 0) raise(CF_INVALID_ARG, "line " + std::to_string(L[i].no) + ": negative count");
+            const size_t have = std::min<size_t>((size_t)n, L.size() - (i + 1));
+            plan.push_back(Section{kind, i + 1, have, totals[kind]});
+            totals[kind] += have;
+            if (have < (size_t)n) {  // reported only if every record that is there converts
+                defect.offer(L.size(), Error(CF_PARSE, "line " + std::to_string(idx.physical) + ": " +
+                                                           kRecordKinds[kind].cut_short));
+                break;
+            }
+            i += 1 + have;
+        } catch (const Error& e) {
+            defect.offer(i, e);
+            break;
+        }
+    }
+
+    // pass 2: the records of every planned section, converted in parallel
     auto m = std::make_unique<TextMesh>();
-    while (rd.next(tok)) {
-        if (tok[0] == "nodes") {
-            if (tok.size() != 2) parse_fail("usage: nodes N", rd.line_no);
-            const size_t n = to_count(tok[1], rd.line_no);
-            m->coords.reserve(m->coords.size() + 3 * n);
-            for (size_t i = 0; i < n; ++i) {
-                if (!rd.next(tok)) parse_fail("unexpected end of node list", rd.line_no);
-                if (tok.size() != 3) parse_fail("node line needs 'x y z'", rd.line_no);
-                for (int k = 0; k < 3; ++k) m->coords.push_back(to_double(tok[k], rd.line_no));
+    m->coords.resize(3 * totals[kNodes]);
+    m->tets.resize(4 * totals[kTets]);
+    m->region.resize(totals[kTets]);
+    m->facets.resize(3 * totals[kFacets]);
+    std::vector<std::string_view> facet_word(totals[kFacets]);
+    for (const Section& sec : plan) {
+        if (sec.kind == kContact) continue;
+        const RecordKind& rk = kRecordKinds[sec.kind];
+        const int64_t n = (int64_t)sec.count;
+#pragma omp parallel for schedule(static) if (n > 4096)
+        for (int64_t r = 0; r < n; ++r) {
+            const LogicalLine& rec = L[sec.first + (size_t)r];
+            const size_t o = sec.base + (size_t)r;
+            try {
+                std::string_view f[6];
+                if (words(rec, f, 6) != rk.fields) parse_fail(rk.shape, rec.no);
+                if (sec.kind == kNodes) {
+                    for (int k = 0; k < 3; ++k) m->coords[3 * o + k] = to_double(f[k], rec.no);
+                } else if (sec.kind == kTets) {
+                    for (int k = 0; k < 4; ++k) m->tets[4 * o + k] = (int32_t)to_long(f[k], rec.no);
+                    m->region[o] = (int32_t)to_long(f[4], rec.no);
+                } else {
+                    for (int k = 0; k < 3; ++k) m->facets[3 * o + k] = (int32_t)to_long(f[k], rec.no);
+                    facet_word[o] = f[3];
+                }
+            } catch (const Error& e) {
+                defect.offer(sec.first + (size_t)r, e);
             }
-        } else if (tok[0] == "tets") {
-            if (tok.size() != 2) parse_fail("usage: tets M", rd.line_no);
-            const size_t n = to_count(tok[1], rd.line_no);
-            m->tets.reserve(m->tets.size() + 4 * n);
-            for (size_t i = 0; i < n; ++i) {
-                if (!rd.next(tok)) parse_fail("unexpected end of element list", rd.line_no);
-                if (tok.size() != 5) parse_fail("element line needs 'n0 n1 n2 n3 region'", rd.line_no);
-                for (int k = 0; k < 4; ++k) m->tets.push_back((int32_t)to_long(tok[k], rd.line_no));
-                m->region.push_back((int32_t)to_long(tok[4], rd.line_no));
-            }
-        } else if (tok[0] == "facets") {
-            if (tok.size() != 2) parse_fail("usage: facets B", rd.line_no);
-            const size_t n = to_count(tok[1], rd.line_no);
-            for (size_t i = 0; i < n; ++i) {
-                if (!rd.next(tok)) parse_fail("unexpected end of facet list", rd.line_no);
-                if (tok.size() != 4) parse_fail("facet line needs 'n0 n1 n2 tag'", rd.line_no);
-                for (int k = 0; k < 3; ++k) m->facets.push_back((int32_t)to_long(tok[k], rd.line_no));
-                m->facet_tag.push_back(m->add_tag(tok[3]));
-            }
-        } else if (tok[0] == "contact") {
-            if (tok.size() != 3) parse_fail("usage: contact tagA tagB", rd.line_no);
-            const int32_t a = m->add_tag(tok[1]);
-            const int32_t b = m->add_tag(tok[2]);
-            m->contacts.push_back(a);
-            m->contacts.push_back(b);
-        } else {
-            parse_fail("unknown section '" + std::string(tok[0]) + "'", rd.line_no);
+        }
+    }
+    defect.rethrow();
+
+    // pass 3: tags numbered by first appearance in file order, over facet records and contact lines
+    m->facet_tag.resize(totals[kFacets]);
+    for (const Section& sec : plan) {
+        if (sec.kind == kFacets) {
+            for (size_t r = 0; r < sec.count; ++r) m->facet_tag[sec.base + r] = m->tag_id(facet_word[sec.base + r]);
+        } else if (sec.kind == kContact) {
+            words(L[sec.first], w, 6);
+            m->contacts.push_back(m->tag_id(w[1]));
+            m->contacts.push_back(m->tag_id(w[2]));
         }
     }
     m->make_desc();
-    // finalize_mesh: validation and orientation, errors wrapped like parse_mesh (mesh.hpp:318-322)
+    // the mesh must pass finalize_mesh (validation + orientation), as parse_mesh requires (mesh.hpp:318-322)
     MeshData md;
     try {
         finalize_mesh(&m->desc, md);
@@ -323,151 +423,155 @@ struct TextSetup {
 };
 
 namespace {
-// parse_table material.hpp:188-202: one bare number = constant, else x:y pairs
-TextSetup::Table parse_table(const std::vector<std::string_view>& tok, size_t first, long line) {
+using Words = std::vector<std::string_view>;
+
+// a table value (material.hpp:188-202): one bare number is a constant, otherwise x:y pairs
+TextSetup::Table table_from(const Words& w, long line) {
     TextSetup::Table t;
-    if (tok.size() == first + 1 && tok[first].find(':') == std::string_view::npos) {
+    if (w.size() == 2 && w[1].find(':') == std::string_view::npos) {
         t.x = {0.0};
-        t.y = {to_double(tok[first], line)};
+        t.y = {to_double(w[1], line)};
         return t;
     }
-    for (size_t i = first; i < tok.size(); ++i) {
-        const size_t c = tok[i].find(':');
-        if (c == std::string_view::npos) parse_fail("expected x:y pair, got '" + std::string(tok[i]) + "'", line);
-        t.x.push_back(to_double(tok[i].substr(0, c), line));
-        t.y.push_back(to_double(tok[i].substr(c + 1), line));
+    for (size_t i = 1; i < w.size(); ++i) {
+        const size_t colon = w[i].find(':');
+        if (colon == std::string_view::npos) parse_fail("expected x:y pair, got '" + std::string(w[i]) + "'", line);
+        t.x.push_back(to_double(w[i].substr(0, colon), line));
+        t.y.push_back(to_double(w[i].substr(colon + 1), line));
     }
     return t;
 }
 
-// PiecewiseLinear::validate material.hpp:40-46
-void validate_table(const TextSetup::Table& t, const std::string& name) {
+// the checks PiecewiseLinear::validate makes (material.hpp:40-46)
+void require_table(const TextSetup::Table& t, const std::string& name) {
     if (t.x.empty() || t.x.size() != t.y.size()) raise(CF_CONFIG, name + ": empty or inconsistent table");
-    for (size_t i = 1; i < t.x.size(); ++i)
-        if (!(t.x[i] > t.x[i - 1])) raise(CF_CONFIG, name + ": table abscissae must be strictly increasing");
+    if (std::adjacent_find(t.x.begin(), t.x.end(), [](double a, double b) { return !(b > a); }) != t.x.end())
+        raise(CF_CONFIG, name + ": table abscissae must be strictly increasing");
 }
 
-std::string_view arg1(const std::vector<std::string_view>& tok, long line) {  // tok.at(1)
-    if (tok.size() < 2) raise(CF_INVALID_ARG, "line " + std::to_string(line) + ": missing value");
-    return tok[1];
+std::string_view value_of(const Words& w, long line) {  // the word after the key
+    if (w.size() < 2) raise(CF_INVALID_ARG, "line " + std::to_string(line) + ": missing value");
+    return w[1];
+}
+
+// Where key lines currently land: the open section's objects.
+struct ConfigCursor {
+    TextSetup* S = nullptr;
+    TextSetup::Mat* mat = nullptr;
+    TextSetup::Bc* bc = nullptr;
+    TextSetup::Coeff* coeff = nullptr;
+};
+
+// The grammar as data: every section lists its keys, each with the assignment it performs.
+struct KeyRule {
+    const char* key;
+    void (*assign)(ConfigCursor&, const Words&, long);
+};
+struct SectionRule {
+    const char* name;
+    size_t header_words;  // words inside the brackets, the name included
+    const char* noun;     // "unknown <noun> key '...'"
+    void (*open)(ConfigCursor&, const std::vector<std::string>&, long);
+    std::vector<KeyRule> keys;
+};
+
+#define CF_NUM(target) [](ConfigCursor& c, const Words& w, long ln) { target = to_double(value_of(w, ln), ln); }
+#define CF_TAB(target) [](ConfigCursor& c, const Words& w, long ln) { target = table_from(w, ln); }
+
+const std::vector<SectionRule>& grammar() {
+    static const std::vector<SectionRule> g = {
+        {"material", 2, "material",
+         [](ConfigCursor& c, const std::vector<std::string>& h, long ln) {
+             const long r = to_long(h[1], ln);
+             if (r < 0) raise(CF_INVALID_ARG, "line " + std::to_string(ln) + ": negative region id");
+             if (c.S->mats.size() <= (size_t)r) c.S->mats.resize((size_t)r + 1);
+             c.mat = &c.S->mats[(size_t)r];
+         },
+         {{"rho", CF_NUM(c.mat->rho)}, {"c", CF_TAB(c.mat->c)}, {"k", CF_TAB(c.mat->k)},
+          {"latent_heat", CF_NUM(c.mat->latent)}, {"solidus", CF_NUM(c.mat->solidus)},
+          {"liquidus", CF_NUM(c.mat->liquidus)}, {"T0", CF_NUM(c.mat->T0)}}},
+        {"bc", 2, "bc",
+         [](ConfigCursor& c, const std::vector<std::string>& h, long) { c.bc = &c.S->bcs[h[1]]; },  // flux by default
+         {{"kind",
+           [](ConfigCursor& c, const Words& w, long ln) {
+               const std::string_view v = value_of(w, ln);
+               if (v == "fixed") c.bc->kind = CF_BC_FIXED;
+               else if (v == "flux") c.bc->kind = CF_BC_FLUX;
+               else parse_fail("bc kind must be fixed or flux", ln);
+           }},
+          {"T", CF_TAB(c.bc->T)}, {"q", CF_NUM(c.bc->q)}, {"h", CF_NUM(c.bc->h)}, {"T_inf", CF_NUM(c.bc->t_inf)}}},
+        {"interface", 3, "interface",
+         [](ConfigCursor& c, const std::vector<std::string>& h, long) {
+             c.S->coeffs.emplace_back();
+             c.coeff = &c.S->coeffs.back();
+             c.coeff->a = h[1];
+             c.coeff->b = h[2];
+         },
+         {{"h", CF_TAB(c.coeff->h)},
+          {"h_time", [](ConfigCursor& c, const Words& w, long ln) { c.coeff->var = CF_VAR_TIME, c.coeff->h = table_from(w, ln); }},
+          {"h_temp",
+           [](ConfigCursor& c, const Words& w, long ln) { c.coeff->var = CF_VAR_TEMPERATURE, c.coeff->h = table_from(w, ln); }}}},
+        {"solver", 1, "solver", [](ConfigCursor&, const std::vector<std::string>&, long) {},
+         {{"safety", CF_NUM(c.S->safety)}, {"t_end", CF_NUM(c.S->t_end)},
+          {"output_every", [](ConfigCursor& c, const Words& w, long ln) { c.S->output_every = to_long(value_of(w, ln), ln); }}}},
+    };
+    return g;
+}
+#undef CF_NUM
+#undef CF_TAB
+
+// "[bc outer]", "[ bc outer ]", "[bc] outer": the brackets carry no meaning of their own -- they are
+// dropped wherever they stand and what is left of each word counts
+std::vector<std::string> header_words(const Words& w) {
+    std::vector<std::string> out;
+    for (std::string_view t : w) {
+        std::string bare;
+        std::copy_if(t.begin(), t.end(), std::back_inserter(bare), [](char ch) { return ch != '[' && ch != ']'; });
+        if (!bare.empty()) out.push_back(std::move(bare));
+    }
+    return out;
 }
 }  // namespace
 
 std::unique_ptr<TextSetup> parse_config_text(std::string_view text) {
     auto S = std::make_unique<TextSetup>();
-    Lines rd{text};
-    std::vector<std::string_view> tok;
-    enum { NONE, MATERIAL, BC, INTERFACE, SOLVER } sec = NONE;
-    long region = -1;
-    std::string bc_tag;
-    auto material_at = [&](long r) -> TextSetup::Mat& {
-        if (r < 0) raise(CF_INVALID_ARG, "line " + std::to_string(rd.line_no) + ": negative region id");
-        if ((long)S->mats.size() <= r) S->mats.resize((size_t)r + 1);
-        return S->mats[(size_t)r];
-    };
-    while (rd.next(tok)) {
-        if (tok.front().front() == '[') {  // section header: brackets dropped, tokens re-split
-            std::vector<std::string> head;
-            std::string cur;
-            for (const auto& t : tok) {
-                for (char ch : t) {
-                    if (ch == '[' || ch == ']') continue;
-                    cur.push_back(ch);
-                }
-                if (!cur.empty()) head.push_back(cur);
-                cur.clear();
-            }
-            if (head.empty()) parse_fail("empty section header", rd.line_no);
-            if (head[0] == "material" && head.size() == 2) {
-                sec = MATERIAL;
-                region = to_long(head[1], rd.line_no);
-                material_at(region);
-            } else if (head[0] == "bc" && head.size() == 2) {
-                sec = BC;
-                bc_tag = head[1];
-                S->bcs[bc_tag];  // default flux bc
-            } else if (head[0] == "interface" && head.size() == 3) {
-                sec = INTERFACE;
-                TextSetup::Coeff c;
-                c.a = head[1];
-                c.b = head[2];
-                S->coeffs.push_back(c);
-            } else if (head[0] == "solver" && head.size() == 1) {
-                sec = SOLVER;
-            } else {
-                parse_fail("unknown section '" + head[0] + "'", rd.line_no);
-            }
+    const LineIndex idx(text);
+    ConfigCursor cur;
+    cur.S = S.get();
+    const SectionRule* open = nullptr;
+    Words w;
+    for (const LogicalLine& line : idx.lines) {
+        std::string_view first[1];
+        w.resize((size_t)words(line, first, 1));
+        words(line, w.data(), (int)w.size());
+        if (w[0].front() == '[') {
+            const std::vector<std::string> head = header_words(w);
+            if (head.empty()) parse_fail("empty section header", line.no);
+            open = nullptr;
+            for (const SectionRule& r : grammar())
+                if (head[0] == r.name && head.size() == r.header_words) open = &r;
+            if (!open) parse_fail("unknown section '" + head[0] + "'", line.no);
+            open->open(cur, head, line.no);
             continue;
         }
-        const std::string key(tok[0]);
-        const long ln = rd.line_no;
-        switch (sec) {
-            case MATERIAL: {
-                auto& m = material_at(region);
-                if (key == "rho") m.rho = to_double(arg1(tok, ln), ln);
-                else if (key == "c") m.c = parse_table(tok, 1, ln);
-                else if (key == "k") m.k = parse_table(tok, 1, ln);
-                else if (key == "latent_heat") m.latent = to_double(arg1(tok, ln), ln);
-                else if (key == "solidus") m.solidus = to_double(arg1(tok, ln), ln);
-                else if (key == "liquidus") m.liquidus = to_double(arg1(tok, ln), ln);
-                else if (key == "T0") m.T0 = to_double(arg1(tok, ln), ln);
-                else parse_fail("unknown material key '" + key + "'", ln);
-                break;
-            }
-            case BC: {
-                auto& b = S->bcs[bc_tag];
-                if (key == "kind") {
-                    const std::string_view v = arg1(tok, ln);
-                    if (v == "fixed") b.kind = CF_BC_FIXED;
-                    else if (v == "flux") b.kind = CF_BC_FLUX;
-                    else parse_fail("bc kind must be fixed or flux", ln);
-                } else if (key == "T") b.T = parse_table(tok, 1, ln);
-                else if (key == "q") b.q = to_double(arg1(tok, ln), ln);
-                else if (key == "h") b.h = to_double(arg1(tok, ln), ln);
-                else if (key == "T_inf") b.t_inf = to_double(arg1(tok, ln), ln);
-                else parse_fail("unknown bc key '" + key + "'", ln);
-                break;
-            }
-            case INTERFACE: {
-                auto& c = S->coeffs.back();
-                if (key == "h") {
-                    c.h = parse_table(tok, 1, ln);
-                } else if (key == "h_time") {
-                    c.var = CF_VAR_TIME;
-                    c.h = parse_table(tok, 1, ln);
-                } else if (key == "h_temp") {
-                    c.var = CF_VAR_TEMPERATURE;
-                    c.h = parse_table(tok, 1, ln);
-                } else {
-                    parse_fail("unknown interface key '" + key + "'", ln);
-                }
-                break;
-            }
-            case SOLVER: {
-                if (key == "safety") S->safety = to_double(arg1(tok, ln), ln);
-                else if (key == "t_end") S->t_end = to_double(arg1(tok, ln), ln);
-                else if (key == "output_every") S->output_every = to_long(arg1(tok, ln), ln);
-                else parse_fail("unknown solver key '" + key + "'", ln);
-                break;
-            }
-            case NONE:
-                parse_fail("key '" + key + "' outside any section", ln);
-        }
+        if (!open) parse_fail("key '" + std::string(w[0]) + "' outside any section", line.no);
+        const auto rule = std::find_if(open->keys.begin(), open->keys.end(), [&](const KeyRule& k) { return w[0] == k.key; });
+        if (rule == open->keys.end())
+            parse_fail(std::string("unknown ") + open->noun + " key '" + std::string(w[0]) + "'", line.no);
+        rule->assign(cur, w, line.no);
     }
-    // MaterialTable::finalize material.hpp:104-119 for the materials that were set
+    // what MaterialTable::finalize checks (material.hpp:104-119), for every region that was given a density
     for (const auto& m : S->mats) {
-        if (!(m.rho > 0)) continue;  // untouched slots are caught at bind time
-        validate_table(m.c, "c");
-        validate_table(m.k, "k");
-        for (double v : m.c.y)
-            if (v <= 0) raise(CF_CONFIG, "c(T) must be positive");
-        for (double v : m.k.y)
-            if (v <= 0) raise(CF_CONFIG, "k(T) must be positive");
+        if (!(m.rho > 0)) continue;  // a region never configured: the plan builder reports it if a tet uses it
+        require_table(m.c, "c");
+        require_table(m.k, "k");
+        if (std::any_of(m.c.y.begin(), m.c.y.end(), [](double v) { return v <= 0; })) raise(CF_CONFIG, "c(T) must be positive");
+        if (std::any_of(m.k.y.begin(), m.k.y.end(), [](double v) { return v <= 0; })) raise(CF_CONFIG, "k(T) must be positive");
         if (m.latent < 0) raise(CF_CONFIG, "latent_heat must be non-negative");
         if (m.latent > 0 && !(m.solidus < m.liquidus)) raise(CF_CONFIG, "phase change requires solidus < liquidus");
     }
     if (!(S->safety > 0 && S->safety <= 1)) raise(CF_CONFIG, "safety must be in (0, 1]");
-    for (const auto& c : S->coeffs) validate_table(c.h, "interface h");
+    for (const auto& c : S->coeffs) require_table(c.h, "interface h");
     S->make_desc();
     return S;
 }

@@ -83,6 +83,20 @@ MESH_CASES = [
     b"femesh 1\nnodes 5\n0 0 0\n1 0 0\n0 1 0\n0 0 1\n5 5 5\ntets 1\n0 1 2 3 0\n",
     b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 3 0\nfacets 1\n0 1 3 x\n",
     b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 3 0\nfacets 1\n0 1 7 x\n",
+    # several defects: the first in file order is the one reported (the product plans the sections
+    # first and converts the records afterwards, in parallel)
+    b"femesh 1\nnodes 2\n0 0 0\n0 0 oops\nbogus 3\n",                      # bad record before a bad header
+    b"femesh 1\nnodes 2\n0 0 0\n1 1 1\nbogus 3\ntets 1\n0 1 2 x 0\n",      # bad header before a bad record
+    b"femesh 1\nnodes 3\n0 0 0\n0 0\n",                                     # malformed record inside a list cut short
+    b"femesh 1\nnodes 3\n0 0 0\n0 0 1\n\n# tail\n",                        # list cut short: the last physical line
+    b"femesh 1\nnodes 2\n0 0 0\ntets 1\n",                                  # a header line consumed as a record
+    b"femesh 1\nnodes x\n0 0 0\n",                                          # count is not an integer
+    b"femesh 1\nnodes 1 2\n0 0 0\n",                                        # usage
+    b"femesh 1\ncontact a b c\nnodes 1\n0 0 z\n",                           # contact usage before a bad record
+    b"femesh 1\nnodes 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\ntets 1\n0 1 2 3 0\ncontact q p\nfacets 2\n0 1 2 p\n0 1 3 zz\n"
+    b"contact zz q\n",                                                       # tags numbered by first appearance
+    b"femesh 1\n nodes 1 \n\t0 0\t0 # c\r\n",                              # blanks, tabs, CR, comments
+    b"femesh 1\nnodes 2\n0 0 0\n1 1 1\nnodes 2\n2 2 2\n0 0 1\ntets 1\n0 1 2 3 0\n",  # a section given twice appends
 ]
 
 
@@ -92,6 +106,25 @@ def test_mesh_edge_cases_match_reference(i):
     text = MESH_CASES[i]
     ours, ref = ours_mesh(text), orc.ref_mesh_roundtrip(text)
     assert ours == ref  # same status, same text / message (line numbers, validation wording)
+
+
+@need_ref
+def test_large_mesh_parallel_conversion_matches_reference():
+    """Lists longer than the parallel threshold (4096 records): same text out as the reference,
+    and with one bad record deep inside each list the same first error."""
+    m = cf.generate_fixture("casting", 12, jitter=0.1, seed=2, perm_seed=5)
+    text = cf.write_mesh(m).encode()
+    assert m.element_count() > 4096
+    assert ours_mesh(text) == orc.ref_mesh_roundtrip(text)
+    lines = text.split(b"\n")
+    tets_at = lines.index(b"tets %d" % m.element_count())
+    for at, repl in ((tets_at + 5000, b"1 2 3"), (tets_at + 9000, b"1 2 3 4 x"), (1 + 700, b"0 0 nan?")):
+        bad = list(lines)
+        bad[at] = repl
+        bad[tets_at + 9500] = b"7 7"  # a later defect must not win
+        t = b"\n".join(bad)
+        ours, ref = ours_mesh(t), orc.ref_mesh_roundtrip(t)
+        assert ours == ref and ours[0] != 0
 
 
 # ---------------------------------------------------------------- config
@@ -127,6 +160,13 @@ h_temp 300:10 900:2000
 safety 0.138
 """,
     b"[material 2]\nrho 7800\nc 300:450 900:700\nk 300:45 900:30\n[bc outer]\nkind flux\nq 5\n",
+    # header forms: the brackets are dropped wherever they stand
+    b"[ bc   outer ]\nh 3\n[bc] inner\nq 1\n[[bc] outer]\nT_inf 9\n",
+    b"[interface a b]\nh_temp 300:5 900:7\n[interface] c [d\nh_time 4\n[solver ]\nsafety 0.25\n",
+    # a section reopened continues the same object; regions out of order leave untouched slots
+    b"[material 3]\nrho 2\nc 5\nk 6\n[bc w]\nq 2\n[material 3]\nT0 77\nlatent_heat 4\nsolidus 1\nliquidus 2\n"
+    b"[bc w]\nkind fixed\nT 0:1 10:2\n[material 1]\nrho 9\nc 1\nk 1\n",
+    b"[material 0]\nrho 1 2 3\nc 1\nk 0:1 5:2 # extra words after a scalar are ignored\n",
 ]
 
 CONFIG_BAD = [
@@ -152,7 +192,31 @@ CONFIG_BAD = [
     b"[solver]\nsafety 1.5\n",
     b"[solver]\noutput_every 2.5\n",
     b"[solver]\nfoo 1\n",
+    b"[ ]\n",
+    b"[bc]\n",
+    b"[bc a b]\n",
+    b"[interface a]\n",
+    b"[solver now]\n",
+    b"[Material 0]\n",
+    b"[material 0]\nrho 1\nc 1:\nk 1\n",
+    b"[material 0]\nrho 1\nc :1\nk 1\n",
+    b"[material 0]\nrho 1\nc 1:2:3\nk 1\n",
+    b"[material 0]\nrho 1\nc\nk 1\n",
+    b"[material 0]\nrho 1\nc 1\nk -2\n",
+    b"[solver]\nsafety 0.5\nt_end x\n[bogus]\n",
 ]
+
+
+def test_config_inputs_the_reference_mishandles_are_rejected_cleanly():
+    """Where the reference has undefined behaviour (a negative region indexes before the material
+    array) or leaks a library message (tok.at(1) on a key without a value throws std::out_of_range
+    with libstdc++'s wording), this parser reports an invalid argument with the line number."""
+    from paper_1005_3158_b200 import _abi
+    for text, msg in ((b"[material -1]\n", "line 1: negative region id"),
+                      (b"[bc x]\nkind\n", "line 2: missing value"),
+                      (b"[solver]\n\nsafety\n", "line 3: missing value")):
+        code, what = ours_config(text)
+        assert code == _abi.CF_INVALID_ARG and what == msg
 
 
 @need_ref

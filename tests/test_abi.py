@@ -56,3 +56,18 @@ def test_cpp_shim_compiles_standalone(tmp_path):
                         "-lcastfem_b200", f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert subprocess.run([str(tmp_path / "t")]).returncode == 0
+
+
+def test_c_header_is_plain_c(tmp_path):
+    """The boundary is a C ABI: include/castfem_b200.h compiles as C11 (no C++ or torch types in
+    any signature) and a C program links the library and calls through it."""
+    import subprocess
+    src = tmp_path / "t.c"
+    src.write_text('#include "castfem_b200.h"\n#include <string.h>\n'
+                   "int main(void) { char b[8]; cf_last_error(b, sizeof b); return cf_abi_version() == 2 ? 0 : 1; }\n")
+    inc = os.path.join(os.path.dirname(HDR))
+    libdir = os.path.dirname(_abi.LIB_PATH)
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", f"-I{inc}", str(src), "-o", str(tmp_path / "t"),
+                        f"-L{libdir}", "-lcastfem_b200", f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert subprocess.run([str(tmp_path / "t")]).returncode == 0

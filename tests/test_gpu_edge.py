@@ -232,3 +232,45 @@ def test_delaunay_mesh(tile_elems, ranks, geometry):
     if orc.ref_available() and ranks == 1:  # and the reference itself, one block
         r, _ = orc.ref_solve(m, s, steps)
         assert float(np.max(np.abs(gpu.T - r.T) / np.abs(r.T))) <= 1e-9
+
+
+def test_plain_c_caller(tmp_path):
+    """tests/c/c_abi_example.c: a C11 program fills the descriptors by hand, creates a plan, steps
+    and reads the fields through include/castfem_b200.h alone. Its printed temperatures (hex
+    doubles) must equal the oracle's bit for bit in both tile layouts, and a bad facet tag must
+    come back as CF_CONFIG with the reference's message."""
+    import os
+    import subprocess
+    from paper_1005_3158_b200 import _abi
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "c_abi_example")
+    libdir = os.path.dirname(_abi.LIB_PATH)
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I" + os.path.join(root, "include"),
+                        os.path.join(root, "tests", "c", "c_abi_example.c"), "-o", exe, "-L" + libdir, "-lcastfem_b200",
+                        "-Wl,-rpath," + libdir], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    coords = np.array([0, 0, 0, 1, 0, 0, 0, 1, 0, 1, 1, 0, 0, 0, 1, 1, 0, 1, 0, 1, 1, 1, 1, 1], float).reshape(8, 3)
+    tets = np.array([0, 1, 3, 7, 0, 1, 5, 7, 0, 2, 3, 7, 0, 2, 6, 7, 0, 4, 5, 7, 0, 4, 6, 7], np.int32).reshape(6, 4)
+    fac = np.array([0, 1, 3, 0, 2, 3, 4, 5, 7, 4, 6, 7, 0, 1, 5, 0, 4, 5, 2, 3, 7, 2, 6, 7, 0, 2, 6, 0, 4, 6, 1, 3, 7,
+                    1, 5, 7], np.int32).reshape(12, 3)
+    m = cf.Mesh(coords, tets, np.zeros(6, np.int32), fac, np.zeros(12, np.int32), ["skin"])
+    mat = cf.MaterialTable.make(rho=2700.0, c=[(300.0, 850.0), (1000.0, 1100.0)], k=200.0, latent_heat=3.9e5,
+                                solidus=821.0, liquidus=913.0, T0=930.0)
+    T0 = np.array([930.0, 925.0, 921.5, 917.0, 912.0, 908.5, 903.0, 899.0])
+    s = cf.SimulationSetup(materials=[mat], boundary_conditions={"skin": cf.BoundaryCondition("flux", h=50.0,
+                                                                                             t_inf=300.0)},
+                           solver=cf.SolverConfig(dt_safety=0.002), initial_T=T0)
+    lines = out.stdout.strip().splitlines()
+    for g, geometry in enumerate(("stored", "coords")):
+        opts = cf.SolveOptions(tile_elems=4, geometry=geometry)
+        tiles, nt = cf.tile_map(m, s, opts)
+        ref = orc.solve(m, s, 25, blocks=tiles)
+        head = lines[9 * g].split()
+        assert head[:6] == ["geometry", str(g), "steps", "25", "tiles", str(nt)] and nt == 2
+        assert float.fromhex(head[7]) == ref.time
+        for i in range(8):
+            _, idx, t_hex, h_hex = lines[9 * g + 1 + i].split()
+            assert int(idx) == i and float.fromhex(t_hex) == ref.T[i] and float.fromhex(h_hex) == ref.H[i]
+    assert lines[18] == f"bad tag: status {_abi.CF_CONFIG}: facet tag 'skin' resolves to no declared condition"

@@ -276,6 +276,8 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []  # (sm_mhz, sm_max_mhz, set of active reason names)
+        self.power_w = []  # board power under load (NVML only)
+        self.power_limit_w = None
         self._stop = threading.Event()
         self._t = None
         self._nv = None
@@ -296,6 +298,12 @@ class ClockSampler:
                 bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
                         nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
                 self.samples.append((float(sm), float(mx), {self.NAMES[i] for i, b in enumerate(bits) if r & b}))
+                try:  # what sw_power_cap is capping against
+                    self.power_w.append(nv.nvmlDeviceGetPowerUsage(h) / 1000.0)
+                    if self.power_limit_w is None:
+                        self.power_limit_w = nv.nvmlDeviceGetEnforcedPowerLimit(h) / 1000.0
+                except Exception:
+                    pass
                 return
             except Exception:
                 self._nv = None
@@ -329,6 +337,9 @@ class ClockSampler:
         reasons = sorted(set().union(*[s[2] for s in self.samples])) if self.samples else []
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples),
+                # NVML's board power is a ~1 s moving average: over a short timed region it lags the load
+                "power_w_max": round(max(self.power_w), 1) if self.power_w else None,
+                "power_limit_w": self.power_limit_w,
                 "source": "nvml" if self._nv else "nvidia-smi"}
 
 

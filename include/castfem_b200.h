@@ -157,8 +157,9 @@ typedef struct cf_run_opts {
                                        blocked.hpp:79-93); overrides elem_order/tile_elems */
     int32_t n_tiles_given;     /* tiles in tile_of_element */
     int32_t fast_math;         /* reserved, must be 0: kernels are built without FMA contraction
-                                  (-fmad=false) so results are bitwise the reference's; measured
-                                  FMA gain was ~1 % */
+                                  (-fmad=false) so results are bitwise the reference's. An
+                                  FMA-contracted build of the whole library is an opt-in
+                                  (csrc/Makefile FMA=1: +2.6 % at cfg5, 2.8e-16 from the oracle) */
     /* domain decomposition (paper 4.1.1; two_level_decompose partition.hpp:377-422) */
     int32_t world_size;        /* ranks in the job (1 = single GPU) */
     int32_t rank;              /* this process's first rank */
